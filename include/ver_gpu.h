@@ -1,0 +1,295 @@
+/*
+ * ver_gpu.h — C-ABI of the B200-native VER learner hot path.
+ *
+ * Every entry point replaces one function of the reference's C++ API
+ * (/root/reference/proj, namespace ver); the reference file:line is cited on
+ * each.  Plain pointers and sizes only: no torch / CUDA / C++ types cross this
+ * boundary.  The C++ wrapper include/ver_gpu.hpp rethrows the status codes as
+ * ver::ProtocolError / ver::ConfigError so callers written against the
+ * reference (train_single bench.cpp:155, ReplicaGroup::replica_main
+ * distributed.cpp:230-234, run_replay bench.cpp:386-409) keep their shape.
+ *
+ * Conventions
+ *  - Every function returns ver_status; ver_last_error() holds the message of
+ *    the last failure on the calling thread.
+ *  - Handles are device-resident and stream-ordered on their ver_ctx's stream.
+ *    They are not thread-safe: one learner per host thread per GPU (the
+ *    reference's replica-per-thread model, distributed.cpp:271-276).
+ *  - Only functions returning host values synchronize the stream.
+ *  - Floating-point payloads are fp32 at the boundary (the reference is
+ *    double; parity tolerances are stated in DESIGN.md).
+ *  - There is no CPU fallback: every compute entry point launches sm_100a
+ *    kernels and fails with VER_ERR_CUDA if no device is present.
+ */
+#ifndef VER_GPU_H
+#define VER_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  VER_OK = 0,
+  VER_ERR_PROTOCOL = 1,  /* ver::ProtocolError (types.hpp:41-44) */
+  VER_ERR_CONFIG = 2,    /* ver::ConfigError   (types.hpp:46-49) / bad argument */
+  VER_ERR_NONFINITE = 3, /* non-finite loss / parameters (learner.cpp:111,140) */
+  VER_ERR_CUDA = 4,
+  VER_ERR_NCCL = 5
+} ver_status;
+
+const char* ver_last_error(void);
+/* library build string (arch, precision modes) */
+const char* ver_version(void);
+
+/* ------------------------------------------------------------------ context */
+typedef struct ver_ctx_s* ver_ctx;
+/* device ordinal; creates a non-blocking stream and the stream-ordered pool */
+ver_status ver_ctx_create(int device, ver_ctx* out);
+ver_status ver_ctx_destroy(ver_ctx ctx);
+ver_status ver_ctx_synchronize(ver_ctx ctx);
+/* the ctx stream as an opaque integer (cudaStream_t) for event timing */
+ver_status ver_ctx_stream(ver_ctx ctx, uint64_t* stream_out);
+/* number of kernels this library launched on ctx since creation / last reset */
+ver_status ver_ctx_launch_count(ver_ctx ctx, int64_t* count, int reset);
+/* precision of the policy GEMMs: 0 = fp32 (parity, default), 1 = bf16 tensor
+   cores (fast mode, looser bound stated in DESIGN.md) */
+ver_status ver_ctx_set_precision(ver_ctx ctx, int mode);
+
+/* NCCL (DD-PPO gradient AllReduce, distributed.cpp:86-116 / C1-C4 of SURVEY §2.2) */
+ver_status ver_nccl_unique_id(uint8_t id_out[128]);
+ver_status ver_ctx_init_nccl(ver_ctx ctx, const uint8_t id[128], int nranks, int rank);
+/* in-place sum of n int64 across ranks (PreemptCoordinator step counts,
+   fresh-step totals; distributed.hpp:111-119, distributed.cpp:222-226) */
+ver_status ver_allreduce_sum_i64(ver_ctx ctx, int64_t* host_inout, int n);
+/* in-place element-wise mean of n doubles across ranks (learn time, C4) */
+ver_status ver_allreduce_mean_f64(ver_ctx ctx, double* host_inout, int n);
+/* all-gather of n doubles per rank into out (nranks * n): pooled tau, C4 */
+ver_status ver_allgather_f64(ver_ctx ctx, const double* host_in, int n, double* host_out);
+
+/* ------------------------------------------------------------- view (L2) */
+/* SequenceDescriptor (rollout.hpp:19-28): 8 x int32 */
+typedef struct {
+  int32_t seq_id, env_index, length, start_offset, h0_index, stale, parent_start_offset, skip;
+} ver_seq_desc;
+
+/* Host image of a RolloutView (rollout.hpp:33-78).  Used to upload an
+   arbitrary view (test fixtures, load_view replay) and to read one back.
+   Array pointers may be NULL on read to skip a field. */
+typedef struct {
+  int T, N, action_kind /*0 discrete, 1 continuous*/, obs_dim, act_dim, hidden_dim;
+  int size, num_seqs, h0_rows;
+  int deficit, stale_steps, replayed_steps;
+  uint64_t snapshot_version;
+  double collect_wall_time;
+  float* obs;        /* size x obs_dim */
+  float* act_cont;   /* size x act_dim  (continuous) */
+  int32_t* act_disc; /* size            (discrete)   */
+  float *log_prob, *value, *reward, *latency, *advantage, *returns;
+  uint8_t *done, *stale, *replayed;
+  int32_t *env_index, *seq_of_slot, *step_in_episode;
+  int64_t* episode_index;
+  uint64_t* version;
+  ver_seq_desc* seqs; /* num_seqs */
+  float* h0;          /* h0_rows x hidden_dim */
+  int32_t* per_env_counts;
+  float* env_bootstrap;
+  uint8_t* env_bootstrap_valid;
+} ver_view_host;
+
+typedef struct ver_view_s* ver_view;
+ver_status ver_view_upload(ver_ctx ctx, const ver_view_host* h, ver_view* out);
+/* fills scalars and sizes of h; pointers untouched */
+ver_status ver_view_info(ver_view v, ver_view_host* h);
+/* copies every field whose pointer is non-NULL (synchronizes) */
+ver_status ver_view_download(ver_view v, ver_view_host* h);
+ver_status ver_view_clone(ver_view v, ver_view* out);
+ver_status ver_view_destroy(ver_view v);
+/* RolloutView::restale (rollout.cpp:15-22) */
+ver_status ver_view_restale(ver_view v, uint64_t learner_version);
+
+/* ------------------------------------------------------ rollout store (L2) */
+typedef struct {
+  int T, N;
+  int mode;        /* 0 Fixed, 1 Variable (rollout.hpp:12) */
+  int action_kind; /* 0 discrete, 1 continuous */
+  int obs_dim, act_dim, hidden_dim;
+} ver_rollout_config;
+
+/* A batch of EnvStepRecords (types.hpp:54-67) in arrival order, SoA.
+   h_before rows are only read for records that start a sequence (the
+   reference copies h_before on every commit but reads it only there,
+   rollout.cpp:81 vs :155); h_before == NULL or h_before_valid[i] == 0 means
+   "absent" (zeros, rollout.cpp:156). */
+typedef struct {
+  int n;
+  const int32_t* env_index;
+  const int64_t* episode_index;   /* may be NULL (0) */
+  const int32_t* step_in_episode; /* may be NULL (0) */
+  const float* obs;               /* n x obs_dim */
+  const int32_t* act_disc;        /* n (discrete) */
+  const float* act_cont;          /* n x act_dim (continuous) */
+  const float *log_prob, *value, *reward;
+  const float* latency;           /* may be NULL (0) */
+  const uint8_t* done;
+  const float* h_before;          /* n x hidden_dim or NULL */
+  const uint8_t* h_before_valid;  /* n or NULL */
+  const uint64_t* snapshot_version; /* may be NULL (0) */
+} ver_step_batch;
+
+typedef struct ver_rollout_s* ver_rollout;
+/* RolloutBuffer(Config) (rollout.cpp:24-31) */
+ver_status ver_rollout_create(ver_ctx ctx, const ver_rollout_config* cfg, ver_rollout* out);
+ver_status ver_rollout_destroy(ver_rollout r);
+/* begin_rollout (rollout.cpp:39-57): commits pending carryovers first, env order */
+ver_status ver_rollout_begin(ver_rollout r, uint64_t snapshot_version);
+/* append_step (rollout.cpp:59-93) for each record in order; outcomes[i] =
+   0 Accepted / 1 RolloutFull (may be NULL).  A ProtocolError stops the batch
+   at that record (earlier records stay applied, as in the reference). */
+ver_status ver_rollout_append(ver_rollout r, const ver_step_batch* batch, int32_t* outcomes);
+ver_status ver_rollout_force_close(ver_rollout r);          /* rollout.cpp:95 */
+ver_status ver_rollout_set_bootstrap(ver_rollout r, int env, float value); /* :97-100 */
+ver_status ver_rollout_state(ver_rollout r, int* open, int* committed, int* carryover);
+/* close_rollout (rollout.cpp:102-190): device compaction of the arrival log
+   into the env-major, sequence-contiguous view */
+ver_status ver_rollout_close(ver_rollout r, ver_view* out);
+
+/* backfill_stale (rollout.cpp:208-276) */
+ver_status ver_backfill_stale(ver_view view, ver_view prev, int deficit);
+
+/* ---------------------------------------------------------------- GAE (L5) */
+/* compute_gae (learner.cpp:11-41): segmented reverse scan on device */
+ver_status ver_compute_gae(ver_view v, double gamma, double lambda);
+
+/* ------------------------------------------------------------ sampler (L3) */
+typedef struct ver_groups_s* ver_groups;
+/* split_minibatches (packseq.cpp:10-16): libstdc++ std::shuffle with
+   mt19937_64(seed) of the K sequence ids on the host (O(K)), the greedy deal
+   with split tails on the device */
+ver_status ver_split_minibatches(ver_view v, int B, uint64_t seed, ver_groups* out);
+/* split_in_order (packseq.cpp:18-54) */
+ver_status ver_split_in_order(ver_view v, int B, const int32_t* order, int n, ver_groups* out);
+ver_status ver_groups_count(ver_groups g, int* B);
+/* group b: number of pieces, steps, and (if seqs != NULL) the pieces in deal order */
+ver_status ver_groups_get(ver_groups g, int b, int* num_seqs, int* total_steps, ver_seq_desc* seqs);
+ver_status ver_groups_destroy(ver_groups g);
+
+typedef struct ver_packed_s* ver_packed;
+/* pack (packseq.cpp:56-88) of group b, plus the time-major gather of the
+   view's learner fields (learner.cpp:56-70) into the packed order */
+ver_status ver_pack(ver_view v, ver_groups g, int b, ver_packed* out);
+/* pack of an explicit group (tests / replay) */
+ver_status ver_pack_seqs(ver_view v, const ver_seq_desc* seqs, int k, ver_packed* out);
+ver_status ver_packed_info(ver_packed p, int* num_seqs, int* max_len, int* total_steps);
+ver_status ver_packed_get(ver_packed p, ver_seq_desc* seqs, int32_t* sorted_to_group,
+                          int32_t* batch_sizes, int32_t* offsets, int32_t* slots);
+/* the gathered, time-major learner fields (obs S x D, act, old log-prob, A, R) */
+ver_status ver_packed_get_gathered(ver_packed p, float* obs, int32_t* act_disc, float* act_cont,
+                                   float* old_logp, float* adv, float* ret);
+ver_status ver_packed_destroy(ver_packed p);
+
+/* ------------------------------------------------------------ policy (L4) */
+typedef struct {
+  int obs_dim, encoder_dim, hidden_dim;
+  int action_kind; /* 0 discrete, 1 continuous */
+  int num_actions, act_dim;
+} ver_model_config;
+
+/* parameter registry in PolicyParams::tensors() order (nn.cpp:83-95) */
+ver_status ver_param_count(const ver_model_config* c, int64_t* count, int* num_tensors);
+ver_status ver_param_tensor(const ver_model_config* c, int idx, char name[16], int* rows,
+                            int* cols, int64_t* offset);
+/* PolicyParams::init (nn.cpp:16-81), host double, one-off setup */
+ver_status ver_params_init(const ver_model_config* c, uint64_t seed, double* out);
+
+typedef struct {
+  double gamma, gae_lambda, clip;
+  int epochs, minibatches;
+  double value_loss_coef, is_cap;
+} ver_ppo_config; /* PPOConfig (learner.hpp:14-22) */
+
+typedef struct {
+  double loss, policy_loss, value_loss, mean_entropy, ratio_sum, clip_count, w_sum, w_max;
+  int steps;
+} ver_loss_result; /* PPOLossResult (learner.hpp:80-92) */
+
+/* ppo_loss (learner.cpp:52-117): forward_packed + fused loss (+ backward).
+   params: host fp32 (P); h0_sorted: host fp32 (k x H); frozen_w: host (S) or
+   NULL; grads_out: host (P) or NULL; is_w_out: host (S) or NULL. */
+ver_status ver_ppo_loss(ver_ctx ctx, const ver_model_config* c, const float* params, ver_view v,
+                        ver_packed p, const ver_ppo_config* cfg, double alpha,
+                        const float* h0_sorted, int want_grads, const float* frozen_w,
+                        ver_loss_result* out, float* grads_out, float* is_w_out);
+
+/* forward_packed (nn.cpp:219-280) over S packed rows with explicit
+   batch_sizes/offsets (L timesteps) and h0 (batch_sizes[0] x H); per-row
+   log-prob, entropy and value; all host arrays */
+ver_status ver_forward_packed(ver_ctx ctx, const ver_model_config* c, const float* params, int S,
+                              const float* obs, const int32_t* act_disc, const float* act_cont,
+                              int L, const int32_t* batch_sizes, const int32_t* offsets,
+                              const float* h0, float* logp_out, float* ent_out, float* value_out);
+
+/* act (nn.cpp:118-126) on n rows: dist (n x A), value (n), h_new (n x H); host */
+ver_status ver_act(ver_ctx ctx, const ver_model_config* c, const float* params, int n,
+                   const float* obs, const float* h, float* dist_out, float* value_out,
+                   float* h_new_out);
+
+/* adam_step (nn.cpp:291-306) on flat host arrays; step is incremented */
+ver_status ver_adam_step(ver_ctx ctx, int64_t count, float* params, const float* grads, float* m,
+                         float* v, int64_t* step, double lr);
+/* CosineSchedule::lr_at (nn.cpp:308-312) */
+double ver_cosine_lr(double base_lr, int64_t total_steps, int64_t consumed);
+
+/* ----------------------------------------------------------- learner (L5) */
+typedef struct {
+  double alpha, target, lower, upper, lr;
+} ver_entropy_controller; /* learner.hpp:29-40 */
+
+typedef struct {
+  int64_t update_index;
+  int steps, fresh_steps, stale_steps;
+  double loss, policy_loss, value_loss, entropy, entropy_loss, mean_ratio, clip_fraction,
+      mean_is_weight, max_is_weight, alpha, lr;
+} ver_train_stats; /* TrainStats (learner.hpp:55-71) */
+
+typedef struct ver_learner_s* ver_learner;
+/* Learner(params, cfg, entropy, schedule, run_seed) (learner.cpp:43-50) */
+ver_status ver_learner_create(ver_ctx ctx, const ver_model_config* c, const float* params,
+                              const ver_ppo_config* cfg, const ver_entropy_controller* ec,
+                              double base_lr, int64_t total_steps, uint64_t run_seed,
+                              ver_learner* out);
+ver_status ver_learner_destroy(ver_learner l);
+/* gradient AllReduce over the ctx's NCCL communicator before every Adam step
+   (grad_hook / entropy_hook -> AllReduce::average, distributed.cpp:152-157) */
+ver_status ver_learner_enable_allreduce(ver_learner l, int enable);
+/* Learner::update (learner.cpp:146-193).  stats may be NULL: then nothing is
+   read back and the call does not synchronize. */
+ver_status ver_learner_update(ver_learner l, ver_view v, ver_train_stats* stats);
+/* Learner::batch_h0 (learner.cpp:119-130): h0 rows for packed batch (k x H) */
+ver_status ver_learner_batch_h0(ver_learner l, ver_view v, ver_packed p, float* h0_out);
+ver_status ver_learner_get_params(ver_learner l, float* out);
+ver_status ver_learner_set_params(ver_learner l, const float* in);
+ver_status ver_learner_get_adam(ver_learner l, float* m, float* v, int64_t* step);
+ver_status ver_learner_set_adam(ver_learner l, const float* m, const float* v, int64_t step);
+ver_status ver_learner_get_state(ver_learner l, double* alpha, int64_t* consumed_steps,
+                                 int64_t* update_index);
+ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed_steps,
+                                 int64_t update_index);
+/* per-phase device time of the last update, ms (gae, sampler, gather, forward,
+   recurrence, loss, backward, allreduce, adam); n in/out */
+ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n);
+
+/* ------------------------------------------------------- distributed (L7) */
+/* estimate_time (distributed.cpp:24-51), bisection with device counting */
+ver_status ver_estimate_time(ver_ctx ctx, const double* tau, int n, int64_t max_steps,
+                             int64_t steps, double* out);
+/* optimal_preempt_steps (distributed.cpp:53-65), sort formulation on device
+   (the equivalence test_distributed.cpp:16-37,122-132 pins) */
+ver_status ver_optimal_preempt_steps(ver_ctx ctx, const double* tau, int n, double learn_time,
+                                     int64_t max_steps, int64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

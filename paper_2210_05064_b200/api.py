@@ -1,0 +1,822 @@
+"""Host-side mirror of the reference's hot-path API over the C-ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj:
+RolloutBuffer / close_rollout / backfill_stale (rollout.hpp:87-151),
+split_minibatches / split_in_order / pack / unpack (packseq.hpp:35-44),
+compute_gae / ppo_loss / Learner (learner.hpp:53-138), act / adam_step /
+CosineSchedule (nn.hpp:67-118), estimate_time / optimal_preempt_steps
+(distributed.hpp:29-32).  Every call goes through libver_b200.so; there is
+no Python or CPU compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib as L
+from .hostview import HostView, SEQ_FIELDS
+
+VER_OK, VER_ERR_PROTOCOL, VER_ERR_CONFIG, VER_ERR_NONFINITE, VER_ERR_CUDA, VER_ERR_NCCL = range(6)
+
+
+class ProtocolError(RuntimeError):
+    """ver::ProtocolError (types.hpp:41-44)."""
+
+
+class ConfigError(RuntimeError):
+    """ver::ConfigError (types.hpp:46-49)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _check(status: int):
+    if status == VER_OK:
+        return
+    msg = _lib().ver_last_error().decode(errors="replace")
+    if status in (VER_ERR_PROTOCOL, VER_ERR_NONFINITE):
+        raise ProtocolError(msg)
+    if status == VER_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise CudaError(f"[{status}] {msg}")
+
+
+def _lib():
+    return L.load()
+
+
+def _ptr(a: np.ndarray | None, ctype):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One device + stream (+ optional NCCL communicator)."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        _check(_lib().ver_ctx_create(device, C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            _lib().ver_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(_lib().ver_ctx_synchronize(self.h))
+
+    @property
+    def stream(self) -> int:
+        s = C.c_uint64()
+        _check(_lib().ver_ctx_stream(self.h, C.byref(s)))
+        return s.value
+
+    def launch_count(self, reset: bool = False) -> int:
+        n = C.c_int64()
+        _check(_lib().ver_ctx_launch_count(self.h, C.byref(n), int(reset)))
+        return n.value
+
+    def set_precision(self, mode: int):
+        _check(_lib().ver_ctx_set_precision(self.h, mode))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib().ver_nccl_unique_id(buf))
+        return buf.raw
+
+    def init_nccl(self, uid: bytes, nranks: int, rank: int):
+        _check(_lib().ver_ctx_init_nccl(self.h, uid, nranks, rank))
+
+    def allreduce_sum_i64(self, values) -> np.ndarray:
+        a = np.ascontiguousarray(values, dtype=np.int64).copy()
+        _check(_lib().ver_allreduce_sum_i64(self.h, _ptr(a, C.c_int64), a.size))
+        return a
+
+    def allreduce_mean_f64(self, values) -> np.ndarray:
+        a = np.ascontiguousarray(values, dtype=np.float64).copy()
+        _check(_lib().ver_allreduce_mean_f64(self.h, _ptr(a, C.c_double), a.size))
+        return a
+
+    def allgather_f64(self, values, nranks: int) -> np.ndarray:
+        a = np.ascontiguousarray(values, dtype=np.float64)
+        out = np.zeros(a.size * nranks, np.float64)
+        _check(_lib().ver_allgather_f64(self.h, _ptr(a, C.c_double), a.size, _ptr(out, C.c_double)))
+        return out
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# --------------------------------------------------------------------- view
+def _viewhost(hv: HostView, copy: bool = True) -> tuple[L.ViewHost, list]:
+    """Build a ViewHost struct pointing into hv's arrays (float32 copies if `copy`)."""
+    h = hv.astype(np.float32) if copy else hv
+    keep = [h]
+    vh = L.ViewHost()
+    vh.T, vh.N, vh.action_kind = h.T, h.N, h.action_kind
+    vh.obs_dim, vh.act_dim, vh.hidden_dim = h.obs_dim, h.act_dim, h.hidden_dim
+    vh.size, vh.num_seqs, vh.h0_rows = h.size, h.num_seqs, h.h0.shape[0]
+    vh.deficit, vh.stale_steps, vh.replayed_steps = h.deficit, h.stale_steps, h.replayed_steps
+    vh.snapshot_version, vh.collect_wall_time = h.snapshot_version, h.collect_wall_time
+    for name, ct in (("obs", C.c_float), ("act_cont", C.c_float), ("act_disc", C.c_int32),
+                     ("log_prob", C.c_float), ("value", C.c_float), ("reward", C.c_float),
+                     ("latency", C.c_float), ("advantage", C.c_float), ("returns", C.c_float),
+                     ("done", C.c_uint8), ("stale", C.c_uint8), ("replayed", C.c_uint8),
+                     ("env_index", C.c_int32), ("seq_of_slot", C.c_int32),
+                     ("step_in_episode", C.c_int32), ("episode_index", C.c_int64),
+                     ("version", C.c_uint64), ("h0", C.c_float), ("per_env_counts", C.c_int32),
+                     ("env_bootstrap", C.c_float), ("env_bootstrap_valid", C.c_uint8)):
+        a = getattr(h, name)
+        setattr(vh, name, _ptr(a, ct) if a.size else None)
+    vh.seqs = h.seqs.ctypes.data_as(C.POINTER(L.SeqDesc)) if h.seqs.size else None
+    if h.action_kind == 0:
+        vh.act_cont = None
+    return vh, keep
+
+
+class RolloutView:
+    """Device-resident RolloutView handle (rollout.hpp:33-78)."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    @staticmethod
+    def from_host(hv: HostView, ctx: Context | None = None) -> "RolloutView":
+        ctx = ctx or default_context()
+        vh, keep = _viewhost(hv)
+        out = C.c_void_p()
+        _check(_lib().ver_view_upload(ctx.h, C.byref(vh), C.byref(out)))
+        del keep
+        return RolloutView(out, ctx)
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().ver_view_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def info(self) -> L.ViewHost:
+        vh = L.ViewHost()
+        _check(_lib().ver_view_info(self.h, C.byref(vh)))
+        return vh
+
+    def size(self) -> int:
+        return self.info().size
+
+    def fresh_steps(self) -> int:
+        i = self.info()
+        return i.size - i.replayed_steps
+
+    @property
+    def deficit(self) -> int:
+        return self.info().deficit
+
+    @property
+    def stale_steps(self) -> int:
+        return self.info().stale_steps
+
+    def to_host(self) -> HostView:
+        i = self.info()
+        hv = HostView.empty(i.T, i.N, i.action_kind, i.obs_dim, i.act_dim, i.hidden_dim, i.size,
+                            i.num_seqs, i.h0_rows, fdtype=np.float32)
+        hv.deficit, hv.stale_steps, hv.replayed_steps = i.deficit, i.stale_steps, i.replayed_steps
+        hv.snapshot_version, hv.collect_wall_time = i.snapshot_version, i.collect_wall_time
+        vh, _ = _viewhost(hv, copy=False)
+        _check(_lib().ver_view_download(self.h, C.byref(vh)))
+        return hv
+
+    def clone(self) -> "RolloutView":
+        out = C.c_void_p()
+        _check(_lib().ver_view_clone(self.h, C.byref(out)))
+        return RolloutView(out, self.ctx)
+
+    def restale(self, learner_version: int):
+        _check(_lib().ver_view_restale(self.h, learner_version))
+
+
+# ------------------------------------------------------------- rollout store
+FIXED, VARIABLE = 0, 1
+ACCEPTED, ROLLOUT_FULL = 0, 1
+
+
+@dataclass
+class StepRecords:
+    """A batch of EnvStepRecords (types.hpp:54-67) in arrival order (SoA)."""
+    env_index: np.ndarray
+    obs: np.ndarray
+    log_prob: np.ndarray
+    value: np.ndarray
+    reward: np.ndarray
+    done: np.ndarray
+    act_disc: np.ndarray | None = None
+    act_cont: np.ndarray | None = None
+    episode_index: np.ndarray | None = None
+    step_in_episode: np.ndarray | None = None
+    latency: np.ndarray | None = None
+    h_before: np.ndarray | None = None
+    h_before_valid: np.ndarray | None = None
+    snapshot_version: np.ndarray | None = None
+
+    def __len__(self):
+        return int(np.asarray(self.env_index).shape[0])
+
+
+class RolloutBuffer:
+    """rollout.hpp:87-142 over the device store."""
+
+    def __init__(self, T: int, N: int, mode: int = VARIABLE, action_kind: int = 0, obs_dim: int = 1,
+                 act_dim: int = 0, hidden_dim: int = 0, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.cfg = L.RolloutConfig(T, N, mode, action_kind, obs_dim, act_dim, hidden_dim)
+        self.h = C.c_void_p()
+        _check(_lib().ver_rollout_create(self.ctx.h, C.byref(self.cfg), C.byref(self.h)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().ver_rollout_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def begin_rollout(self, snapshot_version: int):
+        _check(_lib().ver_rollout_begin(self.h, snapshot_version))
+
+    def append_steps(self, recs: StepRecords) -> np.ndarray:
+        n = len(recs)
+        keep = []
+
+        def arr(x, dt, shape=None):
+            if x is None:
+                return None
+            a = np.ascontiguousarray(x, dtype=dt)
+            keep.append(a)
+            return a
+
+        b = L.StepBatch()
+        b.n = n
+        b.env_index = _ptr(arr(recs.env_index, np.int32), C.c_int32)
+        b.episode_index = _ptr(arr(recs.episode_index, np.int64), C.c_int64)
+        b.step_in_episode = _ptr(arr(recs.step_in_episode, np.int32), C.c_int32)
+        b.obs = _ptr(arr(recs.obs, np.float32), C.c_float)
+        b.act_disc = _ptr(arr(recs.act_disc, np.int32), C.c_int32)
+        b.act_cont = _ptr(arr(recs.act_cont, np.float32), C.c_float)
+        b.log_prob = _ptr(arr(recs.log_prob, np.float32), C.c_float)
+        b.value = _ptr(arr(recs.value, np.float32), C.c_float)
+        b.reward = _ptr(arr(recs.reward, np.float32), C.c_float)
+        b.latency = _ptr(arr(recs.latency, np.float32), C.c_float)
+        b.done = _ptr(arr(recs.done, np.uint8), C.c_uint8)
+        b.h_before = _ptr(arr(recs.h_before, np.float32), C.c_float)
+        b.h_before_valid = _ptr(arr(recs.h_before_valid, np.uint8), C.c_uint8)
+        b.snapshot_version = _ptr(arr(recs.snapshot_version, np.uint64), C.c_uint64)
+        out = np.zeros(n, np.int32)
+        _check(_lib().ver_rollout_append(self.h, C.byref(b), _ptr(out, C.c_int32)))
+        return out
+
+    def append_step(self, env: int, episode: int, t: int, obs, action, log_prob: float, value: float,
+                    reward: float, done: bool, latency: float = 0.0, h_before=None,
+                    snapshot_version: int = 0) -> int:
+        cont = self.cfg.action_kind == 1
+        recs = StepRecords(
+            env_index=np.array([env]), obs=np.asarray(obs, np.float32).reshape(1, -1),
+            log_prob=np.array([log_prob]), value=np.array([value]), reward=np.array([reward]),
+            done=np.array([1 if done else 0]),
+            act_disc=None if cont else np.array([int(action)]),
+            act_cont=np.asarray(action, np.float32).reshape(1, -1) if cont else None,
+            episode_index=np.array([episode]), step_in_episode=np.array([t]),
+            latency=np.array([latency]),
+            h_before=None if h_before is None else np.asarray(h_before, np.float32).reshape(1, -1),
+            snapshot_version=np.array([snapshot_version], np.uint64))
+        return int(self.append_steps(recs)[0])
+
+    def force_close(self):
+        _check(_lib().ver_rollout_force_close(self.h))
+
+    def set_bootstrap(self, env: int, value: float):
+        _check(_lib().ver_rollout_set_bootstrap(self.h, env, value))
+
+    def _state(self):
+        o, c, k = C.c_int(), C.c_int(), C.c_int()
+        _check(_lib().ver_rollout_state(self.h, C.byref(o), C.byref(c), C.byref(k)))
+        return o.value, c.value, k.value
+
+    def open(self) -> bool:
+        return bool(self._state()[0])
+
+    def committed(self) -> int:
+        return self._state()[1]
+
+    def carryover_count(self) -> int:
+        return self._state()[2]
+
+    def capacity(self) -> int:
+        return self.cfg.T * self.cfg.N
+
+    def close_rollout(self) -> RolloutView:
+        out = C.c_void_p()
+        _check(_lib().ver_rollout_close(self.h, C.byref(out)))
+        return RolloutView(out, self.ctx)
+
+
+def backfill_stale(view: RolloutView, prev: RolloutView, deficit: int):
+    _check(_lib().ver_backfill_stale(view.h, prev.h, deficit))
+
+
+def compute_gae(view: RolloutView, gamma: float, lam: float):
+    _check(_lib().ver_compute_gae(view.h, gamma, lam))
+
+
+# ------------------------------------------------------------------ sampler
+def _seqs_from(arr: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(arr, dtype=np.int32).reshape(-1, 8))
+
+
+class SequenceGroup:
+    """packseq.hpp:12-15.  Either a slice of a device deal or explicit host pieces."""
+
+    def __init__(self, seqs: np.ndarray | None = None, total_steps: int | None = None,
+                 _groups=None, _b: int = -1):
+        self._groups = _groups
+        self._b = _b
+        if seqs is not None:
+            self._seqs = _seqs_from(seqs)
+            self.total_steps = int(self._seqs[:, 2].sum()) if total_steps is None else total_steps
+        else:
+            n, tot = C.c_int(), C.c_int()
+            _check(_lib().ver_groups_get(_groups.h, _b, C.byref(n), C.byref(tot), None))
+            self._seqs = None
+            self._n = n.value
+            self.total_steps = tot.value
+
+    @property
+    def seqs(self) -> np.ndarray:
+        if self._seqs is None:
+            a = np.zeros((self._n, 8), np.int32)
+            if self._n:
+                _check(_lib().ver_groups_get(self._groups.h, self._b, None, None,
+                                             a.ctypes.data_as(C.POINTER(L.SeqDesc))))
+            self._seqs = a
+        return self._seqs
+
+    def __len__(self):
+        return self._n if self._seqs is None else self._seqs.shape[0]
+
+
+class _Groups:
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().ver_groups_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+
+def _groups_list(h) -> list[SequenceGroup]:
+    g = _Groups(h)
+    B = C.c_int()
+    _check(_lib().ver_groups_count(h, C.byref(B)))
+    return [SequenceGroup(_groups=g, _b=b) for b in range(B.value)]
+
+
+def split_minibatches(view: RolloutView, B: int, seed: int) -> list[SequenceGroup]:
+    out = C.c_void_p()
+    _check(_lib().ver_split_minibatches(view.h, B, seed, C.byref(out)))
+    return _groups_list(out)
+
+
+def split_in_order(view: RolloutView, B: int, order: Sequence[int]) -> list[SequenceGroup]:
+    o = np.ascontiguousarray(order, dtype=np.int32)
+    out = C.c_void_p()
+    _check(_lib().ver_split_in_order(view.h, B, _ptr(o, C.c_int32), o.size, C.byref(out)))
+    return _groups_list(out)
+
+
+class PackedBatch:
+    """packseq.hpp:20-29 (device) + the gathered time-major learner fields."""
+
+    def __init__(self, h, view: RolloutView):
+        self.h = h
+        self.view = view
+        k, L_, S = C.c_int(), C.c_int(), C.c_int()
+        _check(_lib().ver_packed_info(h, C.byref(k), C.byref(L_), C.byref(S)))
+        self.num_seqs, self._max_len, self.total_steps = k.value, L_.value, S.value
+        self._cache = None
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().ver_packed_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def max_len(self) -> int:
+        return self._max_len
+
+    def _load(self):
+        if self._cache is None:
+            seqs = np.zeros((self.num_seqs, 8), np.int32)
+            s2g = np.zeros(self.num_seqs, np.int32)
+            bs = np.zeros(self._max_len, np.int32)
+            offs = np.zeros(self._max_len, np.int32)
+            slots = np.zeros(self.total_steps, np.int32)
+            _check(_lib().ver_packed_get(self.h, seqs.ctypes.data_as(C.POINTER(L.SeqDesc)),
+                                         _ptr(s2g, C.c_int32), _ptr(bs, C.c_int32),
+                                         _ptr(offs, C.c_int32), _ptr(slots, C.c_int32)))
+            self._cache = (seqs, s2g, bs, offs, slots)
+        return self._cache
+
+    @property
+    def seqs(self):
+        return self._load()[0]
+
+    @property
+    def sorted_to_group(self):
+        return self._load()[1]
+
+    @property
+    def batch_sizes(self):
+        return self._load()[2]
+
+    @property
+    def offsets(self):
+        return self._load()[3]
+
+    @property
+    def slots(self):
+        return self._load()[4]
+
+    def gathered(self, obs_dim: int, action_kind: int = 0, act_dim: int = 0) -> dict:
+        S = self.total_steps
+        obs = np.zeros((S, obs_dim), np.float32)
+        act = np.zeros(S, np.int32) if action_kind == 0 else None
+        actc = np.zeros((S, act_dim), np.float32) if action_kind == 1 else None
+        lp, adv, ret = (np.zeros(S, np.float32) for _ in range(3))
+        _check(_lib().ver_packed_get_gathered(self.h, _ptr(obs, C.c_float), _ptr(act, C.c_int32),
+                                              _ptr(actc, C.c_float), _ptr(lp, C.c_float),
+                                              _ptr(adv, C.c_float), _ptr(ret, C.c_float)))
+        return dict(obs=obs, act_disc=act, act_cont=actc, old_logp=lp, adv=adv, ret=ret)
+
+
+def pack(view: RolloutView, group: SequenceGroup) -> PackedBatch:
+    out = C.c_void_p()
+    if group._groups is not None:
+        _check(_lib().ver_pack(view.h, group._groups.h, group._b, C.byref(out)))
+    else:
+        s = group._seqs
+        _check(_lib().ver_pack_seqs(view.h, s.ctypes.data_as(C.POINTER(L.SeqDesc)) if s.size else None,
+                                    s.shape[0], C.byref(out)))
+    return PackedBatch(out, view)
+
+
+def unpack(batch: PackedBatch) -> list[list[int]]:
+    """packseq.cpp:90-101 — test oracle over the downloaded layout."""
+    seqs, s2g, bs, offs, slots = batch._load()
+    out: list[list[int]] = [[] for _ in range(batch.num_seqs)]
+    for j in range(batch.num_seqs):
+        gi = int(s2g[j])
+        out[gi] = [int(slots[offs[t] + j]) for t in range(int(seqs[j, 2]))]
+    return out
+
+
+# ------------------------------------------------------------------- model
+@dataclass
+class ModelConfig:
+    obs_dim: int
+    encoder_dim: int = 64
+    hidden_dim: int = 64
+    action_kind: int = 0
+    num_actions: int = 0
+    act_dim: int = 0
+
+    def c(self) -> L.ModelConfig:
+        return L.ModelConfig(self.obs_dim, self.encoder_dim, self.hidden_dim, self.action_kind,
+                             self.num_actions, self.act_dim)
+
+
+def param_count(cfg: ModelConfig) -> int:
+    n = C.c_int64()
+    _check(_lib().ver_param_count(C.byref(cfg.c()), C.byref(n), None))
+    return n.value
+
+
+def param_tensors(cfg: ModelConfig) -> list[tuple[str, int, int, int]]:
+    """[(name, rows, cols, offset)] in PolicyParams::tensors() order."""
+    nt = C.c_int()
+    _check(_lib().ver_param_count(C.byref(cfg.c()), None, C.byref(nt)))
+    out = []
+    for i in range(nt.value):
+        name = C.create_string_buffer(16)
+        r, c_, o = C.c_int(), C.c_int(), C.c_int64()
+        _check(_lib().ver_param_tensor(C.byref(cfg.c()), i, name, C.byref(r), C.byref(c_), C.byref(o)))
+        out.append((name.value.decode(), r.value, c_.value, o.value))
+    return out
+
+
+def params_init(cfg: ModelConfig, seed: int) -> np.ndarray:
+    """PolicyParams::init (nn.cpp:16-81) — flat float64 in tensors() order."""
+    out = np.zeros(param_count(cfg), np.float64)
+    _check(_lib().ver_params_init(C.byref(cfg.c()), seed, _ptr(out, C.c_double)))
+    return out
+
+
+@dataclass
+class PPOConfig:
+    gamma: float = 0.99
+    gae_lambda: float = 0.95
+    clip: float = 0.2
+    epochs: int = 3
+    minibatches: int = 2
+    value_loss_coef: float = 0.5
+    is_cap: float = 1.0
+
+    def c(self) -> L.PPOConfig:
+        return L.PPOConfig(self.gamma, self.gae_lambda, self.clip, self.epochs, self.minibatches,
+                           self.value_loss_coef, self.is_cap)
+
+
+@dataclass
+class EntropyController:
+    """learner.hpp:29-40."""
+    alpha: float = 1e-3
+    target: float = 0.0
+    lower: float = 1e-4
+    upper: float = 1.0
+    lr: float = 2.5e-4
+
+    def update(self, mean_entropy: float):
+        self.alpha += self.lr * (self.target - mean_entropy)
+        self.alpha = min(max(self.alpha, self.lower), self.upper)
+
+    def c(self) -> L.EntropyController:
+        return L.EntropyController(self.alpha, self.target, self.lower, self.upper, self.lr)
+
+
+def entropy_loss_value(mean_entropy: float, c: EntropyController) -> float:
+    return c.alpha * (c.target - mean_entropy) - c.alpha * mean_entropy
+
+
+@dataclass
+class CosineSchedule:
+    base_lr: float = 2.5e-4
+    total_steps: int = 1
+
+    def lr_at(self, consumed: int) -> float:
+        return _lib().ver_cosine_lr(self.base_lr, self.total_steps, consumed)
+
+
+@dataclass
+class PPOLossResult:
+    loss: float
+    policy_loss: float
+    value_loss: float
+    mean_entropy: float
+    ratio_sum: float
+    clip_count: float
+    w_sum: float
+    w_max: float
+    steps: int
+    is_weights: np.ndarray
+    grads: np.ndarray | None
+
+
+def ppo_loss(cfg: ModelConfig, params: np.ndarray, view: RolloutView, batch: PackedBatch,
+             ppo: PPOConfig, alpha: float, h0_sorted: np.ndarray, want_grads: bool = True,
+             frozen_is_weights: np.ndarray | None = None,
+             ctx: Context | None = None) -> PPOLossResult:
+    ctx = ctx or view.ctx
+    p = _f32(params)
+    h0 = _f32(h0_sorted)
+    fw = None if frozen_is_weights is None else _f32(frozen_is_weights).reshape(-1)
+    res = L.LossResult()
+    grads = np.zeros(p.size, np.float32) if want_grads else None
+    isw = np.zeros(batch.total_steps, np.float32)
+    _check(_lib().ver_ppo_loss(ctx.h, C.byref(cfg.c()), _ptr(p, C.c_float), view.h, batch.h,
+                               C.byref(ppo.c()), alpha, _ptr(h0, C.c_float), int(want_grads),
+                               _ptr(fw, C.c_float), C.byref(res), _ptr(grads, C.c_float),
+                               _ptr(isw, C.c_float)))
+    return PPOLossResult(res.loss, res.policy_loss, res.value_loss, res.mean_entropy, res.ratio_sum,
+                         res.clip_count, res.w_sum, res.w_max, res.steps, isw, grads)
+
+
+def forward_packed(cfg: ModelConfig, params: np.ndarray, obs: np.ndarray, act_disc, act_cont,
+                   batch_sizes, offsets, h0: np.ndarray, ctx: Context | None = None):
+    """nn.cpp:219-280 -> (log_prob, entropy, value) per packed row."""
+    ctx = ctx or default_context()
+    obs = _f32(obs).reshape(-1, cfg.obs_dim)
+    S = obs.shape[0]
+    bs = np.ascontiguousarray(batch_sizes, np.int32)
+    of = np.ascontiguousarray(offsets, np.int32)
+    h0 = _f32(h0).reshape(-1, cfg.hidden_dim)
+    ad = None if act_disc is None else np.ascontiguousarray(act_disc, np.int32)
+    ac = None if act_cont is None else _f32(act_cont)
+    lp, en, va = (np.zeros(S, np.float32) for _ in range(3))
+    p = _f32(params)
+    _check(_lib().ver_forward_packed(ctx.h, C.byref(cfg.c()), _ptr(p, C.c_float), S, _ptr(obs, C.c_float),
+                                     _ptr(ad, C.c_int32), _ptr(ac, C.c_float), bs.size, _ptr(bs, C.c_int32),
+                                     _ptr(of, C.c_int32), _ptr(h0, C.c_float), _ptr(lp, C.c_float),
+                                     _ptr(en, C.c_float), _ptr(va, C.c_float)))
+    return lp, en, va
+
+
+def act(cfg: ModelConfig, params: np.ndarray, obs: np.ndarray, h: np.ndarray,
+        ctx: Context | None = None):
+    """nn.cpp:118-126 -> (dist, value, h_new)."""
+    ctx = ctx or default_context()
+    obs = _f32(obs).reshape(-1, cfg.obs_dim)
+    h = _f32(h).reshape(-1, cfg.hidden_dim)
+    n = obs.shape[0]
+    A = cfg.num_actions if cfg.action_kind == 0 else cfg.act_dim
+    dist = np.zeros((n, A), np.float32)
+    val = np.zeros(n, np.float32)
+    hn = np.zeros((n, cfg.hidden_dim), np.float32)
+    p = _f32(params)
+    _check(_lib().ver_act(ctx.h, C.byref(cfg.c()), _ptr(p, C.c_float), n, _ptr(obs, C.c_float),
+                          _ptr(h, C.c_float), _ptr(dist, C.c_float), _ptr(val, C.c_float),
+                          _ptr(hn, C.c_float)))
+    return dist, val, hn
+
+
+def adam_step(params: np.ndarray, grads: np.ndarray, m: np.ndarray, v: np.ndarray, step: int,
+              lr: float, ctx: Context | None = None) -> int:
+    """nn.cpp:291-306 on float32 arrays in place; returns the new step."""
+    ctx = ctx or default_context()
+    for a in (params, m, v):
+        assert a.dtype == np.float32 and a.flags.c_contiguous
+    g = _f32(grads)
+    s = C.c_int64(step)
+    _check(_lib().ver_adam_step(ctx.h, params.size, _ptr(params, C.c_float), _ptr(g, C.c_float),
+                                _ptr(m, C.c_float), _ptr(v, C.c_float), C.byref(s), lr))
+    return s.value
+
+
+@dataclass
+class TrainStats:
+    update_index: int
+    steps: int
+    fresh_steps: int
+    stale_steps: int
+    loss: float
+    policy_loss: float
+    value_loss: float
+    entropy: float
+    entropy_loss: float
+    mean_ratio: float
+    clip_fraction: float
+    mean_is_weight: float
+    max_is_weight: float
+    alpha: float
+    lr: float
+
+
+PHASES = ("gae", "sampler", "replay", "forward", "loss", "backward", "allreduce", "adam")
+
+
+class Learner:
+    """learner.hpp:102-138 — owns params, Adam state and alpha on the device."""
+
+    def __init__(self, cfg: ModelConfig, params: np.ndarray, ppo: PPOConfig = PPOConfig(),
+                 entropy: EntropyController = EntropyController(),
+                 schedule: CosineSchedule = CosineSchedule(), run_seed: int = 0,
+                 ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.cfg = cfg
+        self.ppo = ppo
+        self.entropy_cfg = entropy
+        self.h = C.c_void_p()
+        p = _f32(params)
+        _check(_lib().ver_learner_create(self.ctx.h, C.byref(cfg.c()), _ptr(p, C.c_float),
+                                         C.byref(ppo.c()), C.byref(entropy.c()), schedule.base_lr,
+                                         schedule.total_steps, run_seed, C.byref(self.h)))
+        self.P = p.size
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().ver_learner_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def enable_allreduce(self, on: bool = True):
+        _check(_lib().ver_learner_enable_allreduce(self.h, int(on)))
+
+    def update(self, view: RolloutView, read_stats: bool = True) -> TrainStats | None:
+        if not read_stats:
+            _check(_lib().ver_learner_update(self.h, view.h, None))
+            return None
+        s = L.TrainStats()
+        _check(_lib().ver_learner_update(self.h, view.h, C.byref(s)))
+        return TrainStats(*(getattr(s, f) for f, _ in L.TrainStats._fields_))
+
+    def batch_h0(self, view: RolloutView, batch: PackedBatch) -> np.ndarray:
+        out = np.zeros((batch.num_seqs, self.cfg.hidden_dim), np.float32)
+        _check(_lib().ver_learner_batch_h0(self.h, view.h, batch.h, _ptr(out, C.c_float)))
+        return out
+
+    def params(self) -> np.ndarray:
+        out = np.zeros(self.P, np.float32)
+        _check(_lib().ver_learner_get_params(self.h, _ptr(out, C.c_float)))
+        return out
+
+    def set_params(self, p: np.ndarray):
+        p = _f32(p)
+        _check(_lib().ver_learner_set_params(self.h, _ptr(p, C.c_float)))
+
+    def adam(self):
+        m = np.zeros(self.P, np.float32)
+        v = np.zeros(self.P, np.float32)
+        s = C.c_int64()
+        _check(_lib().ver_learner_get_adam(self.h, _ptr(m, C.c_float), _ptr(v, C.c_float), C.byref(s)))
+        return m, v, s.value
+
+    def set_adam(self, m, v, step: int):
+        m, v = _f32(m), _f32(v)
+        _check(_lib().ver_learner_set_adam(self.h, _ptr(m, C.c_float), _ptr(v, C.c_float), step))
+
+    def _state(self):
+        a, c, u = C.c_double(), C.c_int64(), C.c_int64()
+        _check(_lib().ver_learner_get_state(self.h, C.byref(a), C.byref(c), C.byref(u)))
+        return a.value, c.value, u.value
+
+    @property
+    def alpha(self) -> float:
+        return self._state()[0]
+
+    def consumed_steps(self) -> int:
+        return self._state()[1]
+
+    def update_index(self) -> int:
+        return self._state()[2]
+
+    def set_state(self, alpha=None, consumed=None, update_index=None):
+        a, c, u = self._state()
+        _check(_lib().ver_learner_set_state(self.h, a if alpha is None else alpha,
+                                            c if consumed is None else consumed,
+                                            u if update_index is None else update_index))
+
+    def set_consumed_steps(self, n: int):
+        self.set_state(consumed=n)
+
+    def set_update_index(self, n: int):
+        self.set_state(update_index=n)
+
+    def last_timing(self) -> dict:
+        ms = (C.c_float * 16)()
+        n = C.c_int(16)
+        _check(_lib().ver_learner_last_timing(self.h, ms, C.byref(n)))
+        return {PHASES[i]: float(ms[i]) for i in range(min(n.value, len(PHASES)))}
+
+
+# ---------------------------------------------------------- distributed
+def estimate_time(step_times, max_steps: int, steps: int, ctx: Context | None = None) -> float:
+    ctx = ctx or default_context()
+    t = np.ascontiguousarray(step_times, dtype=np.float64)
+    out = C.c_double()
+    _check(_lib().ver_estimate_time(ctx.h, _ptr(t, C.c_double), t.size, max_steps, steps, C.byref(out)))
+    return out.value
+
+
+def optimal_preempt_steps(step_times, learn_time: float, max_steps: int,
+                          ctx: Context | None = None) -> int:
+    ctx = ctx or default_context()
+    t = np.ascontiguousarray(step_times, dtype=np.float64)
+    out = C.c_int64()
+    _check(_lib().ver_optimal_preempt_steps(ctx.h, _ptr(t, C.c_double), t.size, learn_time, max_steps,
+                                            C.byref(out)))
+    return out.value
+
+
+__all__ = [n for n in dir() if not n.startswith("_")] + ["SEQ_FIELDS"]

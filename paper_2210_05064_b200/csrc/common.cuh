@@ -1,0 +1,167 @@
+// common.cuh — shared plumbing of the VER learner library: status/error
+// handling, the per-device context (stream, pool, launch accounting, NCCL),
+// stream-ordered device buffers and small launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ver_gpu.h"
+
+namespace verg {
+
+// ------------------------------------------------------------------ errors
+// Exceptions never cross the C-ABI: every entry point catches and maps them.
+struct Error : std::runtime_error {
+  ver_status code;
+  Error(ver_status c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+[[noreturn]] inline void protocol_error(const std::string& w) { throw Error(VER_ERR_PROTOCOL, w); }
+[[noreturn]] inline void config_error(const std::string& w) { throw Error(VER_ERR_CONFIG, w); }
+
+void set_last_error(const std::string& w);
+
+#define VER_CUDA(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e__ = (expr);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      throw ::verg::Error(VER_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define VER_NCCL(expr)                                                                  \
+  do {                                                                                  \
+    ncclResult_t r__ = (expr);                                                          \
+    if (r__ != ncclSuccess)                                                             \
+      throw ::verg::Error(VER_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r__)); \
+  } while (0)
+
+// Wraps the body of a C-ABI entry point.
+#define VER_API_BEGIN try {
+#define VER_API_END                                       \
+  return VER_OK;                                          \
+  }                                                       \
+  catch (const ::verg::Error& e) {                        \
+    ::verg::set_last_error(e.what());                     \
+    return e.code;                                        \
+  }                                                       \
+  catch (const std::exception& e) {                       \
+    ::verg::set_last_error(e.what());                     \
+    return VER_ERR_CONFIG;                                \
+  }
+
+// --------------------------------------------------------------- context
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;  // kernels launched by this library on `stream`
+  int precision = 0;     // 0 fp32 parity, 1 bf16 tensor cores
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  // pinned scratch for small synchronous reads
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* pinned_buf(size_t bytes);
+};
+
+// Make the ctx's device current for this thread (entry points call this).
+void activate(Ctx* c);
+
+// ---------------------------------------------------------------- buffers
+// Device buffer allocated from the stream-ordered pool of ctx's device.
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;  // capacity in elements
+  Ctx* ctx = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      ctx = o.ctx;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p && ctx) cudaFreeAsync(p, ctx->stream);
+    p = nullptr;
+    n = 0;
+  }
+  // grow to at least `count` elements (contents not preserved)
+  void reserve(Ctx* c, size_t count) {
+    if (count <= n && ctx == c) return;
+    release();
+    ctx = c;
+    size_t want = count ? count : 1;
+    VER_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), want * sizeof(T), c->stream));
+    n = want;
+  }
+  // grow preserving the first `keep` elements
+  void grow_keep(Ctx* c, size_t count, size_t keep) {
+    if (count <= n && ctx == c) return;
+    T* q = nullptr;
+    size_t want = count ? count : 1;
+    VER_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&q), want * sizeof(T), c->stream));
+    if (p && keep)
+      VER_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+    release();
+    ctx = c;
+    p = q;
+    n = want;
+  }
+  void zero(size_t count) {
+    if (count) VER_CUDA(cudaMemsetAsync(p, 0, count * sizeof(T), ctx->stream));
+  }
+  void upload(const T* h, size_t count) {
+    if (count) VER_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  void download(T* h, size_t count) const {
+    if (count && h)
+      VER_CUDA(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+};
+
+inline void sync(Ctx* c) { VER_CUDA(cudaStreamSynchronize(c->stream)); }
+
+inline unsigned cdiv(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// Launch accounting + error check after every kernel launch.
+inline void after_launch(Ctx* c) {
+  c->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(VER_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------- scans etc.
+// Exclusive scan of n int32 on ctx's stream (out may alias in).  If total is
+// non-null it receives the sum (device).  Implemented in util.cu.
+void exclusive_scan_i32(Ctx* c, const int32_t* in, int32_t* out, int64_t n, int32_t* total);
+// Exclusive scan of n uint8 flags into int32.
+void exclusive_scan_u8(Ctx* c, const uint8_t* in, int32_t* out, int64_t n, int32_t* total);
+// Ascending sort of n unique uint64 keys in place (bitonic; n arbitrary).
+void sort_u64(Ctx* c, uint64_t* keys, int64_t n);
+// Ascending sort of n non-negative doubles (as uint64 bit patterns) in place.
+inline void sort_pos_f64(Ctx* c, double* keys, int64_t n) {
+  sort_u64(c, reinterpret_cast<uint64_t*>(keys), n);
+}
+
+}  // namespace verg
+
+// The opaque handle types of the C-ABI.
+struct ver_ctx_s {
+  verg::Ctx c;
+};

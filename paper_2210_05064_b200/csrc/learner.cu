@@ -1,0 +1,699 @@
+// learner.cu — Learner::update (learner.cpp:146-193) and its pieces on the
+// device: GAE -> per epoch split -> per minibatch pack/gather -> split-tail
+// h0 replay (learner.cpp:119-130) -> forward -> fused loss -> backward ->
+// NCCL gradient AllReduce (DD-PPO, distributed.cpp:86-116, with the mean
+// entropy riding in the same buffer, :103-116) -> Adam + log_std clamp ->
+// entropy-controller update (learner.hpp:36-39).  Parameters, Adam moments,
+// alpha and all statistics stay on the device for the whole update; the
+// host reads back once at the end.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "policy.cuh"
+
+namespace verg {
+
+void compute_gae(DView& V, double gamma, double lambda);
+DGroups* split_minibatches(DView& V, int B, uint64_t seed);
+std::vector<int32_t> shuffle_perm(int n, uint64_t seed);
+
+namespace {
+inline uint64_t splitmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+inline uint64_t mix64(uint64_t a, uint64_t b) {
+  return splitmix(a ^ (0x9e3779b97f4a7c15ull + (b << 6) + (b >> 2) + splitmix(b)));
+}
+}  // namespace
+
+enum Phase { PH_GAE, PH_SAMPLER, PH_REPLAY, PH_FORWARD, PH_LOSS, PH_BACKWARD, PH_ALLREDUCE, PH_ADAM, PH_N };
+
+struct Learner {
+  Ctx* ctx = nullptr;
+  ver_model_config mc{};
+  Model m;
+  ver_ppo_config cfg{};
+  ver_entropy_controller ec{};
+  double base_lr = 2.5e-4;
+  int64_t total_steps = 1;
+  uint64_t run_seed = 0;
+  int64_t consumed = 0, update_index = 0, adam_step = 0;
+  bool allreduce = false;
+  DBuf<float> params, grad, mom, vel;
+  DBuf<double> alpha;        // entropy coefficient (device)
+  DBuf<double> acc;          // per-update statistics accumulator
+  DBuf<LossStats> lstats;
+  DBuf<int> flags;           // [0] non-finite parameters
+  Workspace ws, wr;          // minibatch / h0-replay workspaces
+  DBuf<float> h0s;           // sorted h0 of the current minibatch
+  // per-phase timing of the last update
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::pair<int, int>> ev_pairs;  // (phase, event index of start)
+  float phase_ms[PH_N] = {};
+  bool timing = true;
+
+  void mark_begin(int phase) {
+    if (!timing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ctx->stream);
+    ev.push_back(e);
+    ev_pairs.push_back({phase, (int)ev.size() - 1});
+  }
+  void mark_end() {
+    if (!timing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ctx->stream);
+    ev.push_back(e);
+  }
+  void collect_timing() {
+    for (int k = 0; k < PH_N; ++k) phase_ms[k] = 0.f;
+    for (auto& pr : ev_pairs) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[pr.second], ev[pr.second + 1]);
+      phase_ms[pr.first] += ms;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    ev.clear();
+    ev_pairs.clear();
+  }
+};
+
+// -------------------------------------------------------------- kernels
+__global__ void h0_gather_kernel(const ver_seq_desc* __restrict__ seqs, int k, const float* __restrict__ h0,
+                                 int H, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)k * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  out[i] = h0[(size_t)seqs[j].h0_index * H + u];
+}
+
+// replay batch rows: row offr[t] + i = view.obs[parent_i + t]
+__global__ void replay_obs_kernel(const int32_t* __restrict__ offr, int L, const int32_t* __restrict__ parent,
+                                  int R, const float* __restrict__ vobs, int D, float* __restrict__ out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= R) return;
+  int lo = 0, hi = L;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (offr[mid] <= p) lo = mid;
+    else hi = mid;
+  }
+  const int t = lo, i = p - offr[t];
+  const int s = parent[i] + t;
+  for (int d = 0; d < D; ++d) out[(size_t)p * D + d] = vobs[(size_t)s * D + d];
+}
+__global__ void replay_h0_kernel(const int32_t* __restrict__ h0_index, int n, const float* __restrict__ vh0, int H,
+                                 float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  out[i] = vh0[(size_t)h0_index[j] * H + u];
+}
+__global__ void replay_final_kernel(const int32_t* __restrict__ last_row, const int32_t* __restrict__ dst, int n,
+                                    const float* __restrict__ hidden, int H, float* __restrict__ h0s) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  h0s[(size_t)dst[j] * H + u] = hidden[(size_t)last_row[j] * H + u];
+}
+
+__global__ void alpha_update_kernel(double* __restrict__ alpha, const LossStats* __restrict__ st,
+                                    const float* __restrict__ ent_avg, double target, double lr, double lo,
+                                    double hi) {
+  // EntropyController::update (learner.hpp:36-39)
+  const double h = ent_avg ? (double)*ent_avg : st->mean_entropy;
+  double a = *alpha + lr * (target - h);
+  *alpha = fmin(fmax(a, lo), hi);
+}
+
+// acc: loss, policy, value, entropy, ratio_sum, clip, w_sum, w_max, steps, batches
+__global__ void stats_accum_kernel(double* __restrict__ acc, const LossStats* __restrict__ st) {
+  acc[0] += st->loss;
+  acc[1] += st->policy_loss;
+  acc[2] += st->value_loss;
+  acc[3] += st->mean_entropy;
+  acc[4] += st->ratio_sum;
+  acc[5] += st->clip_count;
+  acc[6] += st->w_sum;
+  acc[7] = fmax(acc[7], st->w_max);
+  acc[8] += st->steps;
+  acc[9] += 1.0;
+}
+
+// ------------------------------------------------------------ batch_h0
+// learner.cpp:119-130.  Pieces with skip > 0 (split tails) replay `skip`
+// steps of act() from parent_start_offset with the current parameters; all
+// tails of a minibatch replay together as one packed GRU forward sorted by
+// skip (descending), so the replay costs max(skip) recurrent steps.
+static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, float* h0s) {
+  Ctx* c = Ln.ctx;
+  const int H = V.hidden_dim;
+  h0_gather_kernel<<<cdiv((size_t)P.k * H, 256), 256, 0, c->stream>>>(P.seqs.p, P.k, V.h0.p, H, h0s);
+  after_launch(c);
+  struct Tail {
+    int j, skip, parent, h0i;
+  };
+  std::vector<Tail> tails;
+  for (int j = 0; j < P.k; ++j)
+    if (P.h_seqs[j].skip > 0)
+      tails.push_back({j, P.h_seqs[j].skip, P.h_seqs[j].parent_start_offset, P.h_seqs[j].h0_index});
+  if (tails.empty()) return;
+  std::stable_sort(tails.begin(), tails.end(), [](const Tail& a, const Tail& b) { return a.skip > b.skip; });
+  const int n = (int)tails.size();
+  const int L = tails[0].skip;
+  std::vector<int32_t> bs(L), offs(L);
+  int R = 0;
+  for (int t = 0, alive = n; t < L; ++t) {
+    while (alive > 0 && tails[alive - 1].skip <= t) --alive;
+    bs[t] = alive;
+    offs[t] = R;
+    R += alive;
+  }
+  std::vector<int32_t> meta(4 * (size_t)n + L);
+  for (int i = 0; i < n; ++i) {
+    meta[i] = tails[i].parent;
+    meta[n + i] = tails[i].h0i;
+    meta[2 * n + i] = offs[tails[i].skip - 1] + i;  // row of the last replayed step
+    meta[3 * n + i] = tails[i].j;
+  }
+  std::copy(offs.begin(), offs.end(), meta.begin() + 4 * n);
+  DBuf<int32_t> dm;
+  dm.reserve(c, meta.size());
+  int32_t* pin = static_cast<int32_t*>(c->pinned_buf(sizeof(int32_t) * meta.size()));
+  std::copy(meta.begin(), meta.end(), pin);
+  dm.upload(pin, meta.size());
+  Ln.wr.ensure(Ln.m, R, false);
+  DBuf<float> robs, rh0;
+  robs.reserve(c, (size_t)R * V.obs_dim);
+  rh0.reserve(c, (size_t)n * H);
+  replay_obs_kernel<<<cdiv(R, 256), 256, 0, c->stream>>>(dm.p + 4 * n, L, dm.p, R, V.obs.p, V.obs_dim, robs.p);
+  after_launch(c);
+  replay_h0_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm.p + n, n, V.h0.p, H, rh0.p);
+  after_launch(c);
+  policy_forward(c, Ln.m, params, R, robs.p, rh0.p, bs, offs, Ln.wr, false);
+  replay_final_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm.p + 2 * n, dm.p + 3 * n, n,
+                                                                      Ln.wr.hidden.p, H, h0s);
+  after_launch(c);
+  sync(c);  // pinned staging reused by the next call
+}
+
+// ---------------------------------------------------------- minibatch
+// learner.cpp:132-144
+static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
+  Ctx* c = Ln.ctx;
+  const Model& m = Ln.m;
+  const int S = P.total;
+  Ln.h0s.reserve(c, (size_t)P.k * m.H);
+  Ln.mark_begin(PH_REPLAY);
+  batch_h0(Ln, V, P, Ln.params.p, Ln.h0s.p);
+  Ln.mark_end();
+  Ln.ws.ensure(m, S, true);
+  Ln.mark_begin(PH_FORWARD);
+  policy_forward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.h_bs, P.h_offs, Ln.ws, true);
+  Ln.mark_end();
+  LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, nullptr,
+              Ln.cfg.clip, Ln.cfg.is_cap, Ln.cfg.value_loss_coef, Ln.alpha.p};
+  Ln.mark_begin(PH_LOSS);
+  policy_loss(c, m, Ln.params.p, S, la, Ln.ws, Ln.grad.p, Ln.lstats.p, true);
+  Ln.mark_end();
+  Ln.mark_begin(PH_BACKWARD);
+  policy_backward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.h_bs, P.h_offs, Ln.ws, Ln.grad.p);
+  Ln.mark_end();
+  const bool ar = Ln.allreduce && c->comm && c->nranks > 1;
+  if (ar) {  // grad_hook -> AllReduce::average; entropy_hook -> average_scalar
+    Ln.mark_begin(PH_ALLREDUCE);
+    VER_NCCL(ncclAllReduce(Ln.grad.p, Ln.grad.p, (size_t)m.P + 1, ncclFloat32, ncclAvg, c->comm, c->stream));
+    Ln.mark_end();
+  }
+  Ln.mark_begin(PH_ADAM);
+  ++Ln.adam_step;
+  adam_update(c, m, Ln.params.p, Ln.grad.p, Ln.mom.p, Ln.vel.p, Ln.adam_step, lr, Ln.flags.p);
+  alpha_update_kernel<<<1, 1, 0, c->stream>>>(Ln.alpha.p, Ln.lstats.p, ar ? Ln.grad.p + m.P : nullptr,
+                                              Ln.ec.target, Ln.ec.lr, Ln.ec.lower, Ln.ec.upper);
+  after_launch(c);
+  stats_accum_kernel<<<1, 1, 0, c->stream>>>(Ln.acc.p, Ln.lstats.p);
+  after_launch(c);
+  Ln.mark_end();
+}
+
+
+double cosine_lr(double base, int64_t total, int64_t consumed) {  // nn.cpp:308-312
+  double progress = (double)consumed / (double)std::max<int64_t>(1, total);
+  progress = std::min(std::max(progress, 0.0), 1.0);
+  return base * 0.5 * (1.0 + std::cos(M_PI * progress));
+}
+
+// learner.cpp:146-193
+static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
+  Ctx* c = Ln.ctx;
+  if (V.obs_dim != Ln.m.D || V.hidden_dim != Ln.m.H || (V.action_kind == 1) != (Ln.m.continuous == 1))
+    config_error("learner_update: view shape does not match the model");
+  Ln.mark_begin(PH_GAE);
+  compute_gae(V, Ln.cfg.gamma, Ln.cfg.gae_lambda);
+  Ln.mark_end();
+  const double lr = cosine_lr(Ln.base_lr, Ln.total_steps, Ln.consumed);
+  Ln.acc.zero(10);
+  for (int epoch = 0; epoch < Ln.cfg.epochs; ++epoch) {
+    const uint64_t seed = mix64(mix64(Ln.run_seed, (uint64_t)Ln.update_index), (uint64_t)epoch);
+    Ln.mark_begin(PH_SAMPLER);
+    DGroups* G = split_minibatches(V, Ln.cfg.minibatches, seed);
+    Ln.mark_end();
+    std::unique_ptr<DGroups> gguard(G);
+    for (int b = 0; b < G->B; ++b) {
+      Ln.mark_begin(PH_SAMPLER);
+      DPacked* P = pack_pieces(V, G->pieces.p + G->gstart[b], G->gstart[b + 1] - G->gstart[b]);
+      Ln.mark_end();
+      std::unique_ptr<DPacked> pguard(P);
+      run_minibatch(Ln, V, *P, lr);
+    }
+  }
+  // one read-back per update
+  double* h = static_cast<double*>(c->pinned_buf(sizeof(double) * 12));
+  VER_CUDA(cudaMemcpyAsync(h, Ln.acc.p, sizeof(double) * 10, cudaMemcpyDeviceToHost, c->stream));
+  VER_CUDA(cudaMemcpyAsync(h + 10, Ln.alpha.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  VER_CUDA(cudaMemcpyAsync(h + 11, Ln.flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (Ln.timing) Ln.collect_timing();
+  const int nonfinite = reinterpret_cast<int*>(h + 11)[0];
+  if (nonfinite) {
+    Ln.flags.zero(1);
+    throw Error(VER_ERR_NONFINITE, "update: non-finite parameters");
+  }
+  if (!std::isfinite(h[0])) throw Error(VER_ERR_NONFINITE, "ppo_loss: non-finite loss");
+  if (out) {
+    const double batches = h[9], steps = h[8];
+    ver_train_stats s{};
+    s.update_index = Ln.update_index;
+    s.steps = V.size;
+    s.fresh_steps = V.size - V.replayed_steps;
+    s.stale_steps = V.stale_steps;
+    s.lr = lr;
+    s.loss = h[0] / batches;
+    s.policy_loss = h[1] / batches;
+    s.value_loss = h[2] / batches;
+    s.entropy = h[3] / batches;
+    s.mean_ratio = h[4] / steps;
+    s.clip_fraction = h[5] / steps;
+    s.mean_is_weight = h[6] / steps;
+    s.max_is_weight = h[7];
+    s.alpha = h[10];
+    // entropy_loss_value (learner.hpp:44-46) with the final alpha
+    s.entropy_loss = s.alpha * (Ln.ec.target - s.entropy) - s.alpha * s.entropy;
+    *out = s;
+  }
+  Ln.consumed += V.size - V.replayed_steps;
+  ++Ln.update_index;
+}
+
+static void to_device_layout(const Model& m, const float* tensors_order, std::vector<float>& dev) {
+  dev.assign(m.P, 0.f);
+  for (int64_t k = 0; k < m.P; ++k) dev[m.dev_index[k]] = tensors_order[k];
+}
+static void to_tensor_order(const Model& m, const float* dev, float* out) {
+  for (int64_t k = 0; k < m.P; ++k) out[k] = dev[m.dev_index[k]];
+}
+
+}  // namespace verg
+
+using namespace verg;
+
+struct ver_learner_s {
+  Learner l;
+};
+
+extern "C" {
+
+ver_status ver_param_count(const ver_model_config* c, int64_t* count, int* num_tensors) {
+  VER_API_BEGIN
+  const Model m = Model::make(*c);
+  if (count) *count = m.P;
+  if (num_tensors) *num_tensors = m.continuous ? 18 : 17;
+  VER_API_END
+}
+
+ver_status ver_param_tensor(const ver_model_config* c, int idx, char name[16], int* rows, int* cols,
+                            int64_t* offset) {
+  VER_API_BEGIN
+  static const char* names[] = {"enc_w1", "enc_b1", "enc_w2", "enc_b2", "gru_wr", "gru_ur",
+                                "gru_br", "gru_wz", "gru_uz", "gru_bz", "gru_wn", "gru_un",
+                                "gru_bn", "head_w", "head_b", "value_w", "value_b", "log_std"};
+  const Model m = Model::make(*c);
+  const int nt = m.continuous ? 18 : 17;
+  if (idx < 0 || idx >= nt) config_error("ver_param_tensor: index out of range");
+  const int D = m.D, E = m.E, H = m.H, A = m.A;
+  const int shp[18][2] = {{D, E}, {1, E}, {E, E}, {1, E}, {E, H}, {H, H}, {1, H}, {E, H}, {H, H},
+                          {1, H}, {E, H}, {H, H}, {1, H}, {H, A}, {1, A}, {H, 1}, {1, 1}, {1, A}};
+  int64_t off = 0;
+  for (int i = 0; i < idx; ++i) off += (int64_t)shp[i][0] * shp[i][1];
+  if (name) std::strncpy(name, names[idx], 16);
+  if (rows) *rows = shp[idx][0];
+  if (cols) *cols = shp[idx][1];
+  if (offset) *offset = off;
+  VER_API_END
+}
+
+ver_status ver_params_init(const ver_model_config* c, uint64_t seed, double* out) {
+  VER_API_BEGIN
+  init_params_host(*c, seed, out);
+  VER_API_END
+}
+
+double ver_cosine_lr(double base_lr, int64_t total_steps, int64_t consumed) {
+  return cosine_lr(base_lr, total_steps, consumed);
+}
+
+ver_status ver_ppo_loss(ver_ctx ctx, const ver_model_config* mc, const float* params, ver_view v, ver_packed p,
+                        const ver_ppo_config* cfg, double alpha, const float* h0_sorted, int want_grads,
+                        const float* frozen_w, ver_loss_result* out, float* grads_out, float* is_w_out) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  const Model m = Model::make(*mc);
+  DView& V = v->v;
+  DPacked& P = p->p;
+  if (V.obs_dim != m.D || V.hidden_dim != m.H) config_error("ppo_loss: view shape does not match the model");
+  const int S = P.total;
+  std::vector<float> dev;
+  to_device_layout(m, params, dev);
+  DBuf<float> dparams, grad, h0, fw;
+  DBuf<double> dalpha;
+  DBuf<LossStats> st;
+  dparams.reserve(c, m.P);
+  dparams.upload(dev.data(), m.P);
+  grad.reserve(c, m.P + 1);
+  grad.zero(m.P + 1);
+  h0.reserve(c, (size_t)P.k * m.H);
+  h0.upload(h0_sorted, (size_t)P.k * m.H);
+  dalpha.reserve(c, 1);
+  dalpha.upload(&alpha, 1);
+  st.reserve(c, 1);
+  if (frozen_w) {
+    fw.reserve(c, S);
+    fw.upload(frozen_w, S);
+  }
+  Workspace ws;
+  ws.ctx = c;
+  ws.ensure(m, S, true);
+  policy_forward(c, m, dparams.p, S, P.obs.p, h0.p, P.h_bs, P.h_offs, ws, true);
+  LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, frozen_w ? fw.p : nullptr,
+              cfg->clip, cfg->is_cap, cfg->value_loss_coef, dalpha.p};
+  policy_loss(c, m, dparams.p, S, la, ws, grad.p, st.p, want_grads != 0);
+  if (want_grads) policy_backward(c, m, dparams.p, S, P.obs.p, h0.p, P.h_bs, P.h_offs, ws, grad.p);
+  LossStats hs;
+  st.download(&hs, 1);
+  std::vector<float> g(m.P);
+  if (want_grads && grads_out) grad.download(g.data(), m.P);
+  if (is_w_out) ws.is_w.download(is_w_out, S);
+  sync(c);
+  out->loss = hs.loss;
+  out->policy_loss = hs.policy_loss;
+  out->value_loss = hs.value_loss;
+  out->mean_entropy = hs.mean_entropy;
+  out->ratio_sum = hs.ratio_sum;
+  out->clip_count = hs.clip_count;
+  out->w_sum = hs.w_sum;
+  out->w_max = hs.w_max;
+  out->steps = S;
+  if (want_grads && !std::isfinite(hs.loss)) throw Error(VER_ERR_PROTOCOL, "ppo_loss: non-finite loss");
+  if (want_grads && grads_out) to_tensor_order(m, g.data(), grads_out);
+  VER_API_END
+}
+
+ver_status ver_forward_packed(ver_ctx ctx, const ver_model_config* mc, const float* params, int S,
+                              const float* obs, const int32_t* act_disc, const float* act_cont, int L,
+                              const int32_t* batch_sizes, const int32_t* offsets, const float* h0,
+                              float* logp_out, float* ent_out, float* value_out) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  const Model m = Model::make(*mc);
+  if (S <= 0 || L <= 0) config_error("forward_packed: empty batch");
+  for (int64_t i = 0; i < (int64_t)S * m.D; ++i)
+    if (!std::isfinite(obs[i])) protocol_error("forward_packed: non-finite observations");
+  std::vector<float> dev;
+  to_device_layout(m, params, dev);
+  std::vector<int32_t> bs(batch_sizes, batch_sizes + L), offs(offsets, offsets + L);
+  DBuf<float> dparams, dobs, dh0, dac, out;
+  DBuf<int32_t> dad;
+  dparams.reserve(c, m.P);
+  dparams.upload(dev.data(), m.P);
+  dobs.reserve(c, (size_t)S * m.D);
+  dobs.upload(obs, (size_t)S * m.D);
+  dh0.reserve(c, (size_t)bs[0] * m.H);
+  dh0.upload(h0, (size_t)bs[0] * m.H);
+  if (m.continuous) {
+    dac.reserve(c, (size_t)S * m.A);
+    dac.upload(act_cont, (size_t)S * m.A);
+  } else {
+    dad.reserve(c, S);
+    dad.upload(act_disc, S);
+  }
+  out.reserve(c, (size_t)3 * S);
+  Workspace ws;
+  ws.ctx = c;
+  ws.ensure(m, S, false);
+  policy_forward(c, m, dparams.p, S, dobs.p, dh0.p, bs, offs, ws, false);
+  policy_rows(c, m, dparams.p, S, ws.hidden.p, dad.p, dac.p, out.p, out.p + S, out.p + 2 * (size_t)S);
+  if (logp_out) out.download(logp_out, S);
+  if (ent_out) VER_CUDA(cudaMemcpyAsync(ent_out, out.p + S, sizeof(float) * S, cudaMemcpyDeviceToHost, c->stream));
+  if (value_out)
+    VER_CUDA(cudaMemcpyAsync(value_out, out.p + 2 * (size_t)S, sizeof(float) * S, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  VER_API_END
+}
+
+ver_status ver_act(ver_ctx ctx, const ver_model_config* mc, const float* params, int n, const float* obs,
+                   const float* h, float* dist_out, float* value_out, float* h_new_out) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  const Model m = Model::make(*mc);
+  if (n <= 0) return VER_OK;
+  for (int64_t i = 0; i < (int64_t)n * m.D; ++i)
+    if (!std::isfinite(obs[i])) protocol_error("act: non-finite observation");
+  std::vector<float> dev;
+  to_device_layout(m, params, dev);
+  DBuf<float> dparams, dobs, dh, out;
+  dparams.reserve(c, m.P);
+  dparams.upload(dev.data(), m.P);
+  dobs.reserve(c, (size_t)n * m.D);
+  dobs.upload(obs, (size_t)n * m.D);
+  dh.reserve(c, (size_t)n * m.H);
+  dh.upload(h, (size_t)n * m.H);
+  out.reserve(c, (size_t)n * m.AH);
+  Workspace ws;
+  ws.ctx = c;
+  ws.ensure(m, n, false);
+  std::vector<int32_t> bs{n}, offs{0};
+  policy_forward(c, m, dparams.p, n, dobs.p, dh.p, bs, offs, ws, false);
+  policy_heads(c, m, dparams.p, n, ws.hidden.p, out.p);
+  std::vector<float> ho((size_t)n * m.AH);
+  out.download(ho.data(), ho.size());
+  if (h_new_out) ws.hidden.download(h_new_out, (size_t)n * m.H);
+  sync(c);
+  for (int i = 0; i < n; ++i) {
+    if (dist_out)
+      for (int a = 0; a < m.A; ++a) dist_out[(size_t)i * m.A + a] = ho[(size_t)i * m.AH + a];
+    if (value_out) value_out[i] = ho[(size_t)i * m.AH + m.A];
+  }
+  VER_API_END
+}
+
+ver_status ver_adam_step(ver_ctx ctx, int64_t count, float* params, const float* grads, float* mo, float* ve,
+                         int64_t* step, double lr) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  if (count <= 0) return VER_OK;
+  DBuf<float> w, g, m, v;
+  DBuf<int> flag;
+  w.reserve(c, count);
+  g.reserve(c, count);
+  m.reserve(c, count);
+  v.reserve(c, count);
+  flag.reserve(c, 1);
+  flag.zero(1);
+  w.upload(params, count);
+  g.upload(grads, count);
+  m.upload(mo, count);
+  v.upload(ve, count);
+  Model flat;
+  flat.P = count;
+  flat.continuous = 0;
+  ++*step;
+  adam_update(c, flat, w.p, g.p, m.p, v.p, *step, lr, flag.p);
+  w.download(params, count);
+  m.download(mo, count);
+  v.download(ve, count);
+  sync(c);
+  VER_API_END
+}
+
+ver_status ver_learner_create(ver_ctx ctx, const ver_model_config* mc, const float* params,
+                              const ver_ppo_config* cfg, const ver_entropy_controller* ec, double base_lr,
+                              int64_t total_steps, uint64_t run_seed, ver_learner* out) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  if (cfg->epochs < 0 || cfg->minibatches < 1) config_error("learner: epochs >= 0 and minibatches >= 1");
+  auto* h = new ver_learner_s();
+  Learner& L = h->l;
+  L.ctx = c;
+  L.mc = *mc;
+  L.m = Model::make(*mc);
+  L.cfg = *cfg;
+  L.ec = *ec;
+  L.base_lr = base_lr;
+  L.total_steps = total_steps;
+  L.run_seed = run_seed;
+  L.ws.ctx = c;
+  L.wr.ctx = c;
+  const int64_t P = L.m.P;
+  L.params.reserve(c, P);
+  L.grad.reserve(c, P + 1);
+  L.mom.reserve(c, P);
+  L.vel.reserve(c, P);
+  L.mom.zero(P);
+  L.vel.zero(P);
+  L.grad.zero(P + 1);
+  std::vector<float> dev;
+  to_device_layout(L.m, params, dev);
+  L.params.upload(dev.data(), P);
+  L.alpha.reserve(c, 1);
+  L.alpha.upload(&ec->alpha, 1);
+  L.acc.reserve(c, 10);
+  L.lstats.reserve(c, 1);
+  L.flags.reserve(c, 1);
+  L.flags.zero(1);
+  sync(c);
+  *out = h;
+  VER_API_END
+}
+
+ver_status ver_learner_destroy(ver_learner l) {
+  VER_API_BEGIN
+  if (l) {
+    activate(l->l.ctx);
+    sync(l->l.ctx);
+    delete l;
+  }
+  VER_API_END
+}
+
+ver_status ver_learner_enable_allreduce(ver_learner l, int enable) {
+  VER_API_BEGIN
+  l->l.allreduce = enable != 0;
+  VER_API_END
+}
+
+ver_status ver_learner_update(ver_learner l, ver_view v, ver_train_stats* stats) {
+  VER_API_BEGIN
+  activate(l->l.ctx);
+  learner_update(l->l, v->v, stats);
+  VER_API_END
+}
+
+ver_status ver_learner_batch_h0(ver_learner l, ver_view v, ver_packed p, float* h0_out) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  Ctx* c = L.ctx;
+  activate(c);
+  DPacked& P = p->p;
+  DBuf<float> h0;
+  h0.reserve(c, (size_t)P.k * L.m.H);
+  batch_h0(L, v->v, P, L.params.p, h0.p);
+  h0.download(h0_out, (size_t)P.k * L.m.H);
+  sync(c);
+  VER_API_END
+}
+
+ver_status ver_learner_get_params(ver_learner l, float* out) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  activate(L.ctx);
+  std::vector<float> dev(L.m.P);
+  L.params.download(dev.data(), L.m.P);
+  sync(L.ctx);
+  to_tensor_order(L.m, dev.data(), out);
+  VER_API_END
+}
+
+ver_status ver_learner_set_params(ver_learner l, const float* in) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  activate(L.ctx);
+  std::vector<float> dev;
+  to_device_layout(L.m, in, dev);
+  L.params.upload(dev.data(), L.m.P);
+  sync(L.ctx);
+  VER_API_END
+}
+
+ver_status ver_learner_get_adam(ver_learner l, float* mo, float* ve, int64_t* step) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  activate(L.ctx);
+  std::vector<float> a(L.m.P), b(L.m.P);
+  L.mom.download(a.data(), L.m.P);
+  L.vel.download(b.data(), L.m.P);
+  sync(L.ctx);
+  if (mo) to_tensor_order(L.m, a.data(), mo);
+  if (ve) to_tensor_order(L.m, b.data(), ve);
+  if (step) *step = L.adam_step;
+  VER_API_END
+}
+
+ver_status ver_learner_set_adam(ver_learner l, const float* mo, const float* ve, int64_t step) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  activate(L.ctx);
+  std::vector<float> a, b;
+  to_device_layout(L.m, mo, a);
+  to_device_layout(L.m, ve, b);
+  L.mom.upload(a.data(), L.m.P);
+  L.vel.upload(b.data(), L.m.P);
+  sync(L.ctx);
+  L.adam_step = step;
+  VER_API_END
+}
+
+ver_status ver_learner_get_state(ver_learner l, double* alpha, int64_t* consumed, int64_t* ui) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  activate(L.ctx);
+  if (alpha) {
+    L.alpha.download(alpha, 1);
+    sync(L.ctx);
+  }
+  if (consumed) *consumed = L.consumed;
+  if (ui) *ui = L.update_index;
+  VER_API_END
+}
+
+ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed, int64_t ui) {
+  VER_API_BEGIN
+  Learner& L = l->l;
+  activate(L.ctx);
+  L.alpha.upload(&alpha, 1);
+  sync(L.ctx);
+  L.consumed = consumed;
+  L.update_index = ui;
+  VER_API_END
+}
+
+ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n) {
+  VER_API_BEGIN
+  const int k = std::min(*n, (int)PH_N);
+  for (int i = 0; i < k; ++i) ms[i] = l->l.phase_ms[i];
+  *n = PH_N;
+  VER_API_END
+}
+
+}  // extern "C"

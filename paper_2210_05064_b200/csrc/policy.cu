@@ -1,0 +1,827 @@
+// policy.cu — policy/value network forward + backward, fused PPO loss, Adam.
+//
+// GEMMs (parity mode): a tiled fp32 SIMT GEMM (128x128x8 tiles, 8x8 per
+// thread, double-buffered shared memory) with fused epilogues (bias, tanh,
+// tanh-gradient, additive term) and deterministic split-K for the weight
+// gradients whose K is the packed row count.  fp32 keeps the gradients
+// inside the 1e-5 parity bound the north star sets for fp32.
+//
+// Recurrence (nn.cpp:235-250): per timestep t the rows of t are a prefix of
+// the rows of t-1, so h_{t-1}[0:bs_t] is contiguous and one GEMM
+// hU = h_{t-1} U (bs_t x 3H) plus a gate kernel advances the whole batch.
+// Backward runs the same structure in reverse: a gate-gradient kernel then
+// dh_{t-1} = dhU U^T + g*z; the weight gradients dU = Hprev^T dhU,
+// dWx = enc^T dpre are then single large GEMMs over all rows.
+#include <cmath>
+#include <cstring>
+
+#include "policy.cuh"
+
+namespace verg {
+
+// ------------------------------------------------------------- model
+Model Model::make(const ver_model_config& c) {
+  Model m;
+  m.D = c.obs_dim;
+  m.E = c.encoder_dim;
+  m.H = c.hidden_dim;
+  m.continuous = c.action_kind == 1;
+  m.A = m.continuous ? c.act_dim : c.num_actions;
+  m.AH = m.A + 1;
+  if (m.D < 1 || m.E < 1 || m.H < 1 || m.A < 1) config_error("model: dims must be >= 1");
+  if (m.AH > 32) config_error("model: at most 31 actions supported by the fused loss");
+  const int64_t D = m.D, E = m.E, H = m.H, A = m.A, AH = m.AH;
+  int64_t o = 0;
+  m.o_w1 = o; o += D * E;
+  m.o_b1 = o; o += E;
+  m.o_w2 = o; o += E * E;
+  m.o_b2 = o; o += E;
+  m.o_wx = o; o += E * 3 * H;
+  m.o_ux = o; o += H * 3 * H;
+  m.o_bx = o; o += 3 * H;
+  m.o_wh = o; o += H * AH;
+  m.o_bh = o; o += AH;
+  m.o_ls = o; o += m.continuous ? A : 0;
+  m.P = o;
+  // tensors() order (nn.cpp:83-95) -> device index
+  m.dev_index.resize(m.P);
+  int64_t k = 0;
+  auto put = [&](int64_t dev) { m.dev_index[k++] = dev; };
+  for (int64_t i = 0; i < D * E; ++i) put(m.o_w1 + i);
+  for (int64_t i = 0; i < E; ++i) put(m.o_b1 + i);
+  for (int64_t i = 0; i < E * E; ++i) put(m.o_w2 + i);
+  for (int64_t i = 0; i < E; ++i) put(m.o_b2 + i);
+  for (int g = 0; g < 3; ++g) {  // gru_w{r,z,n} (E x H), gru_u{r,z,n} (H x H), gru_b{r,z,n}
+    for (int64_t r = 0; r < E; ++r)
+      for (int64_t u = 0; u < H; ++u) put(m.o_wx + r * 3 * H + 3 * u + g);
+    for (int64_t r = 0; r < H; ++r)
+      for (int64_t u = 0; u < H; ++u) put(m.o_ux + r * 3 * H + 3 * u + g);
+    for (int64_t u = 0; u < H; ++u) put(m.o_bx + 3 * u + g);
+  }
+  for (int64_t r = 0; r < H; ++r)
+    for (int64_t a = 0; a < A; ++a) put(m.o_wh + r * AH + a);  // head_w
+  for (int64_t a = 0; a < A; ++a) put(m.o_bh + a);            // head_b
+  for (int64_t r = 0; r < H; ++r) put(m.o_wh + r * AH + A);   // value_w
+  put(m.o_bh + A);                                           // value_b
+  if (m.continuous)
+    for (int64_t a = 0; a < A; ++a) put(m.o_ls + a);  // log_std
+  if (k != m.P) config_error("model: layout size mismatch");
+  return m;
+}
+
+void Workspace::ensure(const Model& m, size_t S, bool train) {
+  if (S <= rows && e1.p) return;
+  const size_t R = std::max<size_t>(S, 1);
+  const size_t E = m.E, H = m.H;
+  e1.reserve(ctx, R * E);
+  enc.reserve(ctx, R * E);
+  xp.reserve(ctx, R * 3 * H);
+  hu.reserve(ctx, R * 3 * H);
+  gates.reserve(ctx, R * 3 * H);
+  hidden.reserve(ctx, R * H);
+  hprev.reserve(ctx, R * H);
+  if (train) {
+    dhidden.reserve(ctx, R * H);
+    dhead.reserve(ctx, R * m.AH);
+    g.reserve(ctx, R * H);
+    dpre.reserve(ctx, R * 3 * H);
+    dhu.reserve(ctx, R * 3 * H);
+    carry.reserve(ctx, R * H);
+    dpre2.reserve(ctx, R * E);
+    dpre1.reserve(ctx, R * E);
+    is_w.reserve(ctx, R);
+  }
+  rows = R;
+}
+
+// -------------------------------------------------------------- GEMM
+constexpr int BM = 128, BN = 128, BK = 8, GT = 256;
+
+struct EpiStore {
+  float* C;
+  int ldc;
+  __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v; }
+};
+struct EpiBias {
+  float* C;
+  int ldc;
+  const float* bias;
+  __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v + bias[n]; }
+};
+struct EpiBiasTanh {
+  float* C;
+  int ldc;
+  const float* bias;
+  __device__ void operator()(int m, int n, float v, int) const {
+    C[(size_t)m * ldc + n] = tanhf(v + bias[n]);
+  }
+};
+struct EpiAddTerm {  // C = acc + T
+  float* C;
+  int ldc;
+  const float* T;
+  int ldt;
+  __device__ void operator()(int m, int n, float v, int) const {
+    C[(size_t)m * ldc + n] = v + T[(size_t)m * ldt + n];
+  }
+};
+struct EpiTanhGrad {  // C = acc * (1 - Y^2)
+  float* C;
+  int ldc;
+  const float* Y;
+  int ldy;
+  __device__ void operator()(int m, int n, float v, int) const {
+    const float y = Y[(size_t)m * ldy + n];
+    C[(size_t)m * ldc + n] = v * (1.f - y * y);
+  }
+};
+struct EpiPartial {  // split-K partial z
+  float* W;
+  int M, N;
+  __device__ void operator()(int m, int n, float v, int z) const {
+    W[((size_t)z * M + m) * N + n] = v;
+  }
+};
+
+template <bool TA, bool TB, class Epi>
+__global__ void __launch_bounds__(GT) sgemm_kernel(int M, int N, int K, const float* __restrict__ A,
+                                                   int lda, const float* __restrict__ B, int ldb, Epi epi,
+                                                   int kchunk) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kb = blockIdx.z * kchunk;
+  const int ke = min(K, kb + kchunk);
+  const int tx = tid & 15, ty = tid >> 4;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  float ra[4], rb[4];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid * 4 + q;
+      int m, k;
+      if (!TA) {
+        m = idx / BK;
+        k = idx % BK;
+      } else {
+        k = idx / BM;
+        m = idx % BM;
+      }
+      const int gm = m0 + m, gk = k0 + k;
+      ra[q] = (gm < M && gk < ke) ? (TA ? A[(size_t)gk * lda + gm] : A[(size_t)gm * lda + gk]) : 0.f;
+      int n;
+      if (!TB) {
+        k = idx / BN;
+        n = idx % BN;
+      } else {
+        n = idx / BK;
+        k = idx % BK;
+      }
+      const int gn = n0 + n, gk2 = k0 + k;
+      rb[q] = (gn < N && gk2 < ke) ? (TB ? B[(size_t)gn * ldb + gk2] : B[(size_t)gk2 * ldb + gn]) : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int idx = tid * 4 + q;
+      if (!TA) As[buf][idx % BK][idx / BK] = ra[q];
+      else As[buf][idx / BM][idx % BM] = ra[q];
+      if (!TB) Bs[buf][idx / BN][idx % BN] = rb[q];
+      else Bs[buf][idx % BK][idx / BK] = rb[q];
+    }
+  };
+  const int nk = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  if (nk > 0) {
+    load(kb);
+    store(0);
+  }
+  __syncthreads();
+  for (int it = 0; it < nk; ++it) {
+    const int buf = it & 1;
+    if (it + 1 < nk) load(kb + (it + 1) * BK);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (it + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (n < N) epi(m, n, acc[i][j], blockIdx.z);
+    }
+  }
+}
+
+template <bool TA, bool TB, class Epi>
+static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid(cdiv(N, BN), cdiv(M, BM), 1);
+  sgemm_kernel<TA, TB, Epi><<<grid, GT, 0, c->stream>>>(M, N, K, A, lda, B, ldb, epi, std::max(K, 1));
+  after_launch(c);
+}
+
+__global__ void splitk_reduce_kernel(const float* __restrict__ W, int Z, int M, int N, float* __restrict__ C,
+                                     int ldc) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * N) return;
+  const int m = (int)(i / N), n = (int)(i % N);
+  float s = 0.f;
+  for (int z = 0; z < Z; ++z) s += W[(size_t)z * M * N + i];
+  C[(size_t)m * ldc + n] = s;
+}
+
+// C (M x N, ldc) = op(A) op(B) with deterministic split-K over K.
+template <bool TA, bool TB>
+static void gemm_splitk(Ctx* c, Workspace& ws, int M, int N, int K, const float* A, int lda, const float* B,
+                        int ldb, float* C, int ldc) {
+  if (M <= 0 || N <= 0) return;
+  const int tiles = (int)(cdiv(N, BN) * cdiv(M, BM));
+  int Z = std::max(1, std::min((2 * c->num_sms + tiles - 1) / tiles, (int)cdiv(K, 256)));
+  Z = std::min(Z, 64);
+  if (Z == 1) {
+    gemm<TA, TB>(c, M, N, K, A, lda, B, ldb, EpiStore{C, ldc});
+    return;
+  }
+  const int kchunk = (int)((cdiv(K, Z) + BK - 1) / BK) * BK;
+  Z = (int)cdiv(K, kchunk);
+  ws.splitk.reserve(c, (size_t)Z * M * N);
+  dim3 grid(cdiv(N, BN), cdiv(M, BM), Z);
+  sgemm_kernel<TA, TB, EpiPartial><<<grid, GT, 0, c->stream>>>(M, N, K, A, lda, B, ldb,
+                                                                EpiPartial{ws.splitk.p, M, N}, kchunk);
+  after_launch(c);
+  splitk_reduce_kernel<<<cdiv((size_t)M * N, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc);
+  after_launch(c);
+}
+
+// column sums out[n] = sum_m X[m, n] (deterministic two-stage)
+__global__ void colsum_partial_kernel(const float* __restrict__ X, int M, int N, int ld, int rows_per,
+                                      float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int n = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r = threadIdx.x >> 5;
+  const int m0 = blockIdx.y * rows_per, m1 = min(M, m0 + rows_per);
+  float s = 0.f;
+  if (n < N)
+    for (int m = m0 + r; m < m1; m += 8) s += X[(size_t)m * ld + n];
+  red[r][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (r == 0 && n < N) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x & 31];
+    part[(size_t)blockIdx.y * N + n] = t;
+  }
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int N, float* __restrict__ out) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int k = 0; k < chunks; ++k) s += part[(size_t)k * N + n];
+  out[n] = s;
+}
+static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, float* out) {
+  const int rows_per = 1024;
+  const int chunks = std::max(1, (int)cdiv(M, rows_per));
+  ws.splitk.reserve(c, (size_t)chunks * N);
+  dim3 grid(cdiv(N, 32), chunks);
+  colsum_partial_kernel<<<grid, 256, 0, c->stream>>>(X, M, N, ld, rows_per, ws.splitk.p);
+  after_launch(c);
+  colsum_final_kernel<<<cdiv(N, 256), 256, 0, c->stream>>>(ws.splitk.p, chunks, N, out);
+  after_launch(c);
+}
+
+// ----------------------------------------------------------- forward
+// e1 = tanh(obs w1 + b1)  (K = D is tiny: direct)
+__global__ void enc1_kernel(const float* __restrict__ obs, int S, int D, int E, const float* __restrict__ w1,
+                            const float* __restrict__ b1, float* __restrict__ e1) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)S * E) return;
+  const int p = (int)(i / E), k = (int)(i % E);
+  float s = 0.f;
+  for (int d = 0; d < D; ++d) s = fmaf(obs[(size_t)p * D + d], w1[(size_t)d * E + k], s);
+  e1[i] = tanhf(s + b1[k]);
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
+
+// GRU gates for timestep rows [o, o+bs): nn.cpp:239-248
+__global__ void gru_fwd_gate_kernel(int bs, int o, int H, const float* __restrict__ xp,
+                                    const float* __restrict__ hu, const float* __restrict__ hprev_rows,
+                                    float* __restrict__ gates, float* __restrict__ hidden,
+                                    float* __restrict__ hprev_store) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)bs * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  const size_t p = (size_t)o + j;
+  const size_t g3 = p * 3 * H + 3 * u;
+  const float r = sigmoidf_(xp[g3 + 0] + hu[g3 + 0]);
+  const float z = sigmoidf_(xp[g3 + 1] + hu[g3 + 1]);
+  const float n = tanhf(xp[g3 + 2] + r * hu[g3 + 2]);
+  const float hp = hprev_rows[(size_t)j * H + u];
+  const float h = (1.f - z) * n + z * hp;
+  hidden[p * H + u] = h;
+  if (gates) {
+    gates[g3 + 0] = r;
+    gates[g3 + 1] = z;
+    gates[g3 + 2] = n;
+    hprev_store[p * H + u] = hp;
+  }
+}
+
+void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
+                    const std::vector<int32_t>& hbs, const std::vector<int32_t>& hoffs, Workspace& ws,
+                    bool store) {
+  const int E = m.E, H = m.H, H3 = 3 * m.H;
+  enc1_kernel<<<cdiv((size_t)S * E, 256), 256, 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1,
+                                                                params + m.o_b1, ws.e1.p);
+  after_launch(c);
+  gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2});
+  gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx});
+  const int L = (int)hbs.size();
+  for (int t = 0; t < L; ++t) {
+    const int bs = hbs[t], o = hoffs[t];
+    const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)hoffs[t - 1] * H;
+    gemm<false, false>(c, bs, H3, H, hp, H, params + m.o_ux, H3, EpiStore{ws.hu.p + (size_t)o * H3, H3});
+    gru_fwd_gate_kernel<<<cdiv((size_t)bs * H, 256), 256, 0, c->stream>>>(
+        bs, o, H, ws.xp.p, ws.hu.p, hp, store ? ws.gates.p : nullptr, ws.hidden.p, ws.hprev.p);
+    after_launch(c);
+  }
+}
+
+void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out) {
+  gemm<false, false>(c, n, m.AH, m.H, hidden, m.H, params + m.o_wh, m.AH,
+                     EpiBias{out, m.AH, params + m.o_bh});
+}
+
+// per-row heads: warp per row (nn.cpp:251-278)
+__global__ void policy_rows_kernel(int S, int H, int A, int continuous, const float* __restrict__ hidden,
+                                   const float* __restrict__ wh, const float* __restrict__ bh,
+                                   const float* __restrict__ log_std, const int32_t* __restrict__ act_disc,
+                                   const float* __restrict__ act_cont, float* __restrict__ logp_out,
+                                   float* __restrict__ ent_out, float* __restrict__ value_out) {
+  const int lane = threadIdx.x & 31;
+  const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= S) return;
+  const int AH = A + 1;
+  double lg[32];
+  for (int c = 0; c < AH; ++c) {
+    float acc = 0.f;
+    for (int u = lane; u < H; u += 32) acc = fmaf(hidden[(size_t)p * H + u], wh[(size_t)u * AH + c], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    lg[c] = (double)acc + (double)bh[c];
+  }
+  if (lane != 0) return;
+  double logp, ent;
+  if (!continuous) {
+    double mx = lg[0];
+    for (int c = 1; c < A; ++c) mx = fmax(mx, lg[c]);
+    double se = 0.0;
+    for (int c = 0; c < A; ++c) se += exp(lg[c] - mx);
+    const double lse = log(se);
+    logp = lg[act_disc[p]] - mx - lse;
+    ent = 0.0;
+    for (int c = 0; c < A; ++c) {
+      const double lp = lg[c] - mx - lse;
+      ent -= exp(lp) * lp;
+    }
+  } else {
+    double q = 0.0, sls = 0.0;
+    for (int c = 0; c < A; ++c) {
+      const double ls = log_std[c];
+      const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * exp(-ls);
+      q += z * z;
+      sls += ls;
+    }
+    logp = -0.5 * q - sls - 0.5 * 1.8378770664093453 * A;
+    ent = sls + 0.5 * (1.0 + 1.8378770664093453) * A;
+  }
+  if (logp_out) logp_out[p] = (float)logp;
+  if (ent_out) ent_out[p] = (float)ent;
+  if (value_out) value_out[p] = (float)lg[A];
+}
+
+void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float* hidden,
+                 const int32_t* act_disc, const float* act_cont, float* logp, float* ent, float* value) {
+  policy_rows_kernel<<<cdiv(S, 8), 256, 0, c->stream>>>(S, m.H, m.A, m.continuous, hidden, params + m.o_wh,
+                                                        params + m.o_bh, m.continuous ? params + m.o_ls : nullptr,
+                                                        act_disc, act_cont, logp, ent, value);
+  after_launch(c);
+}
+
+// ---------------------------------------------------------------- loss
+constexpr int kLossWarps = 8;
+constexpr int kLossStats = 8;  // ws, verr2, H, ratio, clip, w, wmax, (pad)
+constexpr double kLog2Pi = 1.8378770664093453;
+
+// One warp per packed row: heads (H -> A+1 dot products), log-softmax /
+// Gaussian log-prob, ratio / clip / IS weight / surrogate / value / entropy,
+// and the row's head gradient dhead (A+1) and dhidden = dhead wh^T.
+// Per-block double partials of the loss statistics (deterministic order).
+__global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
+    int S, int H, int A, int continuous, const float* __restrict__ hidden, const float* __restrict__ wh,
+    const float* __restrict__ bh, const float* __restrict__ log_std, const float* __restrict__ act_cont,
+    const int32_t* __restrict__ act_disc, const float* __restrict__ old_logp, const float* __restrict__ adv,
+    const float* __restrict__ ret, const float* __restrict__ frozen_w, double clip, double is_cap,
+    double vcoef, const double* __restrict__ alpha_p, double inv_S, float* __restrict__ dhead,
+    float* __restrict__ dhidden, float* __restrict__ is_w, double* __restrict__ part, int want_grads) {
+  extern __shared__ float s_wh[];  // H x AH
+  __shared__ double s_red[kLossWarps][kLossStats + 32];
+  const int AH = A + 1;
+  for (int i = threadIdx.x; i < H * AH; i += blockDim.x) s_wh[i] = wh[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double alpha = *alpha_p;
+  const double gH = -alpha * inv_S;
+  double st[kLossStats] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double dls = 0.0;  // lane c < A: log_std gradient (continuous)
+  for (int p = blockIdx.x * kLossWarps + warp; p < S; p += gridDim.x * kLossWarps) {
+    const float* hrow = hidden + (size_t)p * H;
+    float acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+    for (int u = lane; u < H; u += 32) {
+      const float h = hrow[u];
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c < AH) acc[c] = fmaf(h, s_wh[u * AH + c], acc[c]);
+    }
+    double lg[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+      if (c < AH) {
+        float v = acc[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        lg[c] = (double)v + (double)bh[c];
+      } else {
+        lg[c] = 0.0;
+      }
+    }
+    const double value = lg[A];
+    double logp, ent, G[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) G[c] = 0.0;
+    if (!continuous) {
+      double mx = lg[0];
+      for (int c = 1; c < A; ++c) mx = fmax(mx, lg[c]);
+      double se = 0.0;
+      for (int c = 0; c < A; ++c) se += exp(lg[c] - mx);
+      const double lse = log(se);
+      const int a = act_disc[p];
+      logp = lg[a] - mx - lse;
+      ent = 0.0;
+      for (int c = 0; c < A; ++c) {
+        const double lp = lg[c] - mx - lse;
+        ent -= exp(lp) * lp;
+      }
+    } else {
+      double q = 0.0, sls = 0.0;
+      for (int c = 0; c < A; ++c) {
+        const double ls = log_std[c];
+        const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * exp(-ls);
+        q += z * z;
+        sls += ls;
+      }
+      logp = -0.5 * q - sls - 0.5 * kLog2Pi * A;
+      ent = sls + 0.5 * (1.0 + kLog2Pi) * A;
+    }
+    const double ratio = exp(logp - (double)old_logp[p]);
+    const double A_ = adv[p];
+    const double w = frozen_w ? (double)frozen_w[p] : fmin(ratio, is_cap);
+    const double s1 = ratio * A_;
+    const double cr = fmin(fmax(ratio, 1.0 - clip), 1.0 + clip);
+    const double s2 = cr * A_;
+    const double sur = fmin(s1, s2);
+    const double verr = value - (double)ret[p];
+    st[0] += w * sur;
+    st[1] += verr * verr;
+    st[2] += ent;
+    st[3] += ratio;
+    st[4] += (ratio < 1.0 - clip || ratio > 1.0 + clip) ? 1.0 : 0.0;  // strict (learner.cpp:104)
+    st[5] += w;
+    st[6] = fmax(st[6], w);
+    if (lane == 0 && is_w) is_w[p] = (float)w;
+    if (want_grads) {
+      // cmin tie -> first argument (tape.cpp:157); clip mask inclusive (tape.cpp:146)
+      const double m1 = s1 <= s2 ? 1.0 : 0.0;
+      const double cm = (ratio >= 1.0 - clip && ratio <= 1.0 + clip) ? 1.0 : 0.0;
+      const double dratio = -w * inv_S * (m1 * A_ + (1.0 - m1) * A_ * cm);
+      const double dlogp = dratio * ratio;
+      double dh[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) dh[c] = 0.0;
+      if (!continuous) {
+        double mx = lg[0];
+        for (int c = 1; c < A; ++c) mx = fmax(mx, lg[c]);
+        double se = 0.0;
+        for (int c = 0; c < A; ++c) se += exp(lg[c] - mx);
+        const double lse = log(se);
+        const int a = act_disc[p];
+        double sumG = 0.0;
+        for (int c = 0; c < A; ++c) {
+          const double lp = lg[c] - mx - lse;
+          const double pc = exp(lp);
+          G[c] = (c == a ? dlogp : 0.0) + gH * (-pc - pc * lp);
+          sumG += G[c];
+        }
+        for (int c = 0; c < A; ++c) dh[c] = G[c] - exp(lg[c] - mx - lse) * sumG;
+      } else {
+        for (int c = 0; c < A; ++c) {
+          const double ls = log_std[c];
+          const double inv = exp(-ls);
+          const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * inv;
+          dh[c] = dlogp * z * inv;
+          if (lane == c) dls += dlogp * (z * z - 1.0) + gH;
+        }
+      }
+      dh[A] = vcoef * verr * inv_S;
+      if (lane < AH) dhead[(size_t)p * AH + lane] = (float)dh[lane < 32 ? lane : 0];
+      for (int u = lane; u < H; u += 32) {
+        float s = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c < AH) s = fmaf((float)dh[c], s_wh[u * AH + c], s);
+        dhidden[(size_t)p * H + u] = s;
+      }
+    }
+  }
+  // block reduction of the statistics (lane 0 of each warp holds identical st)
+  if (lane == 0)
+    for (int k = 0; k < kLossStats; ++k) s_red[warp][k] = st[k];
+  if (lane < 32) s_red[warp][kLossStats + lane] = dls;
+  __syncthreads();
+  if (threadIdx.x < kLossStats + 32) {
+    const int k = threadIdx.x;
+    double s = (k == 6) ? 0.0 : 0.0;
+    for (int w = 0; w < kLossWarps; ++w) s = (k == 6) ? fmax(s, s_red[w][k]) : s + s_red[w][k];
+    part[(size_t)blockIdx.x * (kLossStats + 32) + k] = s;
+  }
+}
+
+__global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk, int A, int continuous,
+                                      double inv_S, int S, double vcoef, const double* __restrict__ alpha_p,
+                                      LossStats* __restrict__ out, float* __restrict__ grad_ls,
+                                      float* __restrict__ ent_slot) {
+  __shared__ double tot[kLossStats + 32];
+  const int k = threadIdx.x;
+  if (k < kLossStats + 32) {
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+      const double v = part[(size_t)b * (kLossStats + 32) + k];
+      s = (k == 6) ? fmax(s, v) : s + v;
+    }
+    tot[k] = s;
+  }
+  __syncthreads();
+  if (k == 0) {
+    LossStats r;
+    r.policy_loss = -tot[0] * inv_S;
+    r.value_loss = 0.5 * tot[1] * inv_S;
+    r.mean_entropy = tot[2] * inv_S;
+    r.loss = r.policy_loss + vcoef * r.value_loss - (*alpha_p) * r.mean_entropy;
+    r.ratio_sum = tot[3];
+    r.clip_count = tot[4];
+    r.w_sum = tot[5];
+    r.w_max = S > 0 ? tot[6] : 0.0;
+    r.steps = S;
+    *out = r;
+    if (ent_slot) *ent_slot = (float)r.mean_entropy;
+  }
+  if (continuous && grad_ls && k < A) grad_ls[k] = (float)tot[kLossStats + k];
+}
+
+void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossArgs& a, Workspace& ws,
+                 float* grad, LossStats* stats, bool want_grads) {
+  const int nblk = std::max(1, std::min((int)cdiv(S, kLossWarps), 4 * c->num_sms));
+  ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));
+  const size_t smem = sizeof(float) * (size_t)m.H * m.AH;
+  if (smem > 48 * 1024)
+    VER_CUDA(cudaFuncSetAttribute(ppo_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  float* dhead = ws.dhead.p;  // S x (A+1)
+  ppo_loss_kernel<<<nblk, kLossWarps * 32, smem, c->stream>>>(
+      S, m.H, m.A, m.continuous, ws.hidden.p, params + m.o_wh, params + m.o_bh,
+      m.continuous ? params + m.o_ls : nullptr, a.act_cont, a.act_disc, a.old_logp, a.adv, a.ret, a.frozen_w,
+      a.clip, a.is_cap, a.vcoef, a.alpha, 1.0 / (double)S, dhead, ws.dhidden.p, ws.is_w.p, ws.part.p,
+      want_grads ? 1 : 0);
+  after_launch(c);
+  ppo_loss_final_kernel<<<1, 64, 0, c->stream>>>(ws.part.p, nblk, m.A, m.continuous, 1.0 / (double)S, S,
+                                                 a.vcoef, a.alpha, stats,
+                                                 want_grads && m.continuous ? grad + m.o_ls : nullptr,
+                                                 want_grads ? grad + m.P : nullptr);
+  after_launch(c);
+  if (want_grads) {
+    // head weights / biases: dwh = hidden^T dhead, dbh = colsum(dhead)
+    gemm_splitk<true, false>(c, ws, m.H, m.AH, S, ws.hidden.p, m.H, dhead, m.AH, grad + m.o_wh, m.AH);
+    colsum(c, ws, dhead, S, m.AH, m.AH, grad + m.o_bh);
+  }
+}
+
+// ------------------------------------------------------------ backward
+// Gate gradients of timestep rows [o, o+bs) (Appendix A of SURVEY.md):
+//   g = dhidden + carry (rows j < bs_next), dn = g(1-z), dz = g(h-n),
+//   dpre_n = dn(1-n^2), dr = dpre_n * hUn, dpre_r = dr r(1-r), dpre_z = dz z(1-z)
+__global__ void gru_bwd_gate_kernel(int bs, int bs_next, int o, int H, const float* __restrict__ dhidden,
+                                    const float* __restrict__ carry, const float* __restrict__ gates,
+                                    const float* __restrict__ hu, const float* __restrict__ hprev,
+                                    float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)bs * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  const size_t p = (size_t)o + j;
+  float g = dhidden[p * H + u];
+  if (j < bs_next) g += carry[(size_t)j * H + u];
+  const size_t g3 = p * 3 * H + 3 * u;
+  const float r = gates[g3 + 0], z = gates[g3 + 1], n = gates[g3 + 2];
+  const float hn = hu[g3 + 2];
+  const float hp = hprev[p * H + u];
+  const float dn = g * (1.f - z);
+  const float dz = g * (hp - n);
+  const float dpn = dn * (1.f - n * n);
+  const float dr = dpn * hn;
+  const float dpr = dr * r * (1.f - r);
+  const float dpz = dz * z * (1.f - z);
+  dpre[g3 + 0] = dpr;
+  dpre[g3 + 1] = dpz;
+  dpre[g3 + 2] = dpn;
+  dhu[g3 + 0] = dpr;
+  dhu[g3 + 1] = dpz;
+  dhu[g3 + 2] = dpn * r;
+  gz[(size_t)j * H + u] = g * z;
+}
+
+__global__ void dw1_kernel(const float* __restrict__ obs, const float* __restrict__ dpre1, int S, int D, int E,
+                           float* __restrict__ dw1) {
+  // dw1[d, k] = sum_p obs[p, d] dpre1[p, k]  (small: D x E outputs, K = S)
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d = blockIdx.y;
+  if (k >= E) return;
+  float s = 0.f;
+  for (int p = 0; p < S; ++p) s = fmaf(obs[(size_t)p * D + d], dpre1[(size_t)p * E + k], s);
+  dw1[(size_t)d * E + k] = s;
+}
+
+void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
+                     const std::vector<int32_t>& hbs, const std::vector<int32_t>& hoffs, Workspace& ws,
+                     float* grad) {
+  (void)h0;
+  const int E = m.E, H = m.H, H3 = 3 * m.H;
+  const int L = (int)hbs.size();
+  for (int t = L - 1; t >= 0; --t) {
+    const int bs = hbs[t], o = hoffs[t];
+    const int bs_next = t + 1 < L ? hbs[t + 1] : 0;
+    gru_bwd_gate_kernel<<<cdiv((size_t)bs * H, 256), 256, 0, c->stream>>>(
+        bs, bs_next, o, H, ws.dhidden.p, ws.carry.p, ws.gates.p, ws.hu.p, ws.hprev.p, ws.dpre.p, ws.dhu.p, ws.g.p);
+    after_launch(c);
+    if (t > 0) {  // dh_{t-1} = dhU U^T + g z   (h0 needs no gradient)
+      gemm<false, true>(c, bs, H, H3, ws.dhu.p + (size_t)o * H3, H3, params + m.o_ux, H3,
+                        EpiAddTerm{ws.carry.p, H, ws.g.p, H});
+    }
+  }
+  // weight gradients over all rows
+  gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
+  gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);
+  colsum(c, ws, ws.dpre.p, S, H3, H3, grad + m.o_bx);
+  gemm<false, true>(c, S, E, H3, ws.dpre.p, H3, params + m.o_wx, H3, EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E});
+  gemm_splitk<true, false>(c, ws, E, E, S, ws.e1.p, E, ws.dpre2.p, E, grad + m.o_w2, E);
+  colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2);
+  gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E});
+  dim3 g1(cdiv(E, 128), m.D);
+  dw1_kernel<<<g1, 128, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E, grad + m.o_w1);
+  after_launch(c);
+  colsum(c, ws, ws.dpre1.p, S, E, E, grad + m.o_b1);
+}
+
+// ---------------------------------------------------------------- Adam
+__global__ void adam_kernel(int64_t P, float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                            float* __restrict__ v, float lr, float bc1, float bc2, int64_t ls0, int64_t ls1,
+                            int* __restrict__ nonfinite) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const float gi = g[i];
+  const float mi = 0.9f * m[i] + (1.f - 0.9f) * gi;
+  const float vi = 0.999f * v[i] + (1.f - 0.999f) * (gi * gi);
+  m[i] = mi;
+  v[i] = vi;
+  float wi = w[i] - lr * (mi / bc1) / (sqrtf(vi / bc2) + 1e-8f);
+  if (i >= ls0 && i < ls1) wi = fminf(fmaxf(wi, -5.f), 2.f);  // kLogStdMin/Max (nn.hpp:26-27)
+  w[i] = wi;
+  if (!isfinite(wi)) atomicOr(nonfinite, 1);
+}
+
+void adam_update(Ctx* c, const Model& m, float* params, const float* grad, float* mom, float* vel, int64_t step,
+                 double lr, int* nonfinite_flag) {
+  const double bc1 = 1.0 - std::pow(0.9, (double)step);
+  const double bc2 = 1.0 - std::pow(0.999, (double)step);
+  const int64_t ls0 = m.continuous ? m.o_ls : -1, ls1 = m.continuous ? m.o_ls + m.A : -1;
+  adam_kernel<<<cdiv(m.P, 256), 256, 0, c->stream>>>(m.P, params, grad, mom, vel, (float)lr, (float)bc1,
+                                                     (float)bc2, ls0, ls1, nonfinite_flag);
+  after_launch(c);
+}
+
+// --------------------------------------------------------- host init
+// rng.hpp:16-75 (CounterRng) and nn.cpp:16-30 (orthogonal): the thin Q
+// factor of a Gaussian matrix with diag(R) > 0 is unique, computed here by
+// twice-iterated modified Gram-Schmidt.
+namespace {
+inline uint64_t splitmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+inline uint64_t mix64(uint64_t a, uint64_t b) {
+  return splitmix(a ^ (0x9e3779b97f4a7c15ull + (b << 6) + (b >> 2) + splitmix(b)));
+}
+struct Stream {
+  uint64_t key, ctr = 0;
+  double normal() {
+    double u1 = (double)(mix64(key, ctr++) >> 11) * 0x1.0p-53;
+    double u2 = (double)(mix64(key, ctr++) >> 11) * 0x1.0p-53;
+    if (u1 <= 0) u1 = 0x1.0p-53;
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+  }
+};
+// rows x cols, row-major
+std::vector<double> orthogonal(int rows, int cols, double gain, Stream s) {
+  const int big = std::max(rows, cols), small = std::min(rows, cols);
+  std::vector<double> g((size_t)big * small);  // column j at g[i*small + j]
+  for (int i = 0; i < big; ++i)
+    for (int j = 0; j < small; ++j) g[(size_t)i * small + j] = s.normal();
+  std::vector<double> q = g;
+  for (int j = 0; j < small; ++j) {
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int k = 0; k < j; ++k) {
+        double d = 0;
+        for (int i = 0; i < big; ++i) d += q[(size_t)i * small + k] * q[(size_t)i * small + j];
+        for (int i = 0; i < big; ++i) q[(size_t)i * small + j] -= d * q[(size_t)i * small + k];
+      }
+    }
+    double nrm = 0;
+    for (int i = 0; i < big; ++i) nrm += q[(size_t)i * small + j] * q[(size_t)i * small + j];
+    nrm = std::sqrt(nrm);
+    for (int i = 0; i < big; ++i) q[(size_t)i * small + j] /= nrm;
+  }
+  std::vector<double> out((size_t)rows * cols);
+  for (int i = 0; i < big; ++i)
+    for (int j = 0; j < small; ++j) {
+      const double v = gain * q[(size_t)i * small + j];
+      if (rows >= cols) out[(size_t)i * cols + j] = v;
+      else out[(size_t)j * cols + i] = v;  // transpose
+    }
+  return out;
+}
+}  // namespace
+
+void init_params_host(const ver_model_config& c, uint64_t seed, double* out) {
+  const Model m = Model::make(c);
+  std::memset(out, 0, sizeof(double) * m.P);
+  Stream root{splitmix(seed)};
+  auto sub = [&](uint64_t id) { return Stream{mix64(root.key, id)}; };
+  const int D = m.D, E = m.E, H = m.H, A = m.A;
+  int64_t off = 0;
+  auto put = [&](const std::vector<double>& v) {
+    std::memcpy(out + off, v.data(), sizeof(double) * v.size());
+    off += (int64_t)v.size();
+  };
+  auto zeros = [&](int64_t n) { off += n; };
+  put(orthogonal(D, E, std::sqrt(2.0), sub(1)));
+  zeros(E);
+  put(orthogonal(E, E, std::sqrt(2.0), sub(2)));
+  zeros(E);
+  put(orthogonal(E, H, 1.0, sub(3)));
+  put(orthogonal(H, H, 1.0, sub(4)));
+  zeros(H);
+  put(orthogonal(E, H, 1.0, sub(5)));
+  put(orthogonal(H, H, 1.0, sub(6)));
+  zeros(H);
+  put(orthogonal(E, H, 1.0, sub(7)));
+  put(orthogonal(H, H, 1.0, sub(8)));
+  zeros(H);
+  put(orthogonal(H, A, 0.01, sub(9)));
+  zeros(A);
+  put(orthogonal(H, 1, 1.0, sub(10)));
+  zeros(1);
+  if (m.continuous) zeros(A);
+}
+
+}  // namespace verg

@@ -1,0 +1,88 @@
+// policy.cuh — encoder + GRU + heads (nn.cpp:219-280) on the device.
+//
+// Device parameter layout (one flat fp32 buffer; gradients, Adam moments and
+// the NCCL AllReduce use the same layout):
+//   w1[D*E] b1[E] w2[E*E] b2[E]
+//   wx[E*3H] ux[H*3H] bx[3H]      GRU gates interleaved per unit: column 3u+g,
+//                                 g = 0 r, 1 z, 2 n  (so one output tile holds
+//                                 all three gates of its units)
+//   wh[H*(A+1)] bh[A+1]           policy head columns 0..A-1, value column A
+//   log_std[A]                    (continuous only)
+// The reference's tensors() order (nn.cpp:83-95) is a fixed permutation of
+// this layout, applied only at the C-ABI (params/grads/Adam get/set).
+#pragma once
+
+#include "packed.cuh"
+
+namespace verg {
+
+struct Model {
+  int D = 0, E = 0, H = 0, A = 0, AH = 0;
+  int continuous = 0;
+  int64_t P = 0;
+  int64_t o_w1, o_b1, o_w2, o_b2, o_wx, o_ux, o_bx, o_wh, o_bh, o_ls;
+  std::vector<int64_t> dev_index;  // tensors()-order flat index -> device index
+  static Model make(const ver_model_config& c);
+};
+
+struct LossStats {  // device-side per-minibatch loss statistics (double)
+  double loss, policy_loss, value_loss, mean_entropy, ratio_sum, clip_count, w_sum, w_max;
+  double steps;
+};
+
+struct Workspace {
+  Ctx* ctx = nullptr;
+  size_t rows = 0;
+  DBuf<float> e1, enc, xp, hu, gates, hidden, hprev;  // forward
+  DBuf<float> dhidden, dhead, g, dpre, dhu, carry, dpre2, dpre1;  // backward
+  DBuf<float> splitk;                                   // split-K partials
+  DBuf<double> part;                                    // loss partials
+  DBuf<float> wpart;                                    // head-weight partials
+  DBuf<float> is_w;
+  void ensure(const Model& m, size_t S, bool train);
+};
+
+// Forward of the encoder + GRU over a packed batch of S rows.
+//   obs: S x D (packed), h0: bs[0] x H, hbs/hoffs: host batch sizes/offsets.
+//   store: keep e1/enc/xp/hu/gates/hprev for the backward pass.
+void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs,
+                    const float* h0, const std::vector<int32_t>& hbs,
+                    const std::vector<int32_t>& hoffs, Workspace& ws, bool store);
+
+// Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
+// dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights
+// and the LossStats at *stats (device).  alpha: device double.
+struct LossArgs {
+  const float* act_cont;
+  const int32_t* act_disc;
+  const float* old_logp;
+  const float* adv;
+  const float* ret;
+  const float* frozen_w;  // may be null
+  double clip, is_cap, vcoef;
+  const double* alpha;
+};
+void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossArgs& a, Workspace& ws,
+                 float* grad, LossStats* stats, bool want_grads);
+
+// Backward through the recurrence and the encoder; fills the remaining
+// gradient slots of `grad` (device layout).  Requires policy_forward(store).
+void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs,
+                     const float* h0, const std::vector<int32_t>& hbs,
+                     const std::vector<int32_t>& hoffs, Workspace& ws, float* grad);
+
+// Per-row log-prob / entropy / value of the heads (nn.cpp:251-278)
+void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float* hidden,
+                 const int32_t* act_disc, const float* act_cont, float* logp, float* ent, float* value);
+
+// Heads on n rows of hidden: out n x (A+1) = hidden * wh + bh
+void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out);
+
+// Adam (nn.cpp:291-306) + log_std clamp (nn.cpp:105-109) + finiteness flag.
+void adam_update(Ctx* c, const Model& m, float* params, const float* grad, float* mom, float* vel,
+                 int64_t step, double lr, int* nonfinite_flag);
+
+// Host-double parameter init in tensors() order (nn.cpp:16-81).
+void init_params_host(const ver_model_config& c, uint64_t seed, double* out);
+
+}  // namespace verg

@@ -1,0 +1,55 @@
+// view.cuh — device-resident RolloutView (rollout.hpp:33-78) in SoA layout.
+//
+// HBM layout (fp32 values, int32 indices, u8 flags; S = size, K = num_seqs):
+//   obs[S*D] act_disc[S] | act_cont[S*A]  log_prob value reward latency
+//   advantage returns [S]   done stale replayed [S] (u8)
+//   env_index seq_of_slot step_in_episode [S] (i32)  episode_index version [S] (64-bit)
+//   seqs[K] (ver_seq_desc, 32 B)   h0[K*H]
+//   per_env_counts[N] env_bootstrap[N] env_bootstrap_valid[N]
+//   env_offsets[N+1]  — exclusive scan of the per-env fresh counts, valid when
+//                       `env_contiguous` (every close_rollout/backfill output)
+// Capacities are sized for T*N so backfill_stale appends in place.
+#pragma once
+
+#include "common.cuh"
+
+namespace verg {
+
+struct DView {
+  Ctx* ctx = nullptr;
+  int T = 0, N = 0, action_kind = 0, obs_dim = 0, act_dim = 0, hidden_dim = 0;
+  int size = 0, num_seqs = 0, h0_rows = 0;
+  int cap = 0, seq_cap = 0, h0_cap = 0;
+  int deficit = 0, stale_steps = 0, replayed_steps = 0;
+  uint64_t snapshot_version = 0;
+  double collect_wall_time = 0;
+  // fresh slots are [0, fresh) and env-major contiguous with env_offsets
+  bool env_contiguous = false;
+  int fresh_prefix = 0;
+
+  DBuf<float> obs, act_cont, log_prob, value, reward, latency, advantage, returns;
+  DBuf<int32_t> act_disc, env_index, seq_of_slot, step_in_episode;
+  DBuf<uint8_t> done, stale, replayed;
+  DBuf<int64_t> episode_index;
+  DBuf<uint64_t> version;
+  DBuf<ver_seq_desc> seqs;
+  DBuf<float> h0;
+  DBuf<int32_t> per_env_counts, env_offsets;
+  DBuf<float> env_bootstrap;
+  DBuf<uint8_t> env_bootstrap_valid;
+
+  int act_width() const { return action_kind ? act_dim : 1; }
+  // allocate slot arrays for `cap_` slots (contents not preserved)
+  void alloc_slots(int cap_);
+  // grow slot arrays to cap_ keeping the first `size` slots
+  void grow_slots(int cap_);
+  void alloc_seqs(int seq_cap_, int h0_cap_);
+  void grow_seqs(int seq_cap_, int h0_cap_);
+  void alloc_env();
+};
+
+}  // namespace verg
+
+struct ver_view_s {
+  verg::DView v;
+};
