@@ -150,7 +150,7 @@ static double estimate_time(Ctx* c, const double* tau, int n, long long smax, lo
   d.upload(pin, n);
   estimate_time_kernel<<<1, kPT, 0, c->stream>>>(d.p, n, steps, d.p + n);
   after_launch(c);
-  d.download(pin + n, 1);
+  VER_CUDA(cudaMemcpyAsync(pin + n, d.p + n, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   return pin[n];
 }
@@ -166,24 +166,20 @@ static long long optimal_preempt_steps(Ctx* c, const double* tau, int n, double 
   d.upload(pin, n);
   estimate_time_kernel<<<1, kPT, 0, c->stream>>>(d.p, n, smax, d.p + n);
   after_launch(c);
-  DBuf<int32_t> cnt;
-  cnt.reserve(c, (size_t)n + 1);
+  DBuf<int32_t> cnt, off;
+  cnt.reserve(c, (size_t)n);
+  off.reserve(c, (size_t)n + 1);
   yield_count_kernel<<<cdiv(n, 256), 256, 0, c->stream>>>(d.p, n, d.p + n, smax, cnt.p);
   after_launch(c);
-  exclusive_scan_i32(c, cnt.p, cnt.p + 0, n, cnt.p + n);  // in place, total at [n]
-  // counts were overwritten by offsets: recompute counts from offsets on the fly
+  exclusive_scan_i32(c, cnt.p, off.p, n, off.p + n);
   int32_t* htot = static_cast<int32_t*>(static_cast<void*>(pin + n + 1));
-  VER_CUDA(cudaMemcpyAsync(htot, cnt.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  VER_CUDA(cudaMemcpyAsync(htot, off.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   const long long Y = *htot;
   if (Y < smax) protocol_error("optimal_preempt_steps: yield enumeration short of S_max");
-  DBuf<int32_t> cnt2;
-  cnt2.reserve(c, n);
-  yield_count_kernel<<<cdiv(n, 256), 256, 0, c->stream>>>(d.p, n, d.p + n, smax, cnt2.p);
-  after_launch(c);
   DBuf<double> y;
   y.reserve(c, Y);
-  yield_write_kernel<<<n, 128, 0, c->stream>>>(d.p, n, cnt2.p, cnt.p, y.p);
+  yield_write_kernel<<<n, 128, 0, c->stream>>>(d.p, n, cnt.p, off.p, y.p);
   after_launch(c);
   sort_pos_f64(c, y.p, Y);
   const int nb = std::min<long long>(4 * c->num_sms, (smax + 255) / 256);
