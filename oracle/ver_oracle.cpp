@@ -1553,7 +1553,7 @@ long optimal_preempt_steps_sorted(const PreemptionEstimator& m) {
   for (double tau : m.step_times) {
     for (long k = 1;; ++k) {
       const double y = static_cast<double>(k) * tau;
-      if (y > tmax * (1 + 1e-12) || k > m.max_steps) break;
+      if (y > tmax * (1 + 1e-9) || k > m.max_steps) break;
       yields.push_back(y);
     }
   }

@@ -176,7 +176,7 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
     offs[t] = R;
     R += alive;
   }
-  std::vector<int32_t> meta(4 * (size_t)n + L);
+  std::vector<int32_t> meta(4 * (size_t)n + 2 * (size_t)L);
   for (int i = 0; i < n; ++i) {
     meta[i] = tails[i].parent;
     meta[n + i] = tails[i].h0i;
@@ -184,6 +184,7 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
     meta[3 * n + i] = tails[i].j;
   }
   std::copy(offs.begin(), offs.end(), meta.begin() + 4 * n);
+  std::copy(bs.begin(), bs.end(), meta.begin() + 4 * n + L);
   DBuf<int32_t> dm;
   dm.reserve(c, meta.size());
   int32_t* pin = static_cast<int32_t*>(c->pinned_buf(sizeof(int32_t) * meta.size()));
@@ -197,7 +198,7 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
   after_launch(c);
   replay_h0_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm.p + n, n, V.h0.p, H, rh0.p);
   after_launch(c);
-  policy_forward(c, Ln.m, params, R, robs.p, rh0.p, bs, offs, Ln.wr, false);
+  policy_forward(c, Ln.m, params, R, robs.p, rh0.p, L, dm.p + 4 * n + L, dm.p + 4 * n, Ln.wr, false);
   replay_final_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm.p + 2 * n, dm.p + 3 * n, n,
                                                                       Ln.wr.hidden.p, H, h0s);
   after_launch(c);
@@ -216,7 +217,7 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   Ln.mark_end();
   Ln.ws.ensure(m, S, true);
   Ln.mark_begin(PH_FORWARD);
-  policy_forward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.h_bs, P.h_offs, Ln.ws, true);
+  policy_forward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, true);
   Ln.mark_end();
   LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, nullptr,
               Ln.cfg.clip, Ln.cfg.is_cap, Ln.cfg.value_loss_coef, Ln.alpha.p};
@@ -224,7 +225,7 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   policy_loss(c, m, Ln.params.p, S, la, Ln.ws, Ln.grad.p, Ln.lstats.p, true);
   Ln.mark_end();
   Ln.mark_begin(PH_BACKWARD);
-  policy_backward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.h_bs, P.h_offs, Ln.ws, Ln.grad.p);
+  policy_backward(c, m, Ln.params.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, Ln.grad.p);
   Ln.mark_end();
   const bool ar = Ln.allreduce && c->comm && c->nranks > 1;
   if (ar) {  // grad_hook -> AllReduce::average; entropy_hook -> average_scalar
@@ -401,11 +402,11 @@ ver_status ver_ppo_loss(ver_ctx ctx, const ver_model_config* mc, const float* pa
   Workspace ws;
   ws.ctx = c;
   ws.ensure(m, S, true);
-  policy_forward(c, m, dparams.p, S, P.obs.p, h0.p, P.h_bs, P.h_offs, ws, true);
+  policy_forward(c, m, dparams.p, S, P.obs.p, h0.p, P.max_len, P.bs.p, P.offs.p, ws, true);
   LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, frozen_w ? fw.p : nullptr,
               cfg->clip, cfg->is_cap, cfg->value_loss_coef, dalpha.p};
   policy_loss(c, m, dparams.p, S, la, ws, grad.p, st.p, want_grads != 0);
-  if (want_grads) policy_backward(c, m, dparams.p, S, P.obs.p, h0.p, P.h_bs, P.h_offs, ws, grad.p);
+  if (want_grads) policy_backward(c, m, dparams.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, ws, grad.p);
   LossStats hs;
   st.download(&hs, 1);
   std::vector<float> g(m.P);
@@ -439,15 +440,17 @@ ver_status ver_forward_packed(ver_ctx ctx, const ver_model_config* mc, const flo
     if (!std::isfinite(obs[i])) protocol_error("forward_packed: non-finite observations");
   std::vector<float> dev;
   to_device_layout(m, params, dev);
-  std::vector<int32_t> bs(batch_sizes, batch_sizes + L), offs(offsets, offsets + L);
   DBuf<float> dparams, dobs, dh0, dac, out;
-  DBuf<int32_t> dad;
+  DBuf<int32_t> dad, dbo;
+  dbo.reserve(c, 2 * (size_t)L);
+  dbo.upload(batch_sizes, L);
+  VER_CUDA(cudaMemcpyAsync(dbo.p + L, offsets, sizeof(int32_t) * L, cudaMemcpyHostToDevice, c->stream));
   dparams.reserve(c, m.P);
   dparams.upload(dev.data(), m.P);
   dobs.reserve(c, (size_t)S * m.D);
   dobs.upload(obs, (size_t)S * m.D);
-  dh0.reserve(c, (size_t)bs[0] * m.H);
-  dh0.upload(h0, (size_t)bs[0] * m.H);
+  dh0.reserve(c, (size_t)batch_sizes[0] * m.H);
+  dh0.upload(h0, (size_t)batch_sizes[0] * m.H);
   if (m.continuous) {
     dac.reserve(c, (size_t)S * m.A);
     dac.upload(act_cont, (size_t)S * m.A);
@@ -459,7 +462,7 @@ ver_status ver_forward_packed(ver_ctx ctx, const ver_model_config* mc, const flo
   Workspace ws;
   ws.ctx = c;
   ws.ensure(m, S, false);
-  policy_forward(c, m, dparams.p, S, dobs.p, dh0.p, bs, offs, ws, false);
+  policy_forward(c, m, dparams.p, S, dobs.p, dh0.p, L, dbo.p, dbo.p + L, ws, false);
   policy_rows(c, m, dparams.p, S, ws.hidden.p, dad.p, dac.p, out.p, out.p + S, out.p + 2 * (size_t)S);
   if (logp_out) out.download(logp_out, S);
   if (ent_out) VER_CUDA(cudaMemcpyAsync(ent_out, out.p + S, sizeof(float) * S, cudaMemcpyDeviceToHost, c->stream));
@@ -491,8 +494,11 @@ ver_status ver_act(ver_ctx ctx, const ver_model_config* mc, const float* params,
   Workspace ws;
   ws.ctx = c;
   ws.ensure(m, n, false);
-  std::vector<int32_t> bs{n}, offs{0};
-  policy_forward(c, m, dparams.p, n, dobs.p, dh.p, bs, offs, ws, false);
+  DBuf<int32_t> bo;
+  bo.reserve(c, 2);
+  const int32_t hbo[2] = {n, 0};
+  bo.upload(hbo, 2);
+  policy_forward(c, m, dparams.p, n, dobs.p, dh.p, 1, bo.p, bo.p + 1, ws, false);
   policy_heads(c, m, dparams.p, n, ws.hidden.p, out.p);
   std::vector<float> ho((size_t)n * m.AH);
   out.download(ho.data(), ho.size());

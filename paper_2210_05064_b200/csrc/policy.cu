@@ -76,7 +76,7 @@ void Workspace::ensure(const Model& m, size_t S, bool train) {
   e1.reserve(ctx, R * E);
   enc.reserve(ctx, R * E);
   xp.reserve(ctx, R * 3 * H);
-  hu.reserve(ctx, R * 3 * H);
+  hu.reserve(ctx, R * H);  // hUn (the n-gate recurrent term) for the backward
   gates.reserve(ctx, R * 3 * H);
   hidden.reserve(ctx, R * H);
   hprev.reserve(ctx, R * H);
@@ -324,48 +324,15 @@ __global__ void enc1_kernel(const float* __restrict__ obs, int S, int D, int E, 
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
-// GRU gates for timestep rows [o, o+bs): nn.cpp:239-248
-__global__ void gru_fwd_gate_kernel(int bs, int o, int H, const float* __restrict__ xp,
-                                    const float* __restrict__ hu, const float* __restrict__ hprev_rows,
-                                    float* __restrict__ gates, float* __restrict__ hidden,
-                                    float* __restrict__ hprev_store) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)bs * H) return;
-  const int j = (int)(i / H), u = (int)(i % H);
-  const size_t p = (size_t)o + j;
-  const size_t g3 = p * 3 * H + 3 * u;
-  const float r = sigmoidf_(xp[g3 + 0] + hu[g3 + 0]);
-  const float z = sigmoidf_(xp[g3 + 1] + hu[g3 + 1]);
-  const float n = tanhf(xp[g3 + 2] + r * hu[g3 + 2]);
-  const float hp = hprev_rows[(size_t)j * H + u];
-  const float h = (1.f - z) * n + z * hp;
-  hidden[p * H + u] = h;
-  if (gates) {
-    gates[g3 + 0] = r;
-    gates[g3 + 1] = z;
-    gates[g3 + 2] = n;
-    hprev_store[p * H + u] = hp;
-  }
-}
-
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
-                    const std::vector<int32_t>& hbs, const std::vector<int32_t>& hoffs, Workspace& ws,
-                    bool store) {
-  const int E = m.E, H = m.H, H3 = 3 * m.H;
+                    int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store) {
+  const int E = m.E, H3 = 3 * m.H;
   enc1_kernel<<<cdiv((size_t)S * E, 256), 256, 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1,
                                                                 params + m.o_b1, ws.e1.p);
   after_launch(c);
   gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2});
   gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx});
-  const int L = (int)hbs.size();
-  for (int t = 0; t < L; ++t) {
-    const int bs = hbs[t], o = hoffs[t];
-    const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)hoffs[t - 1] * H;
-    gemm<false, false>(c, bs, H3, H, hp, H, params + m.o_ux, H3, EpiStore{ws.hu.p + (size_t)o * H3, H3});
-    gru_fwd_gate_kernel<<<cdiv((size_t)bs * H, 256), 256, 0, c->stream>>>(
-        bs, o, H, ws.xp.p, ws.hu.p, hp, store ? ws.gates.p : nullptr, ws.hidden.p, ws.hprev.p);
-    after_launch(c);
-  }
+  gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store);
 }
 
 void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out) {
@@ -637,38 +604,6 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
 }
 
 // ------------------------------------------------------------ backward
-// Gate gradients of timestep rows [o, o+bs) (Appendix A of SURVEY.md):
-//   g = dhidden + carry (rows j < bs_next), dn = g(1-z), dz = g(h-n),
-//   dpre_n = dn(1-n^2), dr = dpre_n * hUn, dpre_r = dr r(1-r), dpre_z = dz z(1-z)
-__global__ void gru_bwd_gate_kernel(int bs, int bs_next, int o, int H, const float* __restrict__ dhidden,
-                                    const float* __restrict__ carry, const float* __restrict__ gates,
-                                    const float* __restrict__ hu, const float* __restrict__ hprev,
-                                    float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)bs * H) return;
-  const int j = (int)(i / H), u = (int)(i % H);
-  const size_t p = (size_t)o + j;
-  float g = dhidden[p * H + u];
-  if (j < bs_next) g += carry[(size_t)j * H + u];
-  const size_t g3 = p * 3 * H + 3 * u;
-  const float r = gates[g3 + 0], z = gates[g3 + 1], n = gates[g3 + 2];
-  const float hn = hu[g3 + 2];
-  const float hp = hprev[p * H + u];
-  const float dn = g * (1.f - z);
-  const float dz = g * (hp - n);
-  const float dpn = dn * (1.f - n * n);
-  const float dr = dpn * hn;
-  const float dpr = dr * r * (1.f - r);
-  const float dpz = dz * z * (1.f - z);
-  dpre[g3 + 0] = dpr;
-  dpre[g3 + 1] = dpz;
-  dpre[g3 + 2] = dpn;
-  dhu[g3 + 0] = dpr;
-  dhu[g3 + 1] = dpz;
-  dhu[g3 + 2] = dpn * r;
-  gz[(size_t)j * H + u] = g * z;
-}
-
 __global__ void dw1_kernel(const float* __restrict__ obs, const float* __restrict__ dpre1, int S, int D, int E,
                            float* __restrict__ dw1) {
   // dw1[d, k] = sum_p obs[p, d] dpre1[p, k]  (small: D x E outputs, K = S)
@@ -680,23 +615,10 @@ __global__ void dw1_kernel(const float* __restrict__ obs, const float* __restric
   dw1[(size_t)d * E + k] = s;
 }
 
-void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
-                     const std::vector<int32_t>& hbs, const std::vector<int32_t>& hoffs, Workspace& ws,
-                     float* grad) {
-  (void)h0;
+void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
+                     const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad) {
   const int E = m.E, H = m.H, H3 = 3 * m.H;
-  const int L = (int)hbs.size();
-  for (int t = L - 1; t >= 0; --t) {
-    const int bs = hbs[t], o = hoffs[t];
-    const int bs_next = t + 1 < L ? hbs[t + 1] : 0;
-    gru_bwd_gate_kernel<<<cdiv((size_t)bs * H, 256), 256, 0, c->stream>>>(
-        bs, bs_next, o, H, ws.dhidden.p, ws.carry.p, ws.gates.p, ws.hu.p, ws.hprev.p, ws.dpre.p, ws.dhu.p, ws.g.p);
-    after_launch(c);
-    if (t > 0) {  // dh_{t-1} = dhU U^T + g z   (h0 needs no gradient)
-      gemm<false, true>(c, bs, H, H3, ws.dhu.p + (size_t)o * H3, H3, params + m.o_ux, H3,
-                        EpiAddTerm{ws.carry.p, H, ws.g.p, H});
-    }
-  }
+  gru_backward_recurrence(c, m, params, L, d_bs, d_offs, ws);
   // weight gradients over all rows
   gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
   gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);

@@ -39,15 +39,23 @@ struct Workspace {
   DBuf<double> part;                                    // loss partials
   DBuf<float> wpart;                                    // head-weight partials
   DBuf<float> is_w;
+  DBuf<unsigned> bar;                                   // grid barrier of the recurrence
   void ensure(const Model& m, size_t S, bool train);
 };
 
 // Forward of the encoder + GRU over a packed batch of S rows.
-//   obs: S x D (packed), h0: bs[0] x H, hbs/hoffs: host batch sizes/offsets.
-//   store: keep e1/enc/xp/hu/gates/hprev for the backward pass.
+//   obs: S x D (packed), h0: bs[0] x H, d_bs/d_offs: device batch sizes /
+//   offsets of the L timesteps.  store: keep e1/enc/xp/hUn/gates/hprev for
+//   the backward pass.
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs,
-                    const float* h0, const std::vector<int32_t>& hbs,
-                    const std::vector<int32_t>& hoffs, Workspace& ws, bool store);
+                    const float* h0, int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws,
+                    bool store);
+
+// Persistent recurrence kernels (recurrence.cu)
+void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
+                            const int32_t* d_offs, Workspace& ws, const float* h0, bool store);
+void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
+                             const int32_t* d_offs, Workspace& ws);
 
 // Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
 // dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights
@@ -67,9 +75,8 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
 
 // Backward through the recurrence and the encoder; fills the remaining
 // gradient slots of `grad` (device layout).  Requires policy_forward(store).
-void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs,
-                     const float* h0, const std::vector<int32_t>& hbs,
-                     const std::vector<int32_t>& hoffs, Workspace& ws, float* grad);
+void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
+                     const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad);
 
 // Per-row log-prob / entropy / value of the heads (nn.cpp:251-278)
 void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float* hidden,

@@ -83,7 +83,10 @@ __global__ void yield_count_kernel(const double* __restrict__ tau, int n, const 
                                    long long smax, int32_t* __restrict__ cnt) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double bound = *tstar;
+  // the bisection's snapped T* can sit an ulp below the S_max-th product
+  // k*tau (floor(t/tau) vs k*tau rounding): enumerate with a relative slack;
+  // surplus yields beyond S_max are harmless (only sorted[0, S_max) is read)
+  const double bound = *tstar * (1.0 + 1e-9);
   long long k = (long long)floor(bound / tau[i]);
   while (k > 0 && (double)k * tau[i] > bound) --k;
   while ((double)(k + 1) * tau[i] <= bound) ++k;

@@ -1,0 +1,304 @@
+// recurrence.cu — the GRU recurrence over a packed minibatch (nn.cpp:235-250)
+// forward and backward as persistent cooperative kernels.
+//
+// Work split: the H hidden units are cut into UB unit blocks of UPB = 16
+// units; the grid is UB x RB CTAs (H = 512: 32 x 4 = 128 CTAs, one per SM).
+// A CTA keeps the recurrent weights of its units resident in shared memory
+// for the whole minibatch:
+//   forward : U[:, gates of its units]   (H x 48 fp32  = 96 KB at H = 512)
+//   backward: U[its units, :]            (16 x 3H fp32 = 96 KB)
+// Every timestep t the bs_t live rows (a prefix of the rows of t-1, packed
+// sorted by length) are re-split across the RB CTAs of each unit block, the
+// rows' h_{t-1} (forward) / dhU_t (backward) are staged through shared memory
+// from L2, each (row, unit) dot product is split over K by up to 16 threads,
+// and one grid-wide barrier separates timesteps.  No launches per timestep.
+//
+// Forward per (row j, unit u):  r = s(xr + h Ur), z = s(xz + h Uz),
+//   n = tanh(xn + r * (h Un)), h' = (1-z) n + z h      (xp holds x W + b)
+// Backward per (row j, unit u) at step t-1, fused with step t's
+//   dh_{t-1}[j,u] = dhU_t[j,:] . U[u,:] + g_t z_t    (j < bs_t)
+//   g = dhidden + dh_{t-1};  dn = g(1-z), dz = g(h-n), dpre_n = dn(1-n^2),
+//   dr = dpre_n hUn, dpre_r = dr r(1-r), dpre_z = dz z(1-z)
+// so the backward also needs one barrier per timestep.
+#include "policy.cuh"
+
+namespace verg {
+
+constexpr int RT = 256;   // threads per CTA
+constexpr int UPB = 16;   // units per unit block
+constexpr int RCHF = 16;  // forward rows staged per chunk
+constexpr int RCHB = 8;   // backward rows staged per chunk
+
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+
+struct RecGeom {
+  int UB, RB;
+};
+static RecGeom geom(const Ctx* c, int H) {
+  RecGeom g;
+  g.UB = (H + UPB - 1) / UPB;
+  g.RB = std::max(1, c->num_sms / g.UB);
+  return g;
+}
+
+// ------------------------------------------------------------ forward
+__global__ void __launch_bounds__(RT, 1) gru_fwd_persistent(
+    int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int H, int UB, int RB,
+    const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
+    float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar) {
+  extern __shared__ float sm[];
+  constexpr int US = 3 * UPB + 1;
+  float* Us = sm;               // H x US
+  float* hs = Us + H * US;      // RCHF x H
+  float* red = hs + RCHF * H;   // 16 x UPB x 3
+  const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
+  const int u0 = ub * UPB, nu = min(UPB, H - u0);
+  const int H3 = 3 * H;
+  for (int i = threadIdx.x; i < H * 3 * UPB; i += RT) {
+    const int k = i / (3 * UPB), c = i % (3 * UPB);
+    Us[k * US + c] = (c / 3 < nu) ? ux[(size_t)k * H3 + 3 * u0 + c] : 0.f;
+  }
+  __syncthreads();
+  const int ul = threadIdx.x % UPB, q = threadIdx.x / UPB;
+  unsigned target = 0;
+  for (int t = 0; t < L; ++t) {
+    const int B = bs[t], o = offs[t];
+    const float* hp = (t == 0) ? h0 : hidden + (size_t)offs[t - 1] * H;
+    const int rpc = (B + RB - 1) / RB;
+    const int r0 = rb * rpc, r1 = min(B, r0 + rpc);
+    for (int c0 = r0; c0 < r1; c0 += RCHF) {
+      const int nr = min(RCHF, r1 - c0);
+      const float* src = hp + (size_t)c0 * H;
+      for (int i = threadIdx.x; i < nr * H; i += RT) hs[i] = __ldcg(src + i);
+      __syncthreads();
+      int nrp = 1;
+      while (nrp < nr) nrp <<= 1;
+      const int KS = 16 / nrp;
+      const int row = q / KS, ks = q % KS;
+      float ar = 0.f, az = 0.f, an = 0.f;
+      if (row < nr) {
+        const int k0 = (ks * H) / KS, k1 = ((ks + 1) * H) / KS;
+        const float* hrow = hs + row * H;
+        const float* uc = Us + 3 * ul;
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) {
+          const float h = hrow[k];
+          const float* uk = uc + k * US;
+          ar = fmaf(h, uk[0], ar);
+          az = fmaf(h, uk[1], az);
+          an = fmaf(h, uk[2], an);
+        }
+      }
+      float* rq = red + (q * UPB + ul) * 3;
+      rq[0] = ar;
+      rq[1] = az;
+      rq[2] = an;
+      __syncthreads();
+      if (ks == 0 && row < nr && ul < nu) {
+        float sr = 0.f, sz = 0.f, sn = 0.f;
+        for (int s = 0; s < KS; ++s) {
+          const float* rr = red + ((row * KS + s) * UPB + ul) * 3;
+          sr += rr[0];
+          sz += rr[1];
+          sn += rr[2];
+        }
+        const int u = u0 + ul;
+        const size_t p = (size_t)o + c0 + row;
+        const float* x = xp + p * H3 + 3 * u;
+        const float r = sigm(x[0] + sr);
+        const float z = sigm(x[1] + sz);
+        const float n = tanhf(x[2] + r * sn);
+        const float hprev = hs[row * H + u];
+        hidden[p * H + u] = (1.f - z) * n + z * hprev;
+        if (gates) {
+          float* gp = gates + p * H3 + 3 * u;
+          gp[0] = r;
+          gp[1] = z;
+          gp[2] = n;
+          hun[p * H + u] = sn;
+          hprev_store[p * H + u] = hprev;
+        }
+      }
+      __syncthreads();
+    }
+    target += gridDim.x;
+    if (t + 1 < L) grid_barrier(bar, target);
+  }
+}
+
+// ----------------------------------------------------------- backward
+__device__ __forceinline__ void gate_grad(size_t p, int u, int H, float g, const float* __restrict__ gates,
+                                          const float* __restrict__ hun, const float* __restrict__ hprev,
+                                          float* __restrict__ dpre, float* __restrict__ dhu,
+                                          float* __restrict__ gz) {
+  const float* gp = gates + p * 3 * H + 3 * u;
+  const float r = gp[0], z = gp[1], n = gp[2];
+  const float hn = hun[p * H + u];
+  const float hp = hprev[p * H + u];
+  const float dn = g * (1.f - z);
+  const float dz = g * (hp - n);
+  const float dpn = dn * (1.f - n * n);
+  const float dr = dpn * hn;
+  const float dpr = dr * r * (1.f - r);
+  const float dpz = dz * z * (1.f - z);
+  float* d = dpre + p * 3 * H + 3 * u;
+  d[0] = dpr;
+  d[1] = dpz;
+  d[2] = dpn;
+  float* e = dhu + p * 3 * H + 3 * u;
+  e[0] = dpr;
+  e[1] = dpz;
+  e[2] = dpn * r;
+  gz[p * H + u] = g * z;
+}
+
+__global__ void __launch_bounds__(RT, 1) gru_bwd_persistent(
+    int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int H, int UB, int RB,
+    const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
+    const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
+    unsigned* bar) {
+  extern __shared__ float sm[];
+  const int H3 = 3 * H;
+  const int WS = H3 + 1;
+  float* Ws = sm;                 // UPB x WS : U rows of this block's units
+  float* ds = Ws + UPB * WS;      // RCHB x H3 : staged dhU rows
+  float* red = ds + RCHB * H3;    // 16 x UPB
+  const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
+  const int u0 = ub * UPB, nu = min(UPB, H - u0);
+  for (int i = threadIdx.x; i < UPB * H3; i += RT) {
+    const int r = i / H3, c = i % H3;
+    Ws[r * WS + c] = r < nu ? ux[(size_t)(u0 + r) * H3 + c] : 0.f;
+  }
+  __syncthreads();
+  const int ul = threadIdx.x % UPB, q = threadIdx.x / UPB;
+  unsigned target = 0;
+  // step L-1: no carry
+  {
+    const int B = bs[L - 1], o = offs[L - 1];
+    const int rpc = (B + RB - 1) / RB;
+    const int r0 = rb * rpc, r1 = min(B, r0 + rpc);
+    for (int idx = threadIdx.x; idx < (r1 - r0) * UPB; idx += RT) {
+      const int j = r0 + idx / UPB, l = idx % UPB;
+      if (l < nu) {
+        const size_t p = (size_t)o + j;
+        gate_grad(p, u0 + l, H, dhidden[p * H + u0 + l], gates, hun, hprev, dpre, dhu, gz);
+      }
+    }
+  }
+  target += gridDim.x;
+  if (L > 1) grid_barrier(bar, target);
+  for (int t = L - 1; t >= 1; --t) {
+    const int B = bs[t], Bp = bs[t - 1], o = offs[t], op = offs[t - 1];
+    const int rpc = (Bp + RB - 1) / RB;
+    const int r0 = rb * rpc, r1 = min(Bp, r0 + rpc);
+    // rows with a successor at step t: dh_{t-1} = dhU_t U^T + g_t z_t
+    const int rc1 = min(r1, B);
+    for (int c0 = r0; c0 < rc1; c0 += RCHB) {
+      const int nr = min(RCHB, rc1 - c0);
+      const float* src = dhu + ((size_t)o + c0) * H3;
+      for (int i = threadIdx.x; i < nr * H3; i += RT) ds[i] = __ldcg(src + i);
+      __syncthreads();
+      int nrp = 1;
+      while (nrp < nr) nrp <<= 1;
+      const int KS = 16 / nrp;
+      const int row = q / KS, ks = q % KS;
+      float acc = 0.f;
+      if (row < nr) {
+        const int k0 = (ks * H3) / KS, k1 = ((ks + 1) * H3) / KS;
+        const float* drow = ds + row * H3;
+        const float* wr = Ws + ul * WS;
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) acc = fmaf(drow[k], wr[k], acc);
+      }
+      red[q * UPB + ul] = acc;
+      __syncthreads();
+      if (ks == 0 && row < nr && ul < nu) {
+        float s = 0.f;
+        for (int k = 0; k < KS; ++k) s += red[(row * KS + k) * UPB + ul];
+        const int u = u0 + ul;
+        const int j = c0 + row;
+        const float dh = s + __ldcg(gz + ((size_t)o + j) * H + u);
+        const size_t pp = (size_t)op + j;
+        gate_grad(pp, u, H, dhidden[pp * H + u] + dh, gates, hun, hprev, dpre, dhu, gz);
+      }
+      __syncthreads();
+    }
+    // rows that end at step t-1 (j >= bs_t): gradient from the heads only
+    const int re0 = max(r0, B);
+    for (int idx = threadIdx.x; idx < max(0, r1 - re0) * UPB; idx += RT) {
+      const int j = re0 + idx / UPB, l = idx % UPB;
+      if (l < nu) {
+        const size_t pp = (size_t)op + j;
+        gate_grad(pp, u0 + l, H, dhidden[pp * H + u0 + l], gates, hun, hprev, dpre, dhu, gz);
+      }
+    }
+    target += gridDim.x;
+    if (t > 1) grid_barrier(bar, target);
+  }
+}
+
+// ------------------------------------------------------------ launch
+static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** args) {
+  VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, RT, smem));
+  if (per_sm * c->num_sms < grid)
+    config_error("recurrence: grid does not fit co-resident (hidden dim too large for this build)");
+  VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(RT), args, smem, c->stream));
+  after_launch(c);
+}
+
+void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
+                            const int32_t* d_offs, Workspace& ws, const float* h0, bool store) {
+  const RecGeom g = geom(c, m.H);
+  const int grid = g.UB * g.RB;
+  ws.bar.reserve(c, 1);
+  ws.bar.zero(1);
+  const size_t smem = sizeof(float) * ((size_t)m.H * (3 * UPB + 1) + (size_t)RCHF * m.H + 16 * UPB * 3);
+  int H = m.H, UB = g.UB, RB = g.RB;
+  const float* ux = params + m.o_ux;
+  const float* xp = ws.xp.p;
+  float* hidden = ws.hidden.p;
+  float* gates = store ? ws.gates.p : nullptr;
+  float* hun = ws.hu.p;
+  float* hps = ws.hprev.p;
+  unsigned* bar = ws.bar.p;
+  void* args[] = {&L, &d_bs, &d_offs, &H, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar};
+  coop_launch(c, reinterpret_cast<const void*>(gru_fwd_persistent), grid, smem, args);
+}
+
+void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
+                             const int32_t* d_offs, Workspace& ws) {
+  const RecGeom g = geom(c, m.H);
+  const int grid = g.UB * g.RB;
+  ws.bar.reserve(c, 1);
+  ws.bar.zero(1);
+  const size_t smem = sizeof(float) * ((size_t)UPB * (3 * m.H + 1) + (size_t)RCHB * 3 * m.H + 16 * UPB);
+  int H = m.H, UB = g.UB, RB = g.RB;
+  const float* ux = params + m.o_ux;
+  const float* dh = ws.dhidden.p;
+  const float* gates = ws.gates.p;
+  const float* hun = ws.hu.p;
+  const float* hps = ws.hprev.p;
+  float* dpre = ws.dpre.p;
+  float* dhu = ws.dhu.p;
+  float* gz = ws.g.p;
+  unsigned* bar = ws.bar.p;
+  void* args[] = {&L, &d_bs, &d_offs, &H, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar};
+  coop_launch(c, reinterpret_cast<const void*>(gru_bwd_persistent), grid, smem, args);
+}
+
+}  // namespace verg
