@@ -250,6 +250,184 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_persistent(
   }
 }
 
+// ----------------------------------------- register-resident fast path
+// H = 16*KL.  Thread (ul = tid / 16, ks = tid % 16): a warp holds 2 units x
+// 16 K-slices.  The thread keeps its KL x 3 (forward) / 3*KL (backward)
+// weights in registers for the whole minibatch, so per staged row it issues
+// KL*3 FMAs against KL broadcast shared-memory reads and a 4-step xor-shuffle
+// reduction over its 16-lane half warp: FMA-bound instead of LDS-bound.
+constexpr int RCF = 32;  // forward rows per staged chunk (32 x H fp32)
+constexpr int RCB = 8;   // backward rows per staged chunk (8 x 3H fp32)
+
+template <int KL>
+__global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
+    int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
+    const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
+    float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar) {
+  constexpr int H = 16 * KL;
+  constexpr int H3 = 3 * H;
+  extern __shared__ float4 sm4[];
+  float* hs = reinterpret_cast<float*>(sm4);  // RCF x H
+  const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
+  const int ul = threadIdx.x >> 4, ks = threadIdx.x & 15;
+  const int u = ub * UPB + ul;
+  float w[KL][3];
+#pragma unroll
+  for (int k = 0; k < KL; ++k)
+#pragma unroll
+    for (int g = 0; g < 3; ++g) w[k][g] = ux[(size_t)(ks * KL + k) * H3 + 3 * u + g];
+  unsigned target = 0;
+  for (int t = 0; t < L; ++t) {
+    const int B = bs[t], o = offs[t];
+    const float* hp = (t == 0) ? h0 : hidden + (size_t)offs[t - 1] * H;
+    const int rpc = (B + RB - 1) / RB;
+    const int r0 = rb * rpc, r1 = min(B, r0 + rpc);
+    for (int c0 = r0; c0 < r1; c0 += RCF) {
+      const int nr = min(RCF, r1 - c0);
+      const float4* src = reinterpret_cast<const float4*>(hp + (size_t)c0 * H);
+      for (int i = threadIdx.x; i < nr * H / 4; i += RT) sm4[i] = __ldcg(src + i);
+      __syncthreads();
+      for (int row = 0; row < nr; ++row) {
+        const float* hk = hs + row * H + ks * KL;
+        float ar = 0.f, az = 0.f, an = 0.f;
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+          const float h = hk[k];
+          ar = fmaf(h, w[k][0], ar);
+          az = fmaf(h, w[k][1], az);
+          an = fmaf(h, w[k][2], an);
+        }
+#pragma unroll
+        for (int s = 8; s > 0; s >>= 1) {
+          ar += __shfl_xor_sync(0xffffffffu, ar, s);
+          az += __shfl_xor_sync(0xffffffffu, az, s);
+          an += __shfl_xor_sync(0xffffffffu, an, s);
+        }
+        if (ks == 0) {
+          const size_t p = (size_t)o + c0 + row;
+          const float* x = xp + p * H3 + 3 * u;
+          const float r = sigm(x[0] + ar);
+          const float z = sigm(x[1] + az);
+          const float n = tanhf(x[2] + r * an);
+          const float hprev = hs[row * H + u];
+          hidden[p * H + u] = (1.f - z) * n + z * hprev;
+          if (gates) {
+            float* gp = gates + p * H3 + 3 * u;
+            gp[0] = r;
+            gp[1] = z;
+            gp[2] = n;
+            hun[p * H + u] = an;
+            hprev_store[p * H + u] = hprev;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    target += gridDim.x;
+    if (t + 1 < L) grid_barrier(bar, target);
+  }
+}
+
+template <int KL>
+__global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
+    int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
+    const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
+    const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
+    unsigned* bar) {
+  constexpr int H = 16 * KL;
+  constexpr int H3 = 3 * H;
+  constexpr int CL = 3 * KL;  // columns of U[u, :] per K-slice
+  extern __shared__ float4 sm4[];
+  float* ds = reinterpret_cast<float*>(sm4);  // RCB x H3
+  const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
+  const int ul = threadIdx.x >> 4, cs = threadIdx.x & 15;
+  const int u = ub * UPB + ul;
+  float w[CL];
+#pragma unroll
+  for (int k = 0; k < CL; ++k) w[k] = ux[(size_t)u * H3 + cs * CL + k];
+  unsigned target = 0;
+  {
+    const int B = bs[L - 1], o = offs[L - 1];
+    const int rpc = (B + RB - 1) / RB;
+    const int r0 = rb * rpc, r1 = min(B, r0 + rpc);
+    for (int idx = threadIdx.x; idx < (r1 - r0) * UPB; idx += RT) {
+      const int j = r0 + idx / UPB, l = idx % UPB;
+      const size_t p = (size_t)o + j;
+      gate_grad(p, ub * UPB + l, H, dhidden[p * H + ub * UPB + l], gates, hun, hprev, dpre, dhu, gz);
+    }
+  }
+  target += gridDim.x;
+  if (L > 1) grid_barrier(bar, target);
+  for (int t = L - 1; t >= 1; --t) {
+    const int B = bs[t], Bp = bs[t - 1], o = offs[t], op = offs[t - 1];
+    const int rpc = (Bp + RB - 1) / RB;
+    const int r0 = rb * rpc, r1 = min(Bp, r0 + rpc);
+    const int rc1 = min(r1, B);
+    for (int c0 = r0; c0 < rc1; c0 += RCB) {
+      const int nr = min(RCB, rc1 - c0);
+      const float4* src = reinterpret_cast<const float4*>(dhu + ((size_t)o + c0) * H3);
+      for (int i = threadIdx.x; i < nr * H3 / 4; i += RT) sm4[i] = __ldcg(src + i);
+      __syncthreads();
+      for (int row = 0; row < nr; ++row) {
+        const float* dk = ds + row * H3 + cs * CL;
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < CL; ++k) acc = fmaf(dk[k], w[k], acc);
+#pragma unroll
+        for (int s = 8; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+        if (cs == 0) {
+          const int j = c0 + row;
+          const float dh = acc + __ldcg(gz + ((size_t)o + j) * H + u);
+          const size_t pp = (size_t)op + j;
+          gate_grad(pp, u, H, dhidden[pp * H + u] + dh, gates, hun, hprev, dpre, dhu, gz);
+        }
+      }
+      __syncthreads();
+    }
+    const int re0 = max(r0, B);
+    for (int idx = threadIdx.x; idx < max(0, r1 - re0) * UPB; idx += RT) {
+      const int j = re0 + idx / UPB, l = idx % UPB;
+      const size_t pp = (size_t)op + j;
+      gate_grad(pp, ub * UPB + l, H, dhidden[pp * H + ub * UPB + l], gates, hun, hprev, dpre, dhu, gz);
+    }
+    target += gridDim.x;
+    if (t > 1) grid_barrier(bar, target);
+  }
+}
+
+template <int KL>
+static const void* fwd_reg_fn() {
+  return reinterpret_cast<const void*>(gru_fwd_reg<KL>);
+}
+template <int KL>
+static const void* bwd_reg_fn() {
+  return reinterpret_cast<const void*>(gru_bwd_reg<KL>);
+}
+static const void* pick_fwd(int H) {
+  switch (H) {
+    case 16: return fwd_reg_fn<1>();
+    case 32: return fwd_reg_fn<2>();
+    case 48: return fwd_reg_fn<3>();
+    case 64: return fwd_reg_fn<4>();
+    case 128: return fwd_reg_fn<8>();
+    case 256: return fwd_reg_fn<16>();
+    case 512: return fwd_reg_fn<32>();
+    default: return nullptr;
+  }
+}
+static const void* pick_bwd(int H) {
+  switch (H) {
+    case 16: return bwd_reg_fn<1>();
+    case 32: return bwd_reg_fn<2>();
+    case 48: return bwd_reg_fn<3>();
+    case 64: return bwd_reg_fn<4>();
+    case 128: return bwd_reg_fn<8>();
+    case 256: return bwd_reg_fn<16>();
+    case 512: return bwd_reg_fn<32>();
+    default: return nullptr;
+  }
+}
+
 // ------------------------------------------------------------ launch
 static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** args) {
   VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -267,7 +445,6 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   const int grid = g.UB * g.RB;
   ws.bar.reserve(c, 1);
   ws.bar.zero(1);
-  const size_t smem = sizeof(float) * ((size_t)m.H * (3 * UPB + 1) + (size_t)RCHF * m.H + 16 * UPB * 3);
   int H = m.H, UB = g.UB, RB = g.RB;
   const float* ux = params + m.o_ux;
   const float* xp = ws.xp.p;
@@ -276,6 +453,13 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   float* hun = ws.hu.p;
   float* hps = ws.hprev.p;
   unsigned* bar = ws.bar.p;
+  if (const void* fn = pick_fwd(m.H)) {
+    const size_t smem = sizeof(float) * (size_t)RCF * m.H;
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar};
+    coop_launch(c, fn, grid, smem, args);
+    return;
+  }
+  const size_t smem = sizeof(float) * ((size_t)m.H * (3 * UPB + 1) + (size_t)RCHF * m.H + 16 * UPB * 3);
   void* args[] = {&L, &d_bs, &d_offs, &H, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar};
   coop_launch(c, reinterpret_cast<const void*>(gru_fwd_persistent), grid, smem, args);
 }
@@ -286,7 +470,6 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
   const int grid = g.UB * g.RB;
   ws.bar.reserve(c, 1);
   ws.bar.zero(1);
-  const size_t smem = sizeof(float) * ((size_t)UPB * (3 * m.H + 1) + (size_t)RCHB * 3 * m.H + 16 * UPB);
   int H = m.H, UB = g.UB, RB = g.RB;
   const float* ux = params + m.o_ux;
   const float* dh = ws.dhidden.p;
@@ -297,6 +480,13 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
   float* dhu = ws.dhu.p;
   float* gz = ws.g.p;
   unsigned* bar = ws.bar.p;
+  if (const void* fn = pick_bwd(m.H)) {
+    const size_t smem = sizeof(float) * (size_t)RCB * 3 * m.H;
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar};
+    coop_launch(c, fn, grid, smem, args);
+    return;
+  }
+  const size_t smem = sizeof(float) * ((size_t)UPB * (3 * m.H + 1) + (size_t)RCHB * 3 * m.H + 16 * UPB);
   void* args[] = {&L, &d_bs, &d_offs, &H, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar};
   coop_launch(c, reinterpret_cast<const void*>(gru_bwd_persistent), grid, smem, args);
 }
