@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
 #pragma unroll
   for (int k = 0; k < KL; ++k)
 #pragma unroll
-    for (int g = 0; g < 3; ++g) w[k][g] = ux[(size_t)(ks * KL + k) * H3 + 3 * u + g];
+    for (int g = 0; g < 3; ++g) w[k][g] = ux[(size_t)(ks + 16 * k) * H3 + 3 * u + g];
   unsigned target = 0;
   for (int t = 0; t < L; ++t) {
     const int B = bs[t], o = offs[t];
@@ -288,11 +288,11 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
       for (int i = threadIdx.x; i < nr * H / 4; i += RT) sm4[i] = __ldcg(src + i);
       __syncthreads();
       for (int row = 0; row < nr; ++row) {
-        const float* hk = hs + row * H + ks * KL;
+        const float* hk = hs + row * H + ks;  // K index ks + 16k: conflict-free banks
         float ar = 0.f, az = 0.f, an = 0.f;
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
-          const float h = hk[k];
+          const float h = hk[16 * k];
           ar = fmaf(h, w[k][0], ar);
           az = fmaf(h, w[k][1], az);
           an = fmaf(h, w[k][2], an);
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
   const int u = ub * UPB + ul;
   float w[CL];
 #pragma unroll
-  for (int k = 0; k < CL; ++k) w[k] = ux[(size_t)u * H3 + cs * CL + k];
+  for (int k = 0; k < CL; ++k) w[k] = ux[(size_t)u * H3 + cs + 16 * k];
   unsigned target = 0;
   {
     const int B = bs[L - 1], o = offs[L - 1];
@@ -369,10 +369,10 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
       for (int i = threadIdx.x; i < nr * H3 / 4; i += RT) sm4[i] = __ldcg(src + i);
       __syncthreads();
       for (int row = 0; row < nr; ++row) {
-        const float* dk = ds + row * H3 + cs * CL;
+        const float* dk = ds + row * H3 + cs;  // column cs + 16k: conflict-free banks
         float acc = 0.f;
 #pragma unroll
-        for (int k = 0; k < CL; ++k) acc = fmaf(dk[k], w[k], acc);
+        for (int k = 0; k < CL; ++k) acc = fmaf(dk[16 * k], w[k], acc);
 #pragma unroll
         for (int s = 8; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
         if (cs == 0) {
