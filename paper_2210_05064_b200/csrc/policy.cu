@@ -30,6 +30,7 @@ Model Model::make(const ver_model_config& c) {
   m.AH = m.A + 1;
   if (m.D < 1 || m.E < 1 || m.H < 1 || m.A < 1) config_error("model: dims must be >= 1");
   if (m.AH > 32) config_error("model: at most 31 actions supported by the fused loss");
+  if (m.D > 8) config_error("model: obs_dim <= 8 supported by the encoder-gradient kernel");
   const int64_t D = m.D, E = m.E, H = m.H, A = m.A, AH = m.AH;
   int64_t o = 0;
   m.o_w1 = o; o += D * E;
@@ -604,15 +605,44 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
 }
 
 // ------------------------------------------------------------ backward
-__global__ void dw1_kernel(const float* __restrict__ obs, const float* __restrict__ dpre1, int S, int D, int E,
-                           float* __restrict__ dw1) {
-  // dw1[d, k] = sum_p obs[p, d] dpre1[p, k]  (small: D x E outputs, K = S)
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int d = blockIdx.y;
-  if (k >= E) return;
+// db1 and dw1 in one pass over dpre1 (K = S rows, D = obs_dim small):
+// out[0][k] = sum_p dpre1[p,k];  out[1+d][k] = sum_p obs[p,d] dpre1[p,k]
+constexpr int kMaxD = 8;
+__global__ void enc1_grad_partial_kernel(const float* __restrict__ obs, const float* __restrict__ dpre1, int S,
+                                         int D, int E, int rows_per, float* __restrict__ part) {
+  __shared__ float red[8][33 * (kMaxD + 1)];
+  const int k = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r = threadIdx.x >> 5;
+  const int m0 = blockIdx.y * rows_per, m1 = min(S, m0 + rows_per);
+  float acc[kMaxD + 1];
+#pragma unroll
+  for (int d = 0; d <= kMaxD; ++d) acc[d] = 0.f;
+  if (k < E)
+    for (int m = m0 + r; m < m1; m += 8) {
+      const float g = dpre1[(size_t)m * E + k];
+      acc[0] += g;
+#pragma unroll
+      for (int d = 0; d < kMaxD; ++d)
+        if (d < D) acc[1 + d] = fmaf(obs[(size_t)m * D + d], g, acc[1 + d]);
+    }
+  for (int d = 0; d <= D; ++d) red[r][(threadIdx.x & 31) * (kMaxD + 1) + d] = acc[d];
+  __syncthreads();
+  if (r == 0 && k < E)
+    for (int d = 0; d <= D; ++d) {
+      float t = 0.f;
+      for (int q = 0; q < 8; ++q) t += red[q][(threadIdx.x & 31) * (kMaxD + 1) + d];
+      part[((size_t)blockIdx.y * (D + 1) + d) * E + k] = t;
+    }
+}
+__global__ void enc1_grad_final_kernel(const float* __restrict__ part, int chunks, int D, int E,
+                                       float* __restrict__ db1, float* __restrict__ dw1) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (D + 1) * E) return;
+  const int d = i / E, k = i % E;
   float s = 0.f;
-  for (int p = 0; p < S; ++p) s = fmaf(obs[(size_t)p * D + d], dpre1[(size_t)p * E + k], s);
-  dw1[(size_t)d * E + k] = s;
+  for (int c = 0; c < chunks; ++c) s += part[((size_t)c * (D + 1) + d) * E + k];
+  if (d == 0) db1[k] = s;
+  else dw1[(size_t)(d - 1) * E + k] = s;
 }
 
 void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
@@ -627,10 +657,17 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
   gemm_splitk<true, false>(c, ws, E, E, S, ws.e1.p, E, ws.dpre2.p, E, grad + m.o_w2, E);
   colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2);
   gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E});
-  dim3 g1(cdiv(E, 128), m.D);
-  dw1_kernel<<<g1, 128, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E, grad + m.o_w1);
-  after_launch(c);
-  colsum(c, ws, ws.dpre1.p, S, E, E, grad + m.o_b1);
+  {
+    const int rows_per = 512;
+    const int chunks = std::max(1, (int)cdiv(S, rows_per));
+    ws.splitk.reserve(c, (size_t)chunks * (m.D + 1) * E);
+    dim3 g1(cdiv(E, 32), chunks);
+    enc1_grad_partial_kernel<<<g1, 256, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E, rows_per, ws.splitk.p);
+    after_launch(c);
+    enc1_grad_final_kernel<<<cdiv((size_t)(m.D + 1) * E, 256), 256, 0, c->stream>>>(
+        ws.splitk.p, chunks, m.D, E, grad + m.o_b1, grad + m.o_w1);
+    after_launch(c);
+  }
 }
 
 // ---------------------------------------------------------------- Adam

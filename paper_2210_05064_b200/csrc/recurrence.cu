@@ -251,31 +251,69 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_persistent(
 }
 
 // ----------------------------------------- register-resident fast path
-// H = 16*KL.  Thread (ul = tid / 16, ks = tid % 16): a warp holds 2 units x
-// 16 K-slices.  The thread keeps its KL x 3 (forward) / 3*KL (backward)
-// weights in registers for the whole minibatch, so per staged row it issues
-// KL*3 FMAs against KL broadcast shared-memory reads and a 4-step xor-shuffle
-// reduction over its 16-lane half warp: FMA-bound instead of LDS-bound.
+// H multiple of 32.  Warp w of a CTA owns units u0+2w, u0+2w+1; lane l owns
+// the K indices VEC*l + 32*VEC*i + j (vector shared-memory loads, bank
+// conflict free).  The lane keeps its weights in registers for the whole
+// minibatch (forward: (H/32) x 2 units x 3 gates = 96 fp32 at H = 512;
+// backward: (3H/32) x 2 units = 96), so each staged row costs FMAs against
+// vector LDS only.  Rows are processed 4 at a time; the 4 x 2 x 4 (3 gates +
+// pad) forward partial sums are reduce-scattered across the 32 lanes in 31
+// shuffles (lane l ends with value l), the backward's 4 x 2 in 9.
 constexpr int RCF = 32;  // forward rows per staged chunk (32 x H fp32)
 constexpr int RCB = 8;   // backward rows per staged chunk (8 x 3H fp32)
 
-template <int KL>
+template <int NV>
+__device__ __forceinline__ void load_vec(const float* p, float* out) {
+  if constexpr (NV == 4) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+  } else if constexpr (NV == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    out[0] = v.x; out[1] = v.y;
+  } else {
+    out[0] = p[0];
+  }
+}
+
+// 32 partial sums per lane -> lane l holds the warp total of value l
+__device__ __forceinline__ float reduce_scatter32(float* a, int lane) {
+#pragma unroll
+  for (int s = 16, n = 16; s > 0; s >>= 1, n >>= 1) {
+    const bool up = lane & s;
+#pragma unroll
+    for (int v = 0; v < n; ++v) {
+      const float send = up ? a[v] : a[v + n];
+      const float keep = up ? a[v + n] : a[v];
+      a[v] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return a[0];
+}
+
+template <int H>
 __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
     float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar) {
-  constexpr int H = 16 * KL;
   constexpr int H3 = 3 * H;
+  constexpr int KPL = H / 32;
+  constexpr int VEC = KPL % 4 == 0 ? 4 : (KPL % 2 == 0 ? 2 : 1);
+  constexpr int NI = KPL / VEC;
   extern __shared__ float4 sm4[];
   float* hs = reinterpret_cast<float*>(sm4);  // RCF x H
   const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
-  const int ul = threadIdx.x >> 4, ks = threadIdx.x & 15;
-  const int u = ub * UPB + ul;
-  float w[KL][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ua = ub * UPB + 2 * warp;  // units ua, ua + 1
+  float w[NI][VEC][2][3];
 #pragma unroll
-  for (int k = 0; k < KL; ++k)
+  for (int i = 0; i < NI; ++i)
 #pragma unroll
-    for (int g = 0; g < 3; ++g) w[k][g] = ux[(size_t)(ks + 16 * k) * H3 + 3 * u + g];
+    for (int j = 0; j < VEC; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int g = 0; g < 3; ++g)
+          w[i][j][q][g] = ux[(size_t)(VEC * lane + 32 * VEC * i + j) * H3 + 3 * (ua + q) + g];
   unsigned target = 0;
   for (int t = 0; t < L; ++t) {
     const int B = bs[t], o = offs[t];
@@ -287,36 +325,44 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
       const float4* src = reinterpret_cast<const float4*>(hp + (size_t)c0 * H);
       for (int i = threadIdx.x; i < nr * H / 4; i += RT) sm4[i] = __ldcg(src + i);
       __syncthreads();
-      for (int row = 0; row < nr; ++row) {
-        const float* hk = hs + row * H + ks;  // K index ks + 16k: conflict-free banks
-        float ar = 0.f, az = 0.f, an = 0.f;
+      for (int g0 = 0; g0 < nr; g0 += 4) {
+        float acc[32];
 #pragma unroll
-        for (int k = 0; k < KL; ++k) {
-          const float h = hk[16 * k];
-          ar = fmaf(h, w[k][0], ar);
-          az = fmaf(h, w[k][1], az);
-          an = fmaf(h, w[k][2], an);
-        }
+        for (int v = 0; v < 32; ++v) acc[v] = 0.f;
 #pragma unroll
-        for (int s = 8; s > 0; s >>= 1) {
-          ar += __shfl_xor_sync(0xffffffffu, ar, s);
-          az += __shfl_xor_sync(0xffffffffu, az, s);
-          an += __shfl_xor_sync(0xffffffffu, an, s);
+        for (int i = 0; i < NI; ++i) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            float h[VEC];
+            load_vec<VEC>(hs + (g0 + r) * H + VEC * lane + 32 * VEC * i, h);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j)
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int g = 0; g < 3; ++g) acc[r * 8 + q * 4 + g] = fmaf(h[j], w[i][j][q][g], acc[r * 8 + q * 4 + g]);
+          }
         }
-        if (ks == 0) {
+        const float mine = reduce_scatter32(acc, lane);  // value index = lane = r*8 + q*4 + g
+        const float sz = __shfl_down_sync(0xffffffffu, mine, 1);
+        const float sn = __shfl_down_sync(0xffffffffu, mine, 2);
+        const int r = lane >> 3, q = (lane >> 2) & 1;
+        if ((lane & 3) == 0 && g0 + r < nr) {
+          const int u = ua + q;
+          const int row = g0 + r;
           const size_t p = (size_t)o + c0 + row;
           const float* x = xp + p * H3 + 3 * u;
-          const float r = sigm(x[0] + ar);
-          const float z = sigm(x[1] + az);
-          const float n = tanhf(x[2] + r * an);
+          const float rg = sigm(x[0] + mine);
+          const float zg = sigm(x[1] + sz);
+          const float ng = tanhf(x[2] + rg * sn);
           const float hprev = hs[row * H + u];
-          hidden[p * H + u] = (1.f - z) * n + z * hprev;
+          hidden[p * H + u] = (1.f - zg) * ng + zg * hprev;
           if (gates) {
             float* gp = gates + p * H3 + 3 * u;
-            gp[0] = r;
-            gp[1] = z;
-            gp[2] = n;
-            hun[p * H + u] = an;
+            gp[0] = rg;
+            gp[1] = zg;
+            gp[2] = ng;
+            hun[p * H + u] = sn;
             hprev_store[p * H + u] = hprev;
           }
         }
@@ -328,23 +374,28 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
   }
 }
 
-template <int KL>
+template <int H>
 __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
     const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
     unsigned* bar) {
-  constexpr int H = 16 * KL;
   constexpr int H3 = 3 * H;
-  constexpr int CL = 3 * KL;  // columns of U[u, :] per K-slice
+  constexpr int CPL = H3 / 32;  // columns per lane
+  constexpr int VEC = CPL % 4 == 0 ? 4 : (CPL % 2 == 0 ? 2 : 1);
+  constexpr int NI = CPL / VEC;
   extern __shared__ float4 sm4[];
   float* ds = reinterpret_cast<float*>(sm4);  // RCB x H3
   const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
-  const int ul = threadIdx.x >> 4, cs = threadIdx.x & 15;
-  const int u = ub * UPB + ul;
-  float w[CL];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ua = ub * UPB + 2 * warp;
+  float w[NI][VEC][2];
 #pragma unroll
-  for (int k = 0; k < CL; ++k) w[k] = ux[(size_t)u * H3 + cs + 16 * k];
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) w[i][j][q] = ux[(size_t)(ua + q) * H3 + VEC * lane + 32 * VEC * i + j];
   unsigned target = 0;
   {
     const int B = bs[L - 1], o = offs[L - 1];
@@ -368,16 +419,42 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
       const float4* src = reinterpret_cast<const float4*>(dhu + ((size_t)o + c0) * H3);
       for (int i = threadIdx.x; i < nr * H3 / 4; i += RT) sm4[i] = __ldcg(src + i);
       __syncthreads();
-      for (int row = 0; row < nr; ++row) {
-        const float* dk = ds + row * H3 + cs;  // column cs + 16k: conflict-free banks
-        float acc = 0.f;
+      for (int g0 = 0; g0 < nr; g0 += 4) {
+        float acc[8];
 #pragma unroll
-        for (int k = 0; k < CL; ++k) acc = fmaf(dk[16 * k], w[k], acc);
+        for (int v = 0; v < 8; ++v) acc[v] = 0.f;
 #pragma unroll
-        for (int s = 8; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-        if (cs == 0) {
-          const int j = c0 + row;
-          const float dh = acc + __ldcg(gz + ((size_t)o + j) * H + u);
+        for (int i = 0; i < NI; ++i) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            float d[VEC];
+            load_vec<VEC>(ds + (g0 + r) * H3 + VEC * lane + 32 * VEC * i, d);
+#pragma unroll
+            for (int j = 0; j < VEC; ++j)
+#pragma unroll
+              for (int q = 0; q < 2; ++q) acc[r * 2 + q] = fmaf(d[j], w[i][j][q], acc[r * 2 + q]);
+          }
+        }
+        // reduce-scatter 8 values over lane bits 16, 8, 4; then xor over bits 2, 1
+#pragma unroll
+        for (int s = 16, n = 4; s >= 4; s >>= 1, n >>= 1) {
+          const bool up = lane & s;
+#pragma unroll
+          for (int v = 0; v < n; ++v) {
+            const float send = up ? acc[v] : acc[v + n];
+            const float keep = up ? acc[v + n] : acc[v];
+            acc[v] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+          }
+        }
+        float tot = acc[0];
+        tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+        tot += __shfl_xor_sync(0xffffffffu, tot, 1);
+        const int v = lane >> 2;  // = r * 2 + q
+        const int r = v >> 1, q = v & 1;
+        if ((lane & 3) == 0 && g0 + r < nr) {
+          const int u = ua + q;
+          const int j = c0 + g0 + r;
+          const float dh = tot + __ldcg(gz + ((size_t)o + j) * H + u);
           const size_t pp = (size_t)op + j;
           gate_grad(pp, u, H, dhidden[pp * H + u] + dh, gates, hun, hprev, dpre, dhu, gz);
         }
@@ -395,35 +472,33 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
   }
 }
 
-template <int KL>
+template <int H>
 static const void* fwd_reg_fn() {
-  return reinterpret_cast<const void*>(gru_fwd_reg<KL>);
+  return reinterpret_cast<const void*>(gru_fwd_reg<H>);
 }
-template <int KL>
+template <int H>
 static const void* bwd_reg_fn() {
-  return reinterpret_cast<const void*>(gru_bwd_reg<KL>);
+  return reinterpret_cast<const void*>(gru_bwd_reg<H>);
 }
 static const void* pick_fwd(int H) {
   switch (H) {
-    case 16: return fwd_reg_fn<1>();
-    case 32: return fwd_reg_fn<2>();
-    case 48: return fwd_reg_fn<3>();
-    case 64: return fwd_reg_fn<4>();
-    case 128: return fwd_reg_fn<8>();
-    case 256: return fwd_reg_fn<16>();
-    case 512: return fwd_reg_fn<32>();
+    case 32: return fwd_reg_fn<32>();
+    case 64: return fwd_reg_fn<64>();
+    case 96: return fwd_reg_fn<96>();
+    case 128: return fwd_reg_fn<128>();
+    case 256: return fwd_reg_fn<256>();
+    case 512: return fwd_reg_fn<512>();
     default: return nullptr;
   }
 }
 static const void* pick_bwd(int H) {
   switch (H) {
-    case 16: return bwd_reg_fn<1>();
-    case 32: return bwd_reg_fn<2>();
-    case 48: return bwd_reg_fn<3>();
-    case 64: return bwd_reg_fn<4>();
-    case 128: return bwd_reg_fn<8>();
-    case 256: return bwd_reg_fn<16>();
-    case 512: return bwd_reg_fn<32>();
+    case 32: return bwd_reg_fn<32>();
+    case 64: return bwd_reg_fn<64>();
+    case 96: return bwd_reg_fn<96>();
+    case 128: return bwd_reg_fn<128>();
+    case 256: return bwd_reg_fn<256>();
+    case 512: return bwd_reg_fn<512>();
     default: return nullptr;
   }
 }
