@@ -53,9 +53,11 @@ ver_status ver_ctx_synchronize(ver_ctx ctx);
 ver_status ver_ctx_stream(ver_ctx ctx, uint64_t* stream_out);
 /* number of kernels this library launched on ctx since creation / last reset */
 ver_status ver_ctx_launch_count(ver_ctx ctx, int64_t* count, int reset);
-/* precision of the policy GEMMs: 0 = fp32 (parity, default), 1 = bf16 tensor
-   cores (fast mode, looser bound stated in DESIGN.md) */
+/* precision of the tensor-core policy GEMMs: 0 = 3xTF32 (fp32-grade, the
+   parity default), 1 = 1xTF32 (fast mode, looser bound stated in DESIGN.md) */
 ver_status ver_ctx_set_precision(ver_ctx ctx, int mode);
+/* 1 (default): batched policy GEMMs on tcgen05 tensor cores; 0: fp32 SIMT */
+ver_status ver_ctx_set_tensor_cores(ver_ctx ctx, int enable);
 
 /* NCCL (DD-PPO gradient AllReduce, distributed.cpp:86-116 / C1-C4 of SURVEY §2.2) */
 ver_status ver_nccl_unique_id(uint8_t id_out[128]);
@@ -279,6 +281,13 @@ ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed_s
 /* per-phase device time of the last update, ms (gae, sampler, gather, forward,
    recurrence, loss, backward, allreduce, adam); n in/out */
 ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n);
+
+/* Diagnostic: C (M x N, row-major) = op(A) op(B) through the library's GEMM
+   path (op(A) = A^T if transA: A stored K x M; op(B) = B^T if transB: B stored
+   N x K).  engine: 0 fp32 SIMT, 1 tcgen05 3xTF32, 2 tcgen05 1xTF32;
+   splitk > 1 uses the deterministic split-K partial + reduce path. */
+ver_status ver_debug_gemm(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K,
+                          const float* A, int lda, const float* B, int ldb, float* C, int splitk);
 
 /* ------------------------------------------------------- distributed (L7) */
 /* estimate_time (distributed.cpp:24-51), bisection with device counting */

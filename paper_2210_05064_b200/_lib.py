@@ -92,6 +92,7 @@ _SIGS = {
     "ver_ctx_stream": (c_int, [C.c_void_p, P(c_uint64)]),
     "ver_ctx_launch_count": (c_int, [C.c_void_p, P(c_int64), c_int]),
     "ver_ctx_set_precision": (c_int, [C.c_void_p, c_int]),
+    "ver_ctx_set_tensor_cores": (c_int, [C.c_void_p, c_int]),
     "ver_nccl_unique_id": (c_int, [C.c_char_p]),
     "ver_ctx_init_nccl": (c_int, [C.c_void_p, C.c_char_p, c_int, c_int]),
     "ver_allreduce_sum_i64": (c_int, [C.c_void_p, P(c_int64), c_int]),
@@ -152,6 +153,8 @@ _SIGS = {
     "ver_learner_get_state": (c_int, [C.c_void_p, P(c_double), P(c_int64), P(c_int64)]),
     "ver_learner_set_state": (c_int, [C.c_void_p, c_double, c_int64, c_int64]),
     "ver_learner_last_timing": (c_int, [C.c_void_p, P(c_float), P(c_int)]),
+    "ver_debug_gemm": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, P(c_float), c_int,
+                               P(c_float), c_int, P(c_float), c_int]),
     "ver_estimate_time": (c_int, [C.c_void_p, P(c_double), c_int, c_int64, c_int64, P(c_double)]),
     "ver_optimal_preempt_steps": (c_int, [C.c_void_p, P(c_double), c_int, c_double, c_int64,
                                           P(c_int64)]),

@@ -94,7 +94,12 @@ class Context:
         return n.value
 
     def set_precision(self, mode: int):
+        """0 = 3xTF32 tensor-core GEMMs (fp32-grade, default), 1 = 1xTF32 (fast)."""
         _check(_lib().ver_ctx_set_precision(self.h, mode))
+
+    def set_tensor_cores(self, enable: bool):
+        """True (default): tcgen05 GEMMs; False: fp32 SIMT GEMMs."""
+        _check(_lib().ver_ctx_set_tensor_cores(self.h, int(enable)))
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -798,6 +803,20 @@ class Learner:
         n = C.c_int(16)
         _check(_lib().ver_learner_last_timing(self.h, ms, C.byref(n)))
         return {PHASES[i]: float(ms[i]) for i in range(min(n.value, len(PHASES)))}
+
+
+def debug_gemm(A, B, transA=False, transB=False, engine=1, splitk=1, ctx: Context | None = None):
+    """C = op(A) op(B) through the library GEMM (engine 0 SIMT, 1 tcgen05 3xTF32, 2 tcgen05 1xTF32)."""
+    ctx = ctx or default_context()
+    A = _f32(A)
+    B = _f32(B)
+    M = A.shape[1] if transA else A.shape[0]
+    K = A.shape[0] if transA else A.shape[1]
+    N = B.shape[0] if transB else B.shape[1]
+    C_ = np.zeros((M, N), np.float32)
+    _check(_lib().ver_debug_gemm(ctx.h, engine, int(transA), int(transB), M, N, K, _ptr(A, C.c_float),
+                                 A.shape[1], _ptr(B, C.c_float), B.shape[1], _ptr(C_, C.c_float), splitk))
+    return C_
 
 
 # ---------------------------------------------------------- distributed

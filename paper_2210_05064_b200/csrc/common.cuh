@@ -61,7 +61,8 @@ struct Ctx {
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;  // kernels launched by this library on `stream`
-  int precision = 0;     // 0 fp32 parity, 1 bf16 tensor cores
+  int precision = 0;     // tensor-core GEMMs: 0 = 3xTF32 (fp32 parity), 1 = 1xTF32 (fast)
+  bool tensor_cores = true;  // tcgen05 GEMMs on (off: fp32 SIMT GEMMs)
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   // pinned scratch for small synchronous reads

@@ -16,6 +16,7 @@
 #include <cstring>
 
 #include "policy.cuh"
+#include "tc_gemm.cuh"
 
 namespace verg {
 
@@ -97,52 +98,6 @@ void Workspace::ensure(const Model& m, size_t S, bool train) {
 
 // -------------------------------------------------------------- GEMM
 constexpr int BM = 128, BN = 128, BK = 8, GT = 256;
-
-struct EpiStore {
-  float* C;
-  int ldc;
-  __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v; }
-};
-struct EpiBias {
-  float* C;
-  int ldc;
-  const float* bias;
-  __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v + bias[n]; }
-};
-struct EpiBiasTanh {
-  float* C;
-  int ldc;
-  const float* bias;
-  __device__ void operator()(int m, int n, float v, int) const {
-    C[(size_t)m * ldc + n] = tanhf(v + bias[n]);
-  }
-};
-struct EpiAddTerm {  // C = acc + T
-  float* C;
-  int ldc;
-  const float* T;
-  int ldt;
-  __device__ void operator()(int m, int n, float v, int) const {
-    C[(size_t)m * ldc + n] = v + T[(size_t)m * ldt + n];
-  }
-};
-struct EpiTanhGrad {  // C = acc * (1 - Y^2)
-  float* C;
-  int ldc;
-  const float* Y;
-  int ldy;
-  __device__ void operator()(int m, int n, float v, int) const {
-    const float y = Y[(size_t)m * ldy + n];
-    C[(size_t)m * ldc + n] = v * (1.f - y * y);
-  }
-};
-struct EpiPartial {  // split-K partial z
-  float* W;
-  int M, N;
-  __device__ void operator()(int m, int n, float v, int z) const {
-    W[((size_t)z * M + m) * N + n] = v;
-  }
-};
 
 template <bool TA, bool TB, class Epi>
 __global__ void __launch_bounds__(GT) sgemm_kernel(int M, int N, int K, const float* __restrict__ A,
@@ -237,6 +192,11 @@ __global__ void __launch_bounds__(GT) sgemm_kernel(int M, int N, int K, const fl
 template <bool TA, bool TB, class Epi>
 static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi) {
   if (M <= 0 || N <= 0) return;
+  if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb)) {
+    // op(A): TA ? MN-major : K-major;  op(B): TB ? K-major : MN-major
+    tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, epi, 1);
+    return;
+  }
   dim3 grid(cdiv(N, BN), cdiv(M, BM), 1);
   sgemm_kernel<TA, TB, Epi><<<grid, GT, 0, c->stream>>>(M, N, K, A, lda, B, ldb, epi, std::max(K, 1));
   after_launch(c);
@@ -257,6 +217,21 @@ template <bool TA, bool TB>
 static void gemm_splitk(Ctx* c, Workspace& ws, int M, int N, int K, const float* A, int lda, const float* B,
                         int ldb, float* C, int ldc) {
   if (M <= 0 || N <= 0) return;
+  if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb)) {
+    int Z = tc::splits_for(c, M, N, K);
+    if (Z == 1) {
+      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, EpiStore{C, ldc}, 1);
+      return;
+    }
+    const int nkb = (K + tc::BK - 1) / tc::BK;
+    const int per = (nkb + Z - 1) / Z;
+    Z = (nkb + per - 1) / per;
+    ws.splitk.reserve(c, (size_t)Z * M * N);
+    tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, EpiPartial{ws.splitk.p, M, N}, Z);
+    splitk_reduce_kernel<<<cdiv((size_t)M * N, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc);
+    after_launch(c);
+    return;
+  }
   const int tiles = (int)(cdiv(N, BN) * cdiv(M, BM));
   int Z = std::max(1, std::min((2 * c->num_sms + tiles - 1) / tiles, (int)cdiv(K, 256)));
   Z = std::min(Z, 64);
@@ -784,3 +759,46 @@ void init_params_host(const ver_model_config& c, uint64_t seed, double* out) {
 }
 
 }  // namespace verg
+
+using namespace verg;
+
+extern "C" ver_status ver_debug_gemm(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K,
+                                     const float* A, int lda, const float* B, int ldb, float* C, int splitk) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  const size_t na = transA ? (size_t)K * lda : (size_t)M * lda;
+  const size_t nb = transB ? (size_t)N * ldb : (size_t)K * ldb;
+  DBuf<float> dA, dB, dC;
+  dA.reserve(c, na);
+  dB.reserve(c, nb);
+  dC.reserve(c, (size_t)M * N);
+  dA.upload(A, na);
+  dB.upload(B, nb);
+  const bool tc0 = c->tensor_cores;
+  const int p0 = c->precision;
+  c->tensor_cores = engine != 0;
+  c->precision = engine == 2 ? 1 : 0;
+  Workspace ws;
+  ws.ctx = c;
+  try {
+    auto go = [&](auto ta, auto tb) {
+      constexpr bool TA = decltype(ta)::value, TB = decltype(tb)::value;
+      if (splitk > 1) gemm_splitk<TA, TB>(c, ws, M, N, K, dA.p, lda, dB.p, ldb, dC.p, N);
+      else gemm<TA, TB>(c, M, N, K, dA.p, lda, dB.p, ldb, EpiStore{dC.p, N});
+    };
+    if (!transA && !transB) go(std::false_type{}, std::false_type{});
+    else if (!transA && transB) go(std::false_type{}, std::true_type{});
+    else if (transA && !transB) go(std::true_type{}, std::false_type{});
+    else go(std::true_type{}, std::true_type{});
+  } catch (...) {
+    c->tensor_cores = tc0;
+    c->precision = p0;
+    throw;
+  }
+  c->tensor_cores = tc0;
+  c->precision = p0;
+  dC.download(C, (size_t)M * N);
+  sync(c);
+  VER_API_END
+}

@@ -1,0 +1,344 @@
+// tc_gemm.cu — the policy's batched GEMMs on the 5th-generation tensor cores.
+//
+// C (M x N) = op(A) op(B) with fused epilogue, fp32 in / fp32 out, on
+// tcgen05.mma kind::tf32 with accumulators in TMEM:
+//   * operands are staged by TMA (cp.async.bulk.tensor.2d, 128-byte swizzle)
+//     into a 3-stage shared-memory ring; K-major and MN-major operands are
+//     both native (no transposes in HBM);
+//   * parity mode (3xTF32): the four epilogue warps, idle during the main
+//     loop, split every landed stage in place into hi = rna_tf32(x) and
+//     lo = x - hi, so each K-step issues hi*hi + lo*hi + hi*lo.  Dropping
+//     lo*lo leaves ~2^-22 relative error per product: fp32-grade results,
+//     which is what the 1e-5 parity bound needs;  fast mode issues hi*hi only;
+//   * one elected thread issues the MMAs (M = 128, N = 128, K = 8 per
+//     instruction) and commits each stage back to the TMA producer through an
+//     mbarrier; the epilogue warps read the accumulator with tcgen05.ld
+//     (32x32b.x32) and apply bias / tanh / tanh-gradient / split-K partials.
+// Warp roles (192 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer,
+// 2..5 split + epilogue.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "epilogue.cuh"
+
+namespace verg {
+namespace tc {
+
+constexpr int BM = 128, BN = 128, BK = 32;  // BK in fp32 elements: one 128-byte swizzle row
+constexpr int STAGES = 3;
+constexpr int THREADS = 192;
+constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB (A and B tiles alike: BM == BN)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A hi, A lo, B hi, B lo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t mbar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void umma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// shared-memory matrix descriptors (sm_100 UMMA, 128-byte swizzle, version 1)
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+// K-major: rows of 128 B (32 tf32 along K), 8-row atoms 1024 B apart; one
+// MMA (K = 8) advances 32 B inside the swizzled row.
+// MN-major: 128 B along M/N (32 elements) x 8 K-rows per 1024 B atom; atoms
+// along K 1024 B apart (SBO), 32-element M/N chunks 4096 B apart (LBO); one
+// MMA (K = 8) advances one atom.
+template <int MAJ>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t tile, int kk) {
+  if (MAJ == 0) return desc_sw128(tile + kk * 32, 16, 1024);
+  return desc_sw128(tile + kk * 1024, 4096, 1024);
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// A: MAJ 0 = K-major (M x K row-major), 1 = MN-major (K x M row-major)
+// B: MAJ 0 = K-major (N x K row-major), 1 = MN-major (K x N row-major)
+template <int AMAJ, int BMAJ, int SPLIT3, class Epi>
+__global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                             const __grid_constant__ CUtensorMap tmB, int M,
+                                                             int N, int K, int kb_per_split, Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // bars: full[S] split[S] empty[S] tmem_full ; then the TMEM address slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nkb_total = (K + BK - 1) / BK;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int kb1 = min(nkb_total, kb0 + kb_per_split);
+  const int nkb = max(0, kb1 - kb0);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8 * s; };
+  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES + s); };
+  const uint32_t tmem_full = bar0 + 8 * (3 * STAGES);
+  auto tile = [&](int s, int which) { return sbase + s * STAGE_BYTES + which * TILE_BYTES; };  // 0 Ahi 1 Alo 2 Bhi 3 Blo
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(split_bar(s), SPLIT3 ? 4 : 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(empty_bar(s), ph ^ 1);
+        mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+        const int k0 = (kb0 + i) * BK;
+        if (AMAJ == 0) {
+          tma_load_2d(tile(s, 0), &tmA, full_bar(s), k0, m0);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_2d(tile(s, 0) + c * 4096, &tmA, full_bar(s), m0 + 32 * c, k0);
+        }
+        if (BMAJ == 0) {
+          tma_load_2d(tile(s, 2), &tmB, full_bar(s), k0, n0);
+        } else {
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &tmB, full_bar(s), n0 + 32 * c, k0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one thread)
+    const uint32_t idesc = (1u << 4)                         // D format F32
+                           | (2u << 7) | (2u << 10)          // A, B format TF32
+                           | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16)
+                           | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        if (SPLIT3) mbar_wait(split_bar(s), ph);
+        else mbar_wait(full_bar(s), ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
+          const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32(tmem, ah, bh, idesc, acc);
+          if (SPLIT3) {
+            const uint64_t al = operand_desc<AMAJ>(tile(s, 1), kk);
+            const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
+            mma_tf32(tmem, al, bh, idesc, 1u);
+            mma_tf32(tmem, ah, bl, idesc, 1u);
+          }
+        }
+        umma_commit(empty_bar(s));
+      }
+      umma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- split (main loop) + epilogue, warps 2..5
+    const int et = threadIdx.x - 64;  // 0..127
+    if (SPLIT3) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(full_bar(s), ph);
+        uint8_t* st = smem + s * STAGE_BYTES;
+        float4* ahi = reinterpret_cast<float4*>(st);
+        float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
+        float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
+        float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+#pragma unroll 4
+        for (int q = et; q < TILE_BYTES / 16; q += 128) {
+          float4 x = ahi[q], h, l;
+          h.x = rna_tf32(x.x); l.x = x.x - h.x;
+          h.y = rna_tf32(x.y); l.y = x.y - h.y;
+          h.z = rna_tf32(x.z); l.z = x.z - h.z;
+          h.w = rna_tf32(x.w); l.w = x.w - h.w;
+          ahi[q] = h;
+          alo[q] = l;
+          x = bhi[q];
+          h.x = rna_tf32(x.x); l.x = x.x - h.x;
+          h.y = rna_tf32(x.y); l.y = x.y - h.y;
+          h.z = rna_tf32(x.z); l.z = x.z - h.z;
+          h.w = rna_tf32(x.w); l.w = x.w - h.w;
+          bhi[q] = h;
+          blo[q] = l;
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(split_bar(s));
+      }
+    }
+    // epilogue
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int lane_base = 32 * (warp & 3);
+    const int m = m0 + lane_base + lane;
+#pragma unroll 1
+    for (int cc = 0; cc < BN / 32; ++cc) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(cc * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (m < M) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + cc * 32 + j;
+          if (n < N) epi(m, n, nkb > 0 ? __uint_as_float(r[j]) : 0.f, blockIdx.z);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+  }
+}
+
+// ------------------------------------------------------------- host side
+inline PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+inline std::once_flag g_encode_once;
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) throw Error(VER_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  return g_encode;
+}
+
+// 2D fp32 row-major tensor (rows x cols, row stride ld elements), box {32, box_rows}
+inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(VER_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+inline bool usable(int M, int N, int K, const float* A, int lda, const float* B, int ldb) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return M >= 64 && N >= 32 && K >= 32 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) && al16(B);
+}
+
+template <int AMAJ, int BMAJ, class Epi>
+void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits) {
+  // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32)
+  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM) : make_map(A, K, M, lda, 32);
+  const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, BN) : make_map(B, K, N, ldb, 32);
+  const int nkb = (K + BK - 1) / BK;
+  splits = std::max(1, std::min(splits, nkb));
+  const int per = (nkb + splits - 1) / splits;
+  splits = (nkb + per - 1) / per;
+  dim3 grid(cdiv(N, BN), cdiv(M, BM), splits);
+  auto run = [&](auto kern) {
+    VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, epi);
+    after_launch(c);
+  };
+  if (c->precision == 0) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
+  else run(tc_gemm_kernel<AMAJ, BMAJ, 0, Epi>);
+}
+
+inline int splits_for(const Ctx* c, int M, int N, int K) {
+  const int tiles = (int)(cdiv(N, BN) * cdiv(M, BM));
+  const int nkb = (K + BK - 1) / BK;
+  int z = (2 * c->num_sms + tiles - 1) / tiles;
+  z = std::min(z, std::max(1, nkb / 4));  // keep >= 4 K-blocks per split
+  return std::max(1, std::min(z, 64));
+}
+
+}  // namespace tc
+}  // namespace verg

@@ -296,6 +296,12 @@ ver_status ver_ctx_set_precision(ver_ctx ctx, int mode) {
   VER_API_END
 }
 
+ver_status ver_ctx_set_tensor_cores(ver_ctx ctx, int enable) {
+  VER_API_BEGIN
+  ctx->c.tensor_cores = enable != 0;
+  VER_API_END
+}
+
 ver_status ver_nccl_unique_id(uint8_t id_out[128]) {
   VER_API_BEGIN
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");

@@ -1,0 +1,28 @@
+"""tcgen05 GEMM (TMA + TMEM, 3xTF32 / 1xTF32) vs float64 numpy, all operand
+majors and split-K; the SIMT fp32 GEMM as a second reference."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(128, 128, 32), (256, 384, 512), (16384, 512, 512), (300, 200, 100), (512, 1536, 4096)]
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_tc_gemm_3xtf32(ta, tb, M, N, K):
+    import paper_2210_05064_b200 as V
+    rng = np.random.default_rng(M * 7 + N * 3 + K)
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    ref = (A.astype(np.float64).T if ta else A.astype(np.float64)) @ (B.astype(np.float64).T if tb else B)
+    scale = np.sqrt(K)
+    for split in (1, 4):
+        C3 = V.debug_gemm(A, B, ta, tb, engine=1, splitk=split)
+        err3 = np.abs(C3 - ref).max() / scale
+        assert err3 < 2e-6, (split, err3)
+    C1 = V.debug_gemm(A, B, ta, tb, engine=2)
+    err1 = np.abs(C1 - ref).max() / scale
+    assert err1 < 2e-3, err1
+    C0 = V.debug_gemm(A, B, ta, tb, engine=0)
+    assert np.abs(C0 - ref).max() / scale < 2e-6
