@@ -79,24 +79,25 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
 }
 
 // shared-memory matrix descriptors (sm_100 UMMA, 128-byte swizzle, version 1)
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // version (sm_100)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)1 << 46;       // version (sm_100)
+  d |= (uint64_t)layout << 61;  // 2 = SWIZZLE_128B, 1 = SWIZZLE_128B_BASE32B
   return d;
 }
-// K-major: rows of 128 B (32 tf32 along K), 8-row atoms 1024 B apart; one
-// MMA (K = 8) advances 32 B inside the swizzled row.
-// MN-major: 128 B along M/N (32 elements) x 8 K-rows per 1024 B atom; atoms
-// along K 1024 B apart (SBO), 32-element M/N chunks 4096 B apart (LBO); one
-// MMA (K = 8) advances one atom.
+// K-major (SWIZZLE_128B): rows of 128 B (32 tf32 along K), 8-row atoms
+// 1024 B apart (SBO); one MMA (K = 8) advances 32 B inside the swizzled row.
+// MN-major: 32-bit elements need the 32-byte-atom 128B swizzle
+// (SWIZZLE_128B_BASE32B, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 128 B
+// along M/N per K-row, 4-row atoms 512 B apart along K (SBO), 32-element
+// M/N chunks 4096 B apart (LBO); one MMA (K = 8) advances 8 K-rows = 1024 B.
 template <int MAJ>
 __device__ __forceinline__ uint64_t operand_desc(uint32_t tile, int kk) {
-  if (MAJ == 0) return desc_sw128(tile + kk * 32, 16, 1024);
-  return desc_sw128(tile + kk * 1024, 4096, 1024);
+  if (MAJ == 0) return desc_sw128(tile + kk * 32, 16, 1024, 2);
+  return desc_sw128(tile + kk * 1024, 4096, 512, 1);
 }
 
 __device__ __forceinline__ float rna_tf32(float x) {
@@ -295,14 +296,15 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }
 
 // 2D fp32 row-major tensor (rows x cols, row stride ld elements), box {32, box_rows}
-inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int box_rows) {
+inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int box_rows, bool mn_major) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
   const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(VER_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
@@ -316,8 +318,8 @@ inline bool usable(int M, int N, int K, const float* A, int lda, const float* B,
 template <int AMAJ, int BMAJ, class Epi>
 void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits) {
   // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32)
-  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM) : make_map(A, K, M, lda, 32);
-  const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, BN) : make_map(B, K, N, ldb, 32);
+  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
+  const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, BN, false) : make_map(B, K, N, ldb, 32, true);
   const int nkb = (K + BK - 1) / BK;
   splits = std::max(1, std::min(splits, nkb));
   const int per = (nkb + splits - 1) / splits;
