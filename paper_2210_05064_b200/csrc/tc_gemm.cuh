@@ -33,6 +33,11 @@ constexpr int THREADS = 192;
 constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB (A and B tiles alike: BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A hi, A lo, B hi, B lo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+// The tensor core's fp32 accumulation truncates; so that 3xTF32 stays
+// fp32-grade for long K, each group of PROMOTE K-blocks accumulates into one
+// of two TMEM buffers which the epilogue warps drain into fp32 registers
+// (round-to-nearest adds) while the MMA fills the other buffer.
+constexpr int PROMOTE = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -115,8 +120,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  // bars: full[S] split[S] empty[S] tmem_full ; then the TMEM address slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
+  // bars: full[S] split[S] empty[S] acc_full[2] acc_empty[2]; then the TMEM address slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nkb_total = (K + BK - 1) / BK;
@@ -128,7 +133,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
   auto split_bar = [&](int s) { return bar0 + 8 * (STAGES + s); };
   auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES + s); };
-  const uint32_t tmem_full = bar0 + 8 * (3 * STAGES);
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES + 2 + b); };
+  const int ngroups = (nkb + PROMOTE - 1) / PROMOTE;
   auto tile = [&](int s, int which) { return sbase + s * STAGE_BYTES + which * TILE_BYTES; };  // 0 Ahi 1 Alo 2 Bhi 3 Blo
 
   if (threadIdx.x == 0) {
@@ -137,14 +144,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       mbar_init(split_bar(s), SPLIT3 ? 4 : 1);
       mbar_init(empty_bar(s), 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full(b), 1);
+      mbar_init(acc_empty(b), 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN)
+                 "r"(2 * BN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -186,32 +196,68 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       for (int i = 0; i < nkb; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
+        const int g = i / PROMOTE, buf = g & 1;
+        const bool first = (i % PROMOTE) == 0;
+        if (first && g >= 2) mbar_wait(acc_empty(buf), ((g >> 1) - 1) & 1);
         if (SPLIT3) mbar_wait(split_bar(s), ph);
         else mbar_wait(full_bar(s), ph);
         tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(buf * BN);
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
           const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
           const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem, ah, bh, idesc, acc);
+          const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+          mma_tf32(d, ah, bh, idesc, acc);
           if (SPLIT3) {
             const uint64_t al = operand_desc<AMAJ>(tile(s, 1), kk);
             const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
-            mma_tf32(tmem, al, bh, idesc, 1u);
-            mma_tf32(tmem, ah, bl, idesc, 1u);
+            mma_tf32(d, al, bh, idesc, 1u);
+            mma_tf32(d, ah, bl, idesc, 1u);
           }
         }
         umma_commit(empty_bar(s));
+        if ((i % PROMOTE) == PROMOTE - 1 || i == nkb - 1) umma_commit(acc_full(buf));
       }
-      umma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    // ---------------- split (main loop) + epilogue, warps 2..5
+    // ---------------- split (main loop) + promotion + epilogue, warps 2..5
     const int et = threadIdx.x - 64;  // 0..127
-    if (SPLIT3) {
-      for (int i = 0; i < nkb; ++i) {
+    const int lane_base = 32 * (warp & 3);
+    float sums[BN];
+#pragma unroll
+    for (int j = 0; j < BN; ++j) sums[j] = 0.f;
+    auto drain = [&](int g) {
+      const int buf = g & 1;
+      mbar_wait(acc_full(buf), (g >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN + cc * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+              "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+              "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+              "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty(buf));
+    };
+    int drained = 0;
+    for (int i = 0; i < nkb; ++i) {
+      // free the accumulator buffer the MMA needs next before splitting its stage
+      if (i % PROMOTE == 0 && i / PROMOTE >= 2) drain(drained++);
+      if (SPLIT3) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(full_bar(s), ph);
@@ -243,31 +289,14 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         if (lane == 0) mbar_arrive(split_bar(s));
       }
     }
+    while (drained < ngroups) drain(drained++);
     // epilogue
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    const int lane_base = 32 * (warp & 3);
     const int m = m0 + lane_base + lane;
-#pragma unroll 1
-    for (int cc = 0; cc < BN / 32; ++cc) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(cc * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (m < M) {
+    if (m < M) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + cc * 32 + j;
-          if (n < N) epi(m, n, nkb > 0 ? __uint_as_float(r[j]) : 0.f, blockIdx.z);
-        }
+      for (int j = 0; j < BN; ++j) {
+        const int n = n0 + j;
+        if (n < N) epi(m, n, sums[j], blockIdx.z);
       }
     }
   }
@@ -275,7 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN) : "memory");
   }
 }
 
