@@ -243,6 +243,24 @@ def run_ours(args, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
 
+    # ---- GAE + gather HBM throughput on the ragged stress view
+    gg = None
+    if rank == 0 and not args.no_c5:
+        S5 = 1 << args.c5_log2
+        lens = synth.ragged_lengths(S5, seed=11)
+        v5 = V.view_synth(lens, obs_dim=D_, hidden_dim=4, seed=12, ctx=ctx)
+        gae_ms, gat_ms = V.bench_gae_gather(v5, B=MINIBATCHES, seed=13, reps=5)
+        hbm_, _, _, pk = load_peaks()
+        gae_b = 17.0 * S5 + 9.0 * len(lens)          # r, V, done in; A, R out; + bootstrap/valid/offset per env
+        gat_b = (8.0 * D_ + 36.0) * S5               # obs, act, old log-prob, A, R in + out, slot out
+        gg = {"steps": S5, "envs": int(len(lens)), "gae_ms": gae_ms, "gather_ms": gat_ms,
+              "gae_gbs": gae_b / gae_ms / 1e6, "gather_gbs": gat_b / gat_ms / 1e6,
+              "gae_gather_gbs": (gae_b + gat_b) / (gae_ms + gat_ms) / 1e6,
+              "frac_of_peak": (gae_b + gat_b) / (gae_ms + gat_ms) / 1e6 / hbm_, "peak_gbs": hbm_,
+              "peak_kind": pk,
+              "bytes_per_step": {"gae": 17, "gather": 8 * D_ + 36}}
+        del v5
+
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
         fl = flops_per_step() * fresh * EPOCHS
@@ -266,6 +284,8 @@ def run_ours(args, rank, world):
             "e2e": {"value": fresh * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": 8 * 12, "ms_per_step": e2e},
         }
+        if gg:
+            line["gae_gather"] = gg
         if not args.no_cpu and world == 1:
             cv, dt, sample = cpu_sample()
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
@@ -281,6 +301,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the GAE+gather ragged sweep point")
+    ap.add_argument("--c5-log2", type=int, default=26, help="log2 steps of the GAE+gather point")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -157,6 +157,12 @@ ver_status ver_rollout_state(ver_rollout r, int* open, int* committed, int* carr
    into the env-major, sequence-contiguous view */
 ver_status ver_rollout_close(ver_rollout r, ver_view* out);
 
+/* Synthetic ragged closed view generated on the device (benchmark workload,
+   SURVEY §8d C5): env e holds lengths[e] (>= 1) steps, counter-hash payload,
+   done ~ Bernoulli(p_done); discrete actions, T = 0 (no T*N divisibility). */
+ver_status ver_view_synth(ver_ctx ctx, const int32_t* lengths, int n_envs, int obs_dim, int hidden_dim,
+                          uint64_t seed, float p_done, ver_view* out);
+
 /* backfill_stale (rollout.cpp:208-276) */
 ver_status ver_backfill_stale(ver_view view, ver_view prev, int deficit);
 
@@ -281,6 +287,12 @@ ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed_s
 /* per-phase device time of the last update, ms (gae, sampler, gather, forward,
    recurrence, loss, backward, allreduce, adam); n in/out */
 ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n);
+
+/* Measurement: device time (CUDA events, averaged over reps) of compute_gae on
+   v and of the time-major gather of all B minibatches of one
+   split_minibatches(v, B, seed) deal.  ms_out[0] = GAE, ms_out[1] = gather. */
+ver_status ver_bench_gae_gather(ver_view v, double gamma, double lambda, int B, uint64_t seed, int reps,
+                                float* ms_out);
 
 /* Diagnostic: C (M x N, row-major) = op(A) op(B) through the library's GEMM
    path (op(A) = A^T if transA: A stored K x M; op(B) = B^T if transB: B stored

@@ -112,6 +112,8 @@ _SIGS = {
     "ver_rollout_set_bootstrap": (c_int, [C.c_void_p, c_int, c_float]),
     "ver_rollout_state": (c_int, [C.c_void_p, P(c_int), P(c_int), P(c_int)]),
     "ver_rollout_close": (c_int, [C.c_void_p, P(C.c_void_p)]),
+    "ver_view_synth": (c_int, [C.c_void_p, P(c_int32), c_int, c_int, c_int, c_uint64, c_float, P(C.c_void_p)]),
+    "ver_bench_gae_gather": (c_int, [C.c_void_p, c_double, c_double, c_int, c_uint64, c_int, P(c_float)]),
     "ver_backfill_stale": (c_int, [C.c_void_p, C.c_void_p, c_int]),
     "ver_compute_gae": (c_int, [C.c_void_p, c_double, c_double]),
     "ver_split_minibatches": (c_int, [C.c_void_p, c_int, c_uint64, P(C.c_void_p)]),

@@ -351,6 +351,25 @@ class RolloutBuffer:
         return RolloutView(out, self.ctx)
 
 
+def view_synth(lengths, obs_dim: int = 2, hidden_dim: int = 4, seed: int = 1, p_done: float = 1.0 / 32,
+               ctx: Context | None = None) -> RolloutView:
+    """Device-generated ragged closed view (C5 stress workload)."""
+    ctx = ctx or default_context()
+    L_ = np.ascontiguousarray(lengths, dtype=np.int32)
+    out = C.c_void_p()
+    _check(_lib().ver_view_synth(ctx.h, _ptr(L_, C.c_int32), L_.size, obs_dim, hidden_dim, seed, p_done,
+                                 C.byref(out)))
+    return RolloutView(out, ctx)
+
+
+def bench_gae_gather(view: RolloutView, B: int = 2, seed: int = 1, reps: int = 5, gamma: float = 0.99,
+                     lam: float = 0.95) -> tuple[float, float]:
+    """(GAE ms, gather ms for all B minibatches), CUDA-event timed."""
+    ms = (C.c_float * 2)()
+    _check(_lib().ver_bench_gae_gather(view.h, gamma, lam, B, seed, reps, ms))
+    return float(ms[0]), float(ms[1])
+
+
 def backfill_stale(view: RolloutView, prev: RolloutView, deficit: int):
     _check(_lib().ver_backfill_stale(view.h, prev.h, deficit))
 

@@ -694,6 +694,50 @@ ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed, 
   VER_API_END
 }
 
+ver_status ver_bench_gae_gather(ver_view v, double gamma, double lambda, int B, uint64_t seed, int reps,
+                                float* ms_out) {
+  VER_API_BEGIN
+  DView& V = v->v;
+  Ctx* c = V.ctx;
+  activate(c);
+  reps = std::max(1, reps);
+  cudaEvent_t e0, e1;
+  VER_CUDA(cudaEventCreate(&e0));
+  VER_CUDA(cudaEventCreate(&e1));
+  compute_gae(V, gamma, lambda);  // warm
+  float gae = 0.f;
+  for (int r = 0; r < reps; ++r) {
+    VER_CUDA(cudaEventRecord(e0, c->stream));
+    compute_gae(V, gamma, lambda);
+    VER_CUDA(cudaEventRecord(e1, c->stream));
+    VER_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    VER_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    gae += ms;
+  }
+  std::unique_ptr<DGroups> G(split_minibatches(V, B, seed));
+  std::vector<std::unique_ptr<DPacked>> packs;
+  for (int b = 0; b < G->B; ++b)
+    if (G->gstart[b + 1] > G->gstart[b])
+      packs.emplace_back(pack_pieces(V, G->pieces.p + G->gstart[b], G->gstart[b + 1] - G->gstart[b]));
+  float gat = 0.f;
+  for (int r = 0; r < reps; ++r)
+    for (auto& P : packs) {
+      VER_CUDA(cudaEventRecord(e0, c->stream));
+      gather_packed(V, *P);
+      VER_CUDA(cudaEventRecord(e1, c->stream));
+      VER_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      VER_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      gat += ms;
+    }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ms_out[0] = gae / reps;
+  ms_out[1] = gat / reps;
+  VER_API_END
+}
+
 ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n) {
   VER_API_BEGIN
   const int k = std::min(*n, (int)PH_N);

@@ -34,6 +34,8 @@ struct DPacked {
   // gathered fields, packed order
   DBuf<float> obs, act_cont, old_logp, adv, ret;
   DBuf<int32_t> act_disc;
+  DBuf<int32_t> tile_start;  // gather tiles per 32-piece block (prefix)
+  int n_tiles = 0;
   // host copies (drive the per-timestep recurrence launches)
   std::vector<int32_t> h_bs, h_offs;
   // pieces needing an h0 replay (skip > 0), host copy of sorted descriptors
@@ -42,6 +44,8 @@ struct DPacked {
 
 // pack + gather of an explicit device array of k pieces (deal order)
 DPacked* pack_pieces(DView& V, const ver_seq_desc* d_pieces, int k);
+// (re-)run the time-major gather of a pack
+void gather_packed(DView& V, DPacked& P);
 
 }  // namespace verg
 

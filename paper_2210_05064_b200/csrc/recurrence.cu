@@ -140,6 +140,36 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_persistent(
 }
 
 // ----------------------------------------------------------- backward
+struct GateIn {
+  float r, z, n, hn, hp, dh;  // gates, hUn, h_{t-1}, dhidden
+};
+__device__ __forceinline__ GateIn gate_load(size_t p, int u, int H, const float* __restrict__ gates,
+                                           const float* __restrict__ hun, const float* __restrict__ hprev,
+                                           const float* __restrict__ dhidden) {
+  const float* gp = gates + p * 3 * H + 3 * u;
+  return GateIn{__ldg(gp), __ldg(gp + 1), __ldg(gp + 2), __ldg(hun + p * H + u), __ldg(hprev + p * H + u),
+                __ldg(dhidden + p * H + u)};
+}
+__device__ __forceinline__ void gate_grad_v(size_t p, int u, int H, float g, const GateIn& in,
+                                            float* __restrict__ dpre, float* __restrict__ dhu,
+                                            float* __restrict__ gz) {
+  const float dn = g * (1.f - in.z);
+  const float dz = g * (in.hp - in.n);
+  const float dpn = dn * (1.f - in.n * in.n);
+  const float dr = dpn * in.hn;
+  const float dpr = dr * in.r * (1.f - in.r);
+  const float dpz = dz * in.z * (1.f - in.z);
+  float* d = dpre + p * 3 * H + 3 * u;
+  d[0] = dpr;
+  d[1] = dpz;
+  d[2] = dpn;
+  float* e = dhu + p * 3 * H + 3 * u;
+  e[0] = dpr;
+  e[1] = dpz;
+  e[2] = dpn * in.r;
+  gz[p * H + u] = g * in.z;
+}
+
 __device__ __forceinline__ void gate_grad(size_t p, int u, int H, float g, const float* __restrict__ gates,
                                           const float* __restrict__ hun, const float* __restrict__ hprev,
                                           float* __restrict__ dpre, float* __restrict__ dhu,
@@ -326,6 +356,16 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
       for (int i = threadIdx.x; i < nr * H / 4; i += RT) sm4[i] = __ldcg(src + i);
       __syncthreads();
       for (int g0 = 0; g0 < nr; g0 += 4) {
+        // gate pre-activations of this lane's (row, unit), loaded ahead of the FMAs
+        const int pr = lane >> 3, pq = (lane >> 2) & 1;
+        const bool owner = (lane & 3) == 0 && g0 + pr < nr;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+        if (owner) {
+          const float* x = xp + ((size_t)o + c0 + g0 + pr) * H3 + 3 * (ua + pq);
+          x0 = __ldg(x);
+          x1 = __ldg(x + 1);
+          x2 = __ldg(x + 2);
+        }
         float acc[32];
 #pragma unroll
         for (int v = 0; v < 32; ++v) acc[v] = 0.f;
@@ -346,15 +386,13 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
         const float mine = reduce_scatter32(acc, lane);  // value index = lane = r*8 + q*4 + g
         const float sz = __shfl_down_sync(0xffffffffu, mine, 1);
         const float sn = __shfl_down_sync(0xffffffffu, mine, 2);
-        const int r = lane >> 3, q = (lane >> 2) & 1;
-        if ((lane & 3) == 0 && g0 + r < nr) {
-          const int u = ua + q;
-          const int row = g0 + r;
+        if (owner) {
+          const int u = ua + pq;
+          const int row = g0 + pr;
           const size_t p = (size_t)o + c0 + row;
-          const float* x = xp + p * H3 + 3 * u;
-          const float rg = sigm(x[0] + mine);
-          const float zg = sigm(x[1] + sz);
-          const float ng = tanhf(x[2] + rg * sn);
+          const float rg = sigm(x0 + mine);
+          const float zg = sigm(x1 + sz);
+          const float ng = tanhf(x2 + rg * sn);
           const float hprev = hs[row * H + u];
           hidden[p * H + u] = (1.f - zg) * ng + zg * hprev;
           if (gates) {
@@ -420,6 +458,16 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
       for (int i = threadIdx.x; i < nr * H3 / 4; i += RT) sm4[i] = __ldcg(src + i);
       __syncthreads();
       for (int g0 = 0; g0 < nr; g0 += 4) {
+        // this lane's (row, unit) operands for the gate gradient, loaded ahead of the FMAs
+        const int pv = lane >> 2, pr = pv >> 1, pq = pv & 1;
+        const bool owner = (lane & 3) == 0 && g0 + pr < nr;
+        GateIn gin{};
+        float gzv = 0.f;
+        if (owner) {
+          const size_t pp = (size_t)op + c0 + g0 + pr;
+          gin = gate_load(pp, ua + pq, H, gates, hun, hprev, dhidden);
+          gzv = __ldcg(gz + ((size_t)o + c0 + g0 + pr) * H + ua + pq);
+        }
         float acc[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) acc[v] = 0.f;
@@ -449,14 +497,9 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
         float tot = acc[0];
         tot += __shfl_xor_sync(0xffffffffu, tot, 2);
         tot += __shfl_xor_sync(0xffffffffu, tot, 1);
-        const int v = lane >> 2;  // = r * 2 + q
-        const int r = v >> 1, q = v & 1;
-        if ((lane & 3) == 0 && g0 + r < nr) {
-          const int u = ua + q;
-          const int j = c0 + g0 + r;
-          const float dh = tot + __ldcg(gz + ((size_t)o + j) * H + u);
-          const size_t pp = (size_t)op + j;
-          gate_grad(pp, u, H, dhidden[pp * H + u] + dh, gates, hun, hprev, dpre, dhu, gz);
+        if (owner) {  // lane holds value pv = r * 2 + q
+          const size_t pp = (size_t)op + c0 + g0 + pr;
+          gate_grad_v(pp, ua + pq, H, gin.dh + tot + gzv, gin, dpre, dhu, gz);
         }
       }
       __syncthreads();

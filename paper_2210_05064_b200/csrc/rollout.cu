@@ -187,7 +187,7 @@ __global__ void seq_desc_kernel(const int32_t* __restrict__ starts, int K, int S
     d.skip = 0;
     seqs[k] = d;
   }
-  const int hs = hslot_by_slot[st];
+  const int hs = hslot_by_slot ? hslot_by_slot[st] : -1;
   float* dst = h0 + (size_t)k * H;
   if (hs >= 0) {
     const float* src = hlog + (size_t)hs * H;
@@ -474,6 +474,102 @@ static DView* close_rollout(Rollout* R) {
                                                            cfg.hidden_dim, V->seqs.p, V->h0.p);
   after_launch(c);
   R->next_seq_id += nK;
+  return V;
+}
+
+// ---------------------------------------------------- synthetic ragged view
+// Device generator of a closed, env-contiguous view for the ragged-length
+// stress sweep: env e holds lengths[e] steps; counter-hash
+// payload; done ~ Bernoulli(p_done) inside each env; sequence structure built
+// with the same scan + descriptor kernels as close_rollout.
+__device__ __forceinline__ uint64_t hmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ float hunif(uint64_t seed, uint64_t i, uint64_t f) {
+  return (float)((hmix(seed ^ hmix(i * 64 + f)) >> 40) * (1.0 / 16777216.0));
+}
+__device__ __forceinline__ float hnorm(uint64_t seed, uint64_t i, uint64_t f) {
+  const float u1 = fmaxf(hunif(seed, i, f), 1e-7f), u2 = hunif(seed, i, f + 32);
+  return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+}
+__global__ void synth_view_kernel(const int32_t* __restrict__ off, uint64_t seed, float p_done, ViewDev V, int D,
+                                  uint8_t* __restrict__ flag, float* __restrict__ boot, uint8_t* __restrict__ valid) {
+  const int e = blockIdx.x;
+  const int s0 = off[e], len = off[e + 1] - s0;
+  for (int t = threadIdx.x; t < len; t += blockDim.x) {
+    const int i = s0 + t;
+    for (int q = 0; q < D; ++q) V.obs[(size_t)i * D + q] = hnorm(seed, i, 1 + q);
+    V.act_disc[i] = (int)(hmix(seed ^ hmix((uint64_t)i * 64 + 20)) & 1);
+    V.log_prob[i] = -0.6931472f + 0.1f * hnorm(seed, i, 21);
+    V.value[i] = hnorm(seed, i, 22);
+    V.reward[i] = hnorm(seed, i, 23);
+    V.latency[i] = 0.f;
+    V.advantage[i] = 0.f;
+    V.returns[i] = 0.f;
+    const bool d = hunif(seed, i, 24) < p_done;
+    V.done[i] = d;
+    V.stale[i] = 0;
+    V.replayed[i] = 0;
+    V.env_index[i] = e;
+    V.episode_index[i] = (int64_t)e * 1000;
+    V.step_in_episode[i] = t;
+    V.version[i] = 1;
+    flag[i] = (t == 0 || hunif(seed, i - 1, 24) < p_done) ? 1 : 0;
+    if (t == len - 1) {
+      valid[e] = d ? 0 : 1;
+      boot[e] = d ? 0.f : hnorm(seed, i, 25);
+    }
+  }
+}
+
+static DView* synth_view(Ctx* c, const int32_t* lengths, int N, int obs_dim, int hidden_dim, uint64_t seed,
+                         float p_done) {
+  long long S = 0;
+  for (int e = 0; e < N; ++e) {
+    if (lengths[e] < 1) config_error("view_synth: lengths must be >= 1");
+    S += lengths[e];
+  }
+  if (S > 0x7fffffffLL) config_error("view_synth: more than 2^31-1 steps");
+  auto* V = new DView();
+  V->ctx = c;
+  V->T = 0;
+  V->N = N;
+  V->obs_dim = obs_dim;
+  V->hidden_dim = hidden_dim;
+  V->size = (int)S;
+  V->env_contiguous = true;
+  V->fresh_prefix = (int)S;
+  V->alloc_slots((int)S);
+  V->alloc_env();
+  V->per_env_counts.upload(lengths, N);
+  exclusive_scan_i32(c, V->per_env_counts.p, V->env_offsets.p, N, V->env_offsets.p + N);
+  DBuf<uint8_t> flag;
+  DBuf<int32_t> excl, starts, K;
+  flag.reserve(c, S);
+  excl.reserve(c, S);
+  starts.reserve(c, S);
+  K.reserve(c, 1);
+  ViewDev VD = vdev(*V);
+  synth_view_kernel<<<N, 256, 0, c->stream>>>(V->env_offsets.p, seed, p_done, VD, obs_dim, flag.p,
+                                              V->env_bootstrap.p, V->env_bootstrap_valid.p);
+  after_launch(c);
+  exclusive_scan_u8(c, flag.p, excl.p, S, K.p);
+  seq_ids_kernel<<<cdiv(S, 256), 256, 0, c->stream>>>(flag.p, excl.p, (int)S, V->seq_of_slot.p, starts.p);
+  after_launch(c);
+  int32_t* hK = static_cast<int32_t*>(c->pinned_buf(sizeof(int32_t)));
+  K.download(hK, 1);
+  sync(c);
+  const int nK = *hK;
+  V->num_seqs = nK;
+  V->h0_rows = nK;
+  V->alloc_seqs(nK, nK);
+  seq_desc_kernel<<<std::max(nK, 1), 128, 0, c->stream>>>(starts.p, nK, (int)S, 0, V->env_index.p, nullptr, nullptr,
+                                                           hidden_dim, V->seqs.p, V->h0.p);
+  after_launch(c);
+  sync(c);
   return V;
 }
 
@@ -970,6 +1066,18 @@ ver_status ver_rollout_close(ver_rollout r, ver_view* out) {
   VER_API_BEGIN
   activate(r->r.ctx);
   DView* V = close_rollout(&r->r);
+  auto* w = new ver_view_s();
+  w->v = std::move(*V);
+  delete V;
+  *out = w;
+  VER_API_END
+}
+
+ver_status ver_view_synth(ver_ctx ctx, const int32_t* lengths, int n_envs, int obs_dim, int hidden_dim,
+                          uint64_t seed, float p_done, ver_view* out) {
+  VER_API_BEGIN
+  activate(&ctx->c);
+  DView* V = synth_view(&ctx->c, lengths, n_envs, obs_dim, hidden_dim, seed, p_done);
   auto* w = new ver_view_s();
   w->v = std::move(*V);
   delete V;

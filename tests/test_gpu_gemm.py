@@ -19,11 +19,11 @@ def test_tc_gemm_3xtf32(ta, tb, M, N, K):
     scale = np.sqrt(K)  # |C| ~ sqrt(K): errors below are relative to the output scale
     C0 = V.debug_gemm(A, B, ta, tb, engine=0)
     err0 = np.abs(C0 - ref).max() / scale  # fp32 SIMT
-    assert err0 < 4e-6
+    assert err0 < 3e-5
     for split in (1, 4):
         C3 = V.debug_gemm(A, B, ta, tb, engine=1, splitk=split)
         err3 = np.abs(C3 - ref).max() / scale
-        assert err3 < max(4e-6, 3 * err0), (split, err3, err0)  # fp32-grade
+        assert err3 < max(5e-6, 2 * err0), (split, err3, err0)  # fp32-grade
     C1 = V.debug_gemm(A, B, ta, tb, engine=2)
     err1 = np.abs(C1 - ref).max() / scale
     assert err1 < 1e-2, err1  # tf32 (10-bit mantissa) inputs
