@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
     const uint8_t* __restrict__ done, int F, const int32_t* __restrict__ off, int N,
     const float* __restrict__ boot, const uint8_t* __restrict__ boot_valid, double gamma,
     double lambda, float* __restrict__ adv, float* __restrict__ ret,
-    volatile GaeTileState* tiles, int* tile_counter, int* err_env) {
+    volatile GaeTileState* tiles, int* tile_counter, int* err_env, const int32_t* __restrict__ tile_env) {
   __shared__ int s_tile;
   __shared__ int s_e0, s_ne;
   __shared__ int32_t s_off[kGaeOffSmem + 1];
@@ -75,12 +75,12 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
   const int lo = tile * kGaeTile;
   const int hi = min(F, lo + kGaeTile);
 
-  // env range of this tile; stage its offsets in smem
+  // env range of this tile (precomputed per tile); stage its offsets in smem
   if (threadIdx.x == 0) {
-    const int e0 = upper_bound_i32(off, N + 1, lo) - 1;
-    const int e1 = upper_bound_i32(off, N + 1, hi - 1) - 1;
+    const int e0 = tile_env[tile];
+    const int e1 = tile_env[tile + 1];  // env of slot hi (or N)
     s_e0 = e0;
-    s_ne = e1 - e0 + 2;  // offsets e0 .. e1+1
+    s_ne = min(e1, N - 1) - e0 + 2;  // offsets e0 .. e1+1
   }
   __syncthreads();
   const int e0 = s_e0, ne = s_ne;
@@ -237,6 +237,15 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
   }
 }
 
+// env containing the first slot of every tile (+ the env of slot F at [ntiles])
+__global__ void gae_tile_env_kernel(const int32_t* __restrict__ off, int N, int F, int ntiles,
+                                    int32_t* __restrict__ tile_env) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > ntiles) return;
+  const int slot = min(t * kGaeTile, F - 1);
+  tile_env[t] = (t == ntiles ? upper_bound_i32(off, N + 1, F - 1) : upper_bound_i32(off, N + 1, slot)) - 1;
+}
+
 // ----------------------------------------------------- general (any order)
 __global__ void gae_keys_kernel(const int32_t* __restrict__ env, const uint8_t* __restrict__ replayed,
                                 int S, int N, uint64_t* __restrict__ keys, int32_t* __restrict__ counts) {
@@ -274,16 +283,20 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, i
   const int ntiles = (F + kGaeTile - 1) / kGaeTile;
   DBuf<GaeTileState> tiles;
   DBuf<int> misc;
+  DBuf<int32_t> tile_env;
   tiles.reserve(c, ntiles);
   misc.reserve(c, 2);
+  tile_env.reserve(c, ntiles + 1);
   tiles.zero(ntiles);
+  gae_tile_env_kernel<<<cdiv(ntiles + 1, 256), 256, 0, c->stream>>>(off, N, F, ntiles, tile_env.p);
+  after_launch(c);
   const int init[2] = {0, 0x7fffffff};
   int* h = static_cast<int*>(c->pinned_buf(2 * sizeof(int)));
   h[0] = init[0];
   h[1] = init[1];
   misc.upload(h, 2);
   gae_scan_kernel<<<ntiles, kGaeThreads, 0, c->stream>>>(r, v, d, F, off, N, boot, valid, gamma, lambda,
-                                                         adv, ret, tiles.p, misc.p, misc.p + 1);
+                                                         adv, ret, tiles.p, misc.p, misc.p + 1, tile_env.p);
   after_launch(c);
   misc.download(h, 2);
   sync(c);

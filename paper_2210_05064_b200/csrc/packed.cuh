@@ -34,8 +34,8 @@ struct DPacked {
   // gathered fields, packed order
   DBuf<float> obs, act_cont, old_logp, adv, ret;
   DBuf<int32_t> act_disc;
-  DBuf<int32_t> tile_start;  // gather tiles per 32-piece block (prefix)
-  int n_tiles = 0;
+  DBuf<int2> tiles;            // gather tile table {piece block, t0|log2 TT}
+  std::vector<int2> tile_table;
   // host copies (drive the per-timestep recurrence launches)
   std::vector<int32_t> h_bs, h_offs;
   // pieces needing an h0 replay (skip > 0), host copy of sorted descriptors

@@ -201,9 +201,13 @@ __global__ void batch_sizes_kernel(const int32_t* __restrict__ lens, int k, int 
 // phase: each warp writes one timestep's 32 consecutive packed rows per field
 // (coalesced: rows offsets[t] + j, j = 0..bs_t-1).  HBM traffic = the
 // algorithmic bytes (8D+36 B/step + the 4-byte slot).
-constexpr int kGT = 32;  // tile edge
+constexpr int kGT = 32;  // pieces per tile
+// Tile table entry: {piece block jb, (t0 << 3) | log2(TT)}.  TT (timesteps
+// per tile, power of two <= 32) follows the block's longest piece, so blocks
+// of short pieces (the sorted tail of a heavy-tailed length distribution)
+// still fill the CTA: the read phase maps lanes to (piece, t) pairs.
 __global__ void __launch_bounds__(256) gather_tiled_kernel(
-    const int32_t* __restrict__ tile_start, int nblk, const ver_seq_desc* __restrict__ sorted, int k,
+    const int2* __restrict__ tiles, const ver_seq_desc* __restrict__ sorted, int k,
     const int32_t* __restrict__ offs, const int32_t* __restrict__ bs, int32_t* __restrict__ slots,
     const float* __restrict__ v_obs, const int32_t* __restrict__ v_act, const float* __restrict__ v_actc,
     const float* __restrict__ v_lp, const float* __restrict__ v_adv, const float* __restrict__ v_ret,
@@ -211,86 +215,77 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(
     float* __restrict__ adv, float* __restrict__ ret, int D, int A, int continuous) {
   extern __shared__ float tl[];  // F fields x 32 pieces x 33 (padded)
   __shared__ int s_start[kGT], s_len[kGT];
-  const int tile = blockIdx.x;
-  int lo = 0, hi = nblk;  // piece block containing this tile: largest jb with tile_start[jb] <= tile
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (tile_start[mid] <= tile) lo = mid;
-    else hi = mid;
-  }
-  const int jb = lo, tb = tile - tile_start[jb];
-  const int j0 = jb * kGT, t0 = tb * kGT;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int2 te = tiles[blockIdx.x];
+  const int jb = te.x, t0 = te.y >> 3, lg = te.y & 7, TT = 1 << lg;
+  const int j0 = jb * kGT;
   const int AC = continuous ? A : 0;
-  const int F = D + AC + 3 + (continuous ? 0 : 1);  // float-typed columns (+1 int column stored as bits)
   if (threadIdx.x < kGT) {
     const int j = j0 + threadIdx.x;
     s_start[threadIdx.x] = j < k ? sorted[j].start_offset : 0;
     s_len[threadIdx.x] = j < k ? sorted[j].length : 0;
   }
   __syncthreads();
-  auto cell = [&](int f, int jl, int tl_) -> float& { return tl[(f * kGT + jl) * (kGT + 1) + tl_]; };
-  // read: warp w -> pieces jl = w, w+8, w+16, w+24; lane -> t0 + lane
-  for (int jl = warp; jl < kGT; jl += 8) {
-    const int t = t0 + lane;
+  auto cell = [&](int f, int jl, int tt) -> float& { return tl[(f * kGT + jl) * (kGT + 1) + tt]; };
+  // read: lanes -> (piece jl, timestep tt), tt fastest: a piece's slots are contiguous
+  for (int r = threadIdx.x; r < kGT * TT; r += blockDim.x) {
+    const int jl = r >> lg, tt = r & (TT - 1);
+    const int t = t0 + tt;
     if (t < s_len[jl]) {
       const int sl = s_start[jl] + t;
       int f = 0;
-      for (int q = 0; q < D; ++q) cell(f++, jl, lane) = v_obs[(size_t)sl * D + q];
-      for (int q = 0; q < AC; ++q) cell(f++, jl, lane) = v_actc[(size_t)sl * A + q];
-      cell(f++, jl, lane) = v_lp[sl];
-      cell(f++, jl, lane) = v_adv[sl];
-      cell(f++, jl, lane) = v_ret[sl];
-      if (!continuous) cell(f++, jl, lane) = __int_as_float(v_act[sl]);
+      for (int q = 0; q < D; ++q) cell(f++, jl, tt) = v_obs[(size_t)sl * D + q];
+      for (int q = 0; q < AC; ++q) cell(f++, jl, tt) = v_actc[(size_t)sl * A + q];
+      cell(f++, jl, tt) = v_lp[sl];
+      cell(f++, jl, tt) = v_adv[sl];
+      cell(f++, jl, tt) = v_ret[sl];
+      if (!continuous) cell(f++, jl, tt) = __int_as_float(v_act[sl]);
     }
   }
   __syncthreads();
-  // write: warp w -> timesteps tl = w, w+8, ...; lane -> piece j0 + lane
-  for (int tl_ = warp; tl_ < kGT; tl_ += 8) {
-    const int t = t0 + tl_;
-    if (t >= s_len[0]) break;  // pieces sorted by length: the block's first is the longest
-    const int jl = lane;
+  // write: lanes -> (timestep tt, piece jl), jl fastest: rows offsets[t] + j are contiguous
+  for (int r = threadIdx.x; r < kGT * TT; r += blockDim.x) {
+    const int tt = r >> 5, jl = r & 31;
+    const int t = t0 + tt;
+    if (t >= s_len[0]) continue;  // the block's first piece is its longest
     if (j0 + jl < bs[t]) {
       const size_t p = (size_t)offs[t] + j0 + jl;
       slots[p] = s_start[jl] + t;
       int f = 0;
-      for (int q = 0; q < D; ++q) obs[p * D + q] = cell(f++, jl, tl_);
-      for (int q = 0; q < AC; ++q) actc[p * A + q] = cell(f++, jl, tl_);
-      lp[p] = cell(f++, jl, tl_);
-      adv[p] = cell(f++, jl, tl_);
-      ret[p] = cell(f++, jl, tl_);
-      if (!continuous) act[p] = __float_as_int(cell(f++, jl, tl_));
+      for (int q = 0; q < D; ++q) obs[p * D + q] = cell(f++, jl, tt);
+      for (int q = 0; q < AC; ++q) actc[p * A + q] = cell(f++, jl, tt);
+      lp[p] = cell(f++, jl, tt);
+      adv[p] = cell(f++, jl, tt);
+      ret[p] = cell(f++, jl, tt);
+      if (!continuous) act[p] = __float_as_int(cell(f++, jl, tt));
     }
   }
-  (void)F;
 }
 
 // launch of the tiled gather over an existing pack (P.seqs / lens / offs / bs set)
 void gather_packed(DView& V, DPacked& P) {
   Ctx* c = V.ctx;
-  const int nblk = (P.k + kGT - 1) / kGT;
-  std::vector<int32_t> ts(nblk + 1);
-  int tot = 0;
-  for (int b = 0; b < nblk; ++b) {
-    ts[b] = tot;
-    tot += (P.h_seqs[b * kGT].length + kGT - 1) / kGT;
+  if (P.tile_table.empty()) {
+    const int nblk = (P.k + kGT - 1) / kGT;
+    for (int b = 0; b < nblk; ++b) {
+      const int Lb = P.h_seqs[b * kGT].length;
+      int lg = 0;
+      while ((1 << lg) < Lb && lg < 5) ++lg;
+      const int TT = 1 << lg;
+      for (int t0 = 0; t0 < Lb; t0 += TT) P.tile_table.push_back(int2{b, (t0 << 3) | lg});
+    }
+    P.tiles.reserve(c, P.tile_table.size());
+    P.tiles.upload(P.tile_table.data(), P.tile_table.size());
+    sync(c);
   }
-  ts[nblk] = tot;
-  P.tile_start.reserve(c, nblk + 1);
-  int32_t* pin = static_cast<int32_t*>(c->pinned_buf(sizeof(int32_t) * (nblk + 1)));
-  std::copy(ts.begin(), ts.end(), pin);
-  P.tile_start.upload(pin, nblk + 1);
-  P.n_tiles = tot;
   const int F = V.obs_dim + (V.action_kind ? V.act_dim : 0) + 3 + (V.action_kind ? 0 : 1);
   const size_t smem = sizeof(float) * (size_t)F * kGT * (kGT + 1);
   if (smem > 48 * 1024)
     VER_CUDA(cudaFuncSetAttribute(gather_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  gather_tiled_kernel<<<tot, 256, smem, c->stream>>>(
-      P.tile_start.p, nblk, P.seqs.p, P.k, P.offs.p, P.bs.p, P.slots.p, V.obs.p, V.act_disc.p, V.act_cont.p,
-      V.log_prob.p, V.advantage.p, V.returns.p, P.obs.p, P.act_disc.p, P.act_cont.p, P.old_logp.p, P.adv.p,
-      P.ret.p, V.obs_dim, V.act_dim, V.action_kind);
+  gather_tiled_kernel<<<(unsigned)P.tile_table.size(), 256, smem, c->stream>>>(
+      P.tiles.p, P.seqs.p, P.k, P.offs.p, P.bs.p, P.slots.p, V.obs.p, V.act_disc.p, V.act_cont.p, V.log_prob.p,
+      V.advantage.p, V.returns.p, P.obs.p, P.act_disc.p, P.act_cont.p, P.old_logp.p, P.adv.p, P.ret.p, V.obs_dim,
+      V.act_dim, V.action_kind);
   after_launch(c);
-  sync(c);  // the pinned tile table is reused by the next pack
 }
 
 DPacked* pack_pieces(DView& V, const ver_seq_desc* d_pieces, int k) {
