@@ -74,8 +74,35 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
   const int tile = ntiles - 1 - tid;
   const int lo = tile * kGaeTile;
   const int hi = min(F, lo + kGaeTile);
+  const int i0 = lo + threadIdx.x * kGaeItems;
 
-  // env range of this tile (precomputed per tile); stage its offsets in smem
+  // 1) the tile's r, V, done: issued first so their latency overlaps the env setup
+  float r[kGaeItems], v[kGaeItems + 1];
+  uint8_t d[kGaeItems];
+  if (i0 + kGaeItems <= hi && (((uintptr_t)(reward + i0)) & 15) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(reward + i0);
+    const float4* v4 = reinterpret_cast<const float4*>(value + i0);
+    float4 x0 = __ldcs(r4), x1 = __ldcs(r4 + 1), y0 = __ldcs(v4), y1 = __ldcs(v4 + 1);
+    r[0] = x0.x; r[1] = x0.y; r[2] = x0.z; r[3] = x0.w;
+    r[4] = x1.x; r[5] = x1.y; r[6] = x1.z; r[7] = x1.w;
+    v[0] = y0.x; v[1] = y0.y; v[2] = y0.z; v[3] = y0.w;
+    v[4] = y1.x; v[5] = y1.y; v[6] = y1.z; v[7] = y1.w;
+    const uint2 dd = __ldcs(reinterpret_cast<const uint2*>(done + i0));
+    const uint8_t* db = reinterpret_cast<const uint8_t*>(&dd);
+#pragma unroll
+    for (int k = 0; k < kGaeItems; ++k) d[k] = db[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < kGaeItems; ++k) {
+      const int i = i0 + k;
+      r[k] = i < hi ? reward[i] : 0.f;
+      v[k] = i < hi ? value[i] : 0.f;
+      d[k] = i < hi ? done[i] : 1;
+    }
+  }
+  v[kGaeItems] = (i0 + kGaeItems < F) ? value[i0 + kGaeItems] : 0.f;
+
+  // 2) env range of this tile (precomputed per tile); stage its offsets in smem
   if (threadIdx.x == 0) {
     const int e0 = tile_env[tile];
     const int e1 = tile_env[tile + 1];  // env of slot hi (or N)
@@ -89,38 +116,13 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
     for (int k = threadIdx.x; k < ne; k += kGaeThreads) s_off[k] = off[e0 + k];
   __syncthreads();
 
-  // thread-local maps
-  const int i0 = lo + threadIdx.x * kGaeItems;
+  // 3) thread-local maps
   double delta[kGaeItems], acoef[kGaeItems];
   Affine mine{1.0, 0.0};
   const double gl = gamma * lambda;
   if (i0 < hi) {
     int e = smem_off ? e0 + upper_bound_i32(s_off, ne, i0) - 1 : upper_bound_i32(off, N + 1, i0) - 1;
     int next_bound = smem_off ? s_off[e - e0 + 1] : off[e + 1];
-    float r[kGaeItems], v[kGaeItems + 1];
-    uint8_t d[kGaeItems];
-    if (i0 + kGaeItems <= hi && (((uintptr_t)(reward + i0)) & 15) == 0) {
-      const float4* r4 = reinterpret_cast<const float4*>(reward + i0);
-      const float4* v4 = reinterpret_cast<const float4*>(value + i0);
-      float4 x0 = __ldg(r4), x1 = __ldg(r4 + 1), y0 = __ldg(v4), y1 = __ldg(v4 + 1);
-      r[0] = x0.x; r[1] = x0.y; r[2] = x0.z; r[3] = x0.w;
-      r[4] = x1.x; r[5] = x1.y; r[6] = x1.z; r[7] = x1.w;
-      v[0] = y0.x; v[1] = y0.y; v[2] = y0.z; v[3] = y0.w;
-      v[4] = y1.x; v[5] = y1.y; v[6] = y1.z; v[7] = y1.w;
-      const uint2 dd = __ldg(reinterpret_cast<const uint2*>(done + i0));
-      const uint8_t* db = reinterpret_cast<const uint8_t*>(&dd);
-#pragma unroll
-      for (int k = 0; k < kGaeItems; ++k) d[k] = db[k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < kGaeItems; ++k) {
-        const int i = i0 + k;
-        r[k] = i < hi ? reward[i] : 0.f;
-        v[k] = i < hi ? value[i] : 0.f;
-        d[k] = i < hi ? done[i] : 1;
-      }
-    }
-    v[kGaeItems] = (i0 + kGaeItems < F) ? value[i0 + kGaeItems] : 0.f;
 #pragma unroll
     for (int k = 0; k < kGaeItems; ++k) {
       const int i = i0 + k;
@@ -219,15 +221,15 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
     x = fma(acoef[k], x, delta[k]);
     av[k] = (float)x;
     const int i = i0 + k;
-    rv[k] = i < hi ? (float)(x + (double)value[i]) : 0.f;
+    rv[k] = i < hi ? (float)(x + (double)v[k]) : 0.f;
   }
   if (i0 + kGaeItems <= hi && (((uintptr_t)(adv + i0)) & 15) == 0) {
     float4* a4 = reinterpret_cast<float4*>(adv + i0);
     float4* r4 = reinterpret_cast<float4*>(ret + i0);
-    a4[0] = make_float4(av[0], av[1], av[2], av[3]);
-    a4[1] = make_float4(av[4], av[5], av[6], av[7]);
-    r4[0] = make_float4(rv[0], rv[1], rv[2], rv[3]);
-    r4[1] = make_float4(rv[4], rv[5], rv[6], rv[7]);
+    __stcs(a4, make_float4(av[0], av[1], av[2], av[3]));
+    __stcs(a4 + 1, make_float4(av[4], av[5], av[6], av[7]));
+    __stcs(r4, make_float4(rv[0], rv[1], rv[2], rv[3]));
+    __stcs(r4 + 1, make_float4(rv[4], rv[5], rv[6], rv[7]));
   } else {
     for (int k = 0; k < kGaeItems; ++k)
       if (i0 + k < hi) {

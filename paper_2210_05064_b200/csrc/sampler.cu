@@ -233,12 +233,18 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(
     if (t < s_len[jl]) {
       const int sl = s_start[jl] + t;
       int f = 0;
-      for (int q = 0; q < D; ++q) cell(f++, jl, tt) = v_obs[(size_t)sl * D + q];
+      if (D == 2) {  // one 8-byte load per slot (no duplicate sector requests)
+        const float2 o2 = __ldcs(reinterpret_cast<const float2*>(v_obs) + sl);
+        cell(f++, jl, tt) = o2.x;
+        cell(f++, jl, tt) = o2.y;
+      } else {
+        for (int q = 0; q < D; ++q) cell(f++, jl, tt) = __ldcs(v_obs + (size_t)sl * D + q);
+      }
       for (int q = 0; q < AC; ++q) cell(f++, jl, tt) = v_actc[(size_t)sl * A + q];
-      cell(f++, jl, tt) = v_lp[sl];
-      cell(f++, jl, tt) = v_adv[sl];
-      cell(f++, jl, tt) = v_ret[sl];
-      if (!continuous) cell(f++, jl, tt) = __int_as_float(v_act[sl]);
+      cell(f++, jl, tt) = __ldcs(v_lp + sl);
+      cell(f++, jl, tt) = __ldcs(v_adv + sl);
+      cell(f++, jl, tt) = __ldcs(v_ret + sl);
+      if (!continuous) cell(f++, jl, tt) = __int_as_float(__ldcs(v_act + sl));
     }
   }
   __syncthreads();
@@ -251,7 +257,12 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(
       const size_t p = (size_t)offs[t] + j0 + jl;
       slots[p] = s_start[jl] + t;
       int f = 0;
-      for (int q = 0; q < D; ++q) obs[p * D + q] = cell(f++, jl, tt);
+      if (D == 2) {
+        const float a0 = cell(f++, jl, tt), a1 = cell(f++, jl, tt);
+        reinterpret_cast<float2*>(obs)[p] = make_float2(a0, a1);
+      } else {
+        for (int q = 0; q < D; ++q) obs[p * D + q] = cell(f++, jl, tt);
+      }
       for (int q = 0; q < AC; ++q) actc[p * A + q] = cell(f++, jl, tt);
       lp[p] = cell(f++, jl, tt);
       adv[p] = cell(f++, jl, tt);
