@@ -23,6 +23,8 @@
 // e.g. make_view fixtures with env = seq % N) first stable-sort the fresh
 // slots by (env, slot) on the device, run the same scan on the gathered
 // arrays and scatter back.
+#include <cstdlib>
+
 #include "view.cuh"
 
 namespace verg {
@@ -61,7 +63,8 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
     const uint8_t* __restrict__ done, int F, const int32_t* __restrict__ off, int N,
     const float* __restrict__ boot, const uint8_t* __restrict__ boot_valid, double gamma,
     double lambda, float* __restrict__ adv, float* __restrict__ ret,
-    volatile GaeTileState* tiles, int* tile_counter, int* err_env, const int32_t* __restrict__ tile_env) {
+    volatile GaeTileState* tiles, int* tile_counter, int* err_env, const int32_t* __restrict__ tile_env,
+    int dbg) {
   __shared__ int s_tile;
   __shared__ int s_e0, s_ne;
   __shared__ int32_t s_off[kGaeOffSmem + 1];
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
       tiles[tid].flag = 1;
       Affine acc{1.0, 0.0};
       int p = tid - 1;
-      while (true) {
+      while (!(dbg & 1)) {
         int f;
         do {
           f = tiles[p].flag;
@@ -278,6 +281,11 @@ __global__ void gae_scatter_kernel(const uint64_t* __restrict__ keys, int F, con
   ret[i] = ret2[j];
 }
 
+static int gae_debug_mode() {
+  const char* e = getenv("VER_GAE_DEBUG");  // experiments only: 1 = skip the look-back wait
+  return e ? atoi(e) : 0;
+}
+
 static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, int F,
                      const int32_t* off, int N, const float* boot, const uint8_t* valid, double gamma,
                      double lambda, float* adv, float* ret) {
@@ -298,7 +306,8 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, i
   h[1] = init[1];
   misc.upload(h, 2);
   gae_scan_kernel<<<ntiles, kGaeThreads, 0, c->stream>>>(r, v, d, F, off, N, boot, valid, gamma, lambda,
-                                                         adv, ret, tiles.p, misc.p, misc.p + 1, tile_env.p);
+                                                         adv, ret, tiles.p, misc.p, misc.p + 1, tile_env.p,
+                                                         gae_debug_mode());
   after_launch(c);
   misc.download(h, 2);
   sync(c);
