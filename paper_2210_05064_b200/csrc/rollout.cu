@@ -123,7 +123,7 @@ static ViewDev vdev(DView& v) {
 // Scatter of the arrival log into env-major view order (rollout.cpp:143-181).
 // One thread per record; every field write is to slot offsets[env]+rank.
 __global__ void compact_scatter_kernel(LogDev L, ViewDev V, const int32_t* __restrict__ offsets,
-                                       int S, int D, int A, int continuous,
+                                       const int32_t* __restrict__ counts, int S, int D, int A, int continuous,
                                        uint8_t* __restrict__ start_flag,
                                        int32_t* __restrict__ hslot_by_slot) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,7 +142,8 @@ __global__ void compact_scatter_kernel(LogDev L, ViewDev V, const int32_t* __res
   V.latency[dst] = L.latency[r];
   V.advantage[dst] = 0.f;
   V.returns[dst] = 0.f;
-  V.done[dst] = L.done[r];
+  // bit 0: done; bit 1: last fresh slot of its env (the GAE scan's segment tail)
+  V.done[dst] = (L.done[r] ? 1 : 0) | (L.rank[r] == counts[e] - 1 ? 2 : 0);
   V.stale[dst] = 0;
   V.replayed[dst] = 0;
   V.env_index[dst] = e;
@@ -457,7 +458,7 @@ static DView* close_rollout(Rollout* R) {
            R->d_done.p,     R->d_episode.p, R->d_step.p,   R->d_version.p};
   ViewDev VD = vdev(*V);
   compact_scatter_kernel<<<cdiv(S, 256), 256, 0, c->stream>>>(
-      L, VD, V->env_offsets.p, S, cfg.obs_dim, cfg.act_dim, cfg.action_kind, flag.p, hsl.p);
+      L, VD, V->env_offsets.p, V->per_env_counts.p, S, cfg.obs_dim, cfg.act_dim, cfg.action_kind, flag.p, hsl.p);
   after_launch(c);
   exclusive_scan_u8(c, flag.p, excl.p, S, K.p);
   seq_ids_kernel<<<cdiv(S, 256), 256, 0, c->stream>>>(flag.p, excl.p, S, V->seq_of_slot.p, starts.p);
@@ -510,7 +511,7 @@ __global__ void synth_view_kernel(const int32_t* __restrict__ off, uint64_t seed
     V.advantage[i] = 0.f;
     V.returns[i] = 0.f;
     const bool d = hunif(seed, i, 24) < p_done;
-    V.done[i] = d;
+    V.done[i] = (d ? 1 : 0) | (t == len - 1 ? 2 : 0);
     V.stale[i] = 0;
     V.replayed[i] = 0;
     V.env_index[i] = e;
@@ -672,7 +673,7 @@ __global__ void backfill_slots_kernel(ViewDev P, ViewDev V, const ver_seq_desc* 
   V.latency[dst] = P.latency[sp];
   V.advantage[dst] = P.advantage[sp];
   V.returns[dst] = P.returns[sp];
-  V.done[dst] = P.done[sp];
+  V.done[dst] = P.done[sp] & 1;  // replayed slots carry no segment-tail bit
   V.stale[dst] = 1;
   V.replayed[dst] = 1;
   V.env_index[dst] = P.env_index[sp];
@@ -784,7 +785,7 @@ static DView* upload_view(Ctx* c, const ver_view_host* h) {
   up_arr(c, V->latency, h->latency, S);
   up_arr(c, V->advantage, h->advantage, S);
   up_arr(c, V->returns, h->returns, S);
-  up_arr(c, V->done, h->done, S);
+  std::vector<uint8_t> done_bits;  // filled below once contiguity is known
   up_arr(c, V->stale, h->stale, S);
   up_arr(c, V->replayed, h->replayed, S);
   up_arr(c, V->env_index, h->env_index, S);
@@ -810,6 +811,17 @@ static DView* upload_view(Ctx* c, const ver_view_host* h) {
     if (h->env_index[i] < 0 || h->env_index[i] >= h->N) contiguous = false;
   V->env_contiguous = contiguous;
   V->fresh_prefix = fresh;
+  // done bit 0 as given; bit 1 marks the last fresh slot of each env (GAE segment tail)
+  if (S && !h->done) config_error("ver_view_upload: missing array");
+  done_bits.assign(h->done, h->done + S);
+  for (int i = 0; i < S; ++i) done_bits[i] = done_bits[i] ? 1 : 0;
+  if (contiguous)
+    for (int i = 0; i < fresh; ++i)
+      if (i + 1 == fresh || h->env_index[i + 1] != h->env_index[i]) done_bits[i] |= 2;
+  if (S) {
+    V->done.upload(done_bits.data(), S);
+    sync(c);
+  }
   if (contiguous) {
     std::vector<int32_t> off(h->N + 1, 0);
     for (int i = 0; i < fresh; ++i) off[h->env_index[i] + 1]++;
@@ -850,6 +862,8 @@ static void download_view(DView& V, ver_view_host* h) {
   down_arr(V.env_bootstrap, h->env_bootstrap, V.N);
   down_arr(V.env_bootstrap_valid, h->env_bootstrap_valid, V.N);
   sync(V.ctx);
+  if (h->done)
+    for (int i = 0; i < S; ++i) h->done[i] &= 1;  // drop the internal segment-tail bit
 }
 
 template <class T>
