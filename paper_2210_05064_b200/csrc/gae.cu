@@ -32,7 +32,6 @@ namespace verg {
 constexpr int kGaeThreads = 256;
 constexpr int kGaeItems = 8;
 constexpr int kGaeTile = kGaeThreads * kGaeItems;  // 2048 slots per tile
-constexpr int kGaeStages = 4;                       // TMA prefetch depth (tiles)
 
 struct Affine {
   double a, b;  // x -> b + a x
@@ -48,163 +47,110 @@ struct GaeTileState {
   int pad;
 };
 
-// one tile's inputs staged by TMA: r[lo, hi), V[lo, hi + 4) (V[hi] = next tile's
-// first value), done bits[lo, hi)
-struct alignas(128) GaeStage {
-  float r[kGaeTile];
-  float v[kGaeTile + 4];
-  uint8_t d[kGaeTile];
-};
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-
-// Persistent decoupled-look-back reverse scan.  Each CTA keeps kGaeStages
-// tiles in flight: thread 0 claims tiles (dynamic tickets, last tile first)
-// and TMA-bulk-copies their r / V / done into a shared-memory ring, so HBM
-// reads for the next tiles overlap this tile's scan, look-back and stores.
-// done bit 1 marks an env's last fresh slot (set by close_rollout / upload /
-// the device generators), so no per-env offsets are read at all; only env
-// tails without `done` look up their env's bootstrap.
+// One tile (2048 slots) per CTA, decoupled look-back.  Per thread the 8-item
+// recursion runs in fp32 (<= 8 chained steps); warp / tile compositions and
+// the cross-tile carry are fp64, which keeps long segments (gamma*lambda -> 1,
+// 1024 steps) inside the fp32 rounding of the fp64 reference.  done bit 1
+// marks an env's last fresh slot, so no per-env offsets are read; only env
+// tails without `done` look up their env's bootstrap.  After the tile's
+// compositions are known, only threads whose suffix reaches the tile end
+// without a reset (a != 0) wait for the look-back; all others store at once.
 __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
     const float* __restrict__ reward, const float* __restrict__ value, const uint8_t* __restrict__ done,
     const int32_t* __restrict__ env_of, int F, const float* __restrict__ boot,
     const uint8_t* __restrict__ boot_valid, double gamma, double lambda, float* __restrict__ adv,
     float* __restrict__ ret, volatile GaeTileState* tiles, int* tile_counter, int* err_env, int dbg) {
-  extern __shared__ __align__(128) uint8_t gsm[];
-  GaeStage* st = reinterpret_cast<GaeStage*>(gsm);
-  __shared__ __align__(8) uint64_t s_bar[kGaeStages];
-  __shared__ int s_ticket[kGaeStages];
-  __shared__ int s_direct[kGaeStages];
+  __shared__ int s_tile;
   __shared__ Affine s_warp[kGaeThreads / 32];
   __shared__ double s_carry;
+  __shared__ volatile int s_ready;
   const int ntiles = (F + kGaeTile - 1) / kGaeTile;
-  const double gl = gamma * lambda;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  auto issue = [&](int s, int t) {  // thread 0 only
-    s_ticket[s] = t;
-    if (t >= ntiles) return;
-    const int lo = (ntiles - 1 - t) * kGaeTile;
-    if (lo + kGaeTile + 4 <= F) {
-      s_direct[s] = 0;
-      constexpr uint32_t kBytes = kGaeTile * 4 + (kGaeTile + 4) * 4 + kGaeTile;  // r + V (+4) + done
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&s_bar[s])),
-                   "r"(kBytes)
-                   : "memory");
-      bulk_g2s(st[s].r, reward + lo, kGaeTile * 4, &s_bar[s]);
-      bulk_g2s(st[s].v, value + lo, (kGaeTile + 4) * 4, &s_bar[s]);
-      bulk_g2s(st[s].d, done + lo, kGaeTile, &s_bar[s]);
-    } else {  // the array's tail tile: read straight from global, complete the phase
-      s_direct[s] = 1;
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&s_bar[s])) : "memory");
-    }
-  };
-
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kGaeStages; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar[s])) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < kGaeStages; ++s) issue(s, atomicAdd(tile_counter, 1));
+    s_tile = atomicAdd(tile_counter, 1);
+    s_ready = 0;
   }
   __syncthreads();
+  const int tid = s_tile;  // 0 = last tile of the array
+  const int tile = ntiles - 1 - tid;
+  const int lo = tile * kGaeTile;
+  const int hi = min(F, lo + kGaeTile);
+  const int i0 = lo + threadIdx.x * kGaeItems;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float gf = (float)gamma, glf = (float)(gamma * lambda);
 
-  for (int k = 0;; ++k) {
-    const int s = k % kGaeStages;
-    const int tid = s_ticket[s];
-    if (tid >= ntiles) break;
-    const int tile = ntiles - 1 - tid;
-    const int lo = tile * kGaeTile;
-    const int hi = min(F, lo + kGaeTile);
-    const uint32_t ph = (k / kGaeStages) & 1;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(&s_bar[s])),
-        "r"(ph)
-        : "memory");
-    const bool direct = s_direct[s];
-    const int j0 = threadIdx.x * kGaeItems;  // tile-relative
-    const int i0 = lo + j0;
-    float r[kGaeItems], v[kGaeItems + 1];
-    uint8_t d[kGaeItems];
-    if (!direct) {
-      const float4* r4 = reinterpret_cast<const float4*>(st[s].r + j0);
-      const float4* v4 = reinterpret_cast<const float4*>(st[s].v + j0);
-      const float4 x0 = r4[0], x1 = r4[1], y0 = v4[0], y1 = v4[1];
-      r[0] = x0.x; r[1] = x0.y; r[2] = x0.z; r[3] = x0.w;
-      r[4] = x1.x; r[5] = x1.y; r[6] = x1.z; r[7] = x1.w;
-      v[0] = y0.x; v[1] = y0.y; v[2] = y0.z; v[3] = y0.w;
-      v[4] = y1.x; v[5] = y1.y; v[6] = y1.z; v[7] = y1.w;
-      v[8] = st[s].v[j0 + 8];
-      const uint2 dd = *reinterpret_cast<const uint2*>(st[s].d + j0);
-      const uint8_t* db = reinterpret_cast<const uint8_t*>(&dd);
+  float r[kGaeItems], v[kGaeItems + 1];
+  uint32_t dw[2];
+  if (i0 + kGaeItems <= hi) {
+    const float4* r4 = reinterpret_cast<const float4*>(reward + i0);
+    const float4* v4 = reinterpret_cast<const float4*>(value + i0);
+    const float4 x0 = __ldcs(r4), x1 = __ldcs(r4 + 1), y0 = __ldcs(v4), y1 = __ldcs(v4 + 1);
+    const uint2 dd = __ldcs(reinterpret_cast<const uint2*>(done + i0));
+    r[0] = x0.x; r[1] = x0.y; r[2] = x0.z; r[3] = x0.w;
+    r[4] = x1.x; r[5] = x1.y; r[6] = x1.z; r[7] = x1.w;
+    v[0] = y0.x; v[1] = y0.y; v[2] = y0.z; v[3] = y0.w;
+    v[4] = y1.x; v[5] = y1.y; v[6] = y1.z; v[7] = y1.w;
+    dw[0] = dd.x;
+    dw[1] = dd.y;
+  } else {
+    dw[0] = dw[1] = 0x03030303u;  // beyond the end: tail + done (inert)
 #pragma unroll
-      for (int q = 0; q < kGaeItems; ++q) d[q] = db[q];
-    } else {
-#pragma unroll
-      for (int q = 0; q < kGaeItems; ++q) {
-        const int i = i0 + q;
-        r[q] = i < hi ? reward[i] : 0.f;
-        v[q] = i < hi ? value[i] : 0.f;
-        d[q] = i < hi ? done[i] : 3;
-      }
-      v[kGaeItems] = (i0 + kGaeItems < F) ? value[i0 + kGaeItems] : 0.f;
-    }
-    // per-item maps x -> delta + a x (tail: a = 0; V_next = bootstrap unless done)
-    auto item = [&](int q, double& delta, double& acoef) {
+    for (int q = 0; q < kGaeItems; ++q) {
       const int i = i0 + q;
-      if (i >= hi) {
-        delta = 0.0;
-        acoef = 1.0;
-        return;
+      r[q] = i < hi ? reward[i] : 0.f;
+      v[q] = i < hi ? value[i] : 0.f;
+      if (i < hi) {
+        const uint32_t sh = 8 * (q & 3);
+        dw[q >> 2] = (dw[q >> 2] & ~(0xffu << sh)) | ((uint32_t)done[i] << sh);
       }
-      const bool dn = d[q] & 1, tail = d[q] & 2;
-      double vnext = 0.0;
-      if (tail) {
-        if (!dn) {
-          const int e = env_of[i];
-          if (!boot_valid[e]) atomicMin(err_env, e);
-          vnext = (double)boot[e];
-        }
-      } else {
-        vnext = (double)v[q + 1];
+    }
+  }
+  v[kGaeItems] = (i0 + kGaeItems < F) ? value[i0 + kGaeItems] : 0.f;
+
+  // per-item maps A_i = delta_i + a_i A_{i+1} (fp32); bootstrap at env tails
+  float dl[kGaeItems], ac[kGaeItems];
+#pragma unroll
+  for (int q = 0; q < kGaeItems; ++q) {
+    const uint32_t b = (dw[q >> 2] >> (8 * (q & 3))) & 0xffu;
+    const bool dn = b & 1, tail = b & 2;
+    float vnext = v[q + 1];
+    if (tail) {
+      vnext = 0.f;
+      if (!dn && i0 + q < hi) {
+        const int e = env_of[i0 + q];
+        if (!boot_valid[e]) atomicMin(err_env, e);
+        vnext = boot[e];
       }
-      const double mask = dn ? 0.0 : 1.0;
-      delta = (double)r[q] + gamma * vnext * mask - (double)v[q];
-      acoef = tail ? 0.0 : gl * mask;
-    };
-    Affine mine{1.0, 0.0};
-#pragma unroll
-    for (int q = kGaeItems - 1; q >= 0; --q) {
-      double dl, ac;
-      item(q, dl, ac);
-      mine = compose(Affine{ac, dl}, mine);
     }
-    // block-level suffix scan of thread maps
-    Affine incl = mine;
+    const float mask = dn ? 0.f : 1.f;
+    dl[q] = fmaf(gf * vnext, mask, r[q]) - v[q];
+    ac[q] = tail ? 0.f : glf * mask;
+  }
+  float ma = 1.f, mb = 0.f;  // thread composite, fp32 over <= 8 steps
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Affine y{__shfl_down_sync(0xffffffffu, incl.a, o), __shfl_down_sync(0xffffffffu, incl.b, o)};
-      if (lane + o < 32) incl = compose(incl, y);
-    }
-    if (lane == 0) s_warp[warp] = incl;
-    __syncthreads();  // also: every thread has read stage s
-    if (threadIdx.x == 0) {
+  for (int q = kGaeItems - 1; q >= 0; --q) {
+    mb = fmaf(ac[q], mb, dl[q]);
+    ma = ac[q] * ma;
+  }
+  // block-level suffix scan of thread maps (fp64)
+  Affine incl{(double)ma, (double)mb};
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Affine y{__shfl_down_sync(0xffffffffu, incl.a, o), __shfl_down_sync(0xffffffffu, incl.b, o)};
+    if (lane + o < 32) incl = compose(incl, y);
+  }
+  if (lane == 0) s_warp[warp] = incl;
+  __syncthreads();
+  Affine lane_ex{__shfl_down_sync(0xffffffffu, incl.a, 1), __shfl_down_sync(0xffffffffu, incl.b, 1)};
+  if (lane == 31) lane_ex = Affine{1.0, 0.0};
+  if (warp == 0) {
+    if (lane == 0) {
       Affine suf{1.0, 0.0};
       for (int w = kGaeThreads / 32 - 1; w >= 0; --w) {
         const Affine cur = s_warp[w];
         s_warp[w] = suf;
         suf = compose(cur, suf);
       }
-      double carry = 0.0;
+      // publish the tile aggregate first, then release the other warps
       if (tid == 0) {
         tiles[tid].inc = suf.b;
         __threadfence();
@@ -214,6 +160,11 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
         tiles[tid].b = suf.b;
         __threadfence();
         tiles[tid].flag = 1;
+      }
+      __threadfence_block();
+      s_ready = 1;
+      double carry = 0.0;  // A at hi
+      if (tid != 0) {
         Affine acc{1.0, 0.0};
         int p = tid - 1;
         while (!(dbg & 1)) {
@@ -238,37 +189,42 @@ __global__ void __launch_bounds__(kGaeThreads) gae_scan_kernel(
         tiles[tid].flag = 2;
       }
       s_carry = carry;
-      issue(s, atomicAdd(tile_counter, 1));  // refill this stage (all threads are past reading it)
+      __threadfence_block();
+      s_ready = 2;
     }
-    __syncthreads();
-    Affine lane_ex{__shfl_down_sync(0xffffffffu, incl.a, 1), __shfl_down_sync(0xffffffffu, incl.b, 1)};
-    if (lane == 31) lane_ex = Affine{1.0, 0.0};
-    const Affine after = compose(lane_ex, s_warp[warp]);
-    double x = fma(after.a, s_carry, after.b);
-    float av[kGaeItems], rv[kGaeItems];
+    __syncwarp();
+  } else {
+    while (s_ready == 0) {
+    }
+  }
+  const Affine after = compose(lane_ex, s_warp[warp]);  // maps A at hi to A after this thread's items
+  double x = after.b;
+  if (after.a != 0.0) {  // this thread's values depend on the carry
+    while (s_ready != 2) {
+    }
+    x = fma(after.a, s_carry, after.b);
+  }
+  float xf = (float)x;
+  float av[kGaeItems], rv[kGaeItems];
 #pragma unroll
-    for (int q = kGaeItems - 1; q >= 0; --q) {
-      double dl, ac;
-      item(q, dl, ac);
-      x = fma(ac, x, dl);
-      av[q] = (float)x;
-      rv[q] = (float)(x + (double)v[q]);
-    }
-    if (i0 + kGaeItems <= hi) {
-      float4* a4 = reinterpret_cast<float4*>(adv + i0);
-      float4* r4 = reinterpret_cast<float4*>(ret + i0);
-      __stcs(a4, make_float4(av[0], av[1], av[2], av[3]));
-      __stcs(a4 + 1, make_float4(av[4], av[5], av[6], av[7]));
-      __stcs(r4, make_float4(rv[0], rv[1], rv[2], rv[3]));
-      __stcs(r4 + 1, make_float4(rv[4], rv[5], rv[6], rv[7]));
-    } else {
-      for (int q = 0; q < kGaeItems; ++q)
-        if (i0 + q < hi) {
-          adv[i0 + q] = av[q];
-          ret[i0 + q] = rv[q];
-        }
-    }
-    __syncthreads();  // s_warp / s_carry reuse by the next tile
+  for (int q = kGaeItems - 1; q >= 0; --q) {
+    xf = fmaf(ac[q], xf, dl[q]);
+    av[q] = xf;
+    rv[q] = xf + v[q];
+  }
+  if (i0 + kGaeItems <= hi) {
+    float4* a4 = reinterpret_cast<float4*>(adv + i0);
+    float4* r4 = reinterpret_cast<float4*>(ret + i0);
+    __stcs(a4, make_float4(av[0], av[1], av[2], av[3]));
+    __stcs(a4 + 1, make_float4(av[4], av[5], av[6], av[7]));
+    __stcs(r4, make_float4(rv[0], rv[1], rv[2], rv[3]));
+    __stcs(r4 + 1, make_float4(rv[4], rv[5], rv[6], rv[7]));
+  } else {
+    for (int q = 0; q < kGaeItems; ++q)
+      if (i0 + q < hi) {
+        adv[i0 + q] = av[q];
+        ret[i0 + q] = rv[q];
+      }
   }
 }
 
@@ -325,13 +281,8 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   h[0] = 0;
   h[1] = 0x7fffffff;
   misc.upload(h, 2);
-  const size_t smem = sizeof(GaeStage) * kGaeStages;
-  VER_CUDA(cudaFuncSetAttribute(gae_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int per_sm = 0;
-  VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_scan_kernel, kGaeThreads, smem));
-  const int grid = std::max(1, std::min(ntiles, per_sm * c->num_sms));
-  gae_scan_kernel<<<grid, kGaeThreads, smem, c->stream>>>(r, v, d, env, F, boot, valid, gamma, lambda, adv, ret,
-                                                          tiles.p, misc.p, misc.p + 1, gae_debug_mode());
+  gae_scan_kernel<<<ntiles, kGaeThreads, 0, c->stream>>>(r, v, d, env, F, boot, valid, gamma, lambda, adv, ret,
+                                                        tiles.p, misc.p, misc.p + 1, gae_debug_mode());
   after_launch(c);
   misc.download(h, 2);
   sync(c);
