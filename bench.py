@@ -99,9 +99,9 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU side
-def cpu_sample(n_envs_sample=32, seed=1):
+def cpu_sample(n_envs_sample=64, seed=1):
     """The oracle (CPU double restatement, single thread as the reference's
-    learner thread) on a bounded sample: N=32 of the 256 envs (same T, model,
+    learner thread) on a bounded sample: N=64 of the 256 envs (same T, model,
     epochs, B), GAE + minibatch 0 of epoch 0 timed, extrapolated to the full
     4 x 2 minibatch update.  Returns (env-steps/s, seconds measured, sample)."""
     from oracle import oracle as O
@@ -214,6 +214,7 @@ def run_ours(args, rank, world):
     step_ms = [a.elapsed_time(b) for a, b in times]
     ms = sum(step_ms) / len(step_ms)
     phase = learner.last_timing()
+    phase_n = learner.last_timing_counts()
     if dist:
         t = torch.tensor([ms], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -263,9 +264,16 @@ def run_ours(args, rank, world):
 
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
-        fl = flops_per_step() * fresh * EPOCHS
-        dense_ms = phase.get("forward", 0) + phase.get("backward", 0)
-        achieved_tf = fl / (dense_ms / 1000.0) / 1e12 if dense_ms > 0 else 0.0
+        # dominant kernel = the larger of the two recurrence kernels (the launch list in
+        # profiles/ ranks them first); its algorithmic work is one H x 3H matvec per
+        # packed row (6 H^2 FLOP), every row once per epoch, so per launch S_mb rows
+        dom = max(("rec_bwd", "rec_fwd"), key=lambda k: phase.get(k, 0.0))
+        n_dom = max(1, phase_n.get(dom, 0))
+        rows_per_launch = fresh * EPOCHS / n_dom
+        dom_flop = 6.0 * H_ * H_ * rows_per_launch
+        dom_ms = phase.get(dom, 0.0) / n_dom
+        achieved_tf = dom_flop / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
+        simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # fp32 FMA pipe peak at max SM clock
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -276,9 +284,13 @@ def run_ours(args, rank, world):
                        "parallelism": f"dp{world} (DD-PPO, NCCL AllReduce per minibatch)" if world > 1 else "dp1"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
                          "frac": achieved_tf / bf16s, "traffic": None,
-                         "kernel": "forward+backward policy GEMMs + recurrence (fp32 SIMT in this build)",
-                         "peak_kind": f"{peaks_kind} bf16 dense sustained"},
+                         "kernel": f"{'gru_bwd_reg<512>' if dom == 'rec_bwd' else 'gru_fwd_reg<512>'} "
+                                   f"(GRU recurrence, fp32 FMA pipe; {n_dom} launches/step, "
+                                   f"{dom_ms:.3f} ms avg, {rows_per_launch:.0f} rows x 6H^2 FLOP per launch)",
+                         "peak_kind": f"{peaks_kind} bf16 dense sustained",
+                         "fp32_simt_peak": simt_peak, "frac_of_fp32_simt": achieved_tf / simt_peak},
             "phases_ms": phase,
+            "phase_counts": phase_n,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "e2e": {"value": fresh * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -297,7 +309,7 @@ def run_ours(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

@@ -284,9 +284,14 @@ ver_status ver_learner_get_state(ver_learner l, double* alpha, int64_t* consumed
                                  int64_t* update_index);
 ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed_steps,
                                  int64_t update_index);
-/* per-phase device time of the last update, ms (gae, sampler, gather, forward,
-   recurrence, loss, backward, allreduce, adam); n in/out */
+/* per-phase device time of the last update, ms, from CUDA events on the ctx
+   stream: gae, sampler (split + pack + gather), replay (batch_h0), forward,
+   loss, backward, allreduce, adam, then the recurrence kernels alone
+   (rec_fwd nested in forward, rec_bwd nested in backward); n in/out */
 ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n);
+/* number of timed intervals (kernel launches for rec_fwd / rec_bwd) behind each
+   phase of ver_learner_last_timing; n in/out */
+ver_status ver_learner_last_timing_counts(ver_learner l, int* counts, int* n);
 
 /* Measurement: device time (CUDA events, averaged over reps) of compute_gae on
    v and of the time-major gather of all B minibatches of one

@@ -725,7 +725,7 @@ class TrainStats:
     lr: float
 
 
-PHASES = ("gae", "sampler", "replay", "forward", "loss", "backward", "allreduce", "adam")
+PHASES = ("gae", "sampler", "replay", "forward", "loss", "backward", "allreduce", "adam", "rec_fwd", "rec_bwd")
 
 
 class Learner:
@@ -822,6 +822,13 @@ class Learner:
         n = C.c_int(16)
         _check(_lib().ver_learner_last_timing(self.h, ms, C.byref(n)))
         return {PHASES[i]: float(ms[i]) for i in range(min(n.value, len(PHASES)))}
+
+    def last_timing_counts(self) -> dict:
+        """Intervals behind each phase of last_timing (launches for rec_fwd / rec_bwd)."""
+        cnt = (C.c_int * 16)()
+        n = C.c_int(16)
+        _check(_lib().ver_learner_last_timing_counts(self.h, cnt, C.byref(n)))
+        return {PHASES[i]: int(cnt[i]) for i in range(min(n.value, len(PHASES)))}
 
 
 def debug_gemm(A, B, transA=False, transB=False, engine=1, splitk=1, ctx: Context | None = None):

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "ver_gpu.h"
@@ -65,10 +66,35 @@ struct Ctx {
   bool tensor_cores = true;  // tcgen05 GEMMs on (off: fp32 SIMT GEMMs)
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
+  // optional device-time log: (tag, start, end) event pairs recorded on `stream`
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>>* evlog = nullptr;
+  int rec_tag = -1;  // tag for recurrence launches (>= 0 while a learner minibatch is timed)
   // pinned scratch for small synchronous reads
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   void* pinned_buf(size_t bytes);
+};
+
+// Records a (tag, start, end) event pair into ctx->evlog around a scope
+// (no-op when the log is off or tag < 0).
+struct ScopedEv {
+  Ctx* c;
+  int tag;
+  cudaEvent_t a = nullptr;
+  ScopedEv(Ctx* c_, int tag_) : c(c_), tag(tag_) {
+    if (c->evlog && tag >= 0) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~ScopedEv() {
+    if (a) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, c->stream);
+      c->evlog->emplace_back(tag, a, b);
+    }
+  }
 };
 
 // Make the ctx's device current for this thread (entry points call this).

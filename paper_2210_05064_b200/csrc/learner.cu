@@ -31,7 +31,11 @@ inline uint64_t mix64(uint64_t a, uint64_t b) {
 }
 }  // namespace
 
-enum Phase { PH_GAE, PH_SAMPLER, PH_REPLAY, PH_FORWARD, PH_LOSS, PH_BACKWARD, PH_ALLREDUCE, PH_ADAM, PH_N };
+enum Phase {
+  PH_GAE, PH_SAMPLER, PH_REPLAY, PH_FORWARD, PH_LOSS, PH_BACKWARD, PH_ALLREDUCE, PH_ADAM,
+  PH_REC_FWD, PH_REC_BWD,  // recurrence kernels alone (nested in forward / backward)
+  PH_N
+};
 
 struct Learner {
   Ctx* ctx = nullptr;
@@ -51,10 +55,11 @@ struct Learner {
   DBuf<int> flags;           // [0] non-finite parameters
   Workspace ws, wr;          // minibatch / h0-replay workspaces
   DBuf<float> h0s;           // sorted h0 of the current minibatch
-  // per-phase timing of the last update
-  std::vector<cudaEvent_t> ev;
-  std::vector<std::pair<int, int>> ev_pairs;  // (phase, event index of start)
+  // per-phase device timing of the last update (events on ctx->stream)
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> evlog;
+  std::vector<std::pair<int, cudaEvent_t>> open;
   float phase_ms[PH_N] = {};
+  int phase_n[PH_N] = {};
   bool timing = true;
 
   void mark_begin(int phase) {
@@ -62,26 +67,27 @@ struct Learner {
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, ctx->stream);
-    ev.push_back(e);
-    ev_pairs.push_back({phase, (int)ev.size() - 1});
+    open.push_back({phase, e});
   }
   void mark_end() {
-    if (!timing) return;
+    if (!timing || open.empty()) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, ctx->stream);
-    ev.push_back(e);
+    evlog.emplace_back(open.back().first, open.back().second, e);
+    open.pop_back();
   }
   void collect_timing() {
-    for (int k = 0; k < PH_N; ++k) phase_ms[k] = 0.f;
-    for (auto& pr : ev_pairs) {
+    for (int k = 0; k < PH_N; ++k) phase_ms[k] = 0.f, phase_n[k] = 0;
+    for (auto& [tag, a, b] : evlog) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[pr.second], ev[pr.second + 1]);
-      phase_ms[pr.first] += ms;
+      cudaEventElapsedTime(&ms, a, b);
+      phase_ms[tag] += ms;
+      phase_n[tag] += 1;
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
     }
-    for (auto e : ev) cudaEventDestroy(e);
-    ev.clear();
-    ev_pairs.clear();
+    evlog.clear();
   }
 };
 
@@ -217,7 +223,9 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   Ln.mark_end();
   Ln.ws.ensure(m, S, true);
   Ln.mark_begin(PH_FORWARD);
+  c->rec_tag = PH_REC_FWD;
   policy_forward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, true);
+  c->rec_tag = -1;
   Ln.mark_end();
   LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, nullptr,
               Ln.cfg.clip, Ln.cfg.is_cap, Ln.cfg.value_loss_coef, Ln.alpha.p};
@@ -225,7 +233,9 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   policy_loss(c, m, Ln.params.p, S, la, Ln.ws, Ln.grad.p, Ln.lstats.p, true);
   Ln.mark_end();
   Ln.mark_begin(PH_BACKWARD);
+  c->rec_tag = PH_REC_BWD;
   policy_backward(c, m, Ln.params.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, Ln.grad.p);
+  c->rec_tag = -1;
   Ln.mark_end();
   const bool ar = Ln.allreduce && c->comm && c->nranks > 1;
   if (ar) {  // grad_hook -> AllReduce::average; entropy_hook -> average_scalar
@@ -256,6 +266,11 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
   Ctx* c = Ln.ctx;
   if (V.obs_dim != Ln.m.D || V.hidden_dim != Ln.m.H || (V.action_kind == 1) != (Ln.m.continuous == 1))
     config_error("learner_update: view shape does not match the model");
+  struct EvGuard {  // the ctx logs recurrence launches into this learner's timing
+    Ctx* c;
+    ~EvGuard() { c->evlog = nullptr, c->rec_tag = -1; }
+  } evg{c};
+  c->evlog = Ln.timing ? &Ln.evlog : nullptr;
   Ln.mark_begin(PH_GAE);
   compute_gae(V, Ln.cfg.gamma, Ln.cfg.gae_lambda);
   Ln.mark_end();
@@ -742,6 +757,14 @@ ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n) {
   VER_API_BEGIN
   const int k = std::min(*n, (int)PH_N);
   for (int i = 0; i < k; ++i) ms[i] = l->l.phase_ms[i];
+  *n = PH_N;
+  VER_API_END
+}
+
+ver_status ver_learner_last_timing_counts(ver_learner l, int* counts, int* n) {
+  VER_API_BEGIN
+  const int k = std::min(*n, (int)PH_N);
+  for (int i = 0; i < k; ++i) counts[i] = l->l.phase_n[i];
   *n = PH_N;
   VER_API_END
 }

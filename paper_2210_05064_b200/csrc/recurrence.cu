@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_persistent(
 // pad) forward partial sums are reduce-scattered across the 32 lanes in 31
 // shuffles (lane l ends with value l), the backward's 4 x 2 in 9.
 constexpr int RCF = 32;  // forward rows per staged chunk (32 x H fp32)
-constexpr int RCB = 8;   // backward rows per staged chunk (8 x 3H fp32)
 
 template <int NV>
 __device__ __forceinline__ void load_vec(const float* p, float* out) {
@@ -412,7 +411,7 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
   }
 }
 
-template <int H>
+template <int H, int RCB>
 __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
@@ -519,9 +518,10 @@ template <int H>
 static const void* fwd_reg_fn() {
   return reinterpret_cast<const void*>(gru_fwd_reg<H>);
 }
+constexpr int RCB = 32;  // backward rows per staged chunk (32 x 3H fp32 = 192 KB at H = 512)
 template <int H>
 static const void* bwd_reg_fn() {
-  return reinterpret_cast<const void*>(gru_bwd_reg<H>);
+  return reinterpret_cast<const void*>(gru_bwd_reg<H, RCB>);
 }
 static const void* pick_fwd(int H) {
   switch (H) {
@@ -548,6 +548,7 @@ static const void* pick_bwd(int H) {
 
 // ------------------------------------------------------------ launch
 static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** args) {
+  ScopedEv ev(c, c->rec_tag);
   VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, RT, smem));
