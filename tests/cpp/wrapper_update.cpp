@@ -1,0 +1,102 @@
+// C++ caller of the drop-in through include/ver_gpu.hpp, shaped like the
+// reference's train_single (bench.cpp:95-205): RolloutBuffer -> begin_rollout
+// -> append_step* -> set_bootstrap -> close_rollout -> Learner::update.
+//
+//   wrapper_update nodevice        expect DeviceError from Context (no GPU)
+//   wrapper_update <dir>           read the records written by
+//                                  tests/test_cpp_wrapper.py, run one update,
+//                                  write <dir>/params_out.f32, print the stats
+#include <cstdio>
+#include <fstream>
+#include <iostream>
+#include <string>
+#include <vector>
+
+#include "ver_gpu.hpp"
+
+template <class T>
+static std::vector<T> load(const std::string& path, size_t n) {
+  std::vector<T> v(n);
+  std::ifstream f(path, std::ios::binary);
+  if (!f.read(reinterpret_cast<char*>(v.data()), (std::streamsize)(n * sizeof(T))))
+    throw std::runtime_error("short read: " + path);
+  return v;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 2) return 2;
+  const std::string mode = argv[1];
+  if (mode == "nodevice") {
+    try {
+      ver::gpu::Context ctx(0);
+    } catch (const ver::gpu::DeviceError& e) {
+      std::printf("DeviceError: %s\n", e.what());
+      return 0;
+    }
+    std::printf("expected DeviceError\n");
+    return 1;
+  }
+  const std::string d = mode + "/";
+  int T, N, D, H, n;
+  {
+    std::ifstream m(d + "meta.txt");
+    m >> T >> N >> D >> H >> n;
+  }
+  auto env = load<int32_t>(d + "env.i32", n);
+  auto obs = load<float>(d + "obs.f32", (size_t)n * D);
+  auto act = load<int32_t>(d + "act.i32", n);
+  auto logp = load<float>(d + "logp.f32", n);
+  auto val = load<float>(d + "value.f32", n);
+  auto rew = load<float>(d + "reward.f32", n);
+  auto done = load<uint8_t>(d + "done.u8", n);
+  auto hb = load<float>(d + "hb.f32", (size_t)n * H);
+  auto hbv = load<uint8_t>(d + "hbv.u8", n);
+  auto boot = load<float>(d + "boot.f32", N);
+  auto bootv = load<uint8_t>(d + "bootv.u8", N);
+
+  ver::gpu::Context ctx(0);
+  ver_rollout_config rc{T, N, /*Variable*/ 1, 0, D, 0, H};
+  ver::gpu::RolloutBuffer buf(ctx, rc);
+  buf.begin_rollout(1);
+  ver_step_batch b{};
+  b.n = n;
+  b.env_index = env.data();
+  b.obs = obs.data();
+  b.act_disc = act.data();
+  b.log_prob = logp.data();
+  b.value = val.data();
+  b.reward = rew.data();
+  b.done = done.data();
+  b.h_before = hb.data();
+  b.h_before_valid = hbv.data();
+  buf.append(b);
+  for (int e = 0; e < N; ++e)
+    if (bootv[e]) buf.set_bootstrap(e, boot[e]);
+  ver::gpu::RolloutView view = buf.close_rollout();
+  // the reference's contract: closing twice is a ProtocolError (rollout.cpp:103-104)
+  bool threw = false;
+  try {
+    buf.close_rollout();
+  } catch (const ver::gpu::ProtocolError&) {
+    threw = true;
+  }
+  if (!threw) {
+    std::printf("expected ProtocolError on second close\n");
+    return 1;
+  }
+  ver_model_config mc{D, H, H, 0, 2, 0};
+  int64_t P = 0;
+  int nt = 0;
+  ver::gpu::check(ver_param_count(&mc, &P, &nt));
+  auto params = load<float>(d + "params.f32", (size_t)P);
+  ver_ppo_config pc{0.99, 0.95, 0.2, 2, 2, 0.5, 1.0};
+  ver_entropy_controller ec{1e-3, 0.0, 1e-4, 1.0, 2.5e-4};
+  ver::gpu::Learner learner(ctx, mc, params, pc, ec, 2.5e-4, 1000000, 77);
+  const ver_train_stats st = learner.update(view);
+  auto out = learner.params();
+  std::ofstream(d + "params_out.f32", std::ios::binary)
+      .write(reinterpret_cast<const char*>(out.data()), (std::streamsize)(out.size() * sizeof(float)));
+  std::printf("{\"steps\": %d, \"fresh_steps\": %d, \"loss\": %.9g, \"alpha\": %.9g}\n", st.steps,
+              st.fresh_steps, st.loss, st.alpha);
+  return 0;
+}
