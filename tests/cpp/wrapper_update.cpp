@@ -73,16 +73,30 @@ int main(int argc, char** argv) {
   for (int e = 0; e < N; ++e)
     if (bootv[e]) buf.set_bootstrap(e, boot[e]);
   ver::gpu::RolloutView view = buf.close_rollout();
-  // the reference's contract: closing twice is a ProtocolError (rollout.cpp:103-104)
-  bool threw = false;
-  try {
-    buf.close_rollout();
-  } catch (const ver::gpu::ProtocolError&) {
-    threw = true;
-  }
-  if (!threw) {
-    std::printf("expected ProtocolError on second close\n");
-    return 1;
+  // the reference's contract (rollout.cpp:103-104, test_rollout.cpp:180):
+  // closing an empty buffer, or one still open, is a ProtocolError
+  {
+    ver::gpu::RolloutBuffer empty(ctx, rc);
+    bool threw = false;
+    try {
+      empty.close_rollout();
+    } catch (const ver::gpu::ProtocolError&) {
+      threw = true;
+    }
+    empty.begin_rollout(1);
+    ver_step_batch one = b;
+    one.n = 1;
+    empty.append(one);
+    bool threw_open = false;
+    try {
+      empty.close_rollout();
+    } catch (const ver::gpu::ProtocolError&) {
+      threw_open = true;
+    }
+    if (!threw || !threw_open) {
+      std::printf("expected ProtocolError on empty (%d) / open (%d) close\n", (int)threw, (int)threw_open);
+      return 1;
+    }
   }
   ver_model_config mc{D, H, H, 0, 2, 0};
   int64_t P = 0;
