@@ -305,6 +305,11 @@ ver_status ver_bench_gae_gather(ver_view v, double gamma, double lambda, int B, 
    splitk > 1 uses the deterministic split-K partial + reduce path. */
 ver_status ver_debug_gemm(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K,
                           const float* A, int lda, const float* B, int ldb, float* C, int splitk);
+/* Measurement: average device time (CUDA events on the ctx stream, after one
+   warm-up) of `reps` GEMMs of the shape above on library-allocated operands
+   (contents arbitrary; no host copies).  ms_out[0] = ms per GEMM. */
+ver_status ver_debug_gemm_time(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K, int splitk,
+                               int reps, float* ms_out);
 
 /* ------------------------------------------------------- distributed (L7) */
 /* estimate_time (distributed.cpp:24-51), bisection with device counting */

@@ -158,6 +158,8 @@ _SIGS = {
     "ver_learner_last_timing_counts": (c_int, [C.c_void_p, P(c_int), P(c_int)]),
     "ver_debug_gemm": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, P(c_float), c_int,
                                P(c_float), c_int, P(c_float), c_int]),
+    "ver_debug_gemm_time": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                    P(c_float)]),
     "ver_estimate_time": (c_int, [C.c_void_p, P(c_double), c_int, c_int64, c_int64, P(c_double)]),
     "ver_optimal_preempt_steps": (c_int, [C.c_void_p, P(c_double), c_int, c_double, c_int64,
                                           P(c_int64)]),

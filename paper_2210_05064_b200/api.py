@@ -845,6 +845,15 @@ def debug_gemm(A, B, transA=False, transB=False, engine=1, splitk=1, ctx: Contex
     return C_
 
 
+def debug_gemm_time(M, N, K, transA=False, transB=False, engine=1, splitk=1, reps=10,
+                    ctx: Context | None = None) -> float:
+    """Device ms per GEMM of this shape through the library GEMM (operands resident)."""
+    ctx = ctx or default_context()
+    ms = (C.c_float * 1)()
+    _check(_lib().ver_debug_gemm_time(ctx.h, engine, int(transA), int(transB), M, N, K, splitk, reps, ms))
+    return float(ms[0])
+
+
 # ---------------------------------------------------------- distributed
 def estimate_time(step_times, max_steps: int, steps: int, ctx: Context | None = None) -> float:
     ctx = ctx or default_context()

@@ -1,29 +1,50 @@
-// epilogue.cuh — fused GEMM epilogues shared by the SIMT and tcgen05 GEMMs:
-// each is called once per output element (m, n) with the accumulated value
-// and the split-K index z.
+// epilogue.cuh — fused GEMM epilogues shared by the SIMT and tcgen05 GEMMs.
+// operator()(m, n, v, z): one output element (SIMT GEMM).
+// vec4(m, n, v4, z): four consecutive columns n..n+3 of row m (tcgen05 GEMM's
+// coalesced epilogue; n % 4 == 0, every leading dimension % 4 == 0).
 #pragma once
 
 #include "common.cuh"
 
 namespace verg {
 
+inline bool ptr16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
 struct EpiStore {
   float* C;
   int ldc;
+  bool vec_ok() const { return ptr16(C) && ldc % 4 == 0; }
   __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v; }
+  __device__ void vec4(int m, int n, float4 v, int) const {
+    *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) = v;
+  }
 };
 struct EpiBias {
   float* C;
   int ldc;
   const float* bias;
+  bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias); }
   __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v + bias[n]; }
+  __device__ void vec4(int m, int n, float4 v, int) const {
+    *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) = add4(v, __ldg(reinterpret_cast<const float4*>(bias + n)));
+  }
 };
 struct EpiBiasTanh {
   float* C;
   int ldc;
   const float* bias;
+  bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias); }
   __device__ void operator()(int m, int n, float v, int) const {
     C[(size_t)m * ldc + n] = tanhf(v + bias[n]);
+  }
+  __device__ void vec4(int m, int n, float4 v, int) const {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(bias + n));
+    *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) =
+        make_float4(tanhf(v.x + b.x), tanhf(v.y + b.y), tanhf(v.z + b.z), tanhf(v.w + b.w));
   }
 };
 struct EpiAddTerm {  // C = acc + T
@@ -31,8 +52,13 @@ struct EpiAddTerm {  // C = acc + T
   int ldc;
   const float* T;
   int ldt;
+  bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(T) && ldt % 4 == 0; }
   __device__ void operator()(int m, int n, float v, int) const {
     C[(size_t)m * ldc + n] = v + T[(size_t)m * ldt + n];
+  }
+  __device__ void vec4(int m, int n, float4 v, int) const {
+    *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) =
+        add4(v, *reinterpret_cast<const float4*>(T + (size_t)m * ldt + n));
   }
 };
 struct EpiTanhGrad {  // C = acc * (1 - Y^2)
@@ -40,16 +66,27 @@ struct EpiTanhGrad {  // C = acc * (1 - Y^2)
   int ldc;
   const float* Y;
   int ldy;
+  bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(Y) && ldy % 4 == 0; }
   __device__ void operator()(int m, int n, float v, int) const {
     const float y = Y[(size_t)m * ldy + n];
     C[(size_t)m * ldc + n] = v * (1.f - y * y);
+  }
+  __device__ void vec4(int m, int n, float4 v, int) const {
+    const float4 y = *reinterpret_cast<const float4*>(Y + (size_t)m * ldy + n);
+    *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) =
+        make_float4(v.x * (1.f - y.x * y.x), v.y * (1.f - y.y * y.y), v.z * (1.f - y.z * y.z),
+                    v.w * (1.f - y.w * y.w));
   }
 };
 struct EpiPartial {  // split-K partial z
   float* W;
   int M, N;
+  bool vec_ok() const { return ptr16(W) && N % 4 == 0; }
   __device__ void operator()(int m, int n, float v, int z) const {
     W[((size_t)z * M + m) * N + n] = v;
+  }
+  __device__ void vec4(int m, int n, float4 v, int z) const {
+    *reinterpret_cast<float4*>(W + ((size_t)z * M + m) * N + n) = v;
   }
 };
 

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(GT) sgemm_kernel(int M, int N, int K, const fl
 template <bool TA, bool TB, class Epi>
 static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi) {
   if (M <= 0 || N <= 0) return;
-  if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb)) {
+  if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb, epi)) {
     // op(A): TA ? MN-major : K-major;  op(B): TB ? K-major : MN-major
     tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, epi, 1);
     return;
@@ -217,7 +217,7 @@ template <bool TA, bool TB>
 static void gemm_splitk(Ctx* c, Workspace& ws, int M, int N, int K, const float* A, int lda, const float* B,
                         int ldb, float* C, int ldc) {
   if (M <= 0 || N <= 0) return;
-  if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb)) {
+  if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb, EpiStore{C, ldc})) {
     int Z = tc::splits_for(c, M, N, K);
     if (Z == 1) {
       tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, EpiStore{C, ldc}, 1);
@@ -800,5 +800,59 @@ extern "C" ver_status ver_debug_gemm(ver_ctx ctx, int engine, int transA, int tr
   c->precision = p0;
   dC.download(C, (size_t)M * N);
   sync(c);
+  VER_API_END
+}
+
+extern "C" ver_status ver_debug_gemm_time(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K,
+                                          int splitk, int reps, float* ms_out) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  if (M <= 0 || N <= 0 || K <= 0 || reps <= 0) config_error("debug_gemm_time: bad shape");
+  DBuf<float> dA, dB, dC;
+  dA.reserve(c, (size_t)M * K);
+  dB.reserve(c, (size_t)K * N);
+  dC.reserve(c, (size_t)M * N);
+  VER_CUDA(cudaMemsetAsync(dA.p, 0x3f, sizeof(float) * (size_t)M * K, c->stream));
+  VER_CUDA(cudaMemsetAsync(dB.p, 0x3e, sizeof(float) * (size_t)K * N, c->stream));
+  const int lda = transA ? M : K, ldb = transB ? K : N;
+  const bool tc0 = c->tensor_cores;
+  const int p0 = c->precision;
+  c->tensor_cores = engine != 0;
+  c->precision = engine == 2 ? 1 : 0;
+  Workspace ws;
+  ws.ctx = c;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  try {
+    VER_CUDA(cudaEventCreate(&e0));
+    VER_CUDA(cudaEventCreate(&e1));
+    auto go = [&](auto ta, auto tb) {
+      constexpr bool TA = decltype(ta)::value, TB = decltype(tb)::value;
+      for (int r = 0; r <= reps; ++r) {
+        if (r == 1) VER_CUDA(cudaEventRecord(e0, c->stream));
+        if (splitk > 1) gemm_splitk<TA, TB>(c, ws, M, N, K, dA.p, lda, dB.p, ldb, dC.p, N);
+        else gemm<TA, TB>(c, M, N, K, dA.p, lda, dB.p, ldb, EpiStore{dC.p, N});
+      }
+      VER_CUDA(cudaEventRecord(e1, c->stream));
+    };
+    if (!transA && !transB) go(std::false_type{}, std::false_type{});
+    else if (!transA && transB) go(std::false_type{}, std::true_type{});
+    else if (transA && !transB) go(std::true_type{}, std::false_type{});
+    else go(std::true_type{}, std::true_type{});
+    VER_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    VER_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    ms_out[0] = ms / reps;
+  } catch (...) {
+    c->tensor_cores = tc0;
+    c->precision = p0;
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    throw;
+  }
+  c->tensor_cores = tc0;
+  c->precision = p0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   VER_API_END
 }

@@ -40,6 +40,7 @@ struct Workspace {
   DBuf<float> wpart;                                    // head-weight partials
   DBuf<float> is_w;
   DBuf<unsigned> bar;                                   // grid barrier of the recurrence
+  DBuf<long long> trace;                                // VER_REC_TRACE experiments only
   void ensure(const Model& m, size_t S, bool train);
 };
 

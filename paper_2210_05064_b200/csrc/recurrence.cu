@@ -20,6 +20,8 @@
 //   g = dhidden + dh_{t-1};  dn = g(1-z), dz = g(h-n), dpre_n = dn(1-n^2),
 //   dr = dpre_n hUn, dpre_r = dr r(1-r), dpre_z = dz z(1-z)
 // so the backward also needs one barrier per timestep.
+#include <cstdlib>
+
 #include "policy.cuh"
 
 namespace verg {
@@ -319,11 +321,51 @@ __device__ __forceinline__ float reduce_scatter32(float* a, int lane) {
   return a[0];
 }
 
+// Row groups: packed row j of any timestep belongs to row block j % RB for
+// the whole minibatch (rows of step t are a prefix of the rows of t-1, so the
+// interleave stays balanced as bs_t shrinks).  Row j's recurrence only reads
+// row j, so row block rb depends only on its own UB unit-block CTAs: each row
+// block synchronises on its own counter (UB arrivals per step) and the row
+// blocks run independently.  A row block whose rows have all ended leaves.
+__device__ __forceinline__ void group_barrier(unsigned* count, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+constexpr int kBarStride = 32;  // one 128-byte line per row-block counter
+
+__device__ __forceinline__ int rows_of(int B, int rb, int RB) { return B > rb ? (B - rb + RB - 1) / RB : 0; }
+// rows [lo, hi) of step-t rows 0..B-1 owned by row block rb: interleaved
+// (j = rb + RB i, independent row-block groups) or contiguous ranges (all
+// CTAs synchronise every step, VER_REC_MODE=1: A/B measurements)
+struct RowMap {
+  int base, stride, n;
+  __device__ __forceinline__ int row(int i) const { return base + stride * i; }
+};
+__device__ __forceinline__ RowMap rows_in(int inter, int B, int rb, int RB, int lo, int hi) {
+  // the rows j in [lo, hi) with j < B of row block rb
+  if (inter) {
+    const int a = rows_of(lo, rb, RB), b = rows_of(min(hi, B), rb, RB);
+    return RowMap{rb + RB * a, RB, max(0, b - a)};
+  }
+  const int rpc = (B + RB - 1) / RB;
+  const int r0 = max(lo, rb * rpc), r1 = min(min(hi, B), rb * rpc + rpc);
+  return RowMap{r0, 1, max(0, r1 - r0)};
+}
+
 template <int H>
 __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
-    float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar) {
+    float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar,
+    int inter) {
   constexpr int H3 = 3 * H;
   constexpr int KPL = H / 32;
   constexpr int VEC = KPL % 4 == 0 ? 4 : (KPL % 2 == 0 ? 2 : 1);
@@ -333,6 +375,8 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
   const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ua = ub * UPB + 2 * warp;  // units ua, ua + 1
+  unsigned* cnt = inter ? bar + rb * kBarStride : bar;
+  const unsigned arrivals = inter ? UB : gridDim.x;
   float w[NI][VEC][2][3];
 #pragma unroll
   for (int i = 0; i < NI; ++i)
@@ -345,22 +389,31 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
           w[i][j][q][g] = ux[(size_t)(VEC * lane + 32 * VEC * i + j) * H3 + 3 * (ua + q) + g];
   unsigned target = 0;
   for (int t = 0; t < L; ++t) {
-    const int B = bs[t], o = offs[t];
+    const RowMap rm = rows_in(inter, bs[t], rb, RB, 0, 1 << 30);
+    const int nrows = rm.n;
+    if (inter && nrows == 0) break;  // bs is non-increasing: this row block is done
+    if (t > 0) {
+      target += arrivals;
+      group_barrier(cnt, target);
+    }
+    const int o = offs[t];
     const float* hp = (t == 0) ? h0 : hidden + (size_t)offs[t - 1] * H;
-    const int rpc = (B + RB - 1) / RB;
-    const int r0 = rb * rpc, r1 = min(B, r0 + rpc);
-    for (int c0 = r0; c0 < r1; c0 += RCF) {
-      const int nr = min(RCF, r1 - c0);
-      const float4* src = reinterpret_cast<const float4*>(hp + (size_t)c0 * H);
-      for (int i = threadIdx.x; i < nr * H / 4; i += RT) sm4[i] = __ldcg(src + i);
+    for (int c0 = 0; c0 < nrows; c0 += RCF) {
+      const int nr = min(RCF, nrows - c0);
+      const float4* src = reinterpret_cast<const float4*>(hp);
+      for (int i = threadIdx.x; i < nr * H / 4; i += RT) {
+        const int r = i / (H / 4), k = i % (H / 4);
+        sm4[i] = __ldcg(src + (size_t)rm.row(c0 + r) * (H / 4) + k);
+      }
       __syncthreads();
       for (int g0 = 0; g0 < nr; g0 += 4) {
         // gate pre-activations of this lane's (row, unit), loaded ahead of the FMAs
         const int pr = lane >> 3, pq = (lane >> 2) & 1;
         const bool owner = (lane & 3) == 0 && g0 + pr < nr;
+        const size_t p = (size_t)o + rm.row(c0 + g0 + pr);
         float x0 = 0.f, x1 = 0.f, x2 = 0.f;
         if (owner) {
-          const float* x = xp + ((size_t)o + c0 + g0 + pr) * H3 + 3 * (ua + pq);
+          const float* x = xp + p * H3 + 3 * (ua + pq);
           x0 = __ldg(x);
           x1 = __ldg(x + 1);
           x2 = __ldg(x + 2);
@@ -388,7 +441,6 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
         if (owner) {
           const int u = ua + pq;
           const int row = g0 + pr;
-          const size_t p = (size_t)o + c0 + row;
           const float rg = sigm(x0 + mine);
           const float zg = sigm(x1 + sz);
           const float ng = tanhf(x2 + rg * sn);
@@ -406,8 +458,6 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
       }
       __syncthreads();
     }
-    target += gridDim.x;
-    if (t + 1 < L) grid_barrier(bar, target);
   }
 }
 
@@ -416,7 +466,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
     const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
-    unsigned* bar) {
+    unsigned* bar, int inter) {
   constexpr int H3 = 3 * H;
   constexpr int CPL = H3 / 32;  // columns per lane
   constexpr int VEC = CPL % 4 == 0 ? 4 : (CPL % 2 == 0 ? 2 : 1);
@@ -426,6 +476,8 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
   const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ua = ub * UPB + 2 * warp;
+  unsigned* cnt = inter ? bar + rb * kBarStride : bar;
+  const unsigned arrivals = inter ? UB : gridDim.x;
   float w[NI][VEC][2];
 #pragma unroll
   for (int i = 0; i < NI; ++i)
@@ -434,38 +486,47 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
 #pragma unroll
       for (int q = 0; q < 2; ++q) w[i][j][q] = ux[(size_t)(ua + q) * H3 + VEC * lane + 32 * VEC * i + j];
   unsigned target = 0;
+  bool any = false;  // has this row block produced rows yet (then later steps need a barrier)
   {
-    const int B = bs[L - 1], o = offs[L - 1];
-    const int rpc = (B + RB - 1) / RB;
-    const int r0 = rb * rpc, r1 = min(B, r0 + rpc);
-    for (int idx = threadIdx.x; idx < (r1 - r0) * UPB; idx += RT) {
-      const int j = r0 + idx / UPB, l = idx % UPB;
+    const RowMap rm = rows_in(inter, bs[L - 1], rb, RB, 0, 1 << 30);
+    const int n = rm.n, o = offs[L - 1];
+    for (int idx = threadIdx.x; idx < n * UPB; idx += RT) {
+      const int j = rm.row(idx / UPB), l = idx % UPB;
       const size_t p = (size_t)o + j;
       gate_grad(p, ub * UPB + l, H, dhidden[p * H + ub * UPB + l], gates, hun, hprev, dpre, dhu, gz);
     }
+    any = n > 0 || !inter;
   }
-  target += gridDim.x;
-  if (L > 1) grid_barrier(bar, target);
   for (int t = L - 1; t >= 1; --t) {
     const int B = bs[t], Bp = bs[t - 1], o = offs[t], op = offs[t - 1];
-    const int rpc = (Bp + RB - 1) / RB;
-    const int r0 = rb * rpc, r1 = min(Bp, r0 + rpc);
-    const int rc1 = min(r1, B);
-    for (int c0 = r0; c0 < rc1; c0 += RCB) {
-      const int nr = min(RCB, rc1 - c0);
-      const float4* src = reinterpret_cast<const float4*>(dhu + ((size_t)o + c0) * H3);
-      for (int i = threadIdx.x; i < nr * H3 / 4; i += RT) sm4[i] = __ldcg(src + i);
+    const RowMap rc = rows_in(inter, Bp, rb, RB, 0, B);   // rows with a successor at step t
+    const RowMap re = rows_in(inter, Bp, rb, RB, B, Bp);  // rows that end at step t-1
+    const int nc = rc.n;
+    if (inter && nc + re.n == 0) continue;  // nothing yet for this row block (bs grows as t falls)
+    if (any) {
+      target += arrivals;
+      group_barrier(cnt, target);
+    }
+    any = true;
+    // rows with a successor at step t: dh_{t-1} = dhU_t U^T + g_t z_t
+    for (int c0 = 0; c0 < nc; c0 += RCB) {
+      const int nr = min(RCB, nc - c0);
+      const float4* src = reinterpret_cast<const float4*>(dhu + (size_t)o * H3);
+      for (int i = threadIdx.x; i < nr * H3 / 4; i += RT) {
+        const int r = i / (H3 / 4), k = i % (H3 / 4);
+        sm4[i] = __ldcg(src + (size_t)rc.row(c0 + r) * (H3 / 4) + k);
+      }
       __syncthreads();
       for (int g0 = 0; g0 < nr; g0 += 4) {
         // this lane's (row, unit) operands for the gate gradient, loaded ahead of the FMAs
         const int pv = lane >> 2, pr = pv >> 1, pq = pv & 1;
         const bool owner = (lane & 3) == 0 && g0 + pr < nr;
+        const int j = rc.row(c0 + g0 + pr);
         GateIn gin{};
         float gzv = 0.f;
         if (owner) {
-          const size_t pp = (size_t)op + c0 + g0 + pr;
-          gin = gate_load(pp, ua + pq, H, gates, hun, hprev, dhidden);
-          gzv = __ldcg(gz + ((size_t)o + c0 + g0 + pr) * H + ua + pq);
+          gin = gate_load((size_t)op + j, ua + pq, H, gates, hun, hprev, dhidden);
+          gzv = __ldcg(gz + ((size_t)o + j) * H + ua + pq);
         }
         float acc[8];
 #pragma unroll
@@ -477,9 +538,9 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
             float d[VEC];
             load_vec<VEC>(ds + (g0 + r) * H3 + VEC * lane + 32 * VEC * i, d);
 #pragma unroll
-            for (int j = 0; j < VEC; ++j)
+            for (int jj = 0; jj < VEC; ++jj)
 #pragma unroll
-              for (int q = 0; q < 2; ++q) acc[r * 2 + q] = fmaf(d[j], w[i][j][q], acc[r * 2 + q]);
+              for (int q = 0; q < 2; ++q) acc[r * 2 + q] = fmaf(d[jj], w[i][jj][q], acc[r * 2 + q]);
           }
         }
         // reduce-scatter 8 values over lane bits 16, 8, 4; then xor over bits 2, 1
@@ -496,21 +557,371 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_reg(
         float tot = acc[0];
         tot += __shfl_xor_sync(0xffffffffu, tot, 2);
         tot += __shfl_xor_sync(0xffffffffu, tot, 1);
-        if (owner) {  // lane holds value pv = r * 2 + q
-          const size_t pp = (size_t)op + c0 + g0 + pr;
-          gate_grad_v(pp, ua + pq, H, gin.dh + tot + gzv, gin, dpre, dhu, gz);
-        }
+        if (owner)  // lane holds value pv = r * 2 + q
+          gate_grad_v((size_t)op + j, ua + pq, H, gin.dh + tot + gzv, gin, dpre, dhu, gz);
       }
       __syncthreads();
     }
-    const int re0 = max(r0, B);
-    for (int idx = threadIdx.x; idx < max(0, r1 - re0) * UPB; idx += RT) {
-      const int j = re0 + idx / UPB, l = idx % UPB;
+    // rows that end at step t-1 (j >= bs_t): gradient from the heads only
+    for (int idx = threadIdx.x; idx < re.n * UPB; idx += RT) {
+      const int j = re.row(idx / UPB), l = idx % UPB;
       const size_t pp = (size_t)op + j;
       gate_grad(pp, ub * UPB + l, H, dhidden[pp * H + ub * UPB + l], gates, hun, hprev, dpre, dhu, gz);
     }
-    target += gridDim.x;
-    if (t > 1) grid_barrier(bar, target);
+  }
+}
+
+// ------------------------------------------ K-split fast path (H % 256 == 0)
+// The register kernels above give every warp 2 units and the whole K range,
+// so each staged row is read from shared memory by all 8 warps and each
+// value feeds 2 (backward) or 6 (forward) FMAs: the backward is bound by
+// shared-memory bandwidth.  Here warp w owns the K slice [w KW, (w+1) KW)
+// for ALL 16 units of the CTA, lane (cq = lane / 8, kq = lane % 8) owns
+// KL = KW / 8 K indices (k = w KW + 4 kq + 32 i + v) of 4 units (cq): each
+// staged value is read once per CTA (broadcast to the 4 cq lanes) and feeds
+// 12 (forward: 4 units x 3 gates) or 4 (backward) FMAs per lane, i.e. the
+// CTA does 48 / 16 FMAs per shared-memory word instead of 6 / 2.  Partial sums
+// are reduce-scattered over the 8 kq lanes by shuffles, then over the 8 warps
+// through shared memory by the threads that apply the gate math.  Rows are
+// staged with TMA bulk copies (one per row) into a 2-deep ring, so the next
+// chunk of a step lands while this one is computed.
+__device__ __forceinline__ void bulk_row(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mb_init(uint32_t a, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "RW_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra RW_WAIT;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// stage rows map.row(c0 .. c0+nr-1) of src (row stride `row_floats`) into dst
+__device__ __forceinline__ void stage_rows(float* dst, const float* src, int row_floats, const RowMap& rm, int c0,
+                                           int nr, uint32_t mbar) {
+  const uint32_t bytes = (uint32_t)row_floats * 4u;
+  mb_expect(mbar, bytes * (uint32_t)nr);
+  for (int r = 0; r < nr; ++r)
+    bulk_row(su32(dst + (size_t)r * row_floats), src + (size_t)rm.row(c0 + r) * row_floats, bytes, mbar);
+}
+
+__device__ __forceinline__ long long globaltimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int KS_FR = 32;  // forward rows per chunk
+constexpr int KS_BR = 16;  // backward rows per chunk
+
+// values a[0..2n) over the lanes differing in bit s: keep half, add the partner's other half
+template <int N>
+__device__ __forceinline__ void rs_level(float* a, int lane, int s) {
+  const bool up = lane & s;
+#pragma unroll
+  for (int v = 0; v < N; ++v) {
+    const float send = up ? a[v] : a[v + N];
+    const float keep = up ? a[v + N] : a[v];
+    a[v] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+  }
+}
+
+// Forward lane layout: kq = lane % 2, cq = lane / 2 = unit u0 + cq (3 gate
+// columns); lane K indices k = w KW + 8 i + 4 kq + v, so one LDS.128 per lane
+// feeds 12 FMAs and the reduction over kq is one shuffle level.
+template <int H>
+__global__ void __launch_bounds__(RT, 1) gru_fwd_ks(
+    int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
+    const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
+    float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar,
+    long long* trace) {
+  constexpr int H3 = 3 * H;
+  constexpr int KW = H / 8, NI = KW / 8;
+  constexpr int NC = 3 * UPB;  // 48 gate columns of the CTA
+  constexpr int PPT = KS_FR * UPB / RT;  // (row, unit) pairs per thread per chunk
+  extern __shared__ float4 sm4[];
+  float* hs = reinterpret_cast<float*>(sm4);   // [2][KS_FR][H]
+  float* red = hs + 2 * KS_FR * H;             // [8][KS_FR][NC]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 8 * KS_FR * NC);
+  const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kq = lane & 1, cq = lane >> 1;
+  const int u0 = ub * UPB;
+  unsigned* cnt = bar + rb * kBarStride;
+  if (threadIdx.x == 0) {
+    mb_init(su32(&mbar[0]), 1);
+    mb_init(su32(&mbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  float w[NI][4][3];
+#pragma unroll
+  for (int i = 0; i < NI; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int g = 0; g < 3; ++g)
+        w[i][v][g] = ux[(size_t)(warp * KW + 8 * i + 4 * kq + v) * H3 + 3 * (u0 + cq) + g];
+  __syncthreads();
+  unsigned target = 0;
+  uint32_t phase = 0;  // bit b: parity of the next completion of mbar[b]
+  int buf = 0;
+  float xr[PPT][3];
+  // x W + b of this thread's (row, unit) pairs of chunk [c0, c0 + nr): loaded a chunk ahead
+  auto load_x = [&](const RowMap& rm, int o, int c0, int nr) {
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int pidx = threadIdx.x + k * RT;
+      if (pidx < nr * UPB) {
+        const float* x = xp + ((size_t)o + rm.row(c0 + pidx / UPB)) * H3 + 3 * (u0 + pidx % UPB);
+        xr[k][0] = __ldg(x);
+        xr[k][1] = __ldg(x + 1);
+        xr[k][2] = __ldg(x + 2);
+      }
+    }
+  };
+  for (int t = 0; t < L; ++t) {
+    const RowMap rm = rows_in(1, bs[t], rb, RB, 0, 1 << 30);
+    if (rm.n == 0) break;  // bs is non-increasing: this row block is done
+    const int o = offs[t];
+    load_x(rm, o, 0, min(KS_FR, rm.n));
+    if (t > 0) {
+      target += UB;
+      group_barrier(cnt, target);
+    }
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
+    const float* hp = (t == 0) ? h0 : hidden + (size_t)offs[t - 1] * H;
+    const int nch = (rm.n + KS_FR - 1) / KS_FR;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores of other CTAs -> bulk-copy reads
+      stage_rows(hs + buf * KS_FR * H, hp, H, rm, 0, min(KS_FR, rm.n), su32(&mbar[buf]));
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c0 = ch * KS_FR, nr = min(KS_FR, rm.n - c0);
+      if (threadIdx.x == 0 && ch + 1 < nch)
+        stage_rows(hs + (buf ^ 1) * KS_FR * H, hp, H, rm, c0 + KS_FR, min(KS_FR, rm.n - c0 - KS_FR),
+                   su32(&mbar[buf ^ 1]));
+      mb_wait(su32(&mbar[buf]), (phase >> buf) & 1);
+      phase ^= 1u << buf;
+      const float* hc = hs + buf * KS_FR * H;
+      for (int g0 = 0; g0 < nr; g0 += 4) {
+        float acc[12];
+#pragma unroll
+        for (int v = 0; v < 12; ++v) acc[v] = 0.f;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const float4 h4 = *reinterpret_cast<const float4*>(hc + (g0 + r) * H + warp * KW + 8 * i + 4 * kq);
+            const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+              for (int g = 0; g < 3; ++g) acc[r * 3 + g] = fmaf(hv[v], w[i][v][g], acc[r * 3 + g]);
+          }
+        }
+        // reduce over kq: lane keeps values 6 kq .. 6 kq + 5 = rows 2 kq, 2 kq + 1, gates 0..2
+        rs_level<6>(acc, lane, 1);
+        float* dst = red + ((size_t)warp * KS_FR + g0 + 2 * kq) * NC + 3 * cq;
+        dst[0] = acc[0];
+        dst[1] = acc[1];
+        dst[2] = acc[2];
+        dst[NC] = acc[3];
+        dst[NC + 1] = acc[4];
+        dst[NC + 2] = acc[5];
+      }
+      __syncthreads();
+      // gate math: (row, unit) pairs, partials summed over the 8 warps
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int pidx = threadIdx.x + k * RT;
+        if (pidx >= nr * UPB) continue;
+        const int row = pidx / UPB, ul = pidx % UPB;
+        float sr = 0.f, sz = 0.f, sn = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float* rq = red + ((size_t)q * KS_FR + row) * NC + 3 * ul;
+          sr += rq[0];
+          sz += rq[1];
+          sn += rq[2];
+        }
+        const int u = u0 + ul;
+        const size_t p = (size_t)o + rm.row(c0 + row);
+        const float rg = sigm(xr[k][0] + sr);
+        const float zg = sigm(xr[k][1] + sz);
+        const float ng = tanhf(xr[k][2] + rg * sn);
+        const float hprev = hc[row * H + u];
+        hidden[p * H + u] = (1.f - zg) * ng + zg * hprev;
+        if (gates) {
+          float* gp = gates + p * H3 + 3 * u;
+          gp[0] = rg;
+          gp[1] = zg;
+          gp[2] = ng;
+          hun[p * H + u] = sn;
+          hprev_store[p * H + u] = hprev;
+        }
+      }
+      if (ch + 1 < nch) load_x(rm, o, c0 + KS_FR, min(KS_FR, rm.n - c0 - KS_FR));
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
+    int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
+    const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
+    const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
+    unsigned* bar, long long* trace) {
+  constexpr int H3 = 3 * H;
+  constexpr int KW = H3 / 8, KL = KW / 8, NV = KL / 4;
+  extern __shared__ float4 sm4[];
+  float* ds = reinterpret_cast<float*>(sm4);   // [2][KS_BR][H3]
+  float* red = ds + 2 * KS_BR * H3;            // [8][KS_BR][UPB]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 8 * KS_BR * UPB);
+  const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kq = lane & 7, cq = lane >> 3;
+  const int u0 = ub * UPB;
+  unsigned* cnt = bar + rb * kBarStride;
+  if (threadIdx.x == 0) {
+    mb_init(su32(&mbar[0]), 1);
+    mb_init(su32(&mbar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // w[i][v][c] = U[u0 + 4 cq + c, k], k = warp KW + 4 kq + 32 i + v
+  float w[NV][4][4];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        w[i][v][c] = ux[(size_t)(u0 + 4 * cq + c) * H3 + warp * KW + 4 * kq + 32 * i + v];
+  __syncthreads();
+  unsigned target = 0;
+  uint32_t phase = 0;
+  int buf = 0;
+  bool any = false;
+  {
+    const RowMap rm = rows_in(1, bs[L - 1], rb, RB, 0, 1 << 30);
+    const int o = offs[L - 1];
+    for (int idx = threadIdx.x; idx < rm.n * UPB; idx += RT) {
+      const int j = rm.row(idx / UPB), l = idx % UPB;
+      const size_t p = (size_t)o + j;
+      gate_grad(p, u0 + l, H, dhidden[p * H + u0 + l], gates, hun, hprev, dpre, dhu, gz);
+    }
+    any = rm.n > 0;
+  }
+  for (int t = L - 1; t >= 1; --t) {
+    const int B = bs[t], Bp = bs[t - 1], o = offs[t], op = offs[t - 1];
+    const RowMap rc = rows_in(1, Bp, rb, RB, 0, B);   // rows with a successor at step t
+    const RowMap re = rows_in(1, Bp, rb, RB, B, Bp);  // rows that end at step t-1
+    if (rc.n + re.n == 0) continue;
+    if (any) {
+      target += UB;
+      group_barrier(cnt, target);
+    }
+    any = true;
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
+    const float* src = dhu + (size_t)o * H3;
+    const int nch = (rc.n + KS_BR - 1) / KS_BR;
+    if (threadIdx.x == 0 && nch > 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      stage_rows(ds + buf * KS_BR * H3, src, H3, rc, 0, min(KS_BR, rc.n), su32(&mbar[buf]));
+    }
+    // rows that end at step t-1 (j >= bs_t): gradient from the heads only (overlaps the staging)
+    for (int idx = threadIdx.x; idx < re.n * UPB; idx += RT) {
+      const int j = re.row(idx / UPB), l = idx % UPB;
+      const size_t pp = (size_t)op + j;
+      gate_grad(pp, u0 + l, H, dhidden[pp * H + u0 + l], gates, hun, hprev, dpre, dhu, gz);
+    }
+    // this thread's (row, unit) pair of the chunk: forward-pass operands, loaded a chunk ahead
+    GateIn gin{};
+    auto load_g = [&](int c0, int nr) {
+      if (threadIdx.x < nr * UPB)
+        gin = gate_load((size_t)op + rc.row(c0 + threadIdx.x / UPB), u0 + threadIdx.x % UPB, H, gates, hun, hprev,
+                        dhidden);
+    };
+    if (nch > 0) load_g(0, min(KS_BR, rc.n));
+    for (int ch = 0; ch < nch; ++ch) {
+      const int c0 = ch * KS_BR, nr = min(KS_BR, rc.n - c0);
+      if (threadIdx.x == 0 && ch + 1 < nch)
+        stage_rows(ds + (buf ^ 1) * KS_BR * H3, src, H3, rc, c0 + KS_BR, min(KS_BR, rc.n - c0 - KS_BR),
+                   su32(&mbar[buf ^ 1]));
+      float gzv = 0.f;
+      if (threadIdx.x < nr * UPB)
+        gzv = __ldcg(gz + ((size_t)o + rc.row(c0 + threadIdx.x / UPB)) * H + u0 + threadIdx.x % UPB);
+      mb_wait(su32(&mbar[buf]), (phase >> buf) & 1);
+      phase ^= 1u << buf;
+      const float* dc = ds + buf * KS_BR * H3;
+      for (int g0 = 0; g0 < nr; g0 += 4) {
+        float acc[16];
+#pragma unroll
+        for (int v = 0; v < 16; ++v) acc[v] = 0.f;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            const float4 d4 = *reinterpret_cast<const float4*>(dc + (g0 + r) * H3 + warp * KW + 4 * kq + 32 * i);
+            const float dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[r * 4 + c] = fmaf(dv[v], w[i][v][c], acc[r * 4 + c]);
+          }
+        }
+        // reduce-scatter over kq: lane keeps values 2 kq, 2 kq + 1 = row kq / 2, units 2 (kq & 1) + {0, 1}
+        rs_level<8>(acc, lane, 4);
+        rs_level<4>(acc, lane, 2);
+        rs_level<2>(acc, lane, 1);
+        const int row = g0 + (kq >> 1), col = 4 * cq + 2 * (kq & 1);
+        *reinterpret_cast<float2*>(red + ((size_t)warp * KS_BR + row) * UPB + col) = make_float2(acc[0], acc[1]);
+      }
+      __syncthreads();
+      static_assert(KS_BR * UPB == RT, "one (row, unit) pair per thread");
+      if (threadIdx.x < nr * UPB) {
+        const int row = threadIdx.x / UPB, ul = threadIdx.x % UPB;
+        float tot = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot += red[((size_t)q * KS_BR + row) * UPB + ul];
+        gate_grad_v((size_t)op + rc.row(c0 + row), u0 + ul, H, gin.dh + tot + gzv, gin, dpre, dhu, gz);
+      }
+      if (ch + 1 < nch) load_g(c0 + KS_BR, min(KS_BR, rc.n - c0 - KS_BR));
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+}
+
+static size_t ks_fwd_smem(int H) {
+  return sizeof(float) * ((size_t)2 * KS_FR * H + (size_t)8 * KS_FR * 3 * UPB) + 16;
+}
+static size_t ks_bwd_smem(int H) {
+  return sizeof(float) * ((size_t)2 * KS_BR * 3 * H + (size_t)8 * KS_BR * UPB) + 16;
+}
+static const void* pick_fwd_ks(int H) {
+  switch (H) {
+    case 256: return reinterpret_cast<const void*>(gru_fwd_ks<256>);
+    case 512: return reinterpret_cast<const void*>(gru_fwd_ks<512>);
+    default: return nullptr;
+  }
+}
+static const void* pick_bwd_ks(int H) {
+  switch (H) {
+    case 256: return reinterpret_cast<const void*>(gru_bwd_ks<256>);
+    case 512: return reinterpret_cast<const void*>(gru_bwd_ks<512>);
+    default: return nullptr;
   }
 }
 
@@ -547,6 +958,36 @@ static const void* pick_bwd(int H) {
 }
 
 // ------------------------------------------------------------ launch
+// experiments only: VER_REC_TRACE=<file> appends, per K-split launch, the
+// globaltimer (ns) at which CTA 0 starts each timestep, with bs_t
+static void trace_dump(Ctx* c, const char* tag, int L, const int32_t* d_bs, long long* d_tr) {
+  const char* path = getenv("VER_REC_TRACE");
+  if (!path || !d_tr) return;
+  std::vector<long long> tr(L);
+  std::vector<int32_t> b(L);
+  VER_CUDA(cudaMemcpyAsync(tr.data(), d_tr, sizeof(long long) * L, cudaMemcpyDeviceToHost, c->stream));
+  VER_CUDA(cudaMemcpyAsync(b.data(), d_bs, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, c->stream));
+  VER_CUDA(cudaStreamSynchronize(c->stream));
+  FILE* f = fopen(path, "a");
+  if (!f) return;
+  fprintf(f, "%s %d", tag, L);
+  for (int t = 0; t < L; ++t) fprintf(f, " %d:%lld", b[t], tr[t]);
+  fprintf(f, "\n");
+  fclose(f);
+}
+static long long* trace_buf(Ctx* c, Workspace& ws, int L) {
+  if (!getenv("VER_REC_TRACE")) return nullptr;
+  ws.trace.reserve(c, (size_t)L);
+  ws.trace.zero((size_t)L);
+  return ws.trace.p;
+}
+
+static int rec_mode() {
+  // experiments only: 0 = K-split kernels (H = 256, 512), 1 = register kernels with contiguous
+  // rows and a grid-wide barrier, 2 = register kernels with interleaved row-block groups
+  const char* e = getenv("VER_REC_MODE");
+  return e ? atoi(e) : 0;
+}
 static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** args) {
   ScopedEv ev(c, c->rec_tag);
   VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -562,8 +1003,8 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
                             const int32_t* d_offs, Workspace& ws, const float* h0, bool store) {
   const RecGeom g = geom(c, m.H);
   const int grid = g.UB * g.RB;
-  ws.bar.reserve(c, 1);
-  ws.bar.zero(1);
+  ws.bar.reserve(c, (size_t)kBarStride * g.RB);
+  ws.bar.zero((size_t)kBarStride * g.RB);
   int H = m.H, UB = g.UB, RB = g.RB;
   const float* ux = params + m.o_ux;
   const float* xp = ws.xp.p;
@@ -572,9 +1013,17 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   float* hun = ws.hu.p;
   float* hps = ws.hprev.p;
   unsigned* bar = ws.bar.p;
+  if (const void* fn = rec_mode() == 0 ? pick_fwd_ks(m.H) : nullptr) {
+    long long* tr = trace_buf(c, ws, L);
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar, &tr};
+    coop_launch(c, fn, grid, ks_fwd_smem(m.H), args);
+    trace_dump(c, "fwd", L, d_bs, tr);
+    return;
+  }
   if (const void* fn = pick_fwd(m.H)) {
     const size_t smem = sizeof(float) * (size_t)RCF * m.H;
-    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar};
+    int inter = rec_mode() == 2 ? 1 : 0;
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar, &inter};
     coop_launch(c, fn, grid, smem, args);
     return;
   }
@@ -587,8 +1036,8 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
                              const int32_t* d_offs, Workspace& ws) {
   const RecGeom g = geom(c, m.H);
   const int grid = g.UB * g.RB;
-  ws.bar.reserve(c, 1);
-  ws.bar.zero(1);
+  ws.bar.reserve(c, (size_t)kBarStride * g.RB);
+  ws.bar.zero((size_t)kBarStride * g.RB);
   int H = m.H, UB = g.UB, RB = g.RB;
   const float* ux = params + m.o_ux;
   const float* dh = ws.dhidden.p;
@@ -599,9 +1048,17 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
   float* dhu = ws.dhu.p;
   float* gz = ws.g.p;
   unsigned* bar = ws.bar.p;
+  if (const void* fn = rec_mode() == 0 ? pick_bwd_ks(m.H) : nullptr) {
+    long long* tr = trace_buf(c, ws, L);
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar, &tr};
+    coop_launch(c, fn, grid, ks_bwd_smem(m.H), args);
+    trace_dump(c, "bwd", L, d_bs, tr);
+    return;
+  }
   if (const void* fn = pick_bwd(m.H)) {
     const size_t smem = sizeof(float) * (size_t)RCB * 3 * m.H;
-    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar};
+    int inter = rec_mode() == 2 ? 1 : 0;
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar, &inter};
     coop_launch(c, fn, grid, smem, args);
     return;
   }

@@ -13,9 +13,13 @@
 //   * one elected thread issues the MMAs (M = 128, N = 128, K = 8 per
 //     instruction) and commits each stage back to the TMA producer through an
 //     mbarrier; the epilogue warps read the accumulator with tcgen05.ld
-//     (32x32b.x32) and apply bias / tanh / tanh-gradient / split-K partials.
-// Warp roles (192 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer,
-// 2..5 split + epilogue.
+//     (32x32b.x32), transpose 32x32 blocks through shared memory and store
+//     rows as float4 with the fused bias / tanh / tanh-gradient / split-K
+//     functor (coalesced: 4 rows x 128 B per warp store);
+//   * persistent CTAs (one per SM) with the accumulator in four TMEM buffers,
+//     so the next tile's MMAs overlap this tile's epilogue.
+// Warp roles (320 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer,
+// 2..5 3xTF32 operand split, 6..9 accumulator promotion + epilogue.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -29,10 +33,14 @@ namespace tc {
 
 constexpr int BM = 128, BN = 128, BK = 32;  // BK in fp32 elements: one 128-byte swizzle row
 constexpr int STAGES = 3;
-constexpr int THREADS = 192;
+constexpr int SPLIT_WARPS = 4, EPI_WARPS = 4;
+constexpr int THREADS = 32 * (2 + SPLIT_WARPS + EPI_WARPS);  // TMA, MMA, split x4, epilogue x4
 constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB (A and B tiles alike: BM == BN)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A hi, A lo, B hi, B lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int NACC = 4;                      // TMEM accumulator buffers: 4 x 128 columns = all 512
+constexpr int EPI_LD = 36;                   // epilogue staging row stride (floats): float4 writes conflict-free
+constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_LD * 4;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 // The tensor core's fp32 accumulation truncates; so that 3xTF32 stays
 // fp32-grade for long K, each group of PROMOTE K-blocks accumulates into one
 // of two TMEM buffers which the epilogue warps drain into fp32 registers
@@ -113,40 +121,57 @@ __device__ __forceinline__ float rna_tf32(float x) {
 
 // A: MAJ 0 = K-major (M x K row-major), 1 = MN-major (K x M row-major)
 // B: MAJ 0 = K-major (N x K row-major), 1 = MN-major (K x N row-major)
+//
+// Persistent: CTA b walks tiles b, b + grid, ... (n-tile fastest, so the CTAs
+// running at the same time share an A row block in L2).  Every role keeps
+// running counters across tiles, so the smem ring and the four TMEM
+// accumulator buffers flow from one tile into the next: the MMA issuer starts
+// tile i+1 while the epilogue warps are still storing tile i.
 template <int AMAJ, int BMAJ, int SPLIT3, class Epi>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                              const __grid_constant__ CUtensorMap tmB, int M,
-                                                             int N, int K, int kb_per_split, Epi epi) {
+                                                             int N, int K, int kb_per_split, int nsplit, Epi epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  // bars: full[S] split[S] empty[S] acc_full[2] acc_empty[2]; then the TMEM address slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  float* stg_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_BYTES);
+  // bars: full[S] split[S] empty[S] acc_full[NACC] acc_empty[NACC]; then the TMEM address slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * NACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tilesN = (N + BN - 1) / BN, tilesM = (M + BM - 1) / BM;
+  const int ntiles = tilesN * tilesM * nsplit;
   const int nkb_total = (K + BK - 1) / BK;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int kb1 = min(nkb_total, kb0 + kb_per_split);
-  const int nkb = max(0, kb1 - kb0);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
   auto split_bar = [&](int s) { return bar0 + 8 * (STAGES + s); };
   auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES + s); };
   auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES + b); };
-  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES + 2 + b); };
-  const int ngroups = (nkb + PROMOTE - 1) / PROMOTE;
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES + NACC + b); };
   auto tile = [&](int s, int which) { return sbase + s * STAGE_BYTES + which * TILE_BYTES; };  // 0 Ahi 1 Alo 2 Bhi 3 Blo
+  struct Tile {
+    int m0, n0, z, kb0, nkb;
+  };
+  auto decode = [&](int t) {
+    Tile r;
+    const int nt = t % tilesN, q = t / tilesN;
+    r.n0 = nt * BN;
+    r.m0 = (q % tilesM) * BM;
+    r.z = q / tilesM;
+    r.kb0 = r.z * kb_per_split;
+    r.nkb = max(0, min(nkb_total, r.kb0 + kb_per_split) - r.kb0);
+    return r;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(split_bar(s), SPLIT3 ? 4 : 1);
+      mbar_init(split_bar(s), SPLIT_WARPS);
       mbar_init(empty_bar(s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(acc_full(b), 1);
-      mbar_init(acc_empty(b), 4);
+      mbar_init(acc_empty(b), EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -154,7 +179,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN)
+                 "r"(NACC * BN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -166,23 +191,27 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(empty_bar(s), ph ^ 1);
-        mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
-        const int k0 = (kb0 + i) * BK;
-        if (AMAJ == 0) {
-          tma_load_2d(tile(s, 0), &tmA, full_bar(s), k0, m0);
-        } else {
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile T = decode(t);
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(empty_bar(s), ph ^ 1);
+          mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+          const int k0 = (T.kb0 + i) * BK;
+          if (AMAJ == 0) {
+            tma_load_2d(tile(s, 0), &tmA, full_bar(s), k0, T.m0);
+          } else {
 #pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_2d(tile(s, 0) + c * 4096, &tmA, full_bar(s), m0 + 32 * c, k0);
-        }
-        if (BMAJ == 0) {
-          tma_load_2d(tile(s, 2), &tmB, full_bar(s), k0, n0);
-        } else {
+            for (int c = 0; c < BM / 32; ++c) tma_load_2d(tile(s, 0) + c * 4096, &tmA, full_bar(s), T.m0 + 32 * c, k0);
+          }
+          if (BMAJ == 0) {
+            tma_load_2d(tile(s, 2), &tmB, full_bar(s), k0, T.n0);
+          } else {
 #pragma unroll
-          for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &tmB, full_bar(s), n0 + 32 * c, k0);
+            for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &tmB, full_bar(s), T.n0 + 32 * c, k0);
+          }
         }
       }
     }
@@ -193,110 +222,141 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
                            | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16)
                            | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        const int g = i / PROMOTE, buf = g & 1;
-        const bool first = (i % PROMOTE) == 0;
-        if (first && g >= 2) mbar_wait(acc_empty(buf), ((g >> 1) - 1) & 1);
-        if (SPLIT3) mbar_wait(split_bar(s), ph);
-        else mbar_wait(full_bar(s), ph);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(buf * BN);
+      int it = 0, g = 0, buf = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile T = decode(t);
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          const bool first = (i % PROMOTE) == 0;
+          if (first) {
+            buf = g % NACC;
+            const int u = g / NACC;
+            if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
+          }
+          if (SPLIT3) mbar_wait(split_bar(s), ph);
+          else mbar_wait(full_bar(s), ph);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(buf * BN);
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
-          const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
-          const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
-          mma_tf32(d, ah, bh, idesc, acc);
-          if (SPLIT3) {
-            const uint64_t al = operand_desc<AMAJ>(tile(s, 1), kk);
-            const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
-            mma_tf32(d, al, bh, idesc, 1u);
-            mma_tf32(d, ah, bl, idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
+            const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
+            const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+            mma_tf32(d, ah, bh, idesc, acc);
+            if (SPLIT3) {
+              const uint64_t al = operand_desc<AMAJ>(tile(s, 1), kk);
+              const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
+              mma_tf32(d, al, bh, idesc, 1u);
+              mma_tf32(d, ah, bl, idesc, 1u);
+            }
+          }
+          umma_commit(empty_bar(s));
+          if ((i % PROMOTE) == PROMOTE - 1 || i == T.nkb - 1) {
+            umma_commit(acc_full(buf));
+            ++g;
           }
         }
-        umma_commit(empty_bar(s));
-        if ((i % PROMOTE) == PROMOTE - 1 || i == nkb - 1) umma_commit(acc_full(buf));
       }
     }
     __syncwarp();
-  } else {
-    // ---------------- split (main loop) + promotion + epilogue, warps 2..5
-    const int et = threadIdx.x - 64;  // 0..127
-    const int lane_base = 32 * (warp & 3);
-    float sums[BN];
-#pragma unroll
-    for (int j = 0; j < BN; ++j) sums[j] = 0.f;
-    auto drain = [&](int g) {
-      const int buf = g & 1;
-      mbar_wait(acc_full(buf), (g >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int cc = 0; cc < BN / 32; ++cc) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN + cc * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-              "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-              "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-              "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty(buf));
-    };
-    int drained = 0;
-    for (int i = 0; i < nkb; ++i) {
-      // free the accumulator buffer the MMA needs next before splitting its stage
-      if (i % PROMOTE == 0 && i / PROMOTE >= 2) drain(drained++);
-      if (SPLIT3) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(full_bar(s), ph);
-        uint8_t* st = smem + s * STAGE_BYTES;
-        float4* ahi = reinterpret_cast<float4*>(st);
-        float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
-        float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
-        float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+  } else if (warp < 2 + SPLIT_WARPS) {
+    // ---------------- 3xTF32 operand split, warps 2..5
+    if (SPLIT3) {
+      const int et = threadIdx.x - 64;  // 0..127
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const Tile T = decode(t);
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(full_bar(s), ph);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          float4* ahi = reinterpret_cast<float4*>(st);
+          float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
+          float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
+          float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
 #pragma unroll 4
-        for (int q = et; q < TILE_BYTES / 16; q += 128) {
-          float4 x = ahi[q], h, l;
-          h.x = rna_tf32(x.x); l.x = x.x - h.x;
-          h.y = rna_tf32(x.y); l.y = x.y - h.y;
-          h.z = rna_tf32(x.z); l.z = x.z - h.z;
-          h.w = rna_tf32(x.w); l.w = x.w - h.w;
-          ahi[q] = h;
-          alo[q] = l;
-          x = bhi[q];
-          h.x = rna_tf32(x.x); l.x = x.x - h.x;
-          h.y = rna_tf32(x.y); l.y = x.y - h.y;
-          h.z = rna_tf32(x.z); l.z = x.z - h.z;
-          h.w = rna_tf32(x.w); l.w = x.w - h.w;
-          bhi[q] = h;
-          blo[q] = l;
+          for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) {
+            float4 x = ahi[q], h, l;
+            h.x = rna_tf32(x.x); l.x = x.x - h.x;
+            h.y = rna_tf32(x.y); l.y = x.y - h.y;
+            h.z = rna_tf32(x.z); l.z = x.z - h.z;
+            h.w = rna_tf32(x.w); l.w = x.w - h.w;
+            ahi[q] = h;
+            alo[q] = l;
+            x = bhi[q];
+            h.x = rna_tf32(x.x); l.x = x.x - h.x;
+            h.y = rna_tf32(x.y); l.y = x.y - h.y;
+            h.z = rna_tf32(x.z); l.z = x.z - h.z;
+            h.w = rna_tf32(x.w); l.w = x.w - h.w;
+            bhi[q] = h;
+            blo[q] = l;
+          }
+          // generic-proxy smem writes -> visible to the tensor core (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(split_bar(s));
         }
-        // generic-proxy smem writes -> visible to the tensor core (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(split_bar(s));
       }
     }
-    while (drained < ngroups) drain(drained++);
-    // epilogue
-    const int m = m0 + lane_base + lane;
-    if (m < M) {
+  } else {
+    // ---------------- accumulator promotion + epilogue, warps 6..9
+    // TMEM lane quarter of warp w is w % 4; rows lane_base .. lane_base + 31
+    const int lane_base = 32 * (warp & 3);
+    float* stg = stg_all + (warp & 3) * 32 * EPI_LD;
+    int g = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const Tile T = decode(t);
+      const int ngroups = (T.nkb + PROMOTE - 1) / PROMOTE;
+      float sums[BN];
 #pragma unroll
-      for (int j = 0; j < BN; ++j) {
-        const int n = n0 + j;
-        if (n < N) epi(m, n, sums[j], blockIdx.z);
+      for (int j = 0; j < BN; ++j) sums[j] = 0.f;
+      for (int q = 0; q < ngroups; ++q, ++g) {
+        const int buf = g % NACC;
+        mbar_wait(acc_full(buf), (g / NACC) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN + cc * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty(buf));
+      }
+      // epilogue: transpose 32 x 32 blocks through shared memory so each warp
+      // store covers 4 rows x 128 contiguous bytes (float4 per lane)
+      const int rr = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + lane * EPI_LD + 4 * q) =
+              make_float4(sums[cc * 32 + 4 * q], sums[cc * 32 + 4 * q + 1], sums[cc * 32 + 4 * q + 2],
+                          sums[cc * 32 + 4 * q + 3]);
+        __syncwarp();
+        const int n = T.n0 + cc * 32 + c4;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = 4 * k + rr;
+          const int m = T.m0 + lane_base + r;
+          const float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_LD + c4);
+          if (m < M && n < N) epi.vec4(m, n, v, T.z);
+        }
+        __syncwarp();
       }
     }
   }
@@ -304,7 +364,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * BN) : "memory");
   }
 }
 
@@ -339,9 +399,13 @@ inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int b
   return m;
 }
 
-inline bool usable(int M, int N, int K, const float* A, int lda, const float* B, int ldb) {
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  return M >= 64 && N >= 32 && K >= 32 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) && al16(B);
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// the coalesced epilogue stores float4: N, every leading dimension and every
+// epilogue pointer must be 4-float aligned (Epi::vec_ok)
+template <class Epi>
+inline bool usable(int M, int N, int K, const float* A, int lda, const float* B, int ldb, const Epi& epi) {
+  return M >= 64 && N >= 32 && K >= 32 && (N % 4) == 0 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) &&
+         al16(B) && epi.vec_ok();
 }
 
 template <int AMAJ, int BMAJ, class Epi>
@@ -353,10 +417,11 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
   splits = std::max(1, std::min(splits, nkb));
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
-  dim3 grid(cdiv(N, BN), cdiv(M, BM), splits);
+  const long long ntiles = cdiv(N, BN) * cdiv(M, BM) * (long long)splits;
+  const int grid = (int)std::min<long long>(ntiles, c->num_sms);
   auto run = [&](auto kern) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, epi);
+    kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, splits, epi);
     after_launch(c);
   };
   if (c->precision == 0) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
