@@ -164,6 +164,21 @@ struct DBuf {
 
 inline void sync(Ctx* c) { VER_CUDA(cudaStreamSynchronize(c->stream)); }
 
+// L2 prefetch of [p, p + bytes) (bulk-copy engine, no registers held): the
+// range is widened to 16-byte alignment and clipped to [lo, hi).
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes, const void* lo, const void* hi) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  uintptr_t b = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  const uintptr_t l = (reinterpret_cast<uintptr_t>(lo) + 15) & ~uintptr_t(15);
+  const uintptr_t h = reinterpret_cast<uintptr_t>(hi) & ~uintptr_t(15);
+  if (a < l) a = l;
+  if (b > h) b = h;
+  if (b > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(b - a)) : "memory");
+}
+// experiments only: integer tuning knob from the environment
+int env_int(const char* name, int dflt);
+
 inline unsigned cdiv(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 // Launch accounting + error check after every kernel launch.

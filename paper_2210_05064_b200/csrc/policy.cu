@@ -380,6 +380,9 @@ constexpr double kLog2Pi = 1.8378770664093453;
 // Gaussian log-prob, ratio / clip / IS weight / surrogate / value / entropy,
 // and the row's head gradient dhead (A+1) and dhidden = dhead wh^T.
 // Per-block double partials of the loss statistics (deterministic order).
+// NA = A+1 at compile time (common head sizes; every per-head array stays in
+// registers), or 32 with a runtime bound (generic instantiation).
+template <int NA>
 __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
     int S, int H, int A, int continuous, const float* __restrict__ hidden, const float* __restrict__ wh,
     const float* __restrict__ bh, const float* __restrict__ log_std, const float* __restrict__ act_cont,
@@ -399,18 +402,18 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
   double dls = 0.0;  // lane c < A: log_std gradient (continuous)
   for (int p = blockIdx.x * kLossWarps + warp; p < S; p += gridDim.x * kLossWarps) {
     const float* hrow = hidden + (size_t)p * H;
-    float acc[32];
+    float acc[NA];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+    for (int c = 0; c < NA; ++c) acc[c] = 0.f;
     for (int u = lane; u < H; u += 32) {
       const float h = hrow[u];
 #pragma unroll
-      for (int c = 0; c < 32; ++c)
+      for (int c = 0; c < NA; ++c)
         if (c < AH) acc[c] = fmaf(h, s_wh[u * AH + c], acc[c]);
     }
-    double lg[32];
+    double lg[NA];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) {
+    for (int c = 0; c < NA; ++c) {
       if (c < AH) {
         float v = acc[c];
 #pragma unroll
@@ -420,31 +423,44 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
         lg[c] = 0.0;
       }
     }
-    const double value = lg[A];
-    double logp, ent, G[32];
+    double value = 0.0;
 #pragma unroll
-    for (int c = 0; c < 32; ++c) G[c] = 0.0;
+    for (int c = 0; c < NA; ++c)
+      if (c == A) value = lg[c];
+    double logp, ent, mx = 0.0, lse = 0.0;
+    const int a = continuous ? 0 : act_disc[p];
     if (!continuous) {
-      double mx = lg[0];
-      for (int c = 1; c < A; ++c) mx = fmax(mx, lg[c]);
+      mx = lg[0];
+#pragma unroll
+      for (int c = 1; c < NA; ++c)
+        if (c < A) mx = fmax(mx, lg[c]);
       double se = 0.0;
-      for (int c = 0; c < A; ++c) se += exp(lg[c] - mx);
-      const double lse = log(se);
-      const int a = act_disc[p];
-      logp = lg[a] - mx - lse;
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c < A) se += exp(lg[c] - mx);
+      lse = log(se);
+      double lga = 0.0;
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c == a) lga = lg[c];
+      logp = lga - mx - lse;
       ent = 0.0;
-      for (int c = 0; c < A; ++c) {
-        const double lp = lg[c] - mx - lse;
-        ent -= exp(lp) * lp;
-      }
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c < A) {
+          const double lp = lg[c] - mx - lse;
+          ent -= exp(lp) * lp;
+        }
     } else {
       double q = 0.0, sls = 0.0;
-      for (int c = 0; c < A; ++c) {
-        const double ls = log_std[c];
-        const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * exp(-ls);
-        q += z * z;
-        sls += ls;
-      }
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c < A) {
+          const double ls = log_std[c];
+          const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * exp(-ls);
+          q += z * z;
+          sls += ls;
+        }
       logp = -0.5 * q - sls - 0.5 * kLog2Pi * A;
       ent = sls + 0.5 * (1.0 + kLog2Pi) * A;
     }
@@ -470,41 +486,52 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
       const double cm = (ratio >= 1.0 - clip && ratio <= 1.0 + clip) ? 1.0 : 0.0;
       const double dratio = -w * inv_S * (m1 * A_ + (1.0 - m1) * A_ * cm);
       const double dlogp = dratio * ratio;
-      double dh[32];
+      double dh[NA];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) dh[c] = 0.0;
+      for (int c = 0; c < NA; ++c) dh[c] = 0.0;
       if (!continuous) {
-        double mx = lg[0];
-        for (int c = 1; c < A; ++c) mx = fmax(mx, lg[c]);
-        double se = 0.0;
-        for (int c = 0; c < A; ++c) se += exp(lg[c] - mx);
-        const double lse = log(se);
-        const int a = act_disc[p];
-        double sumG = 0.0;
-        for (int c = 0; c < A; ++c) {
-          const double lp = lg[c] - mx - lse;
-          const double pc = exp(lp);
-          G[c] = (c == a ? dlogp : 0.0) + gH * (-pc - pc * lp);
-          sumG += G[c];
-        }
-        for (int c = 0; c < A; ++c) dh[c] = G[c] - exp(lg[c] - mx - lse) * sumG;
-      } else {
-        for (int c = 0; c < A; ++c) {
-          const double ls = log_std[c];
-          const double inv = exp(-ls);
-          const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * inv;
-          dh[c] = dlogp * z * inv;
-          if (lane == c) dls += dlogp * (z * z - 1.0) + gH;
-        }
-      }
-      dh[A] = vcoef * verr * inv_S;
-      if (lane < AH) dhead[(size_t)p * AH + lane] = (float)dh[lane < 32 ? lane : 0];
-      for (int u = lane; u < H; u += 32) {
-        float s = 0.f;
+        double G[NA], sumG = 0.0;
 #pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c < AH) s = fmaf((float)dh[c], s_wh[u * AH + c], s);
-        dhidden[(size_t)p * H + u] = s;
+        for (int c = 0; c < NA; ++c) {
+          G[c] = 0.0;
+          if (c < A) {
+            const double lp = lg[c] - mx - lse;
+            const double pc = exp(lp);
+            G[c] = (c == a ? dlogp : 0.0) + gH * (-pc - pc * lp);
+            sumG += G[c];
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < A) dh[c] = G[c] - exp(lg[c] - mx - lse) * sumG;
+      } else {
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < A) {
+            const double ls = log_std[c];
+            const double inv = exp(-ls);
+            const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * inv;
+            dh[c] = dlogp * z * inv;
+            if (lane == c) dls += dlogp * (z * z - 1.0) + gH;
+          }
+      }
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c == A) dh[c] = vcoef * verr * inv_S;
+      float mine = 0.f;
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c == lane) mine = (float)dh[c];
+      if (lane < AH) dhead[(size_t)p * AH + lane] = mine;
+      float dhf[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) dhf[c] = (float)dh[c];
+      for (int u = lane; u < H; u += 32) {
+        float sacc = 0.f;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < AH) sacc = fmaf(dhf[c], s_wh[u * AH + c], sacc);
+        dhidden[(size_t)p * H + u] = sacc;
       }
     }
   }
@@ -515,7 +542,7 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
   __syncthreads();
   if (threadIdx.x < kLossStats + 32) {
     const int k = threadIdx.x;
-    double s = (k == 6) ? 0.0 : 0.0;
+    double s = 0.0;
     for (int w = 0; w < kLossWarps; ++w) s = (k == 6) ? fmax(s, s_red[w][k]) : s + s_red[w][k];
     part[(size_t)blockIdx.x * (kLossStats + 32) + k] = s;
   }
@@ -558,15 +585,26 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
   const int nblk = std::max(1, std::min((int)cdiv(S, kLossWarps), 4 * c->num_sms));
   ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));
   const size_t smem = sizeof(float) * (size_t)m.H * m.AH;
-  if (smem > 48 * 1024)
-    VER_CUDA(cudaFuncSetAttribute(ppo_loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   float* dhead = ws.dhead.p;  // S x (A+1)
-  ppo_loss_kernel<<<nblk, kLossWarps * 32, smem, c->stream>>>(
-      S, m.H, m.A, m.continuous, ws.hidden.p, params + m.o_wh, params + m.o_bh,
-      m.continuous ? params + m.o_ls : nullptr, a.act_cont, a.act_disc, a.old_logp, a.adv, a.ret, a.frozen_w,
-      a.clip, a.is_cap, a.vcoef, a.alpha, 1.0 / (double)S, dhead, ws.dhidden.p, ws.is_w.p, ws.part.p,
-      want_grads ? 1 : 0);
-  after_launch(c);
+  auto run = [&](auto kern) {
+    if (smem > 48 * 1024)
+      VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<nblk, kLossWarps * 32, smem, c->stream>>>(
+        S, m.H, m.A, m.continuous, ws.hidden.p, params + m.o_wh, params + m.o_bh,
+        m.continuous ? params + m.o_ls : nullptr, a.act_cont, a.act_disc, a.old_logp, a.adv, a.ret, a.frozen_w,
+        a.clip, a.is_cap, a.vcoef, a.alpha, 1.0 / (double)S, dhead, ws.dhidden.p, ws.is_w.p, ws.part.p,
+        want_grads ? 1 : 0);
+    after_launch(c);
+  };
+  switch (m.AH) {
+    case 2: run(ppo_loss_kernel<2>); break;
+    case 3: run(ppo_loss_kernel<3>); break;
+    case 4: run(ppo_loss_kernel<4>); break;
+    case 5: run(ppo_loss_kernel<5>); break;
+    case 7: run(ppo_loss_kernel<7>); break;
+    case 9: run(ppo_loss_kernel<9>); break;
+    default: run(ppo_loss_kernel<32>); break;
+  }
   ppo_loss_final_kernel<<<1, 64, 0, c->stream>>>(ws.part.p, nblk, m.A, m.continuous, 1.0 / (double)S, S,
                                                  a.vcoef, a.alpha, stats,
                                                  want_grads && m.continuous ? grad + m.o_ls : nullptr,

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // util.cu — context lifecycle, error state, NCCL plumbing and the device
 // primitives shared by the hot-path kernels: int32 exclusive scan (3-phase,
 // 1024-thread blocks) and a bitonic sort of unique uint64 keys.
@@ -7,6 +8,11 @@
 #include <mutex>
 
 namespace verg {
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& w) { g_last_error = w; }
