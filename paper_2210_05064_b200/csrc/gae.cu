@@ -87,6 +87,16 @@ __device__ __forceinline__ void gae_wait(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void gae_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+// tile-state flag protocol: payload stores, then a release store of the flag;
+// readers acquire-load the flag before reading the payload
+__device__ __forceinline__ void flag_release(volatile int* f, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(volatile int* f) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
 __device__ __forceinline__ void gae_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kGaeThreads) : "memory"); }
 
 // Persistent CTAs, decoupled look-back, warp-specialised, 3-deep ring.
@@ -180,7 +190,6 @@ __global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
 
   if (warp == kGaeWarps + 1) {
     // ------------------------------------------------- look-back + fix-up
-    const double glf_d = (double)glf;
     for (int it = 0;; ++it) {
       const int s = it % kGaeStages;
       gae_wait(gsm(&s_full[s]), (it / kGaeStages) & 1);
@@ -196,9 +205,8 @@ __global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
         while (!(dbg & 1)) {
           int f;
           do {
-            f = tiles[p].flag;
+            f = flag_acquire(&tiles[p].flag);
           } while (f == 0);
-          __threadfence();
           if (f == 2) {
             carry = fma(acc.a, tiles[p].inc, acc.b);
             break;
@@ -211,16 +219,17 @@ __global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
           --p;
         }
         tiles[tid].inc = fma(hd.sa, carry, hd.sb);
-        __threadfence();
-        tiles[tid].flag = 2;
+        flag_release(&tiles[tid].flag, 2);
       }
       carry = __shfl_sync(0xffffffffu, carry, 0);
       // top segment [seg, hi): partial values (carry 0) staged by the compute warps
       const float* pa = reinterpret_cast<const float*>(stage(s) + kGaeOffR);
       const float* pr = reinterpret_cast<const float*>(stage(s));
       const int seg = max(lo, min(hd.seg, hi));
+      const double lg2 = log2((double)glf);
       for (int i = seg + lane; i < hi; i += 32) {
-        const double cf = pow(glf_d, (double)(hi - i)) * carry;
+        // (gamma lambda)^(hi - i): the top segment has no reset, every a_i = gamma lambda
+        const double cf = exp2(lg2 * (double)(hi - i)) * carry;
         const float av = (float)((double)pa[i - lo] + cf);
         adv[i] = av;
         ret[i] = (float)((double)pr[i - lo] + cf);
@@ -364,13 +373,11 @@ __global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
       const double sa = s_hdr[s].sa, sb = s_hdr[s].sb;
       if (tid == 0) {
         tiles[tid].inc = sb;
-        __threadfence();
-        tiles[tid].flag = 2;
+        flag_release(&tiles[tid].flag, 2);
       } else {
         tiles[tid].a = sa;
         tiles[tid].b = sb;
-        __threadfence();
-        tiles[tid].flag = 1;
+        flag_release(&tiles[tid].flag, 1);
       }
     }
     const Affine after = compose(lane_ex, s_warp[warp]);  // A at hi -> A after this thread's items
