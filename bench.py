@@ -51,6 +51,17 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def dom_traffic(dom):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed `ncu --set full` capture (profiles/traffic.json), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    k = "gru_bwd_ks" if dom == "rec_bwd" else "gru_fwd_ks"
+    return d.get(k, {}).get("dram_bytes_per_launch")
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -283,8 +294,8 @@ def run_ours(args, rank, world):
                        "fresh_steps_per_gpu": fresh, "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"dp{world} (DD-PPO, NCCL AllReduce per minibatch)" if world > 1 else "dp1"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
-                         "frac": achieved_tf / bf16s, "traffic": None,
-                         "kernel": f"{'gru_bwd_reg<512>' if dom == 'rec_bwd' else 'gru_fwd_reg<512>'} "
+                         "frac": achieved_tf / bf16s, "traffic": dom_traffic(dom),
+                         "kernel": f"{'gru_bwd_ks<512>' if dom == 'rec_bwd' else 'gru_fwd_ks<512>'} "
                                    f"(GRU recurrence, fp32 FMA pipe; {n_dom} launches/step, "
                                    f"{dom_ms:.3f} ms avg, {rows_per_launch:.0f} rows x 6H^2 FLOP per launch)",
                          "peak_kind": f"{peaks_kind} bf16 dense sustained",

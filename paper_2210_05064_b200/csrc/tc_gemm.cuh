@@ -5,11 +5,12 @@
 //   * operands are staged by TMA (cp.async.bulk.tensor.2d, 128-byte swizzle)
 //     into a 3-stage shared-memory ring; K-major and MN-major operands are
 //     both native (no transposes in HBM);
-//   * parity mode (3xTF32): the four epilogue warps, idle during the main
-//     loop, split every landed stage in place into hi = rna_tf32(x) and
-//     lo = x - hi, so each K-step issues hi*hi + lo*hi + hi*lo.  Dropping
-//     lo*lo leaves ~2^-22 relative error per product: fp32-grade results,
-//     which is what the 1e-5 parity bound needs;  fast mode issues hi*hi only;
+//   * parity mode (3xTF32): four split warps write lo = x - trunc_tf32(x) of
+//     every landed stage next to it; the landed fp32 tile itself is the hi
+//     operand (the tensor core reads fp32 as tf32 by truncation).  Each K-step
+//     issues hi*hi + lo*hi + hi*lo; dropping lo*lo leaves ~2^-21 relative
+//     error per product: fp32-grade results, which is what the 1e-5 parity
+//     bound needs;  fast mode issues hi*hi only;
 //   * one elected thread issues the MMAs (M = 128, N = 128, K = 8 per
 //     instruction) and commits each stage back to the TMA producer through an
 //     mbarrier; the epilogue warps read the accumulator with tcgen05.ld
@@ -118,6 +119,12 @@ __device__ __forceinline__ float rna_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// lo = x - trunc_tf32(x) (tf32 keeps sign, exponent and the top 10 mantissa
+// bits; the difference is exact in fp32 and the tensor core reads its top 11
+// significant bits).  Rounding lo with cvt.rna would cost ~10% of the split
+// throughput for a term below the dropped lo*lo.
+__device__ __forceinline__ float lo1(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__device__ __forceinline__ float4 lo_tf32(float4 x) { return make_float4(lo1(x.x), lo1(x.y), lo1(x.z), lo1(x.w)); }
 
 // A: MAJ 0 = K-major (M x K row-major), 1 = MN-major (K x M row-major)
 // B: MAJ 0 = K-major (N x K row-major), 1 = MN-major (K x N row-major)
@@ -278,20 +285,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
 #pragma unroll 4
           for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) {
-            float4 x = ahi[q], h, l;
-            h.x = rna_tf32(x.x); l.x = x.x - h.x;
-            h.y = rna_tf32(x.y); l.y = x.y - h.y;
-            h.z = rna_tf32(x.z); l.z = x.z - h.z;
-            h.w = rna_tf32(x.w); l.w = x.w - h.w;
-            ahi[q] = h;
-            alo[q] = l;
-            x = bhi[q];
-            h.x = rna_tf32(x.x); l.x = x.x - h.x;
-            h.y = rna_tf32(x.y); l.y = x.y - h.y;
-            h.z = rna_tf32(x.z); l.z = x.z - h.z;
-            h.w = rna_tf32(x.w); l.w = x.w - h.w;
-            bhi[q] = h;
-            blo[q] = l;
+            // the tensor core reads an fp32 operand as tf32 by truncation, so the
+            // landed tile already is hi = trunc_tf32(x); only lo = x - hi is written
+            alo[q] = lo_tf32(ahi[q]);
+            blo[q] = lo_tf32(bhi[q]);
           }
           // generic-proxy smem writes -> visible to the tensor core (async proxy)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

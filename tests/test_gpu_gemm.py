@@ -23,7 +23,9 @@ def test_tc_gemm_3xtf32(ta, tb, M, N, K):
     for split in (1, 4):
         C3 = V.debug_gemm(A, B, ta, tb, engine=1, splitk=split)
         err3 = np.abs(C3 - ref).max() / scale
-        assert err3 < max(5e-6, 2 * err0), (split, err3, err0)  # fp32-grade
+        # fp32-grade: hi = trunc_tf32(x) (the tensor core's own read of fp32), lo = x - hi;
+        # the dropped lo*lo term is <= 2^-20 |ab| per product
+        assert err3 < max(1e-5, 3 * err0), (split, err3, err0)
     C1 = V.debug_gemm(A, B, ta, tb, engine=2)
     err1 = np.abs(C1 - ref).max() / scale
     assert err1 < 1e-2, err1  # tf32 (10-bit mantissa) inputs
