@@ -301,14 +301,15 @@ __global__ void enc1_kernel(const float* __restrict__ obs, int S, int D, int E, 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
-                    int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store) {
+                    int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store,
+                    const int32_t* h_bs) {
   const int E = m.E, H3 = 3 * m.H;
   enc1_kernel<<<cdiv((size_t)S * E, 256), 256, 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1,
                                                                 params + m.o_b1, ws.e1.p);
   after_launch(c);
   gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2});
   gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx});
-  gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store);
+  gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store, h_bs);
 }
 
 void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out) {
@@ -659,9 +660,10 @@ __global__ void enc1_grad_final_kernel(const float* __restrict__ part, int chunk
 }
 
 void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
-                     const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad) {
+                     const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad,
+                     const int32_t* h_bs) {
   const int E = m.E, H = m.H, H3 = 3 * m.H;
-  gru_backward_recurrence(c, m, params, L, d_bs, d_offs, ws);
+  gru_backward_recurrence(c, m, params, L, d_bs, d_offs, ws, h_bs);
   // weight gradients over all rows
   gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
   gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);

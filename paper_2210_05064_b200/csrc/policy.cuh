@@ -48,15 +48,18 @@ struct Workspace {
 //   obs: S x D (packed), h0: bs[0] x H, d_bs/d_offs: device batch sizes /
 //   offsets of the L timesteps.  store: keep e1/enc/xp/hUn/gates/hprev for
 //   the backward pass.
+//   h_bs: optional host copy of the batch sizes; with it the tail of short
+//   timesteps runs on the single-cluster kernels (recurrence.cu).
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs,
                     const float* h0, int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws,
-                    bool store);
+                    bool store, const int32_t* h_bs = nullptr);
 
 // Persistent recurrence kernels (recurrence.cu)
 void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
-                            const int32_t* d_offs, Workspace& ws, const float* h0, bool store);
+                            const int32_t* d_offs, Workspace& ws, const float* h0, bool store,
+                            const int32_t* h_bs = nullptr);
 void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
-                             const int32_t* d_offs, Workspace& ws);
+                             const int32_t* d_offs, Workspace& ws, const int32_t* h_bs = nullptr);
 
 // Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
 // dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights
@@ -77,7 +80,8 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
 // Backward through the recurrence and the encoder; fills the remaining
 // gradient slots of `grad` (device layout).  Requires policy_forward(store).
 void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
-                     const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad);
+                     const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad,
+                     const int32_t* h_bs = nullptr);
 
 // Per-row log-prob / entropy / value of the heads (nn.cpp:251-278)
 void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float* hidden,

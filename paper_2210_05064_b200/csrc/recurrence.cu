@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
     const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
-    unsigned* bar, long long* trace) {
+    unsigned* bar, long long* trace, int t_start, int do_init) {
   constexpr int H3 = 3 * H;
   constexpr int KW = H3 / 8, KL = KW / 8, NV = KL / 4;
   extern __shared__ float4 sm4[];
@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
   uint32_t phase = 0;
   int buf = 0;
   bool any = false;
-  {
+  if (do_init) {  // step L-1: no carry (else the cluster tail kernel ran steps > t_start)
     const RowMap rm = rows_in(1, bs[L - 1], rb, RB, 0, 1 << 30);
     const int o = offs[L - 1];
     for (int idx = threadIdx.x; idx < rm.n * UPB; idx += RT) {
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
     }
     any = rm.n > 0;
   }
-  for (int t = L - 1; t >= 1; --t) {
+  for (int t = t_start; t >= 1; --t) {
     const int B = bs[t], Bp = bs[t - 1], o = offs[t], op = offs[t - 1];
     const RowMap rc = rows_in(1, Bp, rb, RB, 0, B);   // rows with a successor at step t
     const RowMap re = rows_in(1, Bp, rb, RB, B, Bp);  // rows that end at step t-1
@@ -999,8 +999,356 @@ static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** ar
   after_launch(c);
 }
 
+
+// -------------------------------------- single-cluster tail (H = 512)
+// The last timesteps of a packed minibatch carry few rows (sequences sorted
+// by length: bs_t falls to 1).  There the K-split kernels are bound by the
+// per-step cross-SM handshake (group barrier through L2 + bulk re-staging).
+// For steps with bs_t <= TC_TH one cluster of 16 CTAs holds all of U in
+// registers (CTA r: units 32r .. 32r+31, 96 floats per thread), keeps h_{t-1}
+// (forward) / dhU_t (backward) of all rows in every CTA's shared memory, and
+// pushes each new value to the 16 CTAs with st.shared::cluster; steps are
+// separated by the hardware cluster barrier.  Thread (warp w, lane u): K
+// slice w of unit u; partials reduce over the 16 warps through shared memory.
+constexpr int TC_CL = 16;   // CTAs per cluster (non-portable size)
+constexpr int TC_T = 512;   // threads per CTA
+constexpr int TC_TH = 8;    // steps with at most this many rows run on the cluster
+
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store v at the same shared-memory offset as `local` in every CTA of the cluster
+__device__ __forceinline__ void cl_bcast(const float* local, float v) {
+  const uint32_t a = su32(local);
+#pragma unroll
+  for (int r = 0; r < TC_CL; ++r) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+  }
+}
+
+// copy `n4` float4 of local shared memory at src to offset dst (same layout
+// in every CTA) of all cluster CTAs; item i = (destination, float4)
+__device__ __forceinline__ void cl_push4(const float* src_base, const float* dst_base, int rows, int row_f4,
+                                         int src_ld, int dst_ld) {
+  const int per_dst = rows * row_f4;
+  for (int i = threadIdx.x; i < TC_CL * per_dst; i += blockDim.x) {
+    const int r = i / per_dst, q = i % per_dst, row = q / row_f4, c = q % row_f4;
+    const float4 v = *reinterpret_cast<const float4*>(src_base + row * src_ld + 4 * c);
+    const uint32_t a = su32(dst_base + row * dst_ld + 4 * c);
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(ra), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(TC_T, 1) gru_fwd_tail(
+    int t0, int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, const float* __restrict__ ux,
+    const float* __restrict__ xp, const float* h0, float* hidden, float* __restrict__ gates, float* __restrict__ hun,
+    float* __restrict__ hprev_store, long long* trace) {
+  constexpr int H3 = 3 * H, UT = H / TC_CL, KW = H / (TC_T / 32);
+  static_assert(UT == 32 && KW % 4 == 0, "tail kernel: H = 512");
+  extern __shared__ float4 sm4[];
+  float* hs = reinterpret_cast<float*>(sm4);    // [2][TC_TH][H]
+  float* red = hs + 2 * TC_TH * H;              // [16][TC_TH][3 UT]
+  float* stg = red + (TC_T / 32) * TC_TH * 3 * UT;  // [TC_TH][UT] this CTA's new h slice
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u0 = (int)cl_rank() * UT, u = u0 + lane;
+  float w[KW][3];
+#pragma unroll
+  for (int k = 0; k < KW; ++k)
+#pragma unroll
+    for (int g = 0; g < 3; ++g) w[k][g] = ux[(size_t)(warp * KW + k) * H3 + 3 * u + g];
+  {
+    const int B = bs[t0];
+    const float* hp = t0 == 0 ? h0 : hidden + (size_t)offs[t0 - 1] * H;
+    for (int i = threadIdx.x; i < B * H; i += TC_T) hs[(t0 & 1) * TC_TH * H + i] = __ldcg(hp + i);
+  }
+  cl_sync();
+  const int j = warp;  // gate pair (row warp, unit lane)
+  // x W + b of (row j, unit u) at step t, loaded one step ahead
+  auto load_x = [&](int t, float* x3) {
+    if (t < L && j < bs[t]) {
+      const float* x = xp + ((size_t)offs[t] + j) * H3 + 3 * u;
+      x3[0] = __ldg(x);
+      x3[1] = __ldg(x + 1);
+      x3[2] = __ldg(x + 2);
+    }
+  };
+  float xc[3] = {0.f, 0.f, 0.f}, xn[3] = {0.f, 0.f, 0.f};
+  load_x(t0, xc);
+  for (int t = t0; t < L; ++t) {
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
+    const int B = bs[t], o = offs[t];
+    const float* hc = hs + (t & 1) * TC_TH * H;
+    float* hn = hs + ((t + 1) & 1) * TC_TH * H;
+    load_x(t + 1, xn);
+    const float x0 = xc[0], x1 = xc[1], x2 = xc[2];
+    for (int r0 = 0; r0 < B; r0 += 2) {
+      float a[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+#pragma unroll
+      for (int k = 0; k < KW; k += 4) {
+        const float4 p = *reinterpret_cast<const float4*>(hc + r0 * H + warp * KW + k);
+        const float4 q = *reinterpret_cast<const float4*>(hc + (r0 + 1) * H + warp * KW + k);
+        const float pv[4] = {p.x, p.y, p.z, p.w}, qv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+#pragma unroll
+          for (int g = 0; g < 3; ++g) {
+            a[0][g] = fmaf(pv[v], w[k + v][g], a[0][g]);
+            a[1][g] = fmaf(qv[v], w[k + v][g], a[1][g]);
+          }
+      }
+#pragma unroll
+      for (int g = 0; g < 3; ++g) {
+        red[(warp * TC_TH + r0) * 3 * UT + 3 * lane + g] = a[0][g];
+        red[(warp * TC_TH + r0 + 1) * 3 * UT + 3 * lane + g] = a[1][g];
+      }
+    }
+    __syncthreads();
+    if (j < B) {
+      float sr = 0.f, sz = 0.f, sn = 0.f;
+#pragma unroll
+      for (int q = 0; q < TC_T / 32; ++q) {
+        const float* rq = red + (q * TC_TH + j) * 3 * UT + 3 * lane;
+        sr += rq[0];
+        sz += rq[1];
+        sn += rq[2];
+      }
+      const float rg = sigm(x0 + sr);
+      const float zg = sigm(x1 + sz);
+      const float ng = tanhf(x2 + rg * sn);
+      const float hprev = hc[j * H + u];
+      const float hnew = (1.f - zg) * ng + zg * hprev;
+      const size_t p = (size_t)o + j;
+      hidden[p * H + u] = hnew;
+      if (gates) {
+        float* gp = gates + p * H3 + 3 * u;
+        gp[0] = rg;
+        gp[1] = zg;
+        gp[2] = ng;
+        hun[p * H + u] = sn;
+        hprev_store[p * H + u] = hprev;
+      }
+      stg[j * UT + lane] = hnew;
+    }
+    if (t + 1 < L) {
+      __syncthreads();
+      cl_push4(stg, hn + u0, B, UT / 4, UT, H);
+    }
+    xc[0] = xn[0];
+    xc[1] = xn[1];
+    xc[2] = xn[2];
+    cl_sync();
+  }
+}
+
+// backward: steps t = L-1 .. t_stop+1 (rows of step t-1 <= TC_TH), plus the
+// no-carry step L-1; dhU rows of all 3H columns are pushed to every CTA
+template <int H>
+__global__ void __launch_bounds__(TC_T, 1) gru_bwd_tail(
+    int L, int t_stop, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs,
+    const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
+    const float* __restrict__ hun, const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu,
+    float* __restrict__ gz, long long* trace) {
+  constexpr int H3 = 3 * H, UT = H / TC_CL, KW = H3 / (TC_T / 32);
+  static_assert(UT == 32 && KW % 4 == 0, "tail kernel: H = 512");
+  extern __shared__ float4 sm4[];
+  float* ds = reinterpret_cast<float*>(sm4);    // [2][TC_TH][3H]
+  float* red = ds + 2 * TC_TH * H3;             // [16][TC_TH][UT]
+  float* gzs = red + (TC_T / 32) * TC_TH * UT;  // [2][TC_TH][UT]
+  float* stg = gzs + 2 * TC_TH * UT;            // [TC_TH][3 UT] this CTA's new dhU slice
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u0 = (int)cl_rank() * UT, u = u0 + lane;
+  float w[KW];
+#pragma unroll
+  for (int k = 0; k < KW; ++k) w[k] = ux[(size_t)u * H3 + warp * KW + k];
+  const int j = warp;  // gate pair (row warp, unit lane)
+  // gate gradient of (row j, unit u) at packed row p (operands `in`, loaded
+  // ahead); pushes dhU to every CTA and keeps g z
+  auto gate = [&](size_t p, const GateIn& in, float gsum, float* dnext, float* gznext) {
+    const float g = in.dh + gsum;
+    const float dn = g * (1.f - in.z);
+    const float dz = g * (in.hp - in.n);
+    const float dpn = dn * (1.f - in.n * in.n);
+    const float dr = dpn * in.hn;
+    const float dpr = dr * in.r * (1.f - in.r);
+    const float dpz = dz * in.z * (1.f - in.z);
+    float* d = dpre + p * H3 + 3 * u;
+    d[0] = dpr;
+    d[1] = dpz;
+    d[2] = dpn;
+    float* e = dhu + p * H3 + 3 * u;
+    e[0] = dpr;
+    e[1] = dpz;
+    e[2] = dpn * in.r;
+    gz[p * H + u] = g * in.z;
+    gznext[j * UT + lane] = g * in.z;
+    stg[j * 3 * UT + 3 * lane] = dpr;
+    stg[j * 3 * UT + 3 * lane + 1] = dpz;
+    stg[j * 3 * UT + 3 * lane + 2] = dpn * in.r;
+  };
+  // this step's dhU slices of rows 0..n-1 -> every CTA's buffer dnext
+  auto push = [&](int n, float* dnext) {
+    __syncthreads();
+    cl_push4(stg, dnext + 3 * u0, n, 3 * UT / 4, 3 * UT, H3);
+  };
+  int cur = 0;
+  if (j < bs[L - 1]) {
+    const size_t p = (size_t)offs[L - 1] + j;
+    gate(p, gate_load(p, u, H, gates, hun, hprev, dhidden), 0.f, ds, gzs);
+  }
+  push(bs[L - 1], ds);
+  if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[L - 1] = globaltimer();
+  cl_sync();
+  // forward-pass operands of (row j, unit u) at step t-1, loaded one step ahead
+  GateIn gin{}, gnext{};
+  if (L - 1 > t_stop && j < bs[L - 2]) gin = gate_load((size_t)offs[L - 2] + j, u, H, gates, hun, hprev, dhidden);
+  for (int t = L - 1; t > t_stop; --t) {
+    const int B = bs[t], Bp = bs[t - 1], op = offs[t - 1];
+    const float* dc = ds + cur * TC_TH * H3;
+    if (t - 1 > t_stop && j < bs[t - 2])
+      gnext = gate_load((size_t)offs[t - 2] + j, u, H, gates, hun, hprev, dhidden);
+    for (int r0 = 0; r0 < B; r0 += 2) {
+      float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < KW; k += 4) {
+        const float4 p = *reinterpret_cast<const float4*>(dc + r0 * H3 + warp * KW + k);
+        const float4 q = *reinterpret_cast<const float4*>(dc + (r0 + 1) * H3 + warp * KW + k);
+        a0 = fmaf(p.x, w[k], a0);
+        a1 = fmaf(p.y, w[k + 1], a1);
+        a0 = fmaf(p.z, w[k + 2], a0);
+        a1 = fmaf(p.w, w[k + 3], a1);
+        b0 = fmaf(q.x, w[k], b0);
+        b1 = fmaf(q.y, w[k + 1], b1);
+        b0 = fmaf(q.z, w[k + 2], b0);
+        b1 = fmaf(q.w, w[k + 3], b1);
+      }
+      red[(warp * TC_TH + r0) * UT + lane] = a0 + a1;
+      red[(warp * TC_TH + r0 + 1) * UT + lane] = b0 + b1;
+    }
+    __syncthreads();
+    if (j < Bp) {
+      float tot = 0.f;
+      if (j < B) {
+#pragma unroll
+        for (int q = 0; q < TC_T / 32; ++q) tot += red[(q * TC_TH + j) * UT + lane];
+        tot += gzs[cur * TC_TH * UT + j * UT + lane];
+      }
+      gate((size_t)op + j, gin, tot, ds + (cur ^ 1) * TC_TH * H3, gzs + (cur ^ 1) * TC_TH * UT);
+    }
+    if (t - 1 > t_stop) push(Bp, ds + (cur ^ 1) * TC_TH * H3);
+    gin = gnext;
+    cur ^= 1;
+    cl_sync();
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t - 1] = globaltimer();
+  }
+}
+
+static size_t tail_fwd_smem(int H) {
+  return sizeof(float) *
+         ((size_t)2 * TC_TH * H + (size_t)(TC_T / 32) * TC_TH * 3 * (H / TC_CL) + (size_t)TC_TH * (H / TC_CL));
+}
+static size_t tail_bwd_smem(int H) {
+  return sizeof(float) * ((size_t)2 * TC_TH * 3 * H + (size_t)(TC_T / 32) * TC_TH * (H / TC_CL) +
+                          (size_t)2 * TC_TH * (H / TC_CL) + (size_t)TC_TH * 3 * (H / TC_CL));
+}
+
+// 1 if this device can run one 16-CTA cluster of the tail kernels
+static bool tail_ok(Ctx* c, int H) {
+  static int ok = -1;
+  if (H != 512 || rec_mode() != 0 || env_int("VER_REC_TAIL", 1) == 0) return false;
+  if (ok >= 0) return ok == 1;
+  ok = 0;
+  const void* fns[2] = {reinterpret_cast<const void*>(gru_fwd_tail<512>),
+                        reinterpret_cast<const void*>(gru_bwd_tail<512>)};
+  const size_t sm[2] = {tail_fwd_smem(512), tail_bwd_smem(512)};
+  for (int i = 0; i < 2; ++i) {
+    if (cudaFuncSetAttribute(fns[i], cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm[i]) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(TC_CL);
+    cfg.blockDim = dim3(TC_T);
+    cfg.dynamicSmemBytes = sm[i];
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TC_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fns[i], &cfg) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      return false;
+    }
+  }
+  ok = 1;
+  return true;
+}
+static void tail_launch(Ctx* c, const void* fn, size_t smem, void** args) {
+  ScopedEv ev(c, c->rec_tag);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(TC_CL);
+  cfg.blockDim = dim3(TC_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = TC_CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  VER_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+  after_launch(c);
+}
+// first timestep whose batch is small enough for the cluster tail (L: none).
+// The cluster does the whole matvec on 16 SMs, so its step time grows with the
+// rows (measured on B200 at H = 512: forward 2.0 us at 1 row, 3.7 us at 6;
+// backward 2.2 / 5.3 us) while the K-split kernels take ~3.2 us per short step:
+// the tail takes steps of <= 4 (forward) / <= 3 (backward) rows.
+static int tail_start(const int32_t* h_bs, int L, int th) {
+  if (!h_bs) return L;
+  th = std::min(th, TC_TH);
+  int t0 = L;
+  while (t0 > 0 && h_bs[t0 - 1] <= th) --t0;
+  return t0;
+}
+
 void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
-                            const int32_t* d_offs, Workspace& ws, const float* h0, bool store) {
+                            const int32_t* d_offs, Workspace& ws, const float* h0, bool store,
+                            const int32_t* h_bs) {
+  if (L > 0 && tail_ok(c, m.H)) {
+    const int t0 = tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 4));
+    if (t0 < L) {
+      if (t0 > 0) gru_forward_recurrence(c, m, params, t0, d_bs, d_offs, ws, h0, store, nullptr);
+      int t0_ = t0, L_ = L;
+      const float* ux = params + m.o_ux;
+      const float* xp = ws.xp.p;
+      float* hidden = ws.hidden.p;
+      float* gates = store ? ws.gates.p : nullptr;
+      float* hun = ws.hu.p;
+      float* hps = ws.hprev.p;
+      long long* tr = trace_buf(c, ws, L);
+      void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr};
+      tail_launch(c, reinterpret_cast<const void*>(gru_fwd_tail<512>), tail_fwd_smem(512), args);
+      trace_dump(c, "fwdtail", L, d_bs, tr);
+      return;
+    }
+  }
   const RecGeom g = geom(c, m.H);
   const int grid = g.UB * g.RB;
   ws.bar.reserve(c, (size_t)kBarStride * g.RB);
@@ -1033,7 +1381,31 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
 }
 
 void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
-                             const int32_t* d_offs, Workspace& ws) {
+                             const int32_t* d_offs, Workspace& ws, const int32_t* h_bs) {
+  // steps t > t_stop (rows of t-1 <= TC_TH) on the cluster tail, then t_stop .. 1
+  int t_stop = L, do_init = 1;
+  if (L > 0 && tail_ok(c, m.H)) {
+    const int t0 = tail_start(h_bs, L, env_int("VER_REC_TAIL_BWD", 3));
+    if (t0 < L) {
+      t_stop = t0;
+      int L_ = L, ts = t0;
+      const float* ux = params + m.o_ux;
+      const float* dh = ws.dhidden.p;
+      const float* gates = ws.gates.p;
+      const float* hun = ws.hu.p;
+      const float* hps = ws.hprev.p;
+      float* dpre = ws.dpre.p;
+      float* dhu = ws.dhu.p;
+      float* gz = ws.g.p;
+      long long* tr = trace_buf(c, ws, L);
+      void* args[] = {&L_, &ts, &d_bs, &d_offs, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &tr};
+      tail_launch(c, reinterpret_cast<const void*>(gru_bwd_tail<512>), tail_bwd_smem(512), args);
+      trace_dump(c, "bwdtail", L, d_bs, tr);
+      if (t0 == 0) return;
+      do_init = 0;
+    }
+  }
+  int t_start = std::min(L - 1, t_stop);
   const RecGeom g = geom(c, m.H);
   const int grid = g.UB * g.RB;
   ws.bar.reserve(c, (size_t)kBarStride * g.RB);
@@ -1050,7 +1422,8 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
   unsigned* bar = ws.bar.p;
   if (const void* fn = rec_mode() == 0 ? pick_bwd_ks(m.H) : nullptr) {
     long long* tr = trace_buf(c, ws, L);
-    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &bar, &tr};
+    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux,  &dh,  &gates, &hun,     &hps,
+                    &dpre, &dhu, &gz, &bar, &tr, &t_start, &do_init};
     coop_launch(c, fn, grid, ks_bwd_smem(m.H), args);
     trace_dump(c, "bwd", L, d_bs, tr);
     return;

@@ -5,7 +5,7 @@ for line in open(sys.argv[1]):
     pts = [tuple(map(int, x.split(":"))) for x in rest]
     bs = [p[0] for p in pts]
     ts = [p[1] for p in pts]
-    steps = range(len(ts)) if tag == "fwd" else range(len(ts) - 1, 0, -1)
+    steps = range(len(ts)) if tag.startswith("fwd") else range(len(ts) - 1, -1, -1)
     order = [t for t in steps if ts[t] > 0]
     d = {}
     for a, b in zip(order, order[1:]):
