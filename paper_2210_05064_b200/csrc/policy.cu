@@ -374,6 +374,7 @@ void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float
 
 // ---------------------------------------------------------------- loss
 constexpr int kLossWarps = 8;
+constexpr int kHL = 16;  // fused head gradient: H / 32 <= kHL
 constexpr int kLossStats = 8;  // ws, verr2, H, ratio, clip, w, wmax, (pad)
 constexpr double kLog2Pi = 1.8378770664093453;
 
@@ -384,16 +385,29 @@ constexpr double kLog2Pi = 1.8378770664093453;
 // NA = A+1 at compile time (common head sizes; every per-head array stays in
 // registers), or 32 with a runtime bound (generic instantiation).
 template <int NA>
-__global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
+__global__ void __launch_bounds__(kLossWarps * 32, 2) ppo_loss_kernel(
     int S, int H, int A, int continuous, const float* __restrict__ hidden, const float* __restrict__ wh,
     const float* __restrict__ bh, const float* __restrict__ log_std, const float* __restrict__ act_cont,
     const int32_t* __restrict__ act_disc, const float* __restrict__ old_logp, const float* __restrict__ adv,
     const float* __restrict__ ret, const float* __restrict__ frozen_w, double clip, double is_cap,
     double vcoef, const double* __restrict__ alpha_p, double inv_S, float* __restrict__ dhead,
-    float* __restrict__ dhidden, float* __restrict__ is_w, double* __restrict__ part, int want_grads) {
-  extern __shared__ float s_wh[];  // H x AH
+    float* __restrict__ dhidden, float* __restrict__ is_w, double* __restrict__ part, int want_grads,
+    float* __restrict__ hpart) {
+  extern __shared__ float s_wh[];  // H x AH, then (fused head gradient) H x AH + AH block sums
   __shared__ double s_red[kLossWarps][kLossStats + 32];
   const int AH = A + 1;
+  // fused head gradient (H % 32 == 0, H <= 32 kHL): dwh = hidden^T dhead and
+  // dbh = colsum(dhead) accumulated per lane from the rows' registers
+  const int hl = H / 32;
+  const bool fuse = hpart != nullptr;
+  float* s_hg = s_wh + H * AH;
+  float wacc[kHL][NA], bacc[NA];
+#pragma unroll
+  for (int i = 0; i < kHL; ++i)
+#pragma unroll
+    for (int c = 0; c < NA; ++c) wacc[i][c] = 0.f;
+#pragma unroll
+  for (int c = 0; c < NA; ++c) bacc[c] = 0.f;
   for (int i = threadIdx.x; i < H * AH; i += blockDim.x) s_wh[i] = wh[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -406,11 +420,22 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
     float acc[NA];
 #pragma unroll
     for (int c = 0; c < NA; ++c) acc[c] = 0.f;
-    for (int u = lane; u < H; u += 32) {
-      const float h = hrow[u];
+    float hv[kHL];
+    if (fuse) {
 #pragma unroll
-      for (int c = 0; c < NA; ++c)
-        if (c < AH) acc[c] = fmaf(h, s_wh[u * AH + c], acc[c]);
+      for (int i = 0; i < kHL; ++i) {
+        hv[i] = i < hl ? hrow[lane + 32 * i] : 0.f;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < AH && i < hl) acc[c] = fmaf(hv[i], s_wh[(lane + 32 * i) * AH + c], acc[c]);
+      }
+    } else {
+      for (int u = lane; u < H; u += 32) {
+        const float h = hrow[u];
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < AH) acc[c] = fmaf(h, s_wh[u * AH + c], acc[c]);
+      }
     }
     double lg[NA];
 #pragma unroll
@@ -527,6 +552,14 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
       float dhf[NA];
 #pragma unroll
       for (int c = 0; c < NA; ++c) dhf[c] = (float)dh[c];
+      if (fuse) {
+#pragma unroll
+        for (int c = 0; c < NA; ++c) {
+          bacc[c] += dhf[c];
+#pragma unroll
+          for (int i = 0; i < kHL; ++i) wacc[i][c] = fmaf(hv[i], dhf[c], wacc[i][c]);
+        }
+      }
       for (int u = lane; u < H; u += 32) {
         float sacc = 0.f;
 #pragma unroll
@@ -535,6 +568,27 @@ __global__ void __launch_bounds__(kLossWarps * 32) ppo_loss_kernel(
         dhidden[(size_t)p * H + u] = sacc;
       }
     }
+  }
+  if (fuse && want_grads) {
+    // block sums of the head gradient, warps added in a fixed order (deterministic)
+    for (int i = threadIdx.x; i < H * AH + AH; i += blockDim.x) s_hg[i] = 0.f;
+    for (int w = 0; w < kLossWarps; ++w) {
+      __syncthreads();
+      if (warp == w) {
+#pragma unroll
+        for (int i = 0; i < kHL; ++i)
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (i < hl && c < AH) s_hg[(lane + 32 * i) * AH + c] += wacc[i][c];
+        if (lane == 0)
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (c < AH) s_hg[H * AH + c] += bacc[c];
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < H * AH + AH; i += blockDim.x)
+      hpart[(size_t)blockIdx.x * (H * AH + AH) + i] = s_hg[i];
   }
   // block reduction of the statistics (lane 0 of each warp holds identical st)
   if (lane == 0)
@@ -554,16 +608,24 @@ __global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk,
                                       LossStats* __restrict__ out, float* __restrict__ grad_ls,
                                       float* __restrict__ ent_slot) {
   __shared__ double tot[kLossStats + 32];
-  const int k = threadIdx.x;
-  if (k < kLossStats + 32) {
+  // warp w reduces statistics w, w + 32 over the block partials (lane-strided,
+  // then a fixed shuffle tree: deterministic)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = warp; k < kLossStats + 32; k += blockDim.x >> 5) {
     double s = 0.0;
-    for (int b = 0; b < nblk; ++b) {
+    for (int b = lane; b < nblk; b += 32) {
       const double v = part[(size_t)b * (kLossStats + 32) + k];
       s = (k == 6) ? fmax(s, v) : s + v;
     }
-    tot[k] = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, s, o);
+      s = (k == 6) ? fmax(s, y) : s + y;
+    }
+    if (lane == 0) tot[k] = s;
   }
   __syncthreads();
+  const int k = threadIdx.x;
   if (k == 0) {
     LossStats r;
     r.policy_loss = -tot[0] * inv_S;
@@ -581,11 +643,37 @@ __global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk,
   if (continuous && grad_ls && k < A) grad_ls[k] = (float)tot[kLossStats + k];
 }
 
+// head gradient: sum of the per-block partials -> grad wh, bh.  Block = 32
+// outputs (lanes) x 32 warps; warp w sums partials b = w, w + 32, ...; the 32
+// warp sums are added in a fixed order (deterministic).
+__global__ void __launch_bounds__(1024) head_grad_final_kernel(const float* __restrict__ hpart, int nblk, int n,
+                                                               int nw, float* __restrict__ gwh,
+                                                               float* __restrict__ gbh) {
+  __shared__ float red[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (i < n)
+    for (int b = warp; b < nblk; b += 32) s += hpart[(size_t)b * n + i];
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && i < n) {
+    float t = 0.f;
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
+    if (i < nw) gwh[i] = t;
+    else gbh[i - nw] = t;
+  }
+}
+
 void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossArgs& a, Workspace& ws,
                  float* grad, LossStats* stats, bool want_grads) {
   const int nblk = std::max(1, std::min((int)cdiv(S, kLossWarps), 4 * c->num_sms));
   ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));
-  const size_t smem = sizeof(float) * (size_t)m.H * m.AH;
+  const bool fuse = want_grads && m.H % 32 == 0 && m.H / 32 <= kHL && env_int("VER_LOSS_FUSE", 1);
+  const size_t nhg = (size_t)m.H * m.AH + m.AH;
+  const size_t smem = sizeof(float) * ((size_t)m.H * m.AH + (fuse ? nhg : 0));
+  if (fuse) ws.splitk.reserve(c, (size_t)nblk * nhg);
+  float* hpart = fuse ? ws.splitk.p : nullptr;
   float* dhead = ws.dhead.p;  // S x (A+1)
   auto run = [&](auto kern) {
     if (smem > 48 * 1024)
@@ -594,7 +682,7 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
         S, m.H, m.A, m.continuous, ws.hidden.p, params + m.o_wh, params + m.o_bh,
         m.continuous ? params + m.o_ls : nullptr, a.act_cont, a.act_disc, a.old_logp, a.adv, a.ret, a.frozen_w,
         a.clip, a.is_cap, a.vcoef, a.alpha, 1.0 / (double)S, dhead, ws.dhidden.p, ws.is_w.p, ws.part.p,
-        want_grads ? 1 : 0);
+        want_grads ? 1 : 0, hpart);
     after_launch(c);
   };
   switch (m.AH) {
@@ -606,12 +694,16 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
     case 9: run(ppo_loss_kernel<9>); break;
     default: run(ppo_loss_kernel<32>); break;
   }
-  ppo_loss_final_kernel<<<1, 64, 0, c->stream>>>(ws.part.p, nblk, m.A, m.continuous, 1.0 / (double)S, S,
+  ppo_loss_final_kernel<<<1, 1024, 0, c->stream>>>(ws.part.p, nblk, m.A, m.continuous, 1.0 / (double)S, S,
                                                  a.vcoef, a.alpha, stats,
                                                  want_grads && m.continuous ? grad + m.o_ls : nullptr,
                                                  want_grads ? grad + m.P : nullptr);
   after_launch(c);
-  if (want_grads) {
+  if (fuse) {
+    head_grad_final_kernel<<<cdiv(nhg, 32), 1024, 0, c->stream>>>(hpart, nblk, (int)nhg, m.H * m.AH,
+                                                                  grad + m.o_wh, grad + m.o_bh);
+    after_launch(c);
+  } else if (want_grads) {
     // head weights / biases: dwh = hidden^T dhead, dbh = colsum(dhead)
     gemm_splitk<true, false>(c, ws, m.H, m.AH, S, ws.hidden.p, m.H, dhead, m.AH, grad + m.o_wh, m.AH);
     colsum(c, ws, dhead, S, m.AH, m.AH, grad + m.o_bh);

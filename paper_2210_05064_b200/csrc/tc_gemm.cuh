@@ -401,7 +401,9 @@ inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 // epilogue pointer must be 4-float aligned (Epi::vec_ok)
 template <class Epi>
 inline bool usable(int M, int N, int K, const float* A, int lda, const float* B, int ldb, const Epi& epi) {
-  return M >= 64 && N >= 32 && K >= 32 && (N % 4) == 0 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) &&
+  // TMA boxes (128 or 32 rows) may overhang the tensor: out-of-bounds rows / columns load as zero
+  const int mn_min = env_int("VER_TC_MIN", 1);
+  return M >= mn_min && N >= 16 && K >= 8 && (N % 4) == 0 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) &&
          al16(B) && epi.vec_ok();
 }
 

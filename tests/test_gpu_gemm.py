@@ -5,7 +5,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(128, 128, 32), (256, 384, 512), (16384, 512, 512), (300, 200, 100), (512, 1536, 4096)]
+SHAPES = [(128, 128, 32), (256, 384, 512), (16384, 512, 512), (300, 200, 100), (512, 1536, 4096),
+          (1, 512, 512), (7, 1536, 512), (50, 512, 1536), (33, 20, 12)]
 
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
