@@ -276,7 +276,10 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
   out[n] = s;
 }
 static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, float* out) {
-  const int rows_per = 1024;
+  // enough row chunks for ~4 blocks per SM: each thread walks rows_per / 8 rows
+  const int col_blocks = (int)cdiv(N, 32);
+  int rows_per = 64;
+  while ((int64_t)col_blocks * cdiv(M, rows_per) > 4 * c->num_sms && rows_per < 4096) rows_per *= 2;
   const int chunks = std::max(1, (int)cdiv(M, rows_per));
   ws.splitk.reserve(c, (size_t)chunks * N);
   dim3 grid(cdiv(N, 32), chunks);
@@ -286,16 +289,27 @@ static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, 
   after_launch(c);
 }
 
+constexpr int kMaxD = 8;  // obs_dim bound of the encoder-input kernels (Model::make checks it)
+
 // ----------------------------------------------------------- forward
 // e1 = tanh(obs w1 + b1)  (K = D is tiny: direct)
-__global__ void enc1_kernel(const float* __restrict__ obs, int S, int D, int E, const float* __restrict__ w1,
-                            const float* __restrict__ b1, float* __restrict__ e1) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)S * E) return;
-  const int p = (int)(i / E), k = (int)(i % E);
-  float s = 0.f;
-  for (int d = 0; d < D; ++d) s = fmaf(obs[(size_t)p * D + d], w1[(size_t)d * E + k], s);
-  e1[i] = tanhf(s + b1[k]);
+// block (32 x 8): 32 consecutive features k (w1 / b1 columns in registers) x 8 rows per step
+__global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs, int S, int D, int E,
+                                                   const float* __restrict__ w1, const float* __restrict__ b1,
+                                                   float* __restrict__ e1) {
+  const int k = blockIdx.x * 32 + threadIdx.x;
+  if (k >= E) return;
+  float w[kMaxD];
+#pragma unroll
+  for (int d = 0; d < kMaxD; ++d) w[d] = d < D ? w1[(size_t)d * E + k] : 0.f;
+  const float b = b1[k];
+  for (int p = blockIdx.y * blockDim.y + threadIdx.y; p < S; p += gridDim.y * blockDim.y) {
+    float s = 0.f;
+#pragma unroll
+    for (int d = 0; d < kMaxD; ++d)
+      if (d < D) s = fmaf(__ldg(obs + (size_t)p * D + d), w[d], s);
+    e1[(size_t)p * E + k] = tanhf(s + b);
+  }
 }
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
@@ -304,8 +318,10 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
                     int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store,
                     const int32_t* h_bs) {
   const int E = m.E, H3 = 3 * m.H;
-  enc1_kernel<<<cdiv((size_t)S * E, 256), 256, 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1,
-                                                                params + m.o_b1, ws.e1.p);
+  {
+    dim3 g(cdiv(E, 32), std::max(1u, std::min(cdiv(S, 8), (unsigned)(8 * c->num_sms / std::max(1u, cdiv(E, 32))))));
+    enc1_kernel<<<g, dim3(32, 8), 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
+  }
   after_launch(c);
   gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2});
   gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx});
@@ -713,7 +729,6 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
 // ------------------------------------------------------------ backward
 // db1 and dw1 in one pass over dpre1 (K = S rows, D = obs_dim small):
 // out[0][k] = sum_p dpre1[p,k];  out[1+d][k] = sum_p obs[p,d] dpre1[p,k]
-constexpr int kMaxD = 8;
 __global__ void enc1_grad_partial_kernel(const float* __restrict__ obs, const float* __restrict__ dpre1, int S,
                                          int D, int E, int rows_per, float* __restrict__ part) {
   __shared__ float red[8][33 * (kMaxD + 1)];
