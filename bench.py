@@ -275,14 +275,16 @@ def run_ours(args, rank, world):
 
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
-        # dominant kernel = the larger of the two recurrence kernels (the launch list in
-        # profiles/ ranks them first); its algorithmic work is one H x 3H matvec per
-        # packed row (6 H^2 FLOP), every row once per epoch, so per launch S_mb rows
+        # dominant kernel = the GRU recurrence direction with the larger device time
+        # (the launch list in profiles/ ranks it first): per minibatch one K-split
+        # launch (+ one cluster-tail launch); its algorithmic work is one H x 3H
+        # matvec per packed row (6 H^2 FLOP), every row once per epoch
         dom = max(("rec_bwd", "rec_fwd"), key=lambda k: phase.get(k, 0.0))
+        n_mb = EPOCHS * MINIBATCHES
         n_dom = max(1, phase_n.get(dom, 0))
-        rows_per_launch = fresh * EPOCHS / n_dom
-        dom_flop = 6.0 * H_ * H_ * rows_per_launch
-        dom_ms = phase.get(dom, 0.0) / n_dom
+        rows_per_mb = fresh * EPOCHS / n_mb
+        dom_flop = 6.0 * H_ * H_ * rows_per_mb
+        dom_ms = phase.get(dom, 0.0) / n_mb
         achieved_tf = dom_flop / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
         simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # fp32 FMA pipe peak at max SM clock
         line = {
@@ -295,9 +297,9 @@ def run_ours(args, rank, world):
                        "parallelism": f"dp{world} (DD-PPO, NCCL AllReduce per minibatch)" if world > 1 else "dp1"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
                          "frac": achieved_tf / bf16s, "traffic": dom_traffic(dom),
-                         "kernel": f"{'gru_bwd_ks<512>' if dom == 'rec_bwd' else 'gru_fwd_ks<512>'} "
-                                   f"(GRU recurrence, fp32 FMA pipe; {n_dom} launches/step, "
-                                   f"{dom_ms:.3f} ms avg, {rows_per_launch:.0f} rows x 6H^2 FLOP per launch)",
+                         "kernel": (f"{'gru_bwd_ks<512> + gru_bwd_tail<512>' if dom == 'rec_bwd' else 'gru_fwd_ks<512> + gru_fwd_tail<512>'}"
+                                    f" (GRU recurrence, fp32 FMA pipe; {n_dom} launches/step over {n_mb} minibatches, "
+                                    f"{dom_ms:.3f} ms per minibatch for {rows_per_mb:.0f} rows x 6H^2 FLOP)"),
                          "peak_kind": f"{peaks_kind} bf16 dense sustained",
                          "fp32_simt_peak": simt_peak, "frac_of_fp32_simt": achieved_tf / simt_peak},
             "phases_ms": phase,

@@ -20,13 +20,13 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $OUT/launches.csv python scripts/profile_update.py --updates 2 > $OUT/launches.log 2>&1
 python scripts/launches.py $OUT/launches.csv 0.5 30 > $OUT/launches_summary.txt 2>&1
 cat $OUT/launches_summary.txt
-for k in gru_bwd_reg gru_fwd_reg; do
+for k in gru_bwd_ks gru_fwd_ks; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
   -o $OUT/prof_$k python scripts/profile_update.py --updates 1 > $OUT/prof_$k.log 2>&1
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 20 -c 2 \
   -o $OUT/prof_tc_gemm python scripts/profile_update.py --updates 1 > $OUT/prof_tc_gemm.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"gae_|gather_tiled" -c 4 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"gae_scan|gather_tiled" -c 3 \
   -o $OUT/prof_gae_gather python scripts/profile_c5.py 24 > $OUT/prof_gae_gather.log 2>&1
 fi
 ls -la $OUT
