@@ -621,7 +621,7 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
-constexpr int KS_FR = 32;  // forward rows per chunk
+constexpr int ks_fr(int nw) { return nw == 16 ? 24 : 32; }  // forward rows per chunk (smem)
 constexpr int KS_BR = 16;  // backward rows per chunk
 
 // values a[0..2n) over the lanes differing in bit s: keep half, add the partner's other half
@@ -639,20 +639,22 @@ __device__ __forceinline__ void rs_level(float* a, int lane, int s) {
 // Forward lane layout: kq = lane % 2, cq = lane / 2 = unit u0 + cq (3 gate
 // columns); lane K indices k = w KW + 8 i + 4 kq + v, so one LDS.128 per lane
 // feeds 12 FMAs and the reduction over kq is one shuffle level.
-template <int H>
-__global__ void __launch_bounds__(RT, 1) gru_fwd_ks(
+template <int H, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
     float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar,
     long long* trace) {
-  constexpr int H3 = 3 * H;
-  constexpr int KW = H / 8, NI = KW / 8;
+  constexpr int H3 = 3 * H, NT = NW * 32;
+  constexpr int KS_FR = ks_fr(NW);
+  constexpr int KW = H / NW, NI = KW / 8;
+  static_assert(KW % 8 == 0, "forward K slice");
   constexpr int NC = 3 * UPB;  // 48 gate columns of the CTA
-  constexpr int PPT = KS_FR * UPB / RT;  // (row, unit) pairs per thread per chunk
+  constexpr int PPT = (KS_FR * UPB + NT - 1) / NT;  // (row, unit) pairs per thread per chunk
   extern __shared__ float4 sm4[];
   float* hs = reinterpret_cast<float*>(sm4);   // [2][KS_FR][H]
-  float* red = hs + 2 * KS_FR * H;             // [8][KS_FR][NC]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 8 * KS_FR * NC);
+  float* red = hs + 2 * KS_FR * H;             // [NW][KS_FR][NC]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + NW * KS_FR * NC);
   const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kq = lane & 1, cq = lane >> 1;
@@ -680,7 +682,7 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_ks(
   auto load_x = [&](const RowMap& rm, int o, int c0, int nr) {
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-      const int pidx = threadIdx.x + k * RT;
+      const int pidx = threadIdx.x + k * NT;
       if (pidx < nr * UPB) {
         const float* x = xp + ((size_t)o + rm.row(c0 + pidx / UPB)) * H3 + 3 * (u0 + pidx % UPB);
         xr[k][0] = __ldg(x);
@@ -743,12 +745,12 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_ks(
       // gate math: (row, unit) pairs, partials summed over the 8 warps
 #pragma unroll
       for (int k = 0; k < PPT; ++k) {
-        const int pidx = threadIdx.x + k * RT;
+        const int pidx = threadIdx.x + k * NT;
         if (pidx >= nr * UPB) continue;
         const int row = pidx / UPB, ul = pidx % UPB;
         float sr = 0.f, sz = 0.f, sn = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NW; ++q) {
           const float* rq = red + ((size_t)q * KS_FR + row) * NC + 3 * ul;
           sr += rq[0];
           sz += rq[1];
@@ -777,18 +779,19 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_ks(
   }
 }
 
-template <int H>
-__global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
+template <int H, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) gru_bwd_ks(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
     const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
     unsigned* bar, long long* trace, int t_start, int do_init) {
-  constexpr int H3 = 3 * H;
-  constexpr int KW = H3 / 8, KL = KW / 8, NV = KL / 4;
+  constexpr int H3 = 3 * H, NT = NW * 32;
+  constexpr int KW = H3 / NW, KL = KW / 8, NV = KL / 4;
+  static_assert(KL % 4 == 0, "backward K slice");
   extern __shared__ float4 sm4[];
   float* ds = reinterpret_cast<float*>(sm4);   // [2][KS_BR][H3]
-  float* red = ds + 2 * KS_BR * H3;            // [8][KS_BR][UPB]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + 8 * KS_BR * UPB);
+  float* red = ds + 2 * KS_BR * H3;            // [NW][KS_BR][UPB]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(red + NW * KS_BR * UPB);
   const int ub = blockIdx.x % UB, rb = blockIdx.x / UB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kq = lane & 7, cq = lane >> 3;
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
   if (do_init) {  // step L-1: no carry (else the cluster tail kernel ran steps > t_start)
     const RowMap rm = rows_in(1, bs[L - 1], rb, RB, 0, 1 << 30);
     const int o = offs[L - 1];
-    for (int idx = threadIdx.x; idx < rm.n * UPB; idx += RT) {
+    for (int idx = threadIdx.x; idx < rm.n * UPB; idx += NT) {
       const int j = rm.row(idx / UPB), l = idx % UPB;
       const size_t p = (size_t)o + j;
       gate_grad(p, u0 + l, H, dhidden[p * H + u0 + l], gates, hun, hprev, dpre, dhu, gz);
@@ -841,7 +844,7 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
       stage_rows(ds + buf * KS_BR * H3, src, H3, rc, 0, min(KS_BR, rc.n), su32(&mbar[buf]));
     }
     // rows that end at step t-1 (j >= bs_t): gradient from the heads only (overlaps the staging)
-    for (int idx = threadIdx.x; idx < re.n * UPB; idx += RT) {
+    for (int idx = threadIdx.x; idx < re.n * UPB; idx += NT) {
       const int j = re.row(idx / UPB), l = idx % UPB;
       const size_t pp = (size_t)op + j;
       gate_grad(pp, u0 + l, H, dhidden[pp * H + u0 + l], gates, hun, hprev, dpre, dhu, gz);
@@ -889,12 +892,12 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
         *reinterpret_cast<float2*>(red + ((size_t)warp * KS_BR + row) * UPB + col) = make_float2(acc[0], acc[1]);
       }
       __syncthreads();
-      static_assert(KS_BR * UPB == RT, "one (row, unit) pair per thread");
+      static_assert(KS_BR * UPB <= NT, "one (row, unit) pair per thread");
       if (threadIdx.x < nr * UPB) {
         const int row = threadIdx.x / UPB, ul = threadIdx.x % UPB;
         float tot = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) tot += red[((size_t)q * KS_BR + row) * UPB + ul];
+        for (int q = 0; q < NW; ++q) tot += red[((size_t)q * KS_BR + row) * UPB + ul];
         gate_grad_v((size_t)op + rc.row(c0 + row), u0 + ul, H, gin.dh + tot + gzv, gin, dpre, dhu, gz);
       }
       if (ch + 1 < nch) load_g(c0 + KS_BR, min(KS_BR, rc.n - c0 - KS_BR));
@@ -904,23 +907,31 @@ __global__ void __launch_bounds__(RT, 1) gru_bwd_ks(
   }
 }
 
+// warps per K-split CTA: 8, or 16 sharing the same weights (48 per thread) at
+// H = 512 with VER_REC_NW=16.  Measured equal on B200 (the big steps are not
+// bound by latency hiding), so 8 is the default.
+static int ks_warps(int H) { return (H == 512 && env_int("VER_REC_NW", 8) == 16) ? 16 : 8; }
 static size_t ks_fwd_smem(int H) {
-  return sizeof(float) * ((size_t)2 * KS_FR * H + (size_t)8 * KS_FR * 3 * UPB) + 16;
+  const int nw = ks_warps(H);
+  return sizeof(float) * ((size_t)2 * ks_fr(nw) * H + (size_t)nw * ks_fr(nw) * 3 * UPB) + 16;
 }
 static size_t ks_bwd_smem(int H) {
-  return sizeof(float) * ((size_t)2 * KS_BR * 3 * H + (size_t)8 * KS_BR * UPB) + 16;
+  const int nw = ks_warps(H);
+  return sizeof(float) * ((size_t)2 * KS_BR * 3 * H + (size_t)nw * KS_BR * UPB) + 16;
 }
 static const void* pick_fwd_ks(int H) {
+  if (ks_warps(H) == 16) return reinterpret_cast<const void*>(gru_fwd_ks<512, 16>);
   switch (H) {
-    case 256: return reinterpret_cast<const void*>(gru_fwd_ks<256>);
-    case 512: return reinterpret_cast<const void*>(gru_fwd_ks<512>);
+    case 256: return reinterpret_cast<const void*>(gru_fwd_ks<256, 8>);
+    case 512: return reinterpret_cast<const void*>(gru_fwd_ks<512, 8>);
     default: return nullptr;
   }
 }
 static const void* pick_bwd_ks(int H) {
+  if (ks_warps(H) == 16) return reinterpret_cast<const void*>(gru_bwd_ks<512, 16>);
   switch (H) {
-    case 256: return reinterpret_cast<const void*>(gru_bwd_ks<256>);
-    case 512: return reinterpret_cast<const void*>(gru_bwd_ks<512>);
+    case 256: return reinterpret_cast<const void*>(gru_bwd_ks<256, 8>);
+    case 512: return reinterpret_cast<const void*>(gru_bwd_ks<512, 8>);
     default: return nullptr;
   }
 }
@@ -988,14 +999,14 @@ static int rec_mode() {
   const char* e = getenv("VER_REC_MODE");
   return e ? atoi(e) : 0;
 }
-static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** args) {
+static void coop_launch(Ctx* c, const void* fn, int grid, size_t smem, void** args, int threads = RT) {
   ScopedEv ev(c, c->rec_tag);
   VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, RT, smem));
+  VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
   if (per_sm * c->num_sms < grid)
     config_error("recurrence: grid does not fit co-resident (hidden dim too large for this build)");
-  VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(RT), args, smem, c->stream));
+  VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, c->stream));
   after_launch(c);
 }
 
@@ -1364,7 +1375,7 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   if (const void* fn = rec_mode() == 0 ? pick_fwd_ks(m.H) : nullptr) {
     long long* tr = trace_buf(c, ws, L);
     void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar, &tr};
-    coop_launch(c, fn, grid, ks_fwd_smem(m.H), args);
+    coop_launch(c, fn, grid, ks_fwd_smem(m.H), args, 32 * ks_warps(m.H));
     trace_dump(c, "fwd", L, d_bs, tr);
     return;
   }
@@ -1424,7 +1435,7 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
     long long* tr = trace_buf(c, ws, L);
     void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux,  &dh,  &gates, &hun,     &hps,
                     &dpre, &dhu, &gz, &bar, &tr, &t_start, &do_init};
-    coop_launch(c, fn, grid, ks_bwd_smem(m.H), args);
+    coop_launch(c, fn, grid, ks_bwd_smem(m.H), args, 32 * ks_warps(m.H));
     trace_dump(c, "bwd", L, d_bs, tr);
     return;
   }
