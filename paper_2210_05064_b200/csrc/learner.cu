@@ -55,6 +55,7 @@ struct Learner {
   DBuf<int> flags;           // [0] non-finite parameters
   Workspace ws, wr;          // minibatch / h0-replay workspaces
   DBuf<float> h0s;           // sorted h0 of the current minibatch
+  DBuf<float> robs, rh0;     // split-tail replay inputs
   // per-phase device timing of the last update (events on ctx->stream)
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> evlog;
   std::vector<std::pair<int, cudaEvent_t>> open;
@@ -158,11 +159,11 @@ __global__ void stats_accum_kernel(double* __restrict__ acc, const LossStats* __
 // steps of act() from parent_start_offset with the current parameters; all
 // tails of a minibatch replay together as one packed GRU forward sorted by
 // skip (descending), so the replay costs max(skip) recurrent steps.
-static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, float* h0s) {
-  Ctx* c = Ln.ctx;
-  const int H = V.hidden_dim;
-  h0_gather_kernel<<<cdiv((size_t)P.k * H, 256), 256, 0, c->stream>>>(P.seqs.p, P.k, V.h0.p, H, h0s);
-  after_launch(c);
+// host plan of the replay (depends on the pack only, not on the parameters):
+// built once per pack, before the minibatch loop, so the loop has no host sync
+static void prepare_replay(Ctx* c, DPacked& P) {
+  if (P.rp_ready) return;
+  P.rp_ready = true;
   struct Tail {
     int j, skip, parent, h0i;
   };
@@ -170,6 +171,7 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
   for (int j = 0; j < P.k; ++j)
     if (P.h_seqs[j].skip > 0)
       tails.push_back({j, P.h_seqs[j].skip, P.h_seqs[j].parent_start_offset, P.h_seqs[j].h0_index});
+  P.rp_n = (int)tails.size();
   if (tails.empty()) return;
   std::stable_sort(tails.begin(), tails.end(), [](const Tail& a, const Tail& b) { return a.skip > b.skip; });
   const int n = (int)tails.size();
@@ -191,24 +193,32 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
   }
   std::copy(offs.begin(), offs.end(), meta.begin() + 4 * n);
   std::copy(bs.begin(), bs.end(), meta.begin() + 4 * n + L);
-  DBuf<int32_t> dm;
-  dm.reserve(c, meta.size());
-  int32_t* pin = static_cast<int32_t*>(c->pinned_buf(sizeof(int32_t) * meta.size()));
-  std::copy(meta.begin(), meta.end(), pin);
-  dm.upload(pin, meta.size());
+  P.rp_L = L;
+  P.rp_R = R;
+  P.rp_meta.reserve(c, meta.size());
+  P.rp_meta.upload(meta.data(), meta.size());  // pageable source: consumed before the call returns
+}
+
+static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, float* h0s) {
+  Ctx* c = Ln.ctx;
+  const int H = V.hidden_dim;
+  h0_gather_kernel<<<cdiv((size_t)P.k * H, 256), 256, 0, c->stream>>>(P.seqs.p, P.k, V.h0.p, H, h0s);
+  after_launch(c);
+  prepare_replay(c, P);
+  if (P.rp_n == 0) return;
+  const int n = P.rp_n, L = P.rp_L, R = P.rp_R;
+  const int32_t* dm = P.rp_meta.p;
   Ln.wr.ensure(Ln.m, R, false);
-  DBuf<float> robs, rh0;
-  robs.reserve(c, (size_t)R * V.obs_dim);
-  rh0.reserve(c, (size_t)n * H);
-  replay_obs_kernel<<<cdiv(R, 256), 256, 0, c->stream>>>(dm.p + 4 * n, L, dm.p, R, V.obs.p, V.obs_dim, robs.p);
+  Ln.robs.reserve(c, (size_t)R * V.obs_dim);
+  Ln.rh0.reserve(c, (size_t)n * H);
+  replay_obs_kernel<<<cdiv(R, 256), 256, 0, c->stream>>>(dm + 4 * n, L, dm, R, V.obs.p, V.obs_dim, Ln.robs.p);
   after_launch(c);
-  replay_h0_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm.p + n, n, V.h0.p, H, rh0.p);
+  replay_h0_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm + n, n, V.h0.p, H, Ln.rh0.p);
   after_launch(c);
-  policy_forward(c, Ln.m, params, R, robs.p, rh0.p, L, dm.p + 4 * n + L, dm.p + 4 * n, Ln.wr, false);
-  replay_final_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm.p + 2 * n, dm.p + 3 * n, n,
+  policy_forward(c, Ln.m, params, R, Ln.robs.p, Ln.rh0.p, L, dm + 4 * n + L, dm + 4 * n, Ln.wr, false);
+  replay_final_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm + 2 * n, dm + 3 * n, n,
                                                                       Ln.wr.hidden.p, H, h0s);
   after_launch(c);
-  sync(c);  // pinned staging reused by the next call
 }
 
 // ---------------------------------------------------------- minibatch
@@ -278,20 +288,21 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
   Ln.mark_end();
   const double lr = cosine_lr(Ln.base_lr, Ln.total_steps, Ln.consumed);
   Ln.acc.zero(10);
+  // every epoch's split and pack (and replay plan) first: they depend on the
+  // view and the seeds only, and their host round trips then do not stall
+  // the minibatch loop, which runs without a host sync
+  std::vector<std::unique_ptr<DPacked>> packs;
+  Ln.mark_begin(PH_SAMPLER);
   for (int epoch = 0; epoch < Ln.cfg.epochs; ++epoch) {
     const uint64_t seed = mix64(mix64(Ln.run_seed, (uint64_t)Ln.update_index), (uint64_t)epoch);
-    Ln.mark_begin(PH_SAMPLER);
-    DGroups* G = split_minibatches(V, Ln.cfg.minibatches, seed);
-    Ln.mark_end();
-    std::unique_ptr<DGroups> gguard(G);
+    std::unique_ptr<DGroups> G(split_minibatches(V, Ln.cfg.minibatches, seed));
     for (int b = 0; b < G->B; ++b) {
-      Ln.mark_begin(PH_SAMPLER);
-      DPacked* P = pack_pieces(V, G->pieces.p + G->gstart[b], G->gstart[b + 1] - G->gstart[b]);
-      Ln.mark_end();
-      std::unique_ptr<DPacked> pguard(P);
-      run_minibatch(Ln, V, *P, lr);
+      packs.emplace_back(pack_pieces(V, G->pieces.p + G->gstart[b], G->gstart[b + 1] - G->gstart[b]));
+      prepare_replay(c, *packs.back());
     }
   }
+  Ln.mark_end();
+  for (auto& P : packs) run_minibatch(Ln, V, *P, lr);
   // one read-back per update
   double* h = static_cast<double*>(c->pinned_buf(sizeof(double) * 12));
   VER_CUDA(cudaMemcpyAsync(h, Ln.acc.p, sizeof(double) * 10, cudaMemcpyDeviceToHost, c->stream));

@@ -40,6 +40,11 @@ struct DPacked {
   std::vector<int32_t> h_bs, h_offs;
   // pieces needing an h0 replay (skip > 0), host copy of sorted descriptors
   std::vector<ver_seq_desc> h_seqs;
+  // split-tail replay plan (learner.cu prepare_replay): n tails, L replay
+  // steps, R replay rows; meta = parent[n] h0i[n] last_row[n] j[n] offs[L] bs[L]
+  bool rp_ready = false;
+  int rp_n = 0, rp_L = 0, rp_R = 0;
+  DBuf<int32_t> rp_meta;
 };
 
 // pack + gather of an explicit device array of k pieces (deal order)
