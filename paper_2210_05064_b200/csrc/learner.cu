@@ -56,6 +56,16 @@ struct Learner {
   Workspace ws, wr;          // minibatch / h0-replay workspaces
   DBuf<float> h0s;           // sorted h0 of the current minibatch
   DBuf<float> robs, rh0;     // split-tail replay inputs
+  // sampler context: splits / packs run on their own stream, so pack b+1 (with
+  // its host round trips) overlaps minibatch b on ctx->stream
+  Ctx side{};
+  ~Learner() {
+    if (side.stream) {
+      cudaStreamSynchronize(side.stream);
+      cudaStreamDestroy(side.stream);
+    }
+    if (side.pinned) cudaFreeHost(side.pinned);
+  }
   // per-phase device timing of the last update (events on ctx->stream)
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> evlog;
   std::vector<std::pair<int, cudaEvent_t>> open;
@@ -288,21 +298,47 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
   Ln.mark_end();
   const double lr = cosine_lr(Ln.base_lr, Ln.total_steps, Ln.consumed);
   Ln.acc.zero(10);
-  // every epoch's split and pack (and replay plan) first: they depend on the
-  // view and the seeds only, and their host round trips then do not stall
-  // the minibatch loop, which runs without a host sync
+  // Splits, packs and replay plans depend on the view and the seeds only.  They
+  // run on the sampler stream (Ln.side): while the host waits on pack b+1's
+  // round trips, minibatch b runs on ctx->stream, which waits only on the
+  // event of its own pack.  The minibatch loop has no host sync.
+  if (!Ln.side.stream) {
+    Ln.side.device = c->device;
+    Ln.side.num_sms = c->num_sms;
+    Ln.side.precision = c->precision;
+    Ln.side.tensor_cores = c->tensor_cores;
+    VER_CUDA(cudaStreamCreateWithFlags(&Ln.side.stream, cudaStreamNonBlocking));
+  }
+  Ctx* sc = &Ln.side;
+  auto record_wait = [](cudaStream_t from, cudaStream_t to) {
+    cudaEvent_t e;
+    VER_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    VER_CUDA(cudaEventRecord(e, from));
+    VER_CUDA(cudaStreamWaitEvent(to, e, 0));
+    VER_CUDA(cudaEventDestroy(e));
+  };
+  record_wait(c->stream, sc->stream);  // GAE (advantages / returns) before the gathers
+  struct CtxSwap {  // split / pack allocate and launch through V.ctx
+    DView& V;
+    Ctx* keep;
+    ~CtxSwap() { V.ctx = keep; }
+  } swap{V, V.ctx};
   std::vector<std::unique_ptr<DPacked>> packs;
-  Ln.mark_begin(PH_SAMPLER);
   for (int epoch = 0; epoch < Ln.cfg.epochs; ++epoch) {
     const uint64_t seed = mix64(mix64(Ln.run_seed, (uint64_t)Ln.update_index), (uint64_t)epoch);
+    V.ctx = sc;
     std::unique_ptr<DGroups> G(split_minibatches(V, Ln.cfg.minibatches, seed));
     for (int b = 0; b < G->B; ++b) {
+      V.ctx = sc;
       packs.emplace_back(pack_pieces(V, G->pieces.p + G->gstart[b], G->gstart[b + 1] - G->gstart[b]));
-      prepare_replay(c, *packs.back());
+      prepare_replay(sc, *packs.back());
+      V.ctx = c;
+      record_wait(sc->stream, c->stream);
+      run_minibatch(Ln, V, *packs.back(), lr);
     }
   }
-  Ln.mark_end();
-  for (auto& P : packs) run_minibatch(Ln, V, *P, lr);
+  c->launches += sc->launches;
+  sc->launches = 0;
   // one read-back per update
   double* h = static_cast<double*>(c->pinned_buf(sizeof(double) * 12));
   VER_CUDA(cudaMemcpyAsync(h, Ln.acc.p, sizeof(double) * 10, cudaMemcpyDeviceToHost, c->stream));
