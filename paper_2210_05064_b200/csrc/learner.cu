@@ -245,7 +245,7 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   Ln.mark_begin(PH_FORWARD);
   c->rec_tag = PH_REC_FWD;
   policy_forward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, true,
-                 P.h_bs.data());
+                 P.h_bs.data(), P.h_offs.data());
   c->rec_tag = -1;
   Ln.mark_end();
   LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, nullptr,
@@ -256,7 +256,7 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   Ln.mark_begin(PH_BACKWARD);
   c->rec_tag = PH_REC_BWD;
   policy_backward(c, m, Ln.params.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, Ln.grad.p,
-                  P.h_bs.data());
+                  P.h_bs.data(), P.h_offs.data());
   c->rec_tag = -1;
   Ln.mark_end();
   const bool ar = Ln.allreduce && c->comm && c->nranks > 1;
@@ -466,12 +466,14 @@ ver_status ver_ppo_loss(ver_ctx ctx, const ver_model_config* mc, const float* pa
   Workspace ws;
   ws.ctx = c;
   ws.ensure(m, S, true);
-  policy_forward(c, m, dparams.p, S, P.obs.p, h0.p, P.max_len, P.bs.p, P.offs.p, ws, true, P.h_bs.data());
+  policy_forward(c, m, dparams.p, S, P.obs.p, h0.p, P.max_len, P.bs.p, P.offs.p, ws, true, P.h_bs.data(),
+                 P.h_offs.data());
   LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, frozen_w ? fw.p : nullptr,
               cfg->clip, cfg->is_cap, cfg->value_loss_coef, dalpha.p};
   policy_loss(c, m, dparams.p, S, la, ws, grad.p, st.p, want_grads != 0);
   if (want_grads)
-    policy_backward(c, m, dparams.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, ws, grad.p, P.h_bs.data());
+    policy_backward(c, m, dparams.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, ws, grad.p, P.h_bs.data(),
+                    P.h_offs.data());
   LossStats hs;
   st.download(&hs, 1);
   std::vector<float> g(m.P);

@@ -316,7 +316,7 @@ __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-
 
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
                     int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store,
-                    const int32_t* h_bs) {
+                    const int32_t* h_bs, const int32_t* h_offs) {
   const int E = m.E, H3 = 3 * m.H;
   {
     dim3 g(cdiv(E, 32), std::max(1u, std::min(cdiv(S, 8), (unsigned)(8 * c->num_sms / std::max(1u, cdiv(E, 32))))));
@@ -325,7 +325,144 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
   after_launch(c);
   gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2});
   gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx});
-  gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store, h_bs);
+  gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store, h_bs, h_offs);
+}
+
+// ------------------------------------------------ big recurrence steps
+// Steps whose batch has >= kBigRows rows (a prefix of the timesteps: bs is
+// non-increasing) run as one GEMM per step on the tensor cores instead of the
+// persistent FMA kernel (recurrence.cu), whose step time grows with the rows
+// (~36 us at 623 rows, H = 512) while a 3xTF32 tcgen05 GEMM of the step takes
+// ~8 us up to 640 rows.
+int gru_big_steps(Ctx* c, const Model& m, const int32_t* h_bs, int L, bool backward) {
+  // thresholds measured on B200 at C2 (scripts/ab_bench.py sweeps)
+  const int min_rows = backward ? env_int("VER_REC_BIG_BWD", 200) : env_int("VER_REC_BIG_FWD", 250);
+  if (!h_bs || !c->tensor_cores || m.H % 32 != 0 || min_rows <= 0) return 0;
+  int t = 0;
+  while (t < L && h_bs[t] >= min_rows) ++t;
+  return t;
+}
+
+// forward gates of rows j < B at step t: hU = h_{t-1} U (GEMM), then
+// r = s(xr + hUr), z = s(xz + hUz), n = tanh(xn + r hUn), h = (1-z) n + z h_{t-1}
+// hU: Z split-K partials of B x 3H, summed here in a fixed order
+__global__ void gru_gate_fwd_kernel(int B, int H, int Z, const float* __restrict__ hU,
+                                    const float* __restrict__ xp, const float* __restrict__ hp,
+                                    float* __restrict__ hid, float* __restrict__ gates, float* __restrict__ hun,
+                                    float* __restrict__ hprev_store) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  const size_t g3 = (size_t)j * 3 * H + 3 * u;
+  const size_t zs = (size_t)B * 3 * H;
+  float sr = 0.f, sz = 0.f, sn = 0.f;
+  for (int z = 0; z < Z; ++z) {
+    sr += hU[z * zs + g3];
+    sz += hU[z * zs + g3 + 1];
+    sn += hU[z * zs + g3 + 2];
+  }
+  const float rg = 1.f / (1.f + expf(-(xp[g3] + sr)));
+  const float zg = 1.f / (1.f + expf(-(xp[g3 + 1] + sz)));
+  const float ng = tanhf(xp[g3 + 2] + rg * sn);
+  const float hprev = hp[i];
+  hid[i] = (1.f - zg) * ng + zg * hprev;
+  if (gates) {
+    gates[g3] = rg;
+    gates[g3 + 1] = zg;
+    gates[g3 + 2] = ng;
+    hun[i] = sn;
+    hprev_store[i] = hprev;
+  }
+}
+
+void gru_forward_big(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
+                     const int32_t* h_offs, Workspace& ws, const float* h0, bool store) {
+  const int H = m.H, H3 = 3 * H;
+  if (t_end <= 0) return;
+  for (int t = 0; t < t_end; ++t) {
+    const int B = h_bs[t];
+    const size_t o = (size_t)h_offs[t];
+    const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
+    // hU = h_{t-1}[0:B] U (M = B, N = 3H, K = H), split-K to fill the SMs
+    const int tiles = (int)(cdiv(H3, tc::BN) * cdiv(B, tc::BM));
+    const int nkb = (H + tc::BK - 1) / tc::BK;
+    int Z = std::max(1, std::min(c->num_sms / std::max(1, tiles), std::max(1, nkb / 4)));
+    const int per = (nkb + Z - 1) / Z;
+    Z = (nkb + per - 1) / per;
+    ws.step.reserve(c, (size_t)Z * B * H3);
+    if (c->tensor_cores && tc::usable(B, H3, H, hp, H, params + m.o_ux, H3, EpiPartial{ws.step.p, B, H3})) {
+      tc::launch<0, 1>(c, B, H3, H, hp, H, params + m.o_ux, H3, EpiPartial{ws.step.p, B, H3}, Z);
+    } else {
+      Z = 1;
+      gemm<false, false>(c, B, H3, H, hp, H, params + m.o_ux, H3, EpiStore{ws.step.p, H3});
+    }
+    gru_gate_fwd_kernel<<<cdiv((size_t)B * H, 256), 256, 0, c->stream>>>(
+        B, H, Z, ws.step.p, ws.xp.p + o * H3, hp, ws.hidden.p + o * H, store ? ws.gates.p + o * H3 : nullptr,
+        ws.hu.p + o * H, ws.hprev.p + o * H);
+    after_launch(c);
+  }
+}
+
+// backward gates of rows j < Bp at step t-1: dh_{t-1}[j] = sum_z part + g_t z_t (j < B)
+__global__ void gru_gate_bwd_kernel(int Bp, int B, int H, int Z, const float* __restrict__ part,
+                                    const float* __restrict__ gz_t, const float* __restrict__ dhidden,
+                                    const float* __restrict__ gates, const float* __restrict__ hun,
+                                    const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu,
+                                    float* __restrict__ gz) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)Bp * H) return;
+  const int j = (int)(i / H), u = (int)(i % H);
+  float dh = 0.f;
+  if (j < B) {
+    for (int z = 0; z < Z; ++z) dh += part[((size_t)z * B + j) * H + u];
+    dh += gz_t[i];
+  }
+  const float g = dhidden[i] + dh;
+  const size_t g3 = (size_t)j * 3 * H + 3 * u;
+  const float r = gates[g3], zg = gates[g3 + 1], n = gates[g3 + 2];
+  const float dn = g * (1.f - zg);
+  const float dz = g * (hprev[i] - n);
+  const float dpn = dn * (1.f - n * n);
+  const float dr = dpn * hun[i];
+  const float dpr = dr * r * (1.f - r);
+  const float dpz = dz * zg * (1.f - zg);
+  dpre[g3] = dpr;
+  dpre[g3 + 1] = dpz;
+  dpre[g3 + 2] = dpn;
+  dhu[g3] = dpr;
+  dhu[g3 + 1] = dpz;
+  dhu[g3 + 2] = dpn * r;
+  gz[i] = g * zg;
+}
+
+void gru_backward_big(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
+                      const int32_t* h_offs, Workspace& ws) {
+  const int H = m.H, H3 = 3 * H;
+  for (int t = t_top; t >= 1; --t) {
+    const int B = h_bs[t], Bp = h_bs[t - 1];
+    const size_t o = (size_t)h_offs[t], op = (size_t)h_offs[t - 1];
+    int Z = 1;
+    if (B > 0) {
+      // dh_part = dhU_t[0:B] U^T (M = B, N = H, K = 3H), split-K for parallelism
+      const int tiles = (int)(cdiv(H, tc::BN) * cdiv(B, tc::BM));
+      const int nkb = (H3 + tc::BK - 1) / tc::BK;
+      Z = std::max(1, std::min(c->num_sms / std::max(1, tiles), std::max(1, nkb / 4)));
+      const int per = (nkb + Z - 1) / Z;
+      Z = (nkb + per - 1) / per;
+      ws.step.reserve(c, (size_t)Z * B * H);
+      if (c->tensor_cores && tc::usable(B, H, H3, ws.dhu.p + o * H3, H3, params + m.o_ux, H3,
+                                        EpiPartial{ws.step.p, B, H})) {
+        tc::launch<0, 0>(c, B, H, H3, ws.dhu.p + o * H3, H3, params + m.o_ux, H3, EpiPartial{ws.step.p, B, H}, Z);
+      } else {
+        Z = 1;
+        gemm<false, true>(c, B, H, H3, ws.dhu.p + o * H3, H3, params + m.o_ux, H3, EpiStore{ws.step.p, H});
+      }
+    }
+    gru_gate_bwd_kernel<<<cdiv((size_t)Bp * H, 256), 256, 0, c->stream>>>(
+        Bp, B, H, Z, ws.step.p, ws.g.p + o * H, ws.dhidden.p + op * H, ws.gates.p + op * H3, ws.hu.p + op * H,
+        ws.hprev.p + op * H, ws.dpre.p + op * H3, ws.dhu.p + op * H3, ws.g.p + op * H);
+    after_launch(c);
+  }
 }
 
 void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out) {
@@ -768,9 +905,9 @@ __global__ void enc1_grad_final_kernel(const float* __restrict__ part, int chunk
 
 void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
                      const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad,
-                     const int32_t* h_bs) {
+                     const int32_t* h_bs, const int32_t* h_offs) {
   const int E = m.E, H = m.H, H3 = 3 * m.H;
-  gru_backward_recurrence(c, m, params, L, d_bs, d_offs, ws, h_bs);
+  gru_backward_recurrence(c, m, params, L, d_bs, d_offs, ws, h_bs, h_offs);
   // weight gradients over all rows
   gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
   gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);

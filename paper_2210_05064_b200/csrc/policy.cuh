@@ -41,6 +41,7 @@ struct Workspace {
   DBuf<float> is_w;
   DBuf<unsigned> bar;                                   // grid barrier of the recurrence
   DBuf<long long> trace;                                // VER_REC_TRACE experiments only
+  DBuf<float> step;                                     // per-step GEMM output of the big recurrence steps
   void ensure(const Model& m, size_t S, bool train);
 };
 
@@ -52,14 +53,23 @@ struct Workspace {
 //   timesteps runs on the single-cluster kernels (recurrence.cu).
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs,
                     const float* h0, int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws,
-                    bool store, const int32_t* h_bs = nullptr);
+                    bool store, const int32_t* h_bs = nullptr, const int32_t* h_offs = nullptr);
 
 // Persistent recurrence kernels (recurrence.cu)
 void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
                             const int32_t* d_offs, Workspace& ws, const float* h0, bool store,
-                            const int32_t* h_bs = nullptr);
+                            const int32_t* h_bs = nullptr, const int32_t* h_offs = nullptr);
 void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
-                             const int32_t* d_offs, Workspace& ws, const int32_t* h_bs = nullptr);
+                             const int32_t* d_offs, Workspace& ws, const int32_t* h_bs = nullptr,
+                             const int32_t* h_offs = nullptr);
+// Big recurrence steps on the tensor cores (policy.cu): one 3xTF32 tcgen05
+// GEMM per timestep plus a fused gate kernel.  Forward: steps [0, t_end);
+// backward: steps t_top .. 1.  Host batch sizes / offsets required.
+int gru_big_steps(Ctx* c, const Model& m, const int32_t* h_bs, int L, bool backward);
+void gru_forward_big(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
+                     const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
+void gru_backward_big(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
+                      const int32_t* h_offs, Workspace& ws);
 
 // Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
 // dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights
@@ -81,7 +91,7 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
 // gradient slots of `grad` (device layout).  Requires policy_forward(store).
 void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
                      const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, float* grad,
-                     const int32_t* h_bs = nullptr);
+                     const int32_t* h_bs = nullptr, const int32_t* h_offs = nullptr);
 
 // Per-row log-prob / entropy / value of the heads (nn.cpp:251-278)
 void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float* hidden,

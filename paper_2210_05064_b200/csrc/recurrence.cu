@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
     float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar,
-    long long* trace) {
+    long long* trace, int t_begin) {
   constexpr int H3 = 3 * H, NT = NW * 32;
   constexpr int KS_FR = ks_fr(NW);
   constexpr int KW = H / NW, NI = KW / 8;
@@ -691,12 +691,12 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
       }
     }
   };
-  for (int t = 0; t < L; ++t) {
+  for (int t = t_begin; t < L; ++t) {
     const RowMap rm = rows_in(1, bs[t], rb, RB, 0, 1 << 30);
     if (rm.n == 0) break;  // bs is non-increasing: this row block is done
     const int o = offs[t];
     load_x(rm, o, 0, min(KS_FR, rm.n));
-    if (t > 0) {
+    if (t > t_begin) {
       target += UB;
       group_barrier(cnt, target);
     }
@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_bwd_ks(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
     const float* __restrict__ hun, const float* __restrict__ hprev, float* dpre, float* dhu, float* gz,
-    unsigned* bar, long long* trace, int t_start, int do_init) {
+    unsigned* bar, long long* trace, int t_start, int do_init, int t_stop) {
   constexpr int H3 = 3 * H, NT = NW * 32;
   constexpr int KW = H3 / NW, KL = KW / 8, NV = KL / 4;
   static_assert(KL % 4 == 0, "backward K slice");
@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_bwd_ks(
     }
     any = rm.n > 0;
   }
-  for (int t = t_start; t >= 1; --t) {
+  for (int t = t_start; t > t_stop; --t) {
     const int B = bs[t], Bp = bs[t - 1], o = offs[t], op = offs[t - 1];
     const RowMap rc = rows_in(1, Bp, rb, RB, 0, B);   // rows with a successor at step t
     const RowMap re = rows_in(1, Bp, rb, RB, B, Bp);  // rows that end at step t-1
@@ -1339,9 +1339,37 @@ static int tail_start(const int32_t* h_bs, int L, int th) {
   return t0;
 }
 
+static void fwd_ks_launch(Ctx* c, const Model& m, const float* params, int t_begin, int L, const int32_t* d_bs,
+                          const int32_t* d_offs, Workspace& ws, const float* h0, bool store);
+
 void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
                             const int32_t* d_offs, Workspace& ws, const float* h0, bool store,
-                            const int32_t* h_bs) {
+                            const int32_t* h_bs, const int32_t* h_offs) {
+  // big steps (many rows) as per-step tensor-core GEMMs, then the persistent
+  // FMA kernel, then the cluster tail
+  const int tb = (h_bs && h_offs && pick_fwd_ks(m.H) && rec_mode() == 0) ? gru_big_steps(c, m, h_bs, L, false) : 0;
+  if (tb > 0) {
+    {
+      ScopedEv ev(c, c->rec_tag);
+      gru_forward_big(c, m, params, tb, h_bs, h_offs, ws, h0, store);
+    }
+    const int t0 = tail_ok(c, m.H) ? std::max(tb, tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 4))) : L;
+    if (t0 > tb) fwd_ks_launch(c, m, params, tb, t0, d_bs, d_offs, ws, h0, store);
+    if (t0 < L) {
+      int t0_ = t0, L_ = L;
+      const float* ux = params + m.o_ux;
+      const float* xp = ws.xp.p;
+      float* hidden = ws.hidden.p;
+      float* gates = store ? ws.gates.p : nullptr;
+      float* hun = ws.hu.p;
+      float* hps = ws.hprev.p;
+      long long* tr = trace_buf(c, ws, L);
+      void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr};
+      tail_launch(c, reinterpret_cast<const void*>(gru_fwd_tail<512>), tail_fwd_smem(512), args);
+      trace_dump(c, "fwdtail", L, d_bs, tr);
+    }
+    return;
+  }
   if (L > 0 && tail_ok(c, m.H)) {
     const int t0 = tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 4));
     if (t0 < L) {
@@ -1372,11 +1400,8 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   float* hun = ws.hu.p;
   float* hps = ws.hprev.p;
   unsigned* bar = ws.bar.p;
-  if (const void* fn = rec_mode() == 0 ? pick_fwd_ks(m.H) : nullptr) {
-    long long* tr = trace_buf(c, ws, L);
-    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar, &tr};
-    coop_launch(c, fn, grid, ks_fwd_smem(m.H), args, 32 * ks_warps(m.H));
-    trace_dump(c, "fwd", L, d_bs, tr);
+  if (rec_mode() == 0 && pick_fwd_ks(m.H)) {
+    fwd_ks_launch(c, m, params, 0, L, d_bs, d_offs, ws, h0, store);
     return;
   }
   if (const void* fn = pick_fwd(m.H)) {
@@ -1391,8 +1416,29 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   coop_launch(c, reinterpret_cast<const void*>(gru_fwd_persistent), grid, smem, args);
 }
 
+static void fwd_ks_launch(Ctx* c, const Model& m, const float* params, int t_begin, int L, const int32_t* d_bs,
+                          const int32_t* d_offs, Workspace& ws, const float* h0, bool store) {
+  const RecGeom g = geom(c, m.H);
+  const int grid = g.UB * g.RB;
+  ws.bar.reserve(c, (size_t)kBarStride * g.RB);
+  ws.bar.zero((size_t)kBarStride * g.RB);
+  int UB = g.UB, RB = g.RB, tbeg = t_begin;
+  const float* ux = params + m.o_ux;
+  const float* xp = ws.xp.p;
+  float* hidden = ws.hidden.p;
+  float* gates = store ? ws.gates.p : nullptr;
+  float* hun = ws.hu.p;
+  float* hps = ws.hprev.p;
+  unsigned* bar = ws.bar.p;
+  long long* tr = trace_buf(c, ws, L);
+  const void* fn = pick_fwd_ks(m.H);
+  void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar, &tr, &tbeg};
+  coop_launch(c, fn, grid, ks_fwd_smem(m.H), args, 32 * ks_warps(m.H));
+  trace_dump(c, "fwd", L, d_bs, tr);
+}
+
 void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
-                             const int32_t* d_offs, Workspace& ws, const int32_t* h_bs) {
+                             const int32_t* d_offs, Workspace& ws, const int32_t* h_bs, const int32_t* h_offs) {
   // steps t > t_stop (rows of t-1 <= TC_TH) on the cluster tail, then t_stop .. 1
   int t_stop = L, do_init = 1;
   if (L > 0 && tail_ok(c, m.H)) {
@@ -1417,6 +1463,11 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
     }
   }
   int t_start = std::min(L - 1, t_stop);
+  // big steps t = t_big .. 1 (rows of t-1 >= VER_REC_BIG) run after the
+  // persistent kernel as per-step tensor-core GEMMs
+  const int tb = (h_bs && h_offs && pick_bwd_ks(m.H) && rec_mode() == 0) ? gru_big_steps(c, m, h_bs, L, true) : 0;
+  int t_big = std::min(tb, L - 1);
+  if (t_big > t_start) t_big = t_start;  // (cannot happen: big and tail steps are disjoint)
   const RecGeom g = geom(c, m.H);
   const int grid = g.UB * g.RB;
   ws.bar.reserve(c, (size_t)kBarStride * g.RB);
@@ -1433,10 +1484,16 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
   unsigned* bar = ws.bar.p;
   if (const void* fn = rec_mode() == 0 ? pick_bwd_ks(m.H) : nullptr) {
     long long* tr = trace_buf(c, ws, L);
-    void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux,  &dh,  &gates, &hun,     &hps,
-                    &dpre, &dhu, &gz, &bar, &tr, &t_start, &do_init};
-    coop_launch(c, fn, grid, ks_bwd_smem(m.H), args, 32 * ks_warps(m.H));
-    trace_dump(c, "bwd", L, d_bs, tr);
+    if (t_start > t_big || do_init) {
+      void* args[] = {&L,    &d_bs, &d_offs, &UB, &RB, &ux,      &dh,      &gates,  &hun,
+                      &hps,  &dpre, &dhu,    &gz, &bar, &tr, &t_start, &do_init, &t_big};
+      coop_launch(c, fn, grid, ks_bwd_smem(m.H), args, 32 * ks_warps(m.H));
+      trace_dump(c, "bwd", L, d_bs, tr);
+    }
+    if (t_big > 0) {
+      ScopedEv ev(c, c->rec_tag);
+      gru_backward_big(c, m, params, t_big, h_bs, h_offs, ws);
+    }
     return;
   }
   if (const void* fn = pick_bwd(m.H)) {
