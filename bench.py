@@ -273,6 +273,37 @@ def run_ours(args, rank, world):
               "bytes_per_step": {"gae": 17, "gather": 8 * D_ + 36}}
         del v5
 
+    # ---- C3 (configs[2]): N = 4096 envs, GRU-512, 3 epochs (reference default) x 2 minibatches
+    c3 = None
+    if rank == 0 and not args.no_c3:
+        N3, EP3 = 4096, 3
+        wl3 = synth.make_workload(T_, N3, obs_dim=D_, num_actions=A_, hidden_dim=H_, seed=3)
+        buf3 = V.RolloutBuffer(T_, N3, V.VARIABLE, 0, D_, 0, H_, ctx=ctx)
+        synth.fill_buffer(buf3, wl3)
+        view3 = buf3.close_rollout()
+        l3 = V.Learner(cfg, params, V.PPOConfig(epochs=EP3, minibatches=MINIBATCHES), V.EntropyController(),
+                       V.CosineSchedule(2.5e-4, 2_000_000), mix(3, 0xF00D), ctx=ctx)
+        l3.update(view3, read_stats=False)
+        barrier()
+        t3 = []
+        for _ in range(2):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+                a_ = torch.cuda.Event(enable_timing=True)
+                b_ = torch.cuda.Event(enable_timing=True)
+                a_.record(stream)
+            l3.update(view3, read_stats=False)
+            with torch.cuda.stream(stream):
+                b_.record(stream)
+            t3.append((a_, b_))
+        barrier()
+        ms3 = sum(a_.elapsed_time(b_) for a_, b_ in t3) / len(t3)
+        f3 = view3.fresh_steps()
+        c3 = {"workload": f"configs[2]: N={N3} envs, T={T_}, encoder 2x{E_} + GRU-{H_}, {EP3} epochs x "
+                          f"{MINIBATCHES} minibatches", "fresh_steps": f3, "ms_per_update": ms3,
+              "env_steps_per_s": f3 / (ms3 / 1000.0), "phases_ms": l3.last_timing()}
+        del l3, view3, buf3
+
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
         # dominant kernel = the GRU recurrence direction with the larger device time
@@ -311,6 +342,8 @@ def run_ours(args, rank, world):
         }
         if gg:
             line["gae_gather"] = gg
+        if c3:
+            line["c3"] = c3
         if not args.no_cpu and world == 1:
             cv, dt, sample = cpu_sample()
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
@@ -327,6 +360,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the GAE+gather ragged sweep point")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (N=4096) update measurement")
     ap.add_argument("--c5-log2", type=int, default=26, help="log2 steps of the GAE+gather point")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
