@@ -365,6 +365,284 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   }
 }
 
+// ------------------------------------------------- CTA-pair variant
+// cta_group::2: a cluster of 2 CTAs computes a 256 x 128 tile with one
+// tcgen05.mma.cta_group::2 per K-step, issued by the leader (rank 0).  Each CTA
+// holds its 128 rows of A and 64 of the 128 columns of B (CUTLASS
+// SM100_MMA_TF32_2x1SM: ALayout M/2 per CTA, BLayout N/2 per CTA, C M/2 x N in
+// each CTA's TMEM), so per SM the operand reads of the MMAs, the TMA bytes and
+// the 3xTF32 split traffic all drop by 25% against the single-CTA 128 x 128
+// tile at the same FLOPs: the single-CTA kernel is shared-memory bound.
+//  * each CTA's TMA signals its own full barrier; its split warps then arrive
+//    on the LEADER's split barrier (2 x 4 arrivals) before the MMA may read;
+//  * MMA completion is multicast to both CTAs' empty / acc_full barriers;
+//  * both CTAs' epilogue warps arrive on the leader's acc_empty (2 x 4).
+namespace pair {
+constexpr int BNH = BN / 2;                    // B columns per CTA
+constexpr int STAGES2 = 4;
+constexpr int TILE_A = BM * BK * 4;            // 16 KB
+constexpr int TILE_B = BNH * BK * 4;           // 8 KB
+constexpr int STAGE2 = 2 * TILE_A + 2 * TILE_B;  // A hi, A lo, B hi, B lo
+constexpr int SMEM2 = STAGES2 * STAGE2 + EPI_BYTES + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t to_rank(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void commit2(uint32_t mbar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int AMAJ, int BMAJ, int SPLIT3, class Epi>
+__global__ void __launch_bounds__(THREADS, 1) tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                              const __grid_constant__ CUtensorMap tmB, int M,
+                                                              int N, int K, int kb_per_split, int nsplit, Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tilesN = (N + BN - 1) / BN, tilesM = (M + 2 * BM - 1) / (2 * BM);
+  const int ntiles = tilesN * tilesM * nsplit;
+  const int nkb_total = (K + BK - 1) / BK;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8 * s; };
+  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES2 + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES2 + s); };
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES2 + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES2 + NACC + b); };
+  auto tileA = [&](int s, int lo) { return sbase + s * STAGE2 + lo * TILE_A; };
+  auto tileB = [&](int s, int lo) { return sbase + s * STAGE2 + 2 * TILE_A + lo * TILE_B; };
+  struct Tile {
+    int m0, n0, z, kb0, nkb;
+  };
+  auto decode = [&](int t) {
+    Tile r;
+    const int nt = t % tilesN, q = t / tilesN;
+    r.n0 = nt * BN;
+    r.m0 = (q % tilesM) * 2 * BM;
+    r.z = q / tilesM;
+    r.kb0 = r.z * kb_per_split;
+    r.nkb = max(0, min(nkb_total, r.kb0 + kb_per_split) - r.kb0);
+    return r;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(split_bar(s), 2 * SPLIT_WARPS);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < NACC; ++b) {
+      mbar_init(acc_full(b), 1);
+      mbar_init(acc_empty(b), 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NACC * BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own A rows, own half of B)
+    if (lane == 0) {
+      int it = 0;
+      for (int t = pair_id; t < ntiles; t += npairs) {
+        const Tile T = decode(t);
+        const int am = T.m0 + (int)rank * BM, bn = T.n0 + (int)rank * BNH;
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES2;
+          const uint32_t ph = (it / STAGES2) & 1;
+          mbar_wait(empty_bar(s), ph ^ 1);
+          mbar_expect_tx(full_bar(s), TILE_A + TILE_B);
+          const int k0 = (T.kb0 + i) * BK;
+          if (AMAJ == 0) {
+            tma_load_2d(tileA(s, 0), &tmA, full_bar(s), k0, am);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c) tma_load_2d(tileA(s, 0) + c * 4096, &tmA, full_bar(s), am + 32 * c, k0);
+          }
+          if (BMAJ == 0) {
+            tma_load_2d(tileB(s, 0), &tmB, full_bar(s), k0, bn);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BNH / 32; ++c) tma_load_2d(tileB(s, 0) + c * 4096, &tmB, full_bar(s), bn + 32 * c, k0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA, one thread)
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+    if (leader && lane == 0) {
+      int it = 0, g = 0, buf = 0;
+      for (int t = pair_id; t < ntiles; t += npairs) {
+        const Tile T = decode(t);
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES2;
+          const uint32_t ph = (it / STAGES2) & 1;
+          const bool first = (i % PROMOTE) == 0;
+          if (first) {
+            buf = g % NACC;
+            const int u = g / NACC;
+            if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
+          }
+          mbar_wait(split_bar(s), ph);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(buf * BN);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
+            const uint64_t bh = operand_desc<BMAJ>(tileB(s, 0), kk);
+            const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
+            mma2_tf32(d, ah, bh, idesc, acc);
+            if (SPLIT3) {
+              mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+              mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+            }
+          }
+          commit2(empty_bar(s));
+          if ((i % PROMOTE) == PROMOTE - 1 || i == T.nkb - 1) {
+            commit2(acc_full(buf));
+            ++g;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + SPLIT_WARPS) {
+    // ---------------- operand split (both CTAs), then arrive on the leader
+    const int et = threadIdx.x - 64;
+    int it = 0;
+    for (int t = pair_id; t < ntiles; t += npairs) {
+      const Tile T = decode(t);
+      for (int i = 0; i < T.nkb; ++i, ++it) {
+        const int s = it % STAGES2;
+        const uint32_t ph = (it / STAGES2) & 1;
+        mbar_wait(full_bar(s), ph);
+        if (SPLIT3) {
+          uint8_t* st = smem + s * STAGE2;
+          float4* ahi = reinterpret_cast<float4*>(st);
+          float4* alo = reinterpret_cast<float4*>(st + TILE_A);
+          float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_A);
+          float4* blo = reinterpret_cast<float4*>(st + 2 * TILE_A + TILE_B);
+#pragma unroll 4
+          for (int q = et; q < TILE_A / 16; q += 32 * SPLIT_WARPS) alo[q] = lo_tf32(ahi[q]);
+#pragma unroll 2
+          for (int q = et; q < TILE_B / 16; q += 32 * SPLIT_WARPS) blo[q] = lo_tf32(bhi[q]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) arrive_remote(to_rank(split_bar(s), 0));
+      }
+    }
+  } else {
+    // ---------------- accumulator promotion + epilogue (both CTAs: own 128 rows)
+    const int lane_base = 32 * (warp & 3);
+    float* stg = stg_all + (warp & 3) * 32 * EPI_LD;
+    int g = 0;
+    for (int t = pair_id; t < ntiles; t += npairs) {
+      const Tile T = decode(t);
+      const int ngroups = (T.nkb + PROMOTE - 1) / PROMOTE;
+      float sums[BN];
+#pragma unroll
+      for (int j = 0; j < BN; ++j) sums[j] = 0.f;
+      for (int q = 0; q < ngroups; ++q, ++g) {
+        const int buf = g % NACC;
+        mbar_wait(acc_full(buf), (g / NACC) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN + cc * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
+      }
+      const int rr = lane >> 3, c4 = (lane & 7) * 4;
+      const int mrow0 = T.m0 + (int)rank * BM + lane_base;
+#pragma unroll
+      for (int cc = 0; cc < BN / 32; ++cc) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(stg + lane * EPI_LD + 4 * q) =
+              make_float4(sums[cc * 32 + 4 * q], sums[cc * 32 + 4 * q + 1], sums[cc * 32 + 4 * q + 2],
+                          sums[cc * 32 + 4 * q + 3]);
+        __syncwarp();
+        const int n = T.n0 + cc * 32 + c4;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int r = 4 * k + rr;
+          const int m = mrow0 + r;
+          const float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_LD + c4);
+          if (m < M && n < N) epi.vec4(m, n, v, T.z);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with TMEM and with remote arrivals
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * BN) : "memory");
+  }
+}
+}  // namespace pair
+
 // ------------------------------------------------------------- host side
 inline PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 inline std::once_flag g_encode_once;
@@ -408,7 +686,12 @@ inline bool usable(int M, int N, int K, const float* A, int lda, const float* B,
 }
 
 template <int AMAJ, int BMAJ, class Epi>
+bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
+                 int splits);
+
+template <int AMAJ, int BMAJ, class Epi>
 void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits) {
+  if (launch_pair<AMAJ, BMAJ>(c, M, N, K, A, lda, B, ldb, epi, splits)) return;
   // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32)
   const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
   const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, BN, false) : make_map(B, K, N, ldb, 32, true);
@@ -425,6 +708,45 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
   };
   if (c->precision == 0) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
   else run(tc_gemm_kernel<AMAJ, BMAJ, 0, Epi>);
+}
+
+// CTA-pair launch (cluster of 2): 256 x 128 tiles, opt-in with VER_TC_PAIR=1.
+// Correct (tests/test_gpu_gemm.py passes through it) but measured slower on
+// B200: xp 16384x1536x512 in 198 us against 150 us for the single-CTA kernel
+// (the per-stage cross-CTA split handshake costs more than the 25% of shared
+// memory traffic it saves).
+template <int AMAJ, int BMAJ, class Epi>
+bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
+                 int splits) {
+  if (env_int("VER_TC_PAIR", 0) == 0 || M < 2 * BM) return false;
+  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
+  const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, pair::BNH, false) : make_map(B, K, N, ldb, 32, true);
+  const int nkb = (K + BK - 1) / BK;
+  splits = std::max(1, std::min(splits, nkb));
+  const int per = (nkb + splits - 1) / splits;
+  splits = (nkb + per - 1) / per;
+  const long long ntiles = cdiv(N, BN) * cdiv(M, 2 * BM) * (long long)splits;
+  const int grid = 2 * (int)std::min<long long>(ntiles, c->num_sms / 2);
+  auto run = [&](auto kern) {
+    VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = pair::SMEM2;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi));
+    after_launch(c);
+  };
+  if (c->precision == 0) run(pair::tc_gemm2_kernel<AMAJ, BMAJ, 1, Epi>);
+  else run(pair::tc_gemm2_kernel<AMAJ, BMAJ, 0, Epi>);
+  return true;
 }
 
 inline int splits_for(const Ctx* c, int M, int N, int K) {
