@@ -30,3 +30,19 @@ def test_tc_gemm_3xtf32(ta, tb, M, N, K):
     C1 = V.debug_gemm(A, B, ta, tb, engine=2)
     err1 = np.abs(C1 - ref).max() / scale
     assert err1 < 1e-2, err1  # tf32 (10-bit mantissa) inputs
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
+@pytest.mark.parametrize("M,N,K", [(256, 384, 512), (300, 200, 100), (1024, 1536, 2048)])
+def test_tc_gemm_pair_3xtf32(monkeypatch, ta, tb, M, N, K):
+    """The opt-in CTA-pair kernel (cta_group::2, VER_TC_PAIR=1) at the same bar."""
+    import paper_2210_05064_b200 as V
+    monkeypatch.setenv("VER_TC_PAIR", "1")
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    ref = (A.astype(np.float64).T if ta else A.astype(np.float64)) @ (B.astype(np.float64).T if tb else B)
+    scale = np.sqrt(K)
+    for split in (1, 3):
+        C3 = V.debug_gemm(A, B, ta, tb, engine=1, splitk=split)
+        assert np.abs(C3 - ref).max() / scale < 1e-5, split
