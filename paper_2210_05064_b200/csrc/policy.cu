@@ -624,7 +624,16 @@ __global__ void __launch_bounds__(kLossWarps * 32, 2) ppo_loss_kernel(
   const double gH = -alpha * inv_S;
   double st[kLossStats] = {0, 0, 0, 0, 0, 0, 0, 0};
   double dls = 0.0;  // lane c < A: log_std gradient (continuous)
-  for (int p = blockIdx.x * kLossWarps + warp; p < S; p += gridDim.x * kLossWarps) {
+  // fused path: the next row's hidden values are loaded while this row is
+  // processed (the kernel is bound by that load's latency otherwise)
+  const int pstride = gridDim.x * kLossWarps;
+  float hn[kHL];
+  if (fuse) {
+    const int p0 = blockIdx.x * kLossWarps + warp;
+#pragma unroll
+    for (int i = 0; i < kHL; ++i) hn[i] = (p0 < S && i < hl) ? __ldcs(hidden + (size_t)p0 * H + lane + 32 * i) : 0.f;
+  }
+  for (int p = blockIdx.x * kLossWarps + warp; p < S; p += pstride) {
     const float* hrow = hidden + (size_t)p * H;
     float acc[NA];
 #pragma unroll
@@ -632,12 +641,25 @@ __global__ void __launch_bounds__(kLossWarps * 32, 2) ppo_loss_kernel(
     float hv[kHL];
     if (fuse) {
 #pragma unroll
-      for (int i = 0; i < kHL; ++i) {
-        hv[i] = i < hl ? hrow[lane + 32 * i] : 0.f;
+      for (int i = 0; i < kHL; ++i) hv[i] = hn[i];
+      const int pn = p + pstride;
+#pragma unroll
+      for (int i = 0; i < kHL; ++i) hn[i] = (pn < S && i < hl) ? __ldcs(hidden + (size_t)pn * H + lane + 32 * i) : 0.f;
+      // NA independent partial sums per lane, 2 chains each
+      float acc2[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) acc2[c] = 0.f;
+#pragma unroll
+      for (int i = 0; i < kHL; i += 2) {
 #pragma unroll
         for (int c = 0; c < NA; ++c)
-          if (c < AH && i < hl) acc[c] = fmaf(hv[i], s_wh[(lane + 32 * i) * AH + c], acc[c]);
+          if (c < AH) {
+            if (i < hl) acc[c] = fmaf(hv[i], s_wh[(lane + 32 * i) * AH + c], acc[c]);
+            if (i + 1 < hl) acc2[c] = fmaf(hv[i + 1], s_wh[(lane + 32 * (i + 1)) * AH + c], acc2[c]);
+          }
       }
+#pragma unroll
+      for (int c = 0; c < NA; ++c) acc[c] += acc2[c];
     } else {
       for (int u = lane; u < H; u += 32) {
         const float h = hrow[u];
