@@ -205,6 +205,8 @@ static void prepare_replay(Ctx* c, DPacked& P) {
   std::copy(bs.begin(), bs.end(), meta.begin() + 4 * n + L);
   P.rp_L = L;
   P.rp_R = R;
+  P.rp_bs = bs;
+  P.rp_offs = offs;
   P.rp_meta.reserve(c, meta.size());
   P.rp_meta.upload(meta.data(), meta.size());  // pageable source: consumed before the call returns
 }
@@ -225,7 +227,8 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
   after_launch(c);
   replay_h0_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm + n, n, V.h0.p, H, Ln.rh0.p);
   after_launch(c);
-  policy_forward(c, Ln.m, params, R, Ln.robs.p, Ln.rh0.p, L, dm + 4 * n + L, dm + 4 * n, Ln.wr, false);
+  policy_forward(c, Ln.m, params, R, Ln.robs.p, Ln.rh0.p, L, dm + 4 * n + L, dm + 4 * n, Ln.wr, false,
+                 P.rp_bs.data(), P.rp_offs.data());
   replay_final_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm + 2 * n, dm + 3 * n, n,
                                                                       Ln.wr.hidden.p, H, h0s);
   after_launch(c);

@@ -45,6 +45,7 @@ struct DPacked {
   bool rp_ready = false;
   int rp_n = 0, rp_L = 0, rp_R = 0;
   DBuf<int32_t> rp_meta;
+  std::vector<int32_t> rp_bs, rp_offs;  // host copies (drive the replay recurrence paths)
 };
 
 // pack + gather of an explicit device array of k pieces (deal order)
