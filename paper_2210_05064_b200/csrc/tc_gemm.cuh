@@ -92,6 +92,28 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64
       : "memory");
 }
 
+// D (tmem) += A (tmem, K-major, lane = row, one 32-bit column per k) x B (smem)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 consecutive TMEM columns of this warp's 32 lanes <- v[0..31] (one per lane per column)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
 // shared-memory matrix descriptors (sm_100 UMMA, 128-byte swizzle, version 1)
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
@@ -134,7 +156,12 @@ __device__ __forceinline__ float4 lo_tf32(float4 x) { return make_float4(lo1(x.x
 // running counters across tiles, so the smem ring and the four TMEM
 // accumulator buffers flow from one tile into the next: the MMA issuer starts
 // tile i+1 while the epilogue warps are still storing tile i.
-template <int AMAJ, int BMAJ, int SPLIT3, class Epi>
+// ATM (K-major A, 3xTF32 only): the split warps move A's hi / lo into tensor
+// memory with tcgen05.st and the MMAs read A from TMEM (the .kind::tf32 [a_tmem]
+// form), so shared memory carries only the B operand reads: a third less
+// shared-memory traffic per stage.  Two accumulator buffers then (TMEM:
+// 2 x 128 accumulator columns + 3 stages x 64 A columns).
+template <int AMAJ, int BMAJ, int SPLIT3, class Epi, int ATM = 0>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                              const __grid_constant__ CUtensorMap tmB, int M,
                                                              int N, int K, int kb_per_split, int nsplit, Epi epi) {
@@ -143,7 +170,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   float* stg_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_BYTES);
   // bars: full[S] split[S] empty[S] acc_full[NACC] acc_empty[NACC]; then the TMEM address slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * NACC);
+  constexpr int NACC = ATM ? 2 : tc::NACC;
+  constexpr int A_COL0 = NACC * BN;  // ATM: stage s hi at A_COL0 + 64 s, lo at + 32
+  static_assert(!ATM || (AMAJ == 0 && SPLIT3), "A via TMEM: K-major A, 3xTF32");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * tc::NACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tilesN = (N + BN - 1) / BN, tilesM = (M + BM - 1) / BM;
   const int ntiles = tilesN * tilesM * nsplit;
@@ -186,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(NACC * BN)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -247,15 +277,23 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           const uint32_t d = tmem + (uint32_t)(buf * BN);
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
             const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
             const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
-            mma_tf32(d, ah, bh, idesc, acc);
-            if (SPLIT3) {
-              const uint64_t al = operand_desc<AMAJ>(tile(s, 1), kk);
+            if (ATM) {
+              const uint32_t ah = tmem + (uint32_t)(A_COL0 + 64 * s + 8 * kk);
               const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
-              mma_tf32(d, al, bh, idesc, 1u);
-              mma_tf32(d, ah, bl, idesc, 1u);
+              mma_tf32_ts(d, ah, bh, idesc, acc);
+              mma_tf32_ts(d, ah + 32, bh, idesc, 1u);
+              mma_tf32_ts(d, ah, bl, idesc, 1u);
+            } else {
+              const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
+              mma_tf32(d, ah, bh, idesc, acc);
+              if (SPLIT3) {
+                const uint64_t al = operand_desc<AMAJ>(tile(s, 1), kk);
+                const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
+                mma_tf32(d, al, bh, idesc, 1u);
+                mma_tf32(d, ah, bl, idesc, 1u);
+              }
             }
           }
           umma_commit(empty_bar(s));
@@ -283,12 +321,39 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
           float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
           float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+          if (ATM) {
+            // row r = this thread's TMEM lane: its 32 K values from the SW128
+            // K-major tile (16-byte chunk c of row r sits at chunk c ^ (r % 8))
+            const int r = 32 * (warp & 3) + lane;
+            const uint8_t* rowp = st + (r >> 3) * 1024 + (r & 7) * 128;
+            uint32_t hv[32], lv[32];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 x = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+              const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t hb = __float_as_uint(xs[j]) & 0xffffe000u;
+                hv[4 * c + j] = hb;
+                lv[4 * c + j] = __float_as_uint(xs[j] - __uint_as_float(hb));
+              }
+            }
+            const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(A_COL0 + 64 * s);
+            tmem_st32(ta, hv);
+            tmem_st32(ta + 32, lv);
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 #pragma unroll 4
-          for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) {
-            // the tensor core reads an fp32 operand as tf32 by truncation, so the
-            // landed tile already is hi = trunc_tf32(x); only lo = x - hi is written
-            alo[q] = lo_tf32(ahi[q]);
-            blo[q] = lo_tf32(bhi[q]);
+            for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) blo[q] = lo_tf32(bhi[q]);
+            (void)alo;
+            tc_fence_before();
+          } else {
+#pragma unroll 4
+            for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) {
+              // the tensor core reads an fp32 operand as tf32 by truncation, so the
+              // landed tile already is hi = trunc_tf32(x); only lo = x - hi is written
+              alo[q] = lo_tf32(ahi[q]);
+              blo[q] = lo_tf32(bhi[q]);
+            }
           }
           // generic-proxy smem writes -> visible to the tensor core (async proxy)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -361,7 +426,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * BN) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
 }
 
@@ -706,8 +771,17 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
     kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, splits, epi);
     after_launch(c);
   };
-  if (c->precision == 0) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
-  else run(tc_gemm_kernel<AMAJ, BMAJ, 0, Epi>);
+  if (c->precision == 0) {
+    if constexpr (AMAJ == 0) {
+      if (env_int("VER_TC_ATM", 1)) {
+        run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1>);
+        return;
+      }
+    }
+    run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
+  } else {
+    run(tc_gemm_kernel<AMAJ, BMAJ, 0, Epi>);
+  }
 }
 
 // CTA-pair launch (cluster of 2): 256 x 128 tiles, opt-in with VER_TC_PAIR=1.
