@@ -167,13 +167,18 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
                                                              int N, int K, int kb_per_split, int nsplit, Epi epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* stg_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_BYTES);
+  float* stg_all = reinterpret_cast<float*>(smem + tc::STAGES * tc::STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc::STAGES * tc::STAGE_BYTES + EPI_BYTES);
   // bars: full[S] split[S] empty[S] acc_full[NACC] acc_empty[NACC]; then the TMEM address slot
   constexpr int NACC = ATM ? 2 : tc::NACC;
+  // ATM stages hold A hi, B hi, B lo only (A lo lives in TMEM): 4 x 48 KB
+  constexpr int STAGES = ATM ? 4 : tc::STAGES;
+  constexpr int STAGE_BYTES = ATM ? 3 * TILE_BYTES : tc::STAGE_BYTES;
+  static_assert(STAGES * STAGE_BYTES <= tc::STAGES * tc::STAGE_BYTES, "smem budget");
+  static_assert(!ATM || NACC * BN + STAGES * 64 <= 512, "TMEM budget");
   constexpr int A_COL0 = NACC * BN;  // ATM: stage s hi at A_COL0 + 64 s, lo at + 32
   static_assert(!ATM || (AMAJ == 0 && SPLIT3), "A via TMEM: K-major A, 3xTF32");
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * tc::NACC);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * 4 + 2 * tc::NACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tilesN = (N + BN - 1) / BN, tilesM = (M + BM - 1) / BM;
   const int ntiles = tilesN * tilesM * nsplit;
@@ -185,7 +190,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES + s); };
   auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES + b); };
   auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES + NACC + b); };
-  auto tile = [&](int s, int which) { return sbase + s * STAGE_BYTES + which * TILE_BYTES; };  // 0 Ahi 1 Alo 2 Bhi 3 Blo
+  // 0 A hi, 1 A lo, 2 B hi, 3 B lo (ATM: A hi, B hi, B lo)
+  auto tile = [&](int s, int which) {
+    return sbase + s * STAGE_BYTES + (ATM ? (which == 0 ? 0 : which - 1) : which) * TILE_BYTES;
+  };
   struct Tile {
     int m0, n0, z, kb0, nkb;
   };
@@ -319,8 +327,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           uint8_t* st = smem + s * STAGE_BYTES;
           float4* ahi = reinterpret_cast<float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
-          float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
-          float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+          float4* bhi = reinterpret_cast<float4*>(st + (ATM ? 1 : 2) * TILE_BYTES);
+          float4* blo = reinterpret_cast<float4*>(st + (ATM ? 2 : 3) * TILE_BYTES);
           if (ATM) {
             // row r = this thread's TMEM lane: its 32 K values from the SW128
             // K-major tile (16-byte chunk c of row r sits at chunk c ^ (r % 8))
