@@ -336,8 +336,11 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
 // ~8 us up to 640 rows.
 int gru_big_steps(Ctx* c, const Model& m, const int32_t* h_bs, int L, bool backward) {
   if (m.H % 4 != 0) return 0;  // the gate kernels move 4 units per thread
-  // thresholds measured on B200 at C2 (scripts/ab_bench.py sweeps)
-  const int min_rows = backward ? env_int("VER_REC_BIG_BWD", 200) : env_int("VER_REC_BIG_FWD", 250);
+  // thresholds measured on B200 at C2 (scripts/ab_bench.py sweeps): 150 rows for
+  // the persistent step kernel (stepgemm.cu), 250 / 200 for per-step launches
+  const bool persist = step_gemm_enabled();
+  const int min_rows = backward ? env_int("VER_REC_BIG_BWD", persist ? 150 : 200)
+                                : env_int("VER_REC_BIG_FWD", persist ? 150 : 250);
   if (!h_bs || !c->tensor_cores || m.H % 32 != 0 || min_rows <= 0) return 0;
   int t = 0;
   while (t < L && h_bs[t] >= min_rows) ++t;

@@ -42,6 +42,7 @@ struct Workspace {
   DBuf<unsigned> bar;                                   // grid barrier of the recurrence
   DBuf<long long> trace;                                // VER_REC_TRACE experiments only
   DBuf<float> step;                                     // per-step GEMM output of the big recurrence steps
+  DBuf<float> sgsteps, sgmaps;                          // stepgemm.cu: step table, per-step A tensor maps
   void ensure(const Model& m, size_t S, bool train);
 };
 
@@ -70,6 +71,12 @@ void gru_forward_big(Ctx* c, const Model& m, const float* params, int t_end, con
                      const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
 void gru_backward_big(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
                       const int32_t* h_offs, Workspace& ws);
+// the same steps in one persistent cooperative launch (stepgemm.cu)
+bool step_gemm_enabled();
+void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
+                             const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
+void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
+                              const int32_t* h_offs, Workspace& ws);
 
 // Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
 // dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights

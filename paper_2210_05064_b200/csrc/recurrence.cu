@@ -1349,7 +1349,9 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   // FMA kernel, then the cluster tail
   const int tb = (h_bs && h_offs && pick_fwd_ks(m.H) && rec_mode() == 0) ? gru_big_steps(c, m, h_bs, L, false) : 0;
   if (tb > 0) {
-    {
+    if (step_gemm_enabled()) {
+      gru_forward_big_persist(c, m, params, tb, h_bs, h_offs, ws, h0, store);
+    } else {
       ScopedEv ev(c, c->rec_tag);
       gru_forward_big(c, m, params, tb, h_bs, h_offs, ws, h0, store);
     }
@@ -1491,8 +1493,12 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
       trace_dump(c, "bwd", L, d_bs, tr);
     }
     if (t_big > 0) {
-      ScopedEv ev(c, c->rec_tag);
-      gru_backward_big(c, m, params, t_big, h_bs, h_offs, ws);
+      if (step_gemm_enabled()) {
+        gru_backward_big_persist(c, m, params, t_big, h_bs, h_offs, ws);
+      } else {
+        ScopedEv ev(c, c->rec_tag);
+        gru_backward_big(c, m, params, t_big, h_bs, h_offs, ws);
+      }
     }
     return;
   }

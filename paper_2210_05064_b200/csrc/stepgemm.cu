@@ -1,0 +1,484 @@
+// stepgemm.cu — the big recurrence timesteps as one persistent cooperative
+// kernel: per step a 3xTF32 tcgen05 GEMM phase (split-K work items, at most one
+// per CTA) and an elementwise gate phase, separated by grid barriers.
+//
+//   forward  step t: hU = h_{t-1}[0:B] U   (M = B, N = 3H, K = H), then the GRU
+//                    gates of rows j < B (nn.cpp:235-250);
+//   backward step t: dh = dhU_t[0:B] U^T   (M = B, N = H, K = 3H), then the gate
+//                    gradient of the rows j < B_{t-1} of step t-1.
+//
+// Against one GEMM launch + one gate launch per step (policy.cu
+// gru_forward_big / gru_backward_big) this removes two launches, the TMEM
+// allocation and the tensor-map prefetch per step: the A operand's tensor map
+// of every step is built on the host up front (the batch offsets are known
+// after the pack) and read from global memory.  Warp roles as in the tcgen05
+// GEMM (tc_gemm.cuh): TMA producer, MMA issuer, 4 split warps, 4 epilogue
+// warps; the smem ring, the TMEM accumulator buffers and their mbarrier phases
+// run on across steps.  All 320 threads join the gate phase.
+#include <cstdlib>
+
+#include "policy.cuh"
+#include "tc_gemm.cuh"
+
+namespace verg {
+namespace sg {
+
+using namespace tc;
+
+struct Step {
+  int B;        // GEMM rows (forward: bs_t; backward: bs_t, rows with a successor)
+  int Bg;       // gate rows (forward: bs_t; backward: bs_{t-1})
+  int o, op;    // packed offsets of the GEMM / gate rows (forward: o = offs_t, op = offs_{t-1} or -1 for h0)
+  int Z, per;   // split-K count, K-blocks per split
+  int tilesM;
+  int pad;
+};
+
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(count, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+
+template <int DIR>  // 0 forward (B MN-major: U stored K x N), 1 backward (B K-major: U stored N x K)
+__global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
+    int nsteps, const Step* __restrict__ steps, const CUtensorMap* __restrict__ amaps,
+    const __grid_constant__ CUtensorMap bmap, int H, float* __restrict__ part, unsigned* bar,
+    // forward
+    const float* __restrict__ xp, const float* __restrict__ h0, float* __restrict__ hidden,
+    float* __restrict__ gates_out, float* __restrict__ hun_out, float* __restrict__ hprev_out,
+    // backward
+    const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
+    const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
+    long long* trace) {
+  constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * NACC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H3 = 3 * H, N = DIR == 0 ? H3 : H, K = DIR == 0 ? H : H3;
+  const int tilesN = (N + BN - 1) / BN;
+  const int nkb_total = (K + BK - 1) / BK;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8 * s; };
+  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES + s); };
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES + NACC + b); };
+  auto tile = [&](int s, int which) { return sbase + s * STAGE_BYTES + which * TILE_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(split_bar(s), SPLIT_WARPS);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < NACC; ++b) {
+      mbar_init(acc_full(b), 1);
+      mbar_init(acc_empty(b), EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NACC * BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  unsigned target = 0;
+  // pipeline counters, continued across steps (each role advances its own)
+  int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
+
+  for (int si = 0; si < nsteps; ++si) {
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      long long tn;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tn));
+      trace[2 * si] = tn;
+    }
+    const Step S = steps[si];
+    const int W = S.tilesM * tilesN * S.Z;
+    const int item = blockIdx.x;
+    if (S.B > 0 && item < W) {
+      const int nt = item % tilesN, q = item / tilesN;
+      const int m0 = (q % S.tilesM) * BM, n0 = nt * BN, z = q / S.tilesM;
+      const int kb0 = z * S.per;
+      const int nkb = max(0, min(nkb_total, kb0 + S.per) - kb0);
+      const CUtensorMap* amap = amaps + si;
+      if (warp == 0) {
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // h / dhU rows written by the gate phase
+          for (int i = 0; i < nkb; ++i, ++it_tma) {
+            const int s = it_tma % STAGES;
+            const uint32_t ph = (it_tma / STAGES) & 1;
+            mbar_wait(empty_bar(s), ph ^ 1);
+            mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+            const int k0 = (kb0 + i) * BK;
+            tma_load_2d(tile(s, 0), amap, full_bar(s), k0, m0);
+            if (BMAJ == 0) {
+              tma_load_2d(tile(s, 2), &bmap, full_bar(s), k0, n0);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &bmap, full_bar(s), n0 + 32 * c, k0);
+            }
+          }
+        }
+      } else if (warp == 1) {
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
+                               ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+        if (lane == 0) {
+          int buf = 0;
+          for (int i = 0; i < nkb; ++i, ++it_mma) {
+            const int s = it_mma % STAGES;
+            const uint32_t ph = (it_mma / STAGES) & 1;
+            const bool first = (i % PROMOTE) == 0;
+            if (first) {
+              buf = g_mma % NACC;
+              const int u = g_mma / NACC;
+              if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
+            }
+            mbar_wait(split_bar(s), ph);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(buf * BN);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
+              const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
+              mma_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+              mma_tf32(d, operand_desc<AMAJ>(tile(s, 1), kk), bh, idesc, 1u);
+              mma_tf32(d, ah, operand_desc<BMAJ>(tile(s, 3), kk), idesc, 1u);
+            }
+            umma_commit(empty_bar(s));
+            if ((i % PROMOTE) == PROMOTE - 1 || i == nkb - 1) {
+              umma_commit(acc_full(buf));
+              ++g_mma;
+            }
+          }
+        }
+        __syncwarp();
+      } else if (warp < 2 + SPLIT_WARPS) {
+        const int et = threadIdx.x - 64;
+        for (int i = 0; i < nkb; ++i, ++it_split) {
+          const int s = it_split % STAGES;
+          const uint32_t ph = (it_split / STAGES) & 1;
+          mbar_wait(full_bar(s), ph);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          float4* ahi = reinterpret_cast<float4*>(st);
+          float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
+          float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
+          float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+#pragma unroll 4
+          for (int qq = et; qq < TILE_BYTES / 16; qq += 32 * SPLIT_WARPS) {
+            alo[qq] = lo_tf32(ahi[qq]);
+            blo[qq] = lo_tf32(bhi[qq]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(split_bar(s));
+        }
+      } else {
+        // accumulator promotion + partial-tile epilogue: part[z][m][n]
+        const int lane_base = 32 * (warp & 3);
+        float* stg = stg_all + (warp & 3) * 32 * EPI_LD;
+        const int ngroups = (nkb + PROMOTE - 1) / PROMOTE;
+        float sums[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) sums[j] = 0.f;
+        for (int gq = 0; gq < ngroups; ++gq, ++g_epi) {
+          const int buf = g_epi % NACC;
+          mbar_wait(acc_full(buf), (g_epi / NACC) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < BN / 32; ++cc) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN + cc * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty(buf));
+        }
+        const int rr = lane >> 3, c4 = (lane & 7) * 4;
+#pragma unroll
+        for (int cc = 0; cc < BN / 32; ++cc) {
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq)
+            *reinterpret_cast<float4*>(stg + lane * EPI_LD + 4 * qq) =
+                make_float4(sums[cc * 32 + 4 * qq], sums[cc * 32 + 4 * qq + 1], sums[cc * 32 + 4 * qq + 2],
+                            sums[cc * 32 + 4 * qq + 3]);
+          __syncwarp();
+          const int n = n0 + cc * 32 + c4;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int r = 4 * k + rr;
+            const int m = m0 + lane_base + r;
+            const float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_LD + c4);
+            if (m < S.B && n < N) *reinterpret_cast<float4*>(part + ((size_t)z * S.B + m) * N + n) = v;
+          }
+          __syncwarp();
+        }
+      }
+    }
+    grid_sync(bar, target);  // all partials of step si written
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      long long tn;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tn));
+      trace[2 * si + 1] = tn;
+    }
+
+    // ---------------- gate phase: (row j, units 4x .. 4x+3) over the grid
+    const int H4 = H / 4;
+    const size_t zs = (size_t)S.B * N;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < S.Bg * H4; idx += gridDim.x * blockDim.x) {
+      const int j = idx / H4, u4 = idx % H4;
+      if (DIR == 0) {
+        const size_t row3 = ((size_t)S.o + j) * H3 + 12 * (size_t)u4, row = ((size_t)S.o + j) * H + 4 * (size_t)u4;
+        const size_t prow = (size_t)j * H3 + 12 * (size_t)u4;
+        float s12[12];
+#pragma unroll
+        for (int e = 0; e < 12; ++e) s12[e] = 0.f;
+        for (int z = 0; z < S.Z; ++z) {
+          const float4* p4 = reinterpret_cast<const float4*>(part + z * zs + prow);
+          const float4 a = p4[0], b = p4[1], c = p4[2];
+          s12[0] += a.x; s12[1] += a.y; s12[2] += a.z; s12[3] += a.w; s12[4] += b.x; s12[5] += b.y;
+          s12[6] += b.z; s12[7] += b.w; s12[8] += c.x; s12[9] += c.y; s12[10] += c.z; s12[11] += c.w;
+        }
+        const float4* x4 = reinterpret_cast<const float4*>(xp + row3);
+        const float4 xa = x4[0], xb = x4[1], xc = x4[2];
+        const float x[12] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w, xc.x, xc.y, xc.z, xc.w};
+        const float* hp = S.op < 0 ? h0 + (size_t)j * H : hidden + ((size_t)S.op + j) * H;
+        const float4 hp4 = *reinterpret_cast<const float4*>(hp + 4 * u4);
+        const float hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
+        float hn[4], g[12];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float rg = sigm(x[3 * e] + s12[3 * e]);
+          const float zg = sigm(x[3 * e + 1] + s12[3 * e + 1]);
+          const float ng = tanhf(x[3 * e + 2] + rg * s12[3 * e + 2]);
+          hn[e] = (1.f - zg) * ng + zg * hpv[e];
+          g[3 * e] = rg;
+          g[3 * e + 1] = zg;
+          g[3 * e + 2] = ng;
+        }
+        *reinterpret_cast<float4*>(hidden + row) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+        if (gates_out) {
+          float4* g4 = reinterpret_cast<float4*>(gates_out + row3);
+          g4[0] = make_float4(g[0], g[1], g[2], g[3]);
+          g4[1] = make_float4(g[4], g[5], g[6], g[7]);
+          g4[2] = make_float4(g[8], g[9], g[10], g[11]);
+          *reinterpret_cast<float4*>(hun_out + row) = make_float4(s12[2], s12[5], s12[8], s12[11]);
+          *reinterpret_cast<float4*>(hprev_out + row) = hp4;
+        }
+      } else {
+        const size_t row = ((size_t)S.op + j) * H + 4 * (size_t)u4, row3 = ((size_t)S.op + j) * H3 + 12 * (size_t)u4;
+        float dh[4] = {0.f, 0.f, 0.f, 0.f};
+        if (j < S.B) {
+          for (int z = 0; z < S.Z; ++z) {
+            const float4 p = *reinterpret_cast<const float4*>(part + z * zs + (size_t)j * H + 4 * u4);
+            dh[0] += p.x; dh[1] += p.y; dh[2] += p.z; dh[3] += p.w;
+          }
+          const float4 q = *reinterpret_cast<const float4*>(gz + ((size_t)S.o + j) * H + 4 * u4);
+          dh[0] += q.x; dh[1] += q.y; dh[2] += q.z; dh[3] += q.w;
+        }
+        const float4 d4 = *reinterpret_cast<const float4*>(dhidden + row);
+        const float4 hn4 = *reinterpret_cast<const float4*>(hun + row);
+        const float4 hp4 = *reinterpret_cast<const float4*>(hprev + row);
+        const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hnv[4] = {hn4.x, hn4.y, hn4.z, hn4.w},
+                    hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
+        const float4* g4 = reinterpret_cast<const float4*>(gates + row3);
+        const float4 ga = g4[0], gb = g4[1], gc = g4[2];
+        const float gt[12] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w, gc.x, gc.y, gc.z, gc.w};
+        float o1[12], o2[12], gzv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float gg = dv[e] + dh[e];
+          const float r = gt[3 * e], zg = gt[3 * e + 1], n = gt[3 * e + 2];
+          const float dn = gg * (1.f - zg);
+          const float dz = gg * (hpv[e] - n);
+          const float dpn = dn * (1.f - n * n);
+          const float dr = dpn * hnv[e];
+          const float dpr = dr * r * (1.f - r);
+          const float dpz = dz * zg * (1.f - zg);
+          o1[3 * e] = dpr;
+          o1[3 * e + 1] = dpz;
+          o1[3 * e + 2] = dpn;
+          o2[3 * e] = dpr;
+          o2[3 * e + 1] = dpz;
+          o2[3 * e + 2] = dpn * r;
+          gzv[e] = gg * zg;
+        }
+        float4* p1 = reinterpret_cast<float4*>(dpre + row3);
+        float4* p2 = reinterpret_cast<float4*>(dhu + row3);
+        p1[0] = make_float4(o1[0], o1[1], o1[2], o1[3]);
+        p1[1] = make_float4(o1[4], o1[5], o1[6], o1[7]);
+        p1[2] = make_float4(o1[8], o1[9], o1[10], o1[11]);
+        p2[0] = make_float4(o2[0], o2[1], o2[2], o2[3]);
+        p2[1] = make_float4(o2[4], o2[5], o2[6], o2[7]);
+        p2[2] = make_float4(o2[8], o2[9], o2[10], o2[11]);
+        *reinterpret_cast<float4*>(gz + row) = make_float4(gzv[0], gzv[1], gzv[2], gzv[3]);
+      }
+    }
+    if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * BN) : "memory");
+  }
+}
+
+// host: per-step split-K so that tilesM x tilesN x Z <= grid
+static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
+  Step s{};
+  s.B = B;
+  s.Bg = Bg;
+  s.o = o;
+  s.op = op;
+  s.tilesM = (int)cdiv(std::max(B, 1), BM);
+  const int tilesN = (int)cdiv(N, BN);
+  const int nkb = (K + BK - 1) / BK;
+  int Z = std::max(1, std::min(grid / std::max(1, s.tilesM * tilesN), std::max(1, nkb / 2)));
+  Z = std::min(Z, 8);
+  const int per = (nkb + Z - 1) / Z;
+  s.Z = (nkb + per - 1) / per;
+  s.per = per;
+  return s;
+}
+
+template <int DIR>
+static void launch(Ctx* c, const Model& m, const float* params, const std::vector<Step>& hs,
+                   const std::vector<CUtensorMap>& maps, Workspace& ws, const float* h0, bool store) {
+  const int nsteps = (int)hs.size();
+  if (nsteps == 0) return;
+  const int H = m.H, H3 = 3 * H;
+  const int N = DIR == 0 ? H3 : H;
+  size_t part_n = 0;
+  for (const Step& s : hs) part_n = std::max(part_n, (size_t)s.Z * s.B * N);
+  ws.step.reserve(c, std::max<size_t>(part_n, 4));
+  ws.sgsteps.reserve(c, (size_t)nsteps * sizeof(Step) / 4 + 1);
+  ws.sgmaps.reserve(c, (size_t)nsteps * sizeof(CUtensorMap) / 4 + 16);
+  // 64-byte aligned tensor-map array inside the buffer
+  uint8_t* mbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws.sgmaps.p) + 63) & ~uintptr_t(63));
+  VER_CUDA(cudaMemcpyAsync(ws.sgsteps.p, hs.data(), sizeof(Step) * nsteps, cudaMemcpyHostToDevice, c->stream));
+  VER_CUDA(cudaMemcpyAsync(mbase, maps.data(), sizeof(CUtensorMap) * nsteps, cudaMemcpyHostToDevice, c->stream));
+  ws.bar.reserve(c, 32);
+  ws.bar.zero(32);
+  const float* ux = params + m.o_ux;
+  const CUtensorMap bmap = DIR == 0 ? make_map(ux, H, H3, H3, 32, true) : make_map(ux, H, H3, H3, BN, false);
+  const int grid = c->num_sms;
+  const void* fn = reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
+  static bool attr[2] = {false, false};
+  if (!attr[DIR]) {
+    VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr[DIR] = true;
+  }
+  int ns = nsteps;
+  const Step* dsteps = reinterpret_cast<const Step*>(ws.sgsteps.p);
+  const CUtensorMap* dmaps = reinterpret_cast<const CUtensorMap*>(mbase);
+  float* part = ws.step.p;
+  unsigned* bar = ws.bar.p;
+  const float* xp = ws.xp.p;
+  float* hidden = ws.hidden.p;
+  float* gts = store ? ws.gates.p : nullptr;
+  float* hun_o = ws.hu.p;
+  float* hpv_o = ws.hprev.p;
+  const float* dh = ws.dhidden.p;
+  const float* gates = ws.gates.p;
+  const float* hun = ws.hu.p;
+  const float* hprev = ws.hprev.p;
+  float* dpre = ws.dpre.p;
+  float* dhu = ws.dhu.p;
+  float* gz = ws.g.p;
+  // VER_REC_TRACE (experiments): GEMM-phase start / gate-phase start of every step
+  long long* tr = nullptr;
+  const char* tpath = getenv("VER_REC_TRACE");
+  if (tpath) {
+    ws.trace.reserve(c, 2 * (size_t)nsteps);
+    ws.trace.zero(2 * (size_t)nsteps);
+    tr = ws.trace.p;
+  }
+  void* args[] = {&ns,     &dsteps, &dmaps, const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H), &part, &bar,
+                  &xp,     &h0,     &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre, &dhu, &gz, &tr};
+  {
+    ScopedEv ev(c, c->rec_tag);
+    VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(THREADS), args, SMEM_BYTES, c->stream));
+    after_launch(c);
+  }
+  if (tr) {
+    std::vector<long long> h(2 * (size_t)nsteps);
+    VER_CUDA(cudaMemcpyAsync(h.data(), tr, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c->stream));
+    VER_CUDA(cudaStreamSynchronize(c->stream));
+    if (FILE* f = fopen(tpath, "a")) {
+      fprintf(f, "persist%d %d", DIR, nsteps);
+      for (int i = 0; i < nsteps; ++i)
+        fprintf(f, " %d:%lld:%lld", hs[i].Bg, h[2 * i + 1] - h[2 * i],
+                (i + 1 < nsteps ? h[2 * i + 2] : h[2 * i + 1]) - h[2 * i + 1]);
+      fprintf(f, "\n");
+      fclose(f);
+    }
+  }
+}
+
+}  // namespace sg
+
+bool step_gemm_enabled() { return env_int("VER_REC_PERSIST", 1) != 0; }
+
+// forward big steps t = 0 .. t_end-1 in one persistent launch
+void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
+                             const int32_t* h_offs, Workspace& ws, const float* h0, bool store) {
+  const int H = m.H, H3 = 3 * H;
+  std::vector<sg::Step> hs;
+  std::vector<CUtensorMap> maps;
+  for (int t = 0; t < t_end; ++t) {
+    const int B = h_bs[t];
+    hs.push_back(sg::make_step(B, B, h_offs[t], t == 0 ? -1 : h_offs[t - 1], H3, H, c->num_sms));
+    const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
+    maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
+  }
+  sg::launch<0>(c, m, params, hs, maps, ws, h0, store);
+}
+
+// backward big steps t = t_top .. 1 in one persistent launch
+void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
+                              const int32_t* h_offs, Workspace& ws) {
+  const int H = m.H, H3 = 3 * H;
+  std::vector<sg::Step> hs;
+  std::vector<CUtensorMap> maps;
+  for (int t = t_top; t >= 1; --t) {
+    const int B = h_bs[t], Bp = h_bs[t - 1];
+    hs.push_back(sg::make_step(B, Bp, h_offs[t], h_offs[t - 1], H, H3, c->num_sms));
+    maps.push_back(tc::make_map(ws.dhu.p + (size_t)h_offs[t] * H3, std::max(B, 1), H3, H3, tc::BM, false));
+  }
+  sg::launch<1>(c, m, params, hs, maps, ws, nullptr, false);
+}
+
+}  // namespace verg
