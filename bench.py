@@ -58,8 +58,13 @@ def dom_traffic(dom):
     if not p.exists():
         return None
     d = json.loads(p.read_text())
-    k = "gru_bwd_ks" if dom == "rec_bwd" else "gru_fwd_ks"
-    return d.get(k, {}).get("dram_bytes_per_launch")
+    # one minibatch of one direction = one K-split launch + one persistent step-kernel
+    # launch (the cluster tail moves a few MB); both captured from the same update
+    ks = d.get("gru_bwd_ks" if dom == "rec_bwd" else "gru_fwd_ks", {}).get("dram_bytes_per_launch")
+    sg = d.get("gru_step_gemm_bwd" if dom == "rec_bwd" else "gru_step_gemm_fwd", {}).get("dram_bytes_per_launch")
+    if ks is None:
+        return None
+    return ks + (sg or 0.0)
 
 
 # ------------------------------------------------------------------ clocks
@@ -328,8 +333,8 @@ def run_ours(args, rank, world):
                        "parallelism": f"dp{world} (DD-PPO, NCCL AllReduce per minibatch)" if world > 1 else "dp1"},
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
                          "frac": achieved_tf / bf16s, "traffic": dom_traffic(dom),
-                         "kernel": (f"{'gru_bwd_ks<512> + gru_bwd_tail<512>' if dom == 'rec_bwd' else 'gru_fwd_ks<512> + gru_fwd_tail<512>'}"
-                                    f" (GRU recurrence, fp32 FMA pipe; {n_dom} launches/step over {n_mb} minibatches, "
+                         "kernel": (f"{'gru_step_gemm_kernel<1> + gru_bwd_ks<512> + gru_bwd_tail<512>' if dom == 'rec_bwd' else 'gru_step_gemm_kernel<0> + gru_fwd_ks<512> + gru_fwd_tail<512>'}"
+                                    f" (GRU recurrence: tcgen05 3xTF32 steps >= 150 rows, fp32 FMA pipe below; {n_dom} launches/step over {n_mb} minibatches, "
                                     f"{dom_ms:.3f} ms per minibatch for {rows_per_mb:.0f} rows x 6H^2 FLOP)"),
                          "peak_kind": f"{peaks_kind} bf16 dense sustained",
                          "fp32_simt_peak": simt_peak, "frac_of_fp32_simt": achieved_tf / simt_peak},

@@ -24,6 +24,11 @@ for k in gru_bwd_ks gru_fwd_ks; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
   -o $OUT/prof_$k python scripts/profile_update.py --updates 1 > $OUT/prof_$k.log 2>&1
 done
+for d in 0 1; do
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k "regex:gru_step_gemm_kernel<$d>" -s 2 -c 1 \
+  -o $OUT/prof_gru_step_gemm$d python scripts/profile_update.py --updates 1 > $OUT/prof_gru_step_gemm$d.log 2>&1
+done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 20 -c 2 \
   -o $OUT/prof_tc_gemm python scripts/profile_update.py --updates 1 > $OUT/prof_tc_gemm.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"gae_scan|gather_tiled" -c 3 \
