@@ -182,6 +182,13 @@ int env_int(const char* name, int dflt);
 inline unsigned cdiv(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 
 // Launch accounting + error check after every kernel launch.
+// GRU gate nonlinearities (nn.cpp:235-250) of every recurrence kernel, on the
+// SFU (ex2 + rcp): absolute error ~1e-7, far inside the 1e-5 parity bar, and
+// both tails saturate exactly (exp -> 0 / inf).  They sit on the per-step
+// critical path of the recurrence, where expf / tanhf cost ~3x the latency.
+__device__ __forceinline__ float gate_sigm(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+__device__ __forceinline__ float gate_tanh(float x) { return 1.f - __fdividef(2.f, 1.f + __expf(2.f * x)); }
+
 inline void after_launch(Ctx* c) {
   c->launches++;
   cudaError_t e = cudaGetLastError();

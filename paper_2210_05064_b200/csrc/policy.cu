@@ -312,7 +312,6 @@ __global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs
   }
 }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
 void policy_forward(Ctx* c, const Model& m, const float* params, int S, const float* obs, const float* h0,
                     int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store,
@@ -385,9 +384,9 @@ __global__ void gru_gate_fwd_kernel(int B, int H, int Z, const float* __restrict
   float hn[4], g[12];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float rg = 1.f / (1.f + expf(-(x[3 * q] + s[3 * q])));
-    const float zg = 1.f / (1.f + expf(-(x[3 * q + 1] + s[3 * q + 1])));
-    const float ng = tanhf(x[3 * q + 2] + rg * s[3 * q + 2]);
+    const float rg = gate_sigm(x[3 * q] + s[3 * q]);
+    const float zg = gate_sigm(x[3 * q + 1] + s[3 * q + 1]);
+    const float ng = gate_tanh(x[3 * q + 2] + rg * s[3 * q + 2]);
     hn[q] = (1.f - zg) * ng + zg * hpv[q];
     g[3 * q] = rg;
     g[3 * q + 1] = zg;

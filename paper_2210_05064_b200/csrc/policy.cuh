@@ -77,6 +77,13 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
                              const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
 void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
                               const int32_t* h_offs, Workspace& ws);
+// the same steps on 4-CTA clusters with the split-K reduction and the gates fused
+// into the epilogue, one grid barrier per step (stepfused.cu; H = 256 / 512)
+bool step_fused_ok(int H, bool backward);
+void gru_forward_big_fused(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
+                           const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
+void gru_backward_big_fused(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
+                            const int32_t* h_offs, Workspace& ws);
 
 // Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
 // dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights

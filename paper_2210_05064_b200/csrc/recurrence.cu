@@ -44,7 +44,6 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
   __syncthreads();
 }
 
-__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
 
 struct RecGeom {
   int UB, RB;
@@ -120,9 +119,9 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_persistent(
         const int u = u0 + ul;
         const size_t p = (size_t)o + c0 + row;
         const float* x = xp + p * H3 + 3 * u;
-        const float r = sigm(x[0] + sr);
-        const float z = sigm(x[1] + sz);
-        const float n = tanhf(x[2] + r * sn);
+        const float r = gate_sigm(x[0] + sr);
+        const float z = gate_sigm(x[1] + sz);
+        const float n = gate_tanh(x[2] + r * sn);
         const float hprev = hs[row * H + u];
         hidden[p * H + u] = (1.f - z) * n + z * hprev;
         if (gates) {
@@ -441,9 +440,9 @@ __global__ void __launch_bounds__(RT, 1) gru_fwd_reg(
         if (owner) {
           const int u = ua + pq;
           const int row = g0 + pr;
-          const float rg = sigm(x0 + mine);
-          const float zg = sigm(x1 + sz);
-          const float ng = tanhf(x2 + rg * sn);
+          const float rg = gate_sigm(x0 + mine);
+          const float zg = gate_sigm(x1 + sz);
+          const float ng = gate_tanh(x2 + rg * sn);
           const float hprev = hs[row * H + u];
           hidden[p * H + u] = (1.f - zg) * ng + zg * hprev;
           if (gates) {
@@ -758,9 +757,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
         }
         const int u = u0 + ul;
         const size_t p = (size_t)o + rm.row(c0 + row);
-        const float rg = sigm(xr[k][0] + sr);
-        const float zg = sigm(xr[k][1] + sz);
-        const float ng = tanhf(xr[k][2] + rg * sn);
+        const float rg = gate_sigm(xr[k][0] + sr);
+        const float zg = gate_sigm(xr[k][1] + sz);
+        const float ng = gate_tanh(xr[k][2] + rg * sn);
         const float hprev = hc[row * H + u];
         hidden[p * H + u] = (1.f - zg) * ng + zg * hprev;
         if (gates) {
@@ -1135,9 +1134,9 @@ __global__ void __launch_bounds__(TC_T, 1) gru_fwd_tail(
         sz += rq[1];
         sn += rq[2];
       }
-      const float rg = sigm(x0 + sr);
-      const float zg = sigm(x1 + sz);
-      const float ng = tanhf(x2 + rg * sn);
+      const float rg = gate_sigm(x0 + sr);
+      const float zg = gate_sigm(x1 + sz);
+      const float ng = gate_tanh(x2 + rg * sn);
       const float hprev = hc[j * H + u];
       const float hnew = (1.f - zg) * ng + zg * hprev;
       const size_t p = (size_t)o + j;
@@ -1349,7 +1348,9 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   // FMA kernel, then the cluster tail
   const int tb = (h_bs && h_offs && pick_fwd_ks(m.H) && rec_mode() == 0) ? gru_big_steps(c, m, h_bs, L, false) : 0;
   if (tb > 0) {
-    if (step_gemm_enabled()) {
+    if (step_fused_ok(m.H, false)) {
+      gru_forward_big_fused(c, m, params, tb, h_bs, h_offs, ws, h0, store);
+    } else if (step_gemm_enabled()) {
       gru_forward_big_persist(c, m, params, tb, h_bs, h_offs, ws, h0, store);
     } else {
       ScopedEv ev(c, c->rec_tag);
@@ -1493,7 +1494,9 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
       trace_dump(c, "bwd", L, d_bs, tr);
     }
     if (t_big > 0) {
-      if (step_gemm_enabled()) {
+      if (step_fused_ok(m.H, true)) {
+        gru_backward_big_fused(c, m, params, t_big, h_bs, h_offs, ws);
+      } else if (step_gemm_enabled()) {
         gru_backward_big_persist(c, m, params, t_big, h_bs, h_offs, ws);
       } else {
         ScopedEv ev(c, c->rec_tag);

@@ -48,7 +48,18 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned& target) {
   __syncthreads();
 }
 
-__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+// VER_REC_TRACE slots per step (CTA 0): start, first stage landed, last
+// accumulator ready, partial stored, GEMM-phase barrier passed, gate done
+constexpr int TR = 6;
+// K-blocks per TMEM accumulation group (tc::PROMOTE in the general GEMM): the
+// split-K items here hold <= 4 K-blocks at C2, so one drain per item
+constexpr int SGP = 4;
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 
 template <int DIR>  // 0 forward (B MN-major: U stored K x N), 1 backward (B K-major: U stored N x K)
 __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
@@ -106,13 +117,18 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
   unsigned target = 0;
   // pipeline counters, continued across steps (each role advances its own)
   int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
+  int b_pre = 0;  // producer: B tiles of this step's first stages already issued
+  auto load_b = [&](int s, int k0, int n0) {
+    if (BMAJ == 0) {
+      tma_load_2d(tile(s, 2), &bmap, full_bar(s), k0, n0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &bmap, full_bar(s), n0 + 32 * c, k0);
+    }
+  };
 
   for (int si = 0; si < nsteps; ++si) {
-    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
-      long long tn;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tn));
-      trace[2 * si] = tn;
-    }
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si] = gtimer();
     const Step S = steps[si];
     const int W = S.tilesM * tilesN * S.Z;
     const int item = blockIdx.x;
@@ -128,15 +144,31 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           for (int i = 0; i < nkb; ++i, ++it_tma) {
             const int s = it_tma % STAGES;
             const uint32_t ph = (it_tma / STAGES) & 1;
-            mbar_wait(empty_bar(s), ph ^ 1);
-            mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
             const int k0 = (kb0 + i) * BK;
+            if (i >= b_pre) {
+              mbar_wait(empty_bar(s), ph ^ 1);
+              mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+              load_b(s, k0, n0);
+            }
             tma_load_2d(tile(s, 0), amap, full_bar(s), k0, m0);
-            if (BMAJ == 0) {
-              tma_load_2d(tile(s, 2), &bmap, full_bar(s), k0, n0);
-            } else {
-#pragma unroll
-              for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &bmap, full_bar(s), n0 + 32 * c, k0);
+          }
+          // the next step's first B tiles (U does not change across steps) and its
+          // A tensor map, issued before the grid barriers
+          b_pre = 0;
+          if (si + 1 < nsteps) {
+            const Step S2 = steps[si + 1];
+            if (S2.B > 0 && item < S2.tilesM * tilesN * S2.Z) {
+              asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(amaps + si + 1)) : "memory");
+              const int z2 = item / tilesN / S2.tilesM;
+              const int kb2 = z2 * S2.per;
+              const int nkb2 = max(0, min(nkb_total, kb2 + S2.per) - kb2);
+              b_pre = min(nkb2, STAGES);
+              for (int i = 0; i < b_pre; ++i) {
+                const int s = (it_tma + i) % STAGES;
+                mbar_wait(empty_bar(s), ((it_tma + i) / STAGES & 1) ^ 1);
+                mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+                load_b(s, (kb2 + i) * BK, (item % tilesN) * BN);
+              }
             }
           }
         }
@@ -148,7 +180,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           for (int i = 0; i < nkb; ++i, ++it_mma) {
             const int s = it_mma % STAGES;
             const uint32_t ph = (it_mma / STAGES) & 1;
-            const bool first = (i % PROMOTE) == 0;
+            const bool first = (i % SGP) == 0;
             if (first) {
               buf = g_mma % NACC;
               const int u = g_mma / NACC;
@@ -166,7 +198,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
               mma_tf32(d, ah, operand_desc<BMAJ>(tile(s, 3), kk), idesc, 1u);
             }
             umma_commit(empty_bar(s));
-            if ((i % PROMOTE) == PROMOTE - 1 || i == nkb - 1) {
+            if ((i % SGP) == SGP - 1 || i == nkb - 1) {
               umma_commit(acc_full(buf));
               ++g_mma;
             }
@@ -179,6 +211,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           const int s = it_split % STAGES;
           const uint32_t ph = (it_split / STAGES) & 1;
           mbar_wait(full_bar(s), ph);
+          if (trace && i == 0 && threadIdx.x == 64 && blockIdx.x == 0) trace[TR * si + 1] = gtimer();
           uint8_t* st = smem + s * STAGE_BYTES;
           float4* ahi = reinterpret_cast<float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
@@ -197,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
         // accumulator promotion + partial-tile epilogue: part[z][m][n]
         const int lane_base = 32 * (warp & 3);
         float* stg = stg_all + (warp & 3) * 32 * EPI_LD;
-        const int ngroups = (nkb + PROMOTE - 1) / PROMOTE;
+        const int ngroups = (nkb + SGP - 1) / SGP;
         float sums[BN];
 #pragma unroll
         for (int j = 0; j < BN; ++j) sums[j] = 0.f;
@@ -205,6 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           const int buf = g_epi % NACC;
           mbar_wait(acc_full(buf), (g_epi / NACC) & 1);
           tc_fence_after();
+          if (trace && gq == ngroups - 1 && threadIdx.x == 192 && blockIdx.x == 0) trace[TR * si + 2] = gtimer();
 #pragma unroll
           for (int cc = 0; cc < BN / 32; ++cc) {
             uint32_t r[32];
@@ -245,14 +279,11 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           }
           __syncwarp();
         }
+        if (trace && threadIdx.x == 192 && blockIdx.x == 0) trace[TR * si + 3] = gtimer();
       }
     }
     grid_sync(bar, target);  // all partials of step si written
-    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
-      long long tn;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tn));
-      trace[2 * si + 1] = tn;
-    }
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
 
     // ---------------- gate phase: (row j, units 4x .. 4x+3) over the grid
     const int H4 = H / 4;
@@ -265,11 +296,14 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
         float s12[12];
 #pragma unroll
         for (int e = 0; e < 12; ++e) s12[e] = 0.f;
-        for (int z = 0; z < S.Z; ++z) {
-          const float4* p4 = reinterpret_cast<const float4*>(part + z * zs + prow);
-          const float4 a = p4[0], b = p4[1], c = p4[2];
-          s12[0] += a.x; s12[1] += a.y; s12[2] += a.z; s12[3] += a.w; s12[4] += b.x; s12[5] += b.y;
-          s12[6] += b.z; s12[7] += b.w; s12[8] += c.x; s12[9] += c.y; s12[10] += c.z; s12[11] += c.w;
+#pragma unroll
+        for (int z = 0; z < 8; ++z) {
+          if (z < S.Z) {  // predicated, so all Z partial loads are in flight together
+            const float4* p4 = reinterpret_cast<const float4*>(part + z * zs + prow);
+            const float4 a = p4[0], b = p4[1], c = p4[2];
+            s12[0] += a.x; s12[1] += a.y; s12[2] += a.z; s12[3] += a.w; s12[4] += b.x; s12[5] += b.y;
+            s12[6] += b.z; s12[7] += b.w; s12[8] += c.x; s12[9] += c.y; s12[10] += c.z; s12[11] += c.w;
+          }
         }
         const float4* x4 = reinterpret_cast<const float4*>(xp + row3);
         const float4 xa = x4[0], xb = x4[1], xc = x4[2];
@@ -280,9 +314,9 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
         float hn[4], g[12];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float rg = sigm(x[3 * e] + s12[3 * e]);
-          const float zg = sigm(x[3 * e + 1] + s12[3 * e + 1]);
-          const float ng = tanhf(x[3 * e + 2] + rg * s12[3 * e + 2]);
+          const float rg = gate_sigm(x[3 * e] + s12[3 * e]);
+          const float zg = gate_sigm(x[3 * e + 1] + s12[3 * e + 1]);
+          const float ng = gate_tanh(x[3 * e + 2] + rg * s12[3 * e + 2]);
           hn[e] = (1.f - zg) * ng + zg * hpv[e];
           g[3 * e] = rg;
           g[3 * e + 1] = zg;
@@ -301,9 +335,12 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
         const size_t row = ((size_t)S.op + j) * H + 4 * (size_t)u4, row3 = ((size_t)S.op + j) * H3 + 12 * (size_t)u4;
         float dh[4] = {0.f, 0.f, 0.f, 0.f};
         if (j < S.B) {
-          for (int z = 0; z < S.Z; ++z) {
-            const float4 p = *reinterpret_cast<const float4*>(part + z * zs + (size_t)j * H + 4 * u4);
-            dh[0] += p.x; dh[1] += p.y; dh[2] += p.z; dh[3] += p.w;
+#pragma unroll
+          for (int z = 0; z < 8; ++z) {
+            if (z < S.Z) {
+              const float4 p = *reinterpret_cast<const float4*>(part + z * zs + (size_t)j * H + 4 * u4);
+              dh[0] += p.x; dh[1] += p.y; dh[2] += p.z; dh[3] += p.w;
+            }
           }
           const float4 q = *reinterpret_cast<const float4*>(gz + ((size_t)S.o + j) * H + 4 * u4);
           dh[0] += q.x; dh[1] += q.y; dh[2] += q.z; dh[3] += q.w;
@@ -346,6 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
         *reinterpret_cast<float4*>(gz + row) = make_float4(gzv[0], gzv[1], gzv[2], gzv[3]);
       }
     }
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 5] = gtimer();
     if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
   }
   tc_fence_before();
@@ -422,8 +460,8 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
   long long* tr = nullptr;
   const char* tpath = getenv("VER_REC_TRACE");
   if (tpath) {
-    ws.trace.reserve(c, 2 * (size_t)nsteps);
-    ws.trace.zero(2 * (size_t)nsteps);
+    ws.trace.reserve(c, TR * (size_t)nsteps + 1);
+    ws.trace.zero(TR * (size_t)nsteps + 1);
     tr = ws.trace.p;
   }
   void* args[] = {&ns,     &dsteps, &dmaps, const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H), &part, &bar,
@@ -434,14 +472,18 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     after_launch(c);
   }
   if (tr) {
-    std::vector<long long> h(2 * (size_t)nsteps);
+    std::vector<long long> h(TR * (size_t)nsteps);
     VER_CUDA(cudaMemcpyAsync(h.data(), tr, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, c->stream));
     VER_CUDA(cudaStreamSynchronize(c->stream));
+    // per step: rows, Z, then each slot and the next step's start relative to this step's start (ns)
     if (FILE* f = fopen(tpath, "a")) {
       fprintf(f, "persist%d %d", DIR, nsteps);
-      for (int i = 0; i < nsteps; ++i)
-        fprintf(f, " %d:%lld:%lld", hs[i].Bg, h[2 * i + 1] - h[2 * i],
-                (i + 1 < nsteps ? h[2 * i + 2] : h[2 * i + 1]) - h[2 * i + 1]);
+      for (int i = 0; i < nsteps; ++i) {
+        const long long t0 = h[TR * i];
+        fprintf(f, " %d:%d", hs[i].Bg, hs[i].Z);
+        for (int k = 1; k < TR; ++k) fprintf(f, ":%lld", h[TR * i + k] ? h[TR * i + k] - t0 : -1);
+        fprintf(f, ":%lld", i + 1 < nsteps ? h[TR * (i + 1)] - t0 : -1);
+      }
       fprintf(f, "\n");
       fclose(f);
     }
