@@ -262,6 +262,64 @@ typedef struct {
 } ver_train_stats; /* TrainStats (learner.hpp:55-71) */
 
 typedef struct ver_learner_s* ver_learner;
+
+/* ------------------------------------- inference engine */
+/* InferenceEngine (runtime.hpp:96-160, runtime.cpp:60-229) on the device: the
+   policy snapshot, every env's GRU state and the pending records' h_before stay
+   in device memory; act (nn.cpp:118-126) runs batched on the GPU and actions are
+   sampled there with the reference's counter RNG stream
+   CounterRng(seed).stream(0xAC7101, env).stream(obs_episode, obs_step)
+   (runtime.cpp:166-169); completed steps are appended to the engine's own
+   rollout store (h_before copied device to device, only for records that
+   start a sequence). */
+typedef struct {
+  ver_rollout_config rollout; /* RolloutBuffer config (runtime.cpp:64-74) */
+  ver_model_config model;
+  uint64_t seed;              /* RuntimeConfig::seed */
+} ver_engine_config;
+
+/* InferenceRequest (runtime.hpp:30-42), SoA; NULL optional fields read as 0 */
+typedef struct {
+  int n;
+  const int32_t* env_index;
+  const float* obs;           /* n x obs_dim */
+  const float* reward;
+  const uint8_t* done;
+  const uint8_t* first;       /* initial request after reset: completes nothing */
+  const float* latency;
+  const int64_t* obs_episode;
+  const int32_t* obs_step;
+} ver_request_batch;
+
+/* InferenceEngine::BatchResult (runtime.hpp:102-106); the dispatches go to the
+   caller's arrays (env, discrete action or act_dim floats), n_dispatch of them */
+typedef struct {
+  int n_dispatch;
+  int new_commits;
+  int closed_now;
+} ver_batch_result;
+
+typedef struct ver_engine_s* ver_engine;
+/* InferenceEngine(cfg, snapshot) (runtime.cpp:76-80): params in tensors() order */
+ver_status ver_engine_create(ver_ctx ctx, const ver_engine_config* cfg, const float* params, uint64_t version,
+                             ver_engine* out);
+ver_status ver_engine_destroy(ver_engine e);
+/* set_snapshot (runtime.cpp:82): from host params, or device to device from a learner */
+ver_status ver_engine_set_snapshot(ver_engine e, const float* params, uint64_t version);
+ver_status ver_engine_set_snapshot_learner(ver_engine e, ver_learner l, uint64_t version);
+/* begin_rollout (runtime.cpp:84-113): dispatch arrays hold >= N entries */
+ver_status ver_engine_begin_rollout(ver_engine e, ver_batch_result* res, int32_t* disp_env, int32_t* disp_act,
+                                    float* disp_act_cont);
+/* process_batch (runtime.cpp:192-215): dispatch arrays hold >= reqs->n entries */
+ver_status ver_engine_process_batch(ver_engine e, const ver_request_batch* reqs, ver_batch_result* res,
+                                    int32_t* disp_env, int32_t* disp_act, float* disp_act_cont);
+ver_status ver_engine_force_close(ver_engine e);        /* runtime.hpp:120 */
+ver_status ver_engine_finalize_bootstraps(ver_engine e); /* runtime.cpp:217-229 */
+ver_status ver_engine_close(ver_engine e, ver_view* out); /* runtime.cpp:231-234 */
+ver_status ver_engine_state(ver_engine e, int* open, int* committed, int* capacity, int* carryover,
+                            int* active_envs);
+/* every env's current GRU state, N x hidden_dim (tests) */
+ver_status ver_engine_hidden(ver_engine e, float* h_out);
 /* Learner(params, cfg, entropy, schedule, run_seed) (learner.cpp:43-50) */
 ver_status ver_learner_create(ver_ctx ctx, const ver_model_config* c, const float* params,
                               const ver_ppo_config* cfg, const ver_entropy_controller* ec,

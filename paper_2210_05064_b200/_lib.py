@@ -60,6 +60,20 @@ class ModelConfig(C.Structure):
                 ("action_kind", c_int), ("num_actions", c_int), ("act_dim", c_int)]
 
 
+class EngineConfig(C.Structure):
+    _fields_ = [("rollout", RolloutConfig), ("model", ModelConfig), ("seed", c_uint64)]
+
+
+class RequestBatch(C.Structure):
+    _fields_ = [("n", c_int), ("env_index", P(c_int32)), ("obs", P(c_float)), ("reward", P(c_float)),
+                ("done", P(C.c_uint8)), ("first", P(C.c_uint8)), ("latency", P(c_float)),
+                ("obs_episode", P(c_int64)), ("obs_step", P(c_int32))]
+
+
+class BatchResult(C.Structure):
+    _fields_ = [("n_dispatch", c_int), ("new_commits", c_int), ("closed_now", c_int)]
+
+
 class PPOConfig(C.Structure):
     _fields_ = [("gamma", c_double), ("gae_lambda", c_double), ("clip", c_double),
                 ("epochs", c_int), ("minibatches", c_int), ("value_loss_coef", c_double),
@@ -160,6 +174,18 @@ _SIGS = {
                                P(c_float), c_int, P(c_float), c_int]),
     "ver_debug_gemm_time": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                     P(c_float)]),
+    "ver_engine_create": (c_int, [C.c_void_p, P(EngineConfig), P(c_float), c_uint64, P(C.c_void_p)]),
+    "ver_engine_destroy": (c_int, [C.c_void_p]),
+    "ver_engine_set_snapshot": (c_int, [C.c_void_p, P(c_float), c_uint64]),
+    "ver_engine_set_snapshot_learner": (c_int, [C.c_void_p, C.c_void_p, c_uint64]),
+    "ver_engine_begin_rollout": (c_int, [C.c_void_p, P(BatchResult), P(c_int32), P(c_int32), P(c_float)]),
+    "ver_engine_process_batch": (c_int, [C.c_void_p, P(RequestBatch), P(BatchResult), P(c_int32), P(c_int32),
+                                         P(c_float)]),
+    "ver_engine_force_close": (c_int, [C.c_void_p]),
+    "ver_engine_finalize_bootstraps": (c_int, [C.c_void_p]),
+    "ver_engine_close": (c_int, [C.c_void_p, P(C.c_void_p)]),
+    "ver_engine_state": (c_int, [C.c_void_p, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int)]),
+    "ver_engine_hidden": (c_int, [C.c_void_p, P(c_float)]),
     "ver_estimate_time": (c_int, [C.c_void_p, P(c_double), c_int, c_int64, c_int64, P(c_double)]),
     "ver_optimal_preempt_steps": (c_int, [C.c_void_p, P(c_double), c_int, c_double, c_int64,
                                           P(c_int64)]),

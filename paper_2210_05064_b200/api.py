@@ -873,4 +873,143 @@ def optimal_preempt_steps(step_times, learn_time: float, max_steps: int,
     return out.value
 
 
+
+
+# --------------------------------------------------------- inference engine
+@dataclass
+class InferenceRequest:
+    """runtime.hpp:30-42."""
+    env_index: int
+    observation: np.ndarray
+    reward: float = 0.0
+    done: bool = False
+    first: bool = False
+    latency: float = 0.0
+    obs_episode: int = 0
+    obs_step: int = 0
+
+
+@dataclass
+class BatchResult:
+    """InferenceEngine::BatchResult (runtime.hpp:98-106): dispatches = [(env, action)]."""
+    dispatches: list
+    new_commits: int = 0
+    closed_now: bool = False
+
+
+class InferenceEngine:
+    """InferenceEngine (runtime.hpp:96-160) on the device: batched act + on-device
+    sampling with the reference's counter-RNG streams; every env's GRU state and
+    the pending h_before stay in device memory; completed steps go into the
+    engine's own rollout store (closed with close())."""
+
+    def __init__(self, model: ModelConfig, T: int, N: int, params: np.ndarray, version: int = 0,
+                 mode: int = VARIABLE, seed: int = 0, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.model = model
+        self.N = N
+        mc = model.c()
+        rc = L.RolloutConfig(T, N, mode, model.action_kind, model.obs_dim,
+                             model.act_dim if model.action_kind == 1 else 0, model.hidden_dim)
+        self.cfg = L.EngineConfig(rc, mc, seed)
+        self.h = C.c_void_p()
+        p = _f32(params)
+        _check(_lib().ver_engine_create(self.ctx.h, C.byref(self.cfg), _ptr(p, C.c_float), version,
+                                        C.byref(self.h)))
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().ver_engine_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def set_snapshot(self, params, version: int):
+        p = _f32(params)
+        _check(_lib().ver_engine_set_snapshot(self.h, _ptr(p, C.c_float), version))
+
+    def set_snapshot_from(self, learner: "Learner", version: int):
+        """Device-to-device snapshot of a learner's current parameters."""
+        _check(_lib().ver_engine_set_snapshot_learner(self.h, learner.h, version))
+
+    def _result(self, r: L.BatchResult, env, act_d, act_c) -> BatchResult:
+        n = r.n_dispatch
+        if self.model.action_kind == 1:
+            d = [(int(env[i]), act_c[i].copy()) for i in range(n)]
+        else:
+            d = [(int(env[i]), int(act_d[i])) for i in range(n)]
+        return BatchResult(d, r.new_commits, bool(r.closed_now))
+
+    def _bufs(self, n: int):
+        A = max(1, self.model.act_dim if self.model.action_kind == 1 else 1)
+        return (np.zeros(max(n, 1), np.int32), np.zeros(max(n, 1), np.int32),
+                np.zeros((max(n, 1), A), np.float32))
+
+    def begin_rollout(self) -> BatchResult:
+        env, ad, ac = self._bufs(self.N)
+        r = L.BatchResult()
+        _check(_lib().ver_engine_begin_rollout(self.h, C.byref(r), _ptr(env, C.c_int32), _ptr(ad, C.c_int32),
+                                               _ptr(ac, C.c_float)))
+        return self._result(r, env, ad, ac)
+
+    def process_batch(self, reqs: Sequence[InferenceRequest]) -> BatchResult:
+        n = len(reqs)
+        D = self.model.obs_dim
+        envs = np.array([q.env_index for q in reqs], np.int32)
+        obs = np.zeros((max(n, 1), D), np.float32)
+        for i, q in enumerate(reqs):
+            obs[i] = np.asarray(q.observation, np.float32).reshape(D)
+        rw = np.array([q.reward for q in reqs], np.float32)
+        dn = np.array([1 if q.done else 0 for q in reqs], np.uint8)
+        fs = np.array([1 if q.first else 0 for q in reqs], np.uint8)
+        lat = np.array([q.latency for q in reqs], np.float32)
+        oe = np.array([q.obs_episode for q in reqs], np.int64)
+        os_ = np.array([q.obs_step for q in reqs], np.int32)
+        b = L.RequestBatch(n, _ptr(envs, C.c_int32), _ptr(obs, C.c_float), _ptr(rw, C.c_float),
+                           _ptr(dn, C.c_uint8), _ptr(fs, C.c_uint8), _ptr(lat, C.c_float),
+                           _ptr(oe, C.c_int64), _ptr(os_, C.c_int32))
+        env, ad, ac = self._bufs(n)
+        r = L.BatchResult()
+        _check(_lib().ver_engine_process_batch(self.h, C.byref(b), C.byref(r), _ptr(env, C.c_int32),
+                                               _ptr(ad, C.c_int32), _ptr(ac, C.c_float)))
+        return self._result(r, env, ad, ac)
+
+    def force_close(self):
+        _check(_lib().ver_engine_force_close(self.h))
+
+    def finalize_bootstraps(self):
+        _check(_lib().ver_engine_finalize_bootstraps(self.h))
+
+    def close(self) -> RolloutView:
+        out = C.c_void_p()
+        _check(_lib().ver_engine_close(self.h, C.byref(out)))
+        return RolloutView(out, self.ctx)
+
+    def _state(self):
+        v = [C.c_int() for _ in range(5)]
+        _check(_lib().ver_engine_state(self.h, *[C.byref(x) for x in v]))
+        return [x.value for x in v]
+
+    def rollout_done(self) -> bool:
+        return not self._state()[0]
+
+    def committed(self) -> int:
+        return self._state()[1]
+
+    def capacity(self) -> int:
+        return self._state()[2]
+
+    def carryover_count(self) -> int:
+        return self._state()[3]
+
+    def active_envs(self) -> int:
+        return self._state()[4]
+
+    def hidden(self) -> np.ndarray:
+        h = np.zeros((self.N, self.model.hidden_dim), np.float32)
+        _check(_lib().ver_engine_hidden(self.h, _ptr(h, C.c_float)))
+        return h
+
+
 __all__ = [n for n in dir() if not n.startswith("_")] + ["SEQ_FIELDS"]

@@ -380,7 +380,7 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
   ++Ln.update_index;
 }
 
-static void to_device_layout(const Model& m, const float* tensors_order, std::vector<float>& dev) {
+void to_device_layout(const Model& m, const float* tensors_order, std::vector<float>& dev) {
   dev.assign(m.P, 0.f);
   for (int64_t k = 0; k < m.P; ++k) dev[m.dev_index[k]] = tensors_order[k];
 }
@@ -395,6 +395,15 @@ using namespace verg;
 struct ver_learner_s {
   Learner l;
 };
+
+namespace verg {
+// the learner's current parameters (device layout) for the inference engine's snapshot
+const float* learner_device_params(ver_learner_s* l, Ctx** ctx, int64_t* count) {
+  *ctx = l->l.ctx;
+  *count = l->l.m.P;
+  return l->l.params.p;
+}
+}  // namespace verg
 
 extern "C" {
 

@@ -14,6 +14,8 @@
 
 #include "packed.cuh"
 
+struct ver_learner_s;
+
 namespace verg {
 
 struct Model {
@@ -120,5 +122,10 @@ void adam_update(Ctx* c, const Model& m, float* params, const float* grad, float
 
 // Host-double parameter init in tensors() order (nn.cpp:16-81).
 void init_params_host(const ver_model_config& c, uint64_t seed, double* out);
+
+// tensors()-order host parameters -> device layout (learner.cu)
+void to_device_layout(const Model& m, const float* tensors_order, std::vector<float>& dev);
+// the learner's device parameters (learner.cu), for the inference engine's snapshot
+const float* learner_device_params(ver_learner_s* l, Ctx** ctx, int64_t* count);
 
 }  // namespace verg

@@ -18,7 +18,7 @@
 #include <algorithm>
 #include <cstring>
 
-#include "view.cuh"
+#include "rollout.cuh"
 
 namespace verg {
 
@@ -170,7 +170,7 @@ __global__ void seq_ids_kernel(const uint8_t* __restrict__ flag, const int32_t* 
 __global__ void seq_desc_kernel(const int32_t* __restrict__ starts, int K, int S, int seq_id_base,
                                 const int32_t* __restrict__ env_index,
                                 const int32_t* __restrict__ hslot_by_slot,
-                                const float* __restrict__ hlog, int H,
+                                const float* __restrict__ hlog, const float* __restrict__ hdev, int H,
                                 ver_seq_desc* __restrict__ seqs, float* __restrict__ h0) {
   const int k = blockIdx.x;
   if (k >= K) return;
@@ -190,207 +190,13 @@ __global__ void seq_desc_kernel(const int32_t* __restrict__ starts, int K, int S
   }
   const int hs = hslot_by_slot ? hslot_by_slot[st] : -1;
   float* dst = h0 + (size_t)k * H;
-  if (hs >= 0) {
-    const float* src = hlog + (size_t)hs * H;
+  if (hs >= 0 || hs <= -3) {  // host-logged row, or a device row of the inference engine
+    const float* src = hs >= 0 ? hlog + (size_t)hs * H : hdev + (size_t)(-3 - hs) * H;
     for (int j = threadIdx.x; j < H; j += blockDim.x) dst[j] = src[j];
   } else {
     for (int j = threadIdx.x; j < H; j += blockDim.x) dst[j] = 0.f;
   }
 }
-
-// ------------------------------------------------------------ RolloutBuffer
-template <class T>
-struct Pinned {
-  T* p = nullptr;
-  size_t n = 0;
-  ~Pinned() {
-    if (p) cudaFreeHost(p);
-  }
-  void ensure(size_t count, size_t keep = 0) {
-    if (count <= n) return;
-    size_t want = std::max(count, n * 2);
-    T* q = nullptr;
-    VER_CUDA(cudaMallocHost(reinterpret_cast<void**>(&q), std::max<size_t>(want, 1) * sizeof(T)));
-    if (p && keep) std::memcpy(q, p, keep * sizeof(T));
-    if (p) cudaFreeHost(p);
-    p = q;
-    n = want;
-  }
-};
-
-struct CarryRec {
-  int32_t env, step;
-  int64_t episode;
-  std::vector<float> obs, act_cont, h;
-  int32_t act_disc;
-  float log_prob, value, reward, latency;
-  uint8_t done, has_h;
-  uint64_t version;
-};
-
-struct Rollout {
-  Ctx* ctx = nullptr;
-  ver_rollout_config cfg{};
-  bool open = false;
-  uint64_t snapshot_version = 0;
-  int committed = 0;
-  std::vector<int32_t> counts;
-  std::vector<uint8_t> last_done;
-  int envs_at_cap = 0;
-  std::vector<CarryRec> carry;
-  std::vector<uint8_t> has_carry;
-  std::vector<float> bootstrap;
-  std::vector<uint8_t> bootstrap_valid;
-  int next_seq_id = 0;
-  // pinned arrival log (capacity T*N)
-  Pinned<int32_t> env, rank, hslot, act_disc, step;
-  Pinned<float> obs, act_cont, log_prob, value, reward, latency, hlog;
-  Pinned<uint8_t> done;
-  Pinned<int64_t> episode;
-  Pinned<uint64_t> version;
-  int h_used = 0;
-  // device mirror
-  DBuf<int32_t> d_env, d_rank, d_hslot, d_act_disc, d_step;
-  DBuf<float> d_obs, d_act_cont, d_log_prob, d_value, d_reward, d_latency, d_hlog;
-  DBuf<uint8_t> d_done;
-  DBuf<int64_t> d_episode;
-  DBuf<uint64_t> d_version;
-
-  int capacity() const { return cfg.T * cfg.N; }
-
-  void init() {
-    const int C = capacity();
-    counts.assign(cfg.N, 0);
-    last_done.assign(cfg.N, 0);
-    carry.resize(cfg.N);
-    has_carry.assign(cfg.N, 0);
-    bootstrap.assign(cfg.N, 0.f);
-    bootstrap_valid.assign(cfg.N, 0);
-    env.ensure(C);
-    rank.ensure(C);
-    hslot.ensure(C);
-    step.ensure(C);
-    obs.ensure((size_t)C * cfg.obs_dim);
-    if (cfg.action_kind) act_cont.ensure((size_t)C * cfg.act_dim);
-    else act_disc.ensure(C);
-    log_prob.ensure(C);
-    value.ensure(C);
-    reward.ensure(C);
-    latency.ensure(C);
-    done.ensure(C);
-    episode.ensure(C);
-    version.ensure(C);
-    hlog.ensure((size_t)std::max(1, cfg.N) * cfg.hidden_dim);
-  }
-
-  bool env_at_cap(int e) const { return cfg.mode == 0 && counts[e] >= cfg.T; }
-
-  // rollout.cpp:79-93 (rank / sequence-start bookkeeping added)
-  void commit(int32_t e, int64_t episode_, int32_t step_, const float* obs_, int32_t act_d,
-              const float* act_c, float lp, float v, float rw, float lat, uint8_t dn,
-              const float* h, uint64_t ver) {
-    const int r = committed;
-    const int rk = counts[e];
-    const bool start = rk == 0 || last_done[e];
-    int hs = -2;
-    if (start) {
-      if (h) {
-        hlog.ensure((size_t)(h_used + 1) * cfg.hidden_dim, (size_t)h_used * cfg.hidden_dim);
-        std::memcpy(hlog.p + (size_t)h_used * cfg.hidden_dim, h, sizeof(float) * cfg.hidden_dim);
-        hs = h_used++;
-      } else {
-        hs = -1;
-      }
-    }
-    env.p[r] = e;
-    rank.p[r] = rk;
-    hslot.p[r] = hs;
-    episode.p[r] = episode_;
-    step.p[r] = step_;
-    std::memcpy(obs.p + (size_t)r * cfg.obs_dim, obs_, sizeof(float) * cfg.obs_dim);
-    if (cfg.action_kind) std::memcpy(act_cont.p + (size_t)r * cfg.act_dim, act_c, sizeof(float) * cfg.act_dim);
-    else act_disc.p[r] = act_d;
-    log_prob.p[r] = lp;
-    value.p[r] = v;
-    reward.p[r] = rw;
-    latency.p[r] = lat;
-    done.p[r] = dn;
-    version.p[r] = ver;
-    ++committed;
-    ++counts[e];
-    last_done[e] = dn;
-    if (cfg.mode == 1) {
-      if (committed >= capacity()) open = false;
-    } else {
-      if (counts[e] == cfg.T) ++envs_at_cap;
-      if (envs_at_cap >= cfg.N) open = false;
-    }
-  }
-
-  // rollout.cpp:39-57
-  void begin(uint64_t sv) {
-    open = true;
-    snapshot_version = sv;
-    committed = 0;
-    h_used = 0;
-    envs_at_cap = 0;
-    std::fill(counts.begin(), counts.end(), 0);
-    std::fill(last_done.begin(), last_done.end(), 0);
-    std::fill(bootstrap.begin(), bootstrap.end(), 0.f);
-    std::fill(bootstrap_valid.begin(), bootstrap_valid.end(), 0);
-    for (int e = 0; e < cfg.N && open; ++e) {
-      if (has_carry[e]) {
-        has_carry[e] = 0;
-        const CarryRec& c = carry[e];
-        commit(c.env, c.episode, c.step, c.obs.data(), c.act_disc, c.act_cont.data(), c.log_prob,
-               c.value, c.reward, c.latency, c.done, c.has_h ? c.h.data() : nullptr, c.version);
-      }
-    }
-  }
-
-  // rollout.cpp:59-77 for record i of the batch
-  int append_one(const ver_step_batch* b, int i) {
-    const int e = b->env_index[i];
-    if (e < 0 || e >= cfg.N) protocol_error("append_step: env_index out of range");
-    const float* h = nullptr;
-    if (b->h_before && (!b->h_before_valid || b->h_before_valid[i]))
-      h = b->h_before + (size_t)i * cfg.hidden_dim;
-    const float* o = b->obs + (size_t)i * cfg.obs_dim;
-    const float* ac = cfg.action_kind ? b->act_cont + (size_t)i * cfg.act_dim : nullptr;
-    const int32_t ad = cfg.action_kind ? 0 : b->act_disc[i];
-    const int64_t ep = b->episode_index ? b->episode_index[i] : 0;
-    const int32_t st = b->step_in_episode ? b->step_in_episode[i] : 0;
-    const float lat = b->latency ? b->latency[i] : 0.f;
-    const uint64_t ver = b->snapshot_version ? b->snapshot_version[i] : 0;
-    if (!open) {
-      if (cfg.mode == 1) {
-        if (has_carry[e])
-          protocol_error("append_step: two pending carryovers for env " + std::to_string(e));
-        CarryRec& c = carry[e];
-        c.env = e;
-        c.step = st;
-        c.episode = ep;
-        c.obs.assign(o, o + cfg.obs_dim);
-        if (ac) c.act_cont.assign(ac, ac + cfg.act_dim);
-        c.act_disc = ad;
-        c.log_prob = b->log_prob[i];
-        c.value = b->value[i];
-        c.reward = b->reward[i];
-        c.latency = lat;
-        c.done = b->done[i] ? 1 : 0;
-        c.has_h = h != nullptr;
-        if (h) c.h.assign(h, h + cfg.hidden_dim);
-        c.version = ver;
-        has_carry[e] = 1;
-      }
-      return 1;
-    }
-    if (env_at_cap(e)) return 1;
-    commit(e, ep, st, o, ad, ac, b->log_prob[i], b->value[i], b->reward[i], lat,
-           b->done[i] ? 1 : 0, h, ver);
-    return 0;
-  }
-};
 
 static void upload_log(Rollout* R, int S) {
   Ctx* c = R->ctx;
@@ -417,7 +223,7 @@ static void upload_log(Rollout* R, int S) {
 }
 
 // rollout.cpp:102-190
-static DView* close_rollout(Rollout* R) {
+DView* close_rollout(Rollout* R) {
   if (R->committed == 0) protocol_error("close_rollout: buffer is empty");
   if (R->open) protocol_error("close_rollout: buffer still open (force_close for preemption)");
   Ctx* c = R->ctx;
@@ -471,7 +277,7 @@ static DView* close_rollout(Rollout* R) {
   V->h0_rows = nK;
   V->alloc_seqs(nK + V->deficit, nK + V->deficit);
   seq_desc_kernel<<<std::max(nK, 1), 128, 0, c->stream>>>(starts.p, nK, S, R->next_seq_id,
-                                                           V->env_index.p, hsl.p, R->d_hlog.p,
+                                                           V->env_index.p, hsl.p, R->d_hlog.p, R->d_hdev.p,
                                                            cfg.hidden_dim, V->seqs.p, V->h0.p);
   after_launch(c);
   R->next_seq_id += nK;
@@ -568,7 +374,7 @@ static DView* synth_view(Ctx* c, const int32_t* lengths, int N, int obs_dim, int
   V->h0_rows = nK;
   V->alloc_seqs(nK, nK);
   seq_desc_kernel<<<std::max(nK, 1), 128, 0, c->stream>>>(starts.p, nK, (int)S, 0, V->env_index.p, nullptr, nullptr,
-                                                           hidden_dim, V->seqs.p, V->h0.p);
+                                                           nullptr, hidden_dim, V->seqs.p, V->h0.p);
   after_launch(c);
   sync(c);
   return V;
@@ -925,10 +731,6 @@ static DView* clone_view(DView& V) {
 }  // namespace verg
 
 using namespace verg;
-
-struct ver_rollout_s {
-  Rollout r;
-};
 
 extern "C" {
 
