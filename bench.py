@@ -309,6 +309,52 @@ def run_ours(args, rank, world):
               "env_steps_per_s": f3 / (ms3 / 1000.0), "phases_ms": l3.last_timing()}
         del l3, view3, buf3
 
+    # ---- collection-side inference engine: every env requests
+    # each batch; one process_batch = requests H2D, act + sampling, actions D2H,
+    # protocol bookkeeping and store appends (wall clock around the C-ABI call)
+    coll = None
+    if rank == 0 and not args.no_collect:
+        NC = 4096
+        eng = V.InferenceEngine(cfg, T_, NC, params, version=1, mode=V.VARIABLE, seed=mix(1, 0xC011), ctx=ctx)
+        eng.begin_rollout()
+        crng = np.random.default_rng(21)
+        envc = np.arange(NC, dtype=np.int32)
+        stp = np.zeros(NC, np.int32)
+        epc = np.zeros(NC, np.int64)
+        eng.process_arrays(envc, crng.standard_normal((NC, D_)).astype(np.float32), first=np.ones(NC, np.uint8),
+                           obs_episode=epc, obs_step=stp)
+        ct = []
+        for b in range(40):
+            stp += 1
+            ob = crng.standard_normal((NC, D_)).astype(np.float32)
+            t0 = time.perf_counter()
+            eng.process_arrays(envc, ob, reward=np.ones(NC, np.float32), done=np.zeros(NC, np.uint8),
+                               obs_episode=epc, obs_step=stp)
+            ct.append(time.perf_counter() - t0)
+            if eng.rollout_done():
+                eng.close()
+                eng.begin_rollout()
+        cms = 1000.0 * statistics.median(ct[5:])
+        coll = {"workload": f"InferenceEngine.process_batch, {NC} envs x 1 step, encoder 2x{E_} + GRU-{H_}, "
+                            f"{A_} discrete actions, counter-RNG sampling on device",
+                "envs": NC, "ms_per_batch": cms, "actions_per_s": NC / (cms / 1000.0),
+                "h2d_bytes_per_batch": NC * (4 * D_ + 4 + 4 + 1 + 1 + 4 + 8 + 4),
+                "d2h_bytes_per_batch": NC * (4 + 4)}
+        if not args.no_cpu:
+            from oracle import engine as OE  # CPU baseline leg only
+            NS = 64
+            oe = OE.Engine(cfg, T_, NS, params.astype(np.float64), version=1, mode=1, seed=mix(1, 0xC011))
+            oe.begin_rollout()
+            oe.process_batch([OE.Request(e, crng.standard_normal(D_), first=True) for e in range(NS)])
+            t0 = time.perf_counter()
+            for b in range(2):
+                oe.process_batch([OE.Request(e, crng.standard_normal(D_), reward=1.0, obs_step=b + 1)
+                                  for e in range(NS)])
+            cdt = time.perf_counter() - t0
+            coll["cpu_baseline"] = {"value": 2 * NS / cdt, "unit": "actions/s", "cores": 1, "kind": "port",
+                                    "sample": f"oracle engine (double act), {NS} envs x 2 batches ({cdt:.1f} s)"}
+        del eng
+
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
         # dominant kernel = the GRU recurrence direction with the larger device time
@@ -349,6 +395,8 @@ def run_ours(args, rank, world):
             line["gae_gather"] = gg
         if c3:
             line["c3"] = c3
+        if coll:
+            line["collect"] = coll
         if not args.no_cpu and world == 1:
             cv, dt, sample = cpu_sample()
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
@@ -366,6 +414,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the GAE+gather ragged sweep point")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (N=4096) update measurement")
+    ap.add_argument("--no-collect", action="store_true", help="skip the inference-engine measurement")
     ap.add_argument("--c5-log2", type=int, default=26, help="log2 steps of the GAE+gather point")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))

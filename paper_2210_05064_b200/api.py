@@ -975,6 +975,31 @@ class InferenceEngine:
                                                _ptr(ad, C.c_int32), _ptr(ac, C.c_float)))
         return self._result(r, env, ad, ac)
 
+    def process_arrays(self, env, obs, reward=None, done=None, first=None, latency=None, obs_episode=None,
+                       obs_step=None):
+        """process_batch over SoA host arrays (no per-request Python objects):
+        returns (BatchResult counts, dispatch env array, dispatch action array)."""
+        n = int(np.asarray(env).size)
+        keep = []
+
+        def arr(x, dt):
+            if x is None:
+                return None
+            a = np.ascontiguousarray(x, dtype=dt)
+            keep.append(a)
+            return a
+
+        b = L.RequestBatch(n, _ptr(arr(env, np.int32), C.c_int32), _ptr(arr(obs, np.float32), C.c_float),
+                           _ptr(arr(reward, np.float32), C.c_float), _ptr(arr(done, np.uint8), C.c_uint8),
+                           _ptr(arr(first, np.uint8), C.c_uint8), _ptr(arr(latency, np.float32), C.c_float),
+                           _ptr(arr(obs_episode, np.int64), C.c_int64), _ptr(arr(obs_step, np.int32), C.c_int32))
+        de, ad, ac = self._bufs(n)
+        r = L.BatchResult()
+        _check(_lib().ver_engine_process_batch(self.h, C.byref(b), C.byref(r), _ptr(de, C.c_int32),
+                                               _ptr(ad, C.c_int32), _ptr(ac, C.c_float)))
+        k = r.n_dispatch
+        return r, de[:k], (ac[:k] if self.model.action_kind == 1 else ad[:k])
+
     def force_close(self):
         _check(_lib().ver_engine_force_close(self.h))
 

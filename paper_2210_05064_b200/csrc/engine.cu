@@ -127,26 +127,21 @@ __host__ inline uint64_t h_splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-struct Request {  // InferenceRequest (runtime.hpp:30-42)
+struct Request {  // InferenceRequest (runtime.hpp:30-42); obs points into the caller's batch
   int env = 0;
-  std::vector<float> obs;
+  const float* obs = nullptr;
   float reward = 0.f, latency = 0.f;
   uint8_t done = 0, first = 0;
   int64_t obs_episode = 0;
   int32_t obs_step = 0;
 };
-struct Pending {  // PendingStep (runtime.hpp:135-144); h_before is row `env` of hb
+struct Parked {  // a parked request owns its observation
+  Request r;
   std::vector<float> obs;
-  int32_t act_d = 0;
-  std::vector<float> act_c;
-  float log_prob = 0.f, value = 0.f;
-  int64_t episode = 0;
-  int32_t t = 0;
-  uint64_t version = 0;
 };
-struct Slot {  // EnvSlot (runtime.hpp:145-150); h lives on the device
-  std::optional<Pending> pending;
-  std::optional<Request> parked;
+struct Slot {  // EnvSlot (runtime.hpp:145-150); h lives on the device, the
+               // PendingStep in the engine's per-env arrays (pend_*)
+  std::optional<Parked> parked;
   bool paused = false;
 };
 struct Result {
@@ -167,6 +162,32 @@ struct Engine {
   uint64_t key0 = 0;
   DBuf<float> h, hb;
   std::vector<Slot> envs;
+  // PendingStep (runtime.hpp:135-144) per env, flat; h_before is row `env` of hb
+  std::vector<uint8_t> has_pend;
+  std::vector<float> pend_obs, pend_ac, pend_lp, pend_v;
+  std::vector<int32_t> pend_ad, pend_t;
+  std::vector<int64_t> pend_ep;
+  std::vector<uint64_t> pend_ver;
+
+  void init_envs(int N) {
+    envs.resize(N);
+    has_pend.assign(N, 0);
+    pend_obs.assign((size_t)N * m.D, 0.f);
+    pend_ac.assign((size_t)N * std::max(1, m.A), 0.f);
+    pend_lp.assign(N, 0.f);
+    pend_v.assign(N, 0.f);
+    pend_ad.assign(N, 0);
+    pend_t.assign(N, 0);
+    pend_ep.assign(N, 0);
+    pend_ver.assign(N, 0);
+  }
+  void park(const Request& r) {
+    Parked p;
+    p.obs.assign(r.obs, r.obs + m.D);
+    p.r = r;
+    envs[r.env].parked = std::move(p);
+    envs[r.env].parked->r.obs = envs[r.env].parked->obs.data();
+  }
   Workspace ws;
   DBuf<float> heads, dobs, hbatch, dres;
   DBuf<int32_t> didx, bo;
@@ -182,14 +203,14 @@ struct Engine {
   void run(const std::vector<const Request*>& rq, bool sample) {
     const int n = (int)rq.size(), D = m.D, H = m.H, A = m.A;
     for (const Request* r : rq)
-      for (float v : r->obs)
-        if (!std::isfinite(v)) protocol_error("act: non-finite observation");  // nn.cpp:119
+      for (int k = 0; k < D; ++k)
+        if (!std::isfinite(r->obs[k])) protocol_error("act: non-finite observation");  // nn.cpp:119
     pobs.ensure((size_t)n * D);
     pidx.ensure((size_t)2 * n);
     pep.ensure(n);
     for (int i = 0; i < n; ++i) {
       const Request& r = *rq[i];
-      std::memcpy(pobs.p + (size_t)i * D, r.obs.data(), sizeof(float) * D);
+      std::memcpy(pobs.p + (size_t)i * D, r.obs, sizeof(float) * D);
       pidx.p[i] = r.env;
       pidx.p[n + i] = r.obs_step;
       pep.p[i] = r.obs_episode;
@@ -208,7 +229,9 @@ struct Engine {
     const int32_t hbo[2] = {n, 0};
     bo.reserve(c, 2);
     bo.upload(hbo, 2);
-    policy_forward(c, m, params.p, n, dobs.p, hbatch.p, 1, bo.p, bo.p + 1, ws, false);
+    // one timestep of n rows: with the host batch sizes the GRU step runs on the
+    // tensor cores (stepgemm.cu) once n reaches the big-step threshold
+    policy_forward(c, m, params.p, n, dobs.p, hbatch.p, 1, bo.p, bo.p + 1, ws, false, hbo, hbo + 1);
     policy_heads(c, m, params.p, n, ws.hidden.p, heads.p);
     if (sample) {
       scatter_h_kernel<<<n, 128, 0, c->stream>>>(n, H, didx.p, ws.hidden.p, h.p);
@@ -240,39 +263,39 @@ struct Engine {
     const int32_t* ad = reinterpret_cast<const int32_t*>(pres.p);
     for (int i = 0; i < n; ++i) {
       const Request& r = *needs[i];
-      Pending p;
-      p.obs = r.obs;
-      if (m.continuous) p.act_c.assign(pres.p + 3 * n + (size_t)i * A, pres.p + 3 * n + (size_t)(i + 1) * A);
-      else p.act_d = ad[i];
-      p.log_prob = pres.p[n + i];
-      p.value = pres.p[2 * n + i];
-      p.episode = r.obs_episode;
-      p.t = r.obs_step;
-      p.version = version;
+      const int e = r.env;
+      has_pend[e] = 1;
+      std::memcpy(pend_obs.data() + (size_t)e * m.D, r.obs, sizeof(float) * m.D);
+      if (m.continuous) std::memcpy(pend_ac.data() + (size_t)e * A, pres.p + 3 * n + (size_t)i * A, sizeof(float) * A);
+      else pend_ad[e] = ad[i];
+      pend_lp[e] = pres.p[n + i];
+      pend_v[e] = pres.p[2 * n + i];
+      pend_ep[e] = r.obs_episode;
+      pend_t[e] = r.obs_step;
+      pend_ver[e] = version;
       const int k = out.nd++;
-      if (out.env) out.env[k] = r.env;
-      if (!m.continuous && out.act_d) out.act_d[k] = p.act_d;
-      if (m.continuous && out.act_c) std::memcpy(out.act_c + (size_t)k * A, p.act_c.data(), sizeof(float) * A);
-      envs[r.env].pending = std::move(p);
+      if (out.env) out.env[k] = e;
+      if (!m.continuous && out.act_d) out.act_d[k] = pend_ad[e];
+      if (m.continuous && out.act_c) std::memcpy(out.act_c + (size_t)k * A, pend_ac.data() + (size_t)e * A, sizeof(float) * A);
     }
   }
 
   // complete_pending (runtime.cpp:116-147)
   void complete_pending(const Request& req, Result& out) {
-    Slot& es = envs[req.env];
-    if (!es.pending)
-      protocol_error("inference: completion for env " + std::to_string(req.env) + " without an outstanding action");
-    Pending p = std::move(*es.pending);
-    es.pending.reset();
-    const int oc = buf().append_rec(req.env, p.episode, p.t, p.obs.data(), p.act_d,
-                                    m.continuous ? p.act_c.data() : nullptr, p.log_prob, p.value, req.reward,
-                                    req.latency, req.done ? 1 : 0, nullptr, hb.p + (size_t)req.env * m.H, p.version);
+    const int e = req.env;
+    if (!has_pend[e])
+      protocol_error("inference: completion for env " + std::to_string(e) + " without an outstanding action");
+    has_pend[e] = 0;
+    const int oc = buf().append_rec(e, pend_ep[e], pend_t[e], pend_obs.data() + (size_t)e * m.D, pend_ad[e],
+                                    m.continuous ? pend_ac.data() + (size_t)e * m.A : nullptr, pend_lp[e], pend_v[e],
+                                    req.reward, req.latency, req.done ? 1 : 0, nullptr, hb.p + (size_t)e * m.H,
+                                    pend_ver[e]);
     if (oc == 0) {
       ++out.new_commits;
       if (!buf().open) out.closed_now = true;
-    } else if (p.t > 0) {
-      buf().bootstrap[req.env] = p.value;
-      buf().bootstrap_valid[req.env] = 1;
+    } else if (pend_t[e] > 0) {
+      buf().bootstrap[e] = pend_v[e];
+      buf().bootstrap_valid[e] = 1;
     }
   }
 
@@ -291,7 +314,7 @@ struct Engine {
       if (buf().open && !capped) {
         needs.push_back(&req);
       } else {
-        es.parked = req;
+        park(req);
         if (capped) es.paused = true;
       }
     }
@@ -313,7 +336,7 @@ struct Engine {
     buf().begin(version);
     out.new_commits = buf().committed;
     for (auto& es : envs) es.paused = false;
-    std::vector<Request> parked;
+    std::vector<Parked> parked;
     for (auto& es : envs) {
       if (es.parked) {
         parked.push_back(std::move(*es.parked));
@@ -321,9 +344,10 @@ struct Engine {
       }
     }
     std::vector<const Request*> needs;
-    for (auto& req : parked) {
-      if (buf().open && !buf().env_at_cap(req.env)) needs.push_back(&req);
-      else envs[req.env].parked = req;
+    for (auto& pk : parked) {
+      pk.r.obs = pk.obs.data();
+      if (buf().open && !buf().env_at_cap(pk.r.env)) needs.push_back(&pk.r);
+      else park(pk.r);
     }
     compute_actions(needs, out);
     if (!buf().open) out.closed_now = true;
@@ -335,13 +359,13 @@ struct Engine {
     for (int e = 0; e < cfg.rollout.N; ++e) {
       Slot& es = envs[e];
       if (buf().bootstrap_valid[e]) continue;
-      if (es.pending) {
-        if (es.pending->t > 0) {
-          buf().bootstrap[e] = es.pending->value;
+      if (has_pend[e]) {
+        if (pend_t[e] > 0) {
+          buf().bootstrap[e] = pend_v[e];
           buf().bootstrap_valid[e] = 1;
         }
-      } else if (es.parked && es.parked->obs_step > 0) {
-        vo.push_back(&*es.parked);
+      } else if (es.parked && es.parked->r.obs_step > 0) {
+        vo.push_back(&es.parked->r);
       }
     }
     if (vo.empty()) return;
@@ -404,7 +428,7 @@ ver_status ver_engine_create(ver_ctx ctx, const ver_engine_config* cfg, const fl
   E.h.zero((size_t)rc.N * E.m.H);
   E.hb.reserve(c, (size_t)rc.N * E.m.H);
   E.hb.zero((size_t)rc.N * E.m.H);
-  E.envs.resize(rc.N);
+  E.init_envs(rc.N);
   E.ws.ctx = c;
   *out = w;
   VER_API_END
@@ -462,7 +486,7 @@ ver_status ver_engine_process_batch(ver_engine e, const ver_request_batch* b, ve
   for (int i = 0; i < b->n; ++i) {
     eng::Request& q = reqs[i];
     q.env = b->env_index[i];
-    q.obs.assign(b->obs + (size_t)i * D, b->obs + (size_t)(i + 1) * D);
+    q.obs = b->obs + (size_t)i * D;
     q.reward = b->reward ? b->reward[i] : 0.f;
     q.done = b->done ? b->done[i] : 0;
     q.first = b->first ? b->first[i] : 0;

@@ -5,7 +5,7 @@ for spec in sys.argv[1:]:
     for kv in filter(None, spec.split(",")):
         k, v = kv.split("=")
         env[k] = v
-    out = subprocess.run([sys.executable, "bench.py", "--no-cpu", "--no-c5", "--no-c3", "--steps", "5"], env=env,
+    out = subprocess.run([sys.executable, "bench.py", "--no-cpu", "--no-c5", "--no-c3", "--no-collect", "--steps", "5"], env=env,
                          capture_output=True, text=True).stdout.strip().splitlines()
     d = json.loads(out[-1])
     print(spec or "default", round(d["ms_per_step"], 3),
