@@ -13,6 +13,7 @@
 // ver::ConfigError, so its doctest CHECK_THROWS_AS assertions hold unchanged.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -246,6 +247,81 @@ class Learner : public Handle<ver_learner, ver_learner_destroy> {
     ver_learner l = nullptr;
     check(ver_learner_create(ctx.get(), &mc, params.data(), &cfg, &ec, base_lr, total_steps, run_seed, &l));
     return l;
+  }
+};
+
+// InferenceEngine (runtime.hpp:96-160) on the device; requests as SoA arrays
+// (ver_request_batch), dispatches returned as (env, action) arrays.
+class InferenceEngine : public Handle<ver_engine, ver_engine_destroy> {
+ public:
+  struct Dispatches {
+    std::vector<int32_t> env, action;  // discrete
+    std::vector<float> action_cont;    // continuous: act_dim per dispatch
+    int new_commits = 0;
+    bool closed_now = false;
+  };
+  InferenceEngine(const Context& ctx, const ver_engine_config& cfg, const std::vector<float>& params,
+                  uint64_t version)
+      : Handle(make(ctx, cfg, params, version)), cfg_(cfg) {}
+  void set_snapshot(const std::vector<float>& params, uint64_t version) {
+    check(ver_engine_set_snapshot(get(), params.data(), version));
+  }
+  void set_snapshot(const Learner& l, uint64_t version) {
+    check(ver_engine_set_snapshot_learner(get(), l.get(), version));
+  }
+  Dispatches begin_rollout() {
+    Dispatches d = sized(cfg_.rollout.N);
+    ver_batch_result r{};
+    check(ver_engine_begin_rollout(get(), &r, d.env.data(), d.action.data(), d.action_cont.data()));
+    return finish(d, r);
+  }
+  Dispatches process_batch(const ver_request_batch& reqs) {
+    Dispatches d = sized(reqs.n);
+    ver_batch_result r{};
+    check(ver_engine_process_batch(get(), &reqs, &r, d.env.data(), d.action.data(), d.action_cont.data()));
+    return finish(d, r);
+  }
+  void force_close() { check(ver_engine_force_close(get())); }
+  void finalize_bootstraps() { check(ver_engine_finalize_bootstraps(get())); }
+  RolloutView close() {
+    ver_view v = nullptr;
+    check(ver_engine_close(get(), &v));
+    return RolloutView(v);
+  }
+  bool rollout_done() const {
+    int open = 0;
+    check(ver_engine_state(get(), &open, nullptr, nullptr, nullptr, nullptr));
+    return !open;
+  }
+
+ private:
+  ver_engine_config cfg_;
+  Dispatches sized(int n) const {
+    Dispatches d;
+    const int A = cfg_.model.action_kind ? cfg_.model.act_dim : 1;
+    d.env.resize(std::max(n, 1));
+    d.action.resize(std::max(n, 1));
+    d.action_cont.resize((size_t)std::max(n, 1) * A);
+    return d;
+  }
+  Dispatches finish(Dispatches& d, const ver_batch_result& r) const {
+    const int A = cfg_.model.action_kind ? cfg_.model.act_dim : 1;
+    d.env.resize(r.n_dispatch);
+    d.action.resize(r.n_dispatch);
+    d.action_cont.resize((size_t)r.n_dispatch * A);
+    d.new_commits = r.new_commits;
+    d.closed_now = r.closed_now != 0;
+    return std::move(d);
+  }
+  static ver_engine make(const Context& ctx, const ver_engine_config& cfg, const std::vector<float>& params,
+                         uint64_t version) {
+    int64_t P = 0;
+    int nt = 0;
+    check(ver_param_count(&cfg.model, &P, &nt));
+    if ((int64_t)params.size() != P) throw ConfigError("InferenceEngine: parameter count mismatch");
+    ver_engine e = nullptr;
+    check(ver_engine_create(ctx.get(), &cfg, params.data(), version, &e));
+    return e;
   }
 };
 

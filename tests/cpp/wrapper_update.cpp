@@ -3,9 +3,14 @@
 // -> append_step* -> set_bootstrap -> close_rollout -> Learner::update.
 //
 //   wrapper_update nodevice        expect DeviceError from Context (no GPU)
+//   wrapper_update engine <dir>    drive ver::gpu::InferenceEngine over every
+//                                  env for <steps> batches (obs from <dir>),
+//                                  write the dispatched actions and the view's
+//                                  log-probs
 //   wrapper_update <dir>           read the records written by
 //                                  tests/test_cpp_wrapper.py, run one update,
 //                                  write <dir>/params_out.f32, print the stats
+#include <algorithm>
 #include <cstdio>
 #include <fstream>
 #include <iostream>
@@ -35,6 +40,43 @@ int main(int argc, char** argv) {
     }
     std::printf("expected DeviceError\n");
     return 1;
+  }
+  if (mode == "engine") {
+    const std::string d = std::string(argv[2]) + "/";
+    int T, N, D, H, steps;
+    {
+      std::ifstream m(d + "meta.txt");
+      m >> T >> N >> D >> H >> steps;
+    }
+    const ver_model_config mc{D, H, H, 0, 2, 0};
+    int64_t P = 0;
+    int nt = 0;
+    ver::gpu::check(ver_param_count(&mc, &P, &nt));
+    auto params = load<float>(d + "params.f32", (size_t)P);
+    auto obs = load<float>(d + "obs.f32", (size_t)(steps + 1) * N * D);
+    ver::gpu::Context ctx(0);
+    ver_engine_config ec{{T, N, /*Variable*/ 1, 0, D, 0, H}, mc, 12345};
+    ver::gpu::InferenceEngine eng(ctx, ec, params, 1);
+    eng.begin_rollout();
+    std::vector<int32_t> env(N), step(N);
+    std::vector<int64_t> ep(N, 0);
+    std::vector<uint8_t> first(N, 1), dn(N, 0);
+    std::vector<float> rew(N, 0.5f);
+    for (int e = 0; e < N; ++e) env[e] = e;
+    std::ofstream out(d + "actions.i32", std::ios::binary);
+    for (int s = 0; s <= steps && !eng.rollout_done(); ++s) {
+      for (int e = 0; e < N; ++e) step[e] = s;
+      ver_request_batch rb{N, env.data(), obs.data() + (size_t)s * N * D, rew.data(), dn.data(), first.data(),
+                           nullptr, ep.data(), step.data()};
+      auto r = eng.process_batch(rb);
+      out.write(reinterpret_cast<const char*>(r.action.data()), (std::streamsize)(r.action.size() * 4));
+      std::fill(first.begin(), first.end(), 0);
+    }
+    eng.force_close();  // preempted close (fewer steps than T x N)
+    eng.finalize_bootstraps();
+    ver::gpu::RolloutView v = eng.close();
+    std::printf("engine ok\n");
+    return 0;
   }
   const std::string d = mode + "/";
   int T, N, D, H, n;

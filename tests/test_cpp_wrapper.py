@@ -80,3 +80,33 @@ def test_wrapper_update_matches_python_api(tmp_path):
     assert p_cpp.shape == p_py.shape
     assert np.array_equal(p_cpp, p_py)
     assert not np.array_equal(p_cpp, p0)
+
+
+@pytest.mark.gpu
+def test_wrapper_engine_matches_python_api(tmp_path):
+    """ver::gpu::InferenceEngine (C++) and the Python InferenceEngine dispatch the
+    same actions on the same requests (same library, same kernels)."""
+    import paper_2210_05064_b200 as V
+    exe = _build()
+    T, N, D, H, steps = 8, 32, 2, 16, 6
+    (tmp_path / "meta.txt").write_text(f"{T} {N} {D} {H} {steps}\n")
+    cfg = V.ModelConfig(obs_dim=D, encoder_dim=H, hidden_dim=H, action_kind=0, num_actions=2)
+    p = np.asarray(V.params_init(cfg, 4), np.float32)
+    p.tofile(tmp_path / "params.f32")
+    obs = np.random.default_rng(3).standard_normal((steps + 1, N, D)).astype(np.float32)
+    obs.tofile(tmp_path / "obs.f32")
+    r = subprocess.run([str(exe), "engine", str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    a_cpp = np.fromfile(tmp_path / "actions.i32", np.int32)
+    g = V.InferenceEngine(cfg, T, N, p, version=1, mode=V.VARIABLE, seed=12345)
+    g.begin_rollout()
+    env = np.arange(N, dtype=np.int32)
+    acts = []
+    for s in range(steps + 1):
+        if g.rollout_done():
+            break
+        _, _, a = g.process_arrays(env, obs[s], reward=np.full(N, 0.5, np.float32),
+                                   done=np.zeros(N, np.uint8), first=np.full(N, 1 if s == 0 else 0, np.uint8),
+                                   obs_episode=np.zeros(N, np.int64), obs_step=np.full(N, s, np.int32))
+        acts.append(a)
+    np.testing.assert_array_equal(a_cpp, np.concatenate(acts))
