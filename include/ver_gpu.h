@@ -263,6 +263,18 @@ typedef struct {
 
 typedef struct ver_learner_s* ver_learner;
 
+/* ------------------------------------------ on-disk formats */
+/* dump_view / load_view (rollout.cpp:293-432): the reference's JSONL rollout trace
+   (one "meta", one "seq" per sequence with its h0 row, one "step" per slot) */
+ver_status ver_view_dump_jsonl(ver_view v, const char* path);
+ver_status ver_view_load_jsonl(ver_ctx ctx, const char* path, ver_view* out);
+/* save_checkpoint / load_checkpoint (bench.cpp:411-441, nn.cpp:314-387): the
+   "ver-checkpoint" v1 JSON (params by tensor name, Adam m / v / step, alpha,
+   consumed_steps, update_index) */
+ver_status ver_learner_save_checkpoint(ver_learner l, const char* path);
+ver_status ver_checkpoint_model_config(const char* path, ver_model_config* out);
+ver_status ver_learner_load_checkpoint(ver_learner l, const char* path);
+
 /* ------------------------------------- inference engine */
 /* InferenceEngine (runtime.hpp:96-160, runtime.cpp:60-229) on the device: the
    policy snapshot, every env's GRU state and the pending records' h_before stay

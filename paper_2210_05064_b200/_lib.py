@@ -174,6 +174,11 @@ _SIGS = {
                                P(c_float), c_int, P(c_float), c_int]),
     "ver_debug_gemm_time": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                     P(c_float)]),
+    "ver_view_dump_jsonl": (c_int, [C.c_void_p, C.c_char_p]),
+    "ver_view_load_jsonl": (c_int, [C.c_void_p, C.c_char_p, P(C.c_void_p)]),
+    "ver_learner_save_checkpoint": (c_int, [C.c_void_p, C.c_char_p]),
+    "ver_checkpoint_model_config": (c_int, [C.c_char_p, P(ModelConfig)]),
+    "ver_learner_load_checkpoint": (c_int, [C.c_void_p, C.c_char_p]),
     "ver_engine_create": (c_int, [C.c_void_p, P(EngineConfig), P(c_float), c_uint64, P(C.c_void_p)]),
     "ver_engine_destroy": (c_int, [C.c_void_p]),
     "ver_engine_set_snapshot": (c_int, [C.c_void_p, P(c_float), c_uint64]),

@@ -218,6 +218,18 @@ class RolloutView:
         _check(_lib().ver_view_download(self.h, C.byref(vh)))
         return hv
 
+    def dump_jsonl(self, path):
+        """dump_view (rollout.cpp:293-344): the reference's JSONL trace."""
+        _check(_lib().ver_view_dump_jsonl(self.h, str(path).encode()))
+
+    @staticmethod
+    def load_jsonl(path, ctx: Context | None = None) -> "RolloutView":
+        """load_view (rollout.cpp:346-432)."""
+        ctx = ctx or default_context()
+        out = C.c_void_p()
+        _check(_lib().ver_view_load_jsonl(ctx.h, str(path).encode(), C.byref(out)))
+        return RolloutView(out, ctx)
+
     def clone(self) -> "RolloutView":
         out = C.c_void_p()
         _check(_lib().ver_view_clone(self.h, C.byref(out)))
@@ -811,6 +823,14 @@ class Learner:
                                             c if consumed is None else consumed,
                                             u if update_index is None else update_index))
 
+    def save_checkpoint(self, path):
+        """save_checkpoint (bench.cpp:411-424): "ver-checkpoint" v1 JSON."""
+        _check(_lib().ver_learner_save_checkpoint(self.h, str(path).encode()))
+
+    def load_checkpoint(self, path):
+        """load_checkpoint (bench.cpp:426-441) into this learner (same model)."""
+        _check(_lib().ver_learner_load_checkpoint(self.h, str(path).encode()))
+
     def set_consumed_steps(self, n: int):
         self.set_state(consumed=n)
 
@@ -873,6 +893,14 @@ def optimal_preempt_steps(step_times, learn_time: float, max_steps: int,
     return out.value
 
 
+
+
+def checkpoint_model_config(path) -> ModelConfig:
+    """The model config stored in a "ver-checkpoint" file (nn.cpp:339-348)."""
+    mc = L.ModelConfig()
+    _check(_lib().ver_checkpoint_model_config(str(path).encode(), C.byref(mc)))
+    return ModelConfig(obs_dim=mc.obs_dim, encoder_dim=mc.encoder_dim, hidden_dim=mc.hidden_dim,
+                       action_kind=mc.action_kind, num_actions=mc.num_actions, act_dim=mc.act_dim)
 
 
 # --------------------------------------------------------- inference engine

@@ -398,6 +398,7 @@ struct ver_learner_s {
 
 namespace verg {
 // the learner's current parameters (device layout) for the inference engine's snapshot
+const ver_model_config* learner_model_config(ver_learner_s* l) { return &l->l.mc; }
 const float* learner_device_params(ver_learner_s* l, Ctx** ctx, int64_t* count) {
   *ctx = l->l.ctx;
   *count = l->l.m.P;
