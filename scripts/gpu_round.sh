@@ -26,7 +26,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -
 done
 for d in 0 1; do
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:gru_step_gemm_kernel<$d>" -s 2 -c 1 \
+  -k "regex:gru_step_gemm_kernel<.{0,5}$d>" -s 2 -c 1 \
   -o $OUT/prof_gru_step_gemm$d python scripts/profile_update.py --updates 1 > $OUT/prof_gru_step_gemm$d.log 2>&1
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 20 -c 2 \
