@@ -275,7 +275,59 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
   for (int k = 0; k < chunks; ++k) s += part[(size_t)k * N + n];
   out[n] = s;
 }
+// float4 variant (N, ld multiples of 4, X 16-byte aligned): a block covers 128
+// columns (lane: 4 columns) and a row chunk; each warp walks every 8th row with
+// 4 independent accumulators, so ~2 KB per warp are in flight (HBM-bound)
+__global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __restrict__ X, int M, int N, int ld,
+                                                              int rows_per, float* __restrict__ part) {
+  __shared__ float4 red[8][32];
+  const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int n = blockIdx.x * 128 + 4 * lane;
+  const int m0 = blockIdx.y * rows_per, m1 = min(M, m0 + rows_per);
+  float4 a[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (n < N) {
+    int m = m0 + r;
+    for (; m + 24 < m1; m += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)(m + 8 * u) * ld + n));
+        a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+      }
+    }
+    for (; m < m1; m += 8) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)m * ld + n));
+      a[0].x += x.x; a[0].y += x.y; a[0].z += x.z; a[0].w += x.w;
+    }
+  }
+  red[r][lane] = make_float4((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y),
+                             (a[0].z + a[1].z) + (a[2].z + a[3].z), (a[0].w + a[1].w) + (a[2].w + a[3].w));
+  __syncthreads();
+  if (r == 0 && n < N) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      const float4 q = red[k][lane];
+      t.x += q.x; t.y += q.y; t.z += q.z; t.w += q.w;
+    }
+    *reinterpret_cast<float4*>(part + (size_t)blockIdx.y * N + n) = t;
+  }
+}
+
 static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, float* out) {
+  if (N % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+    const int col_blocks = (int)cdiv(N, 128);
+    int rows_per = 256;
+    while ((int64_t)col_blocks * cdiv(M, rows_per) > 4 * c->num_sms && rows_per < 8192) rows_per *= 2;
+    const int chunks = std::max(1, (int)cdiv(M, rows_per));
+    ws.splitk.reserve(c, (size_t)chunks * N);
+    colsum4_partial_kernel<<<dim3(col_blocks, chunks), 256, 0, c->stream>>>(X, M, N, ld, rows_per, ws.splitk.p);
+    after_launch(c);
+    colsum_final_kernel<<<cdiv(N, 256), 256, 0, c->stream>>>(ws.splitk.p, chunks, N, out);
+    after_launch(c);
+    return;
+  }
   // enough row chunks for ~4 blocks per SM: each thread walks rows_per / 8 rows
   const int col_blocks = (int)cdiv(N, 32);
   int rows_per = 64;
