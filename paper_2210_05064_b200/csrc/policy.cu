@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs
 #pragma unroll
     for (int d = 0; d < kMaxD; ++d)
       if (d < D) s = fmaf(__ldg(obs + (size_t)p * D + d), w[d], s);
-    e1[(size_t)p * E + k] = tanhf(s + b);
+    e1[(size_t)p * E + k] = gate_tanh(s + b);
   }
 }
 
@@ -1024,15 +1024,79 @@ __global__ void enc1_grad_partial_kernel(const float* __restrict__ obs, const fl
       part[((size_t)blockIdx.y * (D + 1) + d) * E + k] = t;
     }
 }
+// float4 variant (E % 4 == 0): lane = 4 features, a block = 128 features x a row
+// chunk, each warp walks every 8th row two rows at a time
+__global__ void __launch_bounds__(256) enc1_grad4_partial_kernel(const float* __restrict__ obs,
+                                                                 const float* __restrict__ dpre1, int S, int D,
+                                                                 int E, int rows_per, float* __restrict__ part) {
+  __shared__ float4 red[8][32][kMaxD + 1];
+  const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;
+  const int k = blockIdx.x * 128 + 4 * lane;
+  const int m0 = blockIdx.y * rows_per, m1 = min(S, m0 + rows_per);
+  float4 acc[kMaxD + 1];
+#pragma unroll
+  for (int d = 0; d <= kMaxD; ++d) acc[d] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (k < E) {
+    int m = m0 + r;
+    for (; m + 8 < m1; m += 16) {
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(dpre1 + (size_t)m * E + k));
+      const float4 g1 = __ldg(reinterpret_cast<const float4*>(dpre1 + (size_t)(m + 8) * E + k));
+      acc[0].x += g0.x + g1.x; acc[0].y += g0.y + g1.y; acc[0].z += g0.z + g1.z; acc[0].w += g0.w + g1.w;
+#pragma unroll
+      for (int d = 0; d < kMaxD; ++d)
+        if (d < D) {
+          const float o0 = __ldg(obs + (size_t)m * D + d), o1 = __ldg(obs + (size_t)(m + 8) * D + d);
+          acc[1 + d].x = fmaf(o1, g1.x, fmaf(o0, g0.x, acc[1 + d].x));
+          acc[1 + d].y = fmaf(o1, g1.y, fmaf(o0, g0.y, acc[1 + d].y));
+          acc[1 + d].z = fmaf(o1, g1.z, fmaf(o0, g0.z, acc[1 + d].z));
+          acc[1 + d].w = fmaf(o1, g1.w, fmaf(o0, g0.w, acc[1 + d].w));
+        }
+    }
+    for (; m < m1; m += 8) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(dpre1 + (size_t)m * E + k));
+      acc[0].x += g.x; acc[0].y += g.y; acc[0].z += g.z; acc[0].w += g.w;
+#pragma unroll
+      for (int d = 0; d < kMaxD; ++d)
+        if (d < D) {
+          const float o = __ldg(obs + (size_t)m * D + d);
+          acc[1 + d].x = fmaf(o, g.x, acc[1 + d].x);
+          acc[1 + d].y = fmaf(o, g.y, acc[1 + d].y);
+          acc[1 + d].z = fmaf(o, g.z, acc[1 + d].z);
+          acc[1 + d].w = fmaf(o, g.w, acc[1 + d].w);
+        }
+    }
+  }
+#pragma unroll
+  for (int d = 0; d <= kMaxD; ++d)
+    if (d <= D) red[r][lane][d] = acc[d];
+  __syncthreads();
+  if (r == 0 && k < E)
+    for (int d = 0; d <= D; ++d) {
+      float4 t = red[0][lane][d];
+      for (int q = 1; q < 8; ++q) {
+        const float4 u = red[q][lane][d];
+        t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+      }
+      *reinterpret_cast<float4*>(part + ((size_t)blockIdx.y * (D + 1) + d) * E + k) = t;
+    }
+}
+// block (32 outputs x 8 chunk groups): thread (i, q) sums chunks q, q + 8, ...;
+// the 8 group sums reduce in a fixed order (deterministic)
 __global__ void enc1_grad_final_kernel(const float* __restrict__ part, int chunks, int D, int E,
                                        float* __restrict__ db1, float* __restrict__ dw1) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (D + 1) * E) return;
-  const int d = i / E, k = i % E;
+  __shared__ float red[8][33];
+  const int i = blockIdx.x * 32 + threadIdx.x, q = threadIdx.y;
   float s = 0.f;
-  for (int c = 0; c < chunks; ++c) s += part[((size_t)c * (D + 1) + d) * E + k];
-  if (d == 0) db1[k] = s;
-  else dw1[(size_t)(d - 1) * E + k] = s;
+  if (i < (D + 1) * E)
+    for (int c = q; c < chunks; c += 8) s += part[(size_t)c * (D + 1) * E + i];
+  red[q][threadIdx.x] = s;
+  __syncthreads();
+  if (q != 0 || i >= (D + 1) * E) return;
+  float t = 0.f;
+  for (int k = 0; k < 8; ++k) t += red[k][threadIdx.x];
+  const int d = i / E, k = i % E;
+  if (d == 0) db1[k] = t;
+  else dw1[(size_t)(d - 1) * E + k] = t;
 }
 
 void policy_backward(Ctx* c, const Model& m, const float* params, int S, const float* obs, int L,
@@ -1049,13 +1113,21 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
   colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2);
   gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E});
   {
-    const int rows_per = 512;
+    // ~4 blocks per SM: 128-feature blocks (float4 path) or 32-feature blocks
+    const int col_blocks = (int)cdiv(E, E % 4 == 0 ? 128 : 32);
+    int rows_per = 64;
+    while ((int64_t)col_blocks * cdiv(S, rows_per) > 4 * c->num_sms && rows_per < 8192) rows_per *= 2;
     const int chunks = std::max(1, (int)cdiv(S, rows_per));
     ws.splitk.reserve(c, (size_t)chunks * (m.D + 1) * E);
-    dim3 g1(cdiv(E, 32), chunks);
-    enc1_grad_partial_kernel<<<g1, 256, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E, rows_per, ws.splitk.p);
+    if (E % 4 == 0) {
+      enc1_grad4_partial_kernel<<<dim3(cdiv(E, 128), chunks), 256, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E,
+                                                                                   rows_per, ws.splitk.p);
+    } else {
+      enc1_grad_partial_kernel<<<dim3(cdiv(E, 32), chunks), 256, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E,
+                                                                                 rows_per, ws.splitk.p);
+    }
     after_launch(c);
-    enc1_grad_final_kernel<<<cdiv((size_t)(m.D + 1) * E, 256), 256, 0, c->stream>>>(
+    enc1_grad_final_kernel<<<cdiv((size_t)(m.D + 1) * E, 32), dim3(32, 8), 0, c->stream>>>(
         ws.splitk.p, chunks, m.D, E, grad + m.o_b1, grad + m.o_w1);
     after_launch(c);
   }
