@@ -1060,19 +1060,55 @@ __device__ __forceinline__ void cl_push4(const float* src_base, const float* dst
   }
 }
 
+// as cl_push4, with st.async: every store completes its bytes on the same-offset
+// mbarrier `bar` of the destination CTA (the owner waits for data, not for a
+// cluster-wide barrier)
+__device__ __forceinline__ void cl_push4_async(const float* src_base, const float* dst_base, int rows, int row_f4,
+                                               int src_ld, int dst_ld, uint32_t bar) {
+  const int per_dst = rows * row_f4;
+  for (int i = threadIdx.x; i < TC_CL * per_dst; i += blockDim.x) {
+    const int r = i / per_dst, q = i % per_dst, row = q / row_f4, c = q % row_f4;
+    const float4 v = *reinterpret_cast<const float4*>(src_base + row * src_ld + 4 * c);
+    const uint32_t a = su32(dst_base + row * dst_ld + 4 * c);
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(r));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(ra),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rb)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void tl_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tl_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TL_WAIT:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TL_WAIT;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 template <int H>
 __global__ void __launch_bounds__(TC_T, 1) gru_fwd_tail(
     int t0, int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, const float* __restrict__ ux,
     const float* __restrict__ xp, const float* h0, float* hidden, float* __restrict__ gates, float* __restrict__ hun,
-    float* __restrict__ hprev_store, long long* trace) {
+    float* __restrict__ hprev_store, long long* trace, int tail_async) {
   constexpr int H3 = 3 * H, UT = H / TC_CL, KW = H / (TC_T / 32);
   static_assert(UT == 32 && KW % 4 == 0, "tail kernel: H = 512");
   extern __shared__ float4 sm4[];
   float* hs = reinterpret_cast<float*>(sm4);    // [2][TC_TH][H]
   float* red = hs + 2 * TC_TH * H;              // [16][TC_TH][3 UT]
   float* stg = red + (TC_T / 32) * TC_TH * 3 * UT;  // [TC_TH][UT] this CTA's new h slice
+  // one mbarrier per h buffer: the 16 CTAs' slices of step s land in buffer s & 1
+  // with st.async; the owner expects bs[s] x H x 4 bytes (posted two steps ahead)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + TC_TH * UT);
+  const uint32_t bar_a[2] = {su32(bars), su32(bars + 1)};
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)cl_rank() * UT, u = u0 + lane;
+  const bool async_push = tail_async != 0;
   float w[KW][3];
 #pragma unroll
   for (int k = 0; k < KW; ++k)
@@ -1082,6 +1118,12 @@ __global__ void __launch_bounds__(TC_T, 1) gru_fwd_tail(
     const int B = bs[t0];
     const float* hp = t0 == 0 ? h0 : hidden + (size_t)offs[t0 - 1] * H;
     for (int i = threadIdx.x; i < B * H; i += TC_T) hs[(t0 & 1) * TC_TH * H + i] = __ldcg(hp + i);
+  }
+  if (async_push && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a[0]) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a[1]) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s2 = t0 + 1; s2 <= t0 + 2 && s2 < L; ++s2) tl_expect(bar_a[s2 & 1], (uint32_t)bs[s2] * H * 4);
   }
   cl_sync();
   const int j = warp;  // gate pair (row warp, unit lane)
@@ -1097,6 +1139,10 @@ __global__ void __launch_bounds__(TC_T, 1) gru_fwd_tail(
   float xc[3] = {0.f, 0.f, 0.f}, xn[3] = {0.f, 0.f, 0.f};
   load_x(t0, xc);
   for (int t = t0; t < L; ++t) {
+    if (async_push && t > t0) {
+      tl_wait(bar_a[t & 1], (uint32_t)(((t - t0 - 1) >> 1) & 1));
+      if (threadIdx.x == 0 && t + 2 < L) tl_expect(bar_a[t & 1], (uint32_t)bs[t + 2] * H * 4);
+    }
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
     const int B = bs[t], o = offs[t];
     const float* hc = hs + (t & 1) * TC_TH * H;
@@ -1153,13 +1199,18 @@ __global__ void __launch_bounds__(TC_T, 1) gru_fwd_tail(
     }
     if (t + 1 < L) {
       __syncthreads();
-      cl_push4(stg, hn + u0, B, UT / 4, UT, H);
+      if (async_push) {
+        cl_push4_async(stg, hn + u0, bs[t + 1], UT / 4, UT, H, bar_a[(t + 1) & 1]);
+      } else {
+        cl_push4(stg, hn + u0, B, UT / 4, UT, H);
+      }
     }
     xc[0] = xn[0];
     xc[1] = xn[1];
     xc[2] = xn[2];
-    cl_sync();
+    if (!async_push) cl_sync();
   }
+  if (async_push) cl_sync();  // no CTA exits while a peer may still push into it
 }
 
 // backward: steps t = L-1 .. t_stop+1 (rows of step t-1 <= TC_TH), plus the
@@ -1266,7 +1317,8 @@ __global__ void __launch_bounds__(TC_T, 1) gru_bwd_tail(
 
 static size_t tail_fwd_smem(int H) {
   return sizeof(float) *
-         ((size_t)2 * TC_TH * H + (size_t)(TC_T / 32) * TC_TH * 3 * (H / TC_CL) + (size_t)TC_TH * (H / TC_CL));
+             ((size_t)2 * TC_TH * H + (size_t)(TC_T / 32) * TC_TH * 3 * (H / TC_CL) + (size_t)TC_TH * (H / TC_CL)) +
+         16 /* two mbarriers */;
 }
 static size_t tail_bwd_smem(int H) {
   return sizeof(float) * ((size_t)2 * TC_TH * 3 * H + (size_t)(TC_T / 32) * TC_TH * (H / TC_CL) +
@@ -1367,7 +1419,8 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
       float* hun = ws.hu.p;
       float* hps = ws.hprev.p;
       long long* tr = trace_buf(c, ws, L);
-      void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr};
+      int ta = env_int("VER_REC_TAIL_ASYNC", 1);
+      void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr, &ta};
       tail_launch(c, reinterpret_cast<const void*>(gru_fwd_tail<512>), tail_fwd_smem(512), args);
       trace_dump(c, "fwdtail", L, d_bs, tr);
     }
@@ -1385,7 +1438,8 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
       float* hun = ws.hu.p;
       float* hps = ws.hprev.p;
       long long* tr = trace_buf(c, ws, L);
-      void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr};
+      int ta = env_int("VER_REC_TAIL_ASYNC", 1);
+      void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr, &ta};
       tail_launch(c, reinterpret_cast<const void*>(gru_fwd_tail<512>), tail_fwd_smem(512), args);
       trace_dump(c, "fwdtail", L, d_bs, tr);
       return;
