@@ -152,6 +152,8 @@ ver_status ver_rollout_begin(ver_rollout r, uint64_t snapshot_version);
 ver_status ver_rollout_append(ver_rollout r, const ver_step_batch* batch, int32_t* outcomes);
 ver_status ver_rollout_force_close(ver_rollout r);          /* rollout.cpp:95 */
 ver_status ver_rollout_set_bootstrap(ver_rollout r, int env, float value); /* :97-100 */
+/* set_bootstrap for n envs at once (same semantics, one call) */
+ver_status ver_rollout_set_bootstraps(ver_rollout r, int n, const int32_t* env, const float* value);
 ver_status ver_rollout_state(ver_rollout r, int* open, int* committed, int* carryover);
 /* close_rollout (rollout.cpp:102-190): device compaction of the arrival log
    into the env-major, sequence-contiguous view */

@@ -124,6 +124,7 @@ _SIGS = {
     "ver_rollout_append": (c_int, [C.c_void_p, P(StepBatch), P(c_int32)]),
     "ver_rollout_force_close": (c_int, [C.c_void_p]),
     "ver_rollout_set_bootstrap": (c_int, [C.c_void_p, c_int, c_float]),
+    "ver_rollout_set_bootstraps": (c_int, [C.c_void_p, c_int, P(c_int32), P(c_float)]),
     "ver_rollout_state": (c_int, [C.c_void_p, P(c_int), P(c_int), P(c_int)]),
     "ver_rollout_close": (c_int, [C.c_void_p, P(C.c_void_p)]),
     "ver_view_synth": (c_int, [C.c_void_p, P(c_int32), c_int, c_int, c_int, c_uint64, c_float, P(C.c_void_p)]),

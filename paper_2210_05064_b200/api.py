@@ -340,6 +340,12 @@ class RolloutBuffer:
     def set_bootstrap(self, env: int, value: float):
         _check(_lib().ver_rollout_set_bootstrap(self.h, env, value))
 
+    def set_bootstraps(self, envs, values):
+        """set_bootstrap for many envs in one call."""
+        e = np.ascontiguousarray(envs, np.int32)
+        v = np.ascontiguousarray(values, np.float32)
+        _check(_lib().ver_rollout_set_bootstraps(self.h, e.size, _ptr(e, C.c_int32), _ptr(v, C.c_float)))
+
     def _state(self):
         o, c, k = C.c_int(), C.c_int(), C.c_int()
         _check(_lib().ver_rollout_state(self.h, C.byref(o), C.byref(c), C.byref(k)))

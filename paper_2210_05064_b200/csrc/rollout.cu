@@ -845,9 +845,28 @@ ver_status ver_rollout_begin(ver_rollout r, uint64_t sv) {
 
 ver_status ver_rollout_append(ver_rollout r, const ver_step_batch* b, int32_t* outcomes) {
   VER_API_BEGIN
-  for (int i = 0; i < b->n; ++i) {
+  int i = 0;
+  while (i < b->n) {
+    const int k = r->r.append_bulk(b, i);
+    if (k > 0) {
+      if (outcomes) std::fill(outcomes + i, outcomes + i + k, 0);
+      i += k;
+      continue;
+    }
     const int o = r->r.append_one(b, i);
     if (outcomes) outcomes[i] = o;
+    ++i;
+  }
+  VER_API_END
+}
+
+ver_status ver_rollout_set_bootstraps(ver_rollout r, int n, const int32_t* env, const float* value) {
+  VER_API_BEGIN
+  for (int i = 0; i < n; ++i)
+    if (env[i] < 0 || env[i] >= r->r.cfg.N) protocol_error("set_bootstrap: env out of range");
+  for (int i = 0; i < n; ++i) {
+    r->r.bootstrap[env[i]] = value[i];
+    r->r.bootstrap_valid[env[i]] = 1;
   }
   VER_API_END
 }

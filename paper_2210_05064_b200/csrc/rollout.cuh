@@ -194,6 +194,62 @@ struct Rollout {
                       nullptr, ver);
   }
 
+  // Variable-mode fast path of a batch (same outcome as append_one per record):
+  // while the store stays open every record commits, so the payload columns are
+  // block-copied into the arrival log and only rank / sequence-start / h_before
+  // bookkeeping runs per record.  Returns how many records [i0, i0 + k) it took.
+  int append_bulk(const ver_step_batch* b, int i0) {
+    if (cfg.mode != 1 || !open) return 0;
+    int n = std::min(b->n - i0, capacity() - committed);
+    for (int i = 0; i < n; ++i)  // a bad env index stops the fast path there (append_one throws)
+      if (b->env_index[i0 + i] < 0 || b->env_index[i0 + i] >= cfg.N) {
+        n = i;
+        break;
+      }
+    if (n <= 0) return 0;
+    const int r0 = committed, D = cfg.obs_dim;
+    auto col = [&](auto* dst, const auto* src, size_t width, auto fill) {
+      if (src) std::memcpy(dst + (size_t)r0 * width, src + (size_t)i0 * width, sizeof(*dst) * width * n);
+      else std::fill(dst + (size_t)r0 * width, dst + (size_t)(r0 + n) * width, fill);
+    };
+    col(env.p, b->env_index, 1, 0);
+    col(episode.p, b->episode_index, 1, (int64_t)0);
+    col(step.p, b->step_in_episode, 1, 0);
+    col(obs.p, b->obs, D, 0.f);
+    if (cfg.action_kind) col(act_cont.p, b->act_cont, cfg.act_dim, 0.f);
+    else col(act_disc.p, b->act_disc, 1, 0);
+    col(log_prob.p, b->log_prob, 1, 0.f);
+    col(value.p, b->value, 1, 0.f);
+    col(reward.p, b->reward, 1, 0.f);
+    col(latency.p, b->latency, 1, 0.f);
+    col(version.p, b->snapshot_version, 1, (uint64_t)0);
+    for (int i = 0; i < n; ++i) {
+      const int e = b->env_index[i0 + i];
+      const int rk = counts[e];
+      const uint8_t dn = b->done[i0 + i] ? 1 : 0;
+      int hs = -2;
+      if (rk == 0 || last_done[e]) {
+        const bool has = b->h_before && (!b->h_before_valid || b->h_before_valid[i0 + i]);
+        if (has) {
+          hlog.ensure((size_t)(h_used + 1) * cfg.hidden_dim, (size_t)h_used * cfg.hidden_dim);
+          std::memcpy(hlog.p + (size_t)h_used * cfg.hidden_dim, b->h_before + (size_t)(i0 + i) * cfg.hidden_dim,
+                      sizeof(float) * cfg.hidden_dim);
+          hs = h_used++;
+        } else {
+          hs = -1;
+        }
+      }
+      rank.p[r0 + i] = rk;
+      hslot.p[r0 + i] = hs;
+      done.p[r0 + i] = dn;
+      counts[e] = rk + 1;
+      last_done[e] = dn;
+    }
+    committed += n;
+    if (committed >= capacity()) open = false;
+    return n;
+  }
+
   // one record; h_before from the host (h) or from device memory (h_dev: the
   // inference engine's pending row, copied device to device)
   int append_rec(int e, int64_t ep, int32_t st, const float* o, int32_t ad, const float* ac, float lp, float v,

@@ -134,8 +134,12 @@ def fill_buffer(buf, wl: Workload, snapshot_version: int = 1):
     """begin_rollout + append all records + bootstraps on a RolloutBuffer-like object."""
     buf.begin_rollout(snapshot_version)
     out = buf.append_steps(wl.records)
-    for e in np.flatnonzero(wl.bootstrap_valid):
-        buf.set_bootstrap(int(e), float(wl.bootstrap[e]))
+    envs = np.flatnonzero(wl.bootstrap_valid)
+    if hasattr(buf, "set_bootstraps"):
+        buf.set_bootstraps(envs, np.asarray(wl.bootstrap, np.float32)[envs])
+    else:
+        for e in envs:
+            buf.set_bootstrap(int(e), float(wl.bootstrap[e]))
     return out
 
 
