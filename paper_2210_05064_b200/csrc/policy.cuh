@@ -45,6 +45,8 @@ struct Workspace {
   DBuf<long long> trace;                                // VER_REC_TRACE experiments only
   DBuf<float> step;                                     // per-step GEMM output of the big recurrence steps
   DBuf<float> sgsteps, sgmaps;                          // stepgemm.cu: step table, per-step A tensor maps
+  DBuf<unsigned long long> hx;                          // K-split kernels: tagged h / dhU rows of short steps
+  unsigned hx_epoch = 0;                                // tag epoch, one per K-split launch
   void ensure(const Model& m, size_t S, bool train);
 };
 

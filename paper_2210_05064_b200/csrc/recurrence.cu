@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
     int L, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs, int UB, int RB,
     const float* __restrict__ ux, const float* __restrict__ xp, const float* h0, float* hidden,
     float* __restrict__ gates, float* __restrict__ hun, float* __restrict__ hprev_store, unsigned* bar,
-    long long* trace, int t_begin) {
+    long long* trace, int t_begin, unsigned long long* hx, int tag_th, unsigned epoch) {
   constexpr int H3 = 3 * H, NT = NW * 32;
   constexpr int KS_FR = ks_fr(NW);
   constexpr int KW = H / NW, NI = KW / 8;
@@ -690,29 +690,56 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
       }
     }
   };
+  // Short steps (bs_t <= tag_th) skip the group barrier and the bulk staging:
+  // the producers of h_{t-1} also write each value with its step tag into hx
+  // (64-bit words: tag << 32 | bits), and the consumers poll those words
+  // straight into shared memory, so data and synchronisation take one L2
+  // round trip instead of two.  hx is double-buffered by step parity (a CTA
+  // reaches step t+1 only after every CTA of its group wrote h_t, i.e. after
+  // they all finished reading h_{t-1}); the host zeroes it per launch and the
+  // tag (epoch * 4096 + t) is unique within and across launches.
+  auto tagged = [&](int s) { return s > t_begin && s < L && bs[s] <= tag_th; };
   for (int t = t_begin; t < L; ++t) {
     const RowMap rm = rows_in(1, bs[t], rb, RB, 0, 1 << 30);
     if (rm.n == 0) break;  // bs is non-increasing: this row block is done
     const int o = offs[t];
+    const bool tag_in = tagged(t), tag_out = tagged(t + 1);
     load_x(rm, o, 0, min(KS_FR, rm.n));
-    if (t > t_begin) {
+    if (t > t_begin && !tag_in) {
       target += UB;
       group_barrier(cnt, target);
     }
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
     const float* hp = (t == 0) ? h0 : hidden + (size_t)offs[t - 1] * H;
     const int nch = (rm.n + KS_FR - 1) / KS_FR;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !tag_in) {
       asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores of other CTAs -> bulk-copy reads
       stage_rows(hs + buf * KS_FR * H, hp, H, rm, 0, min(KS_FR, rm.n), su32(&mbar[buf]));
     }
     for (int ch = 0; ch < nch; ++ch) {
       const int c0 = ch * KS_FR, nr = min(KS_FR, rm.n - c0);
-      if (threadIdx.x == 0 && ch + 1 < nch)
-        stage_rows(hs + (buf ^ 1) * KS_FR * H, hp, H, rm, c0 + KS_FR, min(KS_FR, rm.n - c0 - KS_FR),
-                   su32(&mbar[buf ^ 1]));
-      mb_wait(su32(&mbar[buf]), (phase >> buf) & 1);
-      phase ^= 1u << buf;
+      if (tag_in) {  // one chunk: rm.n <= tag_th / RB <= KS_FR
+        const unsigned want = epoch * 4096u + (unsigned)(t - 1);
+        const unsigned long long* src = hx + (size_t)((t - 1) & 1) * tag_th * H;
+        float* dst = hs + buf * KS_FR * H;
+        for (int i = threadIdx.x; i < nr * (H / 2); i += NT) {
+          const int r = i / (H / 2), k2 = 2 * (i % (H / 2));
+          const unsigned long long* a = src + (size_t)rm.row(c0 + r) * H + k2;
+          unsigned long long v0, v1;
+          do {
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v0), "=l"(v1) : "l"(a) : "memory");
+          } while ((unsigned)(v0 >> 32) != want || (unsigned)(v1 >> 32) != want);
+          *reinterpret_cast<float2*>(dst + r * H + k2) =
+              make_float2(__uint_as_float((unsigned)v0), __uint_as_float((unsigned)v1));
+        }
+        __syncthreads();
+      } else {
+        if (threadIdx.x == 0 && ch + 1 < nch)
+          stage_rows(hs + (buf ^ 1) * KS_FR * H, hp, H, rm, c0 + KS_FR, min(KS_FR, rm.n - c0 - KS_FR),
+                     su32(&mbar[buf ^ 1]));
+        mb_wait(su32(&mbar[buf]), (phase >> buf) & 1);
+        phase ^= 1u << buf;
+      }
       const float* hc = hs + buf * KS_FR * H;
       for (int g0 = 0; g0 < nr; g0 += 4) {
         float acc[12];
@@ -761,7 +788,12 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
         const float zg = gate_sigm(xr[k][1] + sz);
         const float ng = gate_tanh(xr[k][2] + rg * sn);
         const float hprev = hc[row * H + u];
-        hidden[p * H + u] = (1.f - zg) * ng + zg * hprev;
+        const float hnew = (1.f - zg) * ng + zg * hprev;
+        hidden[p * H + u] = hnew;
+        const int jrow = rm.row(c0 + row);
+        if (tag_out && jrow < bs[t + 1])
+          hx[((size_t)(t & 1) * tag_th + jrow) * H + u] =
+              ((unsigned long long)(epoch * 4096u + (unsigned)t) << 32) | __float_as_uint(hnew);
         if (gates) {
           float* gp = gates + p * H3 + 3 * u;
           gp[0] = rg;
@@ -1489,7 +1521,17 @@ static void fwd_ks_launch(Ctx* c, const Model& m, const float* params, int t_beg
   unsigned* bar = ws.bar.p;
   long long* tr = trace_buf(c, ws, L);
   const void* fn = pick_fwd_ks(m.H);
-  void* args[] = {&L, &d_bs, &d_offs, &UB, &RB, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &bar, &tr, &tbeg};
+  // short steps hand h over through tagged words (VER_REC_TAG_ROWS; 0 = group barrier + bulk staging).
+  // Measured on B200 at C2: forward recurrence 9.11 -> 8.73 ms per update at 16 rows, no better at 32,
+  // worse at 64.  The backward (dhU rows are 3H wide) measured slower with the same scheme.
+  int tag_th = std::min(env_int("VER_REC_TAG_ROWS", 16), ks_fr(ks_warps(m.H)) * RB);
+  if (L > 4096) tag_th = 0;  // tags: epoch * 4096 + t
+  ws.hx.reserve(c, (size_t)2 * std::max(tag_th, 1) * m.H);
+  ws.hx.zero((size_t)2 * std::max(tag_th, 1) * m.H);  // no stale tag can match (epochs start at 1)
+  unsigned long long* hx = ws.hx.p;
+  unsigned epoch = ++ws.hx_epoch;
+  void* args[] = {&L,   &d_bs, &d_offs, &UB, &RB,   &ux, &xp,     &h0,    &hidden, &gates,
+                  &hun, &hps,  &bar,    &tr, &tbeg, &hx, &tag_th, &epoch};
   coop_launch(c, fn, grid, ks_fwd_smem(m.H), args, 32 * ks_warps(m.H));
   trace_dump(c, "fwd", L, d_bs, tr);
 }
