@@ -212,6 +212,38 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int Z, int M, 
   C[(size_t)m * ldc + n] = s;
 }
 
+// float4 variant (N % 4 == 0): 4 outputs per thread, the Z partial loads of a
+// group of 4 splits issued together (the partials are L2-resident)
+__global__ void splitk_reduce4_kernel(const float* __restrict__ W, int Z, int M, int N, float* __restrict__ C,
+                                      int ldc, int vec_store) {
+  const int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * i4 >= (int64_t)M * N) return;
+  const int64_t i = 4 * i4;
+  const int m = (int)(i / N), n = (int)(i % N);
+  const size_t MN = (size_t)M * N;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  int z = 0;
+  for (; z + 4 <= Z; z += 4) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcg(reinterpret_cast<const float4*>(W + (size_t)(z + u) * MN + i));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w;
+    }
+  }
+  for (; z < Z; ++z) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(W + (size_t)z * MN + i));
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  float* out = C + (size_t)m * ldc + n;
+  if (vec_store) {
+    *reinterpret_cast<float4*>(out) = s;
+  } else {
+    out[0] = s.x; out[1] = s.y; out[2] = s.z; out[3] = s.w;
+  }
+}
+
 // C (M x N, ldc) = op(A) op(B) with deterministic split-K over K.
 template <bool TA, bool TB>
 static void gemm_splitk(Ctx* c, Workspace& ws, int M, int N, int K, const float* A, int lda, const float* B,
@@ -228,7 +260,12 @@ static void gemm_splitk(Ctx* c, Workspace& ws, int M, int N, int K, const float*
     Z = (nkb + per - 1) / per;
     ws.splitk.reserve(c, (size_t)Z * M * N);
     tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, EpiPartial{ws.splitk.p, M, N}, Z);
-    splitk_reduce_kernel<<<cdiv((size_t)M * N, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc);
+    if (N % 4 == 0) {
+      const int vs = (ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
+      splitk_reduce4_kernel<<<cdiv((size_t)M * N / 4, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc, vs);
+    } else {
+      splitk_reduce_kernel<<<cdiv((size_t)M * N, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc);
+    }
     after_launch(c);
     return;
   }
