@@ -676,6 +676,7 @@ void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float
 constexpr int kLossWarps = 8;
 constexpr int kHL = 16;  // fused head gradient: H / 32 <= kHL
 constexpr int kLossStats = 8;  // ws, verr2, H, ratio, clip, w, wmax, (pad)
+constexpr int kLossRows = 8;   // rows per warp-iteration of ppo_loss_rows_kernel
 constexpr double kLog2Pi = 1.8378770664093453;
 
 // One warp per packed row: heads (H -> A+1 dot products), log-softmax /
@@ -925,6 +926,274 @@ __global__ void __launch_bounds__(kLossWarps * 32, 2) ppo_loss_kernel(
   }
 }
 
+// Fused-path variant (H % 32 == 0, H <= 32 kHL, gradients wanted): a warp takes
+// RBT rows at a time.  The heads (H -> A+1 dot products), the head gradient and
+// dhidden stay warp-cooperative per row, but the per-row double-precision loss
+// math (log-softmax / Gaussian log-prob, ratio, clip, IS weight, surrogate,
+// value error, entropy and dhead) runs once per row in lane r instead of
+// redundantly in all 32 lanes; statistics then reduce over the lanes in a fixed
+// shuffle tree (deterministic).
+template <int NA, int RBT>
+__global__ void __launch_bounds__(kLossWarps * 32, 2) ppo_loss_rows_kernel(
+    int S, int H, int A, int continuous, const float* __restrict__ hidden, const float* __restrict__ wh,
+    const float* __restrict__ bh, const float* __restrict__ log_std, const float* __restrict__ act_cont,
+    const int32_t* __restrict__ act_disc, const float* __restrict__ old_logp, const float* __restrict__ adv,
+    const float* __restrict__ ret, const float* __restrict__ frozen_w, double clip, double is_cap,
+    double vcoef, const double* __restrict__ alpha_p, double inv_S, float* __restrict__ dhead,
+    float* __restrict__ dhidden, float* __restrict__ is_w, double* __restrict__ part, int want_grads,
+    float* __restrict__ hpart) {
+  extern __shared__ float s_wh[];  // H x AH, then H x AH + AH block sums of the head gradient
+  __shared__ double s_red[kLossWarps][kLossStats + 32];
+  const int AH = A + 1;
+  const int hl = H / 32;
+  float* s_hg = s_wh + H * AH;
+  float wacc[kHL][NA], bacc[NA];
+#pragma unroll
+  for (int i = 0; i < kHL; ++i)
+#pragma unroll
+    for (int c = 0; c < NA; ++c) wacc[i][c] = 0.f;
+#pragma unroll
+  for (int c = 0; c < NA; ++c) bacc[c] = 0.f;
+  for (int i = threadIdx.x; i < H * AH; i += blockDim.x) s_wh[i] = wh[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double alpha = *alpha_p;
+  const double gH = -alpha * inv_S;
+  double st[kLossStats] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double dlsv[NA];
+#pragma unroll
+  for (int c = 0; c < NA; ++c) dlsv[c] = 0.0;
+  const int gw = blockIdx.x * kLossWarps + warp, nwarps = gridDim.x * kLossWarps;
+  for (int pb = gw * RBT; pb < S; pb += nwarps * RBT) {
+    const int nr = min(RBT, S - pb);
+    // ---- heads of rows pb .. pb + nr - 1 (lane r keeps row r's logits)
+    float lgm[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) lgm[c] = 0.f;
+    float hn[kHL];
+#pragma unroll
+    for (int i = 0; i < kHL; ++i) hn[i] = i < hl ? __ldg(hidden + (size_t)pb * H + lane + 32 * i) : 0.f;
+    for (int r = 0; r < nr; ++r) {
+      float hv[kHL];
+#pragma unroll
+      for (int i = 0; i < kHL; ++i) hv[i] = hn[i];
+      if (r + 1 < nr) {
+#pragma unroll
+        for (int i = 0; i < kHL; ++i) hn[i] = i < hl ? __ldg(hidden + (size_t)(pb + r + 1) * H + lane + 32 * i) : 0.f;
+      }
+      float acc[NA], acc2[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) acc[c] = acc2[c] = 0.f;
+#pragma unroll
+      for (int i = 0; i < kHL; i += 2) {
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < AH) {
+            if (i < hl) acc[c] = fmaf(hv[i], s_wh[(lane + 32 * i) * AH + c], acc[c]);
+            if (i + 1 < hl) acc2[c] = fmaf(hv[i + 1], s_wh[(lane + 32 * (i + 1)) * AH + c], acc2[c]);
+          }
+      }
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        if (c < AH) {
+          float v = acc[c] + acc2[c];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == r) lgm[c] = v;
+        }
+      }
+    }
+    // ---- the loss math of row pb + lane (lanes < nr)
+    float dhm[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) dhm[c] = 0.f;
+    if (lane < nr) {
+      const int p = pb + lane;
+      double lg[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) lg[c] = c < AH ? (double)lgm[c] + (double)bh[c] : 0.0;
+      double value = 0.0;
+#pragma unroll
+      for (int c = 0; c < NA; ++c)
+        if (c == A) value = lg[c];
+      double logp, ent, mx = 0.0, lse = 0.0;
+      const int a = continuous ? 0 : act_disc[p];
+      if (!continuous) {
+        mx = lg[0];
+#pragma unroll
+        for (int c = 1; c < NA; ++c)
+          if (c < A) mx = fmax(mx, lg[c]);
+        double se = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < A) se += exp(lg[c] - mx);
+        lse = log(se);
+        double lga = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c == a) lga = lg[c];
+        logp = lga - mx - lse;
+        ent = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < A) {
+            const double lp = lg[c] - mx - lse;
+            ent -= exp(lp) * lp;
+          }
+      } else {
+        double q = 0.0, sls = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < A) {
+            const double ls = log_std[c];
+            const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * exp(-ls);
+            q += z * z;
+            sls += ls;
+          }
+        logp = -0.5 * q - sls - 0.5 * kLog2Pi * A;
+        ent = sls + 0.5 * (1.0 + kLog2Pi) * A;
+      }
+      const double ratio = exp(logp - (double)old_logp[p]);
+      const double A_ = adv[p];
+      const double w = frozen_w ? (double)frozen_w[p] : fmin(ratio, is_cap);
+      const double s1 = ratio * A_;
+      const double cr = fmin(fmax(ratio, 1.0 - clip), 1.0 + clip);
+      const double s2 = cr * A_;
+      const double sur = fmin(s1, s2);
+      const double verr = value - (double)ret[p];
+      st[0] += w * sur;
+      st[1] += verr * verr;
+      st[2] += ent;
+      st[3] += ratio;
+      st[4] += (ratio < 1.0 - clip || ratio > 1.0 + clip) ? 1.0 : 0.0;  // strict (learner.cpp:104)
+      st[5] += w;
+      st[6] = fmax(st[6], w);
+      if (is_w) is_w[p] = (float)w;
+      if (want_grads) {
+        // cmin tie -> first argument (tape.cpp:157); clip mask inclusive (tape.cpp:146)
+        const double m1 = s1 <= s2 ? 1.0 : 0.0;
+        const double cm = (ratio >= 1.0 - clip && ratio <= 1.0 + clip) ? 1.0 : 0.0;
+        const double dratio = -w * inv_S * (m1 * A_ + (1.0 - m1) * A_ * cm);
+        const double dlogp = dratio * ratio;
+        double dh[NA];
+#pragma unroll
+        for (int c = 0; c < NA; ++c) dh[c] = 0.0;
+        if (!continuous) {
+          double G[NA], sumG = 0.0;
+#pragma unroll
+          for (int c = 0; c < NA; ++c) {
+            G[c] = 0.0;
+            if (c < A) {
+              const double lp = lg[c] - mx - lse;
+              const double pc = exp(lp);
+              G[c] = (c == a ? dlogp : 0.0) + gH * (-pc - pc * lp);
+              sumG += G[c];
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (c < A) dh[c] = G[c] - exp(lg[c] - mx - lse) * sumG;
+        } else {
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (c < A) {
+              const double ls = log_std[c];
+              const double inv = exp(-ls);
+              const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * inv;
+              dh[c] = dlogp * z * inv;
+              dlsv[c] += dlogp * (z * z - 1.0) + gH;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c == A) dh[c] = vcoef * verr * inv_S;
+#pragma unroll
+        for (int c = 0; c < NA; ++c)
+          if (c < AH) {
+            dhm[c] = (float)dh[c];
+            dhead[(size_t)p * AH + c] = dhm[c];
+          }
+      }
+    }
+    if (!want_grads) continue;
+    // ---- head gradient and dhidden = dhead wh^T, warp-cooperative per row
+    for (int r = 0; r < nr; ++r) {
+      const int p = pb + r;
+      float dhf[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) dhf[c] = __shfl_sync(0xffffffffu, dhm[c], r);
+      float hv[kHL];
+#pragma unroll
+      for (int i = 0; i < kHL; ++i) hv[i] = i < hl ? __ldg(hidden + (size_t)p * H + lane + 32 * i) : 0.f;
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        bacc[c] += dhf[c];
+#pragma unroll
+        for (int i = 0; i < kHL; ++i) wacc[i][c] = fmaf(hv[i], dhf[c], wacc[i][c]);
+      }
+#pragma unroll
+      for (int i = 0; i < kHL; ++i) {
+        if (i < hl) {
+          const int u = lane + 32 * i;
+          float sacc = 0.f;
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (c < AH) sacc = fmaf(dhf[c], s_wh[u * AH + c], sacc);
+          dhidden[(size_t)p * H + u] = sacc;
+        }
+      }
+    }
+  }
+  if (want_grads) {
+    // block sums of the head gradient, warps added in a fixed order (deterministic)
+    for (int i = threadIdx.x; i < H * AH + AH; i += blockDim.x) s_hg[i] = 0.f;
+    for (int w = 0; w < kLossWarps; ++w) {
+      __syncthreads();
+      if (warp == w) {
+#pragma unroll
+        for (int i = 0; i < kHL; ++i)
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (i < hl && c < AH) s_hg[(lane + 32 * i) * AH + c] += wacc[i][c];
+        if (lane == 0)
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (c < AH) s_hg[H * AH + c] += bacc[c];
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < H * AH + AH; i += blockDim.x)
+      hpart[(size_t)blockIdx.x * (H * AH + AH) + i] = s_hg[i];
+  }
+  // statistics and the log_std gradient over the lanes (fixed xor tree), then the block
+#pragma unroll
+  for (int k = 0; k < kLossStats; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, st[k], o);
+      st[k] = (k == 6) ? fmax(st[k], y) : st[k] + y;
+    }
+  }
+  double dls = 0.0;
+#pragma unroll
+  for (int c = 0; c < NA; ++c) {
+    double v = dlsv[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == c) dls = v;
+  }
+  if (lane == 0)
+    for (int k = 0; k < kLossStats; ++k) s_red[warp][k] = st[k];
+  s_red[warp][kLossStats + lane] = dls;
+  __syncthreads();
+  if (threadIdx.x < kLossStats + 32) {
+    const int k = threadIdx.x;
+    double s = 0.0;
+    for (int w = 0; w < kLossWarps; ++w) s = (k == 6) ? fmax(s, s_red[w][k]) : s + s_red[w][k];
+    part[(size_t)blockIdx.x * (kLossStats + 32) + k] = s;
+  }
+}
+
 __global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk, int A, int continuous,
                                       double inv_S, int S, double vcoef, const double* __restrict__ alpha_p,
                                       LossStats* __restrict__ out, float* __restrict__ grad_ls,
@@ -989,9 +1258,13 @@ __global__ void __launch_bounds__(1024) head_grad_final_kernel(const float* __re
 
 void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossArgs& a, Workspace& ws,
                  float* grad, LossStats* stats, bool want_grads) {
-  const int nblk = std::max(1, std::min((int)cdiv(S, kLossWarps), 4 * c->num_sms));
-  ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));
   const bool fuse = want_grads && m.H % 32 == 0 && m.H / 32 <= kHL && env_int("VER_LOSS_FUSE", 1);
+  // fused path: kLossRows rows per warp-iteration with the loss math once per row
+  // (ppo_loss_rows_kernel); VER_LOSS_ROWS=0 keeps one row per warp-iteration
+  const int rows = fuse ? env_int("VER_LOSS_ROWS", kLossRows) : 0;
+  const int per_blk = kLossWarps * std::max(1, rows);
+  const int nblk = std::max(1, std::min((int)cdiv(S, per_blk), 4 * c->num_sms));
+  ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));
   const size_t nhg = (size_t)m.H * m.AH + m.AH;
   const size_t smem = sizeof(float) * ((size_t)m.H * m.AH + (fuse ? nhg : 0));
   if (fuse) ws.splitk.reserve(c, (size_t)nblk * nhg);
@@ -1007,7 +1280,13 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
         want_grads ? 1 : 0, hpart);
     after_launch(c);
   };
-  switch (m.AH) {
+  if (rows == kLossRows && m.AH == 3) {
+    run(ppo_loss_rows_kernel<3, kLossRows>);
+  } else if (rows == kLossRows && m.AH == 2) {
+    run(ppo_loss_rows_kernel<2, kLossRows>);
+  } else if (rows == kLossRows && m.AH <= 9) {
+    run(ppo_loss_rows_kernel<9, kLossRows>);
+  } else switch (m.AH) {
     case 2: run(ppo_loss_kernel<2>); break;
     case 3: run(ppo_loss_kernel<3>); break;
     case 4: run(ppo_loss_kernel<4>); break;
