@@ -355,6 +355,54 @@ def run_ours(args, rank, world):
                                     "sample": f"oracle engine (double act), {NS} envs x 2 batches ({cdt:.1f} s)"}
         del eng
 
+    # ---- overlapped collection + learning (bench.cpp:129-160): C2
+    # iterations (collect one rollout of N envs x T steps through the engine, update on
+    # the previous one) serially and with the engine and the learner on separate
+    # streams / host threads
+    ovl = None
+    if rank == 0 and world == 1 and not args.no_collect:
+        from paper_2210_05064_b200.overlap import OverlappedTrainer
+        ce, cl = V.Context(local), V.Context(local)
+        eng2 = V.InferenceEngine(cfg, T_, N_, params, version=0, mode=V.VARIABLE, seed=mix(2, 0xC011), ctx=ce)
+        lrn2 = V.Learner(cfg, params, V.PPOConfig(epochs=EPOCHS, minibatches=MINIBATCHES), V.EntropyController(),
+                         V.CosineSchedule(2.5e-4, 2_000_000), mix(3, 0xF00D), ctx=cl)
+        orng = np.random.default_rng(33)
+        oenv = np.arange(N_, dtype=np.int32)
+
+        def ocollect(e):
+            e.begin_rollout()
+            st_ = np.zeros(N_, np.int32)
+            ep_ = np.zeros(N_, np.int64)
+            e.process_arrays(oenv, orng.standard_normal((N_, D_)).astype(np.float32), first=np.ones(N_, np.uint8),
+                             obs_episode=ep_, obs_step=st_)
+            while not e.rollout_done():
+                st_ += 1
+                e.process_arrays(oenv, orng.standard_normal((N_, D_)).astype(np.float32),
+                                 reward=np.ones(N_, np.float32), done=np.zeros(N_, np.uint8), obs_episode=ep_,
+                                 obs_step=st_)
+            e.finalize_bootstraps()
+            return e.close()
+
+        tr = OverlappedTrainer(eng2, lrn2, ocollect)
+        tr.prime()
+        tr.iteration(read_stats=False)  # warm-up
+        seq_ms, ovl_ms = [], []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            v_ = ocollect(eng2)
+            ce.synchronize()
+            lrn2.update(v_, read_stats=False)
+            cl.synchronize()
+            seq_ms.append(1000.0 * (time.perf_counter() - t0))
+            t0 = time.perf_counter()
+            tr.iteration(read_stats=False)
+            ovl_ms.append(1000.0 * (time.perf_counter() - t0))
+        ovl = {"workload": f"C2 iteration: collect {N_} envs x {T_} steps through InferenceEngine (synthetic env "
+                           f"loop) + one learner update", "serial_ms": statistics.median(seq_ms),
+               "overlapped_ms": statistics.median(ovl_ms),
+               "env_steps_per_s_overlapped": fresh / (statistics.median(ovl_ms) / 1000.0)}
+        del tr, eng2, lrn2
+
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
         # dominant kernel = the GRU recurrence direction with the larger device time
@@ -397,6 +445,8 @@ def run_ours(args, rank, world):
             line["c3"] = c3
         if coll:
             line["collect"] = coll
+        if ovl:
+            line["overlap"] = ovl
         if not args.no_cpu and world == 1:
             cv, dt, sample = cpu_sample()
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}

@@ -11,6 +11,7 @@ no Python or CPU compute path.
 from __future__ import annotations
 
 import ctypes as C
+import sys as _sys
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -74,6 +75,8 @@ class Context:
             self.h = C.c_void_p()
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             self.close()
         except Exception:
@@ -181,6 +184,8 @@ class RolloutView:
         return RolloutView(out, ctx)
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             if self.h:
                 _lib().ver_view_destroy(self.h)
@@ -277,6 +282,8 @@ class RolloutBuffer:
         _check(_lib().ver_rollout_create(self.ctx.h, C.byref(self.cfg), C.byref(self.h)))
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             if self.h:
                 _lib().ver_rollout_destroy(self.h)
@@ -437,6 +444,8 @@ class _Groups:
         self.h = h
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             if self.h:
                 _lib().ver_groups_destroy(self.h)
@@ -477,6 +486,8 @@ class PackedBatch:
         self._cache = None
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             if self.h:
                 _lib().ver_packed_destroy(self.h)
@@ -765,6 +776,8 @@ class Learner:
         self.P = p.size
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             if self.h:
                 _lib().ver_learner_destroy(self.h)
@@ -952,6 +965,8 @@ class InferenceEngine:
                                         C.byref(self.h)))
 
     def __del__(self):
+        if _sys.is_finalizing():
+            return
         try:
             if self.h:
                 _lib().ver_engine_destroy(self.h)
