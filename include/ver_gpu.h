@@ -265,6 +265,20 @@ typedef struct {
 
 typedef struct ver_learner_s* ver_learner;
 
+/* ------------------------------- joint preemption counter */
+/* PreemptCoordinator (distributed.hpp:95-128) across one process per GPU: a device
+   counter owned by one replica, mapped into the others with CUDA IPC (peer memory
+   over NVLink); add is one system-scope atomic, exactly one add per iteration
+   reports fired_now, no collective (replicas commit asynchronously). */
+typedef struct ver_preempt_s* ver_preempt;
+ver_status ver_preempt_create(ver_ctx ctx, ver_preempt* out);          /* owning replica */
+ver_status ver_preempt_ipc_handle(ver_preempt p, uint8_t handle_out[64]);
+ver_status ver_preempt_open(ver_ctx ctx, const uint8_t handle[64], ver_preempt* out); /* other replicas */
+ver_status ver_preempt_destroy(ver_preempt p);
+ver_status ver_preempt_start(ver_preempt p, int64_t threshold);        /* start_iteration; <= 0 disables */
+ver_status ver_preempt_add(ver_preempt p, int64_t n, int64_t* total, int* fired_now); /* add_steps */
+ver_status ver_preempt_state(ver_preempt p, int64_t* total, int* fired);
+
 /* ------------------------------------------ on-disk formats */
 /* dump_view / load_view (rollout.cpp:293-432): the reference's JSONL rollout trace
    (one "meta", one "seq" per sequence with its h0 row, one "step" per slot) */

@@ -175,6 +175,13 @@ _SIGS = {
                                P(c_float), c_int, P(c_float), c_int]),
     "ver_debug_gemm_time": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                     P(c_float)]),
+    "ver_preempt_create": (c_int, [C.c_void_p, P(C.c_void_p)]),
+    "ver_preempt_ipc_handle": (c_int, [C.c_void_p, P(C.c_uint8)]),
+    "ver_preempt_open": (c_int, [C.c_void_p, P(C.c_uint8), P(C.c_void_p)]),
+    "ver_preempt_destroy": (c_int, [C.c_void_p]),
+    "ver_preempt_start": (c_int, [C.c_void_p, c_int64]),
+    "ver_preempt_add": (c_int, [C.c_void_p, c_int64, P(c_int64), P(c_int)]),
+    "ver_preempt_state": (c_int, [C.c_void_p, P(c_int64), P(c_int)]),
     "ver_view_dump_jsonl": (c_int, [C.c_void_p, C.c_char_p]),
     "ver_view_load_jsonl": (c_int, [C.c_void_p, C.c_char_p, P(C.c_void_p)]),
     "ver_learner_save_checkpoint": (c_int, [C.c_void_p, C.c_char_p]),

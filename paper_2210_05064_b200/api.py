@@ -922,6 +922,53 @@ def checkpoint_model_config(path) -> ModelConfig:
                        action_kind=mc.action_kind, num_actions=mc.num_actions, act_dim=mc.act_dim)
 
 
+# ------------------------------------------------------ preemption counter
+class PreemptCounter:
+    """PreemptCoordinator (distributed.hpp:95-128) across processes: one replica
+    creates the device counter and exports its IPC handle (64 bytes); the others
+    open it.  add_steps returns (total, fired_now); exactly one add per
+    iteration fires, and every replica then force-closes its rollout."""
+
+    def __init__(self, ctx: Context | None = None, handle: bytes | None = None):
+        self.ctx = ctx or default_context()
+        self.h = C.c_void_p()
+        if handle is None:
+            _check(_lib().ver_preempt_create(self.ctx.h, C.byref(self.h)))
+            self.owner = True
+        else:
+            buf = (C.c_uint8 * 64).from_buffer_copy(bytes(handle))
+            _check(_lib().ver_preempt_open(self.ctx.h, buf, C.byref(self.h)))
+            self.owner = False
+
+    def __del__(self):
+        if _sys.is_finalizing():
+            return
+        try:
+            if self.h:
+                _lib().ver_preempt_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_uint8 * 64)()
+        _check(_lib().ver_preempt_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def start_iteration(self, threshold: int):
+        _check(_lib().ver_preempt_start(self.h, threshold))
+
+    def add_steps(self, n: int) -> tuple[int, bool]:
+        t, f = C.c_int64(), C.c_int()
+        _check(_lib().ver_preempt_add(self.h, n, C.byref(t), C.byref(f)))
+        return t.value, bool(f.value)
+
+    def state(self) -> tuple[int, bool]:
+        t, f = C.c_int64(), C.c_int()
+        _check(_lib().ver_preempt_state(self.h, C.byref(t), C.byref(f)))
+        return t.value, bool(f.value)
+
+
 # --------------------------------------------------------- inference engine
 @dataclass
 class InferenceRequest:
