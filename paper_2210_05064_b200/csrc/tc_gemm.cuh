@@ -831,12 +831,31 @@ bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
   return true;
 }
 
+// split-K count: the persistent kernel walks tiles x Z work items over the SMs,
+// so the time goes as ceil(tiles Z / SMs) waves of K / Z (+ a per-item overhead)
+// each; pick the cheapest Z (ties: fewer partials), >= 4 K-blocks per split.
+// (Z = ceil(2 SMs / tiles) gave 2.3 waves for the 48-tile weight gradients.)
 inline int splits_for(const Ctx* c, int M, int N, int K) {
-  const int tiles = (int)(cdiv(N, BN) * cdiv(M, BM));
+  const long long tiles = cdiv(N, BN) * cdiv(M, BM);
   const int nkb = (K + BK - 1) / BK;
-  int z = (2 * c->num_sms + tiles - 1) / tiles;
-  z = std::min(z, std::max(1, nkb / 4));  // keep >= 4 K-blocks per split
-  return std::max(1, std::min(z, 64));
+  const int zmax = std::max(1, std::min(64, nkb / 4));
+  if (env_int("VER_TC_SPLIT_OLD", 0)) {
+    int z = (int)((2 * c->num_sms + tiles - 1) / tiles);
+    return std::max(1, std::min(z, zmax));
+  }
+  int best = 1;
+  double best_cost = 1e300;
+  for (int z = 1; z <= zmax; ++z) {
+    const long long waves = (tiles * z + c->num_sms - 1) / c->num_sms;
+    // + ~6 K-blocks' worth of per-item overhead (pipeline fill, accumulator
+    // drain, 64 KB partial-tile store)
+    const double cost = (double)waves * (double)((nkb + z - 1) / z + 6);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = z;
+    }
+  }
+  return best;
 }
 
 }  // namespace tc
