@@ -387,7 +387,7 @@ def run_ours(args, rank, world):
         tr.prime()
         tr.iteration(read_stats=False)  # warm-up
         seq_ms, ovl_ms = [], []
-        for _ in range(3):
+        for _ in range(5):
             t0 = time.perf_counter()
             v_ = ocollect(eng2)
             ce.synchronize()
