@@ -18,6 +18,7 @@ struct EpiStore {
   float* C;
   int ldc;
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0; }
+  EpiStore shifted(int m0) const { return EpiStore{C + (size_t)m0 * ldc, ldc}; }  // rows m0.. (tail split)
   __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v; }
   __device__ void vec4(int m, int n, float4 v, int) const {
     *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) = v;
@@ -28,6 +29,7 @@ struct EpiBias {
   int ldc;
   const float* bias;
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias); }
+  EpiBias shifted(int m0) const { return EpiBias{C + (size_t)m0 * ldc, ldc, bias}; }
   __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v + bias[n]; }
   __device__ void vec4(int m, int n, float4 v, int) const {
     *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) = add4(v, __ldg(reinterpret_cast<const float4*>(bias + n)));
@@ -38,6 +40,7 @@ struct EpiBiasTanh {
   int ldc;
   const float* bias;
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias); }
+  EpiBiasTanh shifted(int m0) const { return EpiBiasTanh{C + (size_t)m0 * ldc, ldc, bias}; }
   __device__ void operator()(int m, int n, float v, int) const {
     C[(size_t)m * ldc + n] = tanhf(v + bias[n]);
   }
@@ -53,6 +56,7 @@ struct EpiAddTerm {  // C = acc + T
   const float* T;
   int ldt;
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(T) && ldt % 4 == 0; }
+  EpiAddTerm shifted(int m0) const { return EpiAddTerm{C + (size_t)m0 * ldc, ldc, T + (size_t)m0 * ldt, ldt}; }
   __device__ void operator()(int m, int n, float v, int) const {
     C[(size_t)m * ldc + n] = v + T[(size_t)m * ldt + n];
   }
@@ -67,6 +71,7 @@ struct EpiTanhGrad {  // C = acc * (1 - Y^2)
   const float* Y;
   int ldy;
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(Y) && ldy % 4 == 0; }
+  EpiTanhGrad shifted(int m0) const { return EpiTanhGrad{C + (size_t)m0 * ldc, ldc, Y + (size_t)m0 * ldy, ldy}; }
   __device__ void operator()(int m, int n, float v, int) const {
     const float y = Y[(size_t)m * ldy + n];
     C[(size_t)m * ldc + n] = v * (1.f - y * y);

@@ -189,11 +189,47 @@ __global__ void __launch_bounds__(GT) sgemm_kernel(int M, int N, int K, const fl
   }
 }
 
+// split-K partials of the tail rows summed in a fixed order, then the GEMM's epilogue
+template <class Epi>
+__global__ void tail_reduce_kernel(const float* __restrict__ W, int Z, int M, int N, Epi epi) {
+  const int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * i4 >= (int64_t)M * N) return;
+  const int64_t i = 4 * i4;
+  const size_t MN = (size_t)M * N;
+  float4 s = __ldcg(reinterpret_cast<const float4*>(W + i));
+  for (int z = 1; z < Z; ++z) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(W + (size_t)z * MN + i));
+    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+  }
+  epi.vec4((int)(i / N), (int)(i % N), s, 0);
+}
+
 template <bool TA, bool TB, class Epi>
 static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi) {
   if (M <= 0 || N <= 0) return;
   if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb, epi)) {
     // op(A): TA ? MN-major : K-major;  op(B): TB ? K-major : MN-major
+    // Tail split: when the last wave of output tiles would leave most SMs idle,
+    // the last m-tiles run as a second launch split two ways along K (twice as
+    // many half-size items fill that wave), reduced with the same epilogue.
+    const int tilesN = (int)cdiv(N, tc::BN), tilesM = (int)cdiv(M, tc::BM);
+    const long long tiles = (long long)tilesN * tilesM, sms = c->num_sms;
+    const long long rem = tiles % sms;
+    const int tail_mt = (int)cdiv(rem, tilesN);
+    const int nkb = (K + tc::BK - 1) / tc::BK;
+    if (env_int("VER_TC_TAIL", 1) && c->precision == 0 && tiles > sms && rem > 0 && 10 * rem < 6 * sms &&
+        tail_mt < tilesM && nkb >= 32 && N % 4 == 0) {  // K < 1024: half a wave saves less than the extra launches
+      const int M1 = (tilesM - tail_mt) * tc::BM, M2 = M - M1;
+      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M1, N, K, A, lda, B, ldb, epi, 1);
+      const float* A2 = TA ? A + M1 : A + (size_t)M1 * lda;
+      float* W = nullptr;
+      VER_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&W), sizeof(float) * 2 * (size_t)M2 * N, c->stream));
+      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M2, N, K, A2, lda, B, ldb, EpiPartial{W, M2, N}, 2);
+      tail_reduce_kernel<<<cdiv((size_t)M2 * N / 4, 256), 256, 0, c->stream>>>(W, 2, M2, N, epi.shifted(M1));
+      after_launch(c);
+      VER_CUDA(cudaFreeAsync(W, c->stream));
+      return;
+    }
     tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, epi, 1);
     return;
   }
