@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(TC_T, 1) gru_bwd_tail(
     int L, int t_stop, const int32_t* __restrict__ bs, const int32_t* __restrict__ offs,
     const float* __restrict__ ux, const float* __restrict__ dhidden, const float* __restrict__ gates,
     const float* __restrict__ hun, const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu,
-    float* __restrict__ gz, long long* trace) {
+    float* __restrict__ gz, long long* trace, int tail_async) {
   constexpr int H3 = 3 * H, UT = H / TC_CL, KW = H3 / (TC_T / 32);
   static_assert(UT == 32 && KW % 4 == 0, "tail kernel: H = 512");
   extern __shared__ float4 sm4[];
@@ -1260,6 +1260,12 @@ __global__ void __launch_bounds__(TC_T, 1) gru_bwd_tail(
   float* red = ds + 2 * TC_TH * H3;             // [16][TC_TH][UT]
   float* gzs = red + (TC_T / 32) * TC_TH * UT;  // [2][TC_TH][UT]
   float* stg = gzs + 2 * TC_TH * UT;            // [TC_TH][3 UT] this CTA's new dhU slice
+  // async handoff (as gru_fwd_tail): fill f of the dhU buffers (f = 0: the
+  // no-carry step L-1, f >= 1: pushed by iteration f-1) lands in buffer f & 1
+  // and completes bs[L-1-f] x 3H x 4 bytes on that buffer's mbarrier
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + TC_TH * 3 * UT);
+  const uint32_t bar_a[2] = {su32(bars), su32(bars + 1)};
+  const bool async_push = tail_async != 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)cl_rank() * UT, u = u0 + lane;
   float w[KW];
@@ -1291,23 +1297,42 @@ __global__ void __launch_bounds__(TC_T, 1) gru_bwd_tail(
     stg[j * 3 * UT + 3 * lane + 2] = dpn * in.r;
   };
   // this step's dhU slices of rows 0..n-1 -> every CTA's buffer dnext
-  auto push = [&](int n, float* dnext) {
+  auto push = [&](int n, float* dnext, int fill) {
     __syncthreads();
-    cl_push4(stg, dnext + 3 * u0, n, 3 * UT / 4, 3 * UT, H3);
+    if (async_push) cl_push4_async(stg, dnext + 3 * u0, n, 3 * UT / 4, 3 * UT, H3, bar_a[fill & 1]);
+    else cl_push4(stg, dnext + 3 * u0, n, 3 * UT / 4, 3 * UT, H3);
   };
+  // fill f exists iff f == 0 or iteration f-1 (t = L-f) pushes, i.e. L-1-f > t_stop
+  auto fill_rows = [&](int f) { return (f == 0 || L - 1 - f > t_stop) ? bs[L - 1 - f] : -1; };
+  if (async_push) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a[0]) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a[1]) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int f = 0; f < 2; ++f)
+        if (L - 1 - f >= 0 && fill_rows(f) >= 0) tl_expect(bar_a[f & 1], (uint32_t)fill_rows(f) * H3 * 4);
+    }
+    cl_sync();  // every CTA's barriers are live before the first push
+  }
   int cur = 0;
   if (j < bs[L - 1]) {
     const size_t p = (size_t)offs[L - 1] + j;
     gate(p, gate_load(p, u, H, gates, hun, hprev, dhidden), 0.f, ds, gzs);
   }
-  push(bs[L - 1], ds);
+  push(bs[L - 1], ds, 0);
   if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[L - 1] = globaltimer();
-  cl_sync();
+  if (!async_push) cl_sync();
   // forward-pass operands of (row j, unit u) at step t-1, loaded one step ahead
   GateIn gin{}, gnext{};
   if (L - 1 > t_stop && j < bs[L - 2]) gin = gate_load((size_t)offs[L - 2] + j, u, H, gates, hun, hprev, dhidden);
   for (int t = L - 1; t > t_stop; --t) {
     const int B = bs[t], Bp = bs[t - 1], op = offs[t - 1];
+    const int fi = L - 1 - t;  // this iteration reads fill fi
+    if (async_push) {
+      tl_wait(bar_a[fi & 1], (uint32_t)((fi >> 1) & 1));
+      if (threadIdx.x == 0 && L - 1 - (fi + 2) >= 0 && fill_rows(fi + 2) >= 0)
+        tl_expect(bar_a[fi & 1], (uint32_t)fill_rows(fi + 2) * H3 * 4);
+    }
     const float* dc = ds + cur * TC_TH * H3;
     if (t - 1 > t_stop && j < bs[t - 2])
       gnext = gate_load((size_t)offs[t - 2] + j, u, H, gates, hun, hprev, dhidden);
@@ -1339,11 +1364,15 @@ __global__ void __launch_bounds__(TC_T, 1) gru_bwd_tail(
       }
       gate((size_t)op + j, gin, tot, ds + (cur ^ 1) * TC_TH * H3, gzs + (cur ^ 1) * TC_TH * UT);
     }
-    if (t - 1 > t_stop) push(Bp, ds + (cur ^ 1) * TC_TH * H3);
+    if (t - 1 > t_stop) push(Bp, ds + (cur ^ 1) * TC_TH * H3, fi + 1);
     gin = gnext;
     cur ^= 1;
-    cl_sync();
+    if (!async_push) cl_sync();
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t - 1] = globaltimer();
+  }
+  if (async_push) {
+    if (L - 1 <= t_stop) tl_wait(bar_a[0], 0);  // fill 0 had no consumer: let it land first
+    cl_sync();  // no CTA exits while a peer may still push into it
   }
 }
 
@@ -1354,7 +1383,8 @@ static size_t tail_fwd_smem(int H) {
 }
 static size_t tail_bwd_smem(int H) {
   return sizeof(float) * ((size_t)2 * TC_TH * 3 * H + (size_t)(TC_T / 32) * TC_TH * (H / TC_CL) +
-                          (size_t)2 * TC_TH * (H / TC_CL) + (size_t)TC_TH * 3 * (H / TC_CL));
+                          (size_t)2 * TC_TH * (H / TC_CL) + (size_t)TC_TH * 3 * (H / TC_CL)) +
+         16 /* two mbarriers */;
 }
 
 // 1 if this device can run one 16-CTA cluster of the tail kernels
@@ -1554,7 +1584,8 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
       float* dhu = ws.dhu.p;
       float* gz = ws.g.p;
       long long* tr = trace_buf(c, ws, L);
-      void* args[] = {&L_, &ts, &d_bs, &d_offs, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &tr};
+      int ta = env_int("VER_REC_TAIL_ASYNC", 1);
+      void* args[] = {&L_, &ts, &d_bs, &d_offs, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &tr, &ta};
       tail_launch(c, reinterpret_cast<const void*>(gru_bwd_tail<512>), tail_bwd_smem(512), args);
       trace_dump(c, "bwdtail", L, d_bs, tr);
       if (t0 == 0) return;
