@@ -1443,7 +1443,8 @@ static void tail_launch(Ctx* c, const void* fn, size_t smem, void** args) {
 // The cluster does the whole matvec on 16 SMs, so its step time grows with the
 // rows (measured on B200 at H = 512: forward 2.0 us at 1 row, 3.7 us at 6;
 // backward 2.2 / 5.3 us) while the K-split kernels take ~3.2 us per short step:
-// the tail takes steps of <= 4 (forward) / <= 3 (backward) rows.
+// the tail takes steps of <= 2 (forward, whose short K-split steps use the
+// tagged handoff) / <= 3 (backward) rows.
 static int tail_start(const int32_t* h_bs, int L, int th) {
   if (!h_bs) return L;
   th = std::min(th, TC_TH);
@@ -1470,7 +1471,7 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
       ScopedEv ev(c, c->rec_tag);
       gru_forward_big(c, m, params, tb, h_bs, h_offs, ws, h0, store);
     }
-    const int t0 = tail_ok(c, m.H) ? std::max(tb, tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 4))) : L;
+    const int t0 = tail_ok(c, m.H) ? std::max(tb, tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 2))) : L;
     if (t0 > tb) fwd_ks_launch(c, m, params, tb, t0, d_bs, d_offs, ws, h0, store);
     if (t0 < L) {
       int t0_ = t0, L_ = L;
@@ -1489,7 +1490,7 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
     return;
   }
   if (L > 0 && tail_ok(c, m.H)) {
-    const int t0 = tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 4));
+    const int t0 = tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 2));
     if (t0 < L) {
       if (t0 > 0) gru_forward_recurrence(c, m, params, t0, d_bs, d_offs, ws, h0, store, nullptr);
       int t0_ = t0, L_ = L;
@@ -1552,9 +1553,9 @@ static void fwd_ks_launch(Ctx* c, const Model& m, const float* params, int t_beg
   long long* tr = trace_buf(c, ws, L);
   const void* fn = pick_fwd_ks(m.H);
   // short steps hand h over through tagged words (VER_REC_TAG_ROWS; 0 = group barrier + bulk staging).
-  // Measured on B200 at C2: forward recurrence 9.11 -> 8.73 ms per update at 16 rows, no better at 32,
-  // worse at 64.  The backward (dhU rows are 3H wide) measured slower with the same scheme.
-  int tag_th = std::min(env_int("VER_REC_TAG_ROWS", 16), ks_fr(ks_warps(m.H)) * RB);
+  // Measured on B200 at C2: forward recurrence 9.11 -> 8.73 ms per update at 16 rows, 8.61 ms at 24
+  // rows with the cluster tail limited to <= 2 rows (VER_REC_TAIL_FWD), worse at 64.  The backward (dhU rows are 3H wide) measured slower with the same scheme.
+  int tag_th = std::min(env_int("VER_REC_TAG_ROWS", 24), ks_fr(ks_warps(m.H)) * RB);
   if (L > 4096) tag_th = 0;  // tags: epoch * 4096 + t
   ws.hx.reserve(c, (size_t)2 * std::max(tag_th, 1) * m.H);
   ws.hx.zero((size_t)2 * std::max(tag_th, 1) * m.H);  // no stale tag can match (epochs start at 1)
