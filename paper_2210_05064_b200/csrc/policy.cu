@@ -204,8 +204,16 @@ __global__ void tail_reduce_kernel(const float* __restrict__ W, int Z, int M, in
   epi.vec4((int)(i / N), (int)(i % N), s, 0);
 }
 
+// lo = x - trunc_tf32(x) of every parameter, once per forward: the weights'
+// 3xTF32 lo operand then comes in by TMA instead of being split per stage
+__global__ void split_lo_kernel(int64_t n, const float* __restrict__ x, float* __restrict__ lo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) lo[i] = tc::lo1(x[i]);
+}
+
 template <bool TA, bool TB, class Epi>
-static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi) {
+static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
+                 const float* Blo = nullptr) {
   if (M <= 0 || N <= 0) return;
   if (c->tensor_cores && tc::usable(M, N, K, A, lda, B, ldb, epi)) {
     // op(A): TA ? MN-major : K-major;  op(B): TB ? K-major : MN-major
@@ -220,17 +228,17 @@ static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
     if (env_int("VER_TC_TAIL", 1) && c->precision == 0 && tiles > sms && rem > 0 && 10 * rem < 6 * sms &&
         tail_mt < tilesM && nkb >= 32 && N % 4 == 0) {  // K < 1024: half a wave saves less than the extra launches
       const int M1 = (tilesM - tail_mt) * tc::BM, M2 = M - M1;
-      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M1, N, K, A, lda, B, ldb, epi, 1);
+      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M1, N, K, A, lda, B, ldb, epi, 1, Blo);
       const float* A2 = TA ? A + M1 : A + (size_t)M1 * lda;
       float* W = nullptr;
       VER_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&W), sizeof(float) * 2 * (size_t)M2 * N, c->stream));
-      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M2, N, K, A2, lda, B, ldb, EpiPartial{W, M2, N}, 2);
+      tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M2, N, K, A2, lda, B, ldb, EpiPartial{W, M2, N}, 2, Blo);
       tail_reduce_kernel<<<cdiv((size_t)M2 * N / 4, 256), 256, 0, c->stream>>>(W, 2, M2, N, epi.shifted(M1));
       after_launch(c);
       VER_CUDA(cudaFreeAsync(W, c->stream));
       return;
     }
-    tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, epi, 1);
+    tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, epi, 1, Blo);
     return;
   }
   dim3 grid(cdiv(N, BN), cdiv(M, BM), 1);
@@ -447,8 +455,13 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
     enc1_kernel<<<g, dim3(32, 8), 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
   }
   after_launch(c);
-  gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2});
-  gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx});
+  ws.wlo.reserve(c, m.P);
+  split_lo_kernel<<<cdiv(m.P, 256), 256, 0, c->stream>>>(m.P, params, ws.wlo.p);
+  after_launch(c);
+  gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2},
+                     ws.wlo.p + m.o_w2);
+  gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx},
+                     ws.wlo.p + m.o_wx);
   gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store, h_bs, h_offs);
 }
 
@@ -1460,10 +1473,12 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
   gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
   gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);
   colsum(c, ws, ws.dpre.p, S, H3, H3, grad + m.o_bx);
-  gemm<false, true>(c, S, E, H3, ws.dpre.p, H3, params + m.o_wx, H3, EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E});
+  gemm<false, true>(c, S, E, H3, ws.dpre.p, H3, params + m.o_wx, H3, EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E},
+                    ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_wx : nullptr);
   gemm_splitk<true, false>(c, ws, E, E, S, ws.e1.p, E, ws.dpre2.p, E, grad + m.o_w2, E);
   colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2);
-  gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E});
+  gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E},
+                    ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_w2 : nullptr);
   {
     // ~4 blocks per SM: 128-feature blocks (float4 path) or 32-feature blocks
     const int col_blocks = (int)cdiv(E, E % 4 == 0 ? 128 : 32);

@@ -46,6 +46,7 @@ struct Workspace {
   DBuf<float> step;                                     // per-step GEMM output of the big recurrence steps
   DBuf<float> sgsteps, sgmaps;                          // stepgemm.cu: step table, per-step A tensor maps
   DBuf<unsigned long long> hx;                          // K-split kernels: tagged h / dhU rows of short steps
+  DBuf<float> wlo;                                      // lo = x - trunc_tf32(x) of the parameters (3xTF32 B operands)
   unsigned hx_epoch = 0;                                // tag epoch, one per K-split launch
   void ensure(const Model& m, size_t S, bool train);
 };

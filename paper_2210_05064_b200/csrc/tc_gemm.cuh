@@ -161,10 +161,14 @@ __device__ __forceinline__ float4 lo_tf32(float4 x) { return make_float4(lo1(x.x
 // form), so shared memory carries only the B operand reads: a third less
 // shared-memory traffic per stage.  Two accumulator buffers then (TMEM:
 // 2 x 128 accumulator columns + 3 stages x 64 A columns).
-template <int AMAJ, int BMAJ, int SPLIT3, class Epi, int ATM = 0>
+// BLO (3xTF32): B's lo part comes pre-split from global memory through a second
+// tensor map (tmBl, e.g. the weights' lo copy made once per minibatch), so the
+// split warps only split A; bit-identical to splitting B in shared memory.
+template <int AMAJ, int BMAJ, int SPLIT3, class Epi, int ATM = 0, int BLO = 0>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                              const __grid_constant__ CUtensorMap tmB, int M,
-                                                             int N, int K, int kb_per_split, int nsplit, Epi epi) {
+                                                             int N, int K, int kb_per_split, int nsplit, Epi epi,
+                                                             const __grid_constant__ CUtensorMap tmBl) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* stg_all = reinterpret_cast<float*>(smem + tc::STAGES * tc::STAGE_BYTES);
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (BLO) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(empty_bar(s), ph ^ 1);
-          mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+          mbar_expect_tx(full_bar(s), (BLO ? 3 : 2) * TILE_BYTES);
           const int k0 = (T.kb0 + i) * BK;
           if (AMAJ == 0) {
             tma_load_2d(tile(s, 0), &tmA, full_bar(s), k0, T.m0);
@@ -253,9 +258,15 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
           }
           if (BMAJ == 0) {
             tma_load_2d(tile(s, 2), &tmB, full_bar(s), k0, T.n0);
+            if (BLO) tma_load_2d(tile(s, 3), &tmBl, full_bar(s), k0, T.n0);
           } else {
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &tmB, full_bar(s), T.n0 + 32 * c, k0);
+            if (BLO) {
+#pragma unroll
+              for (int c = 0; c < BN / 32; ++c)
+                tma_load_2d(tile(s, 3) + c * 4096, &tmBl, full_bar(s), T.n0 + 32 * c, k0);
+            }
           }
         }
       }
@@ -350,8 +361,10 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
             tmem_st32(ta, hv);
             tmem_st32(ta + 32, lv);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (!BLO) {
 #pragma unroll 4
-            for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) blo[q] = lo_tf32(bhi[q]);
+              for (int q = et; q < TILE_BYTES / 16; q += 32 * SPLIT_WARPS) blo[q] = lo_tf32(bhi[q]);
+            }
             (void)alo;
             tc_fence_before();
           } else {
@@ -360,7 +373,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
               // the tensor core reads an fp32 operand as tf32 by truncation, so the
               // landed tile already is hi = trunc_tf32(x); only lo = x - hi is written
               alo[q] = lo_tf32(ahi[q]);
-              blo[q] = lo_tf32(bhi[q]);
+              if (!BLO) blo[q] = lo_tf32(bhi[q]);
             }
           }
           // generic-proxy smem writes -> visible to the tensor core (async proxy)
@@ -762,12 +775,18 @@ template <int AMAJ, int BMAJ, class Epi>
 bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
                  int splits);
 
+// Blo (optional, 3xTF32): B's lo part (x - trunc_tf32(x)) in global memory with
+// B's layout, e.g. a weight's copy made once per minibatch (BLO kernel variant).
 template <int AMAJ, int BMAJ, class Epi>
-void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits) {
+void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits,
+            const float* Blo = nullptr) {
   if (launch_pair<AMAJ, BMAJ>(c, M, N, K, A, lda, B, ldb, epi, splits)) return;
   // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32)
   const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
   const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, BN, false) : make_map(B, K, N, ldb, 32, true);
+  const bool blo = Blo && c->precision == 0 && env_int("VER_TC_BLO", 1) && al16(Blo);
+  const CUtensorMap tbl =
+      !blo ? tb : (BMAJ == 0 ? make_map(Blo, N, K, ldb, BN, false) : make_map(Blo, K, N, ldb, 32, true));
   const int nkb = (K + BK - 1) / BK;
   splits = std::max(1, std::min(splits, nkb));
   const int per = (nkb + splits - 1) / splits;
@@ -776,17 +795,19 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
   const int grid = (int)std::min<long long>(ntiles, c->num_sms);
   auto run = [&](auto kern) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, splits, epi);
+    kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, splits, epi, tbl);
     after_launch(c);
   };
   if (c->precision == 0) {
     if constexpr (AMAJ == 0) {
       if (env_int("VER_TC_ATM", 1)) {
-        run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1>);
+        if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1, 1>);
+        else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1>);
         return;
       }
     }
-    run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
+    if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 0, 1>);
+    else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
   } else {
     run(tc_gemm_kernel<AMAJ, BMAJ, 0, Epi>);
   }

@@ -46,3 +46,24 @@ def test_tc_gemm_pair_3xtf32(monkeypatch, ta, tb, M, N, K):
     for split in (1, 3):
         C3 = V.debug_gemm(A, B, ta, tb, engine=1, splitk=split)
         assert np.abs(C3 - ref).max() / scale < 1e-5, split
+
+
+def test_presplit_weight_operand_bit_identical(monkeypatch):
+    """The weights' lo operand loaded pre-split by TMA (VER_TC_BLO=1, default) gives
+    the same bits as splitting B in shared memory (VER_TC_BLO=0): one full update."""
+    import paper_2210_05064_b200 as V
+    from paper_2210_05064_b200 import synth
+    from paper_2210_05064_b200.rng import mix
+    T, N, E, H = 32, 24, 256, 256
+    cfg = V.ModelConfig(obs_dim=2, encoder_dim=E, hidden_dim=H, action_kind=0, num_actions=2)
+    p = V.params_init(cfg, mix(2, 0x9A9A)).astype(np.float32)
+    wl = synth.make_workload(T, N, obs_dim=2, num_actions=2, hidden_dim=H, seed=3)
+    out = []
+    for blo in ("1", "0"):
+        monkeypatch.setenv("VER_TC_BLO", blo)
+        lg = V.Learner(cfg, p, V.PPOConfig(epochs=2, minibatches=2), run_seed=mix(2, 0xF00D))
+        buf = V.RolloutBuffer(T, N, V.VARIABLE, 0, 2, 0, H)
+        synth.fill_buffer(buf, wl)
+        lg.update(buf.close_rollout())
+        out.append(lg.params())
+    np.testing.assert_array_equal(out[0], out[1])
