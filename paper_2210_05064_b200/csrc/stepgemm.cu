@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     // backward
     const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
     const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
-    long long* trace) {
+    long long* trace, const __grid_constant__ CUtensorMap bmap_lo, int blo) {
+  // blo: U's lo part (x - trunc_tf32(x)) comes pre-split from the parameters' lo
+  // copy (policy.cu split_lo_kernel) by TMA; the split warps then only split A
   constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -121,11 +123,18 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
   auto load_b = [&](int s, int k0, int n0) {
     if (BMAJ == 0) {
       tma_load_2d(tile(s, 2), &bmap, full_bar(s), k0, n0);
+      if (blo) tma_load_2d(tile(s, 3), &bmap_lo, full_bar(s), k0, n0);
     } else {
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tma_load_2d(tile(s, 2) + c * 4096, &bmap, full_bar(s), n0 + 32 * c, k0);
+      if (blo) {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c)
+          tma_load_2d(tile(s, 3) + c * 4096, &bmap_lo, full_bar(s), n0 + 32 * c, k0);
+      }
     }
   };
+  const uint32_t stage_tx = (blo ? 3u : 2u) * TILE_BYTES;
 
   for (int si = 0; si < nsteps; ++si) {
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si] = gtimer();
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
             const int k0 = (kb0 + i) * BK;
             if (i >= b_pre) {
               mbar_wait(empty_bar(s), ph ^ 1);
-              mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+              mbar_expect_tx(full_bar(s), stage_tx);
               load_b(s, k0, n0);
             }
             tma_load_2d(tile(s, 0), amap, full_bar(s), k0, m0);
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
               for (int i = 0; i < b_pre; ++i) {
                 const int s = (it_tma + i) % STAGES;
                 mbar_wait(empty_bar(s), ((it_tma + i) / STAGES & 1) ^ 1);
-                mbar_expect_tx(full_bar(s), 2 * TILE_BYTES);
+                mbar_expect_tx(full_bar(s), stage_tx);
                 load_b(s, (kb2 + i) * BK, (item % tilesN) * BN);
               }
             }
@@ -216,11 +225,16 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           float4* ahi = reinterpret_cast<float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
           float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_BYTES);
-          float4* blo = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+          float4* blo_t = reinterpret_cast<float4*>(st + 3 * TILE_BYTES);
+          if (blo) {
 #pragma unroll 4
-          for (int qq = et; qq < TILE_BYTES / 16; qq += 32 * SPLIT_WARPS) {
-            alo[qq] = lo_tf32(ahi[qq]);
-            blo[qq] = lo_tf32(bhi[qq]);
+            for (int qq = et; qq < TILE_BYTES / 16; qq += 32 * SPLIT_WARPS) alo[qq] = lo_tf32(ahi[qq]);
+          } else {
+#pragma unroll 4
+            for (int qq = et; qq < TILE_BYTES / 16; qq += 32 * SPLIT_WARPS) {
+              alo[qq] = lo_tf32(ahi[qq]);
+              blo_t[qq] = lo_tf32(bhi[qq]);
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -432,6 +446,11 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
   ws.bar.zero(32);
   const float* ux = params + m.o_ux;
   const CUtensorMap bmap = DIR == 0 ? make_map(ux, H, H3, H3, 32, true) : make_map(ux, H, H3, H3, BN, false);
+  // U's lo copy (made by the forward that precedes this launch, policy.cu)
+  const float* ulo = (ws.wlo.n >= (size_t)m.P && env_int("VER_TC_BLO", 1)) ? ws.wlo.p + m.o_ux : nullptr;
+  int blo = ulo != nullptr ? 1 : 0;
+  const CUtensorMap bmap_lo =
+      !blo ? bmap : (DIR == 0 ? make_map(ulo, H, H3, H3, 32, true) : make_map(ulo, H, H3, H3, BN, false));
   const int grid = c->num_sms;
   const void* fn = reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
   static bool attr[2] = {false, false};
@@ -464,8 +483,9 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     ws.trace.zero(TR * (size_t)nsteps + 1);
     tr = ws.trace.p;
   }
-  void* args[] = {&ns,     &dsteps, &dmaps, const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H), &part, &bar,
-                  &xp,     &h0,     &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre, &dhu, &gz, &tr};
+  void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
+                  &part,  &bar,    &xp,     &h0,  &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre,
+                  &dhu,   &gz,     &tr,     const_cast<CUtensorMap*>(&bmap_lo), &blo};
   {
     ScopedEv ev(c, c->rec_tag);
     VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(THREADS), args, SMEM_BYTES, c->stream));

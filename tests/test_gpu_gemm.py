@@ -49,8 +49,9 @@ def test_tc_gemm_pair_3xtf32(monkeypatch, ta, tb, M, N, K):
 
 
 def test_presplit_weight_operand_bit_identical(monkeypatch):
-    """The weights' lo operand loaded pre-split by TMA (VER_TC_BLO=1, default) gives
-    the same bits as splitting B in shared memory (VER_TC_BLO=0): one full update."""
+    """The weights' lo operand loaded pre-split by TMA (VER_TC_BLO=1, default: the
+    encoder / projection GEMMs and the recurrence step kernel's U) gives the same
+    bits as splitting B in shared memory (VER_TC_BLO=0): one full update."""
     import paper_2210_05064_b200 as V
     from paper_2210_05064_b200 import synth
     from paper_2210_05064_b200.rng import mix
@@ -58,6 +59,9 @@ def test_presplit_weight_operand_bit_identical(monkeypatch):
     cfg = V.ModelConfig(obs_dim=2, encoder_dim=E, hidden_dim=H, action_kind=0, num_actions=2)
     p = V.params_init(cfg, mix(2, 0x9A9A)).astype(np.float32)
     wl = synth.make_workload(T, N, obs_dim=2, num_actions=2, hidden_dim=H, seed=3)
+    # big recurrence steps from 6 rows: the persistent step kernel's U operand too
+    monkeypatch.setenv("VER_REC_BIG_FWD", "6")
+    monkeypatch.setenv("VER_REC_BIG_BWD", "6")
     out = []
     for blo in ("1", "0"):
         monkeypatch.setenv("VER_TC_BLO", blo)
