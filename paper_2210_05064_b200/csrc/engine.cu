@@ -382,6 +382,8 @@ struct Engine {
     to_device_layout(m, p, dev);
     params.reserve(c, m.P);
     params.upload(dev.data(), m.P);
+    ws.wlo_stale = true;  // the snapshot is constant until the next set_snapshot
+    ws.wlo_keep = true;
   }
 };
 
@@ -462,6 +464,8 @@ ver_status ver_engine_set_snapshot_learner(ver_engine e, ver_learner l, uint64_t
   sync(lc);
   E.params.reserve(E.c, E.m.P);
   VER_CUDA(cudaMemcpyAsync(E.params.p, src, sizeof(float) * E.m.P, cudaMemcpyDeviceToDevice, E.c->stream));
+  E.ws.wlo_stale = true;
+  E.ws.wlo_keep = true;
   E.version = version;
   VER_API_END
 }

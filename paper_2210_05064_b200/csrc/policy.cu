@@ -455,9 +455,13 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
     enc1_kernel<<<g, dim3(32, 8), 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
   }
   after_launch(c);
-  ws.wlo.reserve(c, m.P);
-  split_lo_kernel<<<cdiv(m.P, 256), 256, 0, c->stream>>>(m.P, params, ws.wlo.p);
-  after_launch(c);
+  if (ws.wlo_stale || ws.wlo_src != params || ws.wlo.n < (size_t)m.P) {
+    ws.wlo.reserve(c, m.P);
+    split_lo_kernel<<<cdiv(m.P, 256), 256, 0, c->stream>>>(m.P, params, ws.wlo.p);
+    after_launch(c);
+    ws.wlo_src = params;
+  }
+  ws.wlo_stale = !ws.wlo_keep;
   gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2},
                      ws.wlo.p + m.o_w2);
   gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx},

@@ -47,6 +47,11 @@ struct Workspace {
   DBuf<float> sgsteps, sgmaps;                          // stepgemm.cu: step table, per-step A tensor maps
   DBuf<unsigned long long> hx;                          // K-split kernels: tagged h / dhU rows of short steps
   DBuf<float> wlo;                                      // lo = x - trunc_tf32(x) of the parameters (3xTF32 B operands)
+  // wlo holds the lo of wlo_src's current values unless wlo_stale; owners whose
+  // parameters change in place (the learner's Adam) leave it stale (the default)
+  const float* wlo_src = nullptr;
+  bool wlo_stale = true;
+  bool wlo_keep = false;  // the caller promises the parameters stay unchanged until it clears this
   unsigned hx_epoch = 0;                                // tag epoch, one per K-split launch
   void ensure(const Model& m, size_t S, bool train);
 };
