@@ -614,6 +614,18 @@ __device__ __forceinline__ void stage_rows(float* dst, const float* src, int row
     bulk_row(su32(dst + (size_t)r * row_floats), src + (size_t)rm.row(c0 + r) * row_floats, bytes, mbar);
 }
 
+// the same by the 32 lanes of one warp: lane 0 posts the byte count, then the
+// lanes issue the row copies in parallel (one issuing thread serialises them)
+__device__ __forceinline__ void stage_rows_warp(float* dst, const float* src, int row_floats, const RowMap& rm,
+                                                int c0, int nr, uint32_t mbar) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t bytes = (uint32_t)row_floats * 4u;
+  if (lane == 0) mb_expect(mbar, bytes * (uint32_t)nr);
+  __syncwarp();
+  for (int r = lane; r < nr; r += 32)
+    bulk_row(su32(dst + (size_t)r * row_floats), src + (size_t)rm.row(c0 + r) * row_floats, bytes, mbar);
+}
+
 __device__ __forceinline__ long long globaltimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -712,9 +724,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
     const float* hp = (t == 0) ? h0 : hidden + (size_t)offs[t - 1] * H;
     const int nch = (rm.n + KS_FR - 1) / KS_FR;
-    if (threadIdx.x == 0 && !tag_in) {
+    if (threadIdx.x < 32 && !tag_in) {
       asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores of other CTAs -> bulk-copy reads
-      stage_rows(hs + buf * KS_FR * H, hp, H, rm, 0, min(KS_FR, rm.n), su32(&mbar[buf]));
+      stage_rows_warp(hs + buf * KS_FR * H, hp, H, rm, 0, min(KS_FR, rm.n), su32(&mbar[buf]));
     }
     for (int ch = 0; ch < nch; ++ch) {
       const int c0 = ch * KS_FR, nr = min(KS_FR, rm.n - c0);
@@ -734,9 +746,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_fwd_ks(
         }
         __syncthreads();
       } else {
-        if (threadIdx.x == 0 && ch + 1 < nch)
-          stage_rows(hs + (buf ^ 1) * KS_FR * H, hp, H, rm, c0 + KS_FR, min(KS_FR, rm.n - c0 - KS_FR),
-                     su32(&mbar[buf ^ 1]));
+        if (threadIdx.x < 32 && ch + 1 < nch)
+          stage_rows_warp(hs + (buf ^ 1) * KS_FR * H, hp, H, rm, c0 + KS_FR, min(KS_FR, rm.n - c0 - KS_FR),
+                          su32(&mbar[buf ^ 1]));
         mb_wait(su32(&mbar[buf]), (phase >> buf) & 1);
         phase ^= 1u << buf;
       }
@@ -870,9 +882,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_bwd_ks(
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[t] = globaltimer();
     const float* src = dhu + (size_t)o * H3;
     const int nch = (rc.n + KS_BR - 1) / KS_BR;
-    if (threadIdx.x == 0 && nch > 0) {
+    if (threadIdx.x < 32 && nch > 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      stage_rows(ds + buf * KS_BR * H3, src, H3, rc, 0, min(KS_BR, rc.n), su32(&mbar[buf]));
+      stage_rows_warp(ds + buf * KS_BR * H3, src, H3, rc, 0, min(KS_BR, rc.n), su32(&mbar[buf]));
     }
     // rows that end at step t-1 (j >= bs_t): gradient from the heads only (overlaps the staging)
     for (int idx = threadIdx.x; idx < re.n * UPB; idx += NT) {
@@ -890,9 +902,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_bwd_ks(
     if (nch > 0) load_g(0, min(KS_BR, rc.n));
     for (int ch = 0; ch < nch; ++ch) {
       const int c0 = ch * KS_BR, nr = min(KS_BR, rc.n - c0);
-      if (threadIdx.x == 0 && ch + 1 < nch)
-        stage_rows(ds + (buf ^ 1) * KS_BR * H3, src, H3, rc, c0 + KS_BR, min(KS_BR, rc.n - c0 - KS_BR),
-                   su32(&mbar[buf ^ 1]));
+      if (threadIdx.x < 32 && ch + 1 < nch)
+        stage_rows_warp(ds + (buf ^ 1) * KS_BR * H3, src, H3, rc, c0 + KS_BR, min(KS_BR, rc.n - c0 - KS_BR),
+                        su32(&mbar[buf ^ 1]));
       float gzv = 0.f;
       if (threadIdx.x < nr * UPB)
         gzv = __ldcg(gz + ((size_t)o + rc.row(c0 + threadIdx.x / UPB)) * H + u0 + threadIdx.x % UPB);
