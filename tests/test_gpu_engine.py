@@ -52,6 +52,7 @@ def _compare_views(vg, vo, cont):
 @pytest.mark.parametrize("kind,mode,E,H,N,T", [
     (0, 1, 16, 16, 12, 8), (0, 0, 16, 16, 12, 8), (1, 1, 16, 16, 12, 8), (0, 1, 512, 512, 24, 6),
     (0, 1, 256, 256, 200, 3),  # batches of >= 150 requests: the GRU step on the tcgen05 step kernel
+    (1, 0, 512, 512, 24, 4),   # Gaussian head, Fixed mode, H = 512
 ])
 def test_engine_lockstep(kind, mode, E, H, N, T):
     import paper_2210_05064_b200 as V

@@ -150,3 +150,34 @@ def test_replay_entry_point(tmp_path):
     assert text.startswith(f"trace: {vg.size()} steps")
     assert text.count("mini-batch ") == 2 and "replayed update: loss" in text
     assert np.isfinite(st.loss)
+
+
+def test_continuous_view_and_checkpoint_round_trip(tmp_path):
+    """Gaussian-head views (action arrays) and checkpoints (log_std tensor)."""
+    import paper_2210_05064_b200 as V
+    from oracle import oracle as O
+    from paper_2210_05064_b200 import synth
+    T, N, D, A, H = 8, 6, 4, 2, 8
+    wl = synth.make_workload(T, N, obs_dim=D, num_actions=2, hidden_dim=H, seed=9)
+    rng = np.random.default_rng(9)
+    S = len(wl.records)
+    from dataclasses import replace
+    recs = replace(wl.records, act_disc=None, act_cont=rng.standard_normal((S, A)).astype(np.float32))
+    buf = V.RolloutBuffer(T, N, V.VARIABLE, 1, D, A, H)
+    synth.fill_buffer(buf, replace(wl, records=recs))
+    v = buf.close_rollout()
+    path = tmp_path / "c.jsonl"
+    v.dump_jsonl(path)
+    a, b = v.to_host(), V.RolloutView.load_jsonl(path).to_host()
+    np.testing.assert_array_equal(a.act_cont, b.act_cont)
+    np.testing.assert_array_equal(a.obs, b.obs)
+    cfg = V.ModelConfig(obs_dim=D, encoder_dim=H, hidden_dim=H, action_kind=1, act_dim=A)
+    p = O.params_init(cfg, 2).astype(np.float32)
+    p[-A:] = [-0.7, 0.4]
+    lg = V.Learner(cfg, p)
+    ck = tmp_path / "c.json"
+    lg.save_checkpoint(ck)
+    assert V.checkpoint_model_config(ck) == cfg
+    lg2 = V.Learner(cfg, np.zeros_like(p))
+    lg2.load_checkpoint(ck)
+    np.testing.assert_array_equal(lg.params(), lg2.params())
