@@ -237,6 +237,11 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel's tail; its results are visible after this wait.  The next kernel may
+  // be scheduled as soon as SMs free up (it waits the same way).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -795,7 +800,17 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
   const int grid = (int)std::min<long long>(ntiles, c->num_sms);
   auto run = [&](auto kern) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    kern<<<grid, THREADS, SMEM_BYTES, c->stream>>>(ta, tb, M, N, K, per, splits, epi, tbl);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl));
     after_launch(c);
   };
   if (c->precision == 0) {
