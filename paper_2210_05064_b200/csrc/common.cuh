@@ -195,6 +195,29 @@ inline void after_launch(Ctx* c) {
   if (e != cudaSuccess) throw Error(VER_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
+// Programmatic dependent launch of the small kernels between the GEMMs: the
+// kernel must start with pdl_wait() (its inputs are visible after it) and may
+// let its own successor be scheduled early with pdl_trigger().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+int env_int(const char* name, int dflt);
+template <class... KArgs, class... Args>
+inline void launch_pdl(Ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) throw Error(VER_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  after_launch(c);
+}
+
 // ------------------------------------------------------------- scans etc.
 // Exclusive scan of n int32 on ctx's stream (out may alias in).  If total is
 // non-null it receives the sum (device).  Implemented in util.cu.

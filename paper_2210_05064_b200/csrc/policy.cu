@@ -192,6 +192,8 @@ __global__ void __launch_bounds__(GT) sgemm_kernel(int M, int N, int K, const fl
 // split-K partials of the tail rows summed in a fixed order, then the GEMM's epilogue
 template <class Epi>
 __global__ void tail_reduce_kernel(const float* __restrict__ W, int Z, int M, int N, Epi epi) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * i4 >= (int64_t)M * N) return;
   const int64_t i = 4 * i4;
@@ -207,6 +209,8 @@ __global__ void tail_reduce_kernel(const float* __restrict__ W, int Z, int M, in
 // lo = x - trunc_tf32(x) of every parameter, once per forward: the weights'
 // 3xTF32 lo operand then comes in by TMA instead of being split per stage
 __global__ void split_lo_kernel(int64_t n, const float* __restrict__ x, float* __restrict__ lo) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) lo[i] = tc::lo1(x[i]);
 }
@@ -233,8 +237,8 @@ static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
       float* W = nullptr;
       VER_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&W), sizeof(float) * 2 * (size_t)M2 * N, c->stream));
       tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M2, N, K, A2, lda, B, ldb, EpiPartial{W, M2, N}, 2, Blo);
-      tail_reduce_kernel<<<cdiv((size_t)M2 * N / 4, 256), 256, 0, c->stream>>>(W, 2, M2, N, epi.shifted(M1));
-      after_launch(c);
+      launch_pdl(c, tail_reduce_kernel<Epi>, dim3(cdiv((size_t)M2 * N / 4, 256)), dim3(256), 0, (const float*)W, 2,
+                 M2, N, epi.shifted(M1));
       VER_CUDA(cudaFreeAsync(W, c->stream));
       return;
     }
@@ -260,6 +264,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int Z, int M, 
 // group of 4 splits issued together (the partials are L2-resident)
 __global__ void splitk_reduce4_kernel(const float* __restrict__ W, int Z, int M, int N, float* __restrict__ C,
                                       int ldc, int vec_store) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * i4 >= (int64_t)M * N) return;
   const int64_t i = 4 * i4;
@@ -306,7 +312,9 @@ static void gemm_splitk(Ctx* c, Workspace& ws, int M, int N, int K, const float*
     tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M, N, K, A, lda, B, ldb, EpiPartial{ws.splitk.p, M, N}, Z);
     if (N % 4 == 0) {
       const int vs = (ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) ? 1 : 0;
-      splitk_reduce4_kernel<<<cdiv((size_t)M * N / 4, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc, vs);
+      launch_pdl(c, splitk_reduce4_kernel, dim3(cdiv((size_t)M * N / 4, 256)), dim3(256), 0,
+                 (const float*)ws.splitk.p, Z, M, N, C, ldc, vs);
+      return;
     } else {
       splitk_reduce_kernel<<<cdiv((size_t)M * N, 256), 256, 0, c->stream>>>(ws.splitk.p, Z, M, N, C, ldc);
     }
@@ -350,6 +358,8 @@ __global__ void colsum_partial_kernel(const float* __restrict__ X, int M, int N,
   }
 }
 __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int N, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   float s = 0.f;
@@ -361,6 +371,8 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
 // 4 independent accumulators, so ~2 KB per warp are in flight (HBM-bound)
 __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __restrict__ X, int M, int N, int ld,
                                                               int rows_per, float* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float4 red[8][32];
   const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;
   const int n = blockIdx.x * 128 + 4 * lane;
@@ -403,10 +415,8 @@ static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, 
     while ((int64_t)col_blocks * cdiv(M, rows_per) > 4 * c->num_sms && rows_per < 8192) rows_per *= 2;
     const int chunks = std::max(1, (int)cdiv(M, rows_per));
     ws.splitk.reserve(c, (size_t)chunks * N);
-    colsum4_partial_kernel<<<dim3(col_blocks, chunks), 256, 0, c->stream>>>(X, M, N, ld, rows_per, ws.splitk.p);
-    after_launch(c);
-    colsum_final_kernel<<<cdiv(N, 256), 256, 0, c->stream>>>(ws.splitk.p, chunks, N, out);
-    after_launch(c);
+    launch_pdl(c, colsum4_partial_kernel, dim3(col_blocks, chunks), dim3(256), 0, X, M, N, ld, rows_per, ws.splitk.p);
+    launch_pdl(c, colsum_final_kernel, dim3(cdiv(N, 256)), dim3(256), 0, (const float*)ws.splitk.p, chunks, N, out);
     return;
   }
   // enough row chunks for ~4 blocks per SM: each thread walks rows_per / 8 rows
@@ -457,8 +467,7 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
   after_launch(c);
   if (ws.wlo_stale || ws.wlo_src != params || ws.wlo.n < (size_t)m.P) {
     ws.wlo.reserve(c, m.P);
-    split_lo_kernel<<<cdiv(m.P, 256), 256, 0, c->stream>>>(m.P, params, ws.wlo.p);
-    after_launch(c);
+    launch_pdl(c, split_lo_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, ws.wlo.p);
     ws.wlo_src = params;
   }
   ws.wlo_stale = !ws.wlo_keep;
@@ -1398,6 +1407,8 @@ __global__ void enc1_grad_partial_kernel(const float* __restrict__ obs, const fl
 __global__ void __launch_bounds__(256) enc1_grad4_partial_kernel(const float* __restrict__ obs,
                                                                  const float* __restrict__ dpre1, int S, int D,
                                                                  int E, int rows_per, float* __restrict__ part) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float4 red[8][32][kMaxD + 1];
   const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;
   const int k = blockIdx.x * 128 + 4 * lane;
@@ -1453,6 +1464,8 @@ __global__ void __launch_bounds__(256) enc1_grad4_partial_kernel(const float* __
 // the 8 group sums reduce in a fixed order (deterministic)
 __global__ void enc1_grad_final_kernel(const float* __restrict__ part, int chunks, int D, int E,
                                        float* __restrict__ db1, float* __restrict__ dw1) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[8][33];
   const int i = blockIdx.x * 32 + threadIdx.x, q = threadIdx.y;
   float s = 0.f;
@@ -1491,8 +1504,8 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
     const int chunks = std::max(1, (int)cdiv(S, rows_per));
     ws.splitk.reserve(c, (size_t)chunks * (m.D + 1) * E);
     if (E % 4 == 0) {
-      enc1_grad4_partial_kernel<<<dim3(cdiv(E, 128), chunks), 256, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E,
-                                                                                   rows_per, ws.splitk.p);
+      launch_pdl(c, enc1_grad4_partial_kernel, dim3(cdiv(E, 128), chunks), dim3(256), 0, obs,
+                 (const float*)ws.dpre1.p, S, m.D, E, rows_per, ws.splitk.p);
     } else {
       enc1_grad_partial_kernel<<<dim3(cdiv(E, 32), chunks), 256, 0, c->stream>>>(obs, ws.dpre1.p, S, m.D, E,
                                                                                  rows_per, ws.splitk.p);
