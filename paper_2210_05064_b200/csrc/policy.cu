@@ -440,6 +440,8 @@ constexpr int kMaxD = 8;  // obs_dim bound of the encoder-input kernels (Model::
 __global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs, int S, int D, int E,
                                                    const float* __restrict__ w1, const float* __restrict__ b1,
                                                    float* __restrict__ e1) {
+  pdl_wait();
+  pdl_trigger();
   const int k = blockIdx.x * 32 + threadIdx.x;
   if (k >= E) return;
   float w[kMaxD];
@@ -462,9 +464,8 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
   const int E = m.E, H3 = 3 * m.H;
   {
     dim3 g(cdiv(E, 32), std::max(1u, std::min(cdiv(S, 8), (unsigned)(8 * c->num_sms / std::max(1u, cdiv(E, 32))))));
-    enc1_kernel<<<g, dim3(32, 8), 0, c->stream>>>(obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
+    launch_pdl(c, enc1_kernel, g, dim3(32, 8), 0, obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
   }
-  after_launch(c);
   if (ws.wlo_stale || ws.wlo_src != params || ws.wlo.n < (size_t)m.P) {
     ws.wlo.reserve(c, m.P);
     launch_pdl(c, split_lo_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, ws.wlo.p);
@@ -1260,6 +1261,8 @@ __global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk,
                                       double inv_S, int S, double vcoef, const double* __restrict__ alpha_p,
                                       LossStats* __restrict__ out, float* __restrict__ grad_ls,
                                       float* __restrict__ ent_slot) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ double tot[kLossStats + 32];
   // warp w reduces statistics w, w + 32 over the block partials (lane-strided,
   // then a fixed shuffle tree: deterministic)
@@ -1302,6 +1305,8 @@ __global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk,
 __global__ void __launch_bounds__(1024) head_grad_final_kernel(const float* __restrict__ hpart, int nblk, int n,
                                                                int nw, float* __restrict__ gwh,
                                                                float* __restrict__ gbh) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
@@ -1357,15 +1362,12 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
     case 9: run(ppo_loss_kernel<9>); break;
     default: run(ppo_loss_kernel<32>); break;
   }
-  ppo_loss_final_kernel<<<1, 1024, 0, c->stream>>>(ws.part.p, nblk, m.A, m.continuous, 1.0 / (double)S, S,
-                                                 a.vcoef, a.alpha, stats,
-                                                 want_grads && m.continuous ? grad + m.o_ls : nullptr,
-                                                 want_grads ? grad + m.P : nullptr);
-  after_launch(c);
+  launch_pdl(c, ppo_loss_final_kernel, dim3(1), dim3(1024), 0, (const double*)ws.part.p, nblk, m.A, m.continuous,
+             1.0 / (double)S, S, a.vcoef, a.alpha, stats, want_grads && m.continuous ? grad + m.o_ls : nullptr,
+             want_grads ? grad + m.P : nullptr);
   if (fuse) {
-    head_grad_final_kernel<<<cdiv(nhg, 32), 1024, 0, c->stream>>>(hpart, nblk, (int)nhg, m.H * m.AH,
-                                                                  grad + m.o_wh, grad + m.o_bh);
-    after_launch(c);
+    launch_pdl(c, head_grad_final_kernel, dim3(cdiv(nhg, 32)), dim3(1024), 0, (const float*)hpart, nblk, (int)nhg,
+               m.H * m.AH, grad + m.o_wh, grad + m.o_bh);
   } else if (want_grads) {
     // head weights / biases: dwh = hidden^T dhead, dbh = colsum(dhead)
     gemm_splitk<true, false>(c, ws, m.H, m.AH, S, ws.hidden.p, m.H, dhead, m.AH, grad + m.o_wh, m.AH);
@@ -1521,6 +1523,8 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
 __global__ void adam_kernel(int64_t P, float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, float lr, float bc1, float bc2, int64_t ls0, int64_t ls1,
                             int* __restrict__ nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
   const float gi = g[i];
@@ -1539,9 +1543,8 @@ void adam_update(Ctx* c, const Model& m, float* params, const float* grad, float
   const double bc1 = 1.0 - std::pow(0.9, (double)step);
   const double bc2 = 1.0 - std::pow(0.999, (double)step);
   const int64_t ls0 = m.continuous ? m.o_ls : -1, ls1 = m.continuous ? m.o_ls + m.A : -1;
-  adam_kernel<<<cdiv(m.P, 256), 256, 0, c->stream>>>(m.P, params, grad, mom, vel, (float)lr, (float)bc1,
-                                                     (float)bc2, ls0, ls1, nonfinite_flag);
-  after_launch(c);
+  launch_pdl(c, adam_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, (const float*)grad, mom, vel,
+             (float)lr, (float)bc1, (float)bc2, ls0, ls1, nonfinite_flag);
 }
 
 // --------------------------------------------------------- host init
