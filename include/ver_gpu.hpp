@@ -134,6 +134,11 @@ class RolloutBuffer : public Handle<ver_rollout, ver_rollout_destroy> {
   }
   void force_close() { check(ver_rollout_force_close(get())); }
   void set_bootstrap(int env, float v) { check(ver_rollout_set_bootstrap(get(), env, v)); }
+  // set_bootstrap for many envs in one call
+  void set_bootstraps(const std::vector<int32_t>& envs, const std::vector<float>& values) {
+    if (envs.size() != values.size()) throw ConfigError("set_bootstraps: size mismatch");
+    check(ver_rollout_set_bootstraps(get(), (int)envs.size(), envs.data(), values.data()));
+  }
   RolloutView close_rollout() {
     ver_view v = nullptr;
     check(ver_rollout_close(get(), &v));
@@ -322,6 +327,48 @@ class InferenceEngine : public Handle<ver_engine, ver_engine_destroy> {
     ver_engine e = nullptr;
     check(ver_engine_create(ctx.get(), &cfg, params.data(), version, &e));
     return e;
+  }
+};
+
+// PreemptCoordinator (distributed.hpp:95-128) across processes: the owning
+// replica creates the counter and ships ipc_handle() to the others, which open it.
+class PreemptCounter : public Handle<ver_preempt, ver_preempt_destroy> {
+ public:
+  explicit PreemptCounter(const Context& ctx) : Handle(make(ctx)) {}
+  PreemptCounter(const Context& ctx, const std::vector<uint8_t>& handle) : Handle(open(ctx, handle)) {}
+  std::vector<uint8_t> ipc_handle() const {
+    std::vector<uint8_t> h(64);
+    check(ver_preempt_ipc_handle(get(), h.data()));
+    return h;
+  }
+  void start_iteration(int64_t threshold) { check(ver_preempt_start(get(), threshold)); }
+  // returns true on exactly one add per iteration (then every replica force-closes)
+  bool add_steps(int64_t n, int64_t* total = nullptr) {
+    int64_t t = 0;
+    int f = 0;
+    check(ver_preempt_add(get(), n, &t, &f));
+    if (total) *total = t;
+    return f != 0;
+  }
+  bool fired(int64_t* total = nullptr) const {
+    int64_t t = 0;
+    int f = 0;
+    check(ver_preempt_state(get(), &t, &f));
+    if (total) *total = t;
+    return f != 0;
+  }
+
+ private:
+  static ver_preempt make(const Context& ctx) {
+    ver_preempt p = nullptr;
+    check(ver_preempt_create(ctx.get(), &p));
+    return p;
+  }
+  static ver_preempt open(const Context& ctx, const std::vector<uint8_t>& h) {
+    if (h.size() != 64) throw ConfigError("PreemptCounter: the IPC handle has 64 bytes");
+    ver_preempt p = nullptr;
+    check(ver_preempt_open(ctx.get(), h.data(), &p));
+    return p;
   }
 };
 
