@@ -355,10 +355,31 @@ ver_status ver_learner_create(ver_ctx ctx, const ver_model_config* c, const floa
                               ver_learner* out);
 ver_status ver_learner_destroy(ver_learner l);
 /* gradient AllReduce over the ctx's NCCL communicator before every Adam step
-   (grad_hook / entropy_hook -> AllReduce::average, distributed.cpp:152-157) */
+   (grad_hook / entropy_hook -> AllReduce::average, distributed.cpp:152-157):
+   one ncclAllReduce(ncclAvg) of the P gradients + the minibatch mean entropy.
+   Runs whenever the ctx has a communicator, a 1-rank one included. */
 ver_status ver_learner_enable_allreduce(ver_learner l, int enable);
-/* Learner::update (learner.cpp:146-193).  stats may be NULL: then nothing is
-   read back and the call does not synchronize. */
+/* Learner::grad_hook (learner.hpp:119-120, called at learner.cpp:137): once per
+   minibatch, between backward and Adam, on the calling host thread.  dev_grads
+   holds `count` = P fp32 gradients in the library's device layout (element-wise
+   reducers are layout-agnostic; ver_param_device_index maps tensors() order to
+   it) on the ctx's device; `stream` is the ctx stream (cudaStream_t).  The hook
+   averages in place, ordered on `stream` (enqueue on it, or finish before
+   returning).  Non-zero return fails the update (VER_ERR_CONFIG).  NULL clears.
+   The built-in NCCL reducer (ver_learner_enable_allreduce) takes precedence. */
+typedef int (*ver_grad_hook)(void* user, float* dev_grads, int64_t count, uint64_t stream);
+ver_status ver_learner_set_grad_hook(ver_learner l, ver_grad_hook fn, void* user);
+/* Learner::entropy_hook (learner.hpp:121-122, called at learner.cpp:142): the
+   minibatch mean entropy (one fp32 on the device) that drives the alpha update;
+   the hook replaces it with the cross-replica mean, same rules as above. */
+typedef int (*ver_entropy_hook)(void* user, float* dev_entropy, uint64_t stream);
+ver_status ver_learner_set_entropy_hook(ver_learner l, ver_entropy_hook fn, void* user);
+/* index_out[k] = device-layout position of tensors()-order parameter k (P entries) */
+ver_status ver_param_device_index(const ver_model_config* c, int64_t* index_out);
+/* Learner::update (learner.cpp:146-193).  stats may be NULL: then the stats are
+   not returned.  The call synchronizes once at the end (the reference's
+   per-minibatch non-finite errors, learner.cpp:111 and :139-140, are latched on
+   the device and raised here with the reference's message and state). */
 ver_status ver_learner_update(ver_learner l, ver_view v, ver_train_stats* stats);
 /* Learner::batch_h0 (learner.cpp:119-130): h0 rows for packed batch (k x H) */
 ver_status ver_learner_batch_h0(ver_learner l, ver_view v, ver_packed p, float* h0_out);
@@ -373,7 +394,8 @@ ver_status ver_learner_set_state(ver_learner l, double alpha, int64_t consumed_s
 /* per-phase device time of the last update, ms, from CUDA events on the ctx
    stream: gae, sampler (split + pack + gather), replay (batch_h0), forward,
    loss, backward, allreduce, adam, then the recurrence kernels alone
-   (rec_fwd nested in forward, rec_bwd nested in backward); n in/out */
+   (rec_fwd nested in forward, rec_bwd nested in backward) and the tcgen05
+   GEMM launches alone (gemm_fwd / gemm_bwd, nested likewise); n in/out */
 ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n);
 /* number of timed intervals (kernel launches for rec_fwd / rec_bwd) behind each
    phase of ver_learner_last_timing; n in/out */
@@ -396,6 +418,51 @@ ver_status ver_debug_gemm(ver_ctx ctx, int engine, int transA, int transB, int M
    (contents arbitrary; no host copies).  ms_out[0] = ms per GEMM. */
 ver_status ver_debug_gemm_time(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K, int splitk,
                                int reps, float* ms_out);
+
+/* ------------------------------------------------ replica driver (L7, DD-PPO) */
+/* The learner section of ReplicaGroup::replica_main (distributed.cpp:208-264),
+   one process per GPU.  Collectives default to NCCL on the ctx communicator
+   (ver_ctx_init_nccl; identity without one); a caller may supply its own
+   host-side reducers instead (all three, blocking, 0 = success). */
+typedef struct {
+  void* user;
+  int (*sum_i64)(void* user, int64_t* host_inout, int n);
+  int (*mean_f64)(void* user, double* host_inout, int n);
+  int (*allgather_f64)(void* user, const double* host_in, int n, double* host_out); /* nranks*n */
+  int nranks, rank;
+} ver_replica_comm;
+
+typedef struct {
+  int T, N;               /* per-replica rollout shape; S_max = T*N*nranks (:249) */
+  int preempt;            /* 0 None, 1 Optimal (PreemptMode, distributed.hpp:34); FixedFraction is collection-side */
+  int per_replica_budget; /* ablation: threshold / R per replica (:257-259) */
+} ver_replica_config;
+
+typedef struct {
+  int64_t iteration;
+  int rank;
+  int deficit, stale_steps;
+  int64_t global_consumed_before; /* consumed_steps handed to the learner (:228) */
+  int64_t global_fresh;           /* fresh steps summed over replicas (:221-226) */
+  double learn_time, mean_learn_time; /* this replica's / the pooled LT (:233-235, :247) */
+  int64_t next_threshold;         /* S* for the next iteration, 0 = no preemption */
+  int64_t per_replica_threshold;  /* S* / R under per_replica_budget, else 0 */
+  ver_train_stats train;
+} ver_iteration_result; /* IterationResult (distributed.hpp:138-147) */
+
+typedef struct ver_replica_s* ver_replica;
+/* comm == NULL: NCCL on ctx */
+ver_status ver_replica_create(ver_ctx ctx, ver_learner learner, const ver_replica_config* cfg,
+                              const ver_replica_comm* comm, ver_replica* out);
+ver_status ver_replica_destroy(ver_replica r);
+/* the joint counter whose start_iteration this replica group drives (rank 0 starts it) */
+ver_status ver_replica_attach_preempt(ver_replica r, ver_preempt counter);
+/* one iteration after collection closed `view` (collect_wall_time < 0: the
+   view's own collect_wall_time): global step count, backfill from the previous
+   rollout, Learner::update, pooled tau / LT -> S*, counter start, barrier */
+ver_status ver_replica_learn(ver_replica r, ver_view view, double collect_wall_time, int last_iteration,
+                             ver_iteration_result* out);
+ver_status ver_replica_state(ver_replica r, int64_t* global_consumed, int64_t* iteration, int* has_prev);
 
 /* ------------------------------------------------------- distributed (L7) */
 /* estimate_time (distributed.cpp:24-51), bisection with device counting */

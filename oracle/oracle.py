@@ -130,8 +130,30 @@ def lib() -> C.CDLL:
                    "vo_learner_destroy"):
             getattr(L, fn).argtypes = [C.c_void_p]
             getattr(L, fn).restype = None
+        L.vo_set_num_threads.argtypes = [c_int]
+        # threads of the oracle's GEMMs / reductions: results are bit-identical for
+        # any count; VER_ORACLE_THREADS (tests: all cores) or 1 (the reference's
+        # single learner thread)
+        import os
+        L.vo_set_num_threads(int(os.environ.get("VER_ORACLE_THREADS", "1")))
+        L.vo_set_sparse_rows.argtypes = [c_int]
+        L.vo_set_sparse_rows(int(os.environ.get("VER_ORACLE_SPARSE_ROWS", "0")))
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle (bit-identical results for any count)."""
+    lib().vo_set_num_threads(int(n))
+
+
+def set_sparse_rows(on: bool) -> None:
+    """`rows` backward without the full-size scatter temporary (identical sums)."""
+    lib().vo_set_sparse_rows(int(on))
+
+
+def get_threads() -> int:
+    return int(lib().vo_get_num_threads())
 
 
 def _chk(r: int):

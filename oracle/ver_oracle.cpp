@@ -24,6 +24,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace vo {
 
@@ -74,15 +77,31 @@ struct Mat {
   }
 };
 
+// Threading (OpenMP, vo_set_num_threads): every parallel loop below splits
+// OUTPUT elements across threads and keeps each element's accumulation order
+// exactly as in the serial loop, so results are bit-identical for any thread
+// count (the parity tests rely on this).  Default 1 thread: the reference's
+// learner thread (bench.cpp:95-205, one thread per replica).
+static bool par_ok(size_t work) { return work >= (size_t)1 << 16; }
+// Test-speed switch (vo_set_sparse_rows): the `rows` backward adds its slice into
+// the parent's gradient directly instead of through a full-size zero matrix
+// (tape.cpp:166-173).  Identical sums; the timed CPU baseline keeps it off so
+// it runs the reference's O(L * S * E) scatter.
+static bool g_sparse_rows = false;
+
 // C += A * B   (A: m x k, B: k x n), blocked i-k-j; stands in for Eigen's GEMM.
 static void gemm_acc(const Mat& A, const Mat& B, Mat& C) {
   const int m = A.r, k = A.c, n = B.c;
-  const int KB = 128, NB = 512;
-  for (int k0 = 0; k0 < k; k0 += KB) {
-    const int k1 = std::min(k, k0 + KB);
-    for (int n0 = 0; n0 < n; n0 += NB) {
-      const int n1 = std::min(n, n0 + NB);
-      for (int i = 0; i < m; ++i) {
+  const int KB = 128, NB = 128, RB = 16;
+  const int rb = (m + RB - 1) / RB, nb = (n + NB - 1) / NB;
+  // tasks = (row block, column block); each output element still sums kk ascending
+#pragma omp parallel for schedule(dynamic, 1) if (par_ok((size_t)m * k * n / 64))
+  for (int task = 0; task < rb * nb; ++task) {
+    const int i0 = (task / nb) * RB, i1 = std::min(m, i0 + RB);
+    const int n0 = (task % nb) * NB, n1 = std::min(n, n0 + NB);
+    for (int k0 = 0; k0 < k; k0 += KB) {
+      const int k1 = std::min(k, k0 + KB);
+      for (int i = i0; i < i1; ++i) {
         double* crow = &C.d[(size_t)i * n];
         const double* arow = &A.d[(size_t)i * k];
         for (int kk = k0; kk < k1; ++kk) {
@@ -101,18 +120,24 @@ static Mat matmul(const Mat& A, const Mat& B) {
   gemm_acc(A, B, C);
   return C;
 }
-// A^T * B  (A: m x k, B: m x n) -> k x n
+// A^T * B  (A: m x k, B: m x n) -> k x n; rows i of A/B are consumed in
+// ascending order for every output element (threads own output rows kk)
 static Mat matmul_tn(const Mat& A, const Mat& B) {
   const int m = A.r, k = A.c, n = B.c;
   Mat C(k, n);
-  for (int i = 0; i < m; ++i) {
-    const double* arow = &A.d[(size_t)i * k];
-    const double* brow = &B.d[(size_t)i * n];
+  const int IB = 256;
+#pragma omp parallel if (par_ok((size_t)m * k * n / 64))
+  for (int i0 = 0; i0 < m; i0 += IB) {
+    const int i1 = std::min(m, i0 + IB);
+#pragma omp for schedule(static)
     for (int kk = 0; kk < k; ++kk) {
-      const double a = arow[kk];
-      if (a == 0.0) continue;
       double* crow = &C.d[(size_t)kk * n];
-      for (int j = 0; j < n; ++j) crow[j] += a * brow[j];
+      for (int i = i0; i < i1; ++i) {
+        const double a = A.d[(size_t)i * k + kk];
+        if (a == 0.0) continue;
+        const double* brow = &B.d[(size_t)i * n];
+        for (int j = 0; j < n; ++j) crow[j] += a * brow[j];
+      }
     }
   }
   return C;
@@ -747,6 +772,10 @@ class Tape {
   NodeId rows(NodeId a, int start, int count) {  // tape.cpp:166-173: full-size scatter
     Mat v = val(a).middle_rows(start, count);
     return push(std::move(v), rgf(a), [a, start, count](Tape& t, const Mat& g) {
+      if (g_sparse_rows) {  // same sums (x + 0 == x), without the full-size temporary
+        t.accum_rows(a, g, start);
+        return;
+      }
       Mat full(t.val(a).r, t.val(a).c);
       std::memcpy(&full.d[(size_t)start * full.c], g.d.data(),
                   sizeof(double) * (size_t)count * full.c);
@@ -844,10 +873,15 @@ class Tape {
   };
   const Mat& val(NodeId id) const { return nodes_[id].value; }
   bool rgf(NodeId id) const { return nodes_[id].requires_grad; }
-  static Mat colsum(const Mat& g) {
+  static Mat colsum(const Mat& g) {  // rows in ascending order per column
     Mat o(1, g.c);
-    for (int i = 0; i < g.r; ++i)
-      for (int j = 0; j < g.c; ++j) o(0, j) += g(i, j);
+    const int nb = (g.c + 15) / 16;
+#pragma omp parallel for schedule(static) if (par_ok(g.size()))
+    for (int b = 0; b < nb; ++b) {
+      const int j0 = b * 16, j1 = std::min(g.c, j0 + 16);
+      for (int i = 0; i < g.r; ++i)
+        for (int j = j0; j < j1; ++j) o.d[j] += g.d[(size_t)i * g.c + j];
+    }
     return o;
   }
   static Mat rowsum(const Mat& g) {
@@ -867,11 +901,25 @@ class Tape {
     nodes_.push_back(std::move(n));
     return static_cast<NodeId>(nodes_.size()) - 1;
   }
+  void accum_rows(NodeId id, const Mat& g, int start) {  // accum of rows(start, g.r) only
+    Node& n = nodes_[id];
+    if (!n.requires_grad) return;
+    if (n.grad.size() == 0) n.grad = Mat(n.value.r, n.value.c);
+    double* dst = n.grad.d.data() + (size_t)start * n.grad.c;
+    const double* src = g.d.data();
+    const int64_t sz = (int64_t)g.size();
+#pragma omp parallel for schedule(static) if (par_ok((size_t)sz))
+    for (int64_t i = 0; i < sz; ++i) dst[i] += src[i];
+  }
   void accum(NodeId id, const Mat& g) {  // tape.cpp:20-27
     Node& n = nodes_[id];
     if (!n.requires_grad) return;
     if (n.grad.size() == 0) n.grad = Mat(n.value.r, n.value.c);
-    for (size_t i = 0; i < g.size(); ++i) n.grad.d[i] += g.d[i];
+    double* dst = n.grad.d.data();
+    const double* src = g.d.data();
+    const int64_t sz = (int64_t)g.size();
+#pragma omp parallel for schedule(static) if (par_ok((size_t)sz))
+    for (int64_t i = 0; i < sz; ++i) dst[i] += src[i];
   }
   std::vector<Node> nodes_;
 };
@@ -1965,6 +2013,24 @@ int vo_param_tensor(const vo_model_config* c, int idx, char* name, int* rows, in
     if (offset) *offset = off;
   })
 }
+int vo_set_num_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n < 1 ? 1 : n);
+#endif
+  return 0;
+}
+int vo_set_sparse_rows(int on) {
+  g_sparse_rows = on != 0;
+  return 0;
+}
+int vo_get_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
 int vo_params_init(const vo_model_config* c, uint64_t seed, double* out) {
   VO_TRY(init_params(model_from(c), seed).to_flat(out))
 }

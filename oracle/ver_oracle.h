@@ -151,6 +151,11 @@ typedef struct {
 } vo_loss_result;
 
 int vo_compute_gae(vo_view v, double gamma, double lambda);
+/* OpenMP threads of the oracle's GEMMs / reductions (bit-identical for any count; default 1) */
+int vo_set_num_threads(int n);
+int vo_get_num_threads(void);
+/* 1: `rows` backward accumulates its slice only (same sums; test speed); 0 (default): reference's full-size scatter */
+int vo_set_sparse_rows(int on);
 
 /* ppo_loss (learner.cpp:52-117) over packed batch p; h0_sorted k x H;
    grads_out (P) and is_w_out (S) may be NULL; frozen_w may be NULL */

@@ -98,6 +98,29 @@ class TrainStats(C.Structure):
                                 "alpha", "lr")]
 
 
+GradHook = C.CFUNCTYPE(c_int, C.c_void_p, C.c_void_p, c_int64, c_uint64)
+EntropyHook = C.CFUNCTYPE(c_int, C.c_void_p, C.c_void_p, c_uint64)
+SumI64 = C.CFUNCTYPE(c_int, C.c_void_p, P(c_int64), c_int)
+MeanF64 = C.CFUNCTYPE(c_int, C.c_void_p, P(c_double), c_int)
+AllgatherF64 = C.CFUNCTYPE(c_int, C.c_void_p, P(c_double), c_int, P(c_double))
+
+
+class ReplicaComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("sum_i64", SumI64), ("mean_f64", MeanF64),
+                ("allgather_f64", AllgatherF64), ("nranks", c_int), ("rank", c_int)]
+
+
+class ReplicaConfig(C.Structure):
+    _fields_ = [("T", c_int), ("N", c_int), ("preempt", c_int), ("per_replica_budget", c_int)]
+
+
+class IterationResult(C.Structure):
+    _fields_ = [("iteration", c_int64), ("rank", c_int), ("deficit", c_int), ("stale_steps", c_int),
+                ("global_consumed_before", c_int64), ("global_fresh", c_int64), ("learn_time", c_double),
+                ("mean_learn_time", c_double), ("next_threshold", c_int64),
+                ("per_replica_threshold", c_int64), ("train", TrainStats)]
+
+
 _SIGS = {
     "ver_version": (C.c_char_p, []),
     "ver_ctx_create": (c_int, [c_int, P(C.c_void_p)]),
@@ -161,6 +184,14 @@ _SIGS = {
                                    P(EntropyController), c_double, c_int64, c_uint64, P(C.c_void_p)]),
     "ver_learner_destroy": (c_int, [C.c_void_p]),
     "ver_learner_enable_allreduce": (c_int, [C.c_void_p, c_int]),
+    "ver_learner_set_grad_hook": (c_int, [C.c_void_p, GradHook, C.c_void_p]),
+    "ver_learner_set_entropy_hook": (c_int, [C.c_void_p, EntropyHook, C.c_void_p]),
+    "ver_param_device_index": (c_int, [P(ModelConfig), P(c_int64)]),
+    "ver_replica_create": (c_int, [C.c_void_p, C.c_void_p, P(ReplicaConfig), P(ReplicaComm), P(C.c_void_p)]),
+    "ver_replica_destroy": (c_int, [C.c_void_p]),
+    "ver_replica_attach_preempt": (c_int, [C.c_void_p, C.c_void_p]),
+    "ver_replica_learn": (c_int, [C.c_void_p, C.c_void_p, c_double, c_int, P(IterationResult)]),
+    "ver_replica_state": (c_int, [C.c_void_p, P(c_int64), P(c_int64), P(c_int)]),
     "ver_learner_update": (c_int, [C.c_void_p, C.c_void_p, P(TrainStats)]),
     "ver_learner_batch_h0": (c_int, [C.c_void_p, C.c_void_p, C.c_void_p, P(c_float)]),
     "ver_learner_get_params": (c_int, [C.c_void_p, P(c_float)]),

@@ -754,7 +754,33 @@ class TrainStats:
     lr: float
 
 
-PHASES = ("gae", "sampler", "replay", "forward", "loss", "backward", "allreduce", "adam", "rec_fwd", "rec_bwd")
+class DeviceBuffer:
+    """A library-owned fp32 device array handed to a learner hook: ``ptr``
+    (device address), ``count`` floats, the ctx ``stream`` (cudaStream_t as int).
+    ``__cuda_array_interface__`` lets torch / cupy wrap it without a copy."""
+
+    def __init__(self, ptr: int, count: int, stream: int, device: int):
+        self.ptr, self.count, self.stream, self.device = int(ptr or 0), int(count), int(stream), device
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.count,), "typestr": "<f4", "data": (self.ptr, False), "version": 3,
+                "stream": self.stream or None}
+
+    def torch(self):
+        import torch
+        return torch.as_tensor(self, device=f"cuda:{self.device}")
+
+
+def param_device_index(cfg: ModelConfig) -> np.ndarray:
+    """index[k] = device-layout position of the tensors()-order parameter k."""
+    out = np.zeros(param_count(cfg), np.int64)
+    _check(_lib().ver_param_device_index(C.byref(cfg.c()), _ptr(out, C.c_int64)))
+    return out
+
+
+PHASES = ("gae", "sampler", "replay", "forward", "loss", "backward", "allreduce", "adam", "rec_fwd", "rec_bwd",
+          "gemm_fwd", "gemm_bwd")
 
 
 class Learner:
@@ -787,6 +813,43 @@ class Learner:
 
     def enable_allreduce(self, on: bool = True):
         _check(_lib().ver_learner_enable_allreduce(self.h, int(on)))
+
+    def set_hooks(self, grad_hook=None, entropy_hook=None):
+        """Learner::grad_hook / entropy_hook (learner.hpp:119-122).
+
+        Each hook is called once per minibatch between backward and Adam with a
+        :class:`DeviceBuffer` (the P gradients in device layout, or the one-float
+        minibatch mean entropy) and must average it in place before returning
+        (the buffer exposes ``__cuda_array_interface__`` and the ctx stream)."""
+        def wrap_g(fn):
+            if fn is None:
+                return L.GradHook()
+
+            def cb(_user, ptr, n, stream):
+                try:
+                    fn(DeviceBuffer(ptr, n, stream, self.ctx.device))
+                    return 0
+                except Exception as e:  # reported as VER_ERR_CONFIG by the update
+                    self._hook_error = e
+                    return 1
+            return L.GradHook(cb)
+
+        def wrap_h(fn):
+            if fn is None:
+                return L.EntropyHook()
+
+            def cb(_user, ptr, stream):
+                try:
+                    fn(DeviceBuffer(ptr, 1, stream, self.ctx.device))
+                    return 0
+                except Exception as e:
+                    self._hook_error = e
+                    return 1
+            return L.EntropyHook(cb)
+
+        self._hooks = (wrap_g(grad_hook), wrap_h(entropy_hook))  # keep the thunks alive
+        _check(_lib().ver_learner_set_grad_hook(self.h, self._hooks[0], None))
+        _check(_lib().ver_learner_set_entropy_hook(self.h, self._hooks[1], None))
 
     def update(self, view: RolloutView, read_stats: bool = True) -> TrainStats | None:
         if not read_stats:
@@ -868,6 +931,102 @@ class Learner:
         n = C.c_int(16)
         _check(_lib().ver_learner_last_timing_counts(self.h, cnt, C.byref(n)))
         return {PHASES[i]: int(cnt[i]) for i in range(min(n.value, len(PHASES)))}
+
+
+@dataclass
+class IterationResult:
+    """IterationResult (distributed.hpp:138-147) of one ver_replica_learn."""
+    iteration: int
+    rank: int
+    deficit: int
+    stale_steps: int
+    global_consumed_before: int
+    global_fresh: int
+    learn_time: float
+    mean_learn_time: float
+    next_threshold: int
+    per_replica_threshold: int
+    train: TrainStats
+
+
+PREEMPT_NONE, PREEMPT_OPTIMAL = 0, 1
+
+
+class Replica:
+    """The learner section of ReplicaGroup::replica_main (distributed.cpp:208-264)
+    for one process per GPU (csrc/replica.cu).
+
+    ``comm=None`` uses NCCL on the learner's context (``Context.init_nccl``); or
+    pass an object with ``nranks``, ``rank`` and host-side ``sum_i64(arr)``,
+    ``mean_f64(arr)`` (in place) and ``allgather_f64(arr) -> array`` methods."""
+
+    def __init__(self, learner: "Learner", T: int, N: int, preempt: int = PREEMPT_OPTIMAL,
+                 per_replica_budget: bool = False, comm=None):
+        self.learner = learner
+        self.ctx = learner.ctx
+        self.h = C.c_void_p()
+        cfg = L.ReplicaConfig(T, N, preempt, int(per_replica_budget))
+        cp = None
+        if comm is not None:
+            self._comm_obj = comm
+
+            def sum_i64(_u, p, n):
+                try:
+                    a = np.ctypeslib.as_array(p, shape=(n,))
+                    comm.sum_i64(a)
+                    return 0
+                except Exception:
+                    return 1
+
+            def mean_f64(_u, p, n):
+                try:
+                    a = np.ctypeslib.as_array(p, shape=(n,))
+                    comm.mean_f64(a)
+                    return 0
+                except Exception:
+                    return 1
+
+            def allgather(_u, p, n, out):
+                try:
+                    a = np.ctypeslib.as_array(p, shape=(n,)).copy()
+                    o = np.ctypeslib.as_array(out, shape=(n * comm.nranks,))
+                    o[:] = comm.allgather_f64(a)
+                    return 0
+                except Exception:
+                    return 1
+
+            self._thunks = (L.SumI64(sum_i64), L.MeanF64(mean_f64), L.AllgatherF64(allgather))
+            cp = L.ReplicaComm(None, *self._thunks, comm.nranks, comm.rank)
+        _check(_lib().ver_replica_create(self.ctx.h, learner.h, C.byref(cfg), C.byref(cp) if cp else None,
+                                         C.byref(self.h)))
+
+    def __del__(self):
+        if _sys.is_finalizing():
+            return
+        try:
+            if self.h:
+                _lib().ver_replica_destroy(self.h)
+                self.h = C.c_void_p()
+        except Exception:
+            pass
+
+    def attach_preempt(self, counter: "PreemptCounter"):
+        self._counter = counter
+        _check(_lib().ver_replica_attach_preempt(self.h, counter.h))
+
+    def learn(self, view: RolloutView, collect_wall_time: float = -1.0, last_iteration: bool = False
+              ) -> IterationResult:
+        r = L.IterationResult()
+        _check(_lib().ver_replica_learn(self.h, view.h, collect_wall_time, int(last_iteration), C.byref(r)))
+        tr = TrainStats(*(getattr(r.train, f) for f, _ in L.TrainStats._fields_))
+        return IterationResult(r.iteration, r.rank, r.deficit, r.stale_steps, r.global_consumed_before,
+                               r.global_fresh, r.learn_time, r.mean_learn_time, r.next_threshold,
+                               r.per_replica_threshold, tr)
+
+    def state(self) -> tuple[int, int, bool]:
+        g, i, hp = C.c_int64(), C.c_int64(), C.c_int()
+        _check(_lib().ver_replica_state(self.h, C.byref(g), C.byref(i), C.byref(hp)))
+        return g.value, i.value, bool(hp.value)
 
 
 def debug_gemm(A, B, transA=False, transB=False, engine=1, splitk=1, ctx: Context | None = None):

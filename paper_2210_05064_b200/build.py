@@ -19,11 +19,31 @@ LIB = OUT_DIR / "libver_b200.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> Path | None:
+    """torch's bundled NCCL (nvidia-nccl wheel, 2.28): the library links against
+    the same libnccl.so.2 torch loads, so one NCCL serves the whole process
+    whichever of the two is imported first (the system 2.27 copy has the same
+    soname and would shadow torch's if it were loaded first)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []) or []:
+        d = Path(base) / "nccl"
+        if (d / "lib" / "libnccl.so.2").exists() and (d / "include" / "nccl.h").exists():
+            return d
+    return None
+
+
+NCCL = _nccl_dir()
+_NCCL_INC = ["-I", str(NCCL / "include")] if NCCL else []
+_NCCL_LIB = (["-Xlinker", str(NCCL / "lib" / "libnccl.so.2"), "-Xlinker", f"-rpath={NCCL / 'lib'}"] if NCCL
+             else ["-L/usr/lib/x86_64-linux-gnu", "-lnccl"])
 CFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC,-O3", "-I", str(ROOT / "include"), "-I", str(CSRC),
+    "-Xcompiler", "-fPIC,-O3", *_NCCL_INC, "-I", str(ROOT / "include"), "-I", str(CSRC),
 ]
-LDFLAGS = ARCH + ["-shared", "-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
+LDFLAGS = ARCH + ["-shared", *_NCCL_LIB]
 
 
 def _sources() -> list[Path]:

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -69,6 +70,7 @@ struct Ctx {
   // optional device-time log: (tag, start, end) event pairs recorded on `stream`
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>>* evlog = nullptr;
   int rec_tag = -1;  // tag for recurrence launches (>= 0 while a learner minibatch is timed)
+  int gemm_tag = -1;  // tag for tcgen05 GEMM launches (same)
   // pinned scratch for small synchronous reads
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
@@ -176,6 +178,11 @@ __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes, const v
   if (b > a)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(b - a)) : "memory");
 }
+// Per-device once-caches (function attributes, occupancy probes): a process may
+// drive several GPUs from several host threads (one learner thread per GPU), so
+// anything derived from a device is cached per device ordinal, never globally.
+constexpr int kMaxDevices = 64;
+inline int dev_slot(const Ctx* c) { return c->device >= 0 && c->device < kMaxDevices ? c->device : 0; }
 // experiments only: integer tuning knob from the environment
 int env_int(const char* name, int dflt);
 

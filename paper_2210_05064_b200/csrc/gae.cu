@@ -477,11 +477,13 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   h[1] = 0x7fffffff;
   misc.upload(h, 2);
   const int smem = kGaeStages * kGaeStageBytes;
-  static int per_sm = 0;
+  static std::atomic<int> per_sm_cache[kMaxDevices];  // per device (0 = not probed yet)
+  int per_sm = per_sm_cache[dev_slot(c)].load();
   if (!per_sm) {
     VER_CUDA(cudaFuncSetAttribute(gae_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_scan_kernel, kGaeBlock, smem));
     per_sm = std::max(1, per_sm);
+    per_sm_cache[dev_slot(c)].store(per_sm);
   }
   const int grid = std::min(ntiles, per_sm * c->num_sms);
   gae_scan_kernel<<<grid, kGaeBlock, smem, c->stream>>>(r, v, d, env, F, boot, valid, off, N, gamma, lambda, adv, ret,

@@ -34,6 +34,7 @@ inline uint64_t mix64(uint64_t a, uint64_t b) {
 enum Phase {
   PH_GAE, PH_SAMPLER, PH_REPLAY, PH_FORWARD, PH_LOSS, PH_BACKWARD, PH_ALLREDUCE, PH_ADAM,
   PH_REC_FWD, PH_REC_BWD,  // recurrence kernels alone (nested in forward / backward)
+  PH_GEMM_FWD, PH_GEMM_BWD,  // tcgen05 GEMM launches alone (nested in forward / backward)
   PH_N
 };
 
@@ -48,11 +49,20 @@ struct Learner {
   uint64_t run_seed = 0;
   int64_t consumed = 0, update_index = 0, adam_step = 0;
   bool allreduce = false;
+  // grad_hook / entropy_hook (learner.hpp:119-122): user reducers on the device
+  // buffers, called between backward and Adam (learner.cpp:137, :142)
+  ver_grad_hook grad_hook = nullptr;
+  void* grad_user = nullptr;
+  ver_entropy_hook ent_hook = nullptr;
+  void* ent_user = nullptr;
   DBuf<float> params, grad, mom, vel;
   DBuf<double> alpha;        // entropy coefficient (device)
   DBuf<double> acc;          // per-update statistics accumulator
   DBuf<LossStats> lstats;
-  DBuf<int> flags;           // [0] non-finite parameters
+  // [0] non-finite parameters after this minibatch's Adam step (atomicOr in Adam),
+  // [1] stopped (set once by the guard; later Adam / alpha updates are skipped),
+  // [2] minibatch index of the failure, [3] 1 = non-finite loss, 2 = non-finite params
+  DBuf<int> flags;
   Workspace ws, wr;          // minibatch / h0-replay workspaces
   DBuf<float> h0s;           // sorted h0 of the current minibatch
   DBuf<float> robs, rh0;     // split-tail replay inputs
@@ -143,7 +153,20 @@ __global__ void replay_final_kernel(const int32_t* __restrict__ last_row, const 
 
 __global__ void alpha_update_kernel(double* __restrict__ alpha, const LossStats* __restrict__ st,
                                     const float* __restrict__ ent_avg, double target, double lr, double lo,
-                                    double hi) {
+                                    double hi, int* __restrict__ flags, int mb) {
+  // The reference throws per minibatch: ProtocolError on a non-finite loss before
+  // backward / hook / Adam (learner.cpp:111), and on non-finite parameters after
+  // Adam, before the entropy update (learner.cpp:139-140).  The device loop does
+  // not stop, so the first failure latches flags[1]: Adam (adam_kernel) and this
+  // update skip from then on, and the host raises the reference's error at the end.
+  if (flags[1]) return;
+  const bool loss_bad = !isfinite(st->loss), par_bad = flags[0] != 0;
+  if (loss_bad || par_bad) {
+    flags[1] = 1;
+    flags[2] = mb;
+    flags[3] = loss_bad ? 1 : 2;
+    return;
+  }
   // EntropyController::update (learner.hpp:36-39)
   const double h = ent_avg ? (double)*ent_avg : st->mean_entropy;
   double a = *alpha + lr * (target - h);
@@ -236,7 +259,7 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
 
 // ---------------------------------------------------------- minibatch
 // learner.cpp:132-144
-static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
+static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr, int mb) {
   Ctx* c = Ln.ctx;
   const Model& m = Ln.m;
   const int S = P.total;
@@ -247,9 +270,11 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   Ln.ws.ensure(m, S, true);
   Ln.mark_begin(PH_FORWARD);
   c->rec_tag = PH_REC_FWD;
+  c->gemm_tag = PH_GEMM_FWD;
   policy_forward(c, m, Ln.params.p, S, P.obs.p, Ln.h0s.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, true,
                  P.h_bs.data(), P.h_offs.data());
   c->rec_tag = -1;
+  c->gemm_tag = -1;
   Ln.mark_end();
   LossArgs la{P.act_cont.p, P.act_disc.p, P.old_logp.p, P.adv.p, P.ret.p, nullptr,
               Ln.cfg.clip, Ln.cfg.is_cap, Ln.cfg.value_loss_coef, Ln.alpha.p};
@@ -258,21 +283,35 @@ static void run_minibatch(Learner& Ln, DView& V, DPacked& P, double lr) {
   Ln.mark_end();
   Ln.mark_begin(PH_BACKWARD);
   c->rec_tag = PH_REC_BWD;
+  c->gemm_tag = PH_GEMM_BWD;
   policy_backward(c, m, Ln.params.p, S, P.obs.p, P.max_len, P.bs.p, P.offs.p, Ln.ws, Ln.grad.p,
                   P.h_bs.data(), P.h_offs.data());
   c->rec_tag = -1;
+  c->gemm_tag = -1;
   Ln.mark_end();
-  const bool ar = Ln.allreduce && c->comm && c->nranks > 1;
-  if (ar) {  // grad_hook -> AllReduce::average; entropy_hook -> average_scalar
+  // grad_hook -> AllReduce::average, entropy_hook -> average_scalar (distributed.cpp:152-157):
+  // the built-in reducer is one ncclAllReduce(avg) of grads + mean entropy (P + 1
+  // floats, the entropy at [P]); user hooks see the same device buffers instead
+  const bool nccl = Ln.allreduce && c->comm;
+  const bool hook_g = nccl || Ln.grad_hook, hook_h = nccl || Ln.ent_hook;
+  if (hook_g || hook_h) {
     Ln.mark_begin(PH_ALLREDUCE);
-    VER_NCCL(ncclAllReduce(Ln.grad.p, Ln.grad.p, (size_t)m.P + 1, ncclFloat32, ncclAvg, c->comm, c->stream));
+    if (nccl) {
+      VER_NCCL(ncclAllReduce(Ln.grad.p, Ln.grad.p, (size_t)m.P + 1, ncclFloat32, ncclAvg, c->comm, c->stream));
+    } else {
+      const uint64_t st = reinterpret_cast<uint64_t>(c->stream);
+      if (Ln.grad_hook && Ln.grad_hook(Ln.grad_user, Ln.grad.p, m.P, st) != 0)
+        config_error("grad_hook failed");
+      if (Ln.ent_hook && Ln.ent_hook(Ln.ent_user, Ln.grad.p + m.P, st) != 0)
+        config_error("entropy_hook failed");
+    }
     Ln.mark_end();
   }
   Ln.mark_begin(PH_ADAM);
   ++Ln.adam_step;
-  adam_update(c, m, Ln.params.p, Ln.grad.p, Ln.mom.p, Ln.vel.p, Ln.adam_step, lr, Ln.flags.p);
-  alpha_update_kernel<<<1, 1, 0, c->stream>>>(Ln.alpha.p, Ln.lstats.p, ar ? Ln.grad.p + m.P : nullptr,
-                                              Ln.ec.target, Ln.ec.lr, Ln.ec.lower, Ln.ec.upper);
+  adam_update(c, m, Ln.params.p, Ln.grad.p, Ln.mom.p, Ln.vel.p, Ln.adam_step, lr, Ln.flags.p, Ln.lstats.p);
+  alpha_update_kernel<<<1, 1, 0, c->stream>>>(Ln.alpha.p, Ln.lstats.p, hook_h ? Ln.grad.p + m.P : nullptr,
+                                              Ln.ec.target, Ln.ec.lr, Ln.ec.lower, Ln.ec.upper, Ln.flags.p, mb);
   after_launch(c);
   stats_accum_kernel<<<1, 1, 0, c->stream>>>(Ln.acc.p, Ln.lstats.p);
   after_launch(c);
@@ -286,6 +325,16 @@ double cosine_lr(double base, int64_t total, int64_t consumed) {  // nn.cpp:308-
   return base * 0.5 * (1.0 + std::cos(M_PI * progress));
 }
 
+// stream `to` waits for the work queued on `from` so far
+static void record_wait(cudaStream_t from, cudaStream_t to) {
+  if (from == to) return;
+  cudaEvent_t e;
+  VER_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  VER_CUDA(cudaEventRecord(e, from));
+  VER_CUDA(cudaStreamWaitEvent(to, e, 0));
+  VER_CUDA(cudaEventDestroy(e));
+}
+
 // learner.cpp:146-193
 static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
   Ctx* c = Ln.ctx;
@@ -293,9 +342,25 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
     config_error("learner_update: view shape does not match the model");
   struct EvGuard {  // the ctx logs recurrence launches into this learner's timing
     Ctx* c;
-    ~EvGuard() { c->evlog = nullptr, c->rec_tag = -1; }
+    ~EvGuard() { c->evlog = nullptr, c->rec_tag = -1, c->gemm_tag = -1; }
   } evg{c};
   c->evlog = Ln.timing ? &Ln.evlog : nullptr;
+  // The view may belong to another context (an engine's close() on the collector
+  // thread).  Everything of this update -- GAE included -- allocates, launches and
+  // synchronizes on the learner's own context: the learner stream first waits for
+  // the view's producer, and the view's stream waits for the update at the end.
+  Ctx* const vc = V.ctx;
+  struct CtxSwap {  // compute_gae / split / pack allocate and launch through V.ctx
+    DView& V;
+    Ctx* keep;
+    Ctx* learner;
+    ~CtxSwap() {
+      if (keep != learner) record_wait(learner->stream, keep->stream);
+      V.ctx = keep;
+    }
+  } swap{V, vc, c};
+  record_wait(vc->stream, c->stream);
+  V.ctx = c;
   Ln.mark_begin(PH_GAE);
   compute_gae(V, Ln.cfg.gamma, Ln.cfg.gae_lambda);
   Ln.mark_end();
@@ -313,20 +378,10 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
     VER_CUDA(cudaStreamCreateWithFlags(&Ln.side.stream, cudaStreamNonBlocking));
   }
   Ctx* sc = &Ln.side;
-  auto record_wait = [](cudaStream_t from, cudaStream_t to) {
-    cudaEvent_t e;
-    VER_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    VER_CUDA(cudaEventRecord(e, from));
-    VER_CUDA(cudaStreamWaitEvent(to, e, 0));
-    VER_CUDA(cudaEventDestroy(e));
-  };
   record_wait(c->stream, sc->stream);  // GAE (advantages / returns) before the gathers
-  struct CtxSwap {  // split / pack allocate and launch through V.ctx
-    DView& V;
-    Ctx* keep;
-    ~CtxSwap() { V.ctx = keep; }
-  } swap{V, V.ctx};
+  const int64_t adam0 = Ln.adam_step;
   std::vector<std::unique_ptr<DPacked>> packs;
+  int mb = 0;
   for (int epoch = 0; epoch < Ln.cfg.epochs; ++epoch) {
     const uint64_t seed = mix64(mix64(Ln.run_seed, (uint64_t)Ln.update_index), (uint64_t)epoch);
     V.ctx = sc;
@@ -337,24 +392,29 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
       prepare_replay(sc, *packs.back());
       V.ctx = c;
       record_wait(sc->stream, c->stream);
-      run_minibatch(Ln, V, *packs.back(), lr);
+      run_minibatch(Ln, V, *packs.back(), lr, mb++);
     }
   }
   c->launches += sc->launches;
   sc->launches = 0;
   // one read-back per update
-  double* h = static_cast<double*>(c->pinned_buf(sizeof(double) * 12));
+  double* h = static_cast<double*>(c->pinned_buf(sizeof(double) * 13));
   VER_CUDA(cudaMemcpyAsync(h, Ln.acc.p, sizeof(double) * 10, cudaMemcpyDeviceToHost, c->stream));
   VER_CUDA(cudaMemcpyAsync(h + 10, Ln.alpha.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  VER_CUDA(cudaMemcpyAsync(h + 11, Ln.flags.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  VER_CUDA(cudaMemcpyAsync(h + 11, Ln.flags.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   if (Ln.timing) Ln.collect_timing();
-  const int nonfinite = reinterpret_cast<int*>(h + 11)[0];
-  if (nonfinite) {
-    Ln.flags.zero(1);
+  const int* fl = reinterpret_cast<const int*>(h + 11);
+  if (fl[1]) {
+    // the reference's state at its throw: Adam steps of the minibatches before the
+    // failing one (+ the failing one's when its parameters went non-finite);
+    // consumed_steps / update_index unchanged
+    const int fmb = fl[2], kind = fl[3];
+    Ln.adam_step = adam0 + fmb + (kind == 2 ? 1 : 0);
+    Ln.flags.zero(4);
+    if (kind == 1) throw Error(VER_ERR_NONFINITE, "ppo_loss: non-finite loss");
     throw Error(VER_ERR_NONFINITE, "update: non-finite parameters");
   }
-  if (!std::isfinite(h[0])) throw Error(VER_ERR_NONFINITE, "ppo_loss: non-finite loss");
   if (out) {
     const double batches = h[9], steps = h[8];
     ver_train_stats s{};
@@ -656,8 +716,8 @@ ver_status ver_learner_create(ver_ctx ctx, const ver_model_config* mc, const flo
   L.alpha.upload(&ec->alpha, 1);
   L.acc.reserve(c, 10);
   L.lstats.reserve(c, 1);
-  L.flags.reserve(c, 1);
-  L.flags.zero(1);
+  L.flags.reserve(c, 4);
+  L.flags.zero(4);
   sync(c);
   *out = h;
   VER_API_END
@@ -676,6 +736,27 @@ ver_status ver_learner_destroy(ver_learner l) {
 ver_status ver_learner_enable_allreduce(ver_learner l, int enable) {
   VER_API_BEGIN
   l->l.allreduce = enable != 0;
+  VER_API_END
+}
+
+ver_status ver_learner_set_grad_hook(ver_learner l, ver_grad_hook fn, void* user) {
+  VER_API_BEGIN
+  l->l.grad_hook = fn;
+  l->l.grad_user = user;
+  VER_API_END
+}
+
+ver_status ver_learner_set_entropy_hook(ver_learner l, ver_entropy_hook fn, void* user) {
+  VER_API_BEGIN
+  l->l.ent_hook = fn;
+  l->l.ent_user = user;
+  VER_API_END
+}
+
+ver_status ver_param_device_index(const ver_model_config* c, int64_t* index_out) {
+  VER_API_BEGIN
+  const Model m = Model::make(*c);
+  for (int64_t k = 0; k < m.P; ++k) index_out[k] = m.dev_index[k];
   VER_API_END
 }
 

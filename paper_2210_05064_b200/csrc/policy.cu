@@ -1522,11 +1522,15 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
 // ---------------------------------------------------------------- Adam
 __global__ void adam_kernel(int64_t P, float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
                             float* __restrict__ v, float lr, float bc1, float bc2, int64_t ls0, int64_t ls1,
-                            int* __restrict__ nonfinite) {
+                            int* __restrict__ nonfinite, const LossStats* __restrict__ st) {
   pdl_wait();
   pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
+  // learner guard (alpha_update_kernel): no step after a failed minibatch
+  // (flag [1]) or on a non-finite loss (the reference throws before Adam,
+  // learner.cpp:111)
+  if (st && (nonfinite[1] || !isfinite(st->loss))) return;
   const float gi = g[i];
   const float mi = 0.9f * m[i] + (1.f - 0.9f) * gi;
   const float vi = 0.999f * v[i] + (1.f - 0.999f) * (gi * gi);
@@ -1539,12 +1543,12 @@ __global__ void adam_kernel(int64_t P, float* __restrict__ w, const float* __res
 }
 
 void adam_update(Ctx* c, const Model& m, float* params, const float* grad, float* mom, float* vel, int64_t step,
-                 double lr, int* nonfinite_flag) {
+                 double lr, int* nonfinite_flag, const LossStats* guard) {
   const double bc1 = 1.0 - std::pow(0.9, (double)step);
   const double bc2 = 1.0 - std::pow(0.999, (double)step);
   const int64_t ls0 = m.continuous ? m.o_ls : -1, ls1 = m.continuous ? m.o_ls + m.A : -1;
   launch_pdl(c, adam_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, (const float*)grad, mom, vel,
-             (float)lr, (float)bc1, (float)bc2, ls0, ls1, nonfinite_flag);
+             (float)lr, (float)bc1, (float)bc2, ls0, ls1, nonfinite_flag, guard);
 }
 
 // --------------------------------------------------------- host init

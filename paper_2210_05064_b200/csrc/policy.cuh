@@ -125,8 +125,10 @@ void policy_rows(Ctx* c, const Model& m, const float* params, int S, const float
 void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out);
 
 // Adam (nn.cpp:291-306) + log_std clamp (nn.cpp:105-109) + finiteness flag.
+// guard (learner): skip the step when guard->loss is non-finite or
+// nonfinite_flag[1] (an earlier minibatch failed) is set; NULL = always step.
 void adam_update(Ctx* c, const Model& m, float* params, const float* grad, float* mom, float* vel,
-                 int64_t step, double lr, int* nonfinite_flag);
+                 int64_t step, double lr, int* nonfinite_flag, const LossStats* guard = nullptr);
 
 // Host-double parameter init in tensors() order (nn.cpp:16-81).
 void init_params_host(const ver_model_config& c, uint64_t seed, double* out);

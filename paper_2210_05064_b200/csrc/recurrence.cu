@@ -1401,10 +1401,11 @@ static size_t tail_bwd_smem(int H) {
 
 // 1 if this device can run one 16-CTA cluster of the tail kernels
 static bool tail_ok(Ctx* c, int H) {
-  static int ok = -1;
+  static std::atomic<int> ok_cache[kMaxDevices];  // per device: 0 unknown, 1 no, 2 yes
   if (H != 512 || rec_mode() != 0 || env_int("VER_REC_TAIL", 1) == 0) return false;
-  if (ok >= 0) return ok == 1;
-  ok = 0;
+  std::atomic<int>& okc = ok_cache[dev_slot(c)];
+  if (okc.load() != 0) return okc.load() == 2;
+  okc.store(1);
   const void* fns[2] = {reinterpret_cast<const void*>(gru_fwd_tail<512>),
                         reinterpret_cast<const void*>(gru_bwd_tail<512>)};
   const size_t sm[2] = {tail_fwd_smem(512), tail_bwd_smem(512)};
@@ -1431,7 +1432,7 @@ static bool tail_ok(Ctx* c, int H) {
       return false;
     }
   }
-  ok = 1;
+  okc.store(2);
   return true;
 }
 static void tail_launch(Ctx* c, const void* fn, size_t smem, void** args) {

@@ -139,36 +139,41 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
   for (int si = 0; si < nsteps; ++si) {
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si] = gtimer();
     const Step S = steps[si];
-    const int W = S.tilesM * tilesN * S.Z;
-    const int item = blockIdx.x;
-    if (S.B > 0 && item < W) {
+    // work items (tilesM x tilesN output tiles x Z K-splits) walked grid-stride:
+    // a step with more tiles than CTAs (B > 1536 rows forward, > 4736 backward at
+    // H = 512, i.e. C3's first steps) gives a CTA several items in a row; every
+    // role walks the same item sequence
+    const int W = S.B > 0 ? S.tilesM * tilesN * S.Z : 0;
+    const CUtensorMap* amap = amaps + si;
+    for (int item = blockIdx.x; item < W; item += gridDim.x) {
+      const bool first_item = item == (int)blockIdx.x, last_item = item + (int)gridDim.x >= W;
       const int nt = item % tilesN, q = item / tilesN;
       const int m0 = (q % S.tilesM) * BM, n0 = nt * BN, z = q / S.tilesM;
       const int kb0 = z * S.per;
       const int nkb = max(0, min(nkb_total, kb0 + S.per) - kb0);
-      const CUtensorMap* amap = amaps + si;
       if (warp == 0) {
         if (lane == 0) {
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // h / dhU rows written by the gate phase
+          if (first_item) asm volatile("fence.proxy.async.global;" ::: "memory");  // rows of the gate phase
           for (int i = 0; i < nkb; ++i, ++it_tma) {
             const int s = it_tma % STAGES;
             const uint32_t ph = (it_tma / STAGES) & 1;
             const int k0 = (kb0 + i) * BK;
-            if (i >= b_pre) {
+            if (!first_item || i >= b_pre) {
               mbar_wait(empty_bar(s), ph ^ 1);
               mbar_expect_tx(full_bar(s), stage_tx);
               load_b(s, k0, n0);
             }
             tma_load_2d(tile(s, 0), amap, full_bar(s), k0, m0);
           }
-          // the next step's first B tiles (U does not change across steps) and its
-          // A tensor map, issued before the grid barriers
-          b_pre = 0;
-          if (si + 1 < nsteps) {
+          // after this CTA's last item: the next step's first B tiles (U does not
+          // change across steps) and its A tensor map, issued before the grid barriers
+          if (last_item) b_pre = 0;
+          if (last_item && si + 1 < nsteps) {
             const Step S2 = steps[si + 1];
-            if (S2.B > 0 && item < S2.tilesM * tilesN * S2.Z) {
+            if (S2.B > 0 && (int)blockIdx.x < S2.tilesM * tilesN * S2.Z) {
+              const int item2 = blockIdx.x;
               asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(amaps + si + 1)) : "memory");
-              const int z2 = item / tilesN / S2.tilesM;
+              const int z2 = item2 / tilesN / S2.tilesM;
               const int kb2 = z2 * S2.per;
               const int nkb2 = max(0, min(nkb_total, kb2 + S2.per) - kb2);
               b_pre = min(nkb2, STAGES);
@@ -176,7 +181,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
                 const int s = (it_tma + i) % STAGES;
                 mbar_wait(empty_bar(s), ((it_tma + i) / STAGES & 1) ^ 1);
                 mbar_expect_tx(full_bar(s), stage_tx);
-                load_b(s, (kb2 + i) * BK, (item % tilesN) * BN);
+                load_b(s, (kb2 + i) * BK, (item2 % tilesN) * BN);
               }
             }
           }
@@ -453,10 +458,10 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
       !blo ? bmap : (DIR == 0 ? make_map(ulo, H, H3, H3, 32, true) : make_map(ulo, H, H3, H3, BN, false));
   const int grid = c->num_sms;
   const void* fn = reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
-  static bool attr[2] = {false, false};
-  if (!attr[DIR]) {
+  static std::atomic<bool> attr[kMaxDevices][2];  // per device: a function attribute is per device
+  if (!attr[dev_slot(c)][DIR].load()) {
     VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr[DIR] = true;
+    attr[dev_slot(c)][DIR].store(true);
   }
   int ns = nsteps;
   const Step* dsteps = reinterpret_cast<const Step*>(ws.sgsteps.p);

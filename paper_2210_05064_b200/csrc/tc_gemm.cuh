@@ -785,6 +785,7 @@ bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
 template <int AMAJ, int BMAJ, class Epi>
 void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits,
             const float* Blo = nullptr) {
+  ScopedEv ev(c, c->gemm_tag);  // learner timing of the GEMM family (bench roofline)
   if (launch_pair<AMAJ, BMAJ>(c, M, N, K, A, lda, B, ldb, epi, splits)) return;
   // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32)
   const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);

@@ -337,7 +337,7 @@ ver_status ver_allreduce_sum_i64(ver_ctx ctx, int64_t* h, int n) {
   VER_API_BEGIN
   Ctx* c = &ctx->c;
   activate(c);
-  if (!c->comm || c->nranks == 1 || n == 0) return VER_OK;
+  if (!c->comm || n == 0) return VER_OK;  // no communicator: one replica, identity
   DBuf<int64_t> d;
   d.reserve(c, n);
   d.upload(h, n);
@@ -351,7 +351,7 @@ ver_status ver_allreduce_mean_f64(ver_ctx ctx, double* h, int n) {
   VER_API_BEGIN
   Ctx* c = &ctx->c;
   activate(c);
-  if (!c->comm || c->nranks == 1 || n == 0) return VER_OK;
+  if (!c->comm || n == 0) return VER_OK;  // no communicator: one replica, identity
   DBuf<double> d;
   d.reserve(c, n);
   d.upload(h, n);
@@ -365,7 +365,7 @@ ver_status ver_allgather_f64(ver_ctx ctx, const double* in, int n, double* out) 
   VER_API_BEGIN
   Ctx* c = &ctx->c;
   activate(c);
-  if (!c->comm || c->nranks == 1) {
+  if (!c->comm) {  // no communicator: one replica, identity
     std::memcpy(out, in, sizeof(double) * n);
     return VER_OK;
   }

@@ -6,6 +6,9 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
+# the oracle's threaded loops are bit-identical for any thread count: use all cores
+os.environ.setdefault("VER_ORACLE_THREADS", str(os.cpu_count() or 1))
+os.environ.setdefault("VER_ORACLE_SPARSE_ROWS", "1")
 
 
 def pytest_configure(config):
