@@ -2,15 +2,18 @@
 """VER learner hot-path benchmark (BASELINE.json metric: learner env-steps/sec;
 GAE+gather HBM GB/s vs peak).
 
-Workload (configs[1]): N=256 envs/GPU with lognormal step times, T=128 VER
-rollout (32,768 fresh steps), encoder 2x512 + GRU-512 policy (E=H=512, D=2,
-A=2), 4 epochs x 2 minibatches, synthetic data.
+Headline workload (configs[2], C3): N=4096 envs per GPU with lognormal step
+times, T=128 VER rollout (524,288 fresh steps per GPU), encoder 2x512 + GRU-512
+policy (E=H=512, D=2, A=2), 3 epochs x 2 minibatches, synthetic data (SURVEY.md
+§8d).  Under torchrun with N GPUs it is configs[3] (C4): the same 4096 envs per
+GPU (weak scaling, seeds mix(1, rank)) with one NCCL AllReduce of the P+1
+gradient floats per minibatch.
 
-A step = one full Learner::update (GAE -> 4 epochs x 2 x (split, pack, gather,
+A step = one full Learner::update (GAE -> 3 epochs x 2 x (split, pack, gather,
 split-tail replay, forward, fused PPO loss, backward, [NCCL AllReduce], Adam,
 alpha)) on a device-resident closed view.  `e2e` = the same through the C-ABI
 with host buffers: append the host arrival log, close_rollout (H2D + device
-compaction), update, read the stats back.
+compaction), update, read the stats back.  configs[1] (C2) is an extra field.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -23,7 +26,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 from pathlib import Path
 
@@ -32,8 +34,13 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-T_, N_, E_, H_, D_, A_ = 128, 256, 512, 512, 2, 2
-EPOCHS, MINIBATCHES = 4, 2
+T_, E_, H_, D_, A_ = 128, 512, 512, 2, 2
+MINIBATCHES = 2
+# headline: configs[2] (C3) -- N = 4096 envs per GPU, GRU-512, 3 epochs (learner.hpp:18
+# default) x 2 minibatches; at N > 1 GPUs it is configs[3] (C4, 4096 envs per GPU)
+N_, EPOCHS = 4096, 3
+# extra field: configs[1] (C2) -- N = 256 envs, 4 epochs x 2 minibatches
+N2, EPOCHS2 = 256, 4
 METRIC = "learner env-steps/sec"
 UNIT = "env-steps/s"
 
@@ -51,20 +58,13 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def dom_traffic(dom):
-    """DRAM bytes (read + write) per launch of the dominant kernel from the
-    committed `ncu --set full` capture (profiles/traffic.json), or None."""
+def traffic_entry(name):
+    """DRAM bytes (read + write) per launch of a kernel from the committed
+    `ncu --set full` captures (profiles/traffic.json), or None."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
         return None
-    d = json.loads(p.read_text())
-    # one minibatch of one direction = one K-split launch + one persistent step-kernel
-    # launch (the cluster tail moves a few MB); both captured from the same update
-    ks = d.get("gru_bwd_ks" if dom == "rec_bwd" else "gru_fwd_ks", {}).get("dram_bytes_per_launch")
-    sg = d.get("gru_step_gemm_bwd" if dom == "rec_bwd" else "gru_step_gemm_fwd", {}).get("dram_bytes_per_launch")
-    if ks is None:
-        return None
-    return ks + (sg or 0.0)
+    return json.loads(p.read_text()).get(name)
 
 
 # ------------------------------------------------------------------ clocks
@@ -115,58 +115,98 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- CPU side
-def cpu_sample(n_envs_sample=64, seed=1):
-    """The oracle (CPU double restatement, single thread as the reference's
-    learner thread) on a bounded sample: N=64 of the 256 envs (same T, model,
-    epochs, B), GAE + minibatch 0 of epoch 0 timed, extrapolated to the full
-    4 x 2 minibatch update.  Returns (env-steps/s, seconds measured, sample)."""
+def cpu_sample(n_envs=128, epochs=EPOCHS, threads=None, seed=3):
+    """The oracle (CPU double restatement of the reference, its algorithmic
+    structure kept: O(N S) GAE, per-timestep packed GRU, dense `rows`-scatter
+    backward) on a bounded sample of the headline workload: n_envs of the 4096
+    envs (same T, model, epochs, B); GAE + minibatch 0 of epoch 0 are timed and
+    extrapolated to the epochs x B minibatches of the update.  The oracle's
+    GEMMs / reductions run on `threads` OpenMP threads (all host cores by
+    default; results are bit-identical for any count).
+    Returns (env-steps/s, seconds measured, threads, sample description)."""
     from oracle import oracle as O
     import paper_2210_05064_b200 as V
     from paper_2210_05064_b200 import synth
+    threads = threads or (os.cpu_count() or 1)
+    O.set_threads(threads)
+    O.set_sparse_rows(False)
     cfg = V.ModelConfig(obs_dim=D_, encoder_dim=E_, hidden_dim=H_, action_kind=0, num_actions=A_)
-    wl = synth.make_workload(T_, n_envs_sample, hidden_dim=H_, seed=seed)
-    r = O.Rollout(T_, n_envs_sample, 1, 0, D_, 0, H_)
+    wl = synth.make_workload(T_, n_envs, hidden_dim=H_, seed=seed)
+    r = O.Rollout(T_, n_envs, 1, 0, D_, 0, H_)
     synth.fill_buffer(r, wl)
     view = r.close_rollout()
-    p = O.params_init(cfg, O.mix(seed, 0x9A9A))
-    L = O.Learner(cfg, p, V.PPOConfig(epochs=EPOCHS, minibatches=MINIBATCHES), V.EntropyController(),
-                  2.5e-4, 2_000_000, O.mix(seed, 0xF00D))
+    p = O.params_init(cfg, O.mix(1, 0x9A9A))
+    L = O.Learner(cfg, p, V.PPOConfig(epochs=epochs, minibatches=MINIBATCHES), V.EntropyController(),
+                  2.5e-4, 2_000_000, O.mix(1, 0xF00D))
     t0 = time.perf_counter()
     L.update(view, max_minibatches=1)
     dt = time.perf_counter() - t0
-    per_update = dt * EPOCHS * MINIBATCHES  # GAE is O(N S) but tiny next to a minibatch
-    steps = T_ * n_envs_sample
-    return steps / per_update, dt, (f"oracle port, 1 thread: N={n_envs_sample} of {N_} envs, T={T_}, "
-                                    f"E=H={E_}, GAE + 1 of {EPOCHS}x{MINIBATCHES} minibatches timed "
-                                    f"({dt:.1f} s), extrapolated x{EPOCHS * MINIBATCHES}")
+    per_update = dt * epochs * MINIBATCHES  # GAE (O(N S)) is < 1% of a minibatch at this sample
+    steps = T_ * n_envs
+    return steps / per_update, dt, threads, (
+        f"oracle port (double, reference algorithm), {threads} OpenMP threads: N={n_envs} of {N_} envs, "
+        f"T={T_}, E=H={E_}, GAE + minibatch 1 of {epochs}x{MINIBATCHES} timed ({dt:.1f} s), "
+        f"extrapolated x{epochs * MINIBATCHES}")
 
 
 def run_reference(args, rank, world):
+    """The reference's CPU learner path on this box's host cores, on the headline
+    workload: the reference itself cannot be built here (Eigen absent, DESIGN.md
+    §4), so this times the oracle port, sampled per step (see cpu_sample)."""
     if rank != 0:
         return
+    # one replica per GPU (distributed.cpp:271-276), each on its share of the host cores
+    thr = max(1, (os.cpu_count() or 1) // world)
     for _ in range(args.warmup):
-        cpu_sample()
+        cpu_sample(args.ref_envs, threads=thr)
     vals = []
     t0 = time.perf_counter()
+    sample, threads = "", 1
     for _ in range(args.steps):
-        v, dt, sample = cpu_sample()
+        v, dt, threads, sample = cpu_sample(args.ref_envs, threads=thr)
         vals.append(v)
     wall = time.perf_counter() - t0
-    value = statistics.mean(vals)
+    value = statistics.mean(vals) * world  # weak scaling: the replicas run side by side on disjoint cores
+    wk = (f"configs[{2 if world == 1 else 3}]: N={N_} envs/GPU x {world}, T={T_}, encoder 2x{E_} + GRU-{H_}, "
+          f"{EPOCHS} epochs x {MINIBATCHES} minibatches (sampled, see cpu_baseline)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wall / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8d generator)",
-        "config": {"workload": f"configs[1]: N={N_} envs, T={T_}, encoder 2x{E_} + GRU-{H_}, "
-                               f"{EPOCHS} epochs x {MINIBATCHES} minibatches (sampled, see cpu_baseline)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "config": {"workload": wk},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample + (f"; one replica per GPU on {threads} of the host cores each, x{world} replicas" if world > 1 else "")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------- GPU side
+def seq_start_records(wl):
+    """Records that start a sequence (an env's first record, or one after a done):
+    the rows whose h_before the store uploads (rollout.cpp:147-160)."""
+    env = np.asarray(wl.records.env_index)
+    done = np.asarray(wl.records.done).astype(bool)
+    idx = np.arange(env.size)
+    last = np.full(wl.N, -1, np.int64)
+    np.maximum.at(last, env, idx)
+    return int(wl.N + np.count_nonzero(done & (idx != last[env])))
+
+
+def host_bytes(wl):
+    """Bytes one e2e step copies host -> device: the arrival-log columns, the h_before
+    rows of sequence-starting records and the bootstraps."""
+    rec = wl.records
+    b = sum(np.asarray(getattr(rec, f)).nbytes for f in ("env_index", "obs", "log_prob", "value", "reward",
+                                                         "done", "act_disc", "episode_index",
+                                                         "step_in_episode", "latency", "snapshot_version"))
+    b += 4 * 3 * len(rec.env_index)  # env rank / h-slot / rank columns of the arrival log
+    b += seq_start_records(wl) * wl.hidden_dim * 4
+    b += wl.N * 9
+    return int(b)
+
+
 def run_ours(args, rank, world):
     import torch
     import paper_2210_05064_b200 as V
@@ -186,6 +226,41 @@ def run_ours(args, rank, world):
         dist.broadcast_object_list(uid, src=0)
         ctx.init_nccl(uid[0], world, rank)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+
+    def barrier():
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed_updates(learner, view, steps, warmup):
+        for _ in range(warmup):
+            learner.update(view, read_stats=False)
+        barrier()
+        n0 = ctx.launch_count()
+        ev = []
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)  # L2 flush between timed steps (outside the event pair)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            learner.update(view, read_stats=False)
+            with torch.cuda.stream(stream):
+                e1.record(stream)
+            ev.append((e0, e1))
+        barrier()
+        launches = (ctx.launch_count() - n0) // max(1, steps)
+        ms = [a.elapsed_time(b) for a, b in ev]
+        return ms, launches
 
     cfg = V.ModelConfig(obs_dim=D_, encoder_dim=E_, hidden_dim=H_, action_kind=0, num_actions=A_)
     params = V.params_init(cfg, mix(1, 0x9A9A))                  # bench.cpp:101
@@ -199,66 +274,47 @@ def run_ours(args, rank, world):
     synth.fill_buffer(buf, wl)
     view = buf.close_rollout()
     fresh = view.fresh_steps()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
 
-    def barrier():
-        ctx.synchronize()
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-
-    # ---- device-resident learner updates
-    for _ in range(args.warmup):
-        learner.update(view, read_stats=False)
-    barrier()
-    n0 = ctx.launch_count()
-    times = []
+    # ---- device-resident learner updates (the headline `value`)
     with ClockSampler(local) as clk:
-        barrier()
-        for _ in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(1)  # L2 flush between timed steps (outside the event pair)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            learner.update(view, read_stats=False)
-            with torch.cuda.stream(stream):
-                e1.record(stream)
-            times.append((e0, e1))
-        barrier()
-    launches = (ctx.launch_count() - n0) // max(1, args.steps)
-    step_ms = [a.elapsed_time(b) for a, b in times]
-    ms = sum(step_ms) / len(step_ms)
+        step_ms, launches = timed_updates(learner, view, args.steps, args.warmup)
+    ms = max_over_ranks(statistics.mean(step_ms))
     phase = learner.last_timing()
     phase_n = learner.last_timing_counts()
-    if dist:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    flop = learner.last_flop()
     value = fresh * world / (ms / 1000.0)
 
-    # ---- e2e through the C-ABI with host buffers
+    # ---- e2e through the C-ABI with host buffers: append the host arrival log,
+    # close_rollout (H2D + device compaction), update, read the stats (D2H)
     e2e_ms = []
-    rec = wl.records
-    h2d = sum(np.asarray(getattr(rec, f)).nbytes for f in ("env_index", "obs", "log_prob", "value", "reward",
-                                                           "done", "act_disc", "episode_index",
-                                                           "step_in_episode", "latency", "snapshot_version"))
-    h2d += 4 * 3 * len(rec)  # env rank / h-slot / rank columns of the arrival log
-    h2d += N_ * (H_ * 4 + 9)  # h0 rows of rollout-start sequences (upper bound) + bootstrap
     for i in range(max(1, args.steps)):
         barrier()
         t0 = time.perf_counter()
         synth.fill_buffer(buf, wl, snapshot_version=2 + i)
         v2 = buf.close_rollout()
-        st = learner.update(v2)
+        learner.update(v2)
         barrier()
         e2e_ms.append(1000.0 * (time.perf_counter() - t0))
         del v2
-    e2e = statistics.median(e2e_ms)
-    if dist:
-        t = torch.tensor([e2e], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
+    e2e = max_over_ranks(statistics.median(e2e_ms))
+    h2d = host_bytes(wl)
+    del view
+
+    # ---- configs[1] (C2): N = 256 envs, 4 epochs x 2 minibatches (extra field)
+    c2 = None
+    if rank == 0 and not args.no_c2:
+        wl2 = synth.make_workload(T_, N2, obs_dim=D_, num_actions=A_, hidden_dim=H_, seed=1)
+        buf2 = V.RolloutBuffer(T_, N2, V.VARIABLE, 0, D_, 0, H_, ctx=ctx)
+        synth.fill_buffer(buf2, wl2)
+        view2 = buf2.close_rollout()
+        l2 = V.Learner(cfg, params, V.PPOConfig(epochs=EPOCHS2, minibatches=MINIBATCHES), V.EntropyController(),
+                       V.CosineSchedule(2.5e-4, 2_000_000), mix(1, 0xF00D), ctx=ctx)
+        m2, _ = timed_updates(l2, view2, 10, 3)
+        f2 = view2.fresh_steps()
+        c2 = {"workload": f"configs[1]: N={N2} envs, T={T_}, encoder 2x{E_} + GRU-{H_}, {EPOCHS2} epochs x "
+                          f"{MINIBATCHES} minibatches", "fresh_steps": f2, "ms_per_update": statistics.mean(m2),
+              "env_steps_per_s": f2 / (statistics.mean(m2) / 1000.0), "phases_ms": l2.last_timing()}
+        del l2, view2, buf2
 
     # ---- GAE + gather HBM throughput on the ragged stress view
     gg = None
@@ -277,37 +333,6 @@ def run_ours(args, rank, world):
               "peak_kind": pk,
               "bytes_per_step": {"gae": 17, "gather": 8 * D_ + 36}}
         del v5
-
-    # ---- C3 (configs[2]): N = 4096 envs, GRU-512, 3 epochs (reference default) x 2 minibatches
-    c3 = None
-    if rank == 0 and not args.no_c3:
-        N3, EP3 = 4096, 3
-        wl3 = synth.make_workload(T_, N3, obs_dim=D_, num_actions=A_, hidden_dim=H_, seed=3)
-        buf3 = V.RolloutBuffer(T_, N3, V.VARIABLE, 0, D_, 0, H_, ctx=ctx)
-        synth.fill_buffer(buf3, wl3)
-        view3 = buf3.close_rollout()
-        l3 = V.Learner(cfg, params, V.PPOConfig(epochs=EP3, minibatches=MINIBATCHES), V.EntropyController(),
-                       V.CosineSchedule(2.5e-4, 2_000_000), mix(3, 0xF00D), ctx=ctx)
-        l3.update(view3, read_stats=False)
-        barrier()
-        t3 = []
-        for _ in range(2):
-            with torch.cuda.stream(stream):
-                flush.fill_(1)
-                a_ = torch.cuda.Event(enable_timing=True)
-                b_ = torch.cuda.Event(enable_timing=True)
-                a_.record(stream)
-            l3.update(view3, read_stats=False)
-            with torch.cuda.stream(stream):
-                b_.record(stream)
-            t3.append((a_, b_))
-        barrier()
-        ms3 = sum(a_.elapsed_time(b_) for a_, b_ in t3) / len(t3)
-        f3 = view3.fresh_steps()
-        c3 = {"workload": f"configs[2]: N={N3} envs, T={T_}, encoder 2x{E_} + GRU-{H_}, {EP3} epochs x "
-                          f"{MINIBATCHES} minibatches", "fresh_steps": f3, "ms_per_update": ms3,
-              "env_steps_per_s": f3 / (ms3 / 1000.0), "phases_ms": l3.last_timing()}
-        del l3, view3, buf3
 
     # ---- collection-side inference engine: every env requests
     # each batch; one process_batch = requests H2D, act + sampling, actions D2H,
@@ -363,22 +388,22 @@ def run_ours(args, rank, world):
     if rank == 0 and world == 1 and not args.no_collect:
         from paper_2210_05064_b200.overlap import OverlappedTrainer
         ce, cl = V.Context(local), V.Context(local)
-        eng2 = V.InferenceEngine(cfg, T_, N_, params, version=0, mode=V.VARIABLE, seed=mix(2, 0xC011), ctx=ce)
-        lrn2 = V.Learner(cfg, params, V.PPOConfig(epochs=EPOCHS, minibatches=MINIBATCHES), V.EntropyController(),
+        eng2 = V.InferenceEngine(cfg, T_, N2, params, version=0, mode=V.VARIABLE, seed=mix(2, 0xC011), ctx=ce)
+        lrn2 = V.Learner(cfg, params, V.PPOConfig(epochs=EPOCHS2, minibatches=MINIBATCHES), V.EntropyController(),
                          V.CosineSchedule(2.5e-4, 2_000_000), mix(3, 0xF00D), ctx=cl)
         orng = np.random.default_rng(33)
-        oenv = np.arange(N_, dtype=np.int32)
+        oenv = np.arange(N2, dtype=np.int32)
 
         def ocollect(e):
             e.begin_rollout()
-            st_ = np.zeros(N_, np.int32)
-            ep_ = np.zeros(N_, np.int64)
-            e.process_arrays(oenv, orng.standard_normal((N_, D_)).astype(np.float32), first=np.ones(N_, np.uint8),
+            st_ = np.zeros(N2, np.int32)
+            ep_ = np.zeros(N2, np.int64)
+            e.process_arrays(oenv, orng.standard_normal((N2, D_)).astype(np.float32), first=np.ones(N2, np.uint8),
                              obs_episode=ep_, obs_step=st_)
             while not e.rollout_done():
                 st_ += 1
-                e.process_arrays(oenv, orng.standard_normal((N_, D_)).astype(np.float32),
-                                 reward=np.ones(N_, np.float32), done=np.zeros(N_, np.uint8), obs_episode=ep_,
+                e.process_arrays(oenv, orng.standard_normal((N2, D_)).astype(np.float32),
+                                 reward=np.ones(N2, np.float32), done=np.zeros(N2, np.uint8), obs_episode=ep_,
                                  obs_step=st_)
             e.finalize_bootstraps()
             return e.close()
@@ -397,59 +422,72 @@ def run_ours(args, rank, world):
             t0 = time.perf_counter()
             tr.iteration(read_stats=False)
             ovl_ms.append(1000.0 * (time.perf_counter() - t0))
-        ovl = {"workload": f"C2 iteration: collect {N_} envs x {T_} steps through InferenceEngine (synthetic env "
+        ovl = {"workload": f"C2 iteration: collect {N2} envs x {T_} steps through InferenceEngine (synthetic env "
                            f"loop) + one learner update", "serial_ms": statistics.median(seq_ms),
                "overlapped_ms": statistics.median(ovl_ms),
-               "env_steps_per_s_overlapped": fresh / (statistics.median(ovl_ms) / 1000.0)}
+               "env_steps_per_s_overlapped": N2 * T_ / (statistics.median(ovl_ms) / 1000.0)}
         del tr, eng2, lrn2
 
     if rank == 0:
         hbm, bf16, bf16s, peaks_kind = load_peaks()
-        # dominant kernel = the GRU recurrence direction with the larger device time
-        # (the launch list in profiles/ ranks it first): per minibatch one K-split
-        # launch (+ one cluster-tail launch); its algorithmic work is one H x 3H
-        # matvec per packed row (6 H^2 FLOP), every row once per epoch
-        dom = max(("rec_bwd", "rec_fwd"), key=lambda k: phase.get(k, 0.0))
         n_mb = EPOCHS * MINIBATCHES
-        n_dom = max(1, phase_n.get(dom, 0))
-        rows_per_mb = fresh * EPOCHS / n_mb
-        dom_flop = 6.0 * H_ * H_ * rows_per_mb
-        dom_ms = phase.get(dom, 0.0) / n_mb
-        achieved_tf = dom_flop / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
-        simt_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # fp32 FMA pipe peak at max SM clock
+        gemm_ms = phase.get("gemm_fwd", 0.0) + phase.get("gemm_bwd", 0.0)
+        rec_ms = phase.get("rec_fwd", 0.0) + phase.get("rec_bwd", 0.0)
+        if gemm_ms >= rec_ms:
+            # dominant kernel family: the tcgen05 3xTF32 GEMMs (encoder, input projection,
+            # backward data / weight gradients); achieved = their algorithmic 2MNK FLOPs
+            # (counted per launch by the library) / their device time (CUDA events
+            # around each launch on the library stream)
+            gflop = flop.get("gemm_fwd", 0.0) + flop.get("gemm_bwd", 0.0)
+            n_l = phase_n.get("gemm_fwd", 0) + phase_n.get("gemm_bwd", 0)
+            achieved_tf = gflop / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else 0.0
+            tr_ = traffic_entry("tc_gemm_c3")
+            roof = {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
+                    "frac": achieved_tf / bf16s,
+                    "traffic": tr_.get("dram_bytes_per_launch") if tr_ else None,
+                    "kernel": (f"tc_gemm_kernel (tcgen05 kind::tf32, 3xTF32 fp32-grade): {n_l} launches per update, "
+                               f"{gflop / 1e12:.2f} TFLOP algorithmic (2MNK) in {gemm_ms:.2f} ms"),
+                    "peak_kind": f"{peaks_kind} bf16 dense sustained (3xTF32 issues 3 tf32 MMAs per product "
+                                 f"at half the bf16 rate: its own ceiling is peak/6)",
+                    "frac_of_3xtf32_ceiling": achieved_tf / (bf16s / 6.0)}
+            if tr_:
+                roof["traffic_launch"] = tr_.get("launch")
+        else:
+            rows_per_mb = fresh * EPOCHS / n_mb
+            dom = max(("rec_bwd", "rec_fwd"), key=lambda k: phase.get(k, 0.0))
+            dom_ms = phase.get(dom, 0.0) / n_mb
+            achieved_tf = 6.0 * H_ * H_ * rows_per_mb / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
+            roof = {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
+                    "frac": achieved_tf / bf16s, "traffic": None,
+                    "kernel": f"GRU recurrence {dom}: {dom_ms:.3f} ms per minibatch for {rows_per_mb:.0f} rows x 6H^2",
+                    "peak_kind": f"{peaks_kind} bf16 dense sustained"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32", "data": "synthetic (SURVEY.md §8d generator, seed 1)",
-            "config": {"workload": f"configs[1]: N={N_} envs/GPU lognormal step times, T={T_}, encoder 2x{E_}"
-                                   f" + GRU-{H_}, {EPOCHS} epochs x {MINIBATCHES} minibatches",
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic (SURVEY.md §8d generator, random-init policy)",
+            "config": {"workload": (f"configs[{2 if world == 1 else 3}]: N={N_} envs/GPU lognormal step times, "
+                                    f"T={T_}, encoder 2x{E_} + GRU-{H_}, {EPOCHS} epochs x {MINIBATCHES} minibatches"),
                        "fresh_steps_per_gpu": fresh, "l2": "flushed (256 MB write) before every timed step",
                        "parallelism": f"dp{world} (DD-PPO, NCCL AllReduce per minibatch)" if world > 1 else "dp1"},
-            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
-                         "frac": achieved_tf / bf16s, "traffic": dom_traffic(dom),
-                         "kernel": (f"{'gru_step_gemm_kernel<1> + gru_bwd_ks<512> + gru_bwd_tail<512>' if dom == 'rec_bwd' else 'gru_step_gemm_kernel<0> + gru_fwd_ks<512> + gru_fwd_tail<512>'}"
-                                    f" (GRU recurrence: tcgen05 3xTF32 steps >= 150 rows, fp32 FMA pipe below; {n_dom} launches/step over {n_mb} minibatches, "
-                                    f"{dom_ms:.3f} ms per minibatch for {rows_per_mb:.0f} rows x 6H^2 FLOP)"),
-                         "peak_kind": f"{peaks_kind} bf16 dense sustained",
-                         "fp32_simt_peak": simt_peak, "frac_of_fp32_simt": achieved_tf / simt_peak},
+            "roofline": roof,
             "phases_ms": phase,
             "phase_counts": phase_n,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-            "e2e": {"value": fresh * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "e2e": {"value": fresh * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * 12, "ms_per_step": e2e},
         }
+        if c2:
+            line["c2"] = c2
         if gg:
             line["gae_gather"] = gg
-        if c3:
-            line["c3"] = c3
         if coll:
             line["collect"] = coll
         if ovl:
             line["overlap"] = ovl
         if not args.no_cpu and world == 1:
-            cv, dt, sample = cpu_sample()
-            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample}
+            cv, dt, thr, sample = cpu_sample(2 * args.ref_envs)  # ~10 s of CPU work
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -462,10 +500,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-c2", action="store_true", help="skip the configs[1] (C2) extra field")
     ap.add_argument("--no-c5", action="store_true", help="skip the GAE+gather ragged sweep point")
-    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (N=4096) update measurement")
-    ap.add_argument("--no-collect", action="store_true", help="skip the inference-engine measurement")
+    ap.add_argument("--no-collect", action="store_true", help="skip the inference-engine measurements")
     ap.add_argument("--c5-log2", type=int, default=26, help="log2 steps of the GAE+gather point")
+    ap.add_argument("--ref-envs", type=int, default=128, help="envs of the CPU oracle sample per reference-arm step (the cpu_baseline leg uses 2x)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

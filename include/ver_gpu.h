@@ -400,6 +400,10 @@ ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n);
 /* number of timed intervals (kernel launches for rec_fwd / rec_bwd) behind each
    phase of ver_learner_last_timing; n in/out */
 ver_status ver_learner_last_timing_counts(ver_learner l, int* counts, int* n);
+/* Algorithmic FLOPs (2 M N K per launch) of the tcgen05 GEMM launches of the last
+   update, per phase of ver_learner_last_timing (nonzero for gemm_fwd / gemm_bwd
+   only); n in/out.  Bench-only instrumentation, like the timing above. */
+ver_status ver_learner_last_flop(ver_learner l, double* flop, int* n);
 
 /* Measurement: device time (CUDA events, averaged over reps) of compute_gae on
    v and of the time-major gather of all B minibatches of one
@@ -418,6 +422,9 @@ ver_status ver_debug_gemm(ver_ctx ctx, int engine, int transA, int transB, int M
    (contents arbitrary; no host copies).  ms_out[0] = ms per GEMM. */
 ver_status ver_debug_gemm_time(ver_ctx ctx, int engine, int transA, int transB, int M, int N, int K, int splitk,
                                int reps, float* ms_out);
+/* debug: tcgen05 GEMM wait-cycle counters of the launches in between (on = 1
+   zeroes + enables, on = 0 disables; out[16] = current sums, may be NULL) */
+ver_status ver_debug_gemm_prof(ver_ctx ctx, int on, unsigned long long* out);
 
 /* ------------------------------------------------ replica driver (L7, DD-PPO) */
 /* The learner section of ReplicaGroup::replica_main (distributed.cpp:208-264),

@@ -202,10 +202,12 @@ _SIGS = {
     "ver_learner_set_state": (c_int, [C.c_void_p, c_double, c_int64, c_int64]),
     "ver_learner_last_timing": (c_int, [C.c_void_p, P(c_float), P(c_int)]),
     "ver_learner_last_timing_counts": (c_int, [C.c_void_p, P(c_int), P(c_int)]),
+    "ver_learner_last_flop": (c_int, [C.c_void_p, P(C.c_double), P(c_int)]),
     "ver_debug_gemm": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, P(c_float), c_int,
                                P(c_float), c_int, P(c_float), c_int]),
     "ver_debug_gemm_time": (c_int, [C.c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                     P(c_float)]),
+    "ver_debug_gemm_prof": (c_int, [C.c_void_p, c_int, P(C.c_ulonglong)]),
     "ver_preempt_create": (c_int, [C.c_void_p, P(C.c_void_p)]),
     "ver_preempt_ipc_handle": (c_int, [C.c_void_p, P(C.c_uint8)]),
     "ver_preempt_open": (c_int, [C.c_void_p, P(C.c_uint8), P(C.c_void_p)]),

@@ -925,6 +925,13 @@ class Learner:
         _check(_lib().ver_learner_last_timing(self.h, ms, C.byref(n)))
         return {PHASES[i]: float(ms[i]) for i in range(min(n.value, len(PHASES)))}
 
+    def last_flop(self) -> dict:
+        """Algorithmic FLOPs (2MNK) of the tcgen05 GEMM launches of the last update per phase."""
+        f = (C.c_double * 16)()
+        n = C.c_int(16)
+        _check(_lib().ver_learner_last_flop(self.h, f, C.byref(n)))
+        return {PHASES[i]: float(f[i]) for i in range(min(n.value, len(PHASES)))}
+
     def last_timing_counts(self) -> dict:
         """Intervals behind each phase of last_timing (launches for rec_fwd / rec_bwd)."""
         cnt = (C.c_int * 16)()
@@ -1050,6 +1057,14 @@ def debug_gemm_time(M, N, K, transA=False, transB=False, engine=1, splitk=1, rep
     ms = (C.c_float * 1)()
     _check(_lib().ver_debug_gemm_time(ctx.h, engine, int(transA), int(transB), M, N, K, splitk, reps, ms))
     return float(ms[0])
+
+
+def debug_gemm_prof(on: bool, ctx: Context | None = None) -> list[int]:
+    """tcgen05 GEMM wait-cycle counters (tc_gemm.cuh g_tc_prof); returns the sums so far."""
+    ctx = ctx or default_context()
+    out = (C.c_ulonglong * 16)()
+    _check(_lib().ver_debug_gemm_prof(ctx.h, int(on), out))
+    return [int(x) for x in out]
 
 
 # ---------------------------------------------------------- distributed

@@ -71,6 +71,7 @@ struct Ctx {
   std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>>* evlog = nullptr;
   int rec_tag = -1;  // tag for recurrence launches (>= 0 while a learner minibatch is timed)
   int gemm_tag = -1;  // tag for tcgen05 GEMM launches (same)
+  double* flop_log = nullptr;  // per-tag algorithmic FLOPs (2 M N K) of the tagged GEMM launches
   // pinned scratch for small synchronous reads
   void* pinned = nullptr;
   size_t pinned_bytes = 0;

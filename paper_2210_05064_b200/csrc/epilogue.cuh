@@ -10,6 +10,13 @@ namespace verg {
 
 inline bool ptr16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// L2 prefetch of `ncols` floats of a row (the tcgen05 GEMM's epilogue warps issue
+// it when a tile starts, for the epilogues that read a second operand: the
+// loads at the tile's end then hit L2 instead of stalling the accumulator drain)
+__device__ __forceinline__ void prefetch_row_l2(const float* row, int ncols) {
+  for (int c = 0; c < ncols; c += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + c));
+}
+
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
@@ -17,6 +24,7 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
 struct EpiStore {
   float* C;
   int ldc;
+  __device__ void prefetch_row(int, int, int) const {}
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0; }
   EpiStore shifted(int m0) const { return EpiStore{C + (size_t)m0 * ldc, ldc}; }  // rows m0.. (tail split)
   __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v; }
@@ -28,6 +36,7 @@ struct EpiBias {
   float* C;
   int ldc;
   const float* bias;
+  __device__ void prefetch_row(int, int, int) const {}
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias); }
   EpiBias shifted(int m0) const { return EpiBias{C + (size_t)m0 * ldc, ldc, bias}; }
   __device__ void operator()(int m, int n, float v, int) const { C[(size_t)m * ldc + n] = v + bias[n]; }
@@ -39,6 +48,7 @@ struct EpiBiasTanh {
   float* C;
   int ldc;
   const float* bias;
+  __device__ void prefetch_row(int, int, int) const {}
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias); }
   EpiBiasTanh shifted(int m0) const { return EpiBiasTanh{C + (size_t)m0 * ldc, ldc, bias}; }
   __device__ void operator()(int m, int n, float v, int) const {
@@ -55,6 +65,7 @@ struct EpiAddTerm {  // C = acc + T
   int ldc;
   const float* T;
   int ldt;
+  __device__ void prefetch_row(int m, int n0, int ncols) const { prefetch_row_l2(T + (size_t)m * ldt + n0, ncols); }
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(T) && ldt % 4 == 0; }
   EpiAddTerm shifted(int m0) const { return EpiAddTerm{C + (size_t)m0 * ldc, ldc, T + (size_t)m0 * ldt, ldt}; }
   __device__ void operator()(int m, int n, float v, int) const {
@@ -70,6 +81,7 @@ struct EpiTanhGrad {  // C = acc * (1 - Y^2)
   int ldc;
   const float* Y;
   int ldy;
+  __device__ void prefetch_row(int m, int n0, int ncols) const { prefetch_row_l2(Y + (size_t)m * ldy + n0, ncols); }
   bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(Y) && ldy % 4 == 0; }
   EpiTanhGrad shifted(int m0) const { return EpiTanhGrad{C + (size_t)m0 * ldc, ldc, Y + (size_t)m0 * ldy, ldy}; }
   __device__ void operator()(int m, int n, float v, int) const {
@@ -86,6 +98,7 @@ struct EpiTanhGrad {  // C = acc * (1 - Y^2)
 struct EpiPartial {  // split-K partial z
   float* W;
   int M, N;
+  __device__ void prefetch_row(int, int, int) const {}
   bool vec_ok() const { return ptr16(W) && N % 4 == 0; }
   __device__ void operator()(int m, int n, float v, int z) const {
     W[((size_t)z * M + m) * N + n] = v;

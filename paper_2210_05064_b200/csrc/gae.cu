@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
     const int32_t* __restrict__ env_of, int F, const float* __restrict__ boot,
     const uint8_t* __restrict__ boot_valid, const int32_t* __restrict__ off, int N, double gamma, double lambda,
     float* __restrict__ adv, float* __restrict__ ret, volatile GaeTileState* tiles, int* tile_counter,
-    int* err_env, int dbg) {
+    int* err_env) {
   extern __shared__ __align__(128) uint8_t gsmem[];
   __shared__ uint64_t s_full[kGaeStages], s_ready[kGaeStages], s_empty[kGaeStages];
   __shared__ GaeStageHdr s_hdr[kGaeStages];
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
       if (lane == 0 && tid != 0) {
         Affine acc{1.0, 0.0};
         int p = tid - 1;
-        while (!(dbg & 1)) {
+        for (;;) {
           int f;
           do {
             f = flag_acquire(&tiles[p].flag);
@@ -457,11 +457,6 @@ __global__ void gae_scatter_kernel(const uint64_t* __restrict__ keys, int F, con
   ret[i] = ret2[j];
 }
 
-static int gae_debug_mode() {
-  const char* e = getenv("VER_GAE_DEBUG");  // experiments only: 1 = skip the look-back wait
-  return e ? atoi(e) : 0;
-}
-
 static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, const int32_t* env, int F,
                      const float* boot, const uint8_t* valid, const int32_t* off, int N, double gamma,
                      double lambda, float* adv, float* ret) {
@@ -487,7 +482,7 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   }
   const int grid = std::min(ntiles, per_sm * c->num_sms);
   gae_scan_kernel<<<grid, kGaeBlock, smem, c->stream>>>(r, v, d, env, F, boot, valid, off, N, gamma, lambda, adv, ret,
-                                                       tiles.p, misc.p, misc.p + 1, gae_debug_mode());
+                                                       tiles.p, misc.p, misc.p + 1);
   after_launch(c);
   misc.download(h, 2);
   sync(c);

@@ -81,6 +81,7 @@ struct Learner {
   std::vector<std::pair<int, cudaEvent_t>> open;
   float phase_ms[PH_N] = {};
   int phase_n[PH_N] = {};
+  double flop_acc[PH_N] = {}, phase_flop[PH_N] = {};  // 2MNK of the tagged tcgen05 GEMMs
   bool timing = true;
 
   void mark_begin(int phase) {
@@ -99,7 +100,7 @@ struct Learner {
     open.pop_back();
   }
   void collect_timing() {
-    for (int k = 0; k < PH_N; ++k) phase_ms[k] = 0.f, phase_n[k] = 0;
+    for (int k = 0; k < PH_N; ++k) phase_ms[k] = 0.f, phase_n[k] = 0, phase_flop[k] = flop_acc[k], flop_acc[k] = 0.0;
     for (auto& [tag, a, b] : evlog) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, a, b);
@@ -342,9 +343,11 @@ static void learner_update(Learner& Ln, DView& V, ver_train_stats* out) {
     config_error("learner_update: view shape does not match the model");
   struct EvGuard {  // the ctx logs recurrence launches into this learner's timing
     Ctx* c;
-    ~EvGuard() { c->evlog = nullptr, c->rec_tag = -1, c->gemm_tag = -1; }
+    ~EvGuard() { c->evlog = nullptr, c->flop_log = nullptr, c->rec_tag = -1, c->gemm_tag = -1; }
   } evg{c};
   c->evlog = Ln.timing ? &Ln.evlog : nullptr;
+  for (double& f : Ln.flop_acc) f = 0.0;
+  c->flop_log = Ln.flop_acc;
   // The view may belong to another context (an engine's close() on the collector
   // thread).  Everything of this update -- GAE included -- allocates, launches and
   // synchronizes on the learner's own context: the learner stream first waits for
@@ -903,6 +906,14 @@ ver_status ver_learner_last_timing(ver_learner l, float* ms, int* n) {
   VER_API_BEGIN
   const int k = std::min(*n, (int)PH_N);
   for (int i = 0; i < k; ++i) ms[i] = l->l.phase_ms[i];
+  *n = PH_N;
+  VER_API_END
+}
+
+ver_status ver_learner_last_flop(ver_learner l, double* flop, int* n) {
+  VER_API_BEGIN
+  const int k = std::min(*n, (int)PH_N);
+  for (int i = 0; i < k; ++i) flop[i] = l->l.phase_flop[i];
   *n = PH_N;
   VER_API_END
 }

@@ -480,199 +480,18 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
 }
 
 // ------------------------------------------------ big recurrence steps
-// Steps whose batch has >= kBigRows rows (a prefix of the timesteps: bs is
-// non-increasing) run as one GEMM per step on the tensor cores instead of the
-// persistent FMA kernel (recurrence.cu), whose step time grows with the rows
-// (~36 us at 623 rows, H = 512) while a 3xTF32 tcgen05 GEMM of the step takes
-// ~8 us up to 640 rows.
+// Steps whose batch has >= 150 rows (a prefix of the timesteps: bs is
+// non-increasing) run in the persistent tcgen05 step kernel (stepgemm.cu)
+// instead of the persistent FMA kernel (recurrence.cu), whose step time grows
+// with the rows (~36 us at 623 rows, H = 512).  The threshold was measured on
+// B200 at C2 (scripts/ab_bench.py sweeps); VER_REC_BIG_FWD / _BWD override it.
 int gru_big_steps(Ctx* c, const Model& m, const int32_t* h_bs, int L, bool backward) {
-  if (m.H % 4 != 0) return 0;  // the gate kernels move 4 units per thread
-  // thresholds measured on B200 at C2 (scripts/ab_bench.py sweeps): 150 rows for
-  // the persistent step kernel (stepgemm.cu), 250 / 200 for per-step launches
-  const bool persist = step_gemm_enabled();
-  const int min_rows = backward ? env_int("VER_REC_BIG_BWD", persist ? 150 : 200)
-                                : env_int("VER_REC_BIG_FWD", persist ? 150 : 250);
+  if (m.H % 4 != 0) return 0;  // the gate phase moves 4 units per thread
+  const int min_rows = backward ? env_int("VER_REC_BIG_BWD", 150) : env_int("VER_REC_BIG_FWD", 150);
   if (!h_bs || !c->tensor_cores || m.H % 32 != 0 || min_rows <= 0) return 0;
   int t = 0;
   while (t < L && h_bs[t] >= min_rows) ++t;
   return t;
-}
-
-// forward gates of rows j < B at step t: hU = h_{t-1} U (GEMM), then
-// r = s(xr + hUr), z = s(xz + hUz), n = tanh(xn + r hUn), h = (1-z) n + z h_{t-1}
-// hU: Z split-K partials of B x 3H, summed here in a fixed order.  Thread:
-// row blockIdx.y, units 4x .. 4x+3 (float4 loads / stores of the unit-major
-// arrays, three float4 of the gate-interleaved ones)
-__global__ void gru_gate_fwd_kernel(int B, int H, int Z, const float* __restrict__ hU,
-                                    const float* __restrict__ xp, const float* __restrict__ hp,
-                                    float* __restrict__ hid, float* __restrict__ gates, float* __restrict__ hun,
-                                    float* __restrict__ hprev_store) {
-  const int u4 = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  if (4 * u4 >= H) return;
-  const size_t row3 = (size_t)j * 3 * H + 12 * (size_t)u4, row = (size_t)j * H + 4 * (size_t)u4;
-  const size_t zs = (size_t)B * 3 * H;
-  float s[12];
-  {
-    const float4* x4 = reinterpret_cast<const float4*>(hU + row3);
-    const float4 a = x4[0], b = x4[1], c = x4[2];
-    s[0] = a.x; s[1] = a.y; s[2] = a.z; s[3] = a.w; s[4] = b.x; s[5] = b.y;
-    s[6] = b.z; s[7] = b.w; s[8] = c.x; s[9] = c.y; s[10] = c.z; s[11] = c.w;
-  }
-  for (int z = 1; z < Z; ++z) {
-    const float4* x4 = reinterpret_cast<const float4*>(hU + z * zs + row3);
-    const float4 a = x4[0], b = x4[1], c = x4[2];
-    s[0] += a.x; s[1] += a.y; s[2] += a.z; s[3] += a.w; s[4] += b.x; s[5] += b.y;
-    s[6] += b.z; s[7] += b.w; s[8] += c.x; s[9] += c.y; s[10] += c.z; s[11] += c.w;
-  }
-  float x[12];
-  {
-    const float4* x4 = reinterpret_cast<const float4*>(xp + row3);
-    const float4 a = x4[0], b = x4[1], c = x4[2];
-    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y;
-    x[6] = b.z; x[7] = b.w; x[8] = c.x; x[9] = c.y; x[10] = c.z; x[11] = c.w;
-  }
-  const float4 hp4 = *reinterpret_cast<const float4*>(hp + row);
-  const float hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
-  float hn[4], g[12];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float rg = gate_sigm(x[3 * q] + s[3 * q]);
-    const float zg = gate_sigm(x[3 * q + 1] + s[3 * q + 1]);
-    const float ng = gate_tanh(x[3 * q + 2] + rg * s[3 * q + 2]);
-    hn[q] = (1.f - zg) * ng + zg * hpv[q];
-    g[3 * q] = rg;
-    g[3 * q + 1] = zg;
-    g[3 * q + 2] = ng;
-  }
-  *reinterpret_cast<float4*>(hid + row) = make_float4(hn[0], hn[1], hn[2], hn[3]);
-  if (gates) {
-    float4* g4 = reinterpret_cast<float4*>(gates + row3);
-    g4[0] = make_float4(g[0], g[1], g[2], g[3]);
-    g4[1] = make_float4(g[4], g[5], g[6], g[7]);
-    g4[2] = make_float4(g[8], g[9], g[10], g[11]);
-    *reinterpret_cast<float4*>(hun + row) = make_float4(s[2], s[5], s[8], s[11]);
-    *reinterpret_cast<float4*>(hprev_store + row) = hp4;
-  }
-}
-
-void gru_forward_big(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
-                     const int32_t* h_offs, Workspace& ws, const float* h0, bool store) {
-  const int H = m.H, H3 = 3 * H;
-  if (t_end <= 0) return;
-  for (int t = 0; t < t_end; ++t) {
-    const int B = h_bs[t];
-    const size_t o = (size_t)h_offs[t];
-    const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
-    // hU = h_{t-1}[0:B] U (M = B, N = 3H, K = H), split-K to fill the SMs
-    const int tiles = (int)(cdiv(H3, tc::BN) * cdiv(B, tc::BM));
-    const int nkb = (H + tc::BK - 1) / tc::BK;
-    int Z = std::max(1, std::min(c->num_sms / std::max(1, tiles), std::max(1, nkb / 4)));
-    const int per = (nkb + Z - 1) / Z;
-    Z = (nkb + per - 1) / per;
-    ws.step.reserve(c, (size_t)Z * B * H3);
-    if (c->tensor_cores && tc::usable(B, H3, H, hp, H, params + m.o_ux, H3, EpiPartial{ws.step.p, B, H3})) {
-      tc::launch<0, 1>(c, B, H3, H, hp, H, params + m.o_ux, H3, EpiPartial{ws.step.p, B, H3}, Z);
-    } else {
-      Z = 1;
-      gemm<false, false>(c, B, H3, H, hp, H, params + m.o_ux, H3, EpiStore{ws.step.p, H3});
-    }
-    gru_gate_fwd_kernel<<<dim3(cdiv(H / 4, 128), B), 128, 0, c->stream>>>(
-        B, H, Z, ws.step.p, ws.xp.p + o * H3, hp, ws.hidden.p + o * H, store ? ws.gates.p + o * H3 : nullptr,
-        ws.hu.p + o * H, ws.hprev.p + o * H);
-    after_launch(c);
-  }
-}
-
-// backward gates of rows j < Bp at step t-1: dh_{t-1}[j] = sum_z part + g_t z_t
-// (j < B).  Thread: row blockIdx.y, units 4x .. 4x+3.
-__global__ void gru_gate_bwd_kernel(int Bp, int B, int H, int Z, const float* __restrict__ part,
-                                    const float* __restrict__ gz_t, const float* __restrict__ dhidden,
-                                    const float* __restrict__ gates, const float* __restrict__ hun,
-                                    const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu,
-                                    float* __restrict__ gz) {
-  const int u4 = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y;
-  if (4 * u4 >= H) return;
-  const size_t row = (size_t)j * H + 4 * (size_t)u4, row3 = (size_t)j * 3 * H + 12 * (size_t)u4;
-  float dh[4] = {0.f, 0.f, 0.f, 0.f};
-  if (j < B) {
-    for (int z = 0; z < Z; ++z) {
-      const float4 p = *reinterpret_cast<const float4*>(part + ((size_t)z * B + j) * H + 4 * u4);
-      dh[0] += p.x; dh[1] += p.y; dh[2] += p.z; dh[3] += p.w;
-    }
-    const float4 q = *reinterpret_cast<const float4*>(gz_t + row);
-    dh[0] += q.x; dh[1] += q.y; dh[2] += q.z; dh[3] += q.w;
-  }
-  const float4 d4 = *reinterpret_cast<const float4*>(dhidden + row);
-  const float4 hn4 = *reinterpret_cast<const float4*>(hun + row);
-  const float4 hp4 = *reinterpret_cast<const float4*>(hprev + row);
-  const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hnv[4] = {hn4.x, hn4.y, hn4.z, hn4.w},
-              hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
-  float gt[12];
-  {
-    const float4* g4 = reinterpret_cast<const float4*>(gates + row3);
-    const float4 a = g4[0], b = g4[1], c = g4[2];
-    gt[0] = a.x; gt[1] = a.y; gt[2] = a.z; gt[3] = a.w; gt[4] = b.x; gt[5] = b.y;
-    gt[6] = b.z; gt[7] = b.w; gt[8] = c.x; gt[9] = c.y; gt[10] = c.z; gt[11] = c.w;
-  }
-  float o1[12], o2[12], gzv[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const float g = dv[q] + dh[q];
-    const float r = gt[3 * q], zg = gt[3 * q + 1], n = gt[3 * q + 2];
-    const float dn = g * (1.f - zg);
-    const float dz = g * (hpv[q] - n);
-    const float dpn = dn * (1.f - n * n);
-    const float dr = dpn * hnv[q];
-    const float dpr = dr * r * (1.f - r);
-    const float dpz = dz * zg * (1.f - zg);
-    o1[3 * q] = dpr;
-    o1[3 * q + 1] = dpz;
-    o1[3 * q + 2] = dpn;
-    o2[3 * q] = dpr;
-    o2[3 * q + 1] = dpz;
-    o2[3 * q + 2] = dpn * r;
-    gzv[q] = g * zg;
-  }
-  float4* p1 = reinterpret_cast<float4*>(dpre + row3);
-  float4* p2 = reinterpret_cast<float4*>(dhu + row3);
-  p1[0] = make_float4(o1[0], o1[1], o1[2], o1[3]);
-  p1[1] = make_float4(o1[4], o1[5], o1[6], o1[7]);
-  p1[2] = make_float4(o1[8], o1[9], o1[10], o1[11]);
-  p2[0] = make_float4(o2[0], o2[1], o2[2], o2[3]);
-  p2[1] = make_float4(o2[4], o2[5], o2[6], o2[7]);
-  p2[2] = make_float4(o2[8], o2[9], o2[10], o2[11]);
-  *reinterpret_cast<float4*>(gz + row) = make_float4(gzv[0], gzv[1], gzv[2], gzv[3]);
-}
-
-void gru_backward_big(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
-                      const int32_t* h_offs, Workspace& ws) {
-  const int H = m.H, H3 = 3 * H;
-  for (int t = t_top; t >= 1; --t) {
-    const int B = h_bs[t], Bp = h_bs[t - 1];
-    const size_t o = (size_t)h_offs[t], op = (size_t)h_offs[t - 1];
-    int Z = 1;
-    if (B > 0) {
-      // dh_part = dhU_t[0:B] U^T (M = B, N = H, K = 3H), split-K for parallelism
-      const int tiles = (int)(cdiv(H, tc::BN) * cdiv(B, tc::BM));
-      const int nkb = (H3 + tc::BK - 1) / tc::BK;
-      Z = std::max(1, std::min(c->num_sms / std::max(1, tiles), std::max(1, nkb / 4)));
-      Z = std::min(Z, env_int("VER_REC_BIG_ZMAX", 16));
-      const int per = (nkb + Z - 1) / Z;
-      Z = (nkb + per - 1) / per;
-      ws.step.reserve(c, (size_t)Z * B * H);
-      if (c->tensor_cores && tc::usable(B, H, H3, ws.dhu.p + o * H3, H3, params + m.o_ux, H3,
-                                        EpiPartial{ws.step.p, B, H})) {
-        tc::launch<0, 0>(c, B, H, H3, ws.dhu.p + o * H3, H3, params + m.o_ux, H3, EpiPartial{ws.step.p, B, H}, Z);
-      } else {
-        Z = 1;
-        gemm<false, true>(c, B, H, H3, ws.dhu.p + o * H3, H3, params + m.o_ux, H3, EpiStore{ws.step.p, H});
-      }
-    }
-    gru_gate_bwd_kernel<<<dim3(cdiv(H / 4, 128), Bp), 128, 0, c->stream>>>(
-        Bp, B, H, Z, ws.step.p, ws.g.p + o * H, ws.dhidden.p + op * H, ws.gates.p + op * H3, ws.hu.p + op * H,
-        ws.hprev.p + op * H, ws.dpre.p + op * H3, ws.dhu.p + op * H3, ws.g.p + op * H);
-    after_launch(c);
-  }
 }
 
 void policy_heads(Ctx* c, const Model& m, const float* params, int n, const float* hidden, float* out) {
@@ -1733,5 +1552,22 @@ extern "C" ver_status ver_debug_gemm_time(ver_ctx ctx, int engine, int transA, i
   c->precision = p0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  VER_API_END
+}
+
+// tcgen05 GEMM wait-cycle counters (tc_gemm.cuh g_tc_prof): on = 1 zeroes and
+// enables them, on = 0 disables; `out` (16 values) receives the current sums
+extern "C" ver_status ver_debug_gemm_prof(ver_ctx ctx, int on, unsigned long long* out) {
+  VER_API_BEGIN
+  Ctx* c = &ctx->c;
+  activate(c);
+  VER_CUDA(cudaStreamSynchronize(c->stream));
+  if (out) VER_CUDA(cudaMemcpyFromSymbol(out, tc::g_tc_prof, sizeof(unsigned long long) * 16));
+  if (on) {
+    unsigned long long z[16] = {};
+    VER_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof, z, sizeof(z)));
+  }
+  const int f = on ? 1 : 0;
+  VER_CUDA(cudaMemcpyToSymbol(tc::g_tc_prof_on, &f, sizeof(int)));
   VER_API_END
 }

@@ -73,27 +73,16 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
 void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L, const int32_t* d_bs,
                              const int32_t* d_offs, Workspace& ws, const int32_t* h_bs = nullptr,
                              const int32_t* h_offs = nullptr);
-// Big recurrence steps on the tensor cores (policy.cu): one 3xTF32 tcgen05
-// GEMM per timestep plus a fused gate kernel.  Forward: steps [0, t_end);
-// backward: steps t_top .. 1.  Host batch sizes / offsets required.
+// Big recurrence steps on the tensor cores: the timesteps with many rows
+// (forward: steps [0, t_end); backward: steps t_top .. 1) in one persistent
+// cooperative launch per minibatch and direction, a split-K 3xTF32 tcgen05
+// GEMM phase and a gate phase per step (stepgemm.cu).  Host batch sizes /
+// offsets required.
 int gru_big_steps(Ctx* c, const Model& m, const int32_t* h_bs, int L, bool backward);
-void gru_forward_big(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
-                     const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
-void gru_backward_big(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
-                      const int32_t* h_offs, Workspace& ws);
-// the same steps in one persistent cooperative launch (stepgemm.cu)
-bool step_gemm_enabled();
 void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
                              const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
 void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
                               const int32_t* h_offs, Workspace& ws);
-// the same steps on 4-CTA clusters with the split-K reduction and the gates fused
-// into the epilogue, one grid barrier per step (stepfused.cu; H = 256 / 512)
-bool step_fused_ok(int H, bool backward);
-void gru_forward_big_fused(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
-                           const int32_t* h_offs, Workspace& ws, const float* h0, bool store);
-void gru_backward_big_fused(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
-                            const int32_t* h_offs, Workspace& ws);
 
 // Fused heads + PPO loss (learner.cpp:77-115) + head backward.  Writes
 // dhidden, the head/log_std gradient slots of `grad`, the per-row IS weights

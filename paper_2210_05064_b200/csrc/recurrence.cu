@@ -950,10 +950,9 @@ __global__ void __launch_bounds__(NW * 32, 1) gru_bwd_ks(
   }
 }
 
-// warps per K-split CTA: 8, or 16 sharing the same weights (48 per thread) at
-// H = 512 with VER_REC_NW=16.  Measured equal on B200 (the big steps are not
-// bound by latency hiding), so 8 is the default.
-static int ks_warps(int H) { return (H == 512 && env_int("VER_REC_NW", 8) == 16) ? 16 : 8; }
+// warps per K-split CTA (a 16-warp variant sharing the weights measured equal
+// on B200: the steps are not bound by latency hiding)
+static int ks_warps(int) { return 8; }
 static size_t ks_fwd_smem(int H) {
   const int nw = ks_warps(H);
   return sizeof(float) * ((size_t)2 * ks_fr(nw) * H + (size_t)nw * ks_fr(nw) * 3 * UPB) + 16;
@@ -963,7 +962,6 @@ static size_t ks_bwd_smem(int H) {
   return sizeof(float) * ((size_t)2 * KS_BR * 3 * H + (size_t)nw * KS_BR * UPB) + 16;
 }
 static const void* pick_fwd_ks(int H) {
-  if (ks_warps(H) == 16) return reinterpret_cast<const void*>(gru_fwd_ks<512, 16>);
   switch (H) {
     case 256: return reinterpret_cast<const void*>(gru_fwd_ks<256, 8>);
     case 512: return reinterpret_cast<const void*>(gru_fwd_ks<512, 8>);
@@ -971,7 +969,6 @@ static const void* pick_fwd_ks(int H) {
   }
 }
 static const void* pick_bwd_ks(int H) {
-  if (ks_warps(H) == 16) return reinterpret_cast<const void*>(gru_bwd_ks<512, 16>);
   switch (H) {
     case 256: return reinterpret_cast<const void*>(gru_bwd_ks<256, 8>);
     case 512: return reinterpret_cast<const void*>(gru_bwd_ks<512, 8>);
@@ -1476,14 +1473,7 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
   // FMA kernel, then the cluster tail
   const int tb = (h_bs && h_offs && pick_fwd_ks(m.H) && rec_mode() == 0) ? gru_big_steps(c, m, h_bs, L, false) : 0;
   if (tb > 0) {
-    if (step_fused_ok(m.H, false)) {
-      gru_forward_big_fused(c, m, params, tb, h_bs, h_offs, ws, h0, store);
-    } else if (step_gemm_enabled()) {
-      gru_forward_big_persist(c, m, params, tb, h_bs, h_offs, ws, h0, store);
-    } else {
-      ScopedEv ev(c, c->rec_tag);
-      gru_forward_big(c, m, params, tb, h_bs, h_offs, ws, h0, store);
-    }
+    gru_forward_big_persist(c, m, params, tb, h_bs, h_offs, ws, h0, store);
     const int t0 = tail_ok(c, m.H) ? std::max(tb, tail_start(h_bs, L, env_int("VER_REC_TAIL_FWD", 2))) : L;
     if (t0 > tb) fwd_ks_launch(c, m, params, tb, t0, d_bs, d_offs, ws, h0, store);
     if (t0 < L) {
@@ -1634,16 +1624,7 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
       coop_launch(c, fn, grid, ks_bwd_smem(m.H), args, 32 * ks_warps(m.H));
       trace_dump(c, "bwd", L, d_bs, tr);
     }
-    if (t_big > 0) {
-      if (step_fused_ok(m.H, true)) {
-        gru_backward_big_fused(c, m, params, t_big, h_bs, h_offs, ws);
-      } else if (step_gemm_enabled()) {
-        gru_backward_big_persist(c, m, params, t_big, h_bs, h_offs, ws);
-      } else {
-        ScopedEv ev(c, c->rec_tag);
-        gru_backward_big(c, m, params, t_big, h_bs, h_offs, ws);
-      }
-    }
+    if (t_big > 0) gru_backward_big_persist(c, m, params, t_big, h_bs, h_offs, ws);
     return;
   }
   if (const void* fn = pick_bwd(m.H)) {

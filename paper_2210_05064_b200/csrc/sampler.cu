@@ -212,28 +212,9 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(
     const float* __restrict__ v_obs, const int32_t* __restrict__ v_act, const float* __restrict__ v_actc,
     const float* __restrict__ v_lp, const float* __restrict__ v_adv, const float* __restrict__ v_ret,
     float* __restrict__ obs, int32_t* __restrict__ act, float* __restrict__ actc, float* __restrict__ lp,
-    float* __restrict__ adv, float* __restrict__ ret, int D, int A, int continuous, int ntiles, int S, int pf) {
+    float* __restrict__ adv, float* __restrict__ ret, int D, int A, int continuous, int ntiles, int S) {
   extern __shared__ float tl[];  // F fields x 32 pieces x 33 (padded)
   __shared__ int s_start[kGT], s_len[kGT];
-  // L2 prefetch of the view runs of tile blockIdx + pf (last warp, one piece per lane)
-  if (pf > 0 && threadIdx.x >= blockDim.x - 32 && blockIdx.x + pf < ntiles) {
-    const int2 tf = tiles[blockIdx.x + pf];
-    const int jl = threadIdx.x - (blockDim.x - 32), j = tf.x * kGT + jl;
-    const int tf0 = tf.y >> 3, ttf = 1 << (tf.y & 7);
-    if (j < k) {
-      const ver_seq_desc d = sorted[j];
-      const int n = min(ttf, d.length - tf0);
-      if (n > 0) {
-        const int s0 = d.start_offset + tf0;
-        prefetch_l2(v_obs + (size_t)s0 * D, 4u * n * D, v_obs, v_obs + (size_t)S * D);
-        prefetch_l2(v_lp + s0, 4u * n, v_lp, v_lp + S);
-        prefetch_l2(v_adv + s0, 4u * n, v_adv, v_adv + S);
-        prefetch_l2(v_ret + s0, 4u * n, v_ret, v_ret + S);
-        if (!continuous) prefetch_l2(v_act + s0, 4u * n, v_act, v_act + S);
-        else prefetch_l2(v_actc + (size_t)s0 * A, 4u * n * A, v_actc, v_actc + (size_t)S * A);
-      }
-    }
-  }
   const int2 te = tiles[blockIdx.x];
   const int jb = te.x, t0 = te.y >> 3, lg = te.y & 7, TT = 1 << lg;
   const int j0 = jb * kGT;
@@ -314,7 +295,7 @@ void gather_packed(DView& V, DPacked& P) {
   gather_tiled_kernel<<<(unsigned)P.tile_table.size(), 256, smem, c->stream>>>(
       P.tiles.p, P.seqs.p, P.k, P.offs.p, P.bs.p, P.slots.p, V.obs.p, V.act_disc.p, V.act_cont.p, V.log_prob.p,
       V.advantage.p, V.returns.p, P.obs.p, P.act_disc.p, P.act_cont.p, P.old_logp.p, P.adv.p, P.ret.p, V.obs_dim,
-      V.act_dim, V.action_kind, (int)P.tile_table.size(), V.size, env_int("VER_GATHER_PF", 0));
+      V.act_dim, V.action_kind, (int)P.tile_table.size(), V.size);
   after_launch(c);
 }
 

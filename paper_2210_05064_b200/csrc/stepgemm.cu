@@ -517,7 +517,6 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
 
 }  // namespace sg
 
-bool step_gemm_enabled() { return env_int("VER_REC_PERSIST", 1) != 0; }
 
 // forward big steps t = 0 .. t_end-1 in one persistent launch
 void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,

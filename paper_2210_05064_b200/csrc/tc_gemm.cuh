@@ -43,10 +43,20 @@ constexpr int EPI_LD = 36;                   // epilogue staging row stride (flo
 constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_LD * 4;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 // The tensor core's fp32 accumulation truncates; so that 3xTF32 stays
-// fp32-grade for long K, each group of PROMOTE K-blocks accumulates into one
-// of two TMEM buffers which the epilogue warps drain into fp32 registers
-// (round-to-nearest adds) while the MMA fills the other buffer.
-constexpr int PROMOTE = 2;
+// fp32-grade for long K, each group of PROMOTE K-blocks (128 K) accumulates
+// into one TMEM buffer which the epilogue warps drain into fp32 registers
+// (round-to-nearest adds) while the MMA fills the next one.  The drains read
+// 64 KB of TMEM each (tcgen05.ld: ~64 B/cycle/SM), so 4 rather than 2 K-blocks
+// per group: C3 update -3 ms at unchanged parity (VER_TC_PROMOTE overrides).
+constexpr int PROMOTE = 4;
+
+// Debug instrumentation (ver_debug_gemm_prof): per-role clock64 cycles spent
+// waiting, summed over CTAs; off unless g_tc_prof_on is set.  Slots: 0 MMA
+// waits acc_empty, 1 MMA waits split, 2 MMA loop total, 3 split waits full,
+// 4 split waits A slot, 5 epilogue waits acc_full, 6 epilogue final stores,
+// 7 producer waits empty, 8 stages issued, 9 epilogue drains
+static __device__ unsigned long long g_tc_prof[16];
+static __device__ int g_tc_prof_on;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -168,20 +178,24 @@ template <int AMAJ, int BMAJ, int SPLIT3, class Epi, int ATM = 0, int BLO = 0>
 __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                              const __grid_constant__ CUtensorMap tmB, int M,
                                                              int N, int K, int kb_per_split, int nsplit, Epi epi,
-                                                             const __grid_constant__ CUtensorMap tmBl) {
+                                                             const __grid_constant__ CUtensorMap tmBl, int promote) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* stg_all = reinterpret_cast<float*>(smem + tc::STAGES * tc::STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc::STAGES * tc::STAGE_BYTES + EPI_BYTES);
   // bars: full[S] split[S] empty[S] acc_full[NACC] acc_empty[NACC]; then the TMEM address slot
-  constexpr int NACC = ATM ? 2 : tc::NACC;
+  // ATM 1: 2 accumulator buffers + a 4-deep TMEM ring of A stages; ATM 2: 3
+  // accumulator buffers + a 2-deep TMEM A ring (the split warps then also wait
+  // for the MMAs of stage it - 2 before overwriting its A slot)
+  constexpr int NACC = ATM == 2 ? 3 : (ATM ? 2 : tc::NACC);
   // ATM stages hold A hi, B hi, B lo only (A lo lives in TMEM): 4 x 48 KB
   constexpr int STAGES = ATM ? 4 : tc::STAGES;
   constexpr int STAGE_BYTES = ATM ? 3 * TILE_BYTES : tc::STAGE_BYTES;
   static_assert(STAGES * STAGE_BYTES <= tc::STAGES * tc::STAGE_BYTES, "smem budget");
-  static_assert(!ATM || NACC * BN + STAGES * 64 <= 512, "TMEM budget");
-  constexpr int A_COL0 = NACC * BN;  // ATM: stage s hi at A_COL0 + 64 s, lo at + 32
-  static_assert(!ATM || (AMAJ == 0 && SPLIT3), "A via TMEM: K-major A, 3xTF32");
+  constexpr int ARING = ATM == 2 ? 2 : STAGES;
+  static_assert(!ATM || NACC * BN + ARING * 64 <= 512, "TMEM budget");
+  constexpr int A_COL0 = NACC * BN;  // ATM: A slot q hi at A_COL0 + 64 q, lo at + 32
+  static_assert(!ATM || SPLIT3, "A via TMEM: 3xTF32");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * 4 + 2 * tc::NACC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tilesN = (N + BN - 1) / BN, tilesM = (M + BM - 1) / BM;
@@ -237,6 +251,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const bool prof = g_tc_prof_on != 0;
   // programmatic dependent launch: the prologue above overlapped the previous
   // kernel's tail; its results are visible after this wait.  The next kernel may
   // be scheduled as soon as SMs free up (it waits the same way).
@@ -252,7 +267,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         for (int i = 0; i < T.nkb; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
+          const long long w0 = prof ? clock64() : 0;
           mbar_wait(empty_bar(s), ph ^ 1);
+          if (prof) atomicAdd(&g_tc_prof[7], (unsigned long long)(clock64() - w0));
           mbar_expect_tx(full_bar(s), (BLO ? 3 : 2) * TILE_BYTES);
           const int k0 = (T.kb0 + i) * BK;
           if (AMAJ == 0) {
@@ -280,23 +297,29 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     // ---------------- MMA issuer (one thread)
     const uint32_t idesc = (1u << 4)                         // D format F32
                            | (2u << 7) | (2u << 10)          // A, B format TF32
-                           | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16)
+                           | ((uint32_t)(ATM ? 0 : AMAJ) << 15) | ((uint32_t)BMAJ << 16)
                            | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
     if (lane == 0) {
       int it = 0, g = 0, buf = 0;
+      unsigned long long wa = 0, ws_ = 0;
+      const long long t_start = prof ? clock64() : 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const Tile T = decode(t);
         for (int i = 0; i < T.nkb; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
-          const bool first = (i % PROMOTE) == 0;
+          const bool first = (i % promote) == 0;
           if (first) {
             buf = g % NACC;
             const int u = g / NACC;
+            const long long w0 = prof ? clock64() : 0;
             if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
+            if (prof) wa += clock64() - w0;
           }
+          const long long w1 = prof ? clock64() : 0;
           if (SPLIT3) mbar_wait(split_bar(s), ph);
           else mbar_wait(full_bar(s), ph);
+          if (prof) ws_ += clock64() - w1;
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * BN);
 #pragma unroll
@@ -304,7 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
             const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
             const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
             if (ATM) {
-              const uint32_t ah = tmem + (uint32_t)(A_COL0 + 64 * s + 8 * kk);
+              const uint32_t ah = tmem + (uint32_t)(A_COL0 + 64 * (it % ARING) + 8 * kk);
               const uint64_t bl = operand_desc<BMAJ>(tile(s, 3), kk);
               mma_tf32_ts(d, ah, bh, idesc, acc);
               mma_tf32_ts(d, ah + 32, bh, idesc, 1u);
@@ -321,11 +344,17 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
             }
           }
           umma_commit(empty_bar(s));
-          if ((i % PROMOTE) == PROMOTE - 1 || i == T.nkb - 1) {
+          if ((i % promote) == promote - 1 || i == T.nkb - 1) {
             umma_commit(acc_full(buf));
             ++g;
           }
         }
+      }
+      if (prof) {
+        atomicAdd(&g_tc_prof[0], wa);
+        atomicAdd(&g_tc_prof[1], ws_);
+        atomicAdd(&g_tc_prof[2], (unsigned long long)(clock64() - t_start));
+        atomicAdd(&g_tc_prof[8], (unsigned long long)it);
       }
     }
     __syncwarp();
@@ -339,30 +368,53 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         for (int i = 0; i < T.nkb; ++i, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
+          const long long w0 = prof ? clock64() : 0;
           mbar_wait(full_bar(s), ph);
+          if (prof && lane == 0) atomicAdd(&g_tc_prof[3], (unsigned long long)(clock64() - w0));
           uint8_t* st = smem + s * STAGE_BYTES;
           float4* ahi = reinterpret_cast<float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
           float4* bhi = reinterpret_cast<float4*>(st + (ATM ? 1 : 2) * TILE_BYTES);
           float4* blo = reinterpret_cast<float4*>(st + (ATM ? 2 : 3) * TILE_BYTES);
           if (ATM) {
-            // row r = this thread's TMEM lane: its 32 K values from the SW128
-            // K-major tile (16-byte chunk c of row r sits at chunk c ^ (r % 8))
+            // row r = this thread's TMEM lane: its 32 K values
             const int r = 32 * (warp & 3) + lane;
-            const uint8_t* rowp = st + (r >> 3) * 1024 + (r & 7) * 128;
             uint32_t hv[32], lv[32];
+            if (AMAJ == 0) {
+              // SW128 K-major tile: 16-byte chunk c of row r sits at chunk c ^ (r % 8)
+              const uint8_t* rowp = st + (r >> 3) * 1024 + (r & 7) * 128;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float4 x = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
-              const float xs[4] = {x.x, x.y, x.z, x.w};
+              for (int c = 0; c < 8; ++c) {
+                const float4 x = *reinterpret_cast<const float4*>(rowp + ((c ^ (r & 7)) << 4));
+                const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const uint32_t hb = __float_as_uint(xs[j]) & 0xffffe000u;
-                hv[4 * c + j] = hb;
-                lv[4 * c + j] = __float_as_uint(xs[j] - __uint_as_float(hb));
+                for (int j = 0; j < 4; ++j) {
+                  const uint32_t hb = __float_as_uint(xs[j]) & 0xffffe000u;
+                  hv[4 * c + j] = hb;
+                  lv[4 * c + j] = __float_as_uint(xs[j] - __uint_as_float(hb));
+                }
+              }
+            } else {
+              // unswizzled MN-major tile (A never feeds the MMA from shared memory
+              // here): 32-row chunk r / 32 at 4096 B, K-row k at 128 B, row r % 32 at
+              // 4 B -- a warp reads one 128-byte K-row per load (conflict-free)
+              const float* colp = reinterpret_cast<const float*>(st + (r >> 5) * 4096) + (r & 31);
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                const float x = colp[32 * k];
+                const uint32_t hb = __float_as_uint(x) & 0xffffe000u;
+                hv[k] = hb;
+                lv[k] = __float_as_uint(x - __uint_as_float(hb));
               }
             }
-            const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(A_COL0 + 64 * s);
+            if (ATM == 2 && it >= ARING) {  // the MMAs of stage it - ARING have read this A slot
+              const int q = it - ARING;
+              const long long w1 = prof ? clock64() : 0;
+              mbar_wait(empty_bar(q % STAGES), (q / STAGES) & 1);
+              if (prof && lane == 0) atomicAdd(&g_tc_prof[4], (unsigned long long)(clock64() - w1));
+              tc_fence_after();
+            }
+            const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(A_COL0 + 64 * (it % ARING));
             tmem_st32(ta, hv);
             tmem_st32(ta + 32, lv);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -396,13 +448,22 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     int g = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const Tile T = decode(t);
-      const int ngroups = (T.nkb + PROMOTE - 1) / PROMOTE;
+      const int ngroups = (T.nkb + promote - 1) / promote;
+      {  // second epilogue operand (tanh-gradient Y, added term T) of this thread's row -> L2
+        const int m = T.m0 + lane_base + lane;
+        if (m < M) epi.prefetch_row(m, T.n0, min(BN, N - T.n0));
+      }
       float sums[BN];
 #pragma unroll
       for (int j = 0; j < BN; ++j) sums[j] = 0.f;
       for (int q = 0; q < ngroups; ++q, ++g) {
         const int buf = g % NACC;
+        const long long w0 = prof ? clock64() : 0;
         mbar_wait(acc_full(buf), (g / NACC) & 1);
+        if (prof && lane == 0) {
+          atomicAdd(&g_tc_prof[5], (unsigned long long)(clock64() - w0));
+          atomicAdd(&g_tc_prof[9], 1ull);
+        }
         tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < BN / 32; ++cc) {
@@ -427,6 +488,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
       }
       // epilogue: transpose 32 x 32 blocks through shared memory so each warp
       // store covers 4 rows x 128 contiguous bytes (float4 per lane)
+      const long long e0 = prof ? clock64() : 0;
       const int rr = lane >> 3, c4 = (lane & 7) * 4;
 #pragma unroll
       for (int cc = 0; cc < BN / 32; ++cc) {
@@ -446,6 +508,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
         }
         __syncwarp();
       }
+      if (prof && lane == 0) atomicAdd(&g_tc_prof[6], (unsigned long long)(clock64() - e0));
     }
   }
   tc_fence_before();
@@ -455,284 +518,6 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
   }
 }
-
-// ------------------------------------------------- CTA-pair variant
-// cta_group::2: a cluster of 2 CTAs computes a 256 x 128 tile with one
-// tcgen05.mma.cta_group::2 per K-step, issued by the leader (rank 0).  Each CTA
-// holds its 128 rows of A and 64 of the 128 columns of B (CUTLASS
-// SM100_MMA_TF32_2x1SM: ALayout M/2 per CTA, BLayout N/2 per CTA, C M/2 x N in
-// each CTA's TMEM), so per SM the operand reads of the MMAs, the TMA bytes and
-// the 3xTF32 split traffic all drop by 25% against the single-CTA 128 x 128
-// tile at the same FLOPs: the single-CTA kernel is shared-memory bound.
-//  * each CTA's TMA signals its own full barrier; its split warps then arrive
-//    on the LEADER's split barrier (2 x 4 arrivals) before the MMA may read;
-//  * MMA completion is multicast to both CTAs' empty / acc_full barriers;
-//  * both CTAs' epilogue warps arrive on the leader's acc_empty (2 x 4).
-namespace pair {
-constexpr int BNH = BN / 2;                    // B columns per CTA
-constexpr int STAGES2 = 4;
-constexpr int TILE_A = BM * BK * 4;            // 16 KB
-constexpr int TILE_B = BNH * BK * 4;           // 8 KB
-constexpr int STAGE2 = 2 * TILE_A + 2 * TILE_B;  // A hi, A lo, B hi, B lo
-constexpr int SMEM2 = STAGES2 * STAGE2 + EPI_BYTES + 1024 + 256;
-
-__device__ __forceinline__ uint32_t cta_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t to_rank(uint32_t local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void commit2(uint32_t mbar) {
-  asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-          mbar)
-      : "memory");
-}
-__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-template <int AMAJ, int BMAJ, int SPLIT3, class Epi>
-__global__ void __launch_bounds__(THREADS, 1) tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
-                                                              const __grid_constant__ CUtensorMap tmB, int M,
-                                                              int N, int K, int kb_per_split, int nsplit, Epi epi) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cta_rank();
-  const bool leader = rank == 0;
-  const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int tilesN = (N + BN - 1) / BN, tilesM = (M + 2 * BM - 1) / (2 * BM);
-  const int ntiles = tilesN * tilesM * nsplit;
-  const int nkb_total = (K + BK - 1) / BK;
-  const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar0 = smem_u32(bars);
-  auto full_bar = [&](int s) { return bar0 + 8 * s; };
-  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES2 + s); };
-  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES2 + s); };
-  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES2 + b); };
-  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES2 + NACC + b); };
-  auto tileA = [&](int s, int lo) { return sbase + s * STAGE2 + lo * TILE_A; };
-  auto tileB = [&](int s, int lo) { return sbase + s * STAGE2 + 2 * TILE_A + lo * TILE_B; };
-  struct Tile {
-    int m0, n0, z, kb0, nkb;
-  };
-  auto decode = [&](int t) {
-    Tile r;
-    const int nt = t % tilesN, q = t / tilesN;
-    r.n0 = nt * BN;
-    r.m0 = (q % tilesM) * 2 * BM;
-    r.z = q / tilesM;
-    r.kb0 = r.z * kb_per_split;
-    r.nkb = max(0, min(nkb_total, r.kb0 + kb_per_split) - r.kb0);
-    return r;
-  };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(split_bar(s), 2 * SPLIT_WARPS);
-      mbar_init(empty_bar(s), 1);
-    }
-    for (int b = 0; b < NACC; ++b) {
-      mbar_init(acc_full(b), 1);
-      mbar_init(acc_empty(b), 2 * EPI_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(NACC * BN)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ---------------- TMA producer (both CTAs: own A rows, own half of B)
-    if (lane == 0) {
-      int it = 0;
-      for (int t = pair_id; t < ntiles; t += npairs) {
-        const Tile T = decode(t);
-        const int am = T.m0 + (int)rank * BM, bn = T.n0 + (int)rank * BNH;
-        for (int i = 0; i < T.nkb; ++i, ++it) {
-          const int s = it % STAGES2;
-          const uint32_t ph = (it / STAGES2) & 1;
-          mbar_wait(empty_bar(s), ph ^ 1);
-          mbar_expect_tx(full_bar(s), TILE_A + TILE_B);
-          const int k0 = (T.kb0 + i) * BK;
-          if (AMAJ == 0) {
-            tma_load_2d(tileA(s, 0), &tmA, full_bar(s), k0, am);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BM / 32; ++c) tma_load_2d(tileA(s, 0) + c * 4096, &tmA, full_bar(s), am + 32 * c, k0);
-          }
-          if (BMAJ == 0) {
-            tma_load_2d(tileB(s, 0), &tmB, full_bar(s), k0, bn);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BNH / 32; ++c) tma_load_2d(tileB(s, 0) + c * 4096, &tmB, full_bar(s), bn + 32 * c, k0);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (leader CTA, one thread)
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
-    if (leader && lane == 0) {
-      int it = 0, g = 0, buf = 0;
-      for (int t = pair_id; t < ntiles; t += npairs) {
-        const Tile T = decode(t);
-        for (int i = 0; i < T.nkb; ++i, ++it) {
-          const int s = it % STAGES2;
-          const uint32_t ph = (it / STAGES2) & 1;
-          const bool first = (i % PROMOTE) == 0;
-          if (first) {
-            buf = g % NACC;
-            const int u = g / NACC;
-            if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
-          }
-          mbar_wait(split_bar(s), ph);
-          tc_fence_after();
-          const uint32_t d = tmem + (uint32_t)(buf * BN);
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
-            const uint64_t bh = operand_desc<BMAJ>(tileB(s, 0), kk);
-            const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
-            mma2_tf32(d, ah, bh, idesc, acc);
-            if (SPLIT3) {
-              mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
-              mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
-            }
-          }
-          commit2(empty_bar(s));
-          if ((i % PROMOTE) == PROMOTE - 1 || i == T.nkb - 1) {
-            commit2(acc_full(buf));
-            ++g;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp < 2 + SPLIT_WARPS) {
-    // ---------------- operand split (both CTAs), then arrive on the leader
-    const int et = threadIdx.x - 64;
-    int it = 0;
-    for (int t = pair_id; t < ntiles; t += npairs) {
-      const Tile T = decode(t);
-      for (int i = 0; i < T.nkb; ++i, ++it) {
-        const int s = it % STAGES2;
-        const uint32_t ph = (it / STAGES2) & 1;
-        mbar_wait(full_bar(s), ph);
-        if (SPLIT3) {
-          uint8_t* st = smem + s * STAGE2;
-          float4* ahi = reinterpret_cast<float4*>(st);
-          float4* alo = reinterpret_cast<float4*>(st + TILE_A);
-          float4* bhi = reinterpret_cast<float4*>(st + 2 * TILE_A);
-          float4* blo = reinterpret_cast<float4*>(st + 2 * TILE_A + TILE_B);
-#pragma unroll 4
-          for (int q = et; q < TILE_A / 16; q += 32 * SPLIT_WARPS) alo[q] = lo_tf32(ahi[q]);
-#pragma unroll 2
-          for (int q = et; q < TILE_B / 16; q += 32 * SPLIT_WARPS) blo[q] = lo_tf32(bhi[q]);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        __syncwarp();
-        if (lane == 0) arrive_remote(to_rank(split_bar(s), 0));
-      }
-    }
-  } else {
-    // ---------------- accumulator promotion + epilogue (both CTAs: own 128 rows)
-    const int lane_base = 32 * (warp & 3);
-    float* stg = stg_all + (warp & 3) * 32 * EPI_LD;
-    int g = 0;
-    for (int t = pair_id; t < ntiles; t += npairs) {
-      const Tile T = decode(t);
-      const int ngroups = (T.nkb + PROMOTE - 1) / PROMOTE;
-      float sums[BN];
-#pragma unroll
-      for (int j = 0; j < BN; ++j) sums[j] = 0.f;
-      for (int q = 0; q < ngroups; ++q, ++g) {
-        const int buf = g % NACC;
-        mbar_wait(acc_full(buf), (g / NACC) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < BN / 32; ++cc) {
-          uint32_t r[32];
-          const uint32_t taddr = tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN + cc * 32);
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-              : "r"(taddr));
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
-      }
-      const int rr = lane >> 3, c4 = (lane & 7) * 4;
-      const int mrow0 = T.m0 + (int)rank * BM + lane_base;
-#pragma unroll
-      for (int cc = 0; cc < BN / 32; ++cc) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(stg + lane * EPI_LD + 4 * q) =
-              make_float4(sums[cc * 32 + 4 * q], sums[cc * 32 + 4 * q + 1], sums[cc * 32 + 4 * q + 2],
-                          sums[cc * 32 + 4 * q + 3]);
-        __syncwarp();
-        const int n = T.n0 + cc * 32 + c4;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int r = 4 * k + rr;
-          const int m = mrow0 + r;
-          const float4 v = *reinterpret_cast<const float4*>(stg + r * EPI_LD + c4);
-          if (m < M && n < N) epi.vec4(m, n, v, T.z);
-        }
-        __syncwarp();
-      }
-    }
-  }
-  tc_fence_before();
-  cluster_sync_all();  // both CTAs done with TMEM and with remote arrivals
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * BN) : "memory");
-  }
-}
-}  // namespace pair
 
 // ------------------------------------------------------------- host side
 inline PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -750,8 +535,10 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return g_encode;
 }
 
-// 2D fp32 row-major tensor (rows x cols, row stride ld elements), box {32, box_rows}
-inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int box_rows, bool mn_major) {
+// 2D fp32 row-major tensor (rows x cols, row stride ld elements), box {32, box_rows};
+// `plain`: no swizzle (an MN-major A tile that only the split warps read)
+inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int box_rows, bool mn_major,
+                            bool plain = false) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
@@ -759,7 +546,8 @@ inline CUtensorMap make_map(const float* base, int rows, int cols, int ld, int b
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         plain ? CU_TENSOR_MAP_SWIZZLE_NONE
+                               : (mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B),
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(VER_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
@@ -771,14 +559,9 @@ inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 template <class Epi>
 inline bool usable(int M, int N, int K, const float* A, int lda, const float* B, int ldb, const Epi& epi) {
   // TMA boxes (128 or 32 rows) may overhang the tensor: out-of-bounds rows / columns load as zero
-  const int mn_min = env_int("VER_TC_MIN", 1);
-  return M >= mn_min && N >= 16 && K >= 8 && (N % 4) == 0 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) &&
+  return M >= 1 && N >= 16 && K >= 8 && (N % 4) == 0 && (lda % 4) == 0 && (ldb % 4) == 0 && al16(A) &&
          al16(B) && epi.vec_ok();
 }
-
-template <int AMAJ, int BMAJ, class Epi>
-bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
-                 int splits);
 
 // Blo (optional, 3xTF32): B's lo part (x - trunc_tf32(x)) in global memory with
 // B's layout, e.g. a weight's copy made once per minibatch (BLO kernel variant).
@@ -786,9 +569,12 @@ template <int AMAJ, int BMAJ, class Epi>
 void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits,
             const float* Blo = nullptr) {
   ScopedEv ev(c, c->gemm_tag);  // learner timing of the GEMM family (bench roofline)
-  if (launch_pair<AMAJ, BMAJ>(c, M, N, K, A, lda, B, ldb, epi, splits)) return;
-  // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32)
-  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
+  if (c->evlog && c->flop_log && c->gemm_tag >= 0) c->flop_log[c->gemm_tag] += 2.0 * M * (double)N * K;
+  // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32; unswizzled when
+  // the split warps move it into tensor memory)
+  const bool atm = c->precision == 0 && env_int("VER_TC_ATM", 1) && (AMAJ == 0 || env_int("VER_TC_ATM_MN", 1));
+  const CUtensorMap ta =
+      AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true, atm);
   const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, BN, false) : make_map(B, K, N, ldb, 32, true);
   const bool blo = Blo && c->precision == 0 && env_int("VER_TC_BLO", 1) && al16(Blo);
   const CUtensorMap tbl =
@@ -799,6 +585,7 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
   splits = (nkb + per - 1) / per;
   const long long ntiles = cdiv(N, BN) * cdiv(M, BM) * (long long)splits;
   const int grid = (int)std::min<long long>(ntiles, c->num_sms);
+  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
   auto run = [&](auto kern) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     cudaLaunchConfig_t cfg{};
@@ -811,61 +598,25 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
     at[0].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl));
+    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote));
     after_launch(c);
   };
   if (c->precision == 0) {
-    if constexpr (AMAJ == 0) {
-      if (env_int("VER_TC_ATM", 1)) {
+    if (atm) {
+      if (env_int("VER_TC_NACC3", 1)) {
+        if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 2, 1>);
+        else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 2>);
+      } else {
         if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1, 1>);
         else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1>);
-        return;
       }
+      return;
     }
     if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 0, 1>);
     else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi>);
   } else {
     run(tc_gemm_kernel<AMAJ, BMAJ, 0, Epi>);
   }
-}
-
-// CTA-pair launch (cluster of 2): 256 x 128 tiles, opt-in with VER_TC_PAIR=1.
-// Correct (tests/test_gpu_gemm.py passes through it) but measured slower on
-// B200: xp 16384x1536x512 in 198 us against 150 us for the single-CTA kernel
-// (the per-stage cross-CTA split handshake costs more than the 25% of shared
-// memory traffic it saves).
-template <int AMAJ, int BMAJ, class Epi>
-bool launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
-                 int splits) {
-  if (env_int("VER_TC_PAIR", 0) == 0 || M < 2 * BM) return false;
-  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
-  const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, pair::BNH, false) : make_map(B, K, N, ldb, 32, true);
-  const int nkb = (K + BK - 1) / BK;
-  splits = std::max(1, std::min(splits, nkb));
-  const int per = (nkb + splits - 1) / splits;
-  splits = (nkb + per - 1) / per;
-  const long long ntiles = cdiv(N, BN) * cdiv(M, 2 * BM) * (long long)splits;
-  const int grid = 2 * (int)std::min<long long>(ntiles, c->num_sms / 2);
-  auto run = [&](auto kern) {
-    VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM2));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = pair::SMEM2;
-    cfg.stream = c->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi));
-    after_launch(c);
-  };
-  if (c->precision == 0) run(pair::tc_gemm2_kernel<AMAJ, BMAJ, 1, Epi>);
-  else run(pair::tc_gemm2_kernel<AMAJ, BMAJ, 0, Epi>);
-  return true;
 }
 
 // split-K count: the persistent kernel walks tiles x Z work items over the SMs,
@@ -876,10 +627,6 @@ inline int splits_for(const Ctx* c, int M, int N, int K) {
   const long long tiles = cdiv(N, BN) * cdiv(M, BM);
   const int nkb = (K + BK - 1) / BK;
   const int zmax = std::max(1, std::min(64, nkb / 4));
-  if (env_int("VER_TC_SPLIT_OLD", 0)) {
-    int z = (int)((2 * c->num_sms + tiles - 1) / tiles);
-    return std::max(1, std::min(z, zmax));
-  }
   int best = 1;
   double best_cost = 1e300;
   for (int z = 1; z <= zmax; ++z) {

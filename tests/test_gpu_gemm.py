@@ -32,22 +32,6 @@ def test_tc_gemm_3xtf32(ta, tb, M, N, K):
     assert err1 < 1e-2, err1  # tf32 (10-bit mantissa) inputs
 
 
-@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False), (True, True)])
-@pytest.mark.parametrize("M,N,K", [(256, 384, 512), (300, 200, 100), (1024, 1536, 2048)])
-def test_tc_gemm_pair_3xtf32(monkeypatch, ta, tb, M, N, K):
-    """The opt-in CTA-pair kernel (cta_group::2, VER_TC_PAIR=1) at the same bar."""
-    import paper_2210_05064_b200 as V
-    monkeypatch.setenv("VER_TC_PAIR", "1")
-    rng = np.random.default_rng(M + N + K)
-    A = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
-    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
-    ref = (A.astype(np.float64).T if ta else A.astype(np.float64)) @ (B.astype(np.float64).T if tb else B)
-    scale = np.sqrt(K)
-    for split in (1, 3):
-        C3 = V.debug_gemm(A, B, ta, tb, engine=1, splitk=split)
-        assert np.abs(C3 - ref).max() / scale < 1e-5, split
-
-
 def test_presplit_weight_operand_bit_identical(monkeypatch):
     """The weights' lo operand loaded pre-split by TMA (VER_TC_BLO=1, default: the
     encoder / projection GEMMs and the recurrence step kernel's U) gives the same
@@ -71,3 +55,22 @@ def test_presplit_weight_operand_bit_identical(monkeypatch):
         lg.update(buf.close_rollout())
         out.append(lg.params())
     np.testing.assert_array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("M,N,K", [(512, 1536, 4096), (300, 200, 100), (33, 20, 12)])
+def test_mn_major_a_via_tmem_bit_identical(monkeypatch, tb, M, N, K):
+    """MN-major A moved into tensor memory by the split warps (VER_TC_ATM_MN=1,
+    default: the weight-gradient GEMMs) gives the same bits as A read from the
+    swizzled shared-memory tile (VER_TC_ATM_MN=0): same hi / lo operands, same
+    MMA order."""
+    import paper_2210_05064_b200 as V
+    rng = np.random.default_rng(M + 3 * N + 7 * K)
+    A = rng.standard_normal((K, M)).astype(np.float32)
+    B = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+    out = []
+    for on in ("1", "0"):
+        monkeypatch.setenv("VER_TC_ATM_MN", on)
+        out.append([V.debug_gemm(A, B, True, tb, engine=1, splitk=s) for s in (1, 4)])
+    for a, b in zip(*out):
+        np.testing.assert_array_equal(a, b)

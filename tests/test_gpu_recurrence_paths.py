@@ -3,9 +3,8 @@
 
 * the persistent K-split kernels (gru_fwd_ks / gru_bwd_ks),
 * the single-cluster tail kernels for the last short timesteps (H = 512),
-* the tcgen05 paths for timesteps with many rows: the fused cluster step
-  kernel (stepfused.cu), the split-K step kernel (stepgemm.cu) and per-step
-  GEMM + gate launches,
+* the tcgen05 path for timesteps with many rows: the persistent split-K step
+  kernel (stepgemm.cu),
 
 each forced by the row thresholds (VER_REC_BIG_FWD / _BWD, VER_REC_TAIL_*),
 which the library reads at every launch.
@@ -31,11 +30,6 @@ PATHS = {
     # big steps (>= 6 rows) in the split-K tcgen05 step kernel (stepgemm.cu), K-split
     # for 5, cluster tail for <= 4 / <= 3 (the defaults)
     "big+ks+tail": {"VER_REC_TAIL": "1", "VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6"},
-    # both directions in the fused cluster step kernel (stepfused.cu, opt-in)
-    "fused": {"VER_REC_TAIL": "1", "VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6", "VER_REC_PERSIST": "2",
-              "VER_REC_FUSED_BWD": "1"},
-    # one GEMM launch + one gate launch per big step
-    "launch": {"VER_REC_TAIL": "1", "VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6", "VER_REC_PERSIST": "0"},
     # cluster tail for everything it can take, K-split for the rest
     "tail": {"VER_REC_TAIL": "1", "VER_REC_TAIL_FWD": "8", "VER_REC_TAIL_BWD": "8",
              "VER_REC_BIG_FWD": "100000", "VER_REC_BIG_BWD": "100000"},
