@@ -224,14 +224,15 @@ static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
     // Tail split: when the last wave of output tiles would leave most SMs idle,
     // the last m-tiles run as a second launch split two ways along K (twice as
     // many half-size items fill that wave), reduced with the same epilogue.
-    const int tilesN = (int)cdiv(N, tc::BN), tilesM = (int)cdiv(M, tc::BM);
-    const long long tiles = (long long)tilesN * tilesM, sms = c->num_sms;
+    const tc::Geo g = tc::geo(c, M, N);
+    const int tilesN = (int)cdiv(N, g.bn), tilesM = (int)cdiv(M, g.bm);
+    const long long tiles = (long long)tilesN * tilesM, sms = g.units;
     const long long rem = tiles % sms;
     const int tail_mt = (int)cdiv(rem, tilesN);
     const int nkb = (K + tc::BK - 1) / tc::BK;
     if (env_int("VER_TC_TAIL", 1) && c->precision == 0 && tiles > sms && rem > 0 && 10 * rem < 6 * sms &&
         tail_mt < tilesM && nkb >= 32 && N % 4 == 0) {  // K < 1024: half a wave saves less than the extra launches
-      const int M1 = (tilesM - tail_mt) * tc::BM, M2 = M - M1;
+      const int M1 = (tilesM - tail_mt) * g.bm, M2 = M - M1;
       tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M1, N, K, A, lda, B, ldb, epi, 1, Blo);
       const float* A2 = TA ? A + M1 : A + (size_t)M1 * lda;
       float* W = nullptr;

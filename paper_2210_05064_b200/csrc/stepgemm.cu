@@ -61,6 +61,119 @@ __device__ __forceinline__ long long gtimer() {
 }
 
 
+// gate phase of one step over the grid: thread `tid` of `nthreads` walks
+// (row j, units 4x .. 4x+3).  Forward: sum the Z partials of hU, GRU gates,
+// h_t (nn.cpp:235-250); backward: sum the partials of dh_{t-1}, gate gradient
+// of the rows of step t-1.
+template <int DIR>
+__device__ __forceinline__ void gate_phase(const Step& S, int H, const float* __restrict__ part,
+                                           const float* __restrict__ xp, const float* __restrict__ h0,
+                                           float* __restrict__ hidden, float* __restrict__ gates_out,
+                                           float* __restrict__ hun_out, float* __restrict__ hprev_out,
+                                           const float* __restrict__ dhidden, const float* __restrict__ gates,
+                                           const float* __restrict__ hun, const float* __restrict__ hprev,
+                                           float* __restrict__ dpre, float* __restrict__ dhu,
+                                           float* __restrict__ gz, int tid, int nthreads) {
+  const int H3 = 3 * H, N = DIR == 0 ? H3 : H;
+  const int H4 = H / 4;
+  const size_t zs = (size_t)S.B * N;
+  for (int idx = tid; idx < S.Bg * H4; idx += nthreads) {
+    const int j = idx / H4, u4 = idx % H4;
+    if (DIR == 0) {
+      const size_t row3 = ((size_t)S.o + j) * H3 + 12 * (size_t)u4, row = ((size_t)S.o + j) * H + 4 * (size_t)u4;
+      const size_t prow = (size_t)j * H3 + 12 * (size_t)u4;
+      float s12[12];
+#pragma unroll
+      for (int e = 0; e < 12; ++e) s12[e] = 0.f;
+#pragma unroll
+      for (int z = 0; z < 8; ++z) {
+        if (z < S.Z) {  // predicated, so all Z partial loads are in flight together
+          const float4* p4 = reinterpret_cast<const float4*>(part + z * zs + prow);
+          const float4 a = p4[0], b = p4[1], c = p4[2];
+          s12[0] += a.x; s12[1] += a.y; s12[2] += a.z; s12[3] += a.w; s12[4] += b.x; s12[5] += b.y;
+          s12[6] += b.z; s12[7] += b.w; s12[8] += c.x; s12[9] += c.y; s12[10] += c.z; s12[11] += c.w;
+        }
+      }
+      const float4* x4 = reinterpret_cast<const float4*>(xp + row3);
+      const float4 xa = x4[0], xb = x4[1], xc = x4[2];
+      const float x[12] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w, xc.x, xc.y, xc.z, xc.w};
+      const float* hp = S.op < 0 ? h0 + (size_t)j * H : hidden + ((size_t)S.op + j) * H;
+      const float4 hp4 = *reinterpret_cast<const float4*>(hp + 4 * u4);
+      const float hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
+      float hn[4], g[12];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float rg = gate_sigm(x[3 * e] + s12[3 * e]);
+        const float zg = gate_sigm(x[3 * e + 1] + s12[3 * e + 1]);
+        const float ng = gate_tanh(x[3 * e + 2] + rg * s12[3 * e + 2]);
+        hn[e] = (1.f - zg) * ng + zg * hpv[e];
+        g[3 * e] = rg;
+        g[3 * e + 1] = zg;
+        g[3 * e + 2] = ng;
+      }
+      *reinterpret_cast<float4*>(hidden + row) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+      if (gates_out) {
+        float4* g4 = reinterpret_cast<float4*>(gates_out + row3);
+        g4[0] = make_float4(g[0], g[1], g[2], g[3]);
+        g4[1] = make_float4(g[4], g[5], g[6], g[7]);
+        g4[2] = make_float4(g[8], g[9], g[10], g[11]);
+        *reinterpret_cast<float4*>(hun_out + row) = make_float4(s12[2], s12[5], s12[8], s12[11]);
+        *reinterpret_cast<float4*>(hprev_out + row) = hp4;
+      }
+    } else {
+      const size_t row = ((size_t)S.op + j) * H + 4 * (size_t)u4, row3 = ((size_t)S.op + j) * H3 + 12 * (size_t)u4;
+      float dh[4] = {0.f, 0.f, 0.f, 0.f};
+      if (j < S.B) {
+#pragma unroll
+        for (int z = 0; z < 8; ++z) {
+          if (z < S.Z) {
+            const float4 p = *reinterpret_cast<const float4*>(part + z * zs + (size_t)j * H + 4 * u4);
+            dh[0] += p.x; dh[1] += p.y; dh[2] += p.z; dh[3] += p.w;
+          }
+        }
+        const float4 q = *reinterpret_cast<const float4*>(gz + ((size_t)S.o + j) * H + 4 * u4);
+        dh[0] += q.x; dh[1] += q.y; dh[2] += q.z; dh[3] += q.w;
+      }
+      const float4 d4 = *reinterpret_cast<const float4*>(dhidden + row);
+      const float4 hn4 = *reinterpret_cast<const float4*>(hun + row);
+      const float4 hp4 = *reinterpret_cast<const float4*>(hprev + row);
+      const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hnv[4] = {hn4.x, hn4.y, hn4.z, hn4.w},
+                  hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
+      const float4* g4 = reinterpret_cast<const float4*>(gates + row3);
+      const float4 ga = g4[0], gb = g4[1], gc = g4[2];
+      const float gt[12] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w, gc.x, gc.y, gc.z, gc.w};
+      float o1[12], o2[12], gzv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float gg = dv[e] + dh[e];
+        const float r = gt[3 * e], zg = gt[3 * e + 1], n = gt[3 * e + 2];
+        const float dn = gg * (1.f - zg);
+        const float dz = gg * (hpv[e] - n);
+        const float dpn = dn * (1.f - n * n);
+        const float dr = dpn * hnv[e];
+        const float dpr = dr * r * (1.f - r);
+        const float dpz = dz * zg * (1.f - zg);
+        o1[3 * e] = dpr;
+        o1[3 * e + 1] = dpz;
+        o1[3 * e + 2] = dpn;
+        o2[3 * e] = dpr;
+        o2[3 * e + 1] = dpz;
+        o2[3 * e + 2] = dpn * r;
+        gzv[e] = gg * zg;
+      }
+      float4* p1 = reinterpret_cast<float4*>(dpre + row3);
+      float4* p2 = reinterpret_cast<float4*>(dhu + row3);
+      p1[0] = make_float4(o1[0], o1[1], o1[2], o1[3]);
+      p1[1] = make_float4(o1[4], o1[5], o1[6], o1[7]);
+      p1[2] = make_float4(o1[8], o1[9], o1[10], o1[11]);
+      p2[0] = make_float4(o2[0], o2[1], o2[2], o2[3]);
+      p2[1] = make_float4(o2[4], o2[5], o2[6], o2[7]);
+      p2[2] = make_float4(o2[8], o2[9], o2[10], o2[11]);
+      *reinterpret_cast<float4*>(gz + row) = make_float4(gzv[0], gzv[1], gzv[2], gzv[3]);
+    }
+  }
+}
+
 template <int DIR>  // 0 forward (B MN-major: U stored K x N), 1 backward (B K-major: U stored N x K)
 __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     int nsteps, const Step* __restrict__ steps, const CUtensorMap* __restrict__ amaps,
@@ -304,104 +417,8 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     grid_sync(bar, target);  // all partials of step si written
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
 
-    // ---------------- gate phase: (row j, units 4x .. 4x+3) over the grid
-    const int H4 = H / 4;
-    const size_t zs = (size_t)S.B * N;
-    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < S.Bg * H4; idx += gridDim.x * blockDim.x) {
-      const int j = idx / H4, u4 = idx % H4;
-      if (DIR == 0) {
-        const size_t row3 = ((size_t)S.o + j) * H3 + 12 * (size_t)u4, row = ((size_t)S.o + j) * H + 4 * (size_t)u4;
-        const size_t prow = (size_t)j * H3 + 12 * (size_t)u4;
-        float s12[12];
-#pragma unroll
-        for (int e = 0; e < 12; ++e) s12[e] = 0.f;
-#pragma unroll
-        for (int z = 0; z < 8; ++z) {
-          if (z < S.Z) {  // predicated, so all Z partial loads are in flight together
-            const float4* p4 = reinterpret_cast<const float4*>(part + z * zs + prow);
-            const float4 a = p4[0], b = p4[1], c = p4[2];
-            s12[0] += a.x; s12[1] += a.y; s12[2] += a.z; s12[3] += a.w; s12[4] += b.x; s12[5] += b.y;
-            s12[6] += b.z; s12[7] += b.w; s12[8] += c.x; s12[9] += c.y; s12[10] += c.z; s12[11] += c.w;
-          }
-        }
-        const float4* x4 = reinterpret_cast<const float4*>(xp + row3);
-        const float4 xa = x4[0], xb = x4[1], xc = x4[2];
-        const float x[12] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w, xc.x, xc.y, xc.z, xc.w};
-        const float* hp = S.op < 0 ? h0 + (size_t)j * H : hidden + ((size_t)S.op + j) * H;
-        const float4 hp4 = *reinterpret_cast<const float4*>(hp + 4 * u4);
-        const float hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
-        float hn[4], g[12];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float rg = gate_sigm(x[3 * e] + s12[3 * e]);
-          const float zg = gate_sigm(x[3 * e + 1] + s12[3 * e + 1]);
-          const float ng = gate_tanh(x[3 * e + 2] + rg * s12[3 * e + 2]);
-          hn[e] = (1.f - zg) * ng + zg * hpv[e];
-          g[3 * e] = rg;
-          g[3 * e + 1] = zg;
-          g[3 * e + 2] = ng;
-        }
-        *reinterpret_cast<float4*>(hidden + row) = make_float4(hn[0], hn[1], hn[2], hn[3]);
-        if (gates_out) {
-          float4* g4 = reinterpret_cast<float4*>(gates_out + row3);
-          g4[0] = make_float4(g[0], g[1], g[2], g[3]);
-          g4[1] = make_float4(g[4], g[5], g[6], g[7]);
-          g4[2] = make_float4(g[8], g[9], g[10], g[11]);
-          *reinterpret_cast<float4*>(hun_out + row) = make_float4(s12[2], s12[5], s12[8], s12[11]);
-          *reinterpret_cast<float4*>(hprev_out + row) = hp4;
-        }
-      } else {
-        const size_t row = ((size_t)S.op + j) * H + 4 * (size_t)u4, row3 = ((size_t)S.op + j) * H3 + 12 * (size_t)u4;
-        float dh[4] = {0.f, 0.f, 0.f, 0.f};
-        if (j < S.B) {
-#pragma unroll
-          for (int z = 0; z < 8; ++z) {
-            if (z < S.Z) {
-              const float4 p = *reinterpret_cast<const float4*>(part + z * zs + (size_t)j * H + 4 * u4);
-              dh[0] += p.x; dh[1] += p.y; dh[2] += p.z; dh[3] += p.w;
-            }
-          }
-          const float4 q = *reinterpret_cast<const float4*>(gz + ((size_t)S.o + j) * H + 4 * u4);
-          dh[0] += q.x; dh[1] += q.y; dh[2] += q.z; dh[3] += q.w;
-        }
-        const float4 d4 = *reinterpret_cast<const float4*>(dhidden + row);
-        const float4 hn4 = *reinterpret_cast<const float4*>(hun + row);
-        const float4 hp4 = *reinterpret_cast<const float4*>(hprev + row);
-        const float dv[4] = {d4.x, d4.y, d4.z, d4.w}, hnv[4] = {hn4.x, hn4.y, hn4.z, hn4.w},
-                    hpv[4] = {hp4.x, hp4.y, hp4.z, hp4.w};
-        const float4* g4 = reinterpret_cast<const float4*>(gates + row3);
-        const float4 ga = g4[0], gb = g4[1], gc = g4[2];
-        const float gt[12] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w, gc.x, gc.y, gc.z, gc.w};
-        float o1[12], o2[12], gzv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float gg = dv[e] + dh[e];
-          const float r = gt[3 * e], zg = gt[3 * e + 1], n = gt[3 * e + 2];
-          const float dn = gg * (1.f - zg);
-          const float dz = gg * (hpv[e] - n);
-          const float dpn = dn * (1.f - n * n);
-          const float dr = dpn * hnv[e];
-          const float dpr = dr * r * (1.f - r);
-          const float dpz = dz * zg * (1.f - zg);
-          o1[3 * e] = dpr;
-          o1[3 * e + 1] = dpz;
-          o1[3 * e + 2] = dpn;
-          o2[3 * e] = dpr;
-          o2[3 * e + 1] = dpz;
-          o2[3 * e + 2] = dpn * r;
-          gzv[e] = gg * zg;
-        }
-        float4* p1 = reinterpret_cast<float4*>(dpre + row3);
-        float4* p2 = reinterpret_cast<float4*>(dhu + row3);
-        p1[0] = make_float4(o1[0], o1[1], o1[2], o1[3]);
-        p1[1] = make_float4(o1[4], o1[5], o1[6], o1[7]);
-        p1[2] = make_float4(o1[8], o1[9], o1[10], o1[11]);
-        p2[0] = make_float4(o2[0], o2[1], o2[2], o2[3]);
-        p2[1] = make_float4(o2[4], o2[5], o2[6], o2[7]);
-        p2[2] = make_float4(o2[8], o2[9], o2[10], o2[11]);
-        *reinterpret_cast<float4*>(gz + row) = make_float4(gzv[0], gzv[1], gzv[2], gzv[3]);
-      }
-    }
+    gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
+                    gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 5] = gtimer();
     if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
   }
@@ -410,6 +427,238 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC * BN) : "memory");
+  }
+}
+
+// ---------------------------------------------- CTA-pair step kernel (big C3 steps)
+// The same per-step schedule (split-K GEMM phase, grid barrier, gate phase,
+// grid barrier) with the GEMM phase on CTA pairs and 256 x 256 tiles
+// (tc_gemm.cuh p2::tc_gemm2_kernel): per SM and MMA cycle half the TMA bytes
+// of the 128 x 128 single-CTA phase.  Used for the steps with >= 1024 rows
+// (the first ~50 steps of a C3 minibatch; VER_REC_PAIR_ROWS), launched as
+// clusters of 2 with all CTAs resident (one per SM).
+template <int DIR>
+__global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
+    int nsteps, const Step* __restrict__ steps, const CUtensorMap* __restrict__ amaps,
+    const __grid_constant__ CUtensorMap bmap, int H, float* __restrict__ part, unsigned* bar,
+    const float* __restrict__ xp, const float* __restrict__ h0, float* __restrict__ hidden,
+    float* __restrict__ gates_out, float* __restrict__ hun_out, float* __restrict__ hprev_out,
+    const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
+    const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
+    const __grid_constant__ CUtensorMap bmap_lo, int blo) {
+  using namespace p2;
+  constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int H3 = 3 * H, N = DIR == 0 ? H3 : H, K = DIR == 0 ? H : H3;
+  const int tilesN = (N + BN2 - 1) / BN2;
+  const int nkb_total = (K + BK - 1) / BK;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8 * s; };
+  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES2 + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES2 + s); };
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES2 + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES2 + NACC2 + b); };
+  auto tileA = [&](int s, int lo) { return sbase + s * STAGE2 + lo * TILE; };
+  auto tileB = [&](int s, int lo) { return sbase + s * STAGE2 + (2 + lo) * TILE; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(split_bar(s), 2 * SPLITW);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < NACC2; ++b) {
+      mbar_init(acc_full(b), 1);
+      mbar_init(acc_empty(b), 2 * EPIW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NACC2 * BN2)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  unsigned target = 0;
+  int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
+  const uint32_t stage_tx = (blo ? 3u : 2u) * TILE;
+
+  for (int si = 0; si < nsteps; ++si) {
+    const Step S = steps[si];
+    const int W = S.B > 0 ? S.tilesM * tilesN * S.Z : 0;  // tilesM in 256-row pair tiles
+    const CUtensorMap* amap = amaps + si;
+    for (int item = pair_id; item < W; item += npairs) {
+      const bool first_item = item == pair_id;
+      const int nt = item % tilesN, q = item / tilesN;
+      const int m0 = (q % S.tilesM) * BM2, n0 = nt * BN2, z = q / S.tilesM;
+      const int kb0 = z * S.per;
+      const int nkb = max(0, min(nkb_total, kb0 + S.per) - kb0);
+      if (warp == 0) {
+        if (lane == 0) {
+          if (first_item) asm volatile("fence.proxy.async.global;" ::: "memory");  // rows of the gate phase
+          const int am = m0 + (int)rank * BM, bn = n0 + (int)rank * BNH;
+          for (int i = 0; i < nkb; ++i, ++it_tma) {
+            const int s = it_tma % STAGES2;
+            const uint32_t ph = (it_tma / STAGES2) & 1;
+            const int k0 = (kb0 + i) * BK;
+            mbar_wait(empty_bar(s), ph ^ 1);
+            mbar_expect_tx(full_bar(s), stage_tx);
+            if (BMAJ == 0) {
+              tma_load_2d(tileB(s, 0), &bmap, full_bar(s), k0, bn);
+              if (blo) tma_load_2d(tileB(s, 1), &bmap_lo, full_bar(s), k0, bn);
+            } else {
+#pragma unroll
+              for (int c = 0; c < BNH / 32; ++c)
+                tma_load_2d(tileB(s, 0) + c * 4096, &bmap, full_bar(s), bn + 32 * c, k0);
+              if (blo) {
+#pragma unroll
+                for (int c = 0; c < BNH / 32; ++c)
+                  tma_load_2d(tileB(s, 1) + c * 4096, &bmap_lo, full_bar(s), bn + 32 * c, k0);
+              }
+            }
+            tma_load_2d(tileA(s, 0), amap, full_bar(s), k0, am);
+          }
+        }
+      } else if (warp == 1) {
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) |
+                               ((uint32_t)BMAJ << 16) | ((uint32_t)(BN2 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
+        if (leader && lane == 0) {
+          int buf = 0;
+          for (int i = 0; i < nkb; ++i, ++it_mma) {
+            const int s = it_mma % STAGES2;
+            const uint32_t ph = (it_mma / STAGES2) & 1;
+            const bool first = (i % SGP) == 0;
+            if (first) {
+              buf = g_mma % NACC2;
+              const int u = g_mma / NACC2;
+              if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
+            }
+            mbar_wait(split_bar(s), ph);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(buf * BN2);
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
+              const uint64_t bh = operand_desc<BMAJ>(tileB(s, 0), kk);
+              mma2_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+              mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+              mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+            }
+            commit2(empty_bar(s));
+            if ((i % SGP) == SGP - 1 || i == nkb - 1) {
+              commit2(acc_full(buf));
+              ++g_mma;
+            }
+          }
+        }
+        __syncwarp();
+      } else if (warp < 2 + SPLITW) {
+        const int et = threadIdx.x - 64;
+        for (int i = 0; i < nkb; ++i, ++it_split) {
+          const int s = it_split % STAGES2;
+          const uint32_t ph = (it_split / STAGES2) & 1;
+          mbar_wait(full_bar(s), ph);
+          uint8_t* st = smem + s * STAGE2;
+          const float4* ahi = reinterpret_cast<const float4*>(st);
+          float4* alo = reinterpret_cast<float4*>(st + TILE);
+          const float4* bhi = reinterpret_cast<const float4*>(st + 2 * TILE);
+          float4* blo_t = reinterpret_cast<float4*>(st + 3 * TILE);
+          if (blo) {
+#pragma unroll 4
+            for (int qq = et; qq < TILE / 16; qq += 32 * SPLITW) alo[qq] = lo_tf32(ahi[qq]);
+          } else {
+#pragma unroll 4
+            for (int qq = et; qq < TILE / 16; qq += 32 * SPLITW) {
+              alo[qq] = lo_tf32(ahi[qq]);
+              blo_t[qq] = lo_tf32(bhi[qq]);
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) arrive_remote(to_rank(split_bar(s), 0));
+        }
+      } else {
+        // accumulator promotion + partial-tile epilogue: part[z][m][n] (own 128 rows,
+        // column half (warp - 4) / 4)
+        const int lq = warp & 3, half = (warp - 4) >> 2;
+        const int lane_base = 32 * lq;
+        float* stg = stg_all + (warp - 4) * 32 * SLD;
+        const int ngroups = (nkb + SGP - 1) / SGP;
+        float sums[BNH];
+#pragma unroll
+        for (int j = 0; j < BNH; ++j) sums[j] = 0.f;
+        for (int gq = 0; gq < ngroups; ++gq, ++g_epi) {
+          const int buf = g_epi % NACC2;
+          mbar_wait(acc_full(buf), (g_epi / NACC2) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < BNH / 32; ++cc) {
+            uint32_t r[32];
+            const uint32_t taddr =
+                tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN2 + half * BNH + cc * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
+        }
+        const int rr = lane >> 2, c4 = (lane & 3) * 4;
+        const int mrow0 = m0 + (int)rank * BM + lane_base, ncol0 = n0 + half * BNH;
+#pragma unroll
+        for (int cb = 0; cb < BNH / 16; ++cb) {
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            *reinterpret_cast<float4*>(stg + lane * SLD + 4 * qq) =
+                make_float4(sums[cb * 16 + 4 * qq], sums[cb * 16 + 4 * qq + 1], sums[cb * 16 + 4 * qq + 2],
+                            sums[cb * 16 + 4 * qq + 3]);
+          __syncwarp();
+          const int n = ncol0 + cb * 16 + c4;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int r = 8 * k + rr;
+            const int m = mrow0 + r;
+            const float4 v = *reinterpret_cast<const float4*>(stg + r * SLD + c4);
+            if (m < S.B && n < N) *reinterpret_cast<float4*>(part + ((size_t)z * S.B + m) * N + n) = v;
+          }
+          __syncwarp();
+        }
+      }
+    }
+    grid_sync(bar, target);  // all partials of step si written
+    gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
+                    gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+    if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC2 * BN2) : "memory");
   }
 }
 
@@ -431,9 +680,56 @@ static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
   return s;
 }
 
+// pair mode: 256-row x 256-column tiles over the resident CTA pairs
+static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs) {
+  Step s{};
+  s.B = B;
+  s.Bg = Bg;
+  s.o = o;
+  s.op = op;
+  s.tilesM = (int)cdiv(std::max(B, 1), p2::BM2);
+  const int tilesN = (int)cdiv(N, p2::BN2);
+  const int nkb = (K + BK - 1) / BK;
+  int Z = std::max(1, std::min(pairs / std::max(1, s.tilesM * tilesN), std::max(1, nkb / 2)));
+  Z = std::min(Z, 8);
+  const int per = (nkb + Z - 1) / Z;
+  s.Z = (nkb + per - 1) / per;
+  s.per = per;
+  return s;
+}
+
+// CTA pairs resident at once for the pair step kernel (all its CTAs must be, for
+// the grid barriers), per device
+template <int DIR>
+static int step_pairs(Ctx* c) {
+  static std::atomic<int> cache[kMaxDevices];
+  int pairs = cache[dev_slot(c)].load();
+  if (!pairs) {
+    const void* fn = reinterpret_cast<const void*>(gru_step_gemm2_kernel<DIR>);
+    VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p2::SMEM2));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c->num_sms);
+    cfg.blockDim = dim3(p2::THREADS2);
+    cfg.dynamicSmemBytes = p2::SMEM2;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    VER_CUDA(cudaOccupancyMaxActiveClusters(&nc, gru_step_gemm2_kernel<DIR>, &cfg));
+    pairs = std::max(1, std::min(nc, c->num_sms / 2));
+    cache[dev_slot(c)].store(pairs);
+  }
+  return pairs;
+}
+
 template <int DIR>
 static void launch(Ctx* c, const Model& m, const float* params, const std::vector<Step>& hs,
-                   const std::vector<CUtensorMap>& maps, Workspace& ws, const float* h0, bool store) {
+                   const std::vector<CUtensorMap>& maps, Workspace& ws, const float* h0, bool store,
+                   bool pair = false) {
   const int nsteps = (int)hs.size();
   if (nsteps == 0) return;
   const int H = m.H, H3 = 3 * H;
@@ -488,6 +784,28 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     ws.trace.zero(TR * (size_t)nsteps + 1);
     tr = ws.trace.p;
   }
+  if (pair) {
+    const int pairs = step_pairs<DIR>(c);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(p2::THREADS2);
+    cfg.dynamicSmemBytes = p2::SMEM2;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barriers spin on each other
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    ScopedEv ev(c, c->rec_tag);
+    VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<DIR>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
+                                hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo));
+    after_launch(c);
+    return;
+  }
   void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
                   &part,  &bar,    &xp,     &h0,  &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre,
                   &dhu,   &gz,     &tr,     const_cast<CUtensorMap*>(&bmap_lo), &blo};
@@ -518,33 +836,59 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
 }  // namespace sg
 
 
-// forward big steps t = 0 .. t_end-1 in one persistent launch
+// rows from which a big step runs in the CTA-pair kernel (0: never)
+static int pair_rows(const Ctx* c) { return c->precision == 0 ? env_int("VER_REC_PAIR_ROWS", 1024) : 0; }
+
+// forward big steps t = 0 .. t_end-1: the steps with >= pair_rows rows in the
+// CTA-pair launch, the rest in the single-CTA launch
 void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_end, const int32_t* h_bs,
                              const int32_t* h_offs, Workspace& ws, const float* h0, bool store) {
   const int H = m.H, H3 = 3 * H;
-  std::vector<sg::Step> hs;
-  std::vector<CUtensorMap> maps;
-  for (int t = 0; t < t_end; ++t) {
-    const int B = h_bs[t];
-    hs.push_back(sg::make_step(B, B, h_offs[t], t == 0 ? -1 : h_offs[t - 1], H3, H, c->num_sms));
-    const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
-    maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
+  const int pr = pair_rows(c);
+  int t1 = 0;
+  if (pr > 0)
+    while (t1 < t_end && h_bs[t1] >= pr) ++t1;
+  for (int part = 0; part < 2; ++part) {
+    const int ta = part == 0 ? 0 : t1, tz = part == 0 ? t1 : t_end;
+    if (ta >= tz) continue;
+    std::vector<sg::Step> hs;
+    std::vector<CUtensorMap> maps;
+    const int pairs = part == 0 ? sg::step_pairs<0>(c) : 0;
+    for (int t = ta; t < tz; ++t) {
+      const int B = h_bs[t];
+      const int op = t == 0 ? -1 : h_offs[t - 1];
+      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs)
+                             : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms));
+      const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
+      maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
+    }
+    sg::launch<0>(c, m, params, hs, maps, ws, h0, store, part == 0);
   }
-  sg::launch<0>(c, m, params, hs, maps, ws, h0, store);
 }
 
-// backward big steps t = t_top .. 1 in one persistent launch
+// backward big steps t = t_top .. 1: the single-CTA launch for the steps with
+// fewer than pair_rows rows first, then the CTA-pair launch
 void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t_top, const int32_t* h_bs,
                               const int32_t* h_offs, Workspace& ws) {
   const int H = m.H, H3 = 3 * H;
-  std::vector<sg::Step> hs;
-  std::vector<CUtensorMap> maps;
-  for (int t = t_top; t >= 1; --t) {
-    const int B = h_bs[t], Bp = h_bs[t - 1];
-    hs.push_back(sg::make_step(B, Bp, h_offs[t], h_offs[t - 1], H, H3, c->num_sms));
-    maps.push_back(tc::make_map(ws.dhu.p + (size_t)h_offs[t] * H3, std::max(B, 1), H3, H3, tc::BM, false));
+  const int pr = pair_rows(c);
+  int t1 = 0;  // steps 1 .. t1 have >= pr rows
+  if (pr > 0)
+    while (t1 + 1 <= t_top && h_bs[t1 + 1] >= pr) ++t1;
+  for (int part = 0; part < 2; ++part) {
+    const int hi = part == 0 ? t_top : t1, lo = part == 0 ? t1 + 1 : 1;
+    if (hi < lo) continue;
+    std::vector<sg::Step> hs;
+    std::vector<CUtensorMap> maps;
+    const int pairs = part == 1 ? sg::step_pairs<1>(c) : 0;
+    for (int t = hi; t >= lo; --t) {
+      const int B = h_bs[t], Bp = h_bs[t - 1];
+      hs.push_back(part == 1 ? sg::make_step2(B, Bp, h_offs[t], h_offs[t - 1], H, H3, pairs)
+                             : sg::make_step(B, Bp, h_offs[t], h_offs[t - 1], H, H3, c->num_sms));
+      maps.push_back(tc::make_map(ws.dhu.p + (size_t)h_offs[t] * H3, std::max(B, 1), H3, H3, tc::BM, false));
+    }
+    sg::launch<1>(c, m, params, hs, maps, ws, nullptr, false, part == 1);
   }
-  sg::launch<1>(c, m, params, hs, maps, ws, nullptr, false);
 }
 
 }  // namespace verg

@@ -519,6 +519,312 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
   }
 }
 
+// ------------------------------------------------- CTA-pair 256 x 256 tiles
+// cta_group::2: a cluster of 2 CTAs (one TPC) computes a 256 x 256 output tile
+// with one tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8) per K-step and
+// 3xTF32 term, issued by the leader CTA (rank 0).  Each CTA holds its 128 rows
+// of A and its 128-column half of B in its own shared memory; the MMA reads
+// both CTAs' tiles, and each CTA's TMEM receives its 128 rows x 256 columns.
+// Per SM and per MMA cycle this moves half the TMA bytes of the single-CTA
+// 128 x 128 kernel (whose weight GEMMs sit at the chip's TMA/L2 throughput):
+// per K-block stage each CTA loads 16 KB of A + 16 KB of B (+ 16 KB of B lo)
+// for 1536 MMA cycles instead of 48 KB for 768.
+//  * each CTA's TMA signals its own full barrier; its 2 split warps then
+//    arrive on the LEADER's split barrier (2 x 2 arrivals) before the MMA reads;
+//  * MMA completion is multicast to both CTAs' empty / acc_full barriers;
+//  * each CTA runs 8 epilogue warps (TMEM lane quarter = warp % 4, column half
+//    = (warp - 4) / 4) that arrive on the leader's acc_empty (2 x 8).
+// A always comes from shared memory here (two 256-column accumulators fill the
+// 512 TMEM columns).
+namespace p2 {
+constexpr int BM2 = 256, BN2 = 256, BNH = 128;  // pair tile; B columns per CTA
+constexpr int SPLITW = 2, EPIW = 8;
+constexpr int THREADS2 = 32 * (2 + SPLITW + EPIW);  // 384
+constexpr int STAGES2 = 3;
+constexpr int TILE = BM * BK * 4;                 // 16 KB: A rows of one CTA, or its B half
+constexpr int STAGE2 = 4 * TILE;                  // A hi, A lo, B hi, B lo
+constexpr int NACC2 = 2;                          // 2 x 256 TMEM columns
+constexpr int SLD = 20;                           // epilogue staging row stride (16 columns + 4)
+constexpr int EPI2 = EPIW * 32 * SLD * 4;
+constexpr int SMEM2 = STAGES2 * STAGE2 + EPI2 + 1024 + 256;
+static_assert(SMEM2 <= 232448, "smem budget");
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t to_rank(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void commit2(uint32_t mbar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+template <int AMAJ, int BMAJ, class Epi, int BLO>
+__global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                               const __grid_constant__ CUtensorMap tmB, int M,
+                                                               int N, int K, int kb_per_split, int nsplit, Epi epi,
+                                                               const __grid_constant__ CUtensorMap tmBl,
+                                                               int promote) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI2);
+  // bars: full[S] split[S] empty[S] acc_full[NACC2] acc_empty[NACC2]; then the TMEM address slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tilesN = (N + BN2 - 1) / BN2, tilesM = (M + BM2 - 1) / BM2;
+  const int ntiles = tilesN * tilesM * nsplit;
+  const int nkb_total = (K + BK - 1) / BK;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full_bar = [&](int s) { return bar0 + 8 * s; };
+  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES2 + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES2 + s); };
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES2 + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES2 + NACC2 + b); };
+  auto tileA = [&](int s, int lo) { return sbase + s * STAGE2 + lo * TILE; };
+  auto tileB = [&](int s, int lo) { return sbase + s * STAGE2 + (2 + lo) * TILE; };
+  struct Tile {
+    int m0, n0, z, kb0, nkb;
+  };
+  auto decode = [&](int t) {
+    Tile r;
+    const int nt = t % tilesN, q = t / tilesN;
+    r.n0 = nt * BN2;
+    r.m0 = (q % tilesM) * BM2;
+    r.z = q / tilesM;
+    r.kb0 = r.z * kb_per_split;
+    r.nkb = max(0, min(nkb_total, r.kb0 + kb_per_split) - r.kb0);
+    return r;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(split_bar(s), 2 * SPLITW);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int b = 0; b < NACC2; ++b) {
+      mbar_init(acc_full(b), 1);
+      mbar_init(acc_empty(b), 2 * EPIW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (BLO) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NACC2 * BN2)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own 128 rows of A, own half of B)
+    if (lane == 0) {
+      int it = 0;
+      for (int t = pair_id; t < ntiles; t += npairs) {
+        const Tile T = decode(t);
+        const int am = T.m0 + (int)rank * BM, bn = T.n0 + (int)rank * BNH;
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES2;
+          const uint32_t ph = (it / STAGES2) & 1;
+          mbar_wait(empty_bar(s), ph ^ 1);
+          mbar_expect_tx(full_bar(s), (BLO ? 3 : 2) * TILE);
+          const int k0 = (T.kb0 + i) * BK;
+          if (AMAJ == 0) {
+            tma_load_2d(tileA(s, 0), &tmA, full_bar(s), k0, am);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c) tma_load_2d(tileA(s, 0) + c * 4096, &tmA, full_bar(s), am + 32 * c, k0);
+          }
+          if (BMAJ == 0) {
+            tma_load_2d(tileB(s, 0), &tmB, full_bar(s), k0, bn);
+            if (BLO) tma_load_2d(tileB(s, 1), &tmBl, full_bar(s), k0, bn);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BNH / 32; ++c) tma_load_2d(tileB(s, 0) + c * 4096, &tmB, full_bar(s), bn + 32 * c, k0);
+            if (BLO) {
+#pragma unroll
+              for (int c = 0; c < BNH / 32; ++c)
+                tma_load_2d(tileB(s, 1) + c * 4096, &tmBl, full_bar(s), bn + 32 * c, k0);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA, one thread)
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
+                           ((uint32_t)(BN2 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
+    if (leader && lane == 0) {
+      int it = 0, g = 0, buf = 0;
+      for (int t = pair_id; t < ntiles; t += npairs) {
+        const Tile T = decode(t);
+        for (int i = 0; i < T.nkb; ++i, ++it) {
+          const int s = it % STAGES2;
+          const uint32_t ph = (it / STAGES2) & 1;
+          const bool first = (i % promote) == 0;
+          if (first) {
+            buf = g % NACC2;
+            const int u = g / NACC2;
+            if (u >= 1) mbar_wait(acc_empty(buf), (u - 1) & 1);
+          }
+          mbar_wait(split_bar(s), ph);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(buf * BN2);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
+            const uint64_t bh = operand_desc<BMAJ>(tileB(s, 0), kk);
+            mma2_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+            mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+            mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+          }
+          commit2(empty_bar(s));
+          if ((i % promote) == promote - 1 || i == T.nkb - 1) {
+            commit2(acc_full(buf));
+            ++g;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 2 + SPLITW) {
+    // ---------------- 3xTF32 operand split (both CTAs), then arrive on the leader
+    const int et = threadIdx.x - 64;  // 0..63
+    int it = 0;
+    for (int t = pair_id; t < ntiles; t += npairs) {
+      const Tile T = decode(t);
+      for (int i = 0; i < T.nkb; ++i, ++it) {
+        const int s = it % STAGES2;
+        const uint32_t ph = (it / STAGES2) & 1;
+        mbar_wait(full_bar(s), ph);
+        uint8_t* st = smem + s * STAGE2;
+        const float4* ahi = reinterpret_cast<const float4*>(st);
+        float4* alo = reinterpret_cast<float4*>(st + TILE);
+        const float4* bhi = reinterpret_cast<const float4*>(st + 2 * TILE);
+        float4* blo = reinterpret_cast<float4*>(st + 3 * TILE);
+#pragma unroll 4
+        for (int q = et; q < TILE / 16; q += 32 * SPLITW) {
+          alo[q] = lo_tf32(ahi[q]);
+          if (!BLO) blo[q] = lo_tf32(bhi[q]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) arrive_remote(to_rank(split_bar(s), 0));
+      }
+    }
+  } else {
+    // ---------------- accumulator promotion + epilogue (both CTAs: own 128 rows;
+    // warp w: TMEM lanes 32 (w % 4) .., columns 128 ((w - 4) / 4) ..)
+    const int lq = warp & 3, half = (warp - 4) >> 2;
+    const int lane_base = 32 * lq;
+    float* stg = stg_all + (warp - 4) * 32 * SLD;
+    int g = 0;
+    for (int t = pair_id; t < ntiles; t += npairs) {
+      const Tile T = decode(t);
+      const int ngroups = (T.nkb + promote - 1) / promote;
+      const int mrow0 = T.m0 + (int)rank * BM + lane_base;
+      const int ncol0 = T.n0 + half * BNH;
+      {  // second epilogue operand of this thread's row -> L2
+        const int m = mrow0 + lane;
+        if (m < M && ncol0 < N) epi.prefetch_row(m, ncol0, min(BNH, N - ncol0));
+      }
+      float sums[BNH];
+#pragma unroll
+      for (int j = 0; j < BNH; ++j) sums[j] = 0.f;
+      for (int q = 0; q < ngroups; ++q, ++g) {
+        const int buf = g % NACC2;
+        mbar_wait(acc_full(buf), (g / NACC2) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < BNH / 32; ++cc) {
+          uint32_t r[32];
+          const uint32_t taddr =
+              tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN2 + half * BNH + cc * 32);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sums[cc * 32 + j] += __uint_as_float(r[j]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
+      }
+      // epilogue: transpose 32 x 16 blocks through shared memory so each warp
+      // store covers 8 rows x 64 contiguous bytes (float4 per lane)
+      const int rr = lane >> 2, c4 = (lane & 3) * 4;
+#pragma unroll
+      for (int cb = 0; cb < BNH / 16; ++cb) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<float4*>(stg + lane * SLD + 4 * q) =
+              make_float4(sums[cb * 16 + 4 * q], sums[cb * 16 + 4 * q + 1], sums[cb * 16 + 4 * q + 2],
+                          sums[cb * 16 + 4 * q + 3]);
+        __syncwarp();
+        const int n = ncol0 + cb * 16 + c4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = 8 * k + rr;
+          const int m = mrow0 + r;
+          const float4 v = *reinterpret_cast<const float4*>(stg + r * SLD + c4);
+          if (m < M && n < N) epi.vec4(m, n, v, T.z);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with TMEM and with remote arrivals
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(NACC2 * BN2) : "memory");
+  }
+}
+}  // namespace p2
+
 // ------------------------------------------------------------- host side
 inline PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 inline std::once_flag g_encode_once;
@@ -565,11 +871,77 @@ inline bool usable(int M, int N, int K, const float* A, int lda, const float* B,
 
 // Blo (optional, 3xTF32): B's lo part (x - trunc_tf32(x)) in global memory with
 // B's layout, e.g. a weight's copy made once per minibatch (BLO kernel variant).
+// Tile geometry of a launch: 3xTF32 GEMMs with M >= 256 and N > 128 run on
+// CTA pairs with 256 x 256 tiles (p2::tc_gemm2_kernel, one work unit per TPC),
+// the rest on single CTAs with 128 x 128 tiles.
+struct Geo {
+  int bm, bn, units;
+  bool pair;
+};
+inline Geo geo(const Ctx* c, int M, int N) {
+  if (c->precision == 0 && M >= p2::BM2 && N > BN && env_int("VER_TC_PAIR", 1))
+    return Geo{p2::BM2, p2::BN2, c->num_sms / 2, true};
+  return Geo{BM, BN, c->num_sms, false};
+}
+
+template <int AMAJ, int BMAJ, class Epi>
+void launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
+                 int splits, const float* Blo) {
+  // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32, swizzled: the
+  // MMA reads A from shared memory here); B: its 128-column halves
+  const CUtensorMap ta = AMAJ == 0 ? make_map(A, M, K, lda, BM, false) : make_map(A, K, M, lda, 32, true);
+  const CUtensorMap tb = BMAJ == 0 ? make_map(B, N, K, ldb, p2::BNH, false) : make_map(B, K, N, ldb, 32, true);
+  const bool blo = Blo && env_int("VER_TC_BLO", 1) && al16(Blo);
+  const CUtensorMap tbl =
+      !blo ? tb : (BMAJ == 0 ? make_map(Blo, N, K, ldb, p2::BNH, false) : make_map(Blo, K, N, ldb, 32, true));
+  const int nkb = (K + BK - 1) / BK;
+  splits = std::max(1, std::min(splits, nkb));
+  const int per = (nkb + splits - 1) / splits;
+  splits = (nkb + per - 1) / per;
+  const long long ntiles = cdiv(N, p2::BN2) * cdiv(M, p2::BM2) * (long long)splits;
+  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  auto run = [&](auto kern) {
+    VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p2::SMEM2));
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(p2::THREADS2);
+    cfg.dynamicSmemBytes = p2::SMEM2;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    // persistent: as many pairs as can be resident at once (one per TPC)
+    static std::atomic<int> pairs_cache[kMaxDevices];
+    int pairs = pairs_cache[dev_slot(c)].load();
+    if (!pairs) {
+      cfg.gridDim = dim3(c->num_sms);
+      int nc = 0;
+      VER_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+      pairs = std::max(1, std::min(nc, c->num_sms / 2));
+      pairs_cache[dev_slot(c)].store(pairs);
+    }
+    cfg.gridDim = dim3(2 * (int)std::min<long long>(ntiles, pairs));
+    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote));
+    after_launch(c);
+  };
+  if (blo) run(p2::tc_gemm2_kernel<AMAJ, BMAJ, Epi, 1>);
+  else run(p2::tc_gemm2_kernel<AMAJ, BMAJ, Epi, 0>);
+}
+
 template <int AMAJ, int BMAJ, class Epi>
 void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi, int splits,
             const float* Blo = nullptr) {
   ScopedEv ev(c, c->gemm_tag);  // learner timing of the GEMM family (bench roofline)
   if (c->evlog && c->flop_log && c->gemm_tag >= 0) c->flop_log[c->gemm_tag] += 2.0 * M * (double)N * K;
+  if (geo(c, M, N).pair) {
+    launch_pair<AMAJ, BMAJ>(c, M, N, K, A, lda, B, ldb, epi, splits, Blo);
+    return;
+  }
   // A: K-major M x K (box 32 x 128) or MN-major K x M (box 32 x 32; unswizzled when
   // the split warps move it into tensor memory)
   const bool atm = c->precision == 0 && env_int("VER_TC_ATM", 1) && (AMAJ == 0 || env_int("VER_TC_ATM_MN", 1));
@@ -624,13 +996,14 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
 // each; pick the cheapest Z (ties: fewer partials), >= 4 K-blocks per split.
 // (Z = ceil(2 SMs / tiles) gave 2.3 waves for the 48-tile weight gradients.)
 inline int splits_for(const Ctx* c, int M, int N, int K) {
-  const long long tiles = cdiv(N, BN) * cdiv(M, BM);
+  const Geo g = geo(c, M, N);
+  const long long tiles = cdiv(N, g.bn) * cdiv(M, g.bm);
   const int nkb = (K + BK - 1) / BK;
   const int zmax = std::max(1, std::min(64, nkb / 4));
   int best = 1;
   double best_cost = 1e300;
   for (int z = 1; z <= zmax; ++z) {
-    const long long waves = (tiles * z + c->num_sms - 1) / c->num_sms;
+    const long long waves = (tiles * z + g.units - 1) / g.units;
     // + ~6 K-blocks' worth of per-item overhead (pipeline fill, accumulator
     // drain, 64 KB partial-tile store)
     const double cost = (double)waves * (double)((nkb + z - 1) / z + 6);
