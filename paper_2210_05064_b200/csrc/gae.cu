@@ -463,14 +463,12 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   if (F <= 0) return;
   const int ntiles = (F + kGaeTile - 1) / kGaeTile;
   DBuf<GaeTileState> tiles;
-  DBuf<int> misc;
+  DBuf<int> misc;  // [0] tile counter, [1] lowest env with a missing bootstrap
   tiles.reserve(c, ntiles);
   misc.reserve(c, 2);
   tiles.zero(ntiles);
-  int* h = static_cast<int*>(c->pinned_buf(2 * sizeof(int)));
-  h[0] = 0;
-  h[1] = 0x7fffffff;
-  misc.upload(h, 2);
+  VER_CUDA(cudaMemsetAsync(misc.p, 0, sizeof(int), c->stream));
+  VER_CUDA(cudaMemsetAsync(misc.p + 1, 0x7f, sizeof(int), c->stream));  // 0x7f7f7f7f: none
   const int smem = kGaeStages * kGaeStageBytes;
   static std::atomic<int> per_sm_cache[kMaxDevices];  // per device (0 = not probed yet)
   int per_sm = per_sm_cache[dev_slot(c)].load();
@@ -484,9 +482,10 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   gae_scan_kernel<<<grid, kGaeBlock, smem, c->stream>>>(r, v, d, env, F, boot, valid, off, N, gamma, lambda, adv, ret,
                                                        tiles.p, misc.p, misc.p + 1);
   after_launch(c);
+  int* h = static_cast<int*>(c->pinned_buf(2 * sizeof(int)));
   misc.download(h, 2);
   sync(c);
-  if (h[1] != 0x7fffffff)
+  if (h[1] != 0x7f7f7f7f)
     protocol_error("compute_gae: missing bootstrap value for env " + std::to_string(h[1]));
 }
 

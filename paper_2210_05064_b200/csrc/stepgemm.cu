@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   }
   tc_fence_before();
   cluster_sync_all();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   unsigned target = 0;

@@ -647,6 +647,7 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
   }
   tc_fence_before();
   cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+  __syncthreads();     // (the same, as a CTA barrier: the TMEM address slot in shared memory)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   asm volatile("griddepcontrol.wait;" ::: "memory");
