@@ -13,11 +13,11 @@ for line in open(sys.argv[1]):
     for x in rest:
         v = list(map(int, x.split(":")))
         rows, z, pts = v[0], v[1], v[2:]
-        b = (tag, min(rows // 100 * 100, 600), z)
+        b = (tag, min(rows // 100 * 100, 600) if rows < 1000 else min(rows // 1000 * 1000, 12000), z)
         for k, p in enumerate(pts):
             if p >= 0:
                 acc[b][(FUSED if tag.startswith("fused") else NAMES)[k]].append(p / 1000.0)
 for b in sorted(acc):
     d = acc[b]
-    print(f"{b[0]} rows~{b[1]:>3} Z={b[2]} n={len(d['next']):>4} " +
+    print(f"{b[0]} rows~{b[1]:>5} Z={b[2]} n={len(d['next']):>4} " +
           " ".join(f"{k}={sum(v) / len(v):.2f}" for k, v in d.items() if v))
