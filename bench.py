@@ -322,13 +322,16 @@ def run_ours(args, rank, world):
         S5 = 1 << args.c5_log2
         lens = synth.ragged_lengths(S5, seed=11)
         v5 = V.view_synth(lens, obs_dim=D_, hidden_dim=4, seed=12, ctx=ctx)
-        gae_ms, gat_ms = V.bench_gae_gather(v5, B=MINIBATCHES, seed=13, reps=5)
+        gae_call, gat_call, gae_ms, gat_ms = V.bench_gae_gather(v5, B=MINIBATCHES, seed=13, reps=10, kernels=True)
         hbm_, _, _, pk = load_peaks()
         gae_b = 17.0 * S5 + 9.0 * len(lens)          # r, V, done in; A, R out; + bootstrap/valid/offset per env
         gat_b = (8.0 * D_ + 36.0) * S5               # obs, act, old log-prob, A, R in + out, slot out
-        gg = {"steps": S5, "envs": int(len(lens)), "gae_ms": gae_ms, "gather_ms": gat_ms,
+        gg = {"steps": S5, "envs": int(len(lens)),
+              "gae_ms": gae_ms, "gather_ms": gat_ms, "timing": "CUDA events around the kernel launches",
+              "gae_call_ms": gae_call, "gather_call_ms": gat_call,
               "gae_gbs": gae_b / gae_ms / 1e6, "gather_gbs": gat_b / gat_ms / 1e6,
               "gae_gather_gbs": (gae_b + gat_b) / (gae_ms + gat_ms) / 1e6,
+              "gae_frac": gae_b / gae_ms / 1e6 / hbm_, "gather_frac": gat_b / gat_ms / 1e6 / hbm_,
               "frac_of_peak": (gae_b + gat_b) / (gae_ms + gat_ms) / 1e6 / hbm_, "peak_gbs": hbm_,
               "peak_kind": pk,
               "bytes_per_step": {"gae": 17, "gather": 8 * D_ + 36}}

@@ -407,7 +407,10 @@ ver_status ver_learner_last_flop(ver_learner l, double* flop, int* n);
 
 /* Measurement: device time (CUDA events, averaged over reps) of compute_gae on
    v and of the time-major gather of all B minibatches of one
-   split_minibatches(v, B, seed) deal.  ms_out[0] = GAE, ms_out[1] = gather. */
+   split_minibatches(v, B, seed) deal.  ms_out[0] = GAE call (scan kernel, its
+   counter resets and the missing-bootstrap check), ms_out[1] = gather launches;
+   ms_out[2] / ms_out[3] = the GAE scan kernel / the gather kernels alone
+   (events around the launches).  ms_out holds 4 floats. */
 ver_status ver_bench_gae_gather(ver_view v, double gamma, double lambda, int B, uint64_t seed, int reps,
                                 float* ms_out);
 

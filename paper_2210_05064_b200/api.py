@@ -388,10 +388,14 @@ def view_synth(lengths, obs_dim: int = 2, hidden_dim: int = 4, seed: int = 1, p_
 
 
 def bench_gae_gather(view: RolloutView, B: int = 2, seed: int = 1, reps: int = 5, gamma: float = 0.99,
-                     lam: float = 0.95) -> tuple[float, float]:
-    """(GAE ms, gather ms for all B minibatches), CUDA-event timed."""
-    ms = (C.c_float * 2)()
+                     lam: float = 0.95, kernels: bool = False) -> tuple:
+    """(GAE ms, gather ms for all B minibatches), CUDA-event timed around the
+    calls; with kernels=True also (GAE scan kernel ms, gather kernels ms), timed
+    around the launches alone."""
+    ms = (C.c_float * 4)()
     _check(_lib().ver_bench_gae_gather(view.h, gamma, lam, B, seed, reps, ms))
+    if kernels:
+        return float(ms[0]), float(ms[1]), float(ms[2]), float(ms[3])
     return float(ms[0]), float(ms[1])
 
 

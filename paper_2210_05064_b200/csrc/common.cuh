@@ -72,6 +72,7 @@ struct Ctx {
   int rec_tag = -1;  // tag for recurrence launches (>= 0 while a learner minibatch is timed)
   int gemm_tag = -1;  // tag for tcgen05 GEMM launches (same)
   double* flop_log = nullptr;  // per-tag algorithmic FLOPs (2 M N K) of the tagged GEMM launches
+  int hbm_tag = -1;  // tag for the GAE scan (tag) and gather (tag + 1) launches (ver_bench_gae_gather)
   // pinned scratch for small synchronous reads
   void* pinned = nullptr;
   size_t pinned_bytes = 0;

@@ -13,11 +13,29 @@
 // and compositions are fp64 (the kernel is HBM-bound; fp64 is free here) so
 // 1024-step segments stay inside fp32 rounding of the fp64 reference.
 //
-// One pass, decoupled look-back: each CTA claims tiles from the END of the
-// array (dynamic tile id), composes its 2048 maps, publishes the aggregate,
-// looks back only until it meets a tile whose map has a = 0 (any done/env
-// tail inside) or an inclusive value.  HBM traffic: r, V (4+4 B), done (1 B)
-// read once, A, R (4+4 B) written once = 17 B/step, plus offsets per env.
+// Two launches.  (1) gae_boot_kernel, one thread per env: the bootstrap of
+// every env tail that is not done is written into adv[tail] (adv is output
+// only, so it is free scratch until the scan overwrites it), missing ones are
+// reported.  (2) gae_scan_kernel: one pass over 512-slot WARP tiles, no block
+// barrier and (in practice) no inter-tile waiting.  A warp claims tiles from
+// the END of the array (dynamic tile ids) and keeps the next tile in flight in
+// a per-warp ring of bulk copies.  Each tile also reads a 128-slot HALO above
+// it (r, V, done of the next tile's bottom, which that tile's warp has just
+// fetched, so the halo is mostly an L2 hit).  A reset (env tail or done,
+// a_i = 0) inside the halo makes the carry A_hi local: the halo's composed
+// map is a constant.  Only when the halo has no reset does the tile wait for
+// the value A_lo(t-1) = A_hi(t) the tile above publishes; a tile publishes
+// exactly when its own bottom 128 slots have no reset, i.e. exactly when the
+// tile below will ask.  With heavy-tailed segments (C5: a reset every ~30
+// slots) that practically never happens, so the scan streams.
+// Per tile: lane l owns 8 consecutive slots of each of the two 256-slot rows
+// (+ 4 halo slots): per-item maps and the lane composite sequentially in
+// fp32, then one fp64 warp suffix scan per row (the lane composite's discount
+// is the exact fp64 (gamma lambda)^8), rows / halo / carry composed in fp64,
+// then every slot is written once (float4 stores).
+// HBM traffic: r, V (4+4 B), done (1 B) read once, A, R (4+4 B) written once
+// = 17 B/step (the halo re-read is an L2 hit), plus 17 B per env tail for
+// the bootstrap pass.
 //
 // Views whose fresh slots are not env-major contiguous (arbitrary uploads,
 // e.g. make_view fixtures with env = seq % N) first stable-sort the fresh
@@ -30,43 +48,24 @@
 
 namespace verg {
 
-constexpr int kGaeThreads = 256;                     // compute threads (8 warps)
-constexpr int kGaeItems = 8;
-constexpr int kGaeTile = kGaeThreads * kGaeItems;  // 2048 slots per tile
-constexpr int kGaeWarps = kGaeThreads / 32;
-constexpr int kGaeBlock = kGaeThreads + 64;          // + producer warp + look-back / fix-up warp
-constexpr int kGaeStages = 3;                        // tiles in flight per CTA
-constexpr int kGaeWin = 128;                         // env window staged per tile
-// stage layout (bytes): V [tile + 4] | r [tile] | done [tile] | boot [win] | valid [win] | off [win + 4]
-constexpr int kGaeOffR = 4 * kGaeTile + 16;
-constexpr int kGaeOffD = kGaeOffR + 4 * kGaeTile;
-constexpr int kGaeOffB = kGaeOffD + kGaeTile;
-constexpr int kGaeOffBV = kGaeOffB + 4 * kGaeWin;
-constexpr int kGaeOffO = kGaeOffBV + kGaeWin;
-constexpr int kGaeStageBytes = kGaeOffO + 4 * (kGaeWin + 4);
-
-struct Affine {
-  double a, b;  // x -> b + a x
-};
-// x earlier (lower index), y later: A_x = b_x + a_x (b_y + a_y X)
-__device__ __forceinline__ Affine compose(Affine x, Affine y) {
-  return Affine{x.a * y.a, fma(x.a, y.b, x.b)};
-}
+constexpr int kGItems = 8;                 // consecutive slots per lane and row
+constexpr int kGRow = 32 * kGItems;        // 256 slots
+constexpr int kGTile = 2 * kGRow;          // 512 slots
+constexpr int kGHalo = 128;                // 4 slots per lane
+constexpr int kGSpan = kGTile + kGHalo;
+constexpr int kGWarps = 8;                 // warps per CTA
+constexpr int kGStages = 2;                // tiles in flight per warp
+constexpr int kGClaim = 4;                 // tiles per tile-counter atomic (consecutive, processed in order)
+// stage layout (bytes): V [span + 4] | r [span] | done [span]
+constexpr int kGOffR = 4 * kGSpan + 16;
+constexpr int kGOffD = kGOffR + 4 * kGSpan;
+constexpr int kGStageBytes = (kGOffD + kGSpan + 127) & ~127;
+constexpr int kGSmem = kGWarps * kGStages * kGStageBytes;
 
 struct GaeTileState {
-  double a, b, inc;
-  int flag;  // 0 none, 1 aggregate (a,b), 2 inclusive (inc = A at tile start)
+  double inc;  // A at the tile's first slot (published only when its bottom 128 slots have no reset)
+  int flag;    // 0 not yet, 2 published
   int pad;
-};
-
-struct GaeStageHdr {
-  int tid;         // claimed tile id (-1: no more tiles)
-  int e0;          // env of the tile's first slot = env of its first tail
-  int wbase;       // first env of the staged window (16-aligned)
-  int nb, nv, no;  // boot / valid / off entries staged from wbase
-  int seg;         // first slot of the carry-dependent top segment (compute warps: atomicMin)
-  int pad;
-  double sa, sb;   // tile aggregate
 };
 
 __device__ __forceinline__ uint32_t gsm(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -84,11 +83,8 @@ __device__ __forceinline__ void gae_wait(uint32_t a, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void gae_arrive(uint32_t a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-// tile-state flag protocol: payload stores, then a release store of the flag;
-// readers acquire-load the flag before reading the payload
+// tile-state flag protocol: payload store, then a release store of the flag;
+// the reader acquire-loads the flag before reading the payload
 __device__ __forceinline__ void flag_release(volatile int* f, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
 }
@@ -97,329 +93,272 @@ __device__ __forceinline__ int flag_acquire(volatile int* f) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
   return v;
 }
-__device__ __forceinline__ void gae_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kGaeThreads) : "memory"); }
 
-// Persistent CTAs, decoupled look-back, warp-specialised, 3-deep ring.
-//  * Producer warp: claims tiles (dynamic ids from the END of the array:
-//    carries flow downwards), reads env_of at the tile's first slot and
-//    bulk-copies r, V (+ the next tile's first 4 V), done and a window of the
-//    envs' bootstrap values / flags / offsets into the ring.
-//  * 8 compute warps (thread t: 8 consecutive slots): env tails (done bit 1)
-//    are numbered by a block-wide count (tail -> env from the staged offsets,
-//    no dependent DRAM loads); per-item affine maps, block suffix scan, the
-//    tile aggregate is published at once (flag 1), and every slot whose value
-//    does not depend on the carry (all slots below the tile's last reset) is
-//    stored.  The carry-dependent top segment's partial values (carry = 0) go
-//    to shared memory.  The compute warps never wait for a look-back, so an
-//    aggregate is never held back behind another tile's look-back.
-//  * Fix-up warp: looks back (terminates at the first predecessor with a
-//    reset, or an inclusive value), publishes this tile's inclusive value and
-//    patches the top segment: A_i = A_i(0) + (gamma lambda)^(hi - i) carry.
-// A CTA processes its tiles in claim order and all CTAs are resident, so every
-// aggregate a look-back waits on is published without further waiting.
-// Per-thread recursions are fp32 over <= 8 items; compositions and carries
-// are fp64.  The single partial tile at the end is read from global memory.
-__global__ void __launch_bounds__(kGaeBlock) gae_scan_kernel(
+// learner.cpp:23-27 at env tails: V_next = bootstrap[e] unless done (ProtocolError
+// when it was never set).  One thread per env, the value parked in adv[tail].
+__global__ void gae_boot_kernel(const int32_t* __restrict__ off, const uint8_t* __restrict__ done,
+                                const float* __restrict__ boot, const uint8_t* __restrict__ valid, int N,
+                                float* __restrict__ adv, int* __restrict__ err_env) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N) return;
+  const int o0 = off[e], o1 = off[e + 1];
+  if (o1 <= o0 || (done[o1 - 1] & 1)) return;
+  if (!valid[e]) atomicMin(err_env, e);
+  adv[o1 - 1] = boot[e];
+}
+
+// Lane composite of n items: x -> b + a x, a = (gamma lambda)^n in fp64 or 0 (a
+// reset among the items).  Scan operator: x earlier (lower index), y later.
+// fp64 across lanes: a 256-slot row's partial sums reach O(30) at gamma lambda
+// near 1, and fp32 roundings of those would cost ~1e-5 of a small A_i.
+struct Aff {
+  double a, b;
+};
+__device__ __forceinline__ Aff compose(Aff x, Aff y) { return Aff{x.a * y.a, fma(x.a, y.b, x.b)}; }
+__device__ __forceinline__ Aff shfl_down_aff(Aff x, int o) {
+  return Aff{__shfl_down_sync(0xffffffffu, x.a, o), __shfl_down_sync(0xffffffffu, x.b, o)};
+}
+__device__ __forceinline__ Aff shfl_aff(Aff x, int src) {
+  return Aff{__shfl_sync(0xffffffffu, x.a, src), __shfl_sync(0xffffffffu, x.b, src)};
+}
+__device__ __forceinline__ Aff warp_suffix(Aff v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Aff y = shfl_down_aff(v, o);
+    if (lane + o < 32) v = compose(v, y);
+  }
+  return v;
+}
+
+// Persistent CTAs of 8 independent warps.  Progress: a tile only ever waits
+// for a lower-numbered (earlier-claimed) tile, and a warp processes its claims
+// in order, so the lowest unfinished tile is always at the head of some
+// warp's ring and never waits.
+__global__ void __launch_bounds__(32 * kGWarps) gae_scan_kernel(
     const float* __restrict__ reward, const float* __restrict__ value, const uint8_t* __restrict__ done,
-    const int32_t* __restrict__ env_of, int F, const float* __restrict__ boot,
-    const uint8_t* __restrict__ boot_valid, const int32_t* __restrict__ off, int N, double gamma, double lambda,
-    float* __restrict__ adv, float* __restrict__ ret, volatile GaeTileState* tiles, int* tile_counter,
-    int* err_env) {
+    const int32_t* __restrict__ env_of, const int32_t* __restrict__ off, const float* __restrict__ boot, int F,
+    double gamma, double lambda, float* __restrict__ adv, float* __restrict__ ret, volatile GaeTileState* tiles,
+    int* tile_counter) {
   extern __shared__ __align__(128) uint8_t gsmem[];
-  __shared__ uint64_t s_full[kGaeStages], s_ready[kGaeStages], s_empty[kGaeStages];
-  __shared__ GaeStageHdr s_hdr[kGaeStages];
-  __shared__ Affine s_warp[kGaeWarps];
-  __shared__ int s_cnt[kGaeWarps];
-  const int ntiles = (F + kGaeTile - 1) / kGaeTile;
+  __shared__ uint64_t s_full[kGWarps][kGStages];
+  const int ntiles = (F + kGTile - 1) / kGTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float glf = (float)(gamma * lambda);
-  auto stage = [&](int s) { return gsmem + s * kGaeStageBytes; };
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kGaeStages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gsm(&s_full[s])) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(gsm(&s_ready[s])), "r"(kGaeWarps) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gsm(&s_empty[s])) : "memory");
-    }
+  const float gf = (float)gamma, glf = (float)(gamma * lambda);
+  const double gld = gamma * lambda, gl2 = gld * gld, gl4 = gl2 * gl2, gl8 = gl4 * gl4;  // lane discounts
+  uint8_t* wsm = gsmem + warp * kGStages * kGStageBytes;
+  if (lane == 0) {
+    for (int s = 0; s < kGStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(gsm(&s_full[warp][s])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-
-  if (warp == kGaeWarps) {
-    // ------------------------------------------------------------ producer
+  __syncwarp();
+  // claim the next tile and (lane 0) start its bulk copies into stage s when the
+  // whole span (+ 4 V) lies below F; otherwise the lanes fill the stage from
+  // global memory at processing time (the top tile or two)
+  int c_next = 0, c_left = 0;  // lane 0: tiles left of the last counter claim
+  auto claim = [&](int s, int& eh) -> int {
+    int t = 0;
     if (lane == 0) {
-      for (int k = 0;; ++k) {
-        const int s = k % kGaeStages;
-        gae_wait(gsm(&s_empty[s]), ((k / kGaeStages) & 1) ^ 1);
-        const uint32_t mb = gsm(&s_full[s]);
-        const int tid = atomicAdd(tile_counter, 1);
-        GaeStageHdr h{};
-        h.tid = -1;
-        if (tid >= ntiles) {
-          s_hdr[s] = h;
-          gae_arrive(mb);
-          break;
-        }
-        const int lo = (ntiles - 1 - tid) * kGaeTile;
-        h.tid = tid;
-        h.e0 = env_of[lo];
-        h.seg = 0x7fffffff;
-        if (lo + kGaeTile > F) {  // partial tile: the compute threads read global memory
-          s_hdr[s] = h;
-          gae_arrive(mb);
-          continue;
-        }
-        h.wbase = h.e0 & ~15;
-        h.nb = max(0, min(kGaeWin, N - h.wbase)) & ~3;
-        h.nv = max(0, min(kGaeWin, N - h.wbase)) & ~15;
-        h.no = max(0, min(kGaeWin + 4, N + 1 - h.wbase)) & ~3;
-        s_hdr[s] = h;
-        const uint32_t vb = 4 * kGaeTile + (lo + kGaeTile + 4 <= F ? 16 : 0);  // + V of the slots above
-        const uint32_t bytes = vb + 5 * kGaeTile + 4 * h.nb + h.nv + 4 * h.no;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
-        uint8_t* st = stage(s);
-        gae_bulk(gsm(st), value + lo, vb, mb);
-        gae_bulk(gsm(st + kGaeOffR), reward + lo, 4 * kGaeTile, mb);
-        gae_bulk(gsm(st + kGaeOffD), done + lo, kGaeTile, mb);
-        if (h.nb) gae_bulk(gsm(st + kGaeOffB), boot + h.wbase, 4 * h.nb, mb);
-        if (h.nv) gae_bulk(gsm(st + kGaeOffBV), boot_valid + h.wbase, h.nv, mb);
-        if (h.no) gae_bulk(gsm(st + kGaeOffO), off + h.wbase, 4 * h.no, mb);
+      if (c_left == 0) {
+        c_next = atomicAdd(tile_counter, kGClaim);
+        c_left = kGClaim;
+      }
+      t = c_next++;
+      --c_left;
+      const uint32_t mb = gsm(&s_full[warp][s]);
+      const int lo = (ntiles - 1 - t) * kGTile;
+      if (t < ntiles && lo + kGTile < F) eh = env_of[lo + kGTile];  // env of the halo's first slot
+      if (t < ntiles && lo + kGSpan + 4 <= F) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(9 * kGSpan + 16)
+                     : "memory");
+        uint8_t* st = wsm + s * kGStageBytes;
+        gae_bulk(gsm(st), value + lo, 4 * kGSpan + 16, mb);
+        gae_bulk(gsm(st + kGOffR), reward + lo, 4 * kGSpan, mb);
+        gae_bulk(gsm(st + kGOffD), done + lo, kGSpan, mb);
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mb) : "memory");
       }
     }
-    return;
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  int tq[kGStages], eq[kGStages];
+#pragma unroll
+  for (int s = 0; s < kGStages; ++s) {
+    eq[s] = 0;
+    tq[s] = claim(s, eq[s]);
   }
 
-  if (warp == kGaeWarps + 1) {
-    // ------------------------------------------------- look-back + fix-up
-    for (int it = 0;; ++it) {
-      const int s = it % kGaeStages;
-      gae_wait(gsm(&s_full[s]), (it / kGaeStages) & 1);
-      if (s_hdr[s].tid < 0) break;
-      gae_wait(gsm(&s_ready[s]), (it / kGaeStages) & 1);
-      const GaeStageHdr hd = s_hdr[s];
-      const int tid = hd.tid;
-      const int lo = (ntiles - 1 - tid) * kGaeTile, hi = min(F, lo + kGaeTile);
-      double carry = 0.0;  // A at hi
-      if (lane == 0 && tid != 0) {
-        Affine acc{1.0, 0.0};
-        int p = tid - 1;
-        for (;;) {
-          int f;
-          do {
-            f = flag_acquire(&tiles[p].flag);
-          } while (f == 0);
-          if (f == 2) {
-            carry = fma(acc.a, tiles[p].inc, acc.b);
-            break;
-          }
-          acc = compose(acc, Affine{tiles[p].a, tiles[p].b});
-          if (acc.a == 0.0 || p == 0) {
-            carry = acc.b;
-            break;
-          }
-          --p;
+  for (int it = 0;; ++it) {
+    const int s = it % kGStages;
+    int tid = tq[0], eh = eq[0];
+#pragma unroll
+    for (int q = 1; q < kGStages; ++q)
+      if (s == q) tid = tq[q], eh = eq[q];
+    if (tid >= ntiles) break;
+    eh = __shfl_sync(0xffffffffu, eh, 0);
+    gae_wait(gsm(&s_full[warp][s]), (it / kGStages) & 1);
+    const int lo = (ntiles - 1 - tid) * kGTile;
+    const int hi = min(F, lo + kGTile);
+    uint8_t* st = wsm + s * kGStageBytes;
+    float* sv = reinterpret_cast<float*>(st);
+    float* sr = reinterpret_cast<float*>(st + kGOffR);
+    uint8_t* sd = st + kGOffD;
+    if (lo + kGSpan + 4 > F) {  // not bulk-copied: fill from global, inert (tail + done) beyond F
+      for (int j = lane; j < kGSpan + 4; j += 32) {
+        const int i = lo + j;
+        sv[j] = i < F ? value[i] : 0.f;
+        if (j < kGSpan) {
+          sr[j] = i < F ? reward[i] : 0.f;
+          sd[j] = i < F ? done[i] : 3;
         }
-        tiles[tid].inc = fma(hd.sa, carry, hd.sb);
-        flag_release(&tiles[tid].flag, 2);
-      }
-      carry = __shfl_sync(0xffffffffu, carry, 0);
-      // top segment [seg, hi): partial values (carry 0) staged by the compute warps
-      const float* pa = reinterpret_cast<const float*>(stage(s) + kGaeOffR);
-      const float* pr = reinterpret_cast<const float*>(stage(s));
-      const int seg = max(lo, min(hd.seg, hi));
-      const double lg2 = log2((double)glf);
-      for (int i = seg + lane; i < hi; i += 32) {
-        // (gamma lambda)^(hi - i): the top segment has no reset, every a_i = gamma lambda
-        const double cf = exp2(lg2 * (double)(hi - i)) * carry;
-        const float av = (float)((double)pa[i - lo] + cf);
-        adv[i] = av;
-        ret[i] = (float)((double)pr[i - lo] + cf);
       }
       __syncwarp();
-      if (lane == 0) gae_arrive(gsm(&s_empty[s]));
     }
-    return;
-  }
-
-  // -------------------------------------------------------------- compute
-  const float gf = (float)gamma;
-  for (int it = 0;; ++it) {
-    const int s = it % kGaeStages;
-    gae_wait(gsm(&s_full[s]), (it / kGaeStages) & 1);
-    const GaeStageHdr hd = s_hdr[s];
-    if (hd.tid < 0) break;
-    const int tid = hd.tid;
-    const int tile = ntiles - 1 - tid;
-    const int lo = tile * kGaeTile;
-    const int hi = min(F, lo + kGaeTile);
-    const int l0 = threadIdx.x * kGaeItems;  // tile-local first item
-    const int i0 = lo + l0;
-    uint8_t* st = stage(s);
-    float* sv = reinterpret_cast<float*>(st);
-    float* sr = reinterpret_cast<float*>(st + kGaeOffR);
-    float r[kGaeItems], v[kGaeItems + 1];
-    uint32_t dw[2];
-    const bool full = hi - lo == kGaeTile;
-    if (full) {
-      const float4* r4 = reinterpret_cast<const float4*>(sr + l0);
-      const float4* v4 = reinterpret_cast<const float4*>(sv + l0);
-      const float4 x0 = r4[0], x1 = r4[1], y0 = v4[0], y1 = v4[1];
-      const uint2 dd = *reinterpret_cast<const uint2*>(st + kGaeOffD + l0);
-      r[0] = x0.x; r[1] = x0.y; r[2] = x0.z; r[3] = x0.w;
-      r[4] = x1.x; r[5] = x1.y; r[6] = x1.z; r[7] = x1.w;
-      v[0] = y0.x; v[1] = y0.y; v[2] = y0.z; v[3] = y0.w;
-      v[4] = y1.x; v[5] = y1.y; v[6] = y1.z; v[7] = y1.w;
-      dw[0] = dd.x;
-      dw[1] = dd.y;
-      v[kGaeItems] = (l0 + kGaeItems < kGaeTile || hi + 4 <= F) ? sv[l0 + kGaeItems] : (hi < F ? value[hi] : 0.f);
-    } else {
-      dw[0] = dw[1] = 0x03030303u;  // beyond the end: tail + done (inert)
+    // ---- the two 256-slot rows: lane l owns slots 8l .. 8l+7 of each
+    float v[2][kGItems], dl[2][kGItems];
+    uint32_t dd[2][2];
+    Aff lc[2];
+    bool reset0 = false;  // a reset among this lane's row-0 slots (bytes, not the float map)
 #pragma unroll
-      for (int q = 0; q < kGaeItems; ++q) {
-        const int i = i0 + q;
-        r[q] = i < hi ? reward[i] : 0.f;
-        v[q] = i < hi ? value[i] : 0.f;
-        if (i < hi) {
-          const uint32_t sh = 8 * (q & 3);
-          dw[q >> 2] = (dw[q >> 2] & ~(0xffu << sh)) | ((uint32_t)done[i] << sh);
+    for (int k = 0; k < 2; ++k) {
+      const int j0 = kGRow * k + kGItems * lane;
+      const float4 r0 = *reinterpret_cast<const float4*>(sr + j0), r1 = *reinterpret_cast<const float4*>(sr + j0 + 4);
+      const float4 v0 = *reinterpret_cast<const float4*>(sv + j0), v1 = *reinterpret_cast<const float4*>(sv + j0 + 4);
+      const uint2 d2 = *reinterpret_cast<const uint2*>(sd + j0);
+      const float rr[kGItems] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      v[k][0] = v0.x; v[k][1] = v0.y; v[k][2] = v0.z; v[k][3] = v0.w;
+      v[k][4] = v1.x; v[k][5] = v1.y; v[k][6] = v1.z; v[k][7] = v1.w;
+      dd[k][0] = d2.x;
+      dd[k][1] = d2.y;
+      float vnext = sv[j0 + kGItems];  // the next lane's first slot (row 1 lane 31: the halo's)
+      float mb = 0.f;
+      bool reset = false;
+#pragma unroll
+      for (int q = kGItems - 1; q >= 0; --q) {
+        const uint32_t b = (dd[k][q >> 2] >> (8 * (q & 3))) & 3u;
+        float vn = vnext;
+        if (b == 2u) vn = __ldcg(adv + lo + j0 + q);  // env tail, not done: its bootstrap
+        const float mask = (b & 1u) ? 0.f : 1.f;
+        const float ac = b ? 0.f : glf;
+        dl[k][q] = fmaf(gf * vn, mask, rr[q]) - v[k][q];
+        mb = fmaf(ac, mb, dl[k][q]);
+        reset |= b != 0u;
+        vnext = v[k][q];
+      }
+      lc[k] = Aff{reset ? 0.0 : gl8, (double)mb};
+      if (k == 0) reset0 = reset;
+    }
+    // ---- the halo: 4 slots per lane, only its composed map is needed.  Its env
+    // tails belong to the tile above, which may already have overwritten their
+    // parked bootstraps in adv: read boot[env] instead, the r-th tail of the
+    // halo being env eh + r (or env_of when an env without fresh slots intervenes)
+    Aff hc;
+    {
+      const int j0 = kGTile + 4 * lane;
+      const float4 r0 = *reinterpret_cast<const float4*>(sr + j0);
+      const float4 v0 = *reinterpret_cast<const float4*>(sv + j0);
+      const uint32_t d4 = *reinterpret_cast<const uint32_t*>(sd + j0);
+      const float rr[4] = {r0.x, r0.y, r0.z, r0.w}, vv[4] = {v0.x, v0.y, v0.z, v0.w};
+      uint32_t tm = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((d4 >> (8 * q)) & 2u) tm |= 1u << q;
+      int rk = __popc(tm);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, rk, o);
+        if (lane >= o) rk += y;
+      }
+      rk -= __popc(tm);
+      float hb[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        hb[q] = 0.f;
+        const int i = lo + j0 + q;
+        if (((d4 >> (8 * q)) & 3u) == 2u && i < F) {
+          int e = eh + rk + __popc(tm & ((1u << q) - 1u));
+          const int o1 = __ldg(off + e + 1);
+          float b = __ldg(boot + e);
+          if (o1 != i + 1) b = __ldg(boot + __ldg(env_of + i));
+          hb[q] = b;
         }
       }
-      v[kGaeItems] = (i0 + kGaeItems < F) ? value[i0 + kGaeItems] : 0.f;
-    }
-    // env tails (done bit 1) in slot order: rank -> env
-    uint32_t tmask = 0;
+      float vnext = sv[j0 + 4];
+      float mb = 0.f;
+      bool reset = false;
 #pragma unroll
-    for (int q = 0; q < kGaeItems; ++q)
-      if (i0 + q < hi && ((dw[q >> 2] >> (8 * (q & 3))) & 2u)) tmask |= 1u << q;
-    int incl_cnt = __popc(tmask);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl_cnt, o);
-      if (lane >= o) incl_cnt += y;
-    }
-    if (lane == 31) s_cnt[warp] = incl_cnt;
-    gae_sync();
-    int rank = incl_cnt - __popc(tmask);
-    for (int w = 0; w < warp; ++w) rank += s_cnt[w];
-    // per-item maps A_i = delta_i + a_i A_{i+1} (fp32); bootstrap at env tails
-    float dl[kGaeItems], ac[kGaeItems];
-#pragma unroll
-    for (int q = 0; q < kGaeItems; ++q) {
-      const uint32_t b = (dw[q >> 2] >> (8 * (q & 3))) & 0xffu;
-      const bool dn = b & 1, tail = b & 2;
-      float vnext = v[q + 1];
-      if (tail) {
-        vnext = 0.f;
-        if (!dn && i0 + q < hi) {
-          // the rank-th non-empty env from e0; env e's tail slot is off[e+1]-1
-          // (empty envs, off[e+1] == off[e], are skipped)
-          int e = hd.e0 + rank;
-          const int32_t* so = reinterpret_cast<const int32_t*>(st + kGaeOffO);
-          for (;;) {
-            const int j1 = e + 1 - hd.wbase;
-            const int o1 = (full && j1 >= 0 && j1 < hd.no) ? so[j1] : off[e + 1];
-            if (o1 - 1 >= i0 + q) break;
-            ++e;
-          }
-          const int j = e - hd.wbase;
-          float bv;
-          bool ok;
-          if (full && j >= 0 && j < hd.nb && j < hd.nv) {
-            bv = reinterpret_cast<const float*>(st + kGaeOffB)[j];
-            ok = st[kGaeOffBV + j] != 0;
-          } else {
-            bv = boot[e];
-            ok = boot_valid[e] != 0;
-          }
-          if (!ok) atomicMin(err_env, e);
-          vnext = bv;
-        }
+      for (int q = 3; q >= 0; --q) {
+        const uint32_t b = (d4 >> (8 * q)) & 3u;
+        const float vn = b == 2u ? hb[q] : vnext;
+        const float mask = (b & 1u) ? 0.f : 1.f;
+        mb = fmaf(b ? 0.f : glf, mb, fmaf(gf * vn, mask, rr[q]) - vv[q]);
+        reset |= b != 0u;
+        vnext = vv[q];
       }
-      if (tail) ++rank;
-      const float mask = dn ? 0.f : 1.f;
-      dl[q] = fmaf(gf * vnext, mask, r[q]) - v[q];
-      ac[q] = tail ? 0.f : glf * mask;
-    }
-    float ma = 1.f, mb = 0.f;  // thread composite, fp32 over <= 8 steps
-#pragma unroll
-    for (int q = kGaeItems - 1; q >= 0; --q) {
-      mb = fmaf(ac[q], mb, dl[q]);
-      ma = ac[q] * ma;
-    }
-    // block-level suffix scan of thread maps (fp64)
-    Affine incl{(double)ma, (double)mb};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      Affine y{__shfl_down_sync(0xffffffffu, incl.a, o), __shfl_down_sync(0xffffffffu, incl.b, o)};
-      if (lane + o < 32) incl = compose(incl, y);
-    }
-    if (lane == 0) s_warp[warp] = incl;
-    gae_sync();
-    if (threadIdx.x == 0) {
-      Affine suf{1.0, 0.0};
-      for (int w = kGaeWarps - 1; w >= 0; --w) {
-        const Affine cur = s_warp[w];
-        s_warp[w] = suf;
-        suf = compose(cur, suf);
-      }
-      s_hdr[s].sa = suf.a;
-      s_hdr[s].sb = suf.b;
-    }
-    Affine lane_ex{__shfl_down_sync(0xffffffffu, incl.a, 1), __shfl_down_sync(0xffffffffu, incl.b, 1)};
-    if (lane == 31) lane_ex = Affine{1.0, 0.0};
-    gae_sync();
-    if (threadIdx.x == 0) {
-      // publish the tile aggregate (the top tile's is already its inclusive
-      // value); after the barrier, so the fence holds up warp 0 only
-      const double sa = s_hdr[s].sa, sb = s_hdr[s].sb;
-      if (tid == 0) {
-        tiles[tid].inc = sb;
-        flag_release(&tiles[tid].flag, 2);
-      } else {
-        tiles[tid].a = sa;
-        tiles[tid].b = sb;
-        flag_release(&tiles[tid].flag, 1);
-      }
-    }
-    const Affine after = compose(lane_ex, s_warp[warp]);  // A at hi -> A after this thread's items
-    // values with carry 0; c: does the item still depend on the carry
-    float xf = (float)after.b;
-    double cf = after.a;
-    float av[kGaeItems], rv[kGaeItems];
-    uint32_t dep = 0;
-#pragma unroll
-    for (int q = kGaeItems - 1; q >= 0; --q) {
-      xf = fmaf(ac[q], xf, dl[q]);
-      cf *= (double)ac[q];
-      av[q] = xf;
-      rv[q] = xf + v[q];
-      if (cf != 0.0) dep |= 1u << q;
-    }
-    if (dep) {
-      // carry-dependent slots (the tile's top segment) -> staged for the fix-up warp
-      atomicMin(&s_hdr[s].seg, i0 + (__ffs(dep) - 1));
-#pragma unroll
-      for (int q = 0; q < kGaeItems; ++q)
-        if ((dep >> q) & 1) {
-          sr[l0 + q] = av[q];
-          sv[l0 + q] = rv[q];
-        }
-    }
-    if (dep == 0 && i0 + kGaeItems <= hi) {
-      float4* a4 = reinterpret_cast<float4*>(adv + i0);
-      float4* q4 = reinterpret_cast<float4*>(ret + i0);
-      __stcs(a4, make_float4(av[0], av[1], av[2], av[3]));
-      __stcs(a4 + 1, make_float4(av[4], av[5], av[6], av[7]));
-      __stcs(q4, make_float4(rv[0], rv[1], rv[2], rv[3]));
-      __stcs(q4 + 1, make_float4(rv[4], rv[5], rv[6], rv[7]));
-    } else {
-      for (int q = 0; q < kGaeItems; ++q)
-        if (i0 + q < hi && !((dep >> q) & 1)) {
-          adv[i0 + q] = av[q];
-          ret[i0 + q] = rv[q];
-        }
+      hc = Aff{reset ? 0.0 : gl4, (double)mb};
     }
     __syncwarp();
-    if (lane == 0) gae_arrive(gsm(&s_ready[s]));
+    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // the stage is consumed: refill it with the tile after next
+    {
+      int e2 = 0;
+      const int t2 = claim(s, e2);
+#pragma unroll
+      for (int q = 0; q < kGStages; ++q)
+        if (s == q) tq[q] = t2, eq[q] = e2;
+    }
+    // ---- suffix scans over the lanes, the rows and the carry (fp64)
+    const Aff in0 = warp_suffix(lc[0], lane), in1 = warp_suffix(lc[1], lane);
+    const Aff hagg = shfl_aff(warp_suffix(hc, lane), 0);
+    double carry = hagg.b;  // A_hi when the halo holds a reset (a == 0)
+    if (hagg.a != 0.0) {  // no reset in the halo: the tile above published A_hi
+      if (lane == 0) {
+        while (flag_acquire(&tiles[tid - 1].flag) == 0) {
+        }
+        carry = tiles[tid - 1].inc;
+      }
+      carry = __shfl_sync(0xffffffffu, carry, 0);
+    }
+    const Aff row1 = shfl_aff(in1, 0), row0 = shfl_aff(in0, 0);
+    const double c1 = carry;                      // A at the top of row 1
+    const double c0 = fma(row1.a, c1, row1.b);    // A at the top of row 0
+    // ---- final values: the lane's top value, then its 8 items (fp32)
+#pragma unroll
+    for (int k = 1; k >= 0; --k) {
+      Aff ex = shfl_down_aff(k ? in1 : in0, 1);
+      if (lane == 31) ex = Aff{1.0, 0.0};
+      float x = (float)fma(ex.a, k ? c1 : c0, ex.b);
+      float av[kGItems], rv[kGItems];
+#pragma unroll
+      for (int q = kGItems - 1; q >= 0; --q) {
+        const uint32_t b = (dd[k][q >> 2] >> (8 * (q & 3))) & 3u;
+        x = fmaf(b ? 0.f : glf, x, dl[k][q]);
+        av[q] = x;
+        rv[q] = x + v[k][q];
+      }
+      const int i0 = lo + kGRow * k + kGItems * lane;
+      if (i0 + kGItems <= hi) {
+        __stcs(reinterpret_cast<float4*>(adv + i0), make_float4(av[0], av[1], av[2], av[3]));
+        __stcs(reinterpret_cast<float4*>(adv + i0) + 1, make_float4(av[4], av[5], av[6], av[7]));
+        __stcs(reinterpret_cast<float4*>(ret + i0), make_float4(rv[0], rv[1], rv[2], rv[3]));
+        __stcs(reinterpret_cast<float4*>(ret + i0) + 1, make_float4(rv[4], rv[5], rv[6], rv[7]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < kGItems; ++q)
+          if (i0 + q < hi) {
+            adv[i0 + q] = av[q];
+            ret[i0 + q] = rv[q];
+          }
+      }
+    }
+    // the tile below reads A_lo from here iff this tile's bottom 128 slots (its
+    // halo) have no reset: lanes 0..15 of row 0
+    if (tid + 1 < ntiles) {
+      if (!__any_sync(0xffffffffu, lane < 16 && reset0) && lane == 0) {
+        tiles[tid].inc = fma(row0.a, c0, row0.b);
+        flag_release(&tiles[tid].flag, 2);
+      }
+    }
   }
 }
 
@@ -461,7 +400,7 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
                      const float* boot, const uint8_t* valid, const int32_t* off, int N, double gamma,
                      double lambda, float* adv, float* ret) {
   if (F <= 0) return;
-  const int ntiles = (F + kGaeTile - 1) / kGaeTile;
+  const int ntiles = (F + kGTile - 1) / kGTile;
   DBuf<GaeTileState> tiles;
   DBuf<int> misc;  // [0] tile counter, [1] lowest env with a missing bootstrap
   tiles.reserve(c, ntiles);
@@ -469,19 +408,24 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   tiles.zero(ntiles);
   VER_CUDA(cudaMemsetAsync(misc.p, 0, sizeof(int), c->stream));
   VER_CUDA(cudaMemsetAsync(misc.p + 1, 0x7f, sizeof(int), c->stream));  // 0x7f7f7f7f: none
-  const int smem = kGaeStages * kGaeStageBytes;
+  gae_boot_kernel<<<cdiv(N, 256), 256, 0, c->stream>>>(off, d, boot, valid, N, adv, misc.p + 1);
+  after_launch(c);
   static std::atomic<int> per_sm_cache[kMaxDevices];  // per device (0 = not probed yet)
   int per_sm = per_sm_cache[dev_slot(c)].load();
   if (!per_sm) {
-    VER_CUDA(cudaFuncSetAttribute(gae_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_scan_kernel, kGaeBlock, smem));
+    VER_CUDA(cudaFuncSetAttribute(gae_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kGSmem));
+    VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gae_scan_kernel, 32 * kGWarps, kGSmem));
     per_sm = std::max(1, per_sm);
     per_sm_cache[dev_slot(c)].store(per_sm);
   }
-  const int grid = std::min(ntiles, per_sm * c->num_sms);
-  gae_scan_kernel<<<grid, kGaeBlock, smem, c->stream>>>(r, v, d, env, F, boot, valid, off, N, gamma, lambda, adv, ret,
-                                                       tiles.p, misc.p, misc.p + 1);
-  after_launch(c);
+  // warps claim tiles dynamically: CTAs that are not resident yet simply start later
+  const int grid = std::min((ntiles + kGWarps - 1) / kGWarps, per_sm * c->num_sms);
+  {
+    ScopedEv ev(c, c->hbm_tag);
+    gae_scan_kernel<<<grid, 32 * kGWarps, kGSmem, c->stream>>>(r, v, d, env, off, boot, F, gamma, lambda, adv,
+                                                               ret, tiles.p, misc.p);
+    after_launch(c);
+  }
   int* h = static_cast<int*>(c->pinned_buf(2 * sizeof(int)));
   misc.download(h, 2);
   sync(c);
@@ -494,7 +438,8 @@ void compute_gae(DView& V, double gamma, double lambda) {
   if (V.size == 0) return;
   if (V.env_contiguous) {
     run_scan(c, V.reward.p, V.value.p, V.done.p, V.env_index.p, V.fresh_prefix, V.env_bootstrap.p,
-             V.env_bootstrap_valid.p, V.env_offsets.p, V.N, gamma, lambda, V.advantage.p, V.returns.p);
+             V.env_bootstrap_valid.p,
+             V.env_offsets.p, V.N, gamma, lambda, V.advantage.p, V.returns.p);
     return;
   }
   const int S = V.size, N = V.N;
@@ -524,8 +469,8 @@ void compute_gae(DView& V, double gamma, double lambda) {
   gae_gather_kernel<<<cdiv(F, 256), 256, 0, c->stream>>>(keys.p, F, V.reward.p, V.value.p, V.done.p, r2.p,
                                                          v2.p, d2.p, e2.p);
   after_launch(c);
-  run_scan(c, r2.p, v2.p, d2.p, e2.p, F, V.env_bootstrap.p, V.env_bootstrap_valid.p, off.p, N, gamma, lambda,
-           a2.p, ret2.p);
+  run_scan(c, r2.p, v2.p, d2.p, e2.p, F, V.env_bootstrap.p, V.env_bootstrap_valid.p, off.p, N, gamma, lambda, a2.p,
+           ret2.p);
   gae_scatter_kernel<<<cdiv(F, 256), 256, 0, c->stream>>>(keys.p, F, a2.p, ret2.p, V.advantage.p,
                                                           V.returns.p);
   after_launch(c);

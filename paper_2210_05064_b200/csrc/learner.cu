@@ -868,37 +868,56 @@ ver_status ver_bench_gae_gather(ver_view v, double gamma, double lambda, int B, 
   cudaEvent_t e0, e1;
   VER_CUDA(cudaEventCreate(&e0));
   VER_CUDA(cudaEventCreate(&e1));
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> log;
+  struct Restore {
+    Ctx* c;
+    ~Restore() { c->evlog = nullptr, c->hbm_tag = -1; }
+  } restore{c};
+  auto elapsed = [](cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    VER_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  };
   compute_gae(V, gamma, lambda);  // warm
+  c->evlog = &log;
+  c->hbm_tag = 0;
   float gae = 0.f;
   for (int r = 0; r < reps; ++r) {
     VER_CUDA(cudaEventRecord(e0, c->stream));
     compute_gae(V, gamma, lambda);
     VER_CUDA(cudaEventRecord(e1, c->stream));
     VER_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    VER_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    gae += ms;
+    gae += elapsed(e0, e1);
   }
+  c->evlog = nullptr;
   std::unique_ptr<DGroups> G(split_minibatches(V, B, seed));
   std::vector<std::unique_ptr<DPacked>> packs;
   for (int b = 0; b < G->B; ++b)
     if (G->gstart[b + 1] > G->gstart[b])
       packs.emplace_back(pack_pieces(V, G->pieces.p + G->gstart[b], G->gstart[b + 1] - G->gstart[b]));
+  for (auto& P : packs) gather_packed(V, *P);  // warm (tile tables built)
+  sync(c);
+  c->evlog = &log;
   float gat = 0.f;
-  for (int r = 0; r < reps; ++r)
-    for (auto& P : packs) {
-      VER_CUDA(cudaEventRecord(e0, c->stream));
-      gather_packed(V, *P);
-      VER_CUDA(cudaEventRecord(e1, c->stream));
-      VER_CUDA(cudaEventSynchronize(e1));
-      float ms = 0.f;
-      VER_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-      gat += ms;
-    }
+  for (int r = 0; r < reps; ++r) {
+    VER_CUDA(cudaEventRecord(e0, c->stream));
+    for (auto& P : packs) gather_packed(V, *P);
+    VER_CUDA(cudaEventRecord(e1, c->stream));
+    VER_CUDA(cudaEventSynchronize(e1));
+    gat += elapsed(e0, e1);
+  }
+  float kern[2] = {0.f, 0.f};
+  for (auto& [tag, a, b] : log) {
+    if (tag == 0 || tag == 1) kern[tag] += elapsed(a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   ms_out[0] = gae / reps;
   ms_out[1] = gat / reps;
+  ms_out[2] = kern[0] / reps;
+  ms_out[3] = kern[1] / reps;
   VER_API_END
 }
 

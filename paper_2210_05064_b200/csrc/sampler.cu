@@ -206,6 +206,12 @@ constexpr int kGT = 32;  // pieces per tile
 // per tile, power of two <= 32) follows the block's longest piece, so blocks
 // of short pieces (the sorted tail of a heavy-tailed length distribution)
 // still fill the CTA: the read phase maps lanes to (piece, t) pairs.
+// view loads of the gather: ld.global.cg (L2 only; measured 11% faster than
+// ld.global.cs at C5 2^26, r02g)
+template <class T>
+__device__ __forceinline__ T gld(const T* p) {
+  return __ldcg(p);
+}
 __global__ void __launch_bounds__(256) gather_tiled_kernel(
     const int2* __restrict__ tiles, const ver_seq_desc* __restrict__ sorted, int k,
     const int32_t* __restrict__ offs, const int32_t* __restrict__ bs, int32_t* __restrict__ slots,
@@ -234,17 +240,17 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(
       const int sl = s_start[jl] + t;
       int f = 0;
       if (D == 2) {  // one 8-byte load per slot (no duplicate sector requests)
-        const float2 o2 = __ldcs(reinterpret_cast<const float2*>(v_obs) + sl);
+        const float2 o2 = gld(reinterpret_cast<const float2*>(v_obs) + sl);
         cell(f++, jl, tt) = o2.x;
         cell(f++, jl, tt) = o2.y;
       } else {
-        for (int q = 0; q < D; ++q) cell(f++, jl, tt) = __ldcs(v_obs + (size_t)sl * D + q);
+        for (int q = 0; q < D; ++q) cell(f++, jl, tt) = gld(v_obs + (size_t)sl * D + q);
       }
       for (int q = 0; q < AC; ++q) cell(f++, jl, tt) = v_actc[(size_t)sl * A + q];
-      cell(f++, jl, tt) = __ldcs(v_lp + sl);
-      cell(f++, jl, tt) = __ldcs(v_adv + sl);
-      cell(f++, jl, tt) = __ldcs(v_ret + sl);
-      if (!continuous) cell(f++, jl, tt) = __int_as_float(__ldcs(v_act + sl));
+      cell(f++, jl, tt) = gld(v_lp + sl);
+      cell(f++, jl, tt) = gld(v_adv + sl);
+      cell(f++, jl, tt) = gld(v_ret + sl);
+      if (!continuous) cell(f++, jl, tt) = __int_as_float(gld(v_act + sl));
     }
   }
   __syncthreads();
@@ -290,9 +296,11 @@ void gather_packed(DView& V, DPacked& P) {
   }
   const int F = V.obs_dim + (V.action_kind ? V.act_dim : 0) + 3 + (V.action_kind ? 0 : 1);
   const size_t smem = sizeof(float) * (size_t)F * kGT * (kGT + 1);
+  auto kern = gather_tiled_kernel;
   if (smem > 48 * 1024)
-    VER_CUDA(cudaFuncSetAttribute(gather_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  gather_tiled_kernel<<<(unsigned)P.tile_table.size(), 256, smem, c->stream>>>(
+    VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ScopedEv ev(c, c->hbm_tag >= 0 ? c->hbm_tag + 1 : -1);
+  kern<<<(unsigned)P.tile_table.size(), 256, smem, c->stream>>>(
       P.tiles.p, P.seqs.p, P.k, P.offs.p, P.bs.p, P.slots.p, V.obs.p, V.act_disc.p, V.act_cont.p, V.log_prob.p,
       V.advantage.p, V.returns.p, P.obs.p, P.act_disc.p, P.act_cont.p, P.old_logp.p, P.adv.p, P.ret.p, V.obs_dim,
       V.act_dim, V.action_kind, (int)P.tile_table.size(), V.size);

@@ -1,10 +1,13 @@
-"""GAE edge cases of the persistent look-back scan (csrc/gae.cu) vs the oracle's
+"""GAE edge cases of the warp-tile scan (csrc/gae.cu: 512-slot tiles + a
+128-slot halo row, look-back only across reset-free halos) vs the oracle's
 compute_gae (learner.cpp:11-41) and an independent float64 recursion:
 
-* envs with no fresh slot (the tail -> env numbering must skip them);
-* segments longer than a 2048-slot tile (multi-tile look-back, long carry-
-  dependent top segments, gamma * lambda close to 1);
-* array sizes around multiples of the tile (partial last tile, 4-slot tails).
+* envs with no fresh slot (tail slots read their env directly);
+* segments longer than several tiles (reset-free halos: the look-back chain,
+  gamma * lambda close to 1);
+* array sizes around multiples of the tile and of tile + halo (partial top
+  tile, halos read from global memory, 4-slot tails);
+* resets exactly on the halo / bottom-row boundaries.
 
 Bar: |gpu - ref| <= 1e-5 * max(1, |ref|)."""
 from dataclasses import replace
@@ -75,7 +78,8 @@ def test_gae_segments_longer_than_a_tile(gl):
     assert np.abs(hg.returns - ho.returns).max() <= 1e-5 * scale
 
 
-@pytest.mark.parametrize("S", [2048, 2049, 2052, 3 * 2048 - 1, 3 * 2048 + 3, 5 * 2048 + 7])
+@pytest.mark.parametrize("S", [1, 3, 512, 513, 516, 640, 644, 645, 1023, 1024 + 131, 2048, 2049, 2052,
+                               3 * 2048 - 1, 3 * 2048 + 3, 5 * 2048 + 7])
 def test_gae_tile_boundaries(S):
     import paper_2210_05064_b200 as V
     rng = np.random.default_rng(S)
@@ -88,5 +92,23 @@ def test_gae_tile_boundaries(S):
     hv = view.to_host()
     assert hv.size == S
     ref = gae_ref(hv, 0.99, 0.97)
+    err = np.abs(hv.advantage - ref) / np.maximum(1.0, np.abs(ref))
+    assert err.max() <= 1e-5
+
+
+@pytest.mark.parametrize("period", [128, 129, 511, 512, 640, 700])
+def test_gae_reset_at_tile_and_halo_boundaries(period):
+    """Envs of exactly `period` slots without dones: the only resets are env
+    tails, placed on / next to the 128-slot row, 512-slot tile and halo
+    boundaries, so tiles alternate between local carries and look-backs."""
+    import paper_2210_05064_b200 as V
+    S = 40 * 512 + 17
+    lens = np.full(S // period, period, np.int64)
+    if lens.sum() < S:
+        lens = np.append(lens, S - lens.sum())
+    view = V.view_synth(lens.astype(np.int32), seed=period, p_done=0.0)
+    V.compute_gae(view, 0.999, 0.999)
+    hv = view.to_host()
+    ref = gae_ref(hv, 0.999, 0.999)
     err = np.abs(hv.advantage - ref) / np.maximum(1.0, np.abs(ref))
     assert err.max() <= 1e-5
