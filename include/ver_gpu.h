@@ -278,6 +278,14 @@ ver_status ver_preempt_destroy(ver_preempt p);
 ver_status ver_preempt_start(ver_preempt p, int64_t threshold);        /* start_iteration; <= 0 disables */
 ver_status ver_preempt_add(ver_preempt p, int64_t n, int64_t* total, int* fired_now); /* add_steps */
 ver_status ver_preempt_state(ver_preempt p, int64_t* total, int* fired);
+/* NCCL mode ("global committed-step ncclAllReduce(int64) per
+   tick"): every rank creates its own counter on a ctx with NCCL initialised;
+   adds (ver_preempt_add, or an attached engine) accumulate locally, and
+   ver_preempt_tick -- a collective every rank calls once per collection tick,
+   in the same order -- sums the deltas over the ranks, so every rank holds the
+   same global count and fires on the same tick.  start runs on every rank. */
+ver_status ver_preempt_create_nccl(ver_ctx ctx, ver_preempt* out);
+ver_status ver_preempt_tick(ver_preempt p, int64_t* total, int* fired_now);
 
 /* ------------------------------------------ on-disk formats */
 /* dump_view / load_view (rollout.cpp:293-432): the reference's JSONL rollout trace
@@ -325,6 +333,7 @@ typedef struct {
   int n_dispatch;
   int new_commits;
   int closed_now;
+  int preempt_fired; /* attached counter: the group has fired (this rollout was force-closed) */
 } ver_batch_result;
 
 typedef struct ver_engine_s* ver_engine;
@@ -342,6 +351,13 @@ ver_status ver_engine_begin_rollout(ver_engine e, ver_batch_result* res, int32_t
 ver_status ver_engine_process_batch(ver_engine e, const ver_request_batch* reqs, ver_batch_result* res,
                                     int32_t* disp_env, int32_t* disp_act, float* disp_act_cont);
 ver_status ver_engine_force_close(ver_engine e);        /* runtime.hpp:120 */
+/* Joint preemption (distributed.hpp:95-128, runtime.cpp:592-599): each batch's
+   commits are added to `counter` by the batch's sampling kernel (one
+   system-scope atomic on the owner's device word through peer memory, or the
+   local delta of an NCCL-mode counter), and the group's fired flag comes back
+   with the actions in mapped host memory; the first batch that sees it fired
+   force-closes this engine's rollout (closed_now = 1).  NULL detaches. */
+ver_status ver_engine_attach_preempt(ver_engine e, ver_preempt counter);
 ver_status ver_engine_finalize_bootstraps(ver_engine e); /* runtime.cpp:217-229 */
 ver_status ver_engine_close(ver_engine e, ver_view* out); /* runtime.cpp:231-234 */
 ver_status ver_engine_state(ver_engine e, int* open, int* committed, int* capacity, int* carryover,

@@ -287,6 +287,8 @@ class InferenceEngine : public Handle<ver_engine, ver_engine_destroy> {
     return finish(d, r);
   }
   void force_close() { check(ver_engine_force_close(get())); }
+  // joint preemption: commits added from the sampling kernel, force-close when the group fires
+  void attach_preempt(ver_preempt counter) { check(ver_engine_attach_preempt(get(), counter)); }
   void finalize_bootstraps() { check(ver_engine_finalize_bootstraps(get())); }
   RolloutView close() {
     ver_view v = nullptr;
@@ -331,10 +333,13 @@ class InferenceEngine : public Handle<ver_engine, ver_engine_destroy> {
 };
 
 // PreemptCoordinator (distributed.hpp:95-128) across processes: the owning
-// replica creates the counter and ships ipc_handle() to the others, which open it.
+// replica creates the counter and ships ipc_handle() to the others, which open
+// it; or (Nccl{}) one counter per rank, summed by the collective tick().
 class PreemptCounter : public Handle<ver_preempt, ver_preempt_destroy> {
  public:
+  struct Nccl {};
   explicit PreemptCounter(const Context& ctx) : Handle(make(ctx)) {}
+  PreemptCounter(const Context& ctx, Nccl) : Handle(make_nccl(ctx)) {}
   PreemptCounter(const Context& ctx, const std::vector<uint8_t>& handle) : Handle(open(ctx, handle)) {}
   std::vector<uint8_t> ipc_handle() const {
     std::vector<uint8_t> h(64);
@@ -357,11 +362,24 @@ class PreemptCounter : public Handle<ver_preempt, ver_preempt_destroy> {
     if (total) *total = t;
     return f != 0;
   }
+  // NCCL mode: collective over the ranks; true on the tick that reaches the threshold
+  bool tick(int64_t* total = nullptr) {
+    int64_t t = 0;
+    int f = 0;
+    check(ver_preempt_tick(get(), &t, &f));
+    if (total) *total = t;
+    return f != 0;
+  }
 
  private:
   static ver_preempt make(const Context& ctx) {
     ver_preempt p = nullptr;
     check(ver_preempt_create(ctx.get(), &p));
+    return p;
+  }
+  static ver_preempt make_nccl(const Context& ctx) {
+    ver_preempt p = nullptr;
+    check(ver_preempt_create_nccl(ctx.get(), &p));
     return p;
   }
   static ver_preempt open(const Context& ctx, const std::vector<uint8_t>& h) {

@@ -71,7 +71,7 @@ class RequestBatch(C.Structure):
 
 
 class BatchResult(C.Structure):
-    _fields_ = [("n_dispatch", c_int), ("new_commits", c_int), ("closed_now", c_int)]
+    _fields_ = [("n_dispatch", c_int), ("new_commits", c_int), ("closed_now", c_int), ("preempt_fired", c_int)]
 
 
 class PPOConfig(C.Structure):
@@ -215,6 +215,8 @@ _SIGS = {
     "ver_preempt_start": (c_int, [C.c_void_p, c_int64]),
     "ver_preempt_add": (c_int, [C.c_void_p, c_int64, P(c_int64), P(c_int)]),
     "ver_preempt_state": (c_int, [C.c_void_p, P(c_int64), P(c_int)]),
+    "ver_preempt_create_nccl": (c_int, [C.c_void_p, P(C.c_void_p)]),
+    "ver_preempt_tick": (c_int, [C.c_void_p, P(c_int64), P(c_int)]),
     "ver_view_dump_jsonl": (c_int, [C.c_void_p, C.c_char_p]),
     "ver_view_load_jsonl": (c_int, [C.c_void_p, C.c_char_p, P(C.c_void_p)]),
     "ver_learner_save_checkpoint": (c_int, [C.c_void_p, C.c_char_p]),
@@ -228,6 +230,7 @@ _SIGS = {
     "ver_engine_process_batch": (c_int, [C.c_void_p, P(RequestBatch), P(BatchResult), P(c_int32), P(c_int32),
                                          P(c_float)]),
     "ver_engine_force_close": (c_int, [C.c_void_p]),
+    "ver_engine_attach_preempt": (c_int, [C.c_void_p, C.c_void_p]),
     "ver_engine_finalize_bootstraps": (c_int, [C.c_void_p]),
     "ver_engine_close": (c_int, [C.c_void_p, P(C.c_void_p)]),
     "ver_engine_state": (c_int, [C.c_void_p, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int)]),

@@ -1102,15 +1102,25 @@ def checkpoint_model_config(path) -> ModelConfig:
 
 # ------------------------------------------------------ preemption counter
 class PreemptCounter:
-    """PreemptCoordinator (distributed.hpp:95-128) across processes: one replica
-    creates the device counter and exports its IPC handle (64 bytes); the others
-    open it.  add_steps returns (total, fired_now); exactly one add per
-    iteration fires, and every replica then force-closes its rollout."""
+    """PreemptCoordinator (distributed.hpp:95-128) across processes.
 
-    def __init__(self, ctx: Context | None = None, handle: bytes | None = None):
+    IPC mode (default): one replica creates the device counter and exports its
+    IPC handle (64 bytes); the others open it.  add_steps returns (total,
+    fired_now); exactly one add per iteration fires.  NCCL mode (nccl=True, ctx
+    with NCCL initialised, one counter per rank): adds accumulate locally and
+    tick() -- a collective all ranks call once per collection tick -- sums them
+    with ncclAllReduce, so all ranks fire on the same tick.  An InferenceEngine
+    attached with attach_preempt() adds each batch's commits from its sampling
+    kernel and force-closes its rollout once the group has fired."""
+
+    def __init__(self, ctx: Context | None = None, handle: bytes | None = None, nccl: bool = False):
         self.ctx = ctx or default_context()
         self.h = C.c_void_p()
-        if handle is None:
+        self.nccl = nccl
+        if nccl:
+            _check(_lib().ver_preempt_create_nccl(self.ctx.h, C.byref(self.h)))
+            self.owner = True
+        elif handle is None:
             _check(_lib().ver_preempt_create(self.ctx.h, C.byref(self.h)))
             self.owner = True
         else:
@@ -1146,6 +1156,12 @@ class PreemptCounter:
         _check(_lib().ver_preempt_state(self.h, C.byref(t), C.byref(f)))
         return t.value, bool(f.value)
 
+    def tick(self) -> tuple[int, bool]:
+        """NCCL mode: (global total, fired on this tick); collective over the ranks."""
+        t, f = C.c_int64(), C.c_int()
+        _check(_lib().ver_preempt_tick(self.h, C.byref(t), C.byref(f)))
+        return t.value, bool(f.value)
+
 
 # --------------------------------------------------------- inference engine
 @dataclass
@@ -1167,6 +1183,7 @@ class BatchResult:
     dispatches: list
     new_commits: int = 0
     closed_now: bool = False
+    preempt_fired: bool = False
 
 
 class InferenceEngine:
@@ -1213,7 +1230,7 @@ class InferenceEngine:
             d = [(int(env[i]), act_c[i].copy()) for i in range(n)]
         else:
             d = [(int(env[i]), int(act_d[i])) for i in range(n)]
-        return BatchResult(d, r.new_commits, bool(r.closed_now))
+        return BatchResult(d, r.new_commits, bool(r.closed_now), bool(r.preempt_fired))
 
     def _bufs(self, n: int):
         A = max(1, self.model.act_dim if self.model.action_kind == 1 else 1)
@@ -1276,6 +1293,13 @@ class InferenceEngine:
 
     def force_close(self):
         _check(_lib().ver_engine_force_close(self.h))
+
+    def attach_preempt(self, counter: "PreemptCounter | None"):
+        """Joint preemption (runtime.cpp:592-599): each batch's commits go to
+        `counter` from the sampling kernel; the first batch that sees the group
+        fired force-closes this rollout.  None detaches."""
+        self._preempt = counter  # keep the handle alive while attached
+        _check(_lib().ver_engine_attach_preempt(self.h, counter.h if counter is not None else None))
 
     def finalize_bootstraps(self):
         _check(_lib().ver_engine_finalize_bootstraps(self.h))

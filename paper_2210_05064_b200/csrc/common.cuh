@@ -187,6 +187,10 @@ constexpr int kMaxDevices = 64;
 inline int dev_slot(const Ctx* c) { return c->device >= 0 && c->device < kMaxDevices ? c->device : 0; }
 // experiments only: integer tuning knob from the environment
 int env_int(const char* name, int dflt);
+// VER_PROFILING=1: launches that a kernel profiler cannot replay take a
+// profiler-compatible form (the CTA-pair step kernel drops the cooperative
+// attribute; ncu serializes kernels, so its CTAs are co-resident anyway)
+bool profiling();
 
 inline unsigned cdiv(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 

@@ -23,6 +23,7 @@
 // by line.
 #include <optional>
 
+#include "coordinator.cuh"
 #include "policy.cuh"
 #include "rollout.cuh"
 
@@ -76,14 +77,27 @@ __global__ void scatter_h_kernel(int m, int H, const int32_t* __restrict__ env, 
   for (int j = threadIdx.x; j < H; j += blockDim.x) h[(size_t)env[i] * H + j] = hnew[(size_t)i * H + j];
 }
 
+// The attached joint preemption counter (coordinator.cuh): add this batch's
+// commits (add_steps, distributed.hpp:110-119; the reference's driver calls it
+// from on_commits after process_batch, runtime.cpp:592) and mirror the group's
+// fired flag into mapped host memory: flag[0] = fired, flag[1] = this add fired.
+__device__ __forceinline__ void preempt_commit(PreemptWords* pw, long long nadd, int* flag) {
+  const int now = preempt_add_dev(pw, nadd);
+  flag[0] = preempt_fired_dev(pw);
+  flag[1] = now;
+}
+__global__ void preempt_commit_kernel(PreemptWords* pw, long long nadd, int* flag) { preempt_commit(pw, nadd, flag); }
+
 // compute_actions' sampling (runtime.cpp:163-188): one thread per request.
-// out: [m] action index | [m x A] continuous action | [m] log-prob | [m] value
+// out: [m] action index | [m x A] continuous action | [m] log-prob | [m] value.
+// Thread 0 also commits the batch's steps to the attached preemption counter.
 __global__ void sample_kernel(int m, int A, int AH, int continuous, uint64_t key0, const int32_t* __restrict__ env,
                               const int64_t* __restrict__ obs_ep, const int32_t* __restrict__ obs_step,
                               const float* __restrict__ heads, const float* __restrict__ log_std,
                               int32_t* __restrict__ act_d, float* __restrict__ act_c, float* __restrict__ logp,
-                              float* __restrict__ value) {
+                              float* __restrict__ value, PreemptWords* pw, long long nadd, int* pflag) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && pw) preempt_commit(pw, nadd, pflag);
   if (i >= m) return;
   Rng rng{mix(mix(mix(mix(key0, 0xAC7101ull), (uint64_t)env[i]), (uint64_t)obs_ep[i]), (uint64_t)obs_step[i]), 0};
   const float* row = heads + (size_t)i * AH;
@@ -150,6 +164,7 @@ struct Result {
   float* act_c = nullptr;
   int nd = 0, new_commits = 0;
   bool closed_now = false;
+  bool preempt_fired = false;
 };
 
 struct Engine {
@@ -198,6 +213,17 @@ struct Engine {
 
   Rollout& buf() { return store.r; }
 
+  // attached joint preemption counter: commits are added by the sampling kernel,
+  // the group's fired flag comes back in mapped host memory with the actions
+  ver_preempt_s* pre = nullptr;
+  int* pflag_h = nullptr;  // [fired, fired_now], cudaHostAllocMapped
+  int* pflag_d = nullptr;
+  long long commit_add = 0;  // this batch's commits, added by the next sampling launch
+  bool committed_this_batch = false;
+  ~Engine() {
+    if (pflag_h) cudaFreeHost(pflag_h);
+  }
+
   // forward of the listed envs (act: encode + gru_cell + heads) -> heads (m x AH);
   // with `sample`: pending h_before, sampled actions, h <- h_new
   void run(const std::vector<const Request*>& rq, bool sample) {
@@ -245,8 +271,9 @@ struct Engine {
       sample_kernel<<<cdiv(n, 128), 128, 0, c->stream>>>(
           n, A, m.AH, m.continuous, key0, didx.p, dep.p, didx.p + n, heads.p,
           m.continuous ? params.p + m.o_ls : nullptr, reinterpret_cast<int32_t*>(dres.p), dres.p + 3 * n,
-          dres.p + n, dres.p + 2 * n);
+          dres.p + n, dres.p + 2 * n, pre ? pre->w : nullptr, commit_add, pflag_d);
       after_launch(c);
+      if (pre) committed_this_batch = true;
       VER_CUDA(cudaMemcpyAsync(pres.p, dres.p, sizeof(float) * nres, cudaMemcpyDeviceToHost, c->stream));
     } else {
       VER_CUDA(cudaMemcpy2DAsync(pres.p + 2 * n, sizeof(float), heads.p + A, sizeof(float) * m.AH, sizeof(float), n,
@@ -318,6 +345,8 @@ struct Engine {
         if (capped) es.paused = true;
       }
     }
+    commit_add = out.new_commits;
+    committed_this_batch = false;
     if (!zero.empty()) {  // es.h.setZero() for done envs (parked ones too)
       pidx.ensure(std::max<size_t>(zero.size(), 2 * needs.size()));
       DBuf<int32_t> dz;
@@ -328,6 +357,27 @@ struct Engine {
       sync(c);
     }
     compute_actions(needs, out);
+    if (pre) preempt_after_batch(out);
+  }
+
+  // the group's preemption after a batch: commit if no sampling launch carried the
+  // add, then force-close this replica's rollout once the group has fired
+  // (ThreadedDriver::request_force_close -> engine_.force_close() after the
+  // batch, runtime.cpp:596-599)
+  void preempt_after_batch(Result& out) {
+    if (!committed_this_batch) {
+      if (commit_add <= 0) return;
+      preempt_commit_kernel<<<1, 1, 0, c->stream>>>(pre->w, commit_add, pflag_d);
+      after_launch(c);
+      sync(c);
+    }
+    commit_add = 0;
+    const int fired = *(volatile int*)pflag_h;
+    out.preempt_fired = fired != 0;
+    if (fired && buf().open && buf().committed > 0) {
+      buf().open = false;
+      out.closed_now = true;
+    }
   }
 
   // begin_rollout (runtime.cpp:84-113)
@@ -349,6 +399,7 @@ struct Engine {
       if (buf().open && !buf().env_at_cap(pk.r.env)) needs.push_back(&pk.r);
       else park(pk.r);
     }
+    commit_add = 0;  // carryover commits are not counted toward the group (runtime.cpp:521-531)
     compute_actions(needs, out);
     if (!buf().open) out.closed_now = true;
   }
@@ -401,6 +452,7 @@ static void to_result(const eng::Result& r, ver_batch_result* out) {
   out->n_dispatch = r.nd;
   out->new_commits = r.new_commits;
   out->closed_now = r.closed_now ? 1 : 0;
+  out->preempt_fired = r.preempt_fired ? 1 : 0;
 }
 
 extern "C" {
@@ -501,6 +553,20 @@ ver_status ver_engine_process_batch(ver_engine e, const ver_request_batch* b, ve
   eng::Result r{disp_env, disp_act, disp_act_cont};
   E.process_batch(reqs, r);
   to_result(r, res);
+  VER_API_END
+}
+
+ver_status ver_engine_attach_preempt(ver_engine e, ver_preempt p) {
+  VER_API_BEGIN
+  eng::Engine& E = e->e;
+  activate(E.c);
+  if (p && p->c->device != E.c->device) config_error("engine: the preemption counter lives on another device");
+  if (p && !E.pflag_h) {
+    VER_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&E.pflag_h), 2 * sizeof(int), cudaHostAllocMapped));
+    VER_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&E.pflag_d), E.pflag_h, 0));
+  }
+  if (E.pflag_h) E.pflag_h[0] = E.pflag_h[1] = 0;
+  E.pre = p;
   VER_API_END
 }
 

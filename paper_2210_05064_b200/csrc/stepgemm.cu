@@ -800,7 +800,9 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     at[1].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barriers spin on each other
     at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    // ncu cannot replay a cooperative cluster launch (LaunchFailed); it serializes
+    // kernels, so a plain cluster launch of <= one CTA per SM is co-resident there
+    cfg.numAttrs = profiling() ? 1 : 2;
     ScopedEv ev(c, c->rec_tag);
     VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<DIR>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
                                 hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo));

@@ -1,13 +1,18 @@
-#include <cstdlib>
 // util.cu — context lifecycle, error state, NCCL plumbing and the device
 // primitives shared by the hot-path kernels: int32 exclusive scan (3-phase,
 // 1024-thread blocks) and a bitonic sort of unique uint64 keys.
 #include "common.cuh"
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 namespace verg {
+
+bool profiling() {
+  static const bool on = env_int("VER_PROFILING", 0) != 0;
+  return on;
+}
 
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
