@@ -318,6 +318,26 @@ def compute_gae(view: View, gamma: float, lam: float):
     _chk(lib().vo_compute_gae(view.h, c_double(gamma), c_double(lam)))
 
 
+def gae_arrays(reward, value, done, env, replayed, N, boot, boot_valid, gamma, lam, reference_loop=False):
+    """compute_gae (learner.cpp:11-41) over SoA arrays (the C5 CPU baseline):
+    reference_loop = the reference's O(N S) slot search, else an O(S) bucketing
+    pass before the same per-env recursion.  Returns (advantage, returns)."""
+    r = np.ascontiguousarray(reward, np.float32)
+    S = r.size
+    v = np.ascontiguousarray(value, np.float32)
+    d = np.ascontiguousarray(done, np.uint8)
+    e = np.ascontiguousarray(env, np.int32)
+    rp = np.ascontiguousarray(replayed, np.uint8)
+    b = np.ascontiguousarray(boot, np.float32)
+    bv = np.ascontiguousarray(boot_valid, np.uint8)
+    adv = np.zeros(S, np.float32)
+    ret = np.zeros(S, np.float32)
+    _chk(lib().vo_gae_arrays(_p(r, C.c_float), _p(v, C.c_float), _p(d, C.c_uint8), _p(e, c_int32),
+                             _p(rp, C.c_uint8), S, int(N), _p(b, C.c_float), _p(bv, C.c_uint8), c_double(gamma),
+                             c_double(lam), 1 if reference_loop else 0, _p(adv, C.c_float), _p(ret, C.c_float)))
+    return adv, ret
+
+
 def shuffle_perm(n: int, seed: int) -> np.ndarray:
     out = np.zeros(n, np.int32)
     _chk(lib().vo_shuffle_perm(n, seed, _p(out, c_int32)))

@@ -2079,6 +2079,57 @@ int vo_compute_gae(vo_view v, double gamma, double lambda) {
   VO_TRY(compute_gae(v->v, gamma, lambda))
 }
 
+// compute_gae (learner.cpp:11-41) over bare SoA arrays, for the C5 CPU
+// baseline.  reference_loop = 1: the reference's own O(N*S)
+// structure (every env scans the whole view for its slots); 0: the same
+// per-env reverse recursion with the slots bucketed by env in one O(S) pass.
+int vo_gae_arrays(const float* reward, const float* value, const uint8_t* done, const int32_t* env,
+                  const uint8_t* replayed, int S, int N, const float* boot, const uint8_t* boot_valid,
+                  double gamma, double lambda, int reference_loop, float* adv, float* ret) {
+  VO_TRY({
+    auto env_pass = [&](int e, const std::vector<int>& slots) {
+      if (slots.empty()) return;
+      double next_adv = 0, next_value = 0;
+      const int last = slots.back();
+      if (!(done[last] & 1)) {
+        if (!boot_valid[e]) throw ProtocolError("compute_gae: missing bootstrap value for env " + std::to_string(e));
+        next_value = boot[e];
+      }
+      for (int k = (int)slots.size() - 1; k >= 0; --k) {
+        const int i = slots[k];
+        const double mask = (done[i] & 1) ? 0.0 : 1.0;
+        const double delta = reward[i] + gamma * next_value * mask - value[i];
+        next_adv = delta + gamma * lambda * mask * next_adv;
+        adv[i] = (float)next_adv;
+        ret[i] = (float)(next_adv + value[i]);
+        next_value = value[i];
+      }
+    };
+    if (reference_loop) {
+      std::vector<int> slots;
+      for (int e = 0; e < N; ++e) {
+        slots.clear();
+        for (int i = 0; i < S; ++i)
+          if (env[i] == e && !replayed[i]) slots.push_back(i);
+        env_pass(e, slots);
+      }
+    } else {
+      std::vector<int> cnt(N + 1, 0), order(S);
+      for (int i = 0; i < S; ++i)
+        if (!replayed[i]) ++cnt[env[i] + 1];
+      for (int e = 0; e < N; ++e) cnt[e + 1] += cnt[e];
+      std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+      for (int i = 0; i < S; ++i)
+        if (!replayed[i]) order[pos[env[i]]++] = i;
+      std::vector<int> slots;
+      for (int e = 0; e < N; ++e) {
+        slots.assign(order.begin() + cnt[e], order.begin() + cnt[e + 1]);
+        env_pass(e, slots);
+      }
+    }
+  })
+}
+
 int vo_ppo_loss(const vo_model_config* c, const double* params, vo_view v, vo_packed p,
                 const vo_ppo_config* cfg, double alpha, const double* h0_sorted, int want_grads,
                 const double* frozen_w, vo_loss_result* out, double* grads_out, double* is_w_out) {

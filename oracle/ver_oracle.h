@@ -151,6 +151,9 @@ typedef struct {
 } vo_loss_result;
 
 int vo_compute_gae(vo_view v, double gamma, double lambda);
+int vo_gae_arrays(const float* reward, const float* value, const uint8_t* done, const int32_t* env,
+                  const uint8_t* replayed, int S, int N, const float* boot, const uint8_t* boot_valid,
+                  double gamma, double lambda, int reference_loop, float* adv, float* ret);
 /* OpenMP threads of the oracle's GEMMs / reductions (bit-identical for any count; default 1) */
 int vo_set_num_threads(int n);
 int vo_get_num_threads(void);

@@ -223,6 +223,30 @@ class RolloutView:
         _check(_lib().ver_view_download(self.h, C.byref(vh)))
         return hv
 
+    _FIELD_TYPES = {"obs": (np.float32, C.c_float, "S*D"), "log_prob": (np.float32, C.c_float, "S"),
+                    "value": (np.float32, C.c_float, "S"), "reward": (np.float32, C.c_float, "S"),
+                    "advantage": (np.float32, C.c_float, "S"), "returns": (np.float32, C.c_float, "S"),
+                    "done": (np.uint8, C.c_uint8, "S"), "replayed": (np.uint8, C.c_uint8, "S"),
+                    "env_index": (np.int32, C.c_int32, "S"), "act_disc": (np.int32, C.c_int32, "S"),
+                    "per_env_counts": (np.int32, C.c_int32, "N"), "env_bootstrap": (np.float32, C.c_float, "N"),
+                    "env_bootstrap_valid": (np.uint8, C.c_uint8, "N")}
+
+    def fields(self, *names) -> dict:
+        """Download only the named slot / env arrays (ver_view_download skips NULL fields)."""
+        i = self.info()
+        vh = L.ViewHost()
+        vh.T, vh.N, vh.action_kind, vh.obs_dim, vh.act_dim, vh.hidden_dim = (i.T, i.N, i.action_kind, i.obs_dim,
+                                                                             i.act_dim, i.hidden_dim)
+        vh.size, vh.num_seqs, vh.h0_rows = i.size, i.num_seqs, i.h0_rows
+        out = {}
+        for n in names:
+            dt, ct, shape = self._FIELD_TYPES[n]
+            cnt = {"S": i.size, "N": i.N, "S*D": i.size * i.obs_dim}[shape]
+            out[n] = np.empty(cnt, dt)
+            setattr(vh, n, _ptr(out[n], ct))
+        _check(_lib().ver_view_download(self.h, C.byref(vh)))
+        return out
+
     def dump_jsonl(self, path):
         """dump_view (rollout.cpp:293-344): the reference's JSONL trace."""
         _check(_lib().ver_view_dump_jsonl(self.h, str(path).encode()))

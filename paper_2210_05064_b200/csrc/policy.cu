@@ -1077,6 +1077,280 @@ __global__ void __launch_bounds__(kLossWarps * 32, 2) ppo_loss_rows_kernel(
   }
 }
 
+// Staged variant of the fused loss (H % 128 == 0, H <= 512, A + 1 == NA <= 3,
+// gradients wanted): each warp stages its group of kStageRows consecutive
+// packed rows of `hidden` (contiguous, kStageRows x H x 4 B) into shared
+// memory with one bulk copy, so the rows are read from HBM once and both the
+// head pass and the gradient pass read them as float4 from shared memory.
+// The head weights live in registers (lane l owns columns 4l + 128i .. +3),
+// the per-row double loss math runs in lane r for row r (as in
+// ppo_loss_rows_kernel), dhead is not materialised.  Per row: 2H + 16 B read,
+// 2H B... i.e. the head-fused 8H + 16 B of SURVEY §8(d).
+constexpr int kStageRows = 8;
+constexpr int kStageWarps = 4;
+template <int NA>
+__global__ void __launch_bounds__(kStageWarps * 32, 3) ppo_loss_stage_kernel(
+    int S, int H, int A, int continuous, const float* __restrict__ hidden, const float* __restrict__ wh,
+    const float* __restrict__ bh, const float* __restrict__ log_std, const float* __restrict__ act_cont,
+    const int32_t* __restrict__ act_disc, const float* __restrict__ old_logp, const float* __restrict__ adv,
+    const float* __restrict__ ret, const float* __restrict__ frozen_w, double clip, double is_cap,
+    double vcoef, const double* __restrict__ alpha_p, double inv_S, float* __restrict__ dhidden,
+    float* __restrict__ is_w, double* __restrict__ part, float* __restrict__ hpart) {
+  constexpr int HV = 4;  // float4 columns per lane at H = 512 (fewer at smaller H: masked)
+  extern __shared__ __align__(128) float s_rows[];  // kStageWarps x kStageRows x H
+  __shared__ uint64_t s_bar[kStageWarps];
+  __shared__ double s_red[kStageWarps][kLossStats + 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int hv = H / 128;
+  float* rows = s_rows + (size_t)warp * kStageRows * H;
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar[warp]));
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // head weights of this lane's columns: w[i][e][c] = wh[(4 lane + 128 i + e) * NA + c]
+  float w[HV][4][NA], wacc[HV][4][NA], bacc[NA];
+#pragma unroll
+  for (int i = 0; i < HV; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        w[i][e][c] = i < hv ? __ldg(wh + (size_t)(4 * lane + 128 * i + e) * NA + c) : 0.f;
+        wacc[i][e][c] = 0.f;
+      }
+#pragma unroll
+  for (int c = 0; c < NA; ++c) bacc[c] = 0.f;
+  float bhv[NA];
+#pragma unroll
+  for (int c = 0; c < NA; ++c) bhv[c] = bh[c];
+  const double alpha = *alpha_p;
+  const double gH = -alpha * inv_S;
+  double st[kLossStats] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double dlsv[NA];
+#pragma unroll
+  for (int c = 0; c < NA; ++c) dlsv[c] = 0.0;
+  const int gw = blockIdx.x * kStageWarps + warp, nwarps = gridDim.x * kStageWarps;
+  uint32_t phase = 0;
+  for (int pb = gw * kStageRows; pb < S; pb += nwarps * kStageRows, phase ^= 1) {
+    const int nr = min(kStageRows, S - pb);
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)nr * H * 4;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the last group's generic reads first
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(rows))),
+                   "l"(hidden + (size_t)pb * H), "r"(bytes), "r"(bar)
+                   : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "LS_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra LS_WAIT;\n\t}" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+    // ---- heads of the staged rows: lane r keeps row r's logits
+    float lgm[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) lgm[c] = 0.f;
+    for (int r = 0; r < nr; ++r) {
+      const float* row = rows + (size_t)r * H;
+      float acc[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) acc[c] = 0.f;
+#pragma unroll
+      for (int i = 0; i < HV; ++i)
+        if (i < hv) {
+          const float4 x = *reinterpret_cast<const float4*>(row + 4 * lane + 128 * i);
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            acc[c] = fmaf(x.x, w[i][0][c], fmaf(x.y, w[i][1][c], fmaf(x.z, w[i][2][c], fmaf(x.w, w[i][3][c], acc[c]))));
+        }
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        float v = acc[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == r) lgm[c] = v;
+      }
+    }
+    // ---- the loss math of row pb + lane (lanes < nr), learner.cpp:77-115
+    float dhm[NA];
+#pragma unroll
+    for (int c = 0; c < NA; ++c) dhm[c] = 0.f;
+    if (lane < nr) {
+      const int p = pb + lane;
+      double lg[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) lg[c] = (double)lgm[c] + (double)bhv[c];
+      const double value = lg[NA - 1];
+      double logp, ent, mx = 0.0, lse = 0.0;
+      const int a = continuous ? 0 : act_disc[p];
+      if (!continuous) {
+        mx = lg[0];
+#pragma unroll
+        for (int c = 1; c < NA - 1; ++c) mx = fmax(mx, lg[c]);
+        double se = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c) se += exp(lg[c] - mx);
+        lse = log(se);
+        double lga = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c)
+          if (c == a) lga = lg[c];
+        logp = lga - mx - lse;
+        ent = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c) {
+          const double lp = lg[c] - mx - lse;
+          ent -= exp(lp) * lp;
+        }
+      } else {
+        double q = 0.0, sls = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c) {
+          const double ls = log_std[c];
+          const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * exp(-ls);
+          q += z * z;
+          sls += ls;
+        }
+        logp = -0.5 * q - sls - 0.5 * kLog2Pi * A;
+        ent = sls + 0.5 * (1.0 + kLog2Pi) * A;
+      }
+      const double ratio = exp(logp - (double)old_logp[p]);
+      const double A_ = adv[p];
+      const double wv = frozen_w ? (double)frozen_w[p] : fmin(ratio, is_cap);
+      const double s1 = ratio * A_;
+      const double cr = fmin(fmax(ratio, 1.0 - clip), 1.0 + clip);
+      const double s2 = cr * A_;
+      const double sur = fmin(s1, s2);
+      const double verr = value - (double)ret[p];
+      st[0] += wv * sur;
+      st[1] += verr * verr;
+      st[2] += ent;
+      st[3] += ratio;
+      st[4] += (ratio < 1.0 - clip || ratio > 1.0 + clip) ? 1.0 : 0.0;  // strict (learner.cpp:104)
+      st[5] += wv;
+      st[6] = fmax(st[6], wv);
+      if (is_w) is_w[p] = (float)wv;
+      // cmin tie -> first argument (tape.cpp:157); clip mask inclusive (tape.cpp:146)
+      const double m1 = s1 <= s2 ? 1.0 : 0.0;
+      const double cm = (ratio >= 1.0 - clip && ratio <= 1.0 + clip) ? 1.0 : 0.0;
+      const double dratio = -wv * inv_S * (m1 * A_ + (1.0 - m1) * A_ * cm);
+      const double dlogp = dratio * ratio;
+      double dh[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) dh[c] = 0.0;
+      if (!continuous) {
+        double G[NA], sumG = 0.0;
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c) {
+          const double lp = lg[c] - mx - lse;
+          const double pc = exp(lp);
+          G[c] = (c == a ? dlogp : 0.0) + gH * (-pc - pc * lp);
+          sumG += G[c];
+        }
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c) dh[c] = G[c] - exp(lg[c] - mx - lse) * sumG;
+      } else {
+#pragma unroll
+        for (int c = 0; c < NA - 1; ++c) {
+          const double ls = log_std[c];
+          const double inv = exp(-ls);
+          const double z = ((double)act_cont[(size_t)p * A + c] - lg[c]) * inv;
+          dh[c] = dlogp * z * inv;
+          dlsv[c] += dlogp * (z * z - 1.0) + gH;
+        }
+      }
+      dh[NA - 1] = vcoef * verr * inv_S;
+#pragma unroll
+      for (int c = 0; c < NA; ++c) dhm[c] = (float)dh[c];
+    }
+    // ---- head gradient and dhidden = dhead wh^T from the staged rows
+    for (int r = 0; r < nr; ++r) {
+      const int p = pb + r;
+      const float* row = rows + (size_t)r * H;
+      float dhf[NA];
+#pragma unroll
+      for (int c = 0; c < NA; ++c) {
+        dhf[c] = __shfl_sync(0xffffffffu, dhm[c], r);
+        bacc[c] += dhf[c];
+      }
+#pragma unroll
+      for (int i = 0; i < HV; ++i)
+        if (i < hv) {
+          const float4 x = *reinterpret_cast<const float4*>(row + 4 * lane + 128 * i);
+          const float xe[4] = {x.x, x.y, x.z, x.w};
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float sacc = 0.f;
+#pragma unroll
+            for (int c = 0; c < NA; ++c) {
+              wacc[i][e][c] = fmaf(xe[e], dhf[c], wacc[i][e][c]);
+              sacc = fmaf(dhf[c], w[i][e][c], sacc);
+            }
+            o[e] = sacc;
+          }
+          __stcs(reinterpret_cast<float4*>(dhidden + (size_t)p * H + 4 * lane + 128 * i),
+                 make_float4(o[0], o[1], o[2], o[3]));
+        }
+    }
+    __syncwarp();  // every lane is done with the staged rows before the next bulk copy lands there
+  }
+  // block sums of the head gradient, warps added in a fixed order (deterministic);
+  // the staged-row buffer of warp 0 is reused as the accumulator
+  __syncthreads();
+  float* s_hg = s_rows;
+  for (int i = threadIdx.x; i < H * NA + NA; i += blockDim.x) s_hg[i] = 0.f;
+  for (int ww = 0; ww < kStageWarps; ++ww) {
+    __syncthreads();
+    if (warp == ww) {
+#pragma unroll
+      for (int i = 0; i < HV; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int c = 0; c < NA; ++c)
+            if (i < hv) s_hg[(4 * lane + 128 * i + e) * NA + c] += wacc[i][e][c];
+      if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < NA; ++c) s_hg[H * NA + c] += bacc[c];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < H * NA + NA; i += blockDim.x) hpart[(size_t)blockIdx.x * (H * NA + NA) + i] = s_hg[i];
+  // statistics and the log_std gradient over the lanes (fixed xor tree), then the block
+#pragma unroll
+  for (int k = 0; k < kLossStats; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double y = __shfl_xor_sync(0xffffffffu, st[k], o);
+      st[k] = (k == 6) ? fmax(st[k], y) : st[k] + y;
+    }
+  }
+  double dls = 0.0;
+#pragma unroll
+  for (int c = 0; c < NA; ++c) {
+    double v = dlsv[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == c) dls = v;
+  }
+  if (lane == 0)
+    for (int k = 0; k < kLossStats; ++k) s_red[warp][k] = st[k];
+  s_red[warp][kLossStats + lane] = dls;
+  __syncthreads();
+  if (threadIdx.x < kLossStats + 32) {
+    const int k = threadIdx.x;
+    double sum = 0.0;
+    for (int ww = 0; ww < kStageWarps; ++ww) sum = (k == 6) ? fmax(sum, s_red[ww][k]) : sum + s_red[ww][k];
+    part[(size_t)blockIdx.x * (kLossStats + 32) + k] = sum;
+  }
+}
+
 __global__ void ppo_loss_final_kernel(const double* __restrict__ part, int nblk, int A, int continuous,
                                       double inv_S, int S, double vcoef, const double* __restrict__ alpha_p,
                                       LossStats* __restrict__ out, float* __restrict__ grad_ls,
@@ -1145,6 +1419,35 @@ __global__ void __launch_bounds__(1024) head_grad_final_kernel(const float* __re
 
 void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossArgs& a, Workspace& ws,
                  float* grad, LossStats* stats, bool want_grads) {
+  // staged path (ppo_loss_stage_kernel): the bench shapes (H = 512, A + 1 = 3)
+  if (want_grads && m.H % 128 == 0 && m.H <= 512 && (m.AH == 2 || m.AH == 3) && S > 0) {
+    const int blk_rows = kStageWarps * kStageRows;
+    const size_t ssmem = sizeof(float) * std::max((size_t)kStageWarps * kStageRows * m.H, (size_t)m.H * m.AH + m.AH);
+    static std::atomic<int> per_sm_cache[kMaxDevices][2];
+    std::atomic<int>& ps = per_sm_cache[dev_slot(c)][m.AH - 2];
+    auto kern = m.AH == 3 ? ppo_loss_stage_kernel<3> : ppo_loss_stage_kernel<2>;
+    int per_sm = ps.load();
+    if (!per_sm) {
+      VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+      VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageWarps * 32, ssmem));
+      per_sm = std::max(1, per_sm);
+      ps.store(per_sm);
+    }
+    const int nblk = std::max(1, std::min((int)cdiv(S, blk_rows), per_sm * c->num_sms));
+    const size_t nhg = (size_t)m.H * m.AH + m.AH;
+    ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));
+    ws.splitk.reserve(c, (size_t)nblk * nhg);
+    kern<<<nblk, kStageWarps * 32, ssmem, c->stream>>>(
+        S, m.H, m.A, m.continuous, ws.hidden.p, params + m.o_wh, params + m.o_bh,
+        m.continuous ? params + m.o_ls : nullptr, a.act_cont, a.act_disc, a.old_logp, a.adv, a.ret, a.frozen_w,
+        a.clip, a.is_cap, a.vcoef, a.alpha, 1.0 / (double)S, ws.dhidden.p, ws.is_w.p, ws.part.p, ws.splitk.p);
+    after_launch(c);
+    launch_pdl(c, ppo_loss_final_kernel, dim3(1), dim3(1024), 0, (const double*)ws.part.p, nblk, m.A, m.continuous,
+               1.0 / (double)S, S, a.vcoef, a.alpha, stats, m.continuous ? grad + m.o_ls : nullptr, grad + m.P);
+    launch_pdl(c, head_grad_final_kernel, dim3(cdiv(nhg, 32)), dim3(1024), 0, (const float*)ws.splitk.p, nblk,
+               (int)nhg, m.H * m.AH, grad + m.o_wh, grad + m.o_bh);
+    return;
+  }
   const bool fuse = want_grads && m.H % 32 == 0 && m.H / 32 <= kHL && env_int("VER_LOSS_FUSE", 1);
   // fused path: kLossRows rows per warp-iteration with the loss math once per row
   // (ppo_loss_rows_kernel); VER_LOSS_ROWS=0 keeps one row per warp-iteration
