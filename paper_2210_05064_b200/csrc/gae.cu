@@ -14,9 +14,9 @@
 // 1024-step segments stay inside fp32 rounding of the fp64 reference.
 //
 // Two launches.  (1) gae_boot_kernel, one thread per env: the bootstrap of
-// every env tail that is not done is written into adv[tail] (adv is output
-// only, so it is free scratch until the scan overwrites it), missing ones are
-// reported.  (2) gae_scan_kernel: one pass over 512-slot WARP tiles, no block
+// every env tail that is not done is parked in the advantage word of the
+// tail's (A, R) pair (output only, so free scratch until the scan overwrites
+// it), missing ones are reported.  (2) gae_scan_kernel: one pass over 512-slot WARP tiles, no block
 // barrier and (in practice) no inter-tile waiting.  A warp claims tiles from
 // the END of the array (dynamic tile ids) and keeps the next tile in flight in
 // a per-warp ring of bulk copies.  Each tile also reads a 128-slot HALO above
@@ -33,7 +33,7 @@
 // fp32, then one fp64 warp suffix scan per row (the lane composite's discount
 // is the exact fp64 (gamma lambda)^8), rows / halo / carry composed in fp64,
 // then every slot is written once (float4 stores).
-// HBM traffic: r, V (4+4 B), done (1 B) read once, A, R (4+4 B) written once
+// HBM traffic: r, V (4+4 B), done (1 B) read once, the (A, R) pair (8 B) written once
 // = 17 B/step (the halo re-read is an L2 hit), plus 17 B per env tail for
 // the bootstrap pass.
 //
@@ -95,16 +95,16 @@ __device__ __forceinline__ int flag_acquire(volatile int* f) {
 }
 
 // learner.cpp:23-27 at env tails: V_next = bootstrap[e] unless done (ProtocolError
-// when it was never set).  One thread per env, the value parked in adv[tail].
+// when it was never set).  One thread per env, the value parked in ar[2 tail].
 __global__ void gae_boot_kernel(const int32_t* __restrict__ off, const uint8_t* __restrict__ done,
                                 const float* __restrict__ boot, const uint8_t* __restrict__ valid, int N,
-                                float* __restrict__ adv, int* __restrict__ err_env) {
+                                float* __restrict__ ar, int* __restrict__ err_env) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= N) return;
   const int o0 = off[e], o1 = off[e + 1];
   if (o1 <= o0 || (done[o1 - 1] & 1)) return;
   if (!valid[e]) atomicMin(err_env, e);
-  adv[o1 - 1] = boot[e];
+  ar[2 * (size_t)(o1 - 1)] = boot[e];
 }
 
 // Lane composite of n items: x -> b + a x, a = (gamma lambda)^n in fp64 or 0 (a
@@ -137,8 +137,7 @@ __device__ __forceinline__ Aff warp_suffix(Aff v, int lane) {
 __global__ void __launch_bounds__(32 * kGWarps) gae_scan_kernel(
     const float* __restrict__ reward, const float* __restrict__ value, const uint8_t* __restrict__ done,
     const int32_t* __restrict__ env_of, const int32_t* __restrict__ off, const float* __restrict__ boot, int F,
-    double gamma, double lambda, float* __restrict__ adv, float* __restrict__ ret, volatile GaeTileState* tiles,
-    int* tile_counter) {
+    double gamma, double lambda, float* __restrict__ ar, volatile GaeTileState* tiles, int* tile_counter) {
   extern __shared__ __align__(128) uint8_t gsmem[];
   __shared__ uint64_t s_full[kGWarps][kGStages];
   const int ntiles = (F + kGTile - 1) / kGTile;
@@ -237,7 +236,7 @@ __global__ void __launch_bounds__(32 * kGWarps) gae_scan_kernel(
       for (int q = kGItems - 1; q >= 0; --q) {
         const uint32_t b = (dd[k][q >> 2] >> (8 * (q & 3))) & 3u;
         float vn = vnext;
-        if (b == 2u) vn = __ldcg(adv + lo + j0 + q);  // env tail, not done: its bootstrap
+        if (b == 2u) vn = __ldcg(ar + 2 * (size_t)(lo + j0 + q));  // env tail, not done: its bootstrap
         const float mask = (b & 1u) ? 0.f : 1.f;
         const float ac = b ? 0.f : glf;
         dl[k][q] = fmaf(gf * vn, mask, rr[q]) - v[k][q];
@@ -250,7 +249,7 @@ __global__ void __launch_bounds__(32 * kGWarps) gae_scan_kernel(
     }
     // ---- the halo: 4 slots per lane, only its composed map is needed.  Its env
     // tails belong to the tile above, which may already have overwritten their
-    // parked bootstraps in adv: read boot[env] instead, the r-th tail of the
+    // parked bootstraps in ar: read boot[env] instead, the r-th tail of the
     // halo being env eh + r (or env_of when an env without fresh slots intervenes)
     Aff hc;
     {
@@ -337,18 +336,14 @@ __global__ void __launch_bounds__(32 * kGWarps) gae_scan_kernel(
         rv[q] = x + v[k][q];
       }
       const int i0 = lo + kGRow * k + kGItems * lane;
-      if (i0 + kGItems <= hi) {
-        __stcs(reinterpret_cast<float4*>(adv + i0), make_float4(av[0], av[1], av[2], av[3]));
-        __stcs(reinterpret_cast<float4*>(adv + i0) + 1, make_float4(av[4], av[5], av[6], av[7]));
-        __stcs(reinterpret_cast<float4*>(ret + i0), make_float4(rv[0], rv[1], rv[2], rv[3]));
-        __stcs(reinterpret_cast<float4*>(ret + i0) + 1, make_float4(rv[4], rv[5], rv[6], rv[7]));
+      if (i0 + kGItems <= hi) {  // (A, R) pairs: 64 contiguous bytes per lane
+        float4* o4 = reinterpret_cast<float4*>(ar + 2 * (size_t)i0);
+#pragma unroll
+        for (int q = 0; q < kGItems; q += 2) __stcs(o4 + q / 2, make_float4(av[q], rv[q], av[q + 1], rv[q + 1]));
       } else {
 #pragma unroll
         for (int q = 0; q < kGItems; ++q)
-          if (i0 + q < hi) {
-            adv[i0 + q] = av[q];
-            ret[i0 + q] = rv[q];
-          }
+          if (i0 + q < hi) reinterpret_cast<float2*>(ar)[i0 + q] = make_float2(av[q], rv[q]);
       }
     }
     // the tile below reads A_lo from here iff this tile's bottom 128 slots (its
@@ -386,19 +381,17 @@ __global__ void gae_gather_kernel(const uint64_t* __restrict__ keys, int F, cons
   d2[j] = (d[i] & 1) | (tail ? 2 : 0);
   e2[j] = e;
 }
-__global__ void gae_scatter_kernel(const uint64_t* __restrict__ keys, int F, const float* __restrict__ a2,
-                                   const float* __restrict__ ret2, float* __restrict__ adv,
-                                   float* __restrict__ ret) {
+__global__ void gae_scatter_kernel(const uint64_t* __restrict__ keys, int F, const float2* __restrict__ ar2,
+                                   float2* __restrict__ ar) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= F) return;
   const int i = (int)(keys[j] & 0xffffffffu);
-  adv[i] = a2[j];
-  ret[i] = ret2[j];
+  ar[i] = ar2[j];
 }
 
 static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, const int32_t* env, int F,
                      const float* boot, const uint8_t* valid, const int32_t* off, int N, double gamma,
-                     double lambda, float* adv, float* ret) {
+                     double lambda, float* ar) {
   if (F <= 0) return;
   const int ntiles = (F + kGTile - 1) / kGTile;
   DBuf<GaeTileState> tiles;
@@ -408,7 +401,7 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   tiles.zero(ntiles);
   VER_CUDA(cudaMemsetAsync(misc.p, 0, sizeof(int), c->stream));
   VER_CUDA(cudaMemsetAsync(misc.p + 1, 0x7f, sizeof(int), c->stream));  // 0x7f7f7f7f: none
-  gae_boot_kernel<<<cdiv(N, 256), 256, 0, c->stream>>>(off, d, boot, valid, N, adv, misc.p + 1);
+  gae_boot_kernel<<<cdiv(N, 256), 256, 0, c->stream>>>(off, d, boot, valid, N, ar, misc.p + 1);
   after_launch(c);
   static std::atomic<int> per_sm_cache[kMaxDevices];  // per device (0 = not probed yet)
   int per_sm = per_sm_cache[dev_slot(c)].load();
@@ -422,8 +415,8 @@ static void run_scan(Ctx* c, const float* r, const float* v, const uint8_t* d, c
   const int grid = std::min((ntiles + kGWarps - 1) / kGWarps, per_sm * c->num_sms);
   {
     ScopedEv ev(c, c->hbm_tag);
-    gae_scan_kernel<<<grid, 32 * kGWarps, kGSmem, c->stream>>>(r, v, d, env, off, boot, F, gamma, lambda, adv,
-                                                               ret, tiles.p, misc.p);
+    gae_scan_kernel<<<grid, 32 * kGWarps, kGSmem, c->stream>>>(r, v, d, env, off, boot, F, gamma, lambda, ar,
+                                                               tiles.p, misc.p);
     after_launch(c);
   }
   int* h = static_cast<int*>(c->pinned_buf(2 * sizeof(int)));
@@ -438,8 +431,7 @@ void compute_gae(DView& V, double gamma, double lambda) {
   if (V.size == 0) return;
   if (V.env_contiguous) {
     run_scan(c, V.reward.p, V.value.p, V.done.p, V.env_index.p, V.fresh_prefix, V.env_bootstrap.p,
-             V.env_bootstrap_valid.p,
-             V.env_offsets.p, V.N, gamma, lambda, V.advantage.p, V.returns.p);
+             V.env_bootstrap_valid.p, V.env_offsets.p, V.N, gamma, lambda, V.ar.p);
     return;
   }
   const int S = V.size, N = V.N;
@@ -457,22 +449,20 @@ void compute_gae(DView& V, double gamma, double lambda) {
   sync(c);
   const int F = *hF;
   if (F == 0) return;
-  DBuf<float> r2, v2, a2, ret2;
+  DBuf<float> r2, v2, ar2;
   DBuf<uint8_t> d2;
   DBuf<int32_t> e2;
   e2.reserve(c, F);
   r2.reserve(c, F);
   v2.reserve(c, F);
-  a2.reserve(c, F);
-  ret2.reserve(c, F);
+  ar2.reserve(c, 2 * (size_t)F);
   d2.reserve(c, F);
   gae_gather_kernel<<<cdiv(F, 256), 256, 0, c->stream>>>(keys.p, F, V.reward.p, V.value.p, V.done.p, r2.p,
                                                          v2.p, d2.p, e2.p);
   after_launch(c);
-  run_scan(c, r2.p, v2.p, d2.p, e2.p, F, V.env_bootstrap.p, V.env_bootstrap_valid.p, off.p, N, gamma, lambda, a2.p,
-           ret2.p);
-  gae_scatter_kernel<<<cdiv(F, 256), 256, 0, c->stream>>>(keys.p, F, a2.p, ret2.p, V.advantage.p,
-                                                          V.returns.p);
+  run_scan(c, r2.p, v2.p, d2.p, e2.p, F, V.env_bootstrap.p, V.env_bootstrap_valid.p, off.p, N, gamma, lambda, ar2.p);
+  gae_scatter_kernel<<<cdiv(F, 256), 256, 0, c->stream>>>(keys.p, F, reinterpret_cast<const float2*>(ar2.p),
+                                                          reinterpret_cast<float2*>(V.ar.p));
   after_launch(c);
 }
 

@@ -122,9 +122,10 @@ __global__ void h0_gather_kernel(const ver_seq_desc* __restrict__ seqs, int k, c
   out[i] = h0[(size_t)seqs[j].h0_index * H + u];
 }
 
-// replay batch rows: row offr[t] + i = view.obs[parent_i + t]
+// replay batch rows: row offr[t] + i = the obs of view slot parent_i + t (the
+// first D floats of its learner record, stride rs)
 __global__ void replay_obs_kernel(const int32_t* __restrict__ offr, int L, const int32_t* __restrict__ parent,
-                                  int R, const float* __restrict__ vobs, int D, float* __restrict__ out) {
+                                  int R, const float* __restrict__ vrec, int rs, int D, float* __restrict__ out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= R) return;
   int lo = 0, hi = L;
@@ -135,7 +136,7 @@ __global__ void replay_obs_kernel(const int32_t* __restrict__ offr, int L, const
   }
   const int t = lo, i = p - offr[t];
   const int s = parent[i] + t;
-  for (int d = 0; d < D; ++d) out[(size_t)p * D + d] = vobs[(size_t)s * D + d];
+  for (int d = 0; d < D; ++d) out[(size_t)p * D + d] = vrec[(size_t)s * rs + d];
 }
 __global__ void replay_h0_kernel(const int32_t* __restrict__ h0_index, int n, const float* __restrict__ vh0, int H,
                                  float* __restrict__ out) {
@@ -247,7 +248,8 @@ static void batch_h0(Learner& Ln, DView& V, DPacked& P, const float* params, flo
   Ln.wr.ensure(Ln.m, R, false);
   Ln.robs.reserve(c, (size_t)R * V.obs_dim);
   Ln.rh0.reserve(c, (size_t)n * H);
-  replay_obs_kernel<<<cdiv(R, 256), 256, 0, c->stream>>>(dm + 4 * n, L, dm, R, V.obs.p, V.obs_dim, Ln.robs.p);
+  replay_obs_kernel<<<cdiv(R, 256), 256, 0, c->stream>>>(dm + 4 * n, L, dm, R, V.rec.p, V.rs(), V.obs_dim,
+                                                         Ln.robs.p);
   after_launch(c);
   replay_h0_kernel<<<cdiv((size_t)n * H, 256), 256, 0, c->stream>>>(dm + n, n, V.h0.p, H, Ln.rh0.p);
   after_launch(c);

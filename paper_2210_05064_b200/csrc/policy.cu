@@ -1427,9 +1427,10 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
     std::atomic<int>& ps = per_sm_cache[dev_slot(c)][m.AH - 2];
     auto kern = m.AH == 3 ? ppo_loss_stage_kernel<3> : ppo_loss_stage_kernel<2>;
     int per_sm = ps.load();
-    if (!per_sm) {
-      VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
-      VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageWarps * 32, ssmem));
+    if (!per_sm) {  // attribute and occupancy for the largest staging buffer (H = 512), whatever H comes first
+      const size_t smax = sizeof(float) * (size_t)kStageWarps * kStageRows * 512;
+      VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      VER_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStageWarps * 32, smax));
       per_sm = std::max(1, per_sm);
       ps.store(per_sm);
     }

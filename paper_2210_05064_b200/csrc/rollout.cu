@@ -25,15 +25,11 @@ namespace verg {
 // ------------------------------------------------------------ DView alloc
 void DView::alloc_slots(int c) {
   cap = c;
-  obs.reserve(ctx, (size_t)c * obs_dim);
-  if (action_kind) act_cont.reserve(ctx, (size_t)c * act_dim);
-  else act_disc.reserve(ctx, c);
-  log_prob.reserve(ctx, c);
+  rec.reserve(ctx, (size_t)c * rs());
+  ar.reserve(ctx, (size_t)c * 2);
   value.reserve(ctx, c);
   reward.reserve(ctx, c);
   latency.reserve(ctx, c);
-  advantage.reserve(ctx, c);
-  returns.reserve(ctx, c);
   done.reserve(ctx, c);
   stale.reserve(ctx, c);
   replayed.reserve(ctx, c);
@@ -46,15 +42,11 @@ void DView::alloc_slots(int c) {
 void DView::grow_slots(int c) {
   if (c <= cap) return;
   const size_t s = size;
-  obs.grow_keep(ctx, (size_t)c * obs_dim, s * obs_dim);
-  if (action_kind) act_cont.grow_keep(ctx, (size_t)c * act_dim, s * act_dim);
-  else act_disc.grow_keep(ctx, c, s);
-  log_prob.grow_keep(ctx, c, s);
+  rec.grow_keep(ctx, (size_t)c * rs(), s * rs());
+  ar.grow_keep(ctx, (size_t)c * 2, s * 2);
   value.grow_keep(ctx, c, s);
   reward.grow_keep(ctx, c, s);
   latency.grow_keep(ctx, c, s);
-  advantage.grow_keep(ctx, c, s);
-  returns.grow_keep(ctx, c, s);
   done.grow_keep(ctx, c, s);
   stale.grow_keep(ctx, c, s);
   replayed.grow_keep(ctx, c, s);
@@ -102,10 +94,10 @@ struct LogDev {  // device mirror of the arrival log (SoA)
 };
 
 struct ViewDev {  // raw pointers of a DView for kernels
-  float* obs;
-  float* act_cont;
-  int32_t* act_disc;
-  float *log_prob, *value, *reward, *latency, *advantage, *returns;
+  float* rec;  // rs floats per slot: obs[D] | action | log_prob
+  float* ar;   // advantage, returns per slot
+  int rs;
+  float *value, *reward, *latency;
   uint8_t *done, *stale, *replayed;
   int32_t *env_index, *seq_of_slot, *step_in_episode;
   int64_t* episode_index;
@@ -114,10 +106,10 @@ struct ViewDev {  // raw pointers of a DView for kernels
   float* h0;
 };
 static ViewDev vdev(DView& v) {
-  return ViewDev{v.obs.p,        v.act_cont.p,  v.act_disc.p,  v.log_prob.p,        v.value.p,
-                 v.reward.p,     v.latency.p,   v.advantage.p, v.returns.p,          v.done.p,
-                 v.stale.p,      v.replayed.p,  v.env_index.p, v.seq_of_slot.p,      v.step_in_episode.p,
-                 v.episode_index.p, v.version.p, v.seqs.p,     v.h0.p};
+  return ViewDev{v.rec.p,      v.ar.p,        v.rs(),          v.value.p,           v.reward.p,
+                 v.latency.p,  v.done.p,      v.stale.p,       v.replayed.p,        v.env_index.p,
+                 v.seq_of_slot.p, v.step_in_episode.p, v.episode_index.p, v.version.p, v.seqs.p,
+                 v.h0.p};
 }
 
 // Scatter of the arrival log into env-major view order (rollout.cpp:143-181).
@@ -130,18 +122,18 @@ __global__ void compact_scatter_kernel(LogDev L, ViewDev V, const int32_t* __res
   if (r >= S) return;
   const int e = L.env[r];
   const int dst = offsets[e] + L.rank[r];
-  for (int j = 0; j < D; ++j) V.obs[(size_t)dst * D + j] = L.obs[(size_t)r * D + j];
+  float* rc = V.rec + (size_t)dst * V.rs;
+  for (int j = 0; j < D; ++j) rc[j] = L.obs[(size_t)r * D + j];
   if (continuous) {
-    for (int j = 0; j < A; ++j) V.act_cont[(size_t)dst * A + j] = L.act_cont[(size_t)r * A + j];
+    for (int j = 0; j < A; ++j) rc[D + j] = L.act_cont[(size_t)r * A + j];
   } else {
-    V.act_disc[dst] = L.act_disc[r];
+    rc[D] = __int_as_float(L.act_disc[r]);
   }
-  V.log_prob[dst] = L.log_prob[r];
+  rc[V.rs - 1] = L.log_prob[r];
   V.value[dst] = L.value[r];
   V.reward[dst] = L.reward[r];
   V.latency[dst] = L.latency[r];
-  V.advantage[dst] = 0.f;
-  V.returns[dst] = 0.f;
+  reinterpret_cast<float2*>(V.ar)[dst] = make_float2(0.f, 0.f);
   // bit 0: done; bit 1: last fresh slot of its env (the GAE scan's segment tail)
   V.done[dst] = (L.done[r] ? 1 : 0) | (L.rank[r] == counts[e] - 1 ? 2 : 0);
   V.stale[dst] = 0;
@@ -308,14 +300,14 @@ __global__ void synth_view_kernel(const int32_t* __restrict__ off, uint64_t seed
   const int s0 = off[e], len = off[e + 1] - s0;
   for (int t = threadIdx.x; t < len; t += blockDim.x) {
     const int i = s0 + t;
-    for (int q = 0; q < D; ++q) V.obs[(size_t)i * D + q] = hnorm(seed, i, 1 + q);
-    V.act_disc[i] = (int)(hmix(seed ^ hmix((uint64_t)i * 64 + 20)) & 1);
-    V.log_prob[i] = -0.6931472f + 0.1f * hnorm(seed, i, 21);
+    float* rc = V.rec + (size_t)i * V.rs;
+    for (int q = 0; q < D; ++q) rc[q] = hnorm(seed, i, 1 + q);
+    rc[D] = __int_as_float((int)(hmix(seed ^ hmix((uint64_t)i * 64 + 20)) & 1));
+    rc[D + 1] = -0.6931472f + 0.1f * hnorm(seed, i, 21);
     V.value[i] = hnorm(seed, i, 22);
     V.reward[i] = hnorm(seed, i, 23);
     V.latency[i] = 0.f;
-    V.advantage[i] = 0.f;
-    V.returns[i] = 0.f;
+    reinterpret_cast<float2*>(V.ar)[i] = make_float2(0.f, 0.f);
     const bool d = hunif(seed, i, 24) < p_done;
     V.done[i] = (d ? 1 : 0) | (t == len - 1 ? 2 : 0);
     V.stale[i] = 0;
@@ -467,18 +459,11 @@ __global__ void backfill_slots_kernel(ViewDev P, ViewDev V, const ver_seq_desc* 
   const int j = lo;
   const int sp = pseqs[ord[j]].start_offset + (q - cum[j]);
   const int dst = S + q;
-  for (int k = 0; k < D; ++k) V.obs[(size_t)dst * D + k] = P.obs[(size_t)sp * D + k];
-  if (continuous) {
-    for (int k = 0; k < A; ++k) V.act_cont[(size_t)dst * A + k] = P.act_cont[(size_t)sp * A + k];
-  } else {
-    V.act_disc[dst] = P.act_disc[sp];
-  }
-  V.log_prob[dst] = P.log_prob[sp];
+  for (int k = 0; k < V.rs; ++k) V.rec[(size_t)dst * V.rs + k] = P.rec[(size_t)sp * P.rs + k];
   V.value[dst] = P.value[sp];
   V.reward[dst] = P.reward[sp];
   V.latency[dst] = P.latency[sp];
-  V.advantage[dst] = P.advantage[sp];
-  V.returns[dst] = P.returns[sp];
+  reinterpret_cast<float2*>(V.ar)[dst] = reinterpret_cast<const float2*>(P.ar)[sp];
   V.done[dst] = P.done[sp] & 1;  // replayed slots carry no segment-tail bit
   V.stale[dst] = 1;
   V.replayed[dst] = 1;
@@ -553,6 +538,45 @@ __global__ void restale_kernel(const uint64_t* __restrict__ version, uint8_t* __
 }
 
 // ------------------------------------------------------- upload/download
+// record / pair columns <-> the reference's separate arrays (4-byte words, so
+// the int32 action bits travel as they are)
+__global__ void unpack_cols_kernel(const uint32_t* __restrict__ src, int stride, int off, int width, int n,
+                                   uint32_t* __restrict__ dst) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (size_t)n * width) return;
+  const size_t i = k / width, j = k % width;
+  dst[k] = src[i * stride + off + j];
+}
+__global__ void pack_cols_kernel(const uint32_t* __restrict__ src, int width, int n, uint32_t* __restrict__ dst,
+                                 int stride, int off) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (size_t)n * width) return;
+  const size_t i = k / width, j = k % width;
+  dst[i * stride + off + j] = src[k];
+}
+// host array (n x width 4-byte words) -> columns [off, off + width) of the strided device buffer
+static void up_cols(Ctx* c, float* dst, int stride, int off, const void* h, int width, int n) {
+  if (!n || !width) return;
+  if (!h) config_error("ver_view_upload: missing array");
+  DBuf<uint32_t> tmp;
+  tmp.reserve(c, (size_t)n * width);
+  tmp.upload(static_cast<const uint32_t*>(h), (size_t)n * width);
+  pack_cols_kernel<<<cdiv((size_t)n * width, 256), 256, 0, c->stream>>>(tmp.p, width, n,
+                                                                          reinterpret_cast<uint32_t*>(dst), stride, off);
+  after_launch(c);
+  sync(c);  // tmp and the (possibly pageable) host array
+}
+static void down_cols(Ctx* c, const float* src, int stride, int off, void* h, int width, int n) {
+  if (!h || !n || !width) return;
+  DBuf<uint32_t> tmp;
+  tmp.reserve(c, (size_t)n * width);
+  unpack_cols_kernel<<<cdiv((size_t)n * width, 256), 256, 0, c->stream>>>(reinterpret_cast<const uint32_t*>(src),
+                                                                            stride, off, width, n, tmp.p);
+  after_launch(c);
+  tmp.download(static_cast<uint32_t*>(h), (size_t)n * width);
+  sync(c);
+}
+
 template <class T>
 static void up_arr(Ctx* c, DBuf<T>& d, const T* h, size_t n) {
   if (n && !h) config_error("ver_view_upload: missing array");
@@ -582,15 +606,16 @@ static DView* upload_view(Ctx* c, const ver_view_host* h) {
   V->alloc_slots(std::max(S, 1));
   V->alloc_seqs(std::max(h->num_seqs, 1), std::max(h->h0_rows, 1));
   V->alloc_env();
-  up_arr(c, V->obs, h->obs, (size_t)S * h->obs_dim);
-  if (h->action_kind) up_arr(c, V->act_cont, h->act_cont, (size_t)S * h->act_dim);
-  else up_arr(c, V->act_disc, h->act_disc, S);
-  up_arr(c, V->log_prob, h->log_prob, S);
+  const int rs = V->rs(), D = h->obs_dim, AW = V->act_width();
+  up_cols(c, V->rec.p, rs, 0, h->obs, D, S);
+  if (h->action_kind) up_cols(c, V->rec.p, rs, D, h->act_cont, AW, S);
+  else up_cols(c, V->rec.p, rs, D, h->act_disc, 1, S);
+  up_cols(c, V->rec.p, rs, rs - 1, h->log_prob, 1, S);
   up_arr(c, V->value, h->value, S);
   up_arr(c, V->reward, h->reward, S);
   up_arr(c, V->latency, h->latency, S);
-  up_arr(c, V->advantage, h->advantage, S);
-  up_arr(c, V->returns, h->returns, S);
+  up_cols(c, V->ar.p, 2, 0, h->advantage, 1, S);
+  up_cols(c, V->ar.p, 2, 1, h->returns, 1, S);
   std::vector<uint8_t> done_bits;  // filled below once contiguity is known
   up_arr(c, V->stale, h->stale, S);
   up_arr(c, V->replayed, h->replayed, S);
@@ -644,16 +669,17 @@ static void down_arr(const DBuf<T>& d, T* h, size_t n) {
 }
 
 static void download_view(DView& V, ver_view_host* h) {
-  const int S = V.size;
-  down_arr(V.obs, h->obs, (size_t)S * V.obs_dim);
-  if (V.action_kind) down_arr(V.act_cont, h->act_cont, (size_t)S * V.act_dim);
-  else down_arr(V.act_disc, h->act_disc, S);
-  down_arr(V.log_prob, h->log_prob, S);
+  const int S = V.size, rs = V.rs(), D = V.obs_dim;
+  Ctx* c = V.ctx;
+  down_cols(c, V.rec.p, rs, 0, h->obs, D, S);
+  if (V.action_kind) down_cols(c, V.rec.p, rs, D, h->act_cont, V.act_dim, S);
+  else down_cols(c, V.rec.p, rs, D, h->act_disc, 1, S);
+  down_cols(c, V.rec.p, rs, rs - 1, h->log_prob, 1, S);
   down_arr(V.value, h->value, S);
   down_arr(V.reward, h->reward, S);
   down_arr(V.latency, h->latency, S);
-  down_arr(V.advantage, h->advantage, S);
-  down_arr(V.returns, h->returns, S);
+  down_cols(c, V.ar.p, 2, 0, h->advantage, 1, S);
+  down_cols(c, V.ar.p, 2, 1, h->returns, 1, S);
   down_arr(V.done, h->done, S);
   down_arr(V.stale, h->stale, S);
   down_arr(V.replayed, h->replayed, S);
@@ -702,15 +728,11 @@ static DView* clone_view(DView& V) {
   W->alloc_seqs(V.seq_cap, V.h0_cap);
   W->alloc_env();
   const size_t S = V.size;
-  clone_arr(c, W->obs, V.obs, S * V.obs_dim);
-  if (V.action_kind) clone_arr(c, W->act_cont, V.act_cont, S * V.act_dim);
-  else clone_arr(c, W->act_disc, V.act_disc, S);
-  clone_arr(c, W->log_prob, V.log_prob, S);
+  clone_arr(c, W->rec, V.rec, S * V.rs());
+  clone_arr(c, W->ar, V.ar, S * 2);
   clone_arr(c, W->value, V.value, S);
   clone_arr(c, W->reward, V.reward, S);
   clone_arr(c, W->latency, V.latency, S);
-  clone_arr(c, W->advantage, V.advantage, S);
-  clone_arr(c, W->returns, V.returns, S);
   clone_arr(c, W->done, V.done, S);
   clone_arr(c, W->stale, V.stale, S);
   clone_arr(c, W->replayed, V.replayed, S);

@@ -196,11 +196,13 @@ __global__ void batch_sizes_kernel(const int32_t* __restrict__ lens, int k, int 
 }
 // Time-major gather (learner.cpp:56-70) + slots (packseq.cpp:78-85) as a
 // shared-memory transpose.  Tile = 32 consecutive sorted pieces x 32
-// timesteps.  Read phase: each warp reads one piece's 32 consecutive view
-// slots per field (coalesced: a piece is contiguous in the view).  Write
+// timesteps.  Read phase: each warp reads one piece's consecutive view slots,
+// i.e. two contiguous runs (the slots' learner records, 16 B each at D = 2,
+// and their (A, R) pairs; view.cuh), so a short piece wastes at most the
+// partial DRAM sectors at the ends of two runs, not of five fields.  Write
 // phase: each warp writes one timestep's 32 consecutive packed rows per field
-// (coalesced: rows offsets[t] + j, j = 0..bs_t-1).  HBM traffic = the
-// algorithmic bytes (8D+36 B/step + the 4-byte slot).
+// (coalesced: rows offsets[t] + j, j = 0..bs_t-1).  Algorithmic bytes:
+// SURVEY §8d's 8D+36 B/step including the 4-byte slot.
 constexpr int kGT = 32;  // pieces per tile
 // Tile table entry: {piece block jb, (t0 << 3) | log2(TT)}.  TT (timesteps
 // per tile, power of two <= 32) follows the block's longest piece, so blocks
@@ -215,8 +217,7 @@ __device__ __forceinline__ T gld(const T* p) {
 __global__ void __launch_bounds__(256) gather_tiled_kernel(
     const int2* __restrict__ tiles, const ver_seq_desc* __restrict__ sorted, int k,
     const int32_t* __restrict__ offs, const int32_t* __restrict__ bs, int32_t* __restrict__ slots,
-    const float* __restrict__ v_obs, const int32_t* __restrict__ v_act, const float* __restrict__ v_actc,
-    const float* __restrict__ v_lp, const float* __restrict__ v_adv, const float* __restrict__ v_ret,
+    const float* __restrict__ v_rec, int rs, const float* __restrict__ v_ar,
     float* __restrict__ obs, int32_t* __restrict__ act, float* __restrict__ actc, float* __restrict__ lp,
     float* __restrict__ adv, float* __restrict__ ret, int D, int A, int continuous, int ntiles, int S) {
   extern __shared__ float tl[];  // F fields x 32 pieces x 33 (padded)
@@ -239,18 +240,24 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(
     if (t < s_len[jl]) {
       const int sl = s_start[jl] + t;
       int f = 0;
-      if (D == 2) {  // one 8-byte load per slot (no duplicate sector requests)
-        const float2 o2 = gld(reinterpret_cast<const float2*>(v_obs) + sl);
-        cell(f++, jl, tt) = o2.x;
-        cell(f++, jl, tt) = o2.y;
+      const float2 arv = gld(reinterpret_cast<const float2*>(v_ar) + sl);  // (A, R)
+      if (rs == 4 && !continuous) {  // D = 2 discrete: the whole record in one 16-byte load
+        const float4 r4 = gld(reinterpret_cast<const float4*>(v_rec) + sl);
+        cell(f++, jl, tt) = r4.x;
+        cell(f++, jl, tt) = r4.y;
+        cell(f++, jl, tt) = r4.w;
+        cell(f++, jl, tt) = arv.x;
+        cell(f++, jl, tt) = arv.y;
+        cell(f++, jl, tt) = r4.z;  // action bits
       } else {
-        for (int q = 0; q < D; ++q) cell(f++, jl, tt) = gld(v_obs + (size_t)sl * D + q);
+        const float* rc = v_rec + (size_t)sl * rs;
+        for (int q = 0; q < D; ++q) cell(f++, jl, tt) = gld(rc + q);
+        for (int q = 0; q < AC; ++q) cell(f++, jl, tt) = gld(rc + D + q);
+        cell(f++, jl, tt) = gld(rc + rs - 1);
+        cell(f++, jl, tt) = arv.x;
+        cell(f++, jl, tt) = arv.y;
+        if (!continuous) cell(f++, jl, tt) = gld(rc + D);
       }
-      for (int q = 0; q < AC; ++q) cell(f++, jl, tt) = v_actc[(size_t)sl * A + q];
-      cell(f++, jl, tt) = gld(v_lp + sl);
-      cell(f++, jl, tt) = gld(v_adv + sl);
-      cell(f++, jl, tt) = gld(v_ret + sl);
-      if (!continuous) cell(f++, jl, tt) = __int_as_float(gld(v_act + sl));
     }
   }
   __syncthreads();
@@ -301,8 +308,8 @@ void gather_packed(DView& V, DPacked& P) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ScopedEv ev(c, c->hbm_tag >= 0 ? c->hbm_tag + 1 : -1);
   kern<<<(unsigned)P.tile_table.size(), 256, smem, c->stream>>>(
-      P.tiles.p, P.seqs.p, P.k, P.offs.p, P.bs.p, P.slots.p, V.obs.p, V.act_disc.p, V.act_cont.p, V.log_prob.p,
-      V.advantage.p, V.returns.p, P.obs.p, P.act_disc.p, P.act_cont.p, P.old_logp.p, P.adv.p, P.ret.p, V.obs_dim,
+      P.tiles.p, P.seqs.p, P.k, P.offs.p, P.bs.p, P.slots.p, V.rec.p, V.rs(), V.ar.p, P.obs.p, P.act_disc.p,
+      P.act_cont.p, P.old_logp.p, P.adv.p, P.ret.p, V.obs_dim,
       V.act_dim, V.action_kind, (int)P.tile_table.size(), V.size);
   after_launch(c);
 }

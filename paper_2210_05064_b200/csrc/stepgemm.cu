@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     float* __restrict__ gates_out, float* __restrict__ hun_out, float* __restrict__ hprev_out,
     const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
     const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
-    const __grid_constant__ CUtensorMap bmap_lo, int blo) {
+    const __grid_constant__ CUtensorMap bmap_lo, int blo, long long* __restrict__ trace) {
   using namespace p2;
   constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
   extern __shared__ uint8_t smem_raw[];
@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   for (int si = 0; si < nsteps; ++si) {
     const Step S = steps[si];
     const int W = S.B > 0 ? S.tilesM * tilesN * S.Z : 0;  // tilesM in 256-row pair tiles
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si] = gtimer();
     const CUtensorMap* amap = amaps + si;
     for (int item = pair_id; item < W; item += npairs) {
       const bool first_item = item == pair_id;
@@ -650,9 +651,12 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
         }
       }
     }
+    if (trace && blockIdx.x == 0 && threadIdx.x == 128) trace[TR * si + 3] = gtimer();  // CTA 0's items stored
     grid_sync(bar, target);  // all partials of step si written
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
     gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
                     gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 5] = gtimer();
     if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
   }
   tc_fence_before();
@@ -805,14 +809,12 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     cfg.numAttrs = profiling() ? 1 : 2;
     ScopedEv ev(c, c->rec_tag);
     VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<DIR>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
-                                hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo));
+                                hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo, tr));
     after_launch(c);
-    return;
-  }
-  void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
-                  &part,  &bar,    &xp,     &h0,  &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre,
-                  &dhu,   &gz,     &tr,     const_cast<CUtensorMap*>(&bmap_lo), &blo};
-  {
+  } else {
+    void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
+                    &part,  &bar,    &xp,     &h0,  &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre,
+                    &dhu,   &gz,     &tr,     const_cast<CUtensorMap*>(&bmap_lo), &blo};
     ScopedEv ev(c, c->rec_tag);
     VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(THREADS), args, SMEM_BYTES, c->stream));
     after_launch(c);
@@ -823,7 +825,7 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     VER_CUDA(cudaStreamSynchronize(c->stream));
     // per step: rows, Z, then each slot and the next step's start relative to this step's start (ns)
     if (FILE* f = fopen(tpath, "a")) {
-      fprintf(f, "persist%d %d", DIR, nsteps);
+      fprintf(f, "%s%d %d", pair ? "pair" : "persist", DIR, nsteps);
       for (int i = 0; i < nsteps; ++i) {
         const long long t0 = h[TR * i];
         fprintf(f, " %d:%d", hs[i].Bg, hs[i].Z);

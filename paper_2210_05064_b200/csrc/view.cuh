@@ -1,14 +1,20 @@
-// view.cuh — device-resident RolloutView (rollout.hpp:33-78) in SoA layout.
+// view.cuh — device-resident RolloutView (rollout.hpp:33-78): the gathered learner
+// fields as one record per slot, everything else SoA.
 //
 // HBM layout (fp32 values, int32 indices, u8 flags; S = size, K = num_seqs):
-//   obs[S*D] act_disc[S] | act_cont[S*A]  log_prob value reward latency
-//   advantage returns [S]   done stale replayed [S] (u8)
+//   rec[S*RS]: the learner record of a slot, RS = D + AW + 1 floats:
+//              obs[D] | action (AW = 1: the int32 bits; continuous AW = A) | log_prob
+//   ar[S*2]:   advantage, returns (written by compute_gae)
+//   value reward latency [S]   done stale replayed [S] (u8)
 //   env_index seq_of_slot step_in_episode [S] (i32)  episode_index version [S] (64-bit)
 //   seqs[K] (ver_seq_desc, 32 B)   h0[K*H]
 //   per_env_counts[N] env_bootstrap[N] env_bootstrap_valid[N]
 //   env_offsets[N+1]  — exclusive scan of the per-env fresh counts, valid when
 //                       `env_contiguous` (every close_rollout/backfill output)
 // Capacities are sized for T*N so backfill_stale appends in place.
+// The time-major minibatch gather reads exactly rec and ar: two contiguous runs
+// per sequence piece instead of five scattered 4-byte fields, so short pieces
+// waste far fewer partial DRAM sectors (SURVEY §7 hard part 5).
 #pragma once
 
 #include "common.cuh"
@@ -27,8 +33,8 @@ struct DView {
   bool env_contiguous = false;
   int fresh_prefix = 0;
 
-  DBuf<float> obs, act_cont, log_prob, value, reward, latency, advantage, returns;
-  DBuf<int32_t> act_disc, env_index, seq_of_slot, step_in_episode;
+  DBuf<float> rec, ar, value, reward, latency;
+  DBuf<int32_t> env_index, seq_of_slot, step_in_episode;
   DBuf<uint8_t> done, stale, replayed;
   DBuf<int64_t> episode_index;
   DBuf<uint64_t> version;
@@ -39,6 +45,7 @@ struct DView {
   DBuf<uint8_t> env_bootstrap_valid;
 
   int act_width() const { return action_kind ? act_dim : 1; }
+  int rs() const { return obs_dim + act_width() + 1; }  // record stride (floats)
   // allocate slot arrays for `cap_` slots (contents not preserved)
   void alloc_slots(int cap_);
   // grow slot arrays to cap_ keeping the first `size` slots

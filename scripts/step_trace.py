@@ -8,7 +8,7 @@ FUSED = ["landed", "acc_ready", "pushed", "received", "gate_done", "next"]
 acc = defaultdict(lambda: defaultdict(list))
 for line in open(sys.argv[1]):
     tag, n, *rest = line.split()
-    if not tag.startswith(("persist", "fused")):
+    if not tag.startswith(("persist", "fused", "pair")):
         continue
     for x in rest:
         v = list(map(int, x.split(":")))
