@@ -627,7 +627,13 @@ ver_status ver_learner_load_checkpoint(ver_learner l, const char* path) {
   const J& pj = j.at("params");
   const ver_model_config mc = checkpoint_config(pj);
   const ver_model_config& lm = *learner_model_config(l);
-  if (std::memcmp(&mc, &lm, sizeof mc) != 0) config_error("load_checkpoint: model differs from the learner's");
+  // only the fields that fix tensor shapes for this action kind (an unused
+  // num_actions / act_dim may differ); the per-tensor rows / cols checks follow
+  const bool discrete = mc.action_kind == 0;
+  if (mc.obs_dim != lm.obs_dim || mc.encoder_dim != lm.encoder_dim || mc.hidden_dim != lm.hidden_dim ||
+      mc.action_kind != lm.action_kind || (discrete && mc.num_actions != lm.num_actions) ||
+      (!discrete && mc.act_dim != lm.act_dim))
+    config_error("load_checkpoint: model differs from the learner's");
   int64_t P = 0;
   int nt = 0;
   ver_param_count(&mc, &P, &nt);
