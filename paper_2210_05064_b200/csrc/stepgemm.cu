@@ -31,7 +31,7 @@ struct Step {
   int o, op;    // packed offsets of the GEMM / gate rows (forward: o = offs_t, op = offs_{t-1} or -1 for h0)
   int Z, per;   // split-K count, K-blocks per split
   int tilesM;
-  int pad;
+  int pad;      // pair forward: 1 = the gates run in the GEMM epilogue (Z == 1, H % 32 == 0)
 };
 
 __device__ __forceinline__ void grid_sync(unsigned* count, unsigned& target) {
@@ -54,6 +54,14 @@ constexpr int TR = 6;
 // K-blocks per TMEM accumulation group (tc::PROMOTE in the general GEMM): the
 // split-K items here hold <= 4 K-blocks at C2, so one drain per item
 constexpr int SGP = 4;
+// element i of a register-resident float4 array (i a compile-time constant after
+// unrolling, so no local-memory copy)
+template <int N>
+__device__ __forceinline__ float f4at(const float4 (&a)[N], int i) {
+  const float4 v = a[i >> 2];
+  const int k = i & 3;
+  return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+}
 __device__ __forceinline__ long long gtimer() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -189,7 +197,9 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
   // copy (policy.cu split_lo_kernel) by TMA; the split warps then only split A
   constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
+  // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* stg_all = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 2 * NACC);
@@ -437,6 +447,25 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
 // of the 128 x 128 single-CTA phase.  Used for the steps with >= 1024 rows
 // (the first ~50 steps of a C3 minibatch; VER_REC_PAIR_ROWS), launched as
 // clusters of 2 with all CTAs resident (one per SM).
+// Pair tile width per direction: the forward's N = 3H columns interleave the three
+// gates of each unit (column 3u + g), so its tiles are 192 columns = 64 whole
+// units (a 256-column tile would cut a unit at every boundary); that lets a
+// split-K-free forward step apply the GRU gates in the GEMM epilogue.
+template <int DIR>
+struct PairTile {
+  static constexpr int BN = DIR == 0 ? 192 : p2::BN2;
+  static constexpr int BNH = BN / 2;           // B columns per CTA
+  static constexpr int BBYTES = BNH * BK * 4;  // one CTA's B half of a stage
+};
+constexpr int kPairAccStride = p2::BN2;         // TMEM columns per accumulator buffer (2 x 256 allocated)
+// epilogue staging per warp: the partial-tile path uses 32 x SLD floats, the fused
+// gate path two [4][kFRow] row groups (row stride 100: conflict-free float4 rows)
+constexpr int kFRow = 100;
+constexpr int kFuseWarpFloats = 8 * kFRow > 32 * p2::SLD ? 8 * kFRow : 32 * p2::SLD;
+constexpr int kPairEpiBytes = p2::EPIW * kFuseWarpFloats * 4;
+constexpr int kPairSmem = p2::STAGES2 * p2::STAGE2 + kPairEpiBytes + 1024 + 256;
+static_assert(kPairSmem <= 232448, "smem budget");
+
 template <int DIR>
 __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     int nsteps, const Step* __restrict__ steps, const CUtensorMap* __restrict__ amaps,
@@ -448,17 +477,20 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     const __grid_constant__ CUtensorMap bmap_lo, int blo, long long* __restrict__ trace) {
   using namespace p2;
   constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
+  constexpr int PBN = PairTile<DIR>::BN, PBNH = PairTile<DIR>::BNH;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
+  // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + kPairEpiBytes);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int H3 = 3 * H, N = DIR == 0 ? H3 : H, K = DIR == 0 ? H : H3;
-  const int tilesN = (N + BN2 - 1) / BN2;
+  const int tilesN = (N + PBN - 1) / PBN;
   const int nkb_total = (K + BK - 1) / BK;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
@@ -496,7 +528,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   const uint32_t tmem = *tmem_slot;
   unsigned target = 0;
   int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
-  const uint32_t stage_tx = (blo ? 3u : 2u) * TILE;
+  const uint32_t stage_tx = TILE + (blo ? 2u : 1u) * (uint32_t)PairTile<DIR>::BBYTES;
 
   for (int si = 0; si < nsteps; ++si) {
     const Step S = steps[si];
@@ -506,13 +538,17 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     for (int item = pair_id; item < W; item += npairs) {
       const bool first_item = item == pair_id;
       const int nt = item % tilesN, q = item / tilesN;
-      const int m0 = (q % S.tilesM) * BM2, n0 = nt * BN2, z = q / S.tilesM;
+      const int m0 = (q % S.tilesM) * BM2, n0 = nt * PBN, z = q / S.tilesM;
       const int kb0 = z * S.per;
       const int nkb = max(0, min(nkb_total, kb0 + S.per) - kb0);
+      // K-blocks per accumulation group: a fused item accumulates all of K in TMEM,
+      // so the accumulator buffers alternate per item and the gate epilogue of one
+      // item overlaps the MMAs of the next
+      const int sgp = DIR == 0 && S.pad != 0 ? max(nkb, 1) : SGP;
       if (warp == 0) {
         if (lane == 0) {
           if (first_item) asm volatile("fence.proxy.async.global;" ::: "memory");  // rows of the gate phase
-          const int am = m0 + (int)rank * BM, bn = n0 + (int)rank * BNH;
+          const int am = m0 + (int)rank * BM, bn = n0 + (int)rank * PBNH;
           for (int i = 0; i < nkb; ++i, ++it_tma) {
             const int s = it_tma % STAGES2;
             const uint32_t ph = (it_tma / STAGES2) & 1;
@@ -524,11 +560,11 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
               if (blo) tma_load_2d(tileB(s, 1), &bmap_lo, full_bar(s), k0, bn);
             } else {
 #pragma unroll
-              for (int c = 0; c < BNH / 32; ++c)
+              for (int c = 0; c < PBNH / 32; ++c)
                 tma_load_2d(tileB(s, 0) + c * 4096, &bmap, full_bar(s), bn + 32 * c, k0);
               if (blo) {
 #pragma unroll
-                for (int c = 0; c < BNH / 32; ++c)
+                for (int c = 0; c < PBNH / 32; ++c)
                   tma_load_2d(tileB(s, 1) + c * 4096, &bmap_lo, full_bar(s), bn + 32 * c, k0);
               }
             }
@@ -537,13 +573,13 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
         }
       } else if (warp == 1) {
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) |
-                               ((uint32_t)BMAJ << 16) | ((uint32_t)(BN2 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
+                               ((uint32_t)BMAJ << 16) | ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
         if (leader && lane == 0) {
           int buf = 0;
           for (int i = 0; i < nkb; ++i, ++it_mma) {
             const int s = it_mma % STAGES2;
             const uint32_t ph = (it_mma / STAGES2) & 1;
-            const bool first = (i % SGP) == 0;
+            const bool first = (i % sgp) == 0;
             if (first) {
               buf = g_mma % NACC2;
               const int u = g_mma / NACC2;
@@ -551,7 +587,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
             }
             mbar_wait(split_bar(s), ph);
             tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(buf * BN2);
+            const uint32_t d = tmem + (uint32_t)(buf * kPairAccStride);
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
@@ -561,7 +597,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
               mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
             }
             commit2(empty_bar(s));
-            if ((i % SGP) == SGP - 1 || i == nkb - 1) {
+            if ((i % sgp) == sgp - 1 || i == nkb - 1) {
+              if (trace && blockIdx.x == 0) trace[TR * si + 1] = gtimer();  // last group issued
               commit2(acc_full(buf));
               ++g_mma;
             }
@@ -586,7 +623,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
 #pragma unroll 4
             for (int qq = et; qq < TILE / 16; qq += 32 * SPLITW) {
               alo[qq] = lo_tf32(ahi[qq]);
-              blo_t[qq] = lo_tf32(bhi[qq]);
+              if (qq < PairTile<DIR>::BBYTES / 16) blo_t[qq] = lo_tf32(bhi[qq]);
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -598,20 +635,137 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
         // column half (warp - 4) / 4)
         const int lq = warp & 3, half = (warp - 4) >> 2;
         const int lane_base = 32 * lq;
-        float* stg = stg_all + (warp - 4) * 32 * SLD;
-        const int ngroups = (nkb + SGP - 1) / SGP;
-        float sums[BNH];
+        float* stg = stg_all + (warp - 4) * kFuseWarpFloats;
+        const int mrow0 = m0 + (int)rank * BM + lane_base, ncol0 = n0 + half * PBNH;
+        if (DIR == 0 && S.pad != 0) {
+          // GRU gates (nn.cpp:235-250) in the epilogue of a split-K-free item: this
+          // warp's 32 rows x the 32 whole units [ncol0 / 3, ncol0 / 3 + 32).  The
+          // accumulator arrives lane = row (TMEM lanes); the gate math runs lane = unit
+          // so that every global access is a contiguous row segment (h / hUn / h_prev:
+          // 128 B, xp / gates: 384 B).  Rows go in groups of 4 through the warp's
+          // staging area: hU rows from their owner lanes, xp rows from coalesced float4
+          // loads issued one group ahead (the first group's during the item's MMAs).
+          float* fh = stg_all + (warp - 4) * kFuseWarpFloats;  // [4][kFRow] hU rows
+          float* fx = fh + 4 * kFRow;                            // [4][kFRow] xp rows, then gates
+          const int u0 = ncol0 / 3;
+          const bool colok = ncol0 < N;
+          const int blast = max(S.B - 1, 0);
+          const float* hsrc = S.op < 0 ? h0 : hidden + (size_t)S.op * H;
+          {
+            const int m = min(mrow0 + lane, blast);
+            const float* xr = xp + ((size_t)S.o + m) * N + (colok ? ncol0 : 0);
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(xr));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + 32));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + 64));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(hsrc + (size_t)m * H + u0));
+          }
+          const int xl = lane < 24 ? 4 * lane : 0;  // this lane's float4 of a 96-column xp row
+          float4 xva[4], xvb[4];
+          float hva[4], hvb[4];
+#define VER_FUSED_LOAD(k, xv, hv)                                                                \
+  _Pragma("unroll") for (int r = 0; r < 4; ++r) {                                                \
+    const int m = min(mrow0 + 4 * (k) + r, blast);                                               \
+    xv[r] = *reinterpret_cast<const float4*>(xp + ((size_t)S.o + m) * N + (colok ? ncol0 + xl : 0)); \
+    hv[r] = hsrc[(size_t)m * H + (colok ? u0 + lane : 0)];                                       \
+  }
+          VER_FUSED_LOAD(0, xva, hva)
+          VER_FUSED_LOAD(1, xvb, hvb)
+          const int buf = g_epi % NACC2;
+          mbar_wait(acc_full(buf), (g_epi / NACC2) & 1);
+          if (trace && blockIdx.x == 0 && threadIdx.x == 128) trace[TR * si + 2] = gtimer();  // last acc ready
+          tc_fence_after();
+          float acc[PBNH];
 #pragma unroll
-        for (int j = 0; j < BNH; ++j) sums[j] = 0.f;
+          for (int cc = 0; cc < PBNH / 32; ++cc) {
+            uint32_t r[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * kPairAccStride + half * PBNH + cc * 32)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __uint_as_float(r[j]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));  // TMEM free for the item after next
+          ++g_epi;
+#define VER_FUSED_GROUP(k, xv, hv)                                                            \
+          { \
+            if ((lane >> 2) == (k)) { \
+              float4* d = reinterpret_cast<float4*>(fh + (lane & 3) * kFRow); \
+_Pragma("unroll") \
+              for (int q = 0; q < PBNH / 4; ++q) d[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]); \
+            } \
+            if (lane < 24) { \
+_Pragma("unroll") \
+              for (int r = 0; r < 4; ++r) *reinterpret_cast<float4*>(fx + r * kFRow + xl) = xv[r]; \
+            } \
+            float hp[4]; \
+_Pragma("unroll") \
+            for (int r = 0; r < 4; ++r) hp[r] = hv[r]; \
+            __syncwarp(); \
+            if ((k) + 2 < 8) { VER_FUSED_LOAD((k) + 2, xv, hv) } \
+_Pragma("unroll") \
+            for (int r = 0; r < 4; ++r) { \
+              const int m = mrow0 + 4 * (k) + r; \
+              const float* sh = fh + r * kFRow + 3 * lane; \
+              float* sx = fx + r * kFRow + 3 * lane; \
+              const float rg = gate_sigm(sx[0] + sh[0]); \
+              const float zg = gate_sigm(sx[1] + sh[1]); \
+              const float ng = gate_tanh(sx[2] + rg * sh[2]); \
+              if (m < S.B && colok) { \
+                const size_t row = ((size_t)S.o + m) * H + u0 + lane; \
+                hidden[row] = (1.f - zg) * ng + zg * hp[r]; \
+                if (gates_out) { \
+                  hun_out[row] = sh[2]; \
+                  hprev_out[row] = hp[r]; \
+                } \
+              } \
+              sx[0] = rg; \
+              sx[1] = zg; \
+              sx[2] = ng; \
+            } \
+            __syncwarp(); \
+            if (gates_out && lane < 24 && colok) { \
+_Pragma("unroll") \
+              for (int r = 0; r < 4; ++r) { \
+                const int m = mrow0 + 4 * (k) + r; \
+                if (m < S.B) \
+                  *reinterpret_cast<float4*>(gates_out + ((size_t)S.o + m) * N + ncol0 + xl) = \
+                      *reinterpret_cast<const float4*>(fx + r * kFRow + xl); \
+              } \
+            } \
+            __syncwarp(); \
+          }
+#pragma unroll 1
+          for (int k = 0; k < 8; k += 2) {
+            VER_FUSED_GROUP(k, xva, hva)
+            VER_FUSED_GROUP(k + 1, xvb, hvb)
+          }
+#undef VER_FUSED_GROUP
+#undef VER_FUSED_LOAD
+          continue;
+        }
+        const int ngroups = (nkb + sgp - 1) / sgp;
+        float sums[PBNH];
+#pragma unroll
+        for (int j = 0; j < PBNH; ++j) sums[j] = 0.f;
         for (int gq = 0; gq < ngroups; ++gq, ++g_epi) {
           const int buf = g_epi % NACC2;
           mbar_wait(acc_full(buf), (g_epi / NACC2) & 1);
+          if (trace && blockIdx.x == 0 && threadIdx.x == 128) trace[TR * si + 2] = gtimer();  // last acc ready
           tc_fence_after();
 #pragma unroll
-          for (int cc = 0; cc < BNH / 32; ++cc) {
+          for (int cc = 0; cc < PBNH / 32; ++cc) {
             uint32_t r[32];
             const uint32_t taddr =
-                tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * BN2 + half * BNH + cc * 32);
+                tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * kPairAccStride + half * PBNH + cc * 32);
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -630,9 +784,10 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
         }
         const int rr = lane >> 2, c4 = (lane & 3) * 4;
-        const int mrow0 = m0 + (int)rank * BM + lane_base, ncol0 = n0 + half * BNH;
+        // partial tile part[z][m][n] through the staging buffer (each warp store
+        // covers 4 rows x 64 contiguous bytes)
 #pragma unroll
-        for (int cb = 0; cb < BNH / 16; ++cb) {
+        for (int cb = 0; cb < PBNH / 16; ++cb) {
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq)
             *reinterpret_cast<float4*>(stg + lane * SLD + 4 * qq) =
@@ -652,6 +807,10 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
       }
     }
     if (trace && blockIdx.x == 0 && threadIdx.x == 128) trace[TR * si + 3] = gtimer();  // CTA 0's items stored
+    if (DIR == 0 && S.pad != 0) {  // the epilogue applied the gates: h_t is complete
+      if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
+      continue;
+    }
     grid_sync(bar, target);  // all partials of step si written
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
     gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
@@ -685,21 +844,27 @@ static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
   return s;
 }
 
-// pair mode: 256-row x 256-column tiles over the resident CTA pairs
-static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs) {
+// pair mode: 256-row x BN-column tiles over the resident CTA pairs.  fuse (the
+// forward with H % 32 == 0): a step whose split-K count comes out 1 -- or whose
+// tiles fill at least fuse_min_items work items -- runs split-K free with the gates
+// in the GEMM epilogue
+static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs, int BN, bool fuse,
+                       int fuse_min_items) {
   Step s{};
   s.B = B;
   s.Bg = Bg;
   s.o = o;
   s.op = op;
   s.tilesM = (int)cdiv(std::max(B, 1), p2::BM2);
-  const int tilesN = (int)cdiv(N, p2::BN2);
+  const int tilesN = (int)cdiv(N, BN);
   const int nkb = (K + BK - 1) / BK;
   int Z = std::max(1, std::min(pairs / std::max(1, s.tilesM * tilesN), std::max(1, nkb / 2)));
   Z = std::min(Z, 8);
+  if (fuse && s.tilesM * tilesN >= fuse_min_items) Z = 1;
   const int per = (nkb + Z - 1) / Z;
   s.Z = (nkb + per - 1) / per;
   s.per = per;
+  s.pad = fuse && s.Z == 1 ? 1 : 0;
   return s;
 }
 
@@ -711,11 +876,11 @@ static int step_pairs(Ctx* c) {
   int pairs = cache[dev_slot(c)].load();
   if (!pairs) {
     const void* fn = reinterpret_cast<const void*>(gru_step_gemm2_kernel<DIR>);
-    VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, p2::SMEM2));
+    VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(c->num_sms);
     cfg.blockDim = dim3(p2::THREADS2);
-    cfg.dynamicSmemBytes = p2::SMEM2;
+    cfg.dynamicSmemBytes = kPairSmem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -794,7 +959,7 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(p2::THREADS2);
-    cfg.dynamicSmemBytes = p2::SMEM2;
+    cfg.dynamicSmemBytes = kPairSmem;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -859,10 +1024,12 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
     std::vector<sg::Step> hs;
     std::vector<CUtensorMap> maps;
     const int pairs = part == 0 ? sg::step_pairs<0>(c) : 0;
+    const bool fuse = H % 32 == 0 && env_int("VER_REC_FUSE", 1) != 0;
+    const int fuse_min = env_int("VER_REC_FUSE_MIN", 1 << 30);
     for (int t = ta; t < tz; ++t) {
       const int B = h_bs[t];
       const int op = t == 0 ? -1 : h_offs[t - 1];
-      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs)
+      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse, fuse_min)
                              : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms));
       const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
       maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
@@ -888,7 +1055,7 @@ void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t
     const int pairs = part == 1 ? sg::step_pairs<1>(c) : 0;
     for (int t = hi; t >= lo; --t) {
       const int B = h_bs[t], Bp = h_bs[t - 1];
-      hs.push_back(part == 1 ? sg::make_step2(B, Bp, h_offs[t], h_offs[t - 1], H, H3, pairs)
+      hs.push_back(part == 1 ? sg::make_step2(B, Bp, h_offs[t], h_offs[t - 1], H, H3, pairs, sg::PairTile<1>::BN, false, 0)
                              : sg::make_step(B, Bp, h_offs[t], h_offs[t - 1], H, H3, c->num_sms));
       maps.push_back(tc::make_map(ws.dhu.p + (size_t)h_offs[t] * H3, std::max(B, 1), H3, H3, tc::BM, false));
     }

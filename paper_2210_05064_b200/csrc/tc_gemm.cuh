@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_gemm_kernel(const __grid_consta
                                                              int N, int K, int kb_per_split, int nsplit, Epi epi,
                                                              const __grid_constant__ CUtensorMap tmBl, int promote) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
+  // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* stg_all = reinterpret_cast<float*>(smem + tc::STAGES * tc::STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc::STAGES * tc::STAGE_BYTES + EPI_BYTES);
   // bars: full[S] split[S] empty[S] acc_full[NACC] acc_empty[NACC]; then the TMEM address slot
@@ -589,7 +591,9 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmBl,
                                                                int promote) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
+  // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI2);
   // bars: full[S] split[S] empty[S] acc_full[NACC2] acc_empty[NACC2]; then the TMEM address slot
