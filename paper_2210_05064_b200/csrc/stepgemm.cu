@@ -48,6 +48,14 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned& target) {
   __syncthreads();
 }
 
+// wait until *p >= need (acquire at gpu scope: the counted-in stores are visible)
+__device__ __forceinline__ void spin_acquire(const unsigned* p, unsigned need) {
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  } while (v < need);
+}
+
 // VER_REC_TRACE slots per step (CTA 0): start, first stage landed, last
 // accumulator ready, partial stored, GEMM-phase barrier passed, gate done
 constexpr int TR = 6;
@@ -474,7 +482,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     float* __restrict__ gates_out, float* __restrict__ hun_out, float* __restrict__ hprev_out,
     const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
     const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
-    const __grid_constant__ CUtensorMap bmap_lo, int blo, long long* __restrict__ trace) {
+    const __grid_constant__ CUtensorMap bmap_lo, int blo, long long* __restrict__ trace, int rbs) {
   using namespace p2;
   constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
   constexpr int PBN = PairTile<DIR>::BN, PBNH = PairTile<DIR>::BNH;
@@ -527,6 +535,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   unsigned target = 0;
+  unsigned* const rbf = bar + 32;  // row-tile counters of the fused steps, [nsteps][rbs]
   int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
   const uint32_t stage_tx = TILE + (blo ? 2u : 1u) * (uint32_t)PairTile<DIR>::BBYTES;
 
@@ -545,9 +554,19 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
       // so the accumulator buffers alternate per item and the gate epilogue of one
       // item overlaps the MMAs of the next
       const int sgp = DIR == 0 && S.pad != 0 ? max(nkb, 1) : SGP;
+      // Row-block dataflow after a fused step (no grid barrier): this item's A rows
+      // (h_{t-1}, pair row tile m0 / BM2) are complete once all 2 x EPIW epilogue
+      // warps of the previous step's tilesN items on that row tile have counted in
+      unsigned* dep = DIR == 0 && si > 0 && steps[si - 1].pad != 0 ? rbf + (size_t)(si - 1) * rbs + m0 / BM2 : nullptr;
+      const unsigned dep_need = 2u * EPIW * (unsigned)tilesN;
       if (warp == 0) {
         if (lane == 0) {
-          if (first_item) asm volatile("fence.proxy.async.global;" ::: "memory");  // rows of the gate phase
+          if (dep) {
+            spin_acquire(dep, dep_need);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> TMA reads
+          } else if (first_item) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // rows of the gate phase
+          }
           const int am = m0 + (int)rank * BM, bn = n0 + (int)rank * PBNH;
           for (int i = 0; i < nkb; ++i, ++it_tma) {
             const int s = it_tma % STAGES2;
@@ -659,6 +678,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
             asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + 64));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(hsrc + (size_t)m * H + u0));
           }
+          if (dep) spin_acquire(dep, dep_need);  // h_{t-1} rows of this row tile (read below)
           const int xl = lane < 24 ? 4 * lane : 0;  // this lane's float4 of a 96-column xp row
           float4 xva[4], xvb[4];
           float hva[4], hvb[4];
@@ -750,6 +770,10 @@ _Pragma("unroll") \
           }
 #undef VER_FUSED_GROUP
 #undef VER_FUSED_LOAD
+          // this warp's h_t rows of row tile m0 / BM2 are written: count in
+          __threadfence();
+          __syncwarp();
+          if (lane == 0) atomicAdd(rbf + (size_t)si * rbs + m0 / BM2, 1u);
           continue;
         }
         const int ngroups = (nkb + sgp - 1) / sgp;
@@ -807,10 +831,7 @@ _Pragma("unroll") \
       }
     }
     if (trace && blockIdx.x == 0 && threadIdx.x == 128) trace[TR * si + 3] = gtimer();  // CTA 0's items stored
-    if (DIR == 0 && S.pad != 0) {  // the epilogue applied the gates: h_t is complete
-      if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
-      continue;
-    }
+    if (DIR == 0 && S.pad != 0) continue;  // gates applied in the epilogues; the next step's items wait per row tile
     grid_sync(bar, target);  // all partials of step si written
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
     gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
@@ -845,11 +866,11 @@ static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
 }
 
 // pair mode: 256-row x BN-column tiles over the resident CTA pairs.  fuse (the
-// forward with H % 32 == 0): a step whose split-K count comes out 1 -- or whose
-// tiles fill at least fuse_min_items work items -- runs split-K free with the gates
-// in the GEMM epilogue
+// forward with H % 32 == 0): a step whose split-K count comes out 1 runs with the
+// gates in the GEMM epilogue (forcing Z = 1 on the smaller steps measured slower;
+// force_fuse is for the sanitizer / small tests, which never reach Z = 1 naturally)
 static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs, int BN, bool fuse,
-                       int fuse_min_items) {
+                       bool force_fuse = false) {
   Step s{};
   s.B = B;
   s.Bg = Bg;
@@ -860,7 +881,7 @@ static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs, in
   const int nkb = (K + BK - 1) / BK;
   int Z = std::max(1, std::min(pairs / std::max(1, s.tilesM * tilesN), std::max(1, nkb / 2)));
   Z = std::min(Z, 8);
-  if (fuse && s.tilesM * tilesN >= fuse_min_items) Z = 1;
+  if (fuse && force_fuse) Z = 1;
   const int per = (nkb + Z - 1) / Z;
   s.Z = (nkb + per - 1) / per;
   s.per = per;
@@ -913,8 +934,11 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
   uint8_t* mbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws.sgmaps.p) + 63) & ~uintptr_t(63));
   VER_CUDA(cudaMemcpyAsync(ws.sgsteps.p, hs.data(), sizeof(Step) * nsteps, cudaMemcpyHostToDevice, c->stream));
   VER_CUDA(cudaMemcpyAsync(mbase, maps.data(), sizeof(CUtensorMap) * nsteps, cudaMemcpyHostToDevice, c->stream));
-  ws.bar.reserve(c, 32);
-  ws.bar.zero(32);
+  int rbs = 1;  // row tiles per step in the pair launch (step 0 has the most rows)
+  for (const Step& st : hs) rbs = std::max(rbs, st.tilesM);
+  const size_t nbar = pair ? 32 + (size_t)nsteps * rbs : 32;
+  ws.bar.reserve(c, nbar);
+  ws.bar.zero(nbar);
   const float* ux = params + m.o_ux;
   const CUtensorMap bmap = DIR == 0 ? make_map(ux, H, H3, H3, 32, true) : make_map(ux, H, H3, H3, BN, false);
   // U's lo copy (made by the forward that precedes this launch, policy.cu)
@@ -974,7 +998,7 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     cfg.numAttrs = profiling() ? 1 : 2;
     ScopedEv ev(c, c->rec_tag);
     VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<DIR>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
-                                hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo, tr));
+                                hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo, tr, rbs));
     after_launch(c);
   } else {
     void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
@@ -1024,12 +1048,12 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
     std::vector<sg::Step> hs;
     std::vector<CUtensorMap> maps;
     const int pairs = part == 0 ? sg::step_pairs<0>(c) : 0;
-    const bool fuse = H % 32 == 0 && env_int("VER_REC_FUSE", 1) != 0;
-    const int fuse_min = env_int("VER_REC_FUSE_MIN", 1 << 30);
+    const bool fuse = H % 32 == 0;
+    const bool force_fuse = env_int("VER_REC_FUSE_ALL", 0) != 0;  // tests / sanitizer
     for (int t = ta; t < tz; ++t) {
       const int B = h_bs[t];
       const int op = t == 0 ? -1 : h_offs[t - 1];
-      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse, fuse_min)
+      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse, force_fuse)
                              : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms));
       const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
       maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
@@ -1055,7 +1079,7 @@ void gru_backward_big_persist(Ctx* c, const Model& m, const float* params, int t
     const int pairs = part == 1 ? sg::step_pairs<1>(c) : 0;
     for (int t = hi; t >= lo; --t) {
       const int B = h_bs[t], Bp = h_bs[t - 1];
-      hs.push_back(part == 1 ? sg::make_step2(B, Bp, h_offs[t], h_offs[t - 1], H, H3, pairs, sg::PairTile<1>::BN, false, 0)
+      hs.push_back(part == 1 ? sg::make_step2(B, Bp, h_offs[t], h_offs[t - 1], H, H3, pairs, sg::PairTile<1>::BN, false)
                              : sg::make_step(B, Bp, h_offs[t], h_offs[t - 1], H, H3, c->num_sms));
       maps.push_back(tc::make_map(ws.dhu.p + (size_t)h_offs[t] * H3, std::max(B, 1), H3, H3, tc::BM, false));
     }

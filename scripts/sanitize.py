@@ -5,7 +5,8 @@
     tiled gather on a ragged view;
   * one learner update at E = H = 512 (tcgen05 GEMMs incl. CTA pairs, the
     persistent step kernel forced from 6 rows, K-split kernels, cluster tail,
-    fused loss, Adam);
+    fused loss, Adam), and one with the CTA-pair step kernels from 6 rows and
+    every forward pair step fused (gate epilogue + row-tile dataflow);
   * one C1-shaped update (H = 64: register recurrence kernels);
   * the inference engine (act + on-device sampling) for a few batches.
 Prints one line per stage; any sanitizer report goes to its own output."""
@@ -36,8 +37,15 @@ def update(H, T, N, epochs=1, env=None):
     return view
 
 
+if "--pair-only" in sys.argv:  # just the fused CTA-pair update (for a full racecheck listing)
+    update(512, 16, 48, env={"VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6", "VER_REC_PAIR_ROWS": "6",
+                             "VER_REC_FUSE_ALL": "1"})
+    sys.exit(0)
 v = update(512, 16, 24, env={"VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6", "VER_REC_PAIR_ROWS": "200"})
-for k in ("VER_REC_BIG_FWD", "VER_REC_BIG_BWD", "VER_REC_PAIR_ROWS"):
+# CTA-pair step kernels with the fused forward epilogue and row-tile dataflow
+update(512, 16, 48, env={"VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6", "VER_REC_PAIR_ROWS": "6",
+                         "VER_REC_FUSE_ALL": "1"})
+for k in ("VER_REC_BIG_FWD", "VER_REC_BIG_BWD", "VER_REC_PAIR_ROWS", "VER_REC_FUSE_ALL"):
     os.environ.pop(k, None)
 update(64, 16, 16)
 lens = synth.ragged_lengths(1 << 16, seed=3)

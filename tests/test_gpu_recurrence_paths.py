@@ -4,7 +4,8 @@
 * the persistent K-split kernels (gru_fwd_ks / gru_bwd_ks),
 * the single-cluster tail kernels for the last short timesteps (H = 512),
 * the tcgen05 path for timesteps with many rows: the persistent split-K step
-  kernel (stepgemm.cu),
+  kernel (stepgemm.cu), single CTAs and CTA pairs, the latter with the forward
+  gates fused into the GEMM epilogue,
 
 each forced by the row thresholds (VER_REC_BIG_FWD / _BWD, VER_REC_TAIL_*),
 which the library reads at every launch.
@@ -30,6 +31,12 @@ PATHS = {
     # big steps (>= 6 rows) in the split-K tcgen05 step kernel (stepgemm.cu), K-split
     # for 5, cluster tail for <= 4 / <= 3 (the defaults)
     "big+ks+tail": {"VER_REC_TAIL": "1", "VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6"},
+    # big steps (>= 6 rows) on CTA pairs (the C3 path) with every forward step
+    # split-K free and its gates in the GEMM epilogue, consecutive steps chained
+    # per row tile instead of by a grid barrier (VER_REC_FUSE_ALL forces what only
+    # >= ~2,300-row steps reach naturally)
+    "pair+fused": {"VER_REC_TAIL": "1", "VER_REC_BIG_FWD": "6", "VER_REC_BIG_BWD": "6",
+                   "VER_REC_PAIR_ROWS": "6", "VER_REC_FUSE_ALL": "1"},
     # cluster tail for everything it can take, K-split for the rest
     "tail": {"VER_REC_TAIL": "1", "VER_REC_TAIL_FWD": "8", "VER_REC_TAIL_BWD": "8",
              "VER_REC_BIG_FWD": "100000", "VER_REC_BIG_BWD": "100000"},
