@@ -207,6 +207,49 @@ def host_bytes(wl):
     return int(b)
 
 
+def gru_latency(learner, view, phase, phase_n):
+    """SURVEY §8(d) GRU latency floor: L_max sequential timesteps x (fastest forward
+    step + fastest backward step) per minibatch, against the recurrence's measured
+    device time per minibatch.  One extra update (outside the timed region) with the
+    library's per-step globaltimer trace (VER_REC_TRACE); the fastest steps are the
+    1-row steps of the cluster tails."""
+    import tempfile
+    try:
+        with tempfile.NamedTemporaryFile("r", suffix=".txt", delete=False) as f:
+            path = f.name
+        os.environ["VER_REC_TRACE"] = path
+        try:
+            learner.update(view, read_stats=False)
+            learner.ctx.synchronize()
+        finally:
+            os.environ.pop("VER_REC_TRACE", None)
+        Ls, steps = [], {"fwd": [], "bwd": []}
+        for line in open(path):
+            tag, L, *rest = line.split()
+            if not (tag.startswith("fwd") or tag.startswith("bwd")):
+                continue
+            Ls.append(int(L))
+            pts = [tuple(map(int, x.split(":"))) for x in rest]
+            ts = [t for _, t in pts]
+            order = [t for t in (range(len(ts)) if tag.startswith("fwd") else range(len(ts) - 1, -1, -1)) if ts[t] > 0]
+            for a, b in zip(order, order[1:]):
+                if tag.endswith("tail"):
+                    steps[tag[:3]].append((ts[b] - ts[a]) / 1000.0)
+        os.unlink(path)
+        n_mb = max(1, phase_n.get("forward", 1))
+        Lmax = max(Ls) if Ls else 0
+        fmin = statistics.median(steps["fwd"]) if steps["fwd"] else 0.0
+        bmin = statistics.median(steps["bwd"]) if steps["bwd"] else 0.0
+        rec_mb = (phase.get("rec_fwd", 0.0) + phase.get("rec_bwd", 0.0)) / n_mb
+        floor_ms = Lmax * (fmin + bmin) / 1000.0
+        return {"L_max": Lmax, "fwd_step_us": fmin, "bwd_step_us": bmin,
+                "floor_ms_per_minibatch": floor_ms, "recurrence_ms_per_minibatch": rec_mb,
+                "floor_share": floor_ms / rec_mb if rec_mb > 0 else None,
+                "note": "floor = L_max x (median 1-row forward + backward step of the cluster tails)"}
+    except Exception as e:  # diagnostics only: never fail the bench line
+        return {"error": str(e)[:200]}
+
+
 def run_ours(args, rank, world):
     import torch
     import paper_2210_05064_b200 as V
@@ -298,6 +341,7 @@ def run_ours(args, rank, world):
         del v2
     e2e = max_over_ranks(statistics.median(e2e_ms))
     h2d = host_bytes(wl)
+    lat = gru_latency(learner, view, phase, phase_n) if rank == 0 else None
     del view
 
     # ---- configs[1] (C2): N = 256 envs, 4 epochs x 2 minibatches (extra field)
@@ -480,6 +524,8 @@ def run_ours(args, rank, world):
             "e2e": {"value": fresh * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * 12, "ms_per_step": e2e},
         }
+        if lat:
+            line["gru_latency"] = lat
         if c2:
             line["c2"] = c2
         if gg:

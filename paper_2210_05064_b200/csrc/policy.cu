@@ -436,11 +436,53 @@ static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, 
 constexpr int kMaxD = 8;  // obs_dim bound of the encoder-input kernels (Model::make checks it)
 
 // ----------------------------------------------------------- forward
-// e1 = tanh(obs w1 + b1)  (K = D is tiny: direct)
-// block (32 x 8): 32 consecutive features k (w1 / b1 columns in registers) x 8 rows per step
+// e1 = tanh(obs w1 + b1)  (K = D is tiny: direct).  Write-bound (4E bytes per row):
+// block (32 x 8), each thread 4 consecutive features (w1 / b1 columns in registers,
+// one float4 store per row) and 4 rows in flight per iteration
 __global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs, int S, int D, int E,
                                                    const float* __restrict__ w1, const float* __restrict__ b1,
                                                    float* __restrict__ e1) {
+  pdl_wait();
+  pdl_trigger();
+  const int k = 4 * (blockIdx.x * 32 + threadIdx.x);
+  if (k >= E) return;
+  float4 w[kMaxD];
+#pragma unroll
+  for (int d = 0; d < kMaxD; ++d)
+    w[d] = d < D ? *reinterpret_cast<const float4*>(w1 + (size_t)d * E + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 b = *reinterpret_cast<const float4*>(b1 + k);
+  const int stride = gridDim.y * blockDim.y;
+  for (int p0 = blockIdx.y * blockDim.y + threadIdx.y; p0 < S; p0 += 4 * stride) {
+    float4 s[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = min(p0 + u * stride, S - 1);
+      s[u] = make_float4(0.f, 0.f, 0.f, 0.f);  // same order as the scalar kernel: bias last
+#pragma unroll
+      for (int d = 0; d < kMaxD; ++d)
+        if (d < D) {
+          const float o = __ldg(obs + (size_t)p * D + d);
+          s[u].x = fmaf(o, w[d].x, s[u].x);
+          s[u].y = fmaf(o, w[d].y, s[u].y);
+          s[u].z = fmaf(o, w[d].z, s[u].z);
+          s[u].w = fmaf(o, w[d].w, s[u].w);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * stride;
+      if (p < S)
+        *reinterpret_cast<float4*>(e1 + (size_t)p * E + k) =
+            make_float4(gate_tanh(s[u].x + b.x), gate_tanh(s[u].y + b.y), gate_tanh(s[u].z + b.z),
+                        gate_tanh(s[u].w + b.w));
+    }
+  }
+}
+
+// the scalar kernel above for E % 4 != 0 (float4 columns need E % 4 == 0)
+__global__ void __launch_bounds__(256) enc1_scalar_kernel(const float* __restrict__ obs, int S, int D, int E,
+                                                          const float* __restrict__ w1, const float* __restrict__ b1,
+                                                          float* __restrict__ e1) {
   pdl_wait();
   pdl_trigger();
   const int k = blockIdx.x * 32 + threadIdx.x;
@@ -463,9 +505,13 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
                     int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store,
                     const int32_t* h_bs, const int32_t* h_offs) {
   const int E = m.E, H3 = 3 * m.H;
-  {
-    dim3 g(cdiv(E, 32), std::max(1u, std::min(cdiv(S, 8), (unsigned)(8 * c->num_sms / std::max(1u, cdiv(E, 32))))));
+  if (E % 4 == 0) {
+    const unsigned gx = cdiv(E, 128);
+    dim3 g(gx, std::max(1u, std::min(cdiv(S, 32), (unsigned)(8 * c->num_sms / gx))));
     launch_pdl(c, enc1_kernel, g, dim3(32, 8), 0, obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
+  } else {
+    dim3 g(cdiv(E, 32), std::max(1u, std::min(cdiv(S, 8), (unsigned)(8 * c->num_sms / std::max(1u, cdiv(E, 32))))));
+    launch_pdl(c, enc1_scalar_kernel, g, dim3(32, 8), 0, obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
   }
   if (ws.wlo_stale || ws.wlo_src != params || ws.wlo.n < (size_t)m.P) {
     ws.wlo.reserve(c, m.P);

@@ -191,27 +191,12 @@ __global__ void seq_desc_kernel(const int32_t* __restrict__ starts, int K, int S
 }
 
 static void upload_log(Rollout* R, int S) {
-  Ctx* c = R->ctx;
-  const auto& cfg = R->cfg;
-  auto up = [&](auto& d, auto& h, size_t n) {
-    d.reserve(c, std::max<size_t>(n, 1));
-    d.upload(h.p, n);
-  };
-  up(R->d_env, R->env, S);
-  up(R->d_rank, R->rank, S);
-  up(R->d_hslot, R->hslot, S);
-  up(R->d_step, R->step, S);
-  up(R->d_obs, R->obs, (size_t)S * cfg.obs_dim);
-  if (cfg.action_kind) up(R->d_act_cont, R->act_cont, (size_t)S * cfg.act_dim);
-  else up(R->d_act_disc, R->act_disc, S);
-  up(R->d_log_prob, R->log_prob, S);
-  up(R->d_value, R->value, S);
-  up(R->d_reward, R->reward, S);
-  up(R->d_latency, R->latency, S);
-  up(R->d_done, R->done, S);
-  up(R->d_episode, R->episode, S);
-  up(R->d_version, R->version, S);
-  up(R->d_hlog, R->hlog, (size_t)R->h_used * cfg.hidden_dim);
+  // what the bulk appends have not already copied
+  R->upload_rows(R->uploaded, S);
+  R->upload_hrows(R->h_uploaded, R->h_used);
+  if (!R->d_hlog.p) R->d_hlog.reserve(R->ctx, 1);  // seq_desc_kernel takes a valid pointer
+  R->uploaded = S;
+  R->h_uploaded = R->h_used;
 }
 
 // rollout.cpp:102-190

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "view.cuh"
@@ -30,6 +31,27 @@ struct Pinned {
     n = want;
   }
 };
+
+// f(lo, hi) over [0, n) in chunks of >= grain, on up to 16 host threads (the
+// calling thread takes the first chunk); below 2 grains it runs inline
+template <class F>
+inline void host_par_for(size_t n, size_t grain, F f) {
+  const size_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const size_t T = std::min(hw, std::max<size_t>(1, n / std::max<size_t>(grain, 1)));
+  if (T <= 1) {
+    f(size_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T - 1);
+  const size_t per = (n + T - 1) / T;
+  for (size_t t = 1; t < T; ++t) {
+    const size_t lo = std::min(n, t * per), hi = std::min(n, lo + per);
+    if (lo < hi) th.emplace_back(f, lo, hi);
+  }
+  f(size_t(0), std::min(n, per));
+  for (auto& x : th) x.join();
+}
 
 struct CarryRec {
   int32_t env, step;
@@ -63,6 +85,9 @@ struct Rollout {
   Pinned<int64_t> episode;
   Pinned<uint64_t> version;
   int h_used = 0;
+  // rows of the log (and h_before rows) already copied to the device mirror: the
+  // bulk append uploads what it wrote right away, close_rollout the rest
+  int uploaded = 0, h_uploaded = 0;
   // device mirror
   DBuf<int32_t> d_env, d_rank, d_hslot, d_act_disc, d_step;
   DBuf<float> d_obs, d_act_cont, d_log_prob, d_value, d_reward, d_latency, d_hlog;
@@ -76,6 +101,39 @@ struct Rollout {
   int h_dev_used = 0;
 
   int capacity() const { return cfg.T * cfg.N; }
+
+  // copy log rows [a, z) of every column to the device mirror (sized to capacity)
+  void upload_rows(int a, int z) {  // (z == a: only sizes the mirror)
+    const size_t C = (size_t)std::max(capacity(), 1), n = (size_t)std::max(z - a, 0);
+    auto up = [&](auto& d, auto& h, size_t w) {
+      d.reserve(ctx, C * std::max<size_t>(w, 1));
+      if (n * w)
+        VER_CUDA(cudaMemcpyAsync(d.p + (size_t)a * w, h.p + (size_t)a * w, n * w * sizeof(*h.p), cudaMemcpyHostToDevice,
+                               ctx->stream));
+    };
+    up(d_env, env, 1);
+    up(d_rank, rank, 1);
+    up(d_hslot, hslot, 1);
+    up(d_step, step, 1);
+    up(d_obs, obs, (size_t)cfg.obs_dim);
+    if (cfg.action_kind) up(d_act_cont, act_cont, (size_t)cfg.act_dim);
+    else up(d_act_disc, act_disc, 1);
+    up(d_log_prob, log_prob, 1);
+    up(d_value, value, 1);
+    up(d_reward, reward, 1);
+    up(d_latency, latency, 1);
+    up(d_done, done, 1);
+    up(d_episode, episode, 1);
+    up(d_version, version, 1);
+  }
+  // copy h_before rows [a, z) (the device copy keeps rows [0, a))
+  void upload_hrows(int a, int z) {
+    const size_t Hd = (size_t)cfg.hidden_dim;
+    if (z <= a || !Hd) return;
+    d_hlog.grow_keep(ctx, std::max(hlog.n, (size_t)z * Hd), (size_t)a * Hd);
+    VER_CUDA(cudaMemcpyAsync(d_hlog.p + (size_t)a * Hd, hlog.p + (size_t)a * Hd, (size_t)(z - a) * Hd * sizeof(float),
+                             cudaMemcpyHostToDevice, ctx->stream));
+  }
 
   void init() {
     const int C = capacity();
@@ -155,6 +213,10 @@ struct Rollout {
 
   // rollout.cpp:39-57
   void begin(uint64_t sv) {
+    // the pinned log is about to be rewritten: no copy of it may still be in flight
+    if (uploaded || h_uploaded) VER_CUDA(cudaStreamSynchronize(ctx->stream));
+    uploaded = 0;
+    h_uploaded = 0;
     open = true;
     snapshot_version = sv;
     committed = 0;
@@ -207,43 +269,119 @@ struct Rollout {
         break;
       }
     if (n <= 0) return 0;
-    const int r0 = committed, D = cfg.obs_dim;
-    auto col = [&](auto* dst, const auto* src, size_t width, auto fill) {
-      if (src) std::memcpy(dst + (size_t)r0 * width, src + (size_t)i0 * width, sizeof(*dst) * width * n);
-      else std::fill(dst + (size_t)r0 * width, dst + (size_t)(r0 + n) * width, fill);
+    const int r0 = committed, D = cfg.obs_dim, Hd = cfg.hidden_dim, NE = cfg.N;
+    // Bookkeeping (rollout.cpp:79-93 + the rank / sequence-start log of this
+    // store) in parallel over record chunks: (1) per chunk and env the record count
+    // and the last record's done flag; (2) a serial prefix over chunks x envs gives
+    // each chunk the env's rank and "previous record done" on entry; (3) per chunk
+    // the ranks / starts and the chunk's count of h_before rows, whose prefix (4)
+    // numbers the rows in record order; (5) columns and rows copied on all threads.
+    const size_t hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const int nch = (int)std::max<size_t>(1, std::min(hw, (size_t)n / 16384));
+    const int per = (n + nch - 1) / nch;
+    std::vector<int32_t> lc((size_t)nch * NE, 0);    // records of env e in chunk c, then rank base
+    std::vector<int8_t> ld((size_t)nch * NE, -1);    // last record's done in chunk c (-1: none), then done on entry
+    std::vector<int32_t> hcount(nch + 1, 0);
+    auto chunks = [&](auto f) {
+      host_par_for((size_t)nch, 1, [&](size_t lo, size_t hi) {
+        for (size_t c = lo; c < hi; ++c) f((int)c, i0 + (int)c * per, i0 + std::min(n, ((int)c + 1) * per));
+      });
     };
-    col(env.p, b->env_index, 1, 0);
-    col(episode.p, b->episode_index, 1, (int64_t)0);
-    col(step.p, b->step_in_episode, 1, 0);
-    col(obs.p, b->obs, D, 0.f);
-    if (cfg.action_kind) col(act_cont.p, b->act_cont, cfg.act_dim, 0.f);
-    else col(act_disc.p, b->act_disc, 1, 0);
-    col(log_prob.p, b->log_prob, 1, 0.f);
-    col(value.p, b->value, 1, 0.f);
-    col(reward.p, b->reward, 1, 0.f);
-    col(latency.p, b->latency, 1, 0.f);
-    col(version.p, b->snapshot_version, 1, (uint64_t)0);
-    for (int i = 0; i < n; ++i) {
-      const int e = b->env_index[i0 + i];
-      const int rk = counts[e];
-      const uint8_t dn = b->done[i0 + i] ? 1 : 0;
-      int hs = -2;
-      if (rk == 0 || last_done[e]) {
-        const bool has = b->h_before && (!b->h_before_valid || b->h_before_valid[i0 + i]);
-        if (has) {
-          hlog.ensure((size_t)(h_used + 1) * cfg.hidden_dim, (size_t)h_used * cfg.hidden_dim);
-          std::memcpy(hlog.p + (size_t)h_used * cfg.hidden_dim, b->h_before + (size_t)(i0 + i) * cfg.hidden_dim,
-                      sizeof(float) * cfg.hidden_dim);
-          hs = h_used++;
-        } else {
-          hs = -1;
+    chunks([&](int c, int a, int z) {
+      int32_t* l = lc.data() + (size_t)c * NE;
+      int8_t* d = ld.data() + (size_t)c * NE;
+      for (int i = a; i < z; ++i) {
+        const int e = b->env_index[i];
+        ++l[e];
+        d[e] = b->done[i] ? 1 : 0;
+      }
+    });
+    for (int e = 0; e < NE; ++e) {
+      int32_t base = counts[e];
+      int8_t prev = (int8_t)last_done[e];
+      for (int c = 0; c < nch; ++c) {
+        const size_t q = (size_t)c * NE + e;
+        const int32_t cnt = lc[q];
+        const int8_t dl = ld[q];
+        lc[q] = base;
+        ld[q] = prev;
+        base += cnt;
+        if (cnt) prev = dl;
+      }
+      counts[e] = base;
+      last_done[e] = (uint8_t)prev;
+    }
+    const bool hb = b->h_before != nullptr;
+    chunks([&](int c, int a, int z) {
+      int32_t* base = lc.data() + (size_t)c * NE;
+      int8_t* prev = ld.data() + (size_t)c * NE;
+      int32_t nh = 0;
+      for (int i = a; i < z; ++i) {
+        const int e = b->env_index[i];
+        const int rk = base[e]++;
+        const uint8_t dn = b->done[i] ? 1 : 0;
+        int hs = -2;
+        if (rk == 0 || prev[e] == 1) hs = (hb && (!b->h_before_valid || b->h_before_valid[i])) ? nh++ : -1;
+        prev[e] = (int8_t)dn;
+        const int r = r0 + (i - i0);
+        rank.p[r] = rk;
+        hslot.p[r] = hs;  // chunk-local row number for now
+        done.p[r] = dn;
+      }
+      hcount[c + 1] = nh;
+    });
+    for (int c = 0; c < nch; ++c) hcount[c + 1] += hcount[c];
+    const int h0 = h_used, nh_tot = hcount[nch];
+    if (nh_tot) hlog.ensure((size_t)(h_used + nh_tot) * Hd, (size_t)h_used * Hd);
+    h_used += nh_tot;
+    auto col = [&](auto* dst, const auto* src, size_t width, auto fill, size_t lo, size_t hi) {
+      if (src) std::memcpy(dst + (r0 + lo) * width, src + (i0 + lo) * width, sizeof(*dst) * width * (hi - lo));
+      else std::fill(dst + (r0 + lo) * width, dst + (r0 + hi) * width, fill);
+    };
+    // rows committed one by one since the last upload (carryovers, append_one), then
+    // each chunk's rows as soon as they are in the pinned log: the H2D copies overlap
+    // the other chunks' host copies instead of waiting for close_rollout
+    const bool early = ctx != nullptr;
+    if (early) {
+      upload_rows(uploaded, r0);
+      upload_hrows(h_uploaded, h0);
+      if (nh_tot) d_hlog.grow_keep(ctx, std::max(hlog.n, (size_t)(h0 + nh_tot) * Hd), (size_t)h0 * Hd);
+      upload_rows(r0, r0);  // sizes every device column to capacity before the threads use them
+    }
+    chunks([&](int c, int a, int z) {
+      const size_t lo = (size_t)(a - i0), hi = (size_t)(z - i0);
+      col(env.p, b->env_index, 1, 0, lo, hi);
+      col(episode.p, b->episode_index, 1, (int64_t)0, lo, hi);
+      col(step.p, b->step_in_episode, 1, 0, lo, hi);
+      col(obs.p, b->obs, D, 0.f, lo, hi);
+      if (cfg.action_kind) col(act_cont.p, b->act_cont, cfg.act_dim, 0.f, lo, hi);
+      else col(act_disc.p, b->act_disc, 1, 0, lo, hi);
+      col(log_prob.p, b->log_prob, 1, 0.f, lo, hi);
+      col(value.p, b->value, 1, 0.f, lo, hi);
+      col(reward.p, b->reward, 1, 0.f, lo, hi);
+      col(latency.p, b->latency, 1, 0.f, lo, hi);
+      col(version.p, b->snapshot_version, 1, (uint64_t)0, lo, hi);
+      // this chunk's h_before rows, numbered after the earlier chunks' in record order
+      const int hb0 = h0 + hcount[c];
+      for (size_t q = lo; q < hi; ++q) {
+        int32_t& hs = hslot.p[r0 + q];
+        if (hs >= 0) {
+          hs += hb0;
+          std::memcpy(hlog.p + (size_t)hs * Hd, b->h_before + (i0 + q) * Hd, sizeof(float) * Hd);
         }
       }
-      rank.p[r0 + i] = rk;
-      hslot.p[r0 + i] = hs;
-      done.p[r0 + i] = dn;
-      counts[e] = rk + 1;
-      last_done[e] = dn;
+      if (early) {
+        VER_CUDA(cudaSetDevice(ctx->device));  // a worker thread
+        upload_rows(r0 + (int)lo, r0 + (int)hi);
+        if (Hd && hcount[c + 1] > hcount[c])
+          VER_CUDA(cudaMemcpyAsync(d_hlog.p + (size_t)hb0 * Hd, hlog.p + (size_t)hb0 * Hd,
+                                   (size_t)(hcount[c + 1] - hcount[c]) * Hd * sizeof(float), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+      }
+    });
+    if (early) {
+      uploaded = r0 + n;
+      h_uploaded = h_used;
     }
     committed += n;
     if (committed >= capacity()) open = false;
