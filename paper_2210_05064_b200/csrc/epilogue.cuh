@@ -3,6 +3,7 @@
 // vec4(m, n, v4, z): four consecutive columns n..n+3 of row m (tcgen05 GEMM's
 // coalesced epilogue; n % 4 == 0, every leading dimension % 4 == 0).
 #pragma once
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -58,6 +59,45 @@ struct EpiBiasTanh {
     const float4 b = __ldg(reinterpret_cast<const float4*>(bias + n));
     *reinterpret_cast<float4*>(C + (size_t)m * ldc + n) =
         make_float4(tanhf(v.x + b.x), tanhf(v.y + b.y), tanhf(v.z + b.z), tanhf(v.w + b.w));
+  }
+};
+// EpiBiasTanh that also writes the result as fp16x2 halves (scale 2^14, tanh
+// outputs) for the next fp16x2 GEMM (tc_gemm.cuh F16), same row stride
+struct EpiBiasTanhH {
+  float* C;
+  int ldc;
+  const float* bias;
+  __half* hi;
+  __half* lo;
+  __device__ void prefetch_row(int, int, int) const {}
+  bool vec_ok() const { return ptr16(C) && ldc % 4 == 0 && ptr16(bias) && ptr16(hi) && ptr16(lo) && ldc % 8 == 0; }
+  EpiBiasTanhH shifted(int m0) const {
+    return EpiBiasTanhH{C + (size_t)m0 * ldc, ldc, bias, hi + (size_t)m0 * ldc, lo + (size_t)m0 * ldc};
+  }
+  __device__ void operator()(int m, int n, float v, int) const {
+    const float y = tanhf(v + bias[n]);
+    const size_t i = (size_t)m * ldc + n;
+    C[i] = y;
+    const __half h = __float2half_rn(y * 16384.f);
+    hi[i] = h;
+    lo[i] = __float2half_rn(y * 16384.f - __half2float(h));
+  }
+  __device__ void vec4(int m, int n, float4 v, int) const {
+    const float4 b = __ldg(reinterpret_cast<const float4*>(bias + n));
+    const float4 y = make_float4(tanhf(v.x + b.x), tanhf(v.y + b.y), tanhf(v.z + b.z), tanhf(v.w + b.w));
+    const size_t i = (size_t)m * ldc + n;
+    *reinterpret_cast<float4*>(C + i) = y;
+    const float ys[4] = {y.x * 16384.f, y.y * 16384.f, y.z * 16384.f, y.w * 16384.f};
+    __half h[4], l[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      h[q] = __float2half_rn(ys[q]);
+      l[q] = __float2half_rn(ys[q] - __half2float(h[q]));
+    }
+    reinterpret_cast<__half2*>(hi + i)[0] = __halves2half2(h[0], h[1]);
+    reinterpret_cast<__half2*>(hi + i)[1] = __halves2half2(h[2], h[3]);
+    reinterpret_cast<__half2*>(lo + i)[0] = __halves2half2(l[0], l[1]);
+    reinterpret_cast<__half2*>(lo + i)[1] = __halves2half2(l[2], l[3]);
   }
 };
 struct EpiAddTerm {  // C = acc + T

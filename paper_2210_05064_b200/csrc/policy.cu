@@ -215,6 +215,70 @@ __global__ void split_lo_kernel(int64_t n, const float* __restrict__ x, float* _
   if (i < n) lo[i] = tc::lo1(x[i]);
 }
 
+// ---------------------------------------------------------------- fp16x2 operands
+// x s = hi + lo with hi = fp16_rn(x s), lo = fp16_rn(x s - hi) (22 significant
+// bits; tc_gemm.cuh F16).  Activations that are tanh outputs (|x| < 1) use the
+// fixed scale 2^14; a weight's scale is 2^(14 - floor(log2 max|w|)), so that
+// max |w| s < 2^15 < 65504 and its small entries stay normal for ~28 binades.
+constexpr float kActScale = 16384.f;  // 2^14
+__device__ __forceinline__ void split_h2(float y, __half& hi, __half& lo) {
+  hi = __float2half_rn(y);
+  lo = __float2half_rn(y - __half2float(hi));
+}
+__global__ void maxabs_kernel(int64_t n, const float* __restrict__ x, unsigned* __restrict__ out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(x[i]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // non-negative floats order as uints
+}
+__device__ __forceinline__ float weight_scale(unsigned maxbits) {
+  const float mx = __uint_as_float(maxbits);
+  if (!(mx > 0.f) || !isfinite(mx)) return 1.f;
+  return exp2f((float)(14 - ilogbf(mx)));
+}
+// W: K x N row-major (the MN-major B of x W) -> Wt hi / lo: N x K row-major; 32 x 32
+// tiles through shared memory.  inv = 1 / (2^14 s_W) for the GEMM epilogue.
+__global__ void __launch_bounds__(256) weight_f16x2_kernel(const float* __restrict__ W, int K, int N,
+                                                           const unsigned* __restrict__ maxbits, __half* __restrict__ hi,
+                                                           __half* __restrict__ lo, float* __restrict__ inv) {
+  __shared__ float t[32][33];
+  const float s = weight_scale(*maxbits);
+  const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int k = k0 + r, n = n0 + threadIdx.x;
+    t[r][threadIdx.x] = (k < K && n < N) ? W[(size_t)k * N + n] : 0.f;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int n = n0 + r, k = k0 + threadIdx.x;
+    if (n < N && k < K) split_h2(t[threadIdx.x][r] * s, hi[(size_t)n * K + k], lo[(size_t)n * K + k]);
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) *inv = 1.f / (kActScale * s);
+}
+// fp16x2 forward GEMMs (VER_TC_F16=0 restores 3xTF32 for them)
+static bool f16x2_on(const Ctx* c) { return c->precision == 0 && c->tensor_cores && env_int("VER_TC_F16", 1) != 0; }
+// the weight copies of the fp16x2 forward GEMMs: slot 0 wx (3H x E), slot 1 w2 (E x E)
+static void refresh_weights_f16(Ctx* c, const Model& m, const float* params, Workspace& ws) {
+  const int E = m.E, H3 = 3 * m.H;
+  const size_t n0 = (size_t)H3 * E, n1 = (size_t)E * E;
+  ws.w16hi.reserve(c, n0 + n1);
+  ws.w16lo.reserve(c, n0 + n1);
+  ws.w16max.reserve(c, 2);
+  ws.w16inv.reserve(c, 2);
+  ws.w16max.zero(2);
+  maxabs_kernel<<<64, 256, 0, c->stream>>>((int64_t)E * H3, params + m.o_wx, ws.w16max.p);
+  after_launch(c);
+  maxabs_kernel<<<64, 256, 0, c->stream>>>((int64_t)E * E, params + m.o_w2, ws.w16max.p + 1);
+  after_launch(c);
+  weight_f16x2_kernel<<<dim3(cdiv(H3, 32), cdiv(E, 32)), dim3(32, 8), 0, c->stream>>>(
+      params + m.o_wx, E, H3, ws.w16max.p, ws.w16hi.p, ws.w16lo.p, ws.w16inv.p);
+  after_launch(c);
+  weight_f16x2_kernel<<<dim3(cdiv(E, 32), cdiv(E, 32)), dim3(32, 8), 0, c->stream>>>(
+      params + m.o_w2, E, E, ws.w16max.p + 1, ws.w16hi.p + n0, ws.w16lo.p + n0, ws.w16inv.p + 1);
+  after_launch(c);
+}
 template <bool TA, bool TB, class Epi>
 static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B, int ldb, Epi epi,
                  const float* Blo = nullptr) {
@@ -441,7 +505,8 @@ constexpr int kMaxD = 8;  // obs_dim bound of the encoder-input kernels (Model::
 // one float4 store per row) and 4 rows in flight per iteration
 __global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs, int S, int D, int E,
                                                    const float* __restrict__ w1, const float* __restrict__ b1,
-                                                   float* __restrict__ e1) {
+                                                   float* __restrict__ e1, __half* __restrict__ e1hi,
+                                                   __half* __restrict__ e1lo) {
   pdl_wait();
   pdl_trigger();
   const int k = 4 * (blockIdx.x * 32 + threadIdx.x);
@@ -471,10 +536,26 @@ __global__ void __launch_bounds__(256) enc1_kernel(const float* __restrict__ obs
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int p = p0 + u * stride;
-      if (p < S)
-        *reinterpret_cast<float4*>(e1 + (size_t)p * E + k) =
-            make_float4(gate_tanh(s[u].x + b.x), gate_tanh(s[u].y + b.y), gate_tanh(s[u].z + b.z),
-                        gate_tanh(s[u].w + b.w));
+      if (p < S) {
+        const float4 y = make_float4(gate_tanh(s[u].x + b.x), gate_tanh(s[u].y + b.y), gate_tanh(s[u].z + b.z),
+                                     gate_tanh(s[u].w + b.w));
+        *reinterpret_cast<float4*>(e1 + (size_t)p * E + k) = y;
+        if (e1hi) {  // fp16x2 halves for the next GEMM (scale 2^14)
+          const float ys[4] = {y.x * 16384.f, y.y * 16384.f, y.z * 16384.f, y.w * 16384.f};
+          __half h[4], l[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            h[q] = __float2half_rn(ys[q]);
+            l[q] = __float2half_rn(ys[q] - __half2float(h[q]));
+          }
+          __half2* hp = reinterpret_cast<__half2*>(e1hi + (size_t)p * E + k);
+          __half2* lp = reinterpret_cast<__half2*>(e1lo + (size_t)p * E + k);
+          hp[0] = __halves2half2(h[0], h[1]);
+          hp[1] = __halves2half2(h[2], h[3]);
+          lp[0] = __halves2half2(l[0], l[1]);
+          lp[1] = __halves2half2(l[2], l[3]);
+        }
+      }
     }
   }
 }
@@ -505,10 +586,18 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
                     int L, const int32_t* d_bs, const int32_t* d_offs, Workspace& ws, bool store,
                     const int32_t* h_bs, const int32_t* h_offs) {
   const int E = m.E, H3 = 3 * m.H;
+  const bool f16 = f16x2_on(c) && tc::usable_f16(S, H3, E, E, E) && tc::usable_f16(S, E, E, E, E) &&
+                   EpiBias{ws.xp.p, H3, params + m.o_bx}.vec_ok() && E % 8 == 0;
+  const size_t nSE = (size_t)S * E;
+  if (f16) {  // e1's halves at [0, nSE), enc's at [nSE, 2 nSE)
+    ws.a16hi.reserve(c, 2 * nSE);
+    ws.a16lo.reserve(c, 2 * nSE);
+  }
   if (E % 4 == 0) {
     const unsigned gx = cdiv(E, 128);
     dim3 g(gx, std::max(1u, std::min(cdiv(S, 32), (unsigned)(8 * c->num_sms / gx))));
-    launch_pdl(c, enc1_kernel, g, dim3(32, 8), 0, obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
+    launch_pdl(c, enc1_kernel, g, dim3(32, 8), 0, obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p,
+               f16 ? ws.a16hi.p : nullptr, f16 ? ws.a16lo.p : nullptr);
   } else {
     dim3 g(cdiv(E, 32), std::max(1u, std::min(cdiv(S, 8), (unsigned)(8 * c->num_sms / std::max(1u, cdiv(E, 32))))));
     launch_pdl(c, enc1_scalar_kernel, g, dim3(32, 8), 0, obs, S, m.D, E, params + m.o_w1, params + m.o_b1, ws.e1.p);
@@ -516,13 +605,27 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
   if (ws.wlo_stale || ws.wlo_src != params || ws.wlo.n < (size_t)m.P) {
     ws.wlo.reserve(c, m.P);
     launch_pdl(c, split_lo_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, ws.wlo.p);
+    if (f16) refresh_weights_f16(c, m, params, ws);
     ws.wlo_src = params;
+  } else if (f16 && ws.w16inv.n < 2) {
+    refresh_weights_f16(c, m, params, ws);
   }
   ws.wlo_stale = !ws.wlo_keep;
-  gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2},
-                     ws.wlo.p + m.o_w2);
-  gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx},
-                     ws.wlo.p + m.o_wx);
+  if (f16) {
+    // fp16x2: e1 and enc are tanh outputs (fixed scale), the weights' copies are
+    // transposed to K-major
+    // (the enc1 kernel and the enc2 epilogue write the halves next to the fp32 rows)
+    const size_t nW = (size_t)H3 * E;
+    tc::launch_f16(c, S, E, E, ws.a16hi.p, ws.a16lo.p, E, ws.w16hi.p + nW, ws.w16lo.p + nW, E, ws.w16inv.p + 1,
+                   EpiBiasTanhH{ws.enc.p, E, params + m.o_b2, ws.a16hi.p + nSE, ws.a16lo.p + nSE}, 1);
+    tc::launch_f16(c, S, H3, E, ws.a16hi.p + nSE, ws.a16lo.p + nSE, E, ws.w16hi.p, ws.w16lo.p, E, ws.w16inv.p,
+                   EpiBias{ws.xp.p, H3, params + m.o_bx}, 1);
+  } else {
+    gemm<false, false>(c, S, E, E, ws.e1.p, E, params + m.o_w2, E, EpiBiasTanh{ws.enc.p, E, params + m.o_b2},
+                       ws.wlo.p + m.o_w2);
+    gemm<false, false>(c, S, H3, E, ws.enc.p, E, params + m.o_wx, H3, EpiBias{ws.xp.p, H3, params + m.o_bx},
+                       ws.wlo.p + m.o_wx);
+  }
   gru_forward_recurrence(c, m, params, L, d_bs, d_offs, ws, h0, store, h_bs, h_offs);
 }
 

@@ -12,6 +12,8 @@
 // this layout, applied only at the C-ABI (params/grads/Adam get/set).
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "packed.cuh"
 
 struct ver_learner_s;
@@ -47,6 +49,13 @@ struct Workspace {
   DBuf<float> sgsteps, sgmaps;                          // stepgemm.cu: step table, per-step A tensor maps
   DBuf<unsigned long long> hx;                          // K-split kernels: tagged h / dhU rows of short steps
   DBuf<float> wlo;                                      // lo = x - trunc_tf32(x) of the parameters (3xTF32 B operands)
+  // fp16x2 operands (tc_gemm.cuh F16): the forward weights transposed to K-major
+  // (wx: 3H x E, w2: E x E) as scaled hi / lo halves, refreshed with wlo; per
+  // weight the max |w| (float bits) and the GEMM's 1 / (s_A s_B); the activation
+  // operand's halves (enc / e1, fixed scale 2^14: tanh outputs)
+  DBuf<__half> w16hi, w16lo, a16hi, a16lo;
+  DBuf<unsigned> w16max;
+  DBuf<float> w16inv;
   // wlo holds the lo of wlo_src's current values unless wlo_stale; owners whose
   // parameters change in place (the learner's Adam) leave it stale (the default)
   const float* wlo_src = nullptr;

@@ -23,6 +23,7 @@
 // 2..5 3xTF32 operand split, 6..9 accumulator promotion + epilogue.
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <mutex>
@@ -584,12 +585,34 @@ __device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t adesc, uint6
       : "memory");
 }
 
-template <int AMAJ, int BMAJ, class Epi, int BLO>
+__device__ __forceinline__ void mma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// F16 = 1 ("fp16x2", fp32-grade like 3xTF32 at twice the MMA rate): both operands
+// come pre-split from global memory as scaled fp16 pairs, x s = hi + lo (hi =
+// fp16(x s), lo = fp16(x s - hi): 22 significant bits), K-major, 64 elements
+// (128 bytes) per swizzle row, so a stage has the byte layout of the tf32 one
+// with twice the K.  Each K-step issues hi*hi + lo*hi + hi*lo (kind::f16, fp32
+// accumulate; fp16 x fp16 products are exact in fp32); the epilogue multiplies
+// by *fscale = 1 / (s_A s_B), a power of two.  The split warps only relay the
+// stage-landed signal to the leader CTA.
+template <int AMAJ, int BMAJ, class Epi, int BLO, int F16 = 0>
 __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB, int M,
                                                                int N, int K, int kb_per_split, int nsplit, Epi epi,
                                                                const __grid_constant__ CUtensorMap tmBl,
-                                                               int promote) {
+                                                               int promote,
+                                                               const __grid_constant__ CUtensorMap tmAl,
+                                                               const float* __restrict__ fscale) {
+  static_assert(!F16 || (AMAJ == 0 && BMAJ == 0), "fp16x2 operands are K-major");
+  constexpr int BKE = F16 ? 64 : BK;  // K elements per stage
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
   // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
@@ -604,7 +627,7 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
   const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int tilesN = (N + BN2 - 1) / BN2, tilesM = (M + BM2 - 1) / BM2;
   const int ntiles = tilesN * tilesM * nsplit;
-  const int nkb_total = (K + BK - 1) / BK;
+  const int nkb_total = (K + BKE - 1) / BKE;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
@@ -641,7 +664,8 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    if (BLO) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
+    if (BLO || F16) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
+    if (F16) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmAl)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -668,6 +692,15 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
           const int s = it % STAGES2;
           const uint32_t ph = (it / STAGES2) & 1;
           mbar_wait(empty_bar(s), ph ^ 1);
+          if (F16) {
+            mbar_expect_tx(full_bar(s), 4 * TILE);
+            const int k0 = (T.kb0 + i) * BKE;
+            tma_load_2d(tileA(s, 0), &tmA, full_bar(s), k0, am);
+            tma_load_2d(tileA(s, 1), &tmAl, full_bar(s), k0, am);
+            tma_load_2d(tileB(s, 0), &tmB, full_bar(s), k0, bn);
+            tma_load_2d(tileB(s, 1), &tmBl, full_bar(s), k0, bn);
+            continue;
+          }
           mbar_expect_tx(full_bar(s), (BLO ? 3 : 2) * TILE);
           const int k0 = (T.kb0 + i) * BK;
           if (AMAJ == 0) {
@@ -693,7 +726,9 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader CTA, one thread)
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
+    // D f32; A / B tf32 (2) or f16 (0)
+    const uint32_t fmt = F16 ? 0u : 2u;
+    const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
                            ((uint32_t)(BN2 >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
     if (leader && lane == 0) {
       int it = 0, g = 0, buf = 0;
@@ -712,12 +747,18 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * BN2);
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
+          for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K per MMA: 8 tf32 or 16 f16
             const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
             const uint64_t bh = operand_desc<BMAJ>(tileB(s, 0), kk);
-            mma2_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
-            mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
-            mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+            if (F16) {
+              mma2_f16(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+              mma2_f16(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+              mma2_f16(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+            } else {
+              mma2_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+              mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+              mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+            }
           }
           commit2(empty_bar(s));
           if ((i % promote) == promote - 1 || i == T.nkb - 1) {
@@ -738,17 +779,19 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
         const int s = it % STAGES2;
         const uint32_t ph = (it / STAGES2) & 1;
         mbar_wait(full_bar(s), ph);
-        uint8_t* st = smem + s * STAGE2;
-        const float4* ahi = reinterpret_cast<const float4*>(st);
-        float4* alo = reinterpret_cast<float4*>(st + TILE);
-        const float4* bhi = reinterpret_cast<const float4*>(st + 2 * TILE);
-        float4* blo = reinterpret_cast<float4*>(st + 3 * TILE);
+        if (!F16) {
+          uint8_t* st = smem + s * STAGE2;
+          const float4* ahi = reinterpret_cast<const float4*>(st);
+          float4* alo = reinterpret_cast<float4*>(st + TILE);
+          const float4* bhi = reinterpret_cast<const float4*>(st + 2 * TILE);
+          float4* blo = reinterpret_cast<float4*>(st + 3 * TILE);
 #pragma unroll 4
-        for (int q = et; q < TILE / 16; q += 32 * SPLITW) {
-          alo[q] = lo_tf32(ahi[q]);
-          if (!BLO) blo[q] = lo_tf32(bhi[q]);
+          for (int q = et; q < TILE / 16; q += 32 * SPLITW) {
+            alo[q] = lo_tf32(ahi[q]);
+            if (!BLO) blo[q] = lo_tf32(bhi[q]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) arrive_remote(to_rank(split_bar(s), 0));
       }
@@ -797,6 +840,11 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
         tc_fence_before();
         __syncwarp();
         if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
+      }
+      if (F16) {  // undo the operand scales (a power of two: exact)
+        const float sc = *fscale;
+#pragma unroll
+        for (int j = 0; j < BNH; ++j) sums[j] *= sc;
       }
       // epilogue: transpose 32 x 16 blocks through shared memory so each warp
       // store covers 8 rows x 64 contiguous bytes (float4 per lane)
@@ -931,11 +979,75 @@ void launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
       pairs_cache[dev_slot(c)].store(pairs);
     }
     cfg.gridDim = dim3(2 * (int)std::min<long long>(ntiles, pairs));
-    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote));
+    VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote, ta,
+                                static_cast<const float*>(nullptr)));
     after_launch(c);
   };
   if (blo) run(p2::tc_gemm2_kernel<AMAJ, BMAJ, Epi, 1>);
   else run(p2::tc_gemm2_kernel<AMAJ, BMAJ, Epi, 0>);
+}
+
+// 2D fp16 row-major tensor (rows x cols, row stride ld elements), K-major box
+// {64, box_rows} with the 128-byte swizzle (one swizzle row = 64 halves)
+inline CUtensorMap make_map16(const __half* base, int rows, int cols, int ld, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(VER_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// C = (A_hi + A_lo)(B_hi + B_lo)^T * fscale, fp16x2 on CTA pairs (p2::tc_gemm2_kernel
+// F16): A M x K and B N x K, both K-major fp16 (row stride lda / ldb halves,
+// 16-byte aligned rows); *fscale (device) = 1 / (s_A s_B).  M >= 256, N % 4 == 0.
+inline bool usable_f16(int M, int N, int K, int lda, int ldb) {
+  return M >= p2::BM2 && N >= 16 && (N % 4) == 0 && K >= 16 && (lda % 8) == 0 && (ldb % 8) == 0;
+}
+template <class Epi>
+void launch_f16(Ctx* c, int M, int N, int K, const __half* Ahi, const __half* Alo, int lda, const __half* Bhi,
+                const __half* Blo, int ldb, const float* fscale, Epi epi, int splits) {
+  ScopedEv ev(c, c->gemm_tag);
+  if (c->evlog && c->flop_log && c->gemm_tag >= 0) c->flop_log[c->gemm_tag] += 2.0 * M * (double)N * K;
+  const CUtensorMap ta = make_map16(Ahi, M, K, lda, BM), tal = make_map16(Alo, M, K, lda, BM);
+  const CUtensorMap tb = make_map16(Bhi, N, K, ldb, p2::BNH), tbl = make_map16(Blo, N, K, ldb, p2::BNH);
+  const int nkb = (K + 63) / 64;
+  splits = std::max(1, std::min(splits, nkb));
+  const int per = (nkb + splits - 1) / splits;
+  splits = (nkb + per - 1) / per;
+  const long long ntiles = cdiv(N, p2::BN2) * cdiv(M, p2::BM2) * (long long)splits;
+  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  auto kern = p2::tc_gemm2_kernel<0, 0, Epi, 0, 1>;
+  VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p2::SMEM2));
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(p2::THREADS2);
+  cfg.dynamicSmemBytes = p2::SMEM2;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  static std::atomic<int> pairs_cache[kMaxDevices];
+  int pairs = pairs_cache[dev_slot(c)].load();
+  if (!pairs) {
+    cfg.gridDim = dim3(c->num_sms);
+    int nc = 0;
+    VER_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+    pairs = std::max(1, std::min(nc, c->num_sms / 2));
+    pairs_cache[dev_slot(c)].store(pairs);
+  }
+  cfg.gridDim = dim3(2 * (int)std::min<long long>(ntiles, pairs));
+  VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote, tal, fscale));
+  after_launch(c);
 }
 
 template <int AMAJ, int BMAJ, class Epi>

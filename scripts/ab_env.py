@@ -61,7 +61,7 @@ for s in a.settings:
                   V.CosineSchedule(2.5e-4, 2_000_000), mix(1, 0xF00D))
     L.update(view, read_stats=False)
     L.ctx.synchronize()
-    tot, rf, rb = [], [], []
+    tot, rf, rb, gf, gb = [], [], [], [], []
     for _ in range(a.updates):
         L.update(view, read_stats=False)
         L.ctx.synchronize()
@@ -70,5 +70,8 @@ for s in a.settings:
                                                          "allreduce", "adam")))
         rf.append(t["rec_fwd"])
         rb.append(t["rec_bwd"])
+        gf.append(t["gemm_fwd"])
+        gb.append(t["gemm_bwd"])
     print(f"{s}: phases {statistics.median(tot):.2f} ms  rec_fwd {statistics.median(rf):.2f}  "
-          f"rec_bwd {statistics.median(rb):.2f}", flush=True)
+          f"rec_bwd {statistics.median(rb):.2f}  gemm_fwd {statistics.median(gf):.2f}  "
+          f"gemm_bwd {statistics.median(gb):.2f}  forward {t['forward']:.2f}", flush=True)
