@@ -242,7 +242,8 @@ __device__ __forceinline__ float weight_scale(unsigned maxbits) {
 // tiles through shared memory.  inv = 1 / (2^14 s_W) for the GEMM epilogue.
 __global__ void __launch_bounds__(256) weight_f16x2_kernel(const float* __restrict__ W, int K, int N,
                                                            const unsigned* __restrict__ maxbits, __half* __restrict__ hi,
-                                                           __half* __restrict__ lo, float* __restrict__ inv) {
+                                                           __half* __restrict__ lo, float* __restrict__ inv,
+                                                           float act_scale) {
   __shared__ float t[32][33];
   const float s = weight_scale(*maxbits);
   const int k0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
@@ -255,28 +256,36 @@ __global__ void __launch_bounds__(256) weight_f16x2_kernel(const float* __restri
     const int n = n0 + r, k = k0 + threadIdx.x;
     if (n < N && k < K) split_h2(t[threadIdx.x][r] * s, hi[(size_t)n * K + k], lo[(size_t)n * K + k]);
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) *inv = 1.f / (kActScale * s);
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) *inv = 1.f / (act_scale * s);
 }
 // fp16x2 forward GEMMs (VER_TC_F16=0 restores 3xTF32 for them)
 static bool f16x2_on(const Ctx* c) { return c->precision == 0 && c->tensor_cores && env_int("VER_TC_F16", 1) != 0; }
-// the weight copies of the fp16x2 forward GEMMs: slot 0 wx (3H x E), slot 1 w2 (E x E)
-static void refresh_weights_f16(Ctx* c, const Model& m, const float* params, Workspace& ws) {
-  const int E = m.E, H3 = 3 * m.H;
-  const size_t n0 = (size_t)H3 * E, n1 = (size_t)E * E;
-  ws.w16hi.reserve(c, n0 + n1);
-  ws.w16lo.reserve(c, n0 + n1);
-  ws.w16max.reserve(c, 2);
-  ws.w16inv.reserve(c, 2);
-  ws.w16max.zero(2);
+// the weight copies of the fp16x2 forward GEMMs (transposed to K-major): slot 0
+// wx (3H x E), slot 1 w2 (E x E), slot 2 ux (3H x H, the recurrent forward step
+// GEMMs, activation scale 2^13); w16hi / w16lo hold them back to back
+void refresh_weights_f16(Ctx* c, const Model& m, const float* params, Workspace& ws) {
+  const int E = m.E, H = m.H, H3 = 3 * H;
+  const size_t n0 = (size_t)H3 * E, n1 = (size_t)E * E, n2 = (size_t)H3 * H;
+  ws.w16hi.reserve(c, n0 + n1 + n2);
+  ws.w16lo.reserve(c, n0 + n1 + n2);
+  ws.w16max.reserve(c, 3);
+  ws.w16inv.reserve(c, 3);
+  ws.w16max.zero(3);
   maxabs_kernel<<<64, 256, 0, c->stream>>>((int64_t)E * H3, params + m.o_wx, ws.w16max.p);
   after_launch(c);
   maxabs_kernel<<<64, 256, 0, c->stream>>>((int64_t)E * E, params + m.o_w2, ws.w16max.p + 1);
   after_launch(c);
+  maxabs_kernel<<<64, 256, 0, c->stream>>>((int64_t)H * H3, params + m.o_ux, ws.w16max.p + 2);
+  after_launch(c);
   weight_f16x2_kernel<<<dim3(cdiv(H3, 32), cdiv(E, 32)), dim3(32, 8), 0, c->stream>>>(
-      params + m.o_wx, E, H3, ws.w16max.p, ws.w16hi.p, ws.w16lo.p, ws.w16inv.p);
+      params + m.o_wx, E, H3, ws.w16max.p, ws.w16hi.p, ws.w16lo.p, ws.w16inv.p, kActScale);
   after_launch(c);
   weight_f16x2_kernel<<<dim3(cdiv(E, 32), cdiv(E, 32)), dim3(32, 8), 0, c->stream>>>(
-      params + m.o_w2, E, E, ws.w16max.p + 1, ws.w16hi.p + n0, ws.w16lo.p + n0, ws.w16inv.p + 1);
+      params + m.o_w2, E, E, ws.w16max.p + 1, ws.w16hi.p + n0, ws.w16lo.p + n0, ws.w16inv.p + 1, kActScale);
+  after_launch(c);
+  weight_f16x2_kernel<<<dim3(cdiv(H3, 32), cdiv(H, 32)), dim3(32, 8), 0, c->stream>>>(
+      params + m.o_ux, H, H3, ws.w16max.p + 2, ws.w16hi.p + n0 + n1, ws.w16lo.p + n0 + n1, ws.w16inv.p + 2,
+      8192.f);
   after_launch(c);
 }
 template <bool TA, bool TB, class Epi>
@@ -607,10 +616,11 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
     launch_pdl(c, split_lo_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, ws.wlo.p);
     if (f16) refresh_weights_f16(c, m, params, ws);
     ws.wlo_src = params;
-  } else if (f16 && ws.w16inv.n < 2) {
+  } else if (f16 && ws.w16inv.n < 3) {
     refresh_weights_f16(c, m, params, ws);
   }
   ws.wlo_stale = !ws.wlo_keep;
+  ws.f16_fwd = f16;
   if (f16) {
     // fp16x2: e1 and enc are tanh outputs (fixed scale), the weights' copies are
     // transposed to K-major

@@ -54,6 +54,8 @@ struct Workspace {
   // weight the max |w| (float bits) and the GEMM's 1 / (s_A s_B); the activation
   // operand's halves (enc / e1, fixed scale 2^14: tanh outputs)
   DBuf<__half> w16hi, w16lo, a16hi, a16lo;
+  DBuf<__half> h16hi, h16lo;                            // fp16x2 halves of h (forward pair steps; h0's at the end)
+  bool f16_fwd = false;  // this forward's weight halves are fresh (policy_forward): fp16x2 pair steps
   DBuf<unsigned> w16max;
   DBuf<float> w16inv;
   // wlo holds the lo of wlo_src's current values unless wlo_stale; owners whose

@@ -62,6 +62,18 @@ constexpr int TR = 6;
 // K-blocks per TMEM accumulation group (tc::PROMOTE in the general GEMM): the
 // split-K items here hold <= 4 K-blocks at C2, so one drain per item
 constexpr int SGP = 4;
+// fp16x2 operand of the forward step GEMM: h_{t-1} x kHScale = hi + lo (|h| < 8:
+// GRU states are convex combinations of tanh outputs and the initial state)
+constexpr float kHScale = 8192.f;  // 2^13
+__device__ __forceinline__ void split_h(float y, __half& hi, __half& lo) {
+  hi = __float2half_rn(y);
+  lo = __float2half_rn(y - __half2float(hi));
+}
+__global__ void h16_kernel(int64_t n, const float* __restrict__ x, __half* __restrict__ hi, __half* __restrict__ lo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    split_h(x[i] * kHScale, hi[i], lo[i]);
+}
+
 // element i of a register-resident float4 array (i a compile-time constant after
 // unrolling, so no local-memory copy)
 template <int N>
@@ -89,7 +101,8 @@ __device__ __forceinline__ void gate_phase(const Step& S, int H, const float* __
                                            const float* __restrict__ dhidden, const float* __restrict__ gates,
                                            const float* __restrict__ hun, const float* __restrict__ hprev,
                                            float* __restrict__ dpre, float* __restrict__ dhu,
-                                           float* __restrict__ gz, int tid, int nthreads) {
+                                           float* __restrict__ gz, int tid, int nthreads,
+                                           __half* __restrict__ h16hi = nullptr, __half* __restrict__ h16lo = nullptr) {
   const int H3 = 3 * H, N = DIR == 0 ? H3 : H;
   const int H4 = H / 4;
   const size_t zs = (size_t)S.B * N;
@@ -128,6 +141,15 @@ __device__ __forceinline__ void gate_phase(const Step& S, int H, const float* __
         g[3 * e + 2] = ng;
       }
       *reinterpret_cast<float4*>(hidden + row) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+      if (h16hi) {  // fp16x2 halves of h_t for the next fp16x2 step GEMM
+        __half hh[4], hl[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_h(hn[e] * kHScale, hh[e], hl[e]);
+        reinterpret_cast<__half2*>(h16hi + row)[0] = __halves2half2(hh[0], hh[1]);
+        reinterpret_cast<__half2*>(h16hi + row)[1] = __halves2half2(hh[2], hh[3]);
+        reinterpret_cast<__half2*>(h16lo + row)[0] = __halves2half2(hl[0], hl[1]);
+        reinterpret_cast<__half2*>(h16lo + row)[1] = __halves2half2(hl[2], hl[3]);
+      }
       if (gates_out) {
         float4* g4 = reinterpret_cast<float4*>(gates_out + row3);
         g4[0] = make_float4(g[0], g[1], g[2], g[3]);
@@ -474,7 +496,11 @@ constexpr int kPairEpiBytes = p2::EPIW * kFuseWarpFloats * 4;
 constexpr int kPairSmem = p2::STAGES2 * p2::STAGE2 + kPairEpiBytes + 1024 + 256;
 static_assert(kPairSmem <= 232448, "smem budget");
 
-template <int DIR>
+// F16 (forward only): fp16x2 GEMM phase (tc_gemm.cuh F16): A = h_{t-1} halves
+// (amaps[2 si], amaps[2 si + 1]; written next to h_t by the previous step's
+// epilogue / gate phase), B = U's transposed K-major halves (bmap / bmap_lo),
+// accumulator x *fscale; 64 K per stage, the split warps only relay.
+template <int DIR, int F16 = 0>
 __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     int nsteps, const Step* __restrict__ steps, const CUtensorMap* __restrict__ amaps,
     const __grid_constant__ CUtensorMap bmap, int H, float* __restrict__ part, unsigned* bar,
@@ -482,9 +508,12 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     float* __restrict__ gates_out, float* __restrict__ hun_out, float* __restrict__ hprev_out,
     const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
     const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
-    const __grid_constant__ CUtensorMap bmap_lo, int blo, long long* __restrict__ trace, int rbs) {
+    const __grid_constant__ CUtensorMap bmap_lo, int blo, long long* __restrict__ trace, int rbs,
+    __half* __restrict__ h16hi, __half* __restrict__ h16lo, const float* __restrict__ fscale) {
   using namespace p2;
-  constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
+  static_assert(!F16 || DIR == 0, "fp16x2 step GEMMs: forward only");
+  constexpr int AMAJ = 0, BMAJ = (DIR == 0 && !F16) ? 1 : 0;
+  constexpr int BKE = F16 ? 64 : BK;  // K elements per stage
   constexpr int PBN = PairTile<DIR>::BN, PBNH = PairTile<DIR>::BNH;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
@@ -499,7 +528,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int H3 = 3 * H, N = DIR == 0 ? H3 : H, K = DIR == 0 ? H : H3;
   const int tilesN = (N + PBN - 1) / PBN;
-  const int nkb_total = (K + BK - 1) / BK;
+  const int nkb_total = (K + BKE - 1) / BKE;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
@@ -536,14 +565,15 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   const uint32_t tmem = *tmem_slot;
   unsigned target = 0;
   unsigned* const rbf = bar + 32;  // row-tile counters of the fused steps, [nsteps][rbs]
+  const float fsc = F16 ? __ldg(fscale) : 1.f;  // 1 / (s_A s_B) of the fp16x2 GEMM
   int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
-  const uint32_t stage_tx = TILE + (blo ? 2u : 1u) * (uint32_t)PairTile<DIR>::BBYTES;
+  const uint32_t stage_tx = (F16 ? 2u : 1u) * TILE + (blo ? 2u : 1u) * (uint32_t)PairTile<DIR>::BBYTES;
 
   for (int si = 0; si < nsteps; ++si) {
     const Step S = steps[si];
     const int W = S.B > 0 ? S.tilesM * tilesN * S.Z : 0;  // tilesM in 256-row pair tiles
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si] = gtimer();
-    const CUtensorMap* amap = amaps + si;
+    const CUtensorMap* amap = amaps + (F16 ? 2 * si : si);
     for (int item = pair_id; item < W; item += npairs) {
       const bool first_item = item == pair_id;
       const int nt = item % tilesN, q = item / tilesN;
@@ -571,9 +601,16 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           for (int i = 0; i < nkb; ++i, ++it_tma) {
             const int s = it_tma % STAGES2;
             const uint32_t ph = (it_tma / STAGES2) & 1;
-            const int k0 = (kb0 + i) * BK;
+            const int k0 = (kb0 + i) * BKE;
             mbar_wait(empty_bar(s), ph ^ 1);
             mbar_expect_tx(full_bar(s), stage_tx);
+            if (F16) {
+              tma_load_2d(tileB(s, 0), &bmap, full_bar(s), k0, bn);
+              tma_load_2d(tileB(s, 1), &bmap_lo, full_bar(s), k0, bn);
+              tma_load_2d(tileA(s, 0), amap, full_bar(s), k0, am);
+              tma_load_2d(tileA(s, 1), amap + 1, full_bar(s), k0, am);
+              continue;
+            }
             if (BMAJ == 0) {
               tma_load_2d(tileB(s, 0), &bmap, full_bar(s), k0, bn);
               if (blo) tma_load_2d(tileB(s, 1), &bmap_lo, full_bar(s), k0, bn);
@@ -591,7 +628,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           }
         }
       } else if (warp == 1) {
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) |
+        const uint32_t fmt = F16 ? 0u : 2u;  // A / B f16 or tf32
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)AMAJ << 15) |
                                ((uint32_t)BMAJ << 16) | ((uint32_t)(PBN >> 3) << 17) | ((uint32_t)(BM2 >> 4) << 24);
         if (leader && lane == 0) {
           int buf = 0;
@@ -608,12 +646,18 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
             tc_fence_after();
             const uint32_t d = tmem + (uint32_t)(buf * kPairAccStride);
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
+            for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K per MMA
               const uint64_t ah = operand_desc<AMAJ>(tileA(s, 0), kk);
               const uint64_t bh = operand_desc<BMAJ>(tileB(s, 0), kk);
-              mma2_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
-              mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
-              mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+              if (F16) {
+                mma2_f16(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+                mma2_f16(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+                mma2_f16(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+              } else {
+                mma2_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+                mma2_tf32(d, operand_desc<AMAJ>(tileA(s, 1), kk), bh, idesc, 1u);
+                mma2_tf32(d, ah, operand_desc<BMAJ>(tileB(s, 1), kk), idesc, 1u);
+              }
             }
             commit2(empty_bar(s));
             if ((i % sgp) == sgp - 1 || i == nkb - 1) {
@@ -630,6 +674,11 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           const int s = it_split % STAGES2;
           const uint32_t ph = (it_split / STAGES2) & 1;
           mbar_wait(full_bar(s), ph);
+          if (F16) {  // pre-split operands: relay the landed stage to the leader
+            __syncwarp();
+            if (lane == 0) arrive_remote(to_rank(split_bar(s), 0));
+            continue;
+          }
           uint8_t* st = smem + s * STAGE2;
           const float4* ahi = reinterpret_cast<const float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE);
@@ -709,7 +758,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
                 : "r"(tmem + ((uint32_t)lane_base << 16) + (uint32_t)(buf * kPairAccStride + half * PBNH + cc * 32)));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = __uint_as_float(r[j]) * fsc;
           }
           tc_fence_before();
           __syncwarp();
@@ -741,7 +790,9 @@ _Pragma("unroll") \
               const float ng = gate_tanh(sx[2] + rg * sh[2]); \
               if (m < S.B && colok) { \
                 const size_t row = ((size_t)S.o + m) * H + u0 + lane; \
-                hidden[row] = (1.f - zg) * ng + zg * hp[r]; \
+                const float hnv = (1.f - zg) * ng + zg * hp[r]; \
+                hidden[row] = hnv; \
+                if (F16) split_h(hnv * kHScale, h16hi[row], h16lo[row]); \
                 if (gates_out) { \
                   hun_out[row] = sh[2]; \
                   hprev_out[row] = hp[r]; \
@@ -807,6 +858,10 @@ _Pragma("unroll") \
           __syncwarp();
           if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
         }
+        if (F16) {
+#pragma unroll
+          for (int j = 0; j < PBNH; ++j) sums[j] *= fsc;
+        }
         const int rr = lane >> 2, c4 = (lane & 3) * 4;
         // partial tile part[z][m][n] through the staging buffer (each warp store
         // covers 4 rows x 64 contiguous bytes)
@@ -835,7 +890,8 @@ _Pragma("unroll") \
     grid_sync(bar, target);  // all partials of step si written
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
     gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
-                    gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+                    gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, F16 ? h16hi : nullptr,
+                    F16 ? h16lo : nullptr);
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 5] = gtimer();
     if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
   }
@@ -891,12 +947,12 @@ static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs, in
 
 // CTA pairs resident at once for the pair step kernel (all its CTAs must be, for
 // the grid barriers), per device
-template <int DIR>
+template <int DIR, int F16 = 0>
 static int step_pairs(Ctx* c) {
   static std::atomic<int> cache[kMaxDevices];
   int pairs = cache[dev_slot(c)].load();
   if (!pairs) {
-    const void* fn = reinterpret_cast<const void*>(gru_step_gemm2_kernel<DIR>);
+    const void* fn = reinterpret_cast<const void*>(gru_step_gemm2_kernel<DIR, F16>);
     VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(c->num_sms);
@@ -910,7 +966,7 @@ static int step_pairs(Ctx* c) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int nc = 0;
-    VER_CUDA(cudaOccupancyMaxActiveClusters(&nc, gru_step_gemm2_kernel<DIR>, &cfg));
+    VER_CUDA(cudaOccupancyMaxActiveClusters(&nc, gru_step_gemm2_kernel<DIR, F16>, &cfg));
     pairs = std::max(1, std::min(nc, c->num_sms / 2));
     cache[dev_slot(c)].store(pairs);
   }
@@ -920,7 +976,7 @@ static int step_pairs(Ctx* c) {
 template <int DIR>
 static void launch(Ctx* c, const Model& m, const float* params, const std::vector<Step>& hs,
                    const std::vector<CUtensorMap>& maps, Workspace& ws, const float* h0, bool store,
-                   bool pair = false) {
+                   bool pair = false, bool f16 = false) {
   const int nsteps = (int)hs.size();
   if (nsteps == 0) return;
   const int H = m.H, H3 = 3 * H;
@@ -929,23 +985,32 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
   for (const Step& s : hs) part_n = std::max(part_n, (size_t)s.Z * s.B * N);
   ws.step.reserve(c, std::max<size_t>(part_n, 4));
   ws.sgsteps.reserve(c, (size_t)nsteps * sizeof(Step) / 4 + 1);
-  ws.sgmaps.reserve(c, (size_t)nsteps * sizeof(CUtensorMap) / 4 + 16);
+  const size_t nmaps = maps.size();  // one per step (two with f16: hi, lo)
+  ws.sgmaps.reserve(c, nmaps * sizeof(CUtensorMap) / 4 + 16);
   // 64-byte aligned tensor-map array inside the buffer
   uint8_t* mbase = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ws.sgmaps.p) + 63) & ~uintptr_t(63));
   VER_CUDA(cudaMemcpyAsync(ws.sgsteps.p, hs.data(), sizeof(Step) * nsteps, cudaMemcpyHostToDevice, c->stream));
-  VER_CUDA(cudaMemcpyAsync(mbase, maps.data(), sizeof(CUtensorMap) * nsteps, cudaMemcpyHostToDevice, c->stream));
+  VER_CUDA(cudaMemcpyAsync(mbase, maps.data(), sizeof(CUtensorMap) * nmaps, cudaMemcpyHostToDevice, c->stream));
   int rbs = 1;  // row tiles per step in the pair launch (step 0 has the most rows)
   for (const Step& st : hs) rbs = std::max(rbs, st.tilesM);
   const size_t nbar = pair ? 32 + (size_t)nsteps * rbs : 32;
   ws.bar.reserve(c, nbar);
   ws.bar.zero(nbar);
   const float* ux = params + m.o_ux;
-  const CUtensorMap bmap = DIR == 0 ? make_map(ux, H, H3, H3, 32, true) : make_map(ux, H, H3, H3, BN, false);
+  CUtensorMap bmap = DIR == 0 ? make_map(ux, H, H3, H3, 32, true) : make_map(ux, H, H3, H3, BN, false);
   // U's lo copy (made by the forward that precedes this launch, policy.cu)
   const float* ulo = (ws.wlo.n >= (size_t)m.P && env_int("VER_TC_BLO", 1)) ? ws.wlo.p + m.o_ux : nullptr;
   int blo = ulo != nullptr ? 1 : 0;
-  const CUtensorMap bmap_lo =
+  CUtensorMap bmap_lo =
       !blo ? bmap : (DIR == 0 ? make_map(ulo, H, H3, H3, 32, true) : make_map(ulo, H, H3, H3, BN, false));
+  const float* fscale = nullptr;
+  if (f16) {  // U's transposed fp16x2 halves (policy.cu refresh_weights_f16 slot 2): 3H x H, K-major
+    const size_t off = (size_t)H3 * m.E + (size_t)m.E * m.E;
+    bmap = make_map16(ws.w16hi.p + off, H3, H, H, PairTile<0>::BNH);
+    bmap_lo = make_map16(ws.w16lo.p + off, H3, H, H, PairTile<0>::BNH);
+    blo = 1;
+    fscale = ws.w16inv.p + 2;
+  }
   const int grid = c->num_sms;
   const void* fn = reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
   static std::atomic<bool> attr[kMaxDevices][2];  // per device: a function attribute is per device
@@ -979,7 +1044,7 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     tr = ws.trace.p;
   }
   if (pair) {
-    const int pairs = step_pairs<DIR>(c);
+    const int pairs = (DIR == 0 && f16) ? step_pairs<0, 1>(c) : step_pairs<DIR>(c);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(p2::THREADS2);
@@ -997,8 +1062,16 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     // kernels, so a plain cluster launch of <= one CTA per SM is co-resident there
     cfg.numAttrs = profiling() ? 1 : 2;
     ScopedEv ev(c, c->rec_tag);
-    VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<DIR>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
-                                hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo, tr, rbs));
+    __half* h16hi = ws.h16hi.p;
+    __half* h16lo = ws.h16lo.p;
+    if (f16 && DIR == 0)
+      VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<0, 1>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
+                                  hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo, tr,
+                                  rbs, h16hi, h16lo, fscale));
+    else
+      VER_CUDA(cudaLaunchKernelEx(&cfg, gru_step_gemm2_kernel<DIR>, ns, dsteps, dmaps, bmap, H, part, bar, xp, h0,
+                                  hidden, gts, hun_o, hpv_o, dh, gates, hun, hprev, dpre, dhu, gz, bmap_lo, blo, tr,
+                                  rbs, h16hi, h16lo, fscale));
     after_launch(c);
   } else {
     void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
@@ -1047,18 +1120,38 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
     if (ta >= tz) continue;
     std::vector<sg::Step> hs;
     std::vector<CUtensorMap> maps;
-    const int pairs = part == 0 ? sg::step_pairs<0>(c) : 0;
+    // fp16x2 GEMM phase for the pair steps when this forward's weight halves are
+    // fresh (policy_forward) and H fits 64-element K blocks
+    const bool f16 = part == 0 && ws.f16_fwd && H % 64 == 0;
+    const int pairs = part == 0 ? (f16 ? sg::step_pairs<0, 1>(c) : sg::step_pairs<0>(c)) : 0;
     const bool fuse = H % 32 == 0;
+    if (f16) {  // h halves: rows of every pair step (packed offsets), h0's after them
+      const size_t rows = (size_t)h_offs[tz - 1] + h_bs[tz - 1];
+      const size_t need = (rows + (size_t)h_bs[0]) * H;
+      ws.h16hi.reserve(c, need);
+      ws.h16lo.reserve(c, need);
+      const size_t n0 = (size_t)h_bs[0] * H;
+      sg::h16_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 4 * c->num_sms), 256, 0, c->stream>>>(
+          (int64_t)n0, h0, ws.h16hi.p + rows * H, ws.h16lo.p + rows * H);
+      after_launch(c);
+    }
     const bool force_fuse = env_int("VER_REC_FUSE_ALL", 0) != 0;  // tests / sanitizer
     for (int t = ta; t < tz; ++t) {
       const int B = h_bs[t];
       const int op = t == 0 ? -1 : h_offs[t - 1];
       hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse, force_fuse)
                              : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms));
-      const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
-      maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
+      if (f16) {
+        const size_t rows = (size_t)h_offs[tz - 1] + h_bs[tz - 1];
+        const size_t r0 = t == 0 ? rows : (size_t)h_offs[t - 1];
+        maps.push_back(tc::make_map16(ws.h16hi.p + r0 * H, B, H, H, tc::BM));
+        maps.push_back(tc::make_map16(ws.h16lo.p + r0 * H, B, H, H, tc::BM));
+      } else {
+        const float* hp = t == 0 ? h0 : ws.hidden.p + (size_t)h_offs[t - 1] * H;
+        maps.push_back(tc::make_map(hp, B, H, H, tc::BM, false));
+      }
     }
-    sg::launch<0>(c, m, params, hs, maps, ws, h0, store, part == 0);
+    sg::launch<0>(c, m, params, hs, maps, ws, h0, store, part == 0, f16);
   }
 }
 
