@@ -488,13 +488,24 @@ struct PairTile {
   static constexpr int BBYTES = BNH * BK * 4;  // one CTA's B half of a stage
 };
 constexpr int kPairAccStride = p2::BN2;         // TMEM columns per accumulator buffer (2 x 256 allocated)
-// epilogue staging per warp: the partial-tile path uses 32 x SLD floats, the fused
-// gate path two [4][kFRow] row groups (row stride 100: conflict-free float4 rows)
+// Shared memory of the pair step kernel: NST operand stages, then the epilogue
+// staging per warp -- the partial-tile path 32 x SLD floats, the fused gate path
+// CH accumulator rows [CH][kFRow] + a RING-slot cp.async ring of xp rows [2][kFRow] and
+// h_{t-1} rows [2][32] (row stride 100: conflict-free float4 rows).  The fp16x2
+// variant trades one operand stage for a deep ring: its MMAs are twice as fast,
+// and the gate epilogue needs ~9 groups of loads in flight to run at HBM speed.
 constexpr int kFRow = 100;
-constexpr int kFuseWarpFloats = 8 * kFRow > 32 * p2::SLD ? 8 * kFRow : 32 * p2::SLD;
-constexpr int kPairEpiBytes = p2::EPIW * kFuseWarpFloats * 4;
-constexpr int kPairSmem = p2::STAGES2 * p2::STAGE2 + kPairEpiBytes + 1024 + 256;
-static_assert(kPairSmem <= 232448, "smem budget");
+template <int F16>
+struct PairCfg {
+  static constexpr int NST = F16 ? 2 : p2::STAGES2;
+  static constexpr int RING = F16 ? 6 : 2;
+  static constexpr int CH = F16 ? 8 : 4;  // accumulator rows staged at a time
+  static constexpr int FUSED = CH * kFRow + RING * (2 * kFRow + 64);
+  static constexpr int WF = FUSED > 32 * p2::SLD ? FUSED : 32 * p2::SLD;  // floats per epilogue warp
+  static constexpr int EPI = p2::EPIW * WF * 4;
+  static constexpr int SMEM = NST * p2::STAGE2 + EPI + 1024 + 256;
+  static_assert(SMEM <= 232448, "smem budget");
+};
 
 // F16 (forward only): fp16x2 GEMM phase (tc_gemm.cuh F16): A = h_{t-1} halves
 // (amaps[2 si], amaps[2 si + 1]; written next to h_t by the previous step's
@@ -514,14 +525,15 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   static_assert(!F16 || DIR == 0, "fp16x2 step GEMMs: forward only");
   constexpr int AMAJ = 0, BMAJ = (DIR == 0 && !F16) ? 1 : 0;
   constexpr int BKE = F16 ? 64 : BK;  // K elements per stage
+  constexpr int NST = PairCfg<F16>::NST, RING = PairCfg<F16>::RING;
   constexpr int PBN = PairTile<DIR>::BN, PBNH = PairTile<DIR>::BNH;
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
   // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + kPairEpiBytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC2);
+  float* stg_all = reinterpret_cast<float*>(smem + NST * STAGE2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE2 + PairCfg<F16>::EPI);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * NACC2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
@@ -532,15 +544,15 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
-  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES2 + s); };
-  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES2 + s); };
-  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES2 + b); };
-  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES2 + NACC2 + b); };
+  auto split_bar = [&](int s) { return bar0 + 8 * (NST + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * NST + s); };
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * NST + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * NST + NACC2 + b); };
   auto tileA = [&](int s, int lo) { return sbase + s * STAGE2 + lo * TILE; };
   auto tileB = [&](int s, int lo) { return sbase + s * STAGE2 + (2 + lo) * TILE; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(split_bar(s), 2 * SPLITW);
       mbar_init(empty_bar(s), 1);
@@ -599,8 +611,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           }
           const int am = m0 + (int)rank * BM, bn = n0 + (int)rank * PBNH;
           for (int i = 0; i < nkb; ++i, ++it_tma) {
-            const int s = it_tma % STAGES2;
-            const uint32_t ph = (it_tma / STAGES2) & 1;
+            const int s = it_tma % NST;
+            const uint32_t ph = (it_tma / NST) & 1;
             const int k0 = (kb0 + i) * BKE;
             mbar_wait(empty_bar(s), ph ^ 1);
             mbar_expect_tx(full_bar(s), stage_tx);
@@ -634,8 +646,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
         if (leader && lane == 0) {
           int buf = 0;
           for (int i = 0; i < nkb; ++i, ++it_mma) {
-            const int s = it_mma % STAGES2;
-            const uint32_t ph = (it_mma / STAGES2) & 1;
+            const int s = it_mma % NST;
+            const uint32_t ph = (it_mma / NST) & 1;
             const bool first = (i % sgp) == 0;
             if (first) {
               buf = g_mma % NACC2;
@@ -671,8 +683,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
       } else if (warp < 2 + SPLITW) {
         const int et = threadIdx.x - 64;
         for (int i = 0; i < nkb; ++i, ++it_split) {
-          const int s = it_split % STAGES2;
-          const uint32_t ph = (it_split / STAGES2) & 1;
+          const int s = it_split % NST;
+          const uint32_t ph = (it_split / NST) & 1;
           mbar_wait(full_bar(s), ph);
           if (F16) {  // pre-split operands: relay the landed stage to the leader
             __syncwarp();
@@ -703,18 +715,21 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
         // column half (warp - 4) / 4)
         const int lq = warp & 3, half = (warp - 4) >> 2;
         const int lane_base = 32 * lq;
-        float* stg = stg_all + (warp - 4) * kFuseWarpFloats;
+        float* stg = stg_all + (warp - 4) * PairCfg<F16>::WF;
         const int mrow0 = m0 + (int)rank * BM + lane_base, ncol0 = n0 + half * PBNH;
         if (DIR == 0 && S.pad != 0) {
           // GRU gates (nn.cpp:235-250) in the epilogue of a split-K-free item: this
           // warp's 32 rows x the 32 whole units [ncol0 / 3, ncol0 / 3 + 32).  The
           // accumulator arrives lane = row (TMEM lanes); the gate math runs lane = unit
           // so that every global access is a contiguous row segment (h / hUn / h_prev:
-          // 128 B, xp / gates: 384 B).  Rows go in groups of 4 through the warp's
-          // staging area: hU rows from their owner lanes, xp rows from coalesced float4
-          // loads issued one group ahead (the first group's during the item's MMAs).
-          float* fh = stg_all + (warp - 4) * kFuseWarpFloats;  // [4][kFRow] hU rows
-          float* fx = fh + 4 * kFRow;                            // [4][kFRow] xp rows, then gates
+          // 128 B, xp / gates: 384 B).  Rows go in 16 groups of 2 through the warp's
+          // staging area: hU rows from their owner lanes (CH at a time); the xp and h_{t-1} rows by
+          // cp.async into a 3-buffer ring, two groups ahead (the first two during the
+          // item's MMAs), so the loads cost no registers and their latency hides
+          // behind two groups of gate math.
+          float* fh = stg_all + (warp - 4) * PairCfg<F16>::WF;  // [CH][kFRow] hU rows
+          float* fx0 = fh + PairCfg<F16>::CH * kFRow;            // [RING][2][kFRow] xp rows, then gates
+          float* fp0 = fx0 + RING * 2 * kFRow;                   // [RING][2][32] h_{t-1} rows
           const int u0 = ncol0 / 3;
           const bool colok = ncol0 < N;
           const int blast = max(S.B - 1, 0);
@@ -725,20 +740,29 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
             asm volatile("prefetch.global.L2 [%0];" ::"l"(xr));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + 32));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + 64));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(hsrc + (size_t)m * H + u0));
           }
           if (dep) spin_acquire(dep, dep_need);  // h_{t-1} rows of this row tile (read below)
           const int xl = lane < 24 ? 4 * lane : 0;  // this lane's float4 of a 96-column xp row
-          float4 xva[4], xvb[4];
-          float hva[4], hvb[4];
-#define VER_FUSED_LOAD(k, xv, hv)                                                                \
-  _Pragma("unroll") for (int r = 0; r < 4; ++r) {                                                \
-    const int m = min(mrow0 + 4 * (k) + r, blast);                                               \
-    xv[r] = *reinterpret_cast<const float4*>(xp + ((size_t)S.o + m) * N + (colok ? ncol0 + xl : 0)); \
-    hv[r] = hsrc[(size_t)m * H + (colok ? u0 + lane : 0)];                                       \
-  }
-          VER_FUSED_LOAD(0, xva, hva)
-          VER_FUSED_LOAD(1, xvb, hvb)
+          auto issue = [&](int k) {  // rows 2k, 2k + 1 -> ring slot k % RING
+            float* fx = fx0 + (k % RING) * 2 * kFRow;
+            float* fp = fp0 + (k % RING) * 64;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const int m = min(mrow0 + 2 * k + r, blast);
+              if (lane < 24)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(fx + r * kFRow + xl)),
+                             "l"(xp + ((size_t)S.o + m) * N + (colok ? ncol0 + xl : 0))
+                             : "memory");
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(fp + r * 32 + lane)),
+                           "l"(hsrc + (size_t)m * H + (colok ? u0 + lane : 0))
+                           : "memory");
+            }
+          };
+#pragma unroll
+          for (int k = 0; k < RING - 1; ++k) {  // the first RING - 1 groups during the item's MMAs
+            issue(k);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+          }
           const int buf = g_epi % NACC2;
           mbar_wait(acc_full(buf), (g_epi / NACC2) & 1);
           if (trace && blockIdx.x == 0 && threadIdx.x == 128) trace[TR * si + 2] = gtimer();  // last acc ready
@@ -764,63 +788,59 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           __syncwarp();
           if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));  // TMEM free for the item after next
           ++g_epi;
-#define VER_FUSED_GROUP(k, xv, hv)                                                            \
-          { \
-            if ((lane >> 2) == (k)) { \
-              float4* d = reinterpret_cast<float4*>(fh + (lane & 3) * kFRow); \
-_Pragma("unroll") \
-              for (int q = 0; q < PBNH / 4; ++q) d[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]); \
-            } \
-            if (lane < 24) { \
-_Pragma("unroll") \
-              for (int r = 0; r < 4; ++r) *reinterpret_cast<float4*>(fx + r * kFRow + xl) = xv[r]; \
-            } \
-            float hp[4]; \
-_Pragma("unroll") \
-            for (int r = 0; r < 4; ++r) hp[r] = hv[r]; \
-            __syncwarp(); \
-            if ((k) + 2 < 8) { VER_FUSED_LOAD((k) + 2, xv, hv) } \
-_Pragma("unroll") \
-            for (int r = 0; r < 4; ++r) { \
-              const int m = mrow0 + 4 * (k) + r; \
-              const float* sh = fh + r * kFRow + 3 * lane; \
-              float* sx = fx + r * kFRow + 3 * lane; \
-              const float rg = gate_sigm(sx[0] + sh[0]); \
-              const float zg = gate_sigm(sx[1] + sh[1]); \
-              const float ng = gate_tanh(sx[2] + rg * sh[2]); \
-              if (m < S.B && colok) { \
-                const size_t row = ((size_t)S.o + m) * H + u0 + lane; \
-                const float hnv = (1.f - zg) * ng + zg * hp[r]; \
-                hidden[row] = hnv; \
-                if (F16) split_h(hnv * kHScale, h16hi[row], h16lo[row]); \
-                if (gates_out) { \
-                  hun_out[row] = sh[2]; \
-                  hprev_out[row] = hp[r]; \
-                } \
-              } \
-              sx[0] = rg; \
-              sx[1] = zg; \
-              sx[2] = ng; \
-            } \
-            __syncwarp(); \
-            if (gates_out && lane < 24 && colok) { \
-_Pragma("unroll") \
-              for (int r = 0; r < 4; ++r) { \
-                const int m = mrow0 + 4 * (k) + r; \
-                if (m < S.B) \
-                  *reinterpret_cast<float4*>(gates_out + ((size_t)S.o + m) * N + ncol0 + xl) = \
-                      *reinterpret_cast<const float4*>(fx + r * kFRow + xl); \
-              } \
-            } \
-            __syncwarp(); \
-          }
 #pragma unroll 1
-          for (int k = 0; k < 8; k += 2) {
-            VER_FUSED_GROUP(k, xva, hva)
-            VER_FUSED_GROUP(k + 1, xvb, hvb)
+          for (int k = 0; k < 16; ++k) {
+            if (k + RING - 1 < 16) issue(k + RING - 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");  // (empty near the end: keeps the count)
+            asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");  // group k has landed
+            constexpr int CH = PairCfg<F16>::CH, GPC = CH / 2;  // groups per staged chunk
+            if (k % GPC == 0) {  // rows CH c .. CH c + CH - 1 from their owner lanes (fh is free: last group synced)
+              if (lane / CH == k / GPC) {
+                float4* d = reinterpret_cast<float4*>(fh + (lane % CH) * kFRow);
+#pragma unroll
+                for (int q = 0; q < PBNH / 4; ++q)
+                  d[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+              }
+            }
+            __syncwarp();
+            float* fx = fx0 + (k % RING) * 2 * kFRow;
+            const float* fp = fp0 + (k % RING) * 64;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const int m = mrow0 + 2 * k + r;
+              const float* sh = fh + (2 * (k % GPC) + r) * kFRow + 3 * lane;
+              float* sx = fx + r * kFRow + 3 * lane;
+              const float hpv = fp[r * 32 + lane];
+              const float rg = gate_sigm(sx[0] + sh[0]);
+              const float zg = gate_sigm(sx[1] + sh[1]);
+              const float ng = gate_tanh(sx[2] + rg * sh[2]);
+              if (m < S.B && colok) {
+                const size_t row = ((size_t)S.o + m) * H + u0 + lane;
+                const float hnv = (1.f - zg) * ng + zg * hpv;
+                hidden[row] = hnv;
+                if (F16) split_h(hnv * kHScale, h16hi[row], h16lo[row]);
+                if (gates_out) {
+                  hun_out[row] = sh[2];
+                  hprev_out[row] = hpv;
+                }
+              }
+              sx[0] = rg;
+              sx[1] = zg;
+              sx[2] = ng;
+            }
+            __syncwarp();
+            if (gates_out && lane < 24 && colok) {
+#pragma unroll
+              for (int r = 0; r < 2; ++r) {
+                const int m = mrow0 + 2 * k + r;
+                if (m < S.B)
+                  *reinterpret_cast<float4*>(gates_out + ((size_t)S.o + m) * N + ncol0 + xl) =
+                      *reinterpret_cast<const float4*>(fx + r * kFRow + xl);
+              }
+            }
+            __syncwarp();  // this ring slot and fh are rewritten by later groups
           }
-#undef VER_FUSED_GROUP
-#undef VER_FUSED_LOAD
+          asm volatile("cp.async.wait_group 0;" ::: "memory");
           // this warp's h_t rows of row tile m0 / BM2 are written: count in
           __threadfence();
           __syncwarp();
@@ -953,11 +973,11 @@ static int step_pairs(Ctx* c) {
   int pairs = cache[dev_slot(c)].load();
   if (!pairs) {
     const void* fn = reinterpret_cast<const void*>(gru_step_gemm2_kernel<DIR, F16>);
-    VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmem));
+    VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<F16>::SMEM));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(c->num_sms);
     cfg.blockDim = dim3(p2::THREADS2);
-    cfg.dynamicSmemBytes = kPairSmem;
+    cfg.dynamicSmemBytes = PairCfg<F16>::SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 2;
@@ -1048,7 +1068,7 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(p2::THREADS2);
-    cfg.dynamicSmemBytes = kPairSmem;
+    cfg.dynamicSmemBytes = (DIR == 0 && f16) ? PairCfg<1>::SMEM : PairCfg<0>::SMEM;
     cfg.stream = c->stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
