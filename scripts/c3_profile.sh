@@ -27,7 +27,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_g
   -o $OUT/prof_c3_tc_gemm $P --updates 1 > $OUT/prof_c3_tc_gemm.log 2>&1
 for d in 0 1; do
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:gru_step_gemm2?_kernel<.{0,5}$d>" -s 2 -c 2 \
+  -k "regex:gru_step_gemm2?_kernel<.{0,5}$d(, .{0,8})?>" -s 2 -c 2 \
   -o $OUT/prof_c3_gru_step_gemm$d $P --updates 1 > $OUT/prof_c3_gru_step_gemm$d.log 2>&1
 done
 ls -la $OUT
