@@ -263,13 +263,23 @@ static bool f16x2_on(const Ctx* c) { return c->precision == 0 && c->tensor_cores
 // the weight copies of the fp16x2 forward GEMMs (transposed to K-major): slot 0
 // wx (3H x E), slot 1 w2 (E x E), slot 2 ux (3H x H, the recurrent forward step
 // GEMMs, activation scale 2^13); w16hi / w16lo hold them back to back
+// slots 3 / 4: wx (E x 3H) and w2 (E x E) as they lie (K-major B of the backward
+// data-gradient GEMMs, fp16x2 with the gradient converted in-kernel), inv = 1 / s_W
+__global__ void weight_f16x2_plain_kernel(int64_t n, const float* __restrict__ W,
+                                          const unsigned* __restrict__ maxbits, __half* __restrict__ hi,
+                                          __half* __restrict__ lo, float* __restrict__ inv) {
+  const float s = weight_scale(*maxbits);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    split_h2(W[i] * s, hi[i], lo[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *inv = 1.f / s;
+}
 void refresh_weights_f16(Ctx* c, const Model& m, const float* params, Workspace& ws) {
   const int E = m.E, H = m.H, H3 = 3 * H;
   const size_t n0 = (size_t)H3 * E, n1 = (size_t)E * E, n2 = (size_t)H3 * H;
-  ws.w16hi.reserve(c, n0 + n1 + n2);
-  ws.w16lo.reserve(c, n0 + n1 + n2);
+  ws.w16hi.reserve(c, 2 * (n0 + n1) + n2);
+  ws.w16lo.reserve(c, 2 * (n0 + n1) + n2);
   ws.w16max.reserve(c, 3);
-  ws.w16inv.reserve(c, 3);
+  ws.w16inv.reserve(c, 5);
   ws.w16max.zero(3);
   maxabs_kernel<<<64, 256, 0, c->stream>>>((int64_t)E * H3, params + m.o_wx, ws.w16max.p);
   after_launch(c);
@@ -286,6 +296,15 @@ void refresh_weights_f16(Ctx* c, const Model& m, const float* params, Workspace&
   weight_f16x2_kernel<<<dim3(cdiv(H3, 32), cdiv(H, 32)), dim3(32, 8), 0, c->stream>>>(
       params + m.o_ux, H, H3, ws.w16max.p + 2, ws.w16hi.p + n0 + n1, ws.w16lo.p + n0 + n1, ws.w16inv.p + 2,
       8192.f);
+  after_launch(c);
+  const size_t o3 = n0 + n1 + n2, o4 = o3 + n0;
+  weight_f16x2_plain_kernel<<<(unsigned)cdiv(n0, 256), 256, 0, c->stream>>>((int64_t)n0, params + m.o_wx, ws.w16max.p,
+                                                                           ws.w16hi.p + o3, ws.w16lo.p + o3,
+                                                                           ws.w16inv.p + 3);
+  after_launch(c);
+  weight_f16x2_plain_kernel<<<(unsigned)cdiv(n1, 256), 256, 0, c->stream>>>((int64_t)n1, params + m.o_w2,
+                                                                           ws.w16max.p + 1, ws.w16hi.p + o4,
+                                                                           ws.w16lo.p + o4, ws.w16inv.p + 4);
   after_launch(c);
 }
 template <bool TA, bool TB, class Epi>
@@ -616,7 +635,7 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
     launch_pdl(c, split_lo_kernel, dim3(cdiv(m.P, 256)), dim3(256), 0, (int64_t)m.P, params, ws.wlo.p);
     if (f16) refresh_weights_f16(c, m, params, ws);
     ws.wlo_src = params;
-  } else if (f16 && ws.w16inv.n < 3) {
+  } else if (f16 && ws.w16inv.n < 5) {
     refresh_weights_f16(c, m, params, ws);
   }
   ws.wlo_stale = !ws.wlo_keep;
@@ -1775,12 +1794,35 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
   gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
   gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);
   colsum(c, ws, ws.dpre.p, S, H3, H3, grad + m.o_bx);
-  gemm<false, true>(c, S, E, H3, ws.dpre.p, H3, params + m.o_wx, H3, EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E},
-                    ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_wx : nullptr);
+  // data gradients: fp16x2 when this minibatch's forward made the weight halves
+  // (the gradient operand's max by a pass, its halves written in the GEMM)
+  const bool f16 = ws.f16_fwd && ws.w16inv.n >= 5 && tc::usable_f16(S, E, H3, H3, H3) &&
+                   tc::usable_f16(S, E, E, E, E) && tc::usable(S, E, H3, ws.dpre.p, H3, ws.dpre.p, H3,
+                                                               EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E});
+  // slots 3 / 4 of refresh_weights_f16: after wx^T (3H x E), w2^T (E x E), ux^T (3H x H)
+  const size_t o3 = (size_t)H3 * E + (size_t)E * E + (size_t)H3 * H, o4 = o3 + (size_t)H3 * E;
+  if (f16) {
+    ws.gmax.reserve(c, 2);
+    ws.gmax.zero(2);
+    maxabs_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>((int64_t)S * H3, ws.dpre.p, ws.gmax.p);
+    after_launch(c);
+    tc::launch_f16a(c, S, E, H3, ws.dpre.p, H3, ws.w16hi.p + o3, ws.w16lo.p + o3, H3, ws.gmax.p, ws.w16inv.p + 3,
+                    EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E}, 1);
+  } else {
+    gemm<false, true>(c, S, E, H3, ws.dpre.p, H3, params + m.o_wx, H3, EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E},
+                      ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_wx : nullptr);
+  }
   gemm_splitk<true, false>(c, ws, E, E, S, ws.e1.p, E, ws.dpre2.p, E, grad + m.o_w2, E);
   colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2);
-  gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E},
-                    ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_w2 : nullptr);
+  if (f16) {
+    maxabs_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>((int64_t)S * E, ws.dpre2.p, ws.gmax.p + 1);
+    after_launch(c);
+    tc::launch_f16a(c, S, E, E, ws.dpre2.p, E, ws.w16hi.p + o4, ws.w16lo.p + o4, E, ws.gmax.p + 1, ws.w16inv.p + 4,
+                    EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E}, 1);
+  } else {
+    gemm<false, true>(c, S, E, E, ws.dpre2.p, E, params + m.o_w2, E, EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E},
+                      ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_w2 : nullptr);
+  }
   {
     // ~4 blocks per SM: 128-feature blocks (float4 path) or 32-feature blocks
     const int col_blocks = (int)cdiv(E, E % 4 == 0 ? 128 : 32);

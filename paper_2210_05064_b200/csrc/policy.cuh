@@ -57,6 +57,7 @@ struct Workspace {
   DBuf<__half> h16hi, h16lo;                            // fp16x2 halves of h (forward pair steps; h0's at the end)
   bool f16_fwd = false;  // this forward's weight halves are fresh (policy_forward): fp16x2 pair steps
   DBuf<unsigned> w16max;
+  DBuf<unsigned> gmax;  // max |dpre|, max |dpre2| (float bits) of this backward: the fp16x2 data-gradient scales
   DBuf<float> w16inv;
   // wlo holds the lo of wlo_src's current values unless wlo_stale; owners whose
   // parameters change in place (the learner's Adam) leave it stale (the default)

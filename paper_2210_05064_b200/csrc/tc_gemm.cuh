@@ -610,17 +610,23 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
                                                                const __grid_constant__ CUtensorMap tmBl,
                                                                int promote,
                                                                const __grid_constant__ CUtensorMap tmAl,
-                                                               const float* __restrict__ fscale) {
+                                                               const float* __restrict__ fscale,
+                                                               const unsigned* __restrict__ amax) {
   static_assert(!F16 || (AMAJ == 0 && BMAJ == 0), "fp16x2 operands are K-major");
   constexpr int BKE = F16 ? 64 : BK;  // K elements per stage
+  // F16 == 2: A lands as fp32 (two 32-K boxes) and the split warps write its scaled
+  // halves; stage = A fp32 32 KB | A hi | A lo | B hi | B lo, two stages
+  constexpr int NS = F16 == 2 ? 2 : STAGES2;
+  constexpr int SB = F16 == 2 ? 6 * TILE : STAGE2;
+  constexpr int A0 = F16 == 2 ? 2 * TILE : 0;  // A hi offset in the stage
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
   // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* stg_all = reinterpret_cast<float*>(smem + STAGES2 * STAGE2);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES2 * STAGE2 + EPI2);
+  float* stg_all = reinterpret_cast<float*>(smem + NS * SB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * SB + EPI2);
   // bars: full[S] split[S] empty[S] acc_full[NACC2] acc_empty[NACC2]; then the TMEM address slot
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES2 + 2 * NACC2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 2 * NACC2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
@@ -631,12 +637,12 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
-  auto split_bar = [&](int s) { return bar0 + 8 * (STAGES2 + s); };
-  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * STAGES2 + s); };
-  auto acc_full = [&](int b) { return bar0 + 8 * (3 * STAGES2 + b); };
-  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * STAGES2 + NACC2 + b); };
-  auto tileA = [&](int s, int lo) { return sbase + s * STAGE2 + lo * TILE; };
-  auto tileB = [&](int s, int lo) { return sbase + s * STAGE2 + (2 + lo) * TILE; };
+  auto split_bar = [&](int s) { return bar0 + 8 * (NS + s); };
+  auto empty_bar = [&](int s) { return bar0 + 8 * (2 * NS + s); };
+  auto acc_full = [&](int b) { return bar0 + 8 * (3 * NS + b); };
+  auto acc_empty = [&](int b) { return bar0 + 8 * (3 * NS + NACC2 + b); };
+  auto tileA = [&](int s, int lo) { return sbase + s * SB + A0 + lo * TILE; };
+  auto tileB = [&](int s, int lo) { return sbase + s * SB + A0 + (2 + lo) * TILE; };
   struct Tile {
     int m0, n0, z, kb0, nkb;
   };
@@ -652,7 +658,7 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES2; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(full_bar(s), 1);
       mbar_init(split_bar(s), 2 * SPLITW);
       mbar_init(empty_bar(s), 1);
@@ -665,7 +671,7 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     if (BLO || F16) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmBl)) : "memory");
-    if (F16) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmAl)) : "memory");
+    if (F16 == 1) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmAl)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -689,9 +695,19 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
         const Tile T = decode(t);
         const int am = T.m0 + (int)rank * BM, bn = T.n0 + (int)rank * BNH;
         for (int i = 0; i < T.nkb; ++i, ++it) {
-          const int s = it % STAGES2;
-          const uint32_t ph = (it / STAGES2) & 1;
+          const int s = it % NS;
+          const uint32_t ph = (it / NS) & 1;
           mbar_wait(empty_bar(s), ph ^ 1);
+          if (F16 == 2) {
+            mbar_expect_tx(full_bar(s), 4 * TILE);
+            const int k0 = (T.kb0 + i) * BKE;
+            const uint32_t a32 = sbase + s * SB;
+            tma_load_2d(a32, &tmA, full_bar(s), k0, am);
+            tma_load_2d(a32 + TILE, &tmA, full_bar(s), k0 + 32, am);
+            tma_load_2d(tileB(s, 0), &tmB, full_bar(s), k0, bn);
+            tma_load_2d(tileB(s, 1), &tmBl, full_bar(s), k0, bn);
+            continue;
+          }
           if (F16) {
             mbar_expect_tx(full_bar(s), 4 * TILE);
             const int k0 = (T.kb0 + i) * BKE;
@@ -735,8 +751,8 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
       for (int t = pair_id; t < ntiles; t += npairs) {
         const Tile T = decode(t);
         for (int i = 0; i < T.nkb; ++i, ++it) {
-          const int s = it % STAGES2;
-          const uint32_t ph = (it / STAGES2) & 1;
+          const int s = it % NS;
+          const uint32_t ph = (it / NS) & 1;
           const bool first = (i % promote) == 0;
           if (first) {
             buf = g % NACC2;
@@ -772,14 +788,49 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
   } else if (warp < 2 + SPLITW) {
     // ---------------- 3xTF32 operand split (both CTAs), then arrive on the leader
     const int et = threadIdx.x - 64;  // 0..63
+    // A's scale (F16 == 2): 2^(14 - floor(log2 max|A|)) from the max its producer pass took
+    float a_s = 1.f;
+    if (F16 == 2) {
+      const float mx = __uint_as_float(*amax);
+      a_s = (mx > 0.f && isfinite(mx)) ? exp2f((float)(14 - ilogbf(mx))) : 1.f;
+    }
     int it = 0;
     for (int t = pair_id; t < ntiles; t += npairs) {
       const Tile T = decode(t);
       for (int i = 0; i < T.nkb; ++i, ++it) {
-        const int s = it % STAGES2;
-        const uint32_t ph = (it / STAGES2) & 1;
+        const int s = it % NS;
+        const uint32_t ph = (it / NS) & 1;
         mbar_wait(full_bar(s), ph);
-        if (!F16) {
+        if (F16 == 2) {
+          // fp32 A (two 32-K swizzled boxes: row r's 16-byte chunk j at j ^ (r & 7))
+          // -> scaled halves, 64 K per 128-byte row (chunk c' = 8 halves at c' ^ (r & 7))
+          const uint8_t* a32 = smem + s * SB;
+          uint8_t* ahi = smem + s * SB + A0;
+          uint8_t* alo = ahi + TILE;
+#pragma unroll 4
+          for (int q = et; q < BM * 8; q += 32 * SPLITW) {
+            const int r = q >> 3, c = q & 7, sw = r & 7;
+            const uint8_t* src = a32 + (c >> 2) * TILE + r * 128;
+            const int j0 = (2 * c) & 7;
+            const float4 x0 = *reinterpret_cast<const float4*>(src + ((j0 ^ sw) << 4));
+            const float4 x1 = *reinterpret_cast<const float4*>(src + (((j0 + 1) ^ sw) << 4));
+            const float2 v[4] = {make_float2(x0.x * a_s, x0.y * a_s), make_float2(x0.z * a_s, x0.w * a_s),
+                                 make_float2(x1.x * a_s, x1.y * a_s), make_float2(x1.z * a_s, x1.w * a_s)};
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {  // packed conversions: one cvt per pair of values
+              const __half2 hh = __float22half2_rn(v[e]);
+              const float2 hb = __half22float2(hh);
+              const __half2 ll = __float22half2_rn(make_float2(v[e].x - hb.x, v[e].y - hb.y));
+              hw[e] = *reinterpret_cast<const uint32_t*>(&hh);
+              lw[e] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+            const int o = r * 128 + ((c ^ sw) << 4);
+            *reinterpret_cast<uint4*>(ahi + o) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(alo + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        } else if (!F16) {
           uint8_t* st = smem + s * STAGE2;
           const float4* ahi = reinterpret_cast<const float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE);
@@ -842,7 +893,11 @@ __global__ void __launch_bounds__(THREADS2, 1) tc_gemm2_kernel(const __grid_cons
         if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));
       }
       if (F16) {  // undo the operand scales (a power of two: exact)
-        const float sc = *fscale;
+        float sc = *fscale;
+        if (F16 == 2) {
+          const float mx = __uint_as_float(*amax);
+          sc /= (mx > 0.f && isfinite(mx)) ? exp2f((float)(14 - ilogbf(mx))) : 1.f;
+        }
 #pragma unroll
         for (int j = 0; j < BNH; ++j) sums[j] *= sc;
       }
@@ -980,7 +1035,7 @@ void launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
     }
     cfg.gridDim = dim3(2 * (int)std::min<long long>(ntiles, pairs));
     VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote, ta,
-                                static_cast<const float*>(nullptr)));
+                                static_cast<const float*>(nullptr), static_cast<const unsigned*>(nullptr)));
     after_launch(c);
   };
   if (blo) run(p2::tc_gemm2_kernel<AMAJ, BMAJ, Epi, 1>);
@@ -1046,7 +1101,55 @@ void launch_f16(Ctx* c, int M, int N, int K, const __half* Ahi, const __half* Al
     pairs_cache[dev_slot(c)].store(pairs);
   }
   cfg.gridDim = dim3(2 * (int)std::min<long long>(ntiles, pairs));
-  VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote, tal, fscale));
+  VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote, tal, fscale,
+                              static_cast<const unsigned*>(nullptr)));
+  after_launch(c);
+}
+
+// C = A (B_hi + B_lo)^T / s_B with A fp32 (M x K, K-major, row stride lda floats)
+// converted to scaled fp16 halves inside the kernel (F16 == 2): *amax (device) =
+// max |A| bits taken by a pass before, *binv = 1 / s_B; B N x K K-major halves.
+constexpr int SMEM2_F16A = 2 * 6 * p2::TILE + p2::EPI2 + 1024 + 256;
+static_assert(SMEM2_F16A <= 232448, "smem budget");
+template <class Epi>
+void launch_f16a(Ctx* c, int M, int N, int K, const float* A, int lda, const __half* Bhi, const __half* Blo,
+                 int ldb, const unsigned* amax, const float* binv, Epi epi, int splits) {
+  ScopedEv ev(c, c->gemm_tag);
+  if (c->evlog && c->flop_log && c->gemm_tag >= 0) c->flop_log[c->gemm_tag] += 2.0 * M * (double)N * K;
+  const CUtensorMap ta = make_map(A, M, K, lda, BM, false);
+  const CUtensorMap tb = make_map16(Bhi, N, K, ldb, p2::BNH), tbl = make_map16(Blo, N, K, ldb, p2::BNH);
+  const int nkb = (K + 63) / 64;
+  splits = std::max(1, std::min(splits, nkb));
+  const int per = (nkb + splits - 1) / splits;
+  splits = (nkb + per - 1) / per;
+  const long long ntiles = cdiv(N, p2::BN2) * cdiv(M, p2::BM2) * (long long)splits;
+  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  auto kern = p2::tc_gemm2_kernel<0, 0, Epi, 0, 2>;
+  VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_F16A));
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(p2::THREADS2);
+  cfg.dynamicSmemBytes = SMEM2_F16A;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  static std::atomic<int> pairs_cache[kMaxDevices];
+  int pairs = pairs_cache[dev_slot(c)].load();
+  if (!pairs) {
+    cfg.gridDim = dim3(c->num_sms);
+    int nc = 0;
+    VER_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+    pairs = std::max(1, std::min(nc, c->num_sms / 2));
+    pairs_cache[dev_slot(c)].store(pairs);
+  }
+  cfg.gridDim = dim3(2 * (int)std::min<long long>(ntiles, pairs));
+  VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote, ta, binv, amax));
   after_launch(c);
 }
 
