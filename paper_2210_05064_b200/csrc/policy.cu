@@ -226,6 +226,7 @@ __device__ __forceinline__ void split_h2(float y, __half& hi, __half& lo) {
   lo = __float2half_rn(y - __half2float(hi));
 }
 __global__ void maxabs_kernel(int64_t n, const float* __restrict__ x, unsigned* __restrict__ out) {
+  pdl_wait();
   float m = 0.f;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     m = fmaxf(m, fabsf(x[i]));
@@ -295,7 +296,7 @@ void refresh_weights_f16(Ctx* c, const Model& m, const float* params, Workspace&
   after_launch(c);
   weight_f16x2_kernel<<<dim3(cdiv(H3, 32), cdiv(H, 32)), dim3(32, 8), 0, c->stream>>>(
       params + m.o_ux, H, H3, ws.w16max.p + 2, ws.w16hi.p + n0 + n1, ws.w16lo.p + n0 + n1, ws.w16inv.p + 2,
-      8192.f);
+      1.f);  // 1 / s_U: the step kernel divides by h's scale, set per launch from max |h0|
   after_launch(c);
   const size_t o3 = n0 + n1 + n2, o4 = o3 + n0;
   weight_f16x2_plain_kernel<<<(unsigned)cdiv(n0, 256), 256, 0, c->stream>>>((int64_t)n0, params + m.o_wx, ws.w16max.p,

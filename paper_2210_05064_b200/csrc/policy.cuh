@@ -29,6 +29,9 @@ struct Model {
   static Model make(const ver_model_config& c);
 };
 
+// max |x| over n floats into *out (float bits; atomicMax, *out zeroed by the caller)
+__global__ void maxabs_kernel(int64_t n, const float* __restrict__ x, unsigned* __restrict__ out);
+
 struct LossStats {  // device-side per-minibatch loss statistics (double)
   double loss, policy_loss, value_loss, mean_entropy, ratio_sum, clip_count, w_sum, w_max;
   double steps;
@@ -55,6 +58,8 @@ struct Workspace {
   // operand's halves (enc / e1, fixed scale 2^14: tanh outputs)
   DBuf<__half> w16hi, w16lo, a16hi, a16lo;
   DBuf<__half> h16hi, h16lo;                            // fp16x2 halves of h (forward pair steps; h0's at the end)
+  DBuf<unsigned> hmax;                                  // max |h0| bits of the current forward pair launch
+  DBuf<float> hsc;                                      // [s_h, 1 / (s_h s_U)] of that launch
   bool f16_fwd = false;  // this forward's weight halves are fresh (policy_forward): fp16x2 pair steps
   DBuf<unsigned> w16max;
   DBuf<unsigned> gmax;  // max |dpre|, max |dpre2| (float bits) of this backward: the fp16x2 data-gradient scales

@@ -62,16 +62,28 @@ constexpr int TR = 6;
 // K-blocks per TMEM accumulation group (tc::PROMOTE in the general GEMM): the
 // split-K items here hold <= 4 K-blocks at C2, so one drain per item
 constexpr int SGP = 4;
-// fp16x2 operand of the forward step GEMM: h_{t-1} x kHScale = hi + lo (|h| < 8:
-// GRU states are convex combinations of tanh outputs and the initial state)
-constexpr float kHScale = 8192.f;  // 2^13
+// fp16x2 operand of the forward step GEMM: h_{t-1} s_h = hi + lo.  GRU states are
+// convex combinations of tanh outputs and the initial state, so |h_t| <= M =
+// max(1, max |h0|) for the whole launch; s_h = 2^(14 - floor(log2 M)) keeps
+// M s_h < 2^15 < 65504 (hscale_kernel, from the max over h0).
 __device__ __forceinline__ void split_h(float y, __half& hi, __half& lo) {
   hi = __float2half_rn(y);
   lo = __float2half_rn(y - __half2float(hi));
 }
-__global__ void h16_kernel(int64_t n, const float* __restrict__ x, __half* __restrict__ hi, __half* __restrict__ lo) {
+// hsc[0] = s_h, hsc[1] = (1 / s_U) / s_h for the GEMM epilogue
+__global__ void hscale_kernel(const unsigned* __restrict__ hmax, const float* __restrict__ inv_u,
+                              float* __restrict__ hsc) {
+  float mx = __uint_as_float(*hmax);
+  if (!(mx >= 1.f) || !isfinite(mx)) mx = 1.f;  // (a NaN / inf h0 makes the result non-finite anyway)
+  const float sh = exp2f((float)(14 - ilogbf(mx)));
+  hsc[0] = sh;
+  hsc[1] = *inv_u / sh;
+}
+__global__ void h16_kernel(int64_t n, const float* __restrict__ x, const float* __restrict__ hsc,
+                           __half* __restrict__ hi, __half* __restrict__ lo) {
+  const float sh = hsc[0];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    split_h(x[i] * kHScale, hi[i], lo[i]);
+    split_h(x[i] * sh, hi[i], lo[i]);
 }
 
 // element i of a register-resident float4 array (i a compile-time constant after
@@ -102,7 +114,8 @@ __device__ __forceinline__ void gate_phase(const Step& S, int H, const float* __
                                            const float* __restrict__ hun, const float* __restrict__ hprev,
                                            float* __restrict__ dpre, float* __restrict__ dhu,
                                            float* __restrict__ gz, int tid, int nthreads,
-                                           __half* __restrict__ h16hi = nullptr, __half* __restrict__ h16lo = nullptr) {
+                                           __half* __restrict__ h16hi = nullptr, __half* __restrict__ h16lo = nullptr,
+                                           float hs = 1.f) {
   const int H3 = 3 * H, N = DIR == 0 ? H3 : H;
   const int H4 = H / 4;
   const size_t zs = (size_t)S.B * N;
@@ -144,7 +157,7 @@ __device__ __forceinline__ void gate_phase(const Step& S, int H, const float* __
       if (h16hi) {  // fp16x2 halves of h_t for the next fp16x2 step GEMM
         __half hh[4], hl[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) split_h(hn[e] * kHScale, hh[e], hl[e]);
+        for (int e = 0; e < 4; ++e) split_h(hn[e] * hs, hh[e], hl[e]);
         reinterpret_cast<__half2*>(h16hi + row)[0] = __halves2half2(hh[0], hh[1]);
         reinterpret_cast<__half2*>(h16hi + row)[1] = __halves2half2(hh[2], hh[3]);
         reinterpret_cast<__half2*>(h16lo + row)[0] = __halves2half2(hl[0], hl[1]);
@@ -577,7 +590,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
   const uint32_t tmem = *tmem_slot;
   unsigned target = 0;
   unsigned* const rbf = bar + 32;  // row-tile counters of the fused steps, [nsteps][rbs]
-  const float fsc = F16 ? __ldg(fscale) : 1.f;  // 1 / (s_A s_B) of the fp16x2 GEMM
+  const float fsc = F16 ? fscale[1] : 1.f;  // 1 / (s_h s_U) of the fp16x2 GEMM (hscale_kernel)
+  const float hs = F16 ? fscale[0] : 1.f;   // s_h: h_t's halves for the next step
   int it_tma = 0, it_mma = 0, it_split = 0, g_mma = 0, g_epi = 0;
   const uint32_t stage_tx = (F16 ? 2u : 1u) * TILE + (blo ? 2u : 1u) * (uint32_t)PairTile<DIR>::BBYTES;
 
@@ -818,7 +832,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
                 const size_t row = ((size_t)S.o + m) * H + u0 + lane;
                 const float hnv = (1.f - zg) * ng + zg * hpv;
                 hidden[row] = hnv;
-                if (F16) split_h(hnv * kHScale, h16hi[row], h16lo[row]);
+                if (F16) split_h(hnv * hs, h16hi[row], h16lo[row]);
                 if (gates_out) {
                   hun_out[row] = sh[2];
                   hprev_out[row] = hpv;
@@ -911,7 +925,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
     gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
                     gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, F16 ? h16hi : nullptr,
-                    F16 ? h16lo : nullptr);
+                    F16 ? h16lo : nullptr, hs);
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 5] = gtimer();
     if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
   }
@@ -1029,7 +1043,7 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
     bmap = make_map16(ws.w16hi.p + off, H3, H, H, PairTile<0>::BNH);
     bmap_lo = make_map16(ws.w16lo.p + off, H3, H, H, PairTile<0>::BNH);
     blo = 1;
-    fscale = ws.w16inv.p + 2;
+    fscale = ws.hsc.p;  // [s_h, 1 / (s_h s_U)] (gru_forward_big_persist)
   }
   const int grid = c->num_sms;
   const void* fn = reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
@@ -1151,8 +1165,16 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
       ws.h16hi.reserve(c, need);
       ws.h16lo.reserve(c, need);
       const size_t n0 = (size_t)h_bs[0] * H;
+      ws.hmax.reserve(c, 1);
+      ws.hsc.reserve(c, 2);
+      ws.hmax.zero(1);
+      maxabs_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 2 * c->num_sms), 256, 0, c->stream>>>(
+          (int64_t)n0, h0, ws.hmax.p);
+      after_launch(c);
+      sg::hscale_kernel<<<1, 1, 0, c->stream>>>(ws.hmax.p, ws.w16inv.p + 2, ws.hsc.p);
+      after_launch(c);
       sg::h16_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 4 * c->num_sms), 256, 0, c->stream>>>(
-          (int64_t)n0, h0, ws.h16hi.p + rows * H, ws.h16lo.p + rows * H);
+          (int64_t)n0, h0, ws.hsc.p, ws.h16hi.p + rows * H, ws.h16lo.p + rows * H);
       after_launch(c);
     }
     const bool force_fuse = env_int("VER_REC_FUSE_ALL", 0) != 0;  // tests / sanitizer
