@@ -463,8 +463,11 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
 // float4 variant (N, ld multiples of 4, X 16-byte aligned): a block covers 128
 // columns (lane: 4 columns) and a row chunk; each warp walks every 8th row with
 // 4 independent accumulators, so ~2 KB per warp are in flight (HBM-bound)
+// (maxout: also max |X| into *maxout as float bits -- the fp16x2 scale of X as the
+// next GEMM's operand, taken on the same pass)
 __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __restrict__ X, int M, int N, int ld,
-                                                              int rows_per, float* __restrict__ part) {
+                                                              int rows_per, float* __restrict__ part,
+                                                              unsigned* __restrict__ maxout) {
   pdl_wait();
   pdl_trigger();
   __shared__ float4 red[8][32];
@@ -474,6 +477,7 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
   float4 a[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float mx = 0.f;
   if (n < N) {
     int m = m0 + r;
     for (; m + 24 < m1; m += 32) {
@@ -481,12 +485,19 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
       for (int u = 0; u < 4; ++u) {
         const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)(m + 8 * u) * ld + n));
         a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
       }
     }
     for (; m < m1; m += 8) {
       const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)m * ld + n));
       a[0].x += x.x; a[0].y += x.y; a[0].z += x.z; a[0].w += x.w;
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
     }
+  }
+  if (maxout) {  // (fmaxf drops NaN: a NaN gradient is caught by the finite checks, not by the scale)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(maxout, __float_as_uint(mx));
   }
   red[r][lane] = make_float4((a[0].x + a[1].x) + (a[2].x + a[3].x), (a[0].y + a[1].y) + (a[2].y + a[3].y),
                              (a[0].z + a[1].z) + (a[2].z + a[3].z), (a[0].w + a[1].w) + (a[2].w + a[3].w));
@@ -502,14 +513,16 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
   }
 }
 
-static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, float* out) {
+static void colsum(Ctx* c, Workspace& ws, const float* X, int M, int N, int ld, float* out,
+                   unsigned* maxout = nullptr) {
   if (N % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
     const int col_blocks = (int)cdiv(N, 128);
     int rows_per = 256;
     while ((int64_t)col_blocks * cdiv(M, rows_per) > 4 * c->num_sms && rows_per < 8192) rows_per *= 2;
     const int chunks = std::max(1, (int)cdiv(M, rows_per));
     ws.splitk.reserve(c, (size_t)chunks * N);
-    launch_pdl(c, colsum4_partial_kernel, dim3(col_blocks, chunks), dim3(256), 0, X, M, N, ld, rows_per, ws.splitk.p);
+    launch_pdl(c, colsum4_partial_kernel, dim3(col_blocks, chunks), dim3(256), 0, X, M, N, ld, rows_per, ws.splitk.p,
+               maxout);
     launch_pdl(c, colsum_final_kernel, dim3(cdiv(N, 256)), dim3(256), 0, (const float*)ws.splitk.p, chunks, N, out);
     return;
   }
@@ -1794,19 +1807,20 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
   // weight gradients over all rows
   gemm_splitk<true, false>(c, ws, H, H3, S, ws.hprev.p, H, ws.dhu.p, H3, grad + m.o_ux, H3);
   gemm_splitk<true, false>(c, ws, E, H3, S, ws.enc.p, E, ws.dpre.p, H3, grad + m.o_wx, H3);
-  colsum(c, ws, ws.dpre.p, S, H3, H3, grad + m.o_bx);
   // data gradients: fp16x2 when this minibatch's forward made the weight halves
-  // (the gradient operand's max by a pass, its halves written in the GEMM)
+  // (the gradient operand's max taken by its bias column-sum pass, its halves
+  // written in the GEMM)
   const bool f16 = ws.f16_fwd && ws.w16inv.n >= 5 && tc::usable_f16(S, E, H3, H3, H3) &&
-                   tc::usable_f16(S, E, E, E, E) && tc::usable(S, E, H3, ws.dpre.p, H3, ws.dpre.p, H3,
-                                                               EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E});
-  // slots 3 / 4 of refresh_weights_f16: after wx^T (3H x E), w2^T (E x E), ux^T (3H x H)
-  const size_t o3 = (size_t)H3 * E + (size_t)E * E + (size_t)H3 * H, o4 = o3 + (size_t)H3 * E;
+                   tc::usable_f16(S, E, E, E, E) && H3 % 4 == 0 && E % 4 == 0 &&
+                   tc::usable(S, E, H3, ws.dpre.p, H3, ws.dpre.p, H3, EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E});
   if (f16) {
     ws.gmax.reserve(c, 2);
     ws.gmax.zero(2);
-    maxabs_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>((int64_t)S * H3, ws.dpre.p, ws.gmax.p);
-    after_launch(c);
+  }
+  colsum(c, ws, ws.dpre.p, S, H3, H3, grad + m.o_bx, f16 ? ws.gmax.p : nullptr);
+  // slots 3 / 4 of refresh_weights_f16: after wx^T (3H x E), w2^T (E x E), ux^T (3H x H)
+  const size_t o3 = (size_t)H3 * E + (size_t)E * E + (size_t)H3 * H, o4 = o3 + (size_t)H3 * E;
+  if (f16) {
     tc::launch_f16a(c, S, E, H3, ws.dpre.p, H3, ws.w16hi.p + o3, ws.w16lo.p + o3, H3, ws.gmax.p, ws.w16inv.p + 3,
                     EpiTanhGrad{ws.dpre2.p, E, ws.enc.p, E}, 1);
   } else {
@@ -1814,10 +1828,8 @@ void policy_backward(Ctx* c, const Model& m, const float* params, int S, const f
                       ws.wlo.n >= (size_t)m.P ? ws.wlo.p + m.o_wx : nullptr);
   }
   gemm_splitk<true, false>(c, ws, E, E, S, ws.e1.p, E, ws.dpre2.p, E, grad + m.o_w2, E);
-  colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2);
+  colsum(c, ws, ws.dpre2.p, S, E, E, grad + m.o_b2, f16 ? ws.gmax.p + 1 : nullptr);
   if (f16) {
-    maxabs_kernel<<<8 * c->num_sms, 256, 0, c->stream>>>((int64_t)S * E, ws.dpre2.p, ws.gmax.p + 1);
-    after_launch(c);
     tc::launch_f16a(c, S, E, E, ws.dpre2.p, E, ws.w16hi.p + o4, ws.w16lo.p + o4, E, ws.gmax.p + 1, ws.w16inv.p + 4,
                     EpiTanhGrad{ws.dpre1.p, E, ws.e1.p, E}, 1);
   } else {
