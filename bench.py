@@ -507,7 +507,10 @@ def run_ours(args, rank, world):
             roof = {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
                     "frac": achieved_tf / bf16s, "traffic": None,
                     "kernel": f"GRU recurrence {dom}: {dom_ms:.3f} ms per minibatch for {rows_per_mb:.0f} rows x 6H^2",
-                    "peak_kind": f"{peaks_kind} bf16 dense sustained"}
+                    "peak_kind": f"{peaks_kind} bf16 dense sustained",
+                    # the backward recurrence issues 3 tf32 MMAs per product (3xTF32) at half
+                    # the bf16 rate: its own tensor ceiling is peak / 6
+                    "frac_of_3xtf32_ceiling": achieved_tf / (bf16s / 6.0)}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
