@@ -323,7 +323,7 @@ static void gemm(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
     const long long rem = tiles % sms;
     const int tail_mt = (int)cdiv(rem, tilesN);
     const int nkb = (K + tc::BK - 1) / tc::BK;
-    if (env_int("VER_TC_TAIL", 1) && c->precision == 0 && tiles > sms && rem > 0 && 10 * rem < 6 * sms &&
+    if (c->precision == 0 && tiles > sms && rem > 0 && 10 * rem < 6 * sms &&
         tail_mt < tilesM && nkb >= 32 && N % 4 == 0) {  // K < 1024: half a wave saves less than the extra launches
       const int M1 = (tilesM - tail_mt) * g.bm, M2 = M - M1;
       tc::launch<TA ? 1 : 0, TB ? 0 : 1>(c, M1, N, K, A, lda, B, ldb, epi, 1, Blo);
@@ -1641,10 +1641,10 @@ void policy_loss(Ctx* c, const Model& m, const float* params, int S, const LossA
                (int)nhg, m.H * m.AH, grad + m.o_wh, grad + m.o_bh);
     return;
   }
-  const bool fuse = want_grads && m.H % 32 == 0 && m.H / 32 <= kHL && env_int("VER_LOSS_FUSE", 1);
+  const bool fuse = want_grads && m.H % 32 == 0 && m.H / 32 <= kHL;
   // fused path: kLossRows rows per warp-iteration with the loss math once per row
-  // (ppo_loss_rows_kernel); VER_LOSS_ROWS=0 keeps one row per warp-iteration
-  const int rows = fuse ? env_int("VER_LOSS_ROWS", kLossRows) : 0;
+  // (ppo_loss_rows_kernel)
+  const int rows = fuse ? kLossRows : 0;
   const int per_blk = kLossWarps * std::max(1, rows);
   const int nblk = std::max(1, std::min((int)cdiv(S, per_blk), 4 * c->num_sms));
   ws.part.reserve(c, (size_t)nblk * (kLossStats + 32));

@@ -1485,7 +1485,7 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
       float* hun = ws.hu.p;
       float* hps = ws.hprev.p;
       long long* tr = trace_buf(c, ws, L);
-      int ta = env_int("VER_REC_TAIL_ASYNC", 1);
+      int ta = 1;  // st.async + mbarrier handoff (0: cluster barrier)
       void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr, &ta};
       tail_launch(c, reinterpret_cast<const void*>(gru_fwd_tail<512>), tail_fwd_smem(512), args);
       trace_dump(c, "fwdtail", L, d_bs, tr);
@@ -1504,7 +1504,7 @@ void gru_forward_recurrence(Ctx* c, const Model& m, const float* params, int L, 
       float* hun = ws.hu.p;
       float* hps = ws.hprev.p;
       long long* tr = trace_buf(c, ws, L);
-      int ta = env_int("VER_REC_TAIL_ASYNC", 1);
+      int ta = 1;  // st.async + mbarrier handoff (0: cluster barrier)
       void* args[] = {&t0_, &L_, &d_bs, &d_offs, &ux, &xp, &h0, &hidden, &gates, &hun, &hps, &tr, &ta};
       tail_launch(c, reinterpret_cast<const void*>(gru_fwd_tail<512>), tail_fwd_smem(512), args);
       trace_dump(c, "fwdtail", L, d_bs, tr);
@@ -1555,10 +1555,10 @@ static void fwd_ks_launch(Ctx* c, const Model& m, const float* params, int t_beg
   unsigned* bar = ws.bar.p;
   long long* tr = trace_buf(c, ws, L);
   const void* fn = pick_fwd_ks(m.H);
-  // short steps hand h over through tagged words (VER_REC_TAG_ROWS; 0 = group barrier + bulk staging).
+  // short steps hand h over through tagged words (up to 24 rows; beyond: group barrier + bulk staging).
   // Measured on B200 at C2: forward recurrence 9.11 -> 8.73 ms per update at 16 rows, 8.61 ms at 24
   // rows with the cluster tail limited to <= 2 rows (VER_REC_TAIL_FWD), worse at 64.  The backward (dhU rows are 3H wide) measured slower with the same scheme.
-  int tag_th = std::min(env_int("VER_REC_TAG_ROWS", 24), ks_fr(ks_warps(m.H)) * RB);
+  int tag_th = std::min(24, ks_fr(ks_warps(m.H)) * RB);
   if (L > 4096) tag_th = 0;  // tags: epoch * 4096 + t
   ws.hx.reserve(c, (size_t)2 * std::max(tag_th, 1) * m.H);
   ws.hx.zero((size_t)2 * std::max(tag_th, 1) * m.H);  // no stale tag can match (epochs start at 1)
@@ -1588,7 +1588,7 @@ void gru_backward_recurrence(Ctx* c, const Model& m, const float* params, int L,
       float* dhu = ws.dhu.p;
       float* gz = ws.g.p;
       long long* tr = trace_buf(c, ws, L);
-      int ta = env_int("VER_REC_TAIL_ASYNC", 1);
+      int ta = 1;  // st.async + mbarrier handoff (0: cluster barrier)
       void* args[] = {&L_, &ts, &d_bs, &d_offs, &ux, &dh, &gates, &hun, &hps, &dpre, &dhu, &gz, &tr, &ta};
       tail_launch(c, reinterpret_cast<const void*>(gru_bwd_tail<512>), tail_bwd_smem(512), args);
       trace_dump(c, "bwdtail", L, d_bs, tr);

@@ -48,7 +48,7 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 2
 // into one TMEM buffer which the epilogue warps drain into fp32 registers
 // (round-to-nearest adds) while the MMA fills the next one.  The drains read
 // 64 KB of TMEM each (tcgen05.ld: ~64 B/cycle/SM), so 4 rather than 2 K-blocks
-// per group: C3 update -3 ms at unchanged parity (VER_TC_PROMOTE overrides).
+// per group: C3 update -3 ms at unchanged parity.
 constexpr int PROMOTE = 4;
 
 // Debug instrumentation (ver_debug_gemm_prof): per-role clock64 cycles spent
@@ -987,7 +987,7 @@ struct Geo {
   bool pair;
 };
 inline Geo geo(const Ctx* c, int M, int N) {
-  if (c->precision == 0 && M >= p2::BM2 && N > BN && env_int("VER_TC_PAIR", 1))
+  if (c->precision == 0 && M >= p2::BM2 && N > BN)
     return Geo{p2::BM2, p2::BN2, c->num_sms / 2, true};
   return Geo{BM, BN, c->num_sms, false};
 }
@@ -1007,7 +1007,7 @@ void launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   const long long ntiles = cdiv(N, p2::BN2) * cdiv(M, p2::BM2) * (long long)splits;
-  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  const int promote = PROMOTE;
   auto run = [&](auto kern) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p2::SMEM2));
     cudaLaunchConfig_t cfg{};
@@ -1020,7 +1020,7 @@ void launch_pair(Ctx* c, int M, int N, int K, const float* A, int lda, const flo
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
     // persistent: as many pairs as can be resident at once (one per TPC)
@@ -1075,7 +1075,7 @@ void launch_f16(Ctx* c, int M, int N, int K, const __half* Ahi, const __half* Al
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   const long long ntiles = cdiv(N, p2::BN2) * cdiv(M, p2::BM2) * (long long)splits;
-  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  const int promote = PROMOTE;
   auto kern = p2::tc_gemm2_kernel<0, 0, Epi, 0, 1>;
   VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p2::SMEM2));
   cudaLaunchConfig_t cfg{};
@@ -1088,7 +1088,7 @@ void launch_f16(Ctx* c, int M, int N, int K, const __half* Ahi, const __half* Al
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
   static std::atomic<int> pairs_cache[kMaxDevices];
@@ -1123,7 +1123,7 @@ void launch_f16a(Ctx* c, int M, int N, int K, const float* A, int lda, const __h
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   const long long ntiles = cdiv(N, p2::BN2) * cdiv(M, p2::BM2) * (long long)splits;
-  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  const int promote = PROMOTE;
   auto kern = p2::tc_gemm2_kernel<0, 0, Epi, 0, 2>;
   VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_F16A));
   cudaLaunchConfig_t cfg{};
@@ -1136,7 +1136,7 @@ void launch_f16a(Ctx* c, int M, int N, int K, const float* A, int lda, const __h
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
   static std::atomic<int> pairs_cache[kMaxDevices];
@@ -1177,7 +1177,7 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
   splits = (nkb + per - 1) / per;
   const long long ntiles = cdiv(N, BN) * cdiv(M, BM) * (long long)splits;
   const int grid = (int)std::min<long long>(ntiles, c->num_sms);
-  const int promote = std::max(1, env_int("VER_TC_PROMOTE", PROMOTE));
+  const int promote = PROMOTE;
   auto run = [&](auto kern) {
     VER_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     cudaLaunchConfig_t cfg{};
@@ -1187,21 +1187,16 @@ void launch(Ctx* c, int M, int N, int K, const float* A, int lda, const float* B
     cfg.stream = c->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = env_int("VER_TC_PDL", 1) ? 1 : 0;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     VER_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, per, splits, epi, tbl, promote));
     after_launch(c);
   };
   if (c->precision == 0) {
-    if (atm) {
-      if (env_int("VER_TC_NACC3", 1)) {
-        if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 2, 1>);
-        else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 2>);
-      } else {
-        if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1, 1>);
-        else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 1>);
-      }
+    if (atm) {  // TMEM-A with 3 accumulator buffers
+      if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 2, 1>);
+      else run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 2>);
       return;
     }
     if (blo) run(tc_gemm_kernel<AMAJ, BMAJ, 1, Epi, 0, 1>);
