@@ -959,8 +959,14 @@ static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
 // forward with H % 32 == 0): a step whose split-K count comes out 1 runs with the
 // gates in the GEMM epilogue (forcing Z = 1 on the smaller steps measured slower;
 // force_fuse is for the sanitizer / small tests, which never reach Z = 1 naturally)
+// (bk: K elements per stage -- 32 for tf32, 64 for the fp16x2 forward.)  Unfused
+// steps take the split-K count with the least modelled time: rounds of items over
+// the pairs x K-blocks per item (+2 of pipeline fill), plus the extra partial tiles
+// the gate phase reads back (~0.00065 K-block times per row and extra split at
+// H = 512; B200 step traces): e.g. 5,000 backward rows run Z = 3 (2 rounds of 16
+// K-blocks) instead of Z = 1 (one round of 48 on 40 of the 74 pairs).
 static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs, int BN, bool fuse,
-                       bool force_fuse = false) {
+                       bool force_fuse = false, int bk = BK) {
   Step s{};
   s.B = B;
   s.Bg = Bg;
@@ -968,9 +974,21 @@ static Step make_step2(int B, int Bg, int o, int op, int N, int K, int pairs, in
   s.op = op;
   s.tilesM = (int)cdiv(std::max(B, 1), p2::BM2);
   const int tilesN = (int)cdiv(N, BN);
-  const int nkb = (K + BK - 1) / BK;
-  int Z = std::max(1, std::min(pairs / std::max(1, s.tilesM * tilesN), std::max(1, nkb / 2)));
+  const int nkb = (K + bk - 1) / bk;
+  const int items = s.tilesM * tilesN;
+  int Z = std::max(1, std::min(pairs / std::max(1, items), std::max(1, nkb / 2)));
   Z = std::min(Z, 8);
+  if (!fuse) {
+    double best = 1e300;
+    for (int z = 1; z <= std::min(8, std::max(1, nkb / 2)); ++z) {
+      const double rounds = (double)cdiv((long long)items * z, std::max(1, pairs));
+      const double cost = rounds * (double)(cdiv(nkb, z) + 2) + (z - 1) * (double)B * 0.00065;
+      if (cost < best * 0.999) {
+        best = cost;
+        Z = z;
+      }
+    }
+  }
   if (fuse && force_fuse) Z = 1;
   const int per = (nkb + Z - 1) / Z;
   s.Z = (nkb + per - 1) / per;
@@ -1181,7 +1199,8 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
     for (int t = ta; t < tz; ++t) {
       const int B = h_bs[t];
       const int op = t == 0 ? -1 : h_offs[t - 1];
-      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse, force_fuse)
+      hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse,
+                                              force_fuse, f16 ? 64 : tc::BK)
                              : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms));
       if (f16) {
         const size_t rows = (size_t)h_offs[tz - 1] + h_bs[tz - 1];
