@@ -53,8 +53,12 @@ ver_status ver_ctx_synchronize(ver_ctx ctx);
 ver_status ver_ctx_stream(ver_ctx ctx, uint64_t* stream_out);
 /* number of kernels this library launched on ctx since creation / last reset */
 ver_status ver_ctx_launch_count(ver_ctx ctx, int64_t* count, int reset);
-/* precision of the tensor-core policy GEMMs: 0 = 3xTF32 (fp32-grade, the
-   parity default), 1 = 1xTF32 (fast mode, looser bound stated in DESIGN.md) */
+/* precision of the tensor-core policy GEMMs: 0 = fp32-grade (the parity
+   default: 3xTF32, or fp16x2 -- scaled fp16 hi + lo pairs, 22 significant bits,
+   three kind::f16 MMAs per product -- for the forward GEMMs, the forward
+   recurrence steps on CTA pairs and the backward data gradients; environment
+   VER_TC_F16=0 keeps 3xTF32 everywhere), 1 = 1xTF32 (fast mode, looser bound
+   stated in DESIGN.md) */
 ver_status ver_ctx_set_precision(ver_ctx ctx, int mode);
 /* 1 (default): batched policy GEMMs on tcgen05 tensor cores; 0: fp32 SIMT */
 ver_status ver_ctx_set_tensor_cores(ver_ctx ctx, int enable);
