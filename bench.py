@@ -341,7 +341,8 @@ def run_ours(args, rank, world):
         del v2
     e2e = max_over_ranks(statistics.median(e2e_ms))
     h2d = host_bytes(wl)
-    lat = gru_latency(learner, view, phase, phase_n) if rank == 0 else None
+    # (one traced update: at N > 1 every rank would have to join its AllReduces, so N = 1 only)
+    lat = gru_latency(learner, view, phase, phase_n) if world == 1 else None
     del view
 
     # ---- configs[1] (C2): N = 256 envs, 4 epochs x 2 minibatches (extra field)
