@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
   float4 a[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-  float mx = 0.f;
+  float mxu[4] = {0.f, 0.f, 0.f, 0.f};  // one running max per unrolled row (no serial chain)
   if (n < N) {
     int m = m0 + r;
     for (; m + 24 < m1; m += 32) {
@@ -485,16 +485,17 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
       for (int u = 0; u < 4; ++u) {
         const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)(m + 8 * u) * ld + n));
         a[u].x += x.x; a[u].y += x.y; a[u].z += x.z; a[u].w += x.w;
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+        if (maxout) mxu[u] = fmaxf(mxu[u], fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
       }
     }
     for (; m < m1; m += 8) {
       const float4 x = __ldg(reinterpret_cast<const float4*>(X + (size_t)m * ld + n));
       a[0].x += x.x; a[0].y += x.y; a[0].z += x.z; a[0].w += x.w;
-      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+      if (maxout) mxu[0] = fmaxf(mxu[0], fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
     }
   }
   if (maxout) {  // (fmaxf drops NaN: a NaN gradient is caught by the finite checks, not by the scale)
+    float mx = fmaxf(fmaxf(mxu[0], mxu[1]), fmaxf(mxu[2], mxu[3]));
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) atomicMax(maxout, __float_as_uint(mx));
