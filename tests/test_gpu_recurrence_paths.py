@@ -142,3 +142,28 @@ def test_loss_gradient_parity_fp16x2_h0_range(env_paths, h0_scale):
     else:
         assert errs["1"][0] <= 1.25 * errs["0"][0] + 1e-7, errs
         assert errs["1"][1] <= 1.25 * errs["0"][1] + 1e-7, errs
+
+
+@pytest.mark.parametrize("EH", [(160, 160), (96, 224)])
+def test_loss_gradient_parity_fp16x2_odd_widths(EH):
+    """fp16x2 GEMMs with K and N that are not multiples of the 64-element stage or
+    the 256-column pair tile (zero-filled TMA boxes, masked epilogue columns): loss and
+    gradients of one packed minibatch (S = 384 rows) against the oracle."""
+    import paper_2210_05064_b200 as V
+    from oracle import oracle as O
+    from test_gpu_parity import _model
+    E, H = EH
+    cfg = _model(E, H)
+    p = O.params_init(cfg, O.mix(5, 0x9A9A)).astype(np.float32).astype(np.float64)
+    vg, vo, _ = close_both(16, 24, H, seed=35)
+    V.compute_gae(vg, 0.99, 0.95)
+    O.compute_gae(vo, 0.99, 0.95)
+    hv = vo.to_host()
+    bo = O.pack(hv.seqs)
+    bg = V.pack(vg, V.SequenceGroup(hv.seqs))
+    h0 = np.stack([hv.h0[s[4]] for s in bo.seqs])
+    ro = O.ppo_loss(cfg, p, vo, bo, V.PPOConfig(), 0.01, h0, True)
+    rg = V.ppo_loss(cfg, p, vg, bg, V.PPOConfig(), 0.01, h0, True)
+    assert abs(rg.loss - ro["loss"]) <= 1e-5 * max(1.0, abs(ro["loss"]))
+    g, go = rg.grads.astype(np.float64), ro["grads"]
+    assert np.all(np.abs(g - go) <= 1e-5 * np.maximum(1.0, np.abs(go))), np.abs(g - go).max()
