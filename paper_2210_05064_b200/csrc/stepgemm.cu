@@ -511,9 +511,10 @@ constexpr int kFRow = 100;
 template <int F16>
 struct PairCfg {
   static constexpr int NST = F16 ? 2 : p2::STAGES2;
-  static constexpr int RING = F16 ? 6 : 2;
+  static constexpr int RING = F16 ? 4 : 2;
   static constexpr int CH = F16 ? 8 : 4;  // accumulator rows staged at a time
-  static constexpr int FUSED = CH * kFRow + RING * (2 * kFRow + 64);
+  static constexpr int GR = F16 ? 4 : 2;  // rows per epilogue group (cp.async ring slot)
+  static constexpr int FUSED = CH * kFRow + RING * GR * (kFRow + 32);
   static constexpr int WF = FUSED > 32 * p2::SLD ? FUSED : 32 * p2::SLD;  // floats per epilogue warp
   static constexpr int EPI = p2::EPIW * WF * 4;
   static constexpr int SMEM = NST * p2::STAGE2 + EPI + 1024 + 256;
@@ -743,7 +744,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           // behind two groups of gate math.
           float* fh = stg_all + (warp - 4) * PairCfg<F16>::WF;  // [CH][kFRow] hU rows
           float* fx0 = fh + PairCfg<F16>::CH * kFRow;            // [RING][2][kFRow] xp rows, then gates
-          float* fp0 = fx0 + RING * 2 * kFRow;                   // [RING][2][32] h_{t-1} rows
+          constexpr int GR = PairCfg<F16>::GR, NG = 32 / GR;    // rows per group, groups per item
+          float* fp0 = fx0 + RING * GR * kFRow;                  // [RING][GR][32] h_{t-1} rows
           const int u0 = ncol0 / 3;
           const bool colok = ncol0 < N;
           const int blast = max(S.B - 1, 0);
@@ -757,12 +759,12 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           }
           if (dep) spin_acquire(dep, dep_need);  // h_{t-1} rows of this row tile (read below)
           const int xl = lane < 24 ? 4 * lane : 0;  // this lane's float4 of a 96-column xp row
-          auto issue = [&](int k) {  // rows 2k, 2k + 1 -> ring slot k % RING
-            float* fx = fx0 + (k % RING) * 2 * kFRow;
-            float* fp = fp0 + (k % RING) * 64;
+          auto issue = [&](int k) {  // rows GR k .. GR k + GR - 1 -> ring slot k % RING
+            float* fx = fx0 + (k % RING) * GR * kFRow;
+            float* fp = fp0 + (k % RING) * GR * 32;
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int m = min(mrow0 + 2 * k + r, blast);
+            for (int r = 0; r < GR; ++r) {
+              const int m = min(mrow0 + GR * k + r, blast);
               if (lane < 24)
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(fx + r * kFRow + xl)),
                              "l"(xp + ((size_t)S.o + m) * N + (colok ? ncol0 + xl : 0))
@@ -803,11 +805,11 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
           if (lane == 0) arrive_remote(to_rank(acc_empty(buf), 0));  // TMEM free for the item after next
           ++g_epi;
 #pragma unroll 1
-          for (int k = 0; k < 16; ++k) {
-            if (k + RING - 1 < 16) issue(k + RING - 1);
+          for (int k = 0; k < NG; ++k) {
+            if (k + RING - 1 < NG) issue(k + RING - 1);
             asm volatile("cp.async.commit_group;" ::: "memory");  // (empty near the end: keeps the count)
             asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");  // group k has landed
-            constexpr int CH = PairCfg<F16>::CH, GPC = CH / 2;  // groups per staged chunk
+            constexpr int CH = PairCfg<F16>::CH, GPC = CH / GR;  // groups per staged chunk
             if (k % GPC == 0) {  // rows CH c .. CH c + CH - 1 from their owner lanes (fh is free: last group synced)
               if (lane / CH == k / GPC) {
                 float4* d = reinterpret_cast<float4*>(fh + (lane % CH) * kFRow);
@@ -817,12 +819,12 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
               }
             }
             __syncwarp();
-            float* fx = fx0 + (k % RING) * 2 * kFRow;
-            const float* fp = fp0 + (k % RING) * 64;
+            float* fx = fx0 + (k % RING) * GR * kFRow;
+            const float* fp = fp0 + (k % RING) * GR * 32;
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int m = mrow0 + 2 * k + r;
-              const float* sh = fh + (2 * (k % GPC) + r) * kFRow + 3 * lane;
+            for (int r = 0; r < GR; ++r) {
+              const int m = mrow0 + GR * k + r;
+              const float* sh = fh + (GR * (k % GPC) + r) * kFRow + 3 * lane;
               float* sx = fx + r * kFRow + 3 * lane;
               const float hpv = fp[r * 32 + lane];
               const float rg = gate_sigm(sx[0] + sh[0]);
@@ -845,8 +847,8 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
             __syncwarp();
             if (gates_out && lane < 24 && colok) {
 #pragma unroll
-              for (int r = 0; r < 2; ++r) {
-                const int m = mrow0 + 2 * k + r;
+              for (int r = 0; r < GR; ++r) {
+                const int m = mrow0 + GR * k + r;
                 if (m < S.B)
                   *reinterpret_cast<float4*>(gates_out + ((size_t)S.o + m) * N + ncol0 + xl) =
                       *reinterpret_cast<const float4*>(fx + r * kFRow + xl);
