@@ -20,6 +20,7 @@ compaction), update, read the stats back.  configs[1] (C2) is an extra field.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -85,6 +86,14 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
                 stderr=subprocess.DEVNULL)
+            # nvidia-smi's start-up (driver attach, first query) can stall this process's
+            # CUDA calls for tens of ms: let it finish before the warm-up / timed steps
+            t0 = time.time()
+            while time.time() - t0 < 5.0 and self.proc.poll() is None:
+                self.f.flush()
+                if Path(self.f.name).stat().st_size > 0:
+                    break
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
@@ -285,6 +294,16 @@ def run_ours(args, rank, world):
         return float(t.item())
 
     def timed_updates(learner, view, steps, warmup):
+        # the Python cycle collector would otherwise run inside a timed step now and
+        # then (a full collection stalls the host thread that feeds the GPU)
+        gc.collect()
+        gc.disable()
+        try:
+            return _timed_updates(learner, view, steps, warmup)
+        finally:
+            gc.enable()
+
+    def _timed_updates(learner, view, steps, warmup):
         for _ in range(warmup):
             learner.update(view, read_stats=False)
         barrier()
@@ -524,6 +543,7 @@ def run_ours(args, rank, world):
             "phases_ms": phase,
             "phase_counts": phase_n,
             "gpu_launches": int(launches),
+            "step_ms_rank0": [round(x, 3) for x in step_ms],  # each timed step (CUDA events), this rank
             "clocks": clk.summary(),
             "e2e": {"value": fresh * world / (e2e / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": 8 * 12, "ms_per_step": e2e},

@@ -73,7 +73,9 @@ Model Model::make(const ver_model_config& c) {
 
 void Workspace::ensure(const Model& m, size_t S, bool train) {
   if (S <= rows && e1.p) return;
-  const size_t R = std::max<size_t>(S, 1);
+  // 1/8 headroom: minibatch row counts vary from split to split, and every growth
+  // reallocates gigabytes (the stream-ordered pool maps new memory inside a step)
+  const size_t R = std::max<size_t>(S + S / 8, 1);
   const size_t E = m.E, H = m.H;
   e1.reserve(ctx, R * E);
   enc.reserve(ctx, R * E);
@@ -632,9 +634,10 @@ void policy_forward(Ctx* c, const Model& m, const float* params, int S, const fl
   const bool f16 = f16x2_on(c) && tc::usable_f16(S, H3, E, E, E) && tc::usable_f16(S, E, E, E, E) &&
                    EpiBias{ws.xp.p, H3, params + m.o_bx}.vec_ok() && E % 8 == 0;
   const size_t nSE = (size_t)S * E;
-  if (f16) {  // e1's halves at [0, nSE), enc's at [nSE, 2 nSE)
-    ws.a16hi.reserve(c, 2 * nSE);
-    ws.a16lo.reserve(c, 2 * nSE);
+  if (f16) {  // e1's halves at [0, nSE), enc's at [nSE, 2 nSE) (sized by the workspace rows)
+    const size_t cap = 2 * std::max(ws.rows, (size_t)S) * E;
+    ws.a16hi.reserve(c, cap);
+    ws.a16lo.reserve(c, cap);
   }
   if (E % 4 == 0) {
     const unsigned gx = cdiv(E, 128);

@@ -1181,7 +1181,8 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
     const bool fuse = H % 32 == 0;
     if (f16) {  // h halves: rows of every pair step (packed offsets), h0's after them
       const size_t rows = (size_t)h_offs[tz - 1] + h_bs[tz - 1];
-      const size_t need = (rows + (size_t)h_bs[0]) * H;
+      // (sized by the workspace rows: no regrowth from one minibatch to the next)
+      const size_t need = std::max(rows + (size_t)h_bs[0], 2 * ws.rows) * H;
       ws.h16hi.reserve(c, need);
       ws.h16lo.reserve(c, need);
       const size_t n0 = (size_t)h_bs[0] * H;
