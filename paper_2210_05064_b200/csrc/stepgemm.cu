@@ -225,7 +225,10 @@ __device__ __forceinline__ void gate_phase(const Step& S, int H, const float* __
   }
 }
 
-template <int DIR>  // 0 forward (B MN-major: U stored K x N), 1 backward (B K-major: U stored N x K)
+// F16 (forward only): the fp16x2 GEMM phase of the pair kernel on single CTAs --
+// A = h_{t-1} halves (amaps[2 si], [2 si + 1]), B = U's transposed K-major halves,
+// accumulator x fscale[1]; the gate phase writes h_t's halves (scale fscale[0])
+template <int DIR, int F16 = 0>  // 0 forward (B MN-major: U stored K x N), 1 backward (B K-major: U stored N x K)
 __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     int nsteps, const Step* __restrict__ steps, const CUtensorMap* __restrict__ amaps,
     const __grid_constant__ CUtensorMap bmap, int H, float* __restrict__ part, unsigned* bar,
@@ -235,10 +238,13 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     // backward
     const float* __restrict__ dhidden, const float* __restrict__ gates, const float* __restrict__ hun,
     const float* __restrict__ hprev, float* __restrict__ dpre, float* __restrict__ dhu, float* __restrict__ gz,
-    long long* trace, const __grid_constant__ CUtensorMap bmap_lo, int blo) {
+    long long* trace, const __grid_constant__ CUtensorMap bmap_lo, int blo, __half* __restrict__ h16hi,
+    __half* __restrict__ h16lo, const float* __restrict__ fscale) {
   // blo: U's lo part (x - trunc_tf32(x)) comes pre-split from the parameters' lo
   // copy (policy.cu split_lo_kernel) by TMA; the split warps then only split A
-  constexpr int AMAJ = 0, BMAJ = DIR == 0 ? 1 : 0;
+  static_assert(!F16 || DIR == 0, "fp16x2 single-CTA steps: forward only");
+  constexpr int AMAJ = 0, BMAJ = (DIR == 0 && !F16) ? 1 : 0;
+  constexpr int BKE = F16 ? 64 : BK;  // K elements per stage
   extern __shared__ uint8_t smem_raw[];
   // 1024-aligned by pointer arithmetic on the __shared__ array, so that the compiler
   // keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers
@@ -249,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H3 = 3 * H, N = DIR == 0 ? H3 : H, K = DIR == 0 ? H : H3;
   const int tilesN = (N + BN - 1) / BN;
-  const int nkb_total = (K + BK - 1) / BK;
+  const int nkb_total = (K + BKE - 1) / BKE;
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bar0 = smem_u32(bars);
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
@@ -300,7 +306,8 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
       }
     }
   };
-  const uint32_t stage_tx = (blo ? 3u : 2u) * TILE_BYTES;
+  const uint32_t stage_tx = (F16 ? 4u : (blo ? 3u : 2u)) * TILE_BYTES;
+  const float fsc = F16 ? fscale[1] : 1.f, hs = F16 ? fscale[0] : 1.f;
 
   for (int si = 0; si < nsteps; ++si) {
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si] = gtimer();
@@ -310,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     // H = 512, i.e. C3's first steps) gives a CTA several items in a row; every
     // role walks the same item sequence
     const int W = S.B > 0 ? S.tilesM * tilesN * S.Z : 0;
-    const CUtensorMap* amap = amaps + si;
+    const CUtensorMap* amap = amaps + (F16 ? 2 * si : si);
     for (int item = blockIdx.x; item < W; item += gridDim.x) {
       const bool first_item = item == (int)blockIdx.x, last_item = item + (int)gridDim.x >= W;
       const int nt = item % tilesN, q = item / tilesN;
@@ -323,13 +330,14 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           for (int i = 0; i < nkb; ++i, ++it_tma) {
             const int s = it_tma % STAGES;
             const uint32_t ph = (it_tma / STAGES) & 1;
-            const int k0 = (kb0 + i) * BK;
+            const int k0 = (kb0 + i) * BKE;
             if (!first_item || i >= b_pre) {
               mbar_wait(empty_bar(s), ph ^ 1);
               mbar_expect_tx(full_bar(s), stage_tx);
               load_b(s, k0, n0);
             }
             tma_load_2d(tile(s, 0), amap, full_bar(s), k0, m0);
+            if (F16) tma_load_2d(tile(s, 1), amap + 1, full_bar(s), k0, m0);
           }
           // after this CTA's last item: the next step's first B tiles (U does not
           // change across steps) and its A tensor map, issued before the grid barriers
@@ -338,7 +346,8 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
             const Step S2 = steps[si + 1];
             if (S2.B > 0 && (int)blockIdx.x < S2.tilesM * tilesN * S2.Z) {
               const int item2 = blockIdx.x;
-              asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(amaps + si + 1)) : "memory");
+              asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(amaps + (F16 ? 2 : 1) * (si + 1)))
+                           : "memory");
               const int z2 = item2 / tilesN / S2.tilesM;
               const int kb2 = z2 * S2.per;
               const int nkb2 = max(0, min(nkb_total, kb2 + S2.per) - kb2);
@@ -347,13 +356,14 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
                 const int s = (it_tma + i) % STAGES;
                 mbar_wait(empty_bar(s), ((it_tma + i) / STAGES & 1) ^ 1);
                 mbar_expect_tx(full_bar(s), stage_tx);
-                load_b(s, (kb2 + i) * BK, (item2 % tilesN) * BN);
+                load_b(s, (kb2 + i) * BKE, (item2 % tilesN) * BN);
               }
             }
           }
         }
       } else if (warp == 1) {
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
+        const uint32_t fmt = F16 ? 0u : 2u;  // A / B f16 or tf32
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)AMAJ << 15) | ((uint32_t)BMAJ << 16) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
         if (lane == 0) {
           int buf = 0;
@@ -370,12 +380,18 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
             tc_fence_after();
             const uint32_t d = tmem + (uint32_t)(buf * BN);
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
+            for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K per MMA
               const uint64_t ah = operand_desc<AMAJ>(tile(s, 0), kk);
               const uint64_t bh = operand_desc<BMAJ>(tile(s, 2), kk);
-              mma_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
-              mma_tf32(d, operand_desc<AMAJ>(tile(s, 1), kk), bh, idesc, 1u);
-              mma_tf32(d, ah, operand_desc<BMAJ>(tile(s, 3), kk), idesc, 1u);
+              if (F16) {
+                mma_f16(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+                mma_f16(d, operand_desc<AMAJ>(tile(s, 1), kk), bh, idesc, 1u);
+                mma_f16(d, ah, operand_desc<BMAJ>(tile(s, 3), kk), idesc, 1u);
+              } else {
+                mma_tf32(d, ah, bh, idesc, (!first || kk > 0) ? 1u : 0u);
+                mma_tf32(d, operand_desc<AMAJ>(tile(s, 1), kk), bh, idesc, 1u);
+                mma_tf32(d, ah, operand_desc<BMAJ>(tile(s, 3), kk), idesc, 1u);
+              }
             }
             umma_commit(empty_bar(s));
             if ((i % SGP) == SGP - 1 || i == nkb - 1) {
@@ -392,6 +408,11 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           const uint32_t ph = (it_split / STAGES) & 1;
           mbar_wait(full_bar(s), ph);
           if (trace && i == 0 && threadIdx.x == 64 && blockIdx.x == 0) trace[TR * si + 1] = gtimer();
+          if (F16) {  // pre-split operands: relay
+            __syncwarp();
+            if (lane == 0) mbar_arrive(split_bar(s));
+            continue;
+          }
           uint8_t* st = smem + s * STAGE_BYTES;
           float4* ahi = reinterpret_cast<float4*>(st);
           float4* alo = reinterpret_cast<float4*>(st + TILE_BYTES);
@@ -445,6 +466,10 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
           __syncwarp();
           if (lane == 0) mbar_arrive(acc_empty(buf));
         }
+        if (F16) {  // undo the operand scales (powers of two)
+#pragma unroll
+          for (int j = 0; j < BN; ++j) sums[j] *= fsc;
+        }
         const int rr = lane >> 3, c4 = (lane & 7) * 4;
 #pragma unroll
         for (int cc = 0; cc < BN / 32; ++cc) {
@@ -471,7 +496,8 @@ __global__ void __launch_bounds__(THREADS, 1) gru_step_gemm_kernel(
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 4] = gtimer();
 
     gate_phase<DIR>(S, H, part, xp, h0, hidden, gates_out, hun_out, hprev_out, dhidden, gates, hun, hprev, dpre, dhu,
-                    gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+                    gz, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, F16 ? h16hi : nullptr,
+                    F16 ? h16lo : nullptr, hs);
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR * si + 5] = gtimer();
     if (si + 1 < nsteps) grid_sync(bar, target);  // step si's rows before step si+1's GEMM reads them
   }
@@ -940,7 +966,7 @@ __global__ void __launch_bounds__(p2::THREADS2, 1) gru_step_gemm2_kernel(
 }
 
 // host: per-step split-K so that tilesM x tilesN x Z <= grid
-static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
+static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid, int bk = BK) {
   Step s{};
   s.B = B;
   s.Bg = Bg;
@@ -948,7 +974,7 @@ static Step make_step(int B, int Bg, int o, int op, int N, int K, int grid) {
   s.op = op;
   s.tilesM = (int)cdiv(std::max(B, 1), BM);
   const int tilesN = (int)cdiv(N, BN);
-  const int nkb = (K + BK - 1) / BK;
+  const int nkb = (K + bk - 1) / bk;
   int Z = std::max(1, std::min(grid / std::max(1, s.tilesM * tilesN), std::max(1, nkb / 2)));
   Z = std::min(Z, 8);
   const int per = (nkb + Z - 1) / Z;
@@ -1060,17 +1086,21 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
   const float* fscale = nullptr;
   if (f16) {  // U's transposed fp16x2 halves (policy.cu refresh_weights_f16 slot 2): 3H x H, K-major
     const size_t off = (size_t)H3 * m.E + (size_t)m.E * m.E;
-    bmap = make_map16(ws.w16hi.p + off, H3, H, H, PairTile<0>::BNH);
-    bmap_lo = make_map16(ws.w16lo.p + off, H3, H, H, PairTile<0>::BNH);
+    const int brows = pair ? PairTile<0>::BNH : BN;  // a CTA's B rows: its half of a pair tile, or a 128-column tile
+    bmap = make_map16(ws.w16hi.p + off, H3, H, H, brows);
+    bmap_lo = make_map16(ws.w16lo.p + off, H3, H, H, brows);
     blo = 1;
     fscale = ws.hsc.p;  // [s_h, 1 / (s_h s_U)] (gru_forward_big_persist)
   }
   const int grid = c->num_sms;
-  const void* fn = reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
-  static std::atomic<bool> attr[kMaxDevices][2];  // per device: a function attribute is per device
-  if (!attr[dev_slot(c)][DIR].load()) {
+  const bool f16s = f16 && DIR == 0 && !pair;  // the single-CTA kernel's fp16x2 variant
+  const void* fn = f16s ? reinterpret_cast<const void*>(gru_step_gemm_kernel<0, 1>)
+                        : reinterpret_cast<const void*>(gru_step_gemm_kernel<DIR>);
+  static std::atomic<bool> attr[kMaxDevices][3];  // per device: a function attribute is per device
+  const int av = f16s ? 2 : DIR;
+  if (!attr[dev_slot(c)][av].load()) {
     VER_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    attr[dev_slot(c)][DIR].store(true);
+    attr[dev_slot(c)][av].store(true);
   }
   int ns = nsteps;
   const Step* dsteps = reinterpret_cast<const Step*>(ws.sgsteps.p);
@@ -1128,9 +1158,12 @@ static void launch(Ctx* c, const Model& m, const float* params, const std::vecto
                                   rbs, h16hi, h16lo, fscale));
     after_launch(c);
   } else {
+    __half* sh16hi = ws.h16hi.p;
+    __half* sh16lo = ws.h16lo.p;
     void* args[] = {&ns,    &dsteps, &dmaps,  const_cast<CUtensorMap*>(&bmap), const_cast<int*>(&H),
                     &part,  &bar,    &xp,     &h0,  &hidden, &gts, &hun_o, &hpv_o, &dh, &gates, &hun, &hprev, &dpre,
-                    &dhu,   &gz,     &tr,     const_cast<CUtensorMap*>(&bmap_lo), &blo};
+                    &dhu,   &gz,     &tr,     const_cast<CUtensorMap*>(&bmap_lo), &blo, &sh16hi, &sh16lo,
+                    const_cast<const float**>(&fscale)};
     ScopedEv ev(c, c->rec_tag);
     VER_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(THREADS), args, SMEM_BYTES, c->stream));
     after_launch(c);
@@ -1169,44 +1202,45 @@ void gru_forward_big_persist(Ctx* c, const Model& m, const float* params, int t_
   int t1 = 0;
   if (pr > 0)
     while (t1 < t_end && h_bs[t1] >= pr) ++t1;
+  if (t_end <= 0) return;
+  // fp16x2 GEMM phase (pair and single-CTA steps) when this forward's weight halves
+  // are fresh (policy_forward) and H fits 64-element K blocks: h halves for the rows
+  // of every big step (packed offsets), h0's after them, h's scale from max |h0|
+  const bool f16 = ws.f16_fwd && H % 64 == 0;
+  const size_t rows = (size_t)h_offs[t_end - 1] + h_bs[t_end - 1];
+  if (f16) {
+    // (sized by the workspace rows: no regrowth from one minibatch to the next)
+    const size_t need = std::max(rows + (size_t)h_bs[0], 2 * ws.rows) * H;
+    ws.h16hi.reserve(c, need);
+    ws.h16lo.reserve(c, need);
+    const size_t n0 = (size_t)h_bs[0] * H;
+    ws.hmax.reserve(c, 1);
+    ws.hsc.reserve(c, 2);
+    ws.hmax.zero(1);
+    maxabs_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 2 * c->num_sms), 256, 0, c->stream>>>(
+        (int64_t)n0, h0, ws.hmax.p);
+    after_launch(c);
+    sg::hscale_kernel<<<1, 1, 0, c->stream>>>(ws.hmax.p, ws.w16inv.p + 2, ws.hsc.p);
+    after_launch(c);
+    sg::h16_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 4 * c->num_sms), 256, 0, c->stream>>>(
+        (int64_t)n0, h0, ws.hsc.p, ws.h16hi.p + rows * H, ws.h16lo.p + rows * H);
+    after_launch(c);
+  }
   for (int part = 0; part < 2; ++part) {
     const int ta = part == 0 ? 0 : t1, tz = part == 0 ? t1 : t_end;
     if (ta >= tz) continue;
     std::vector<sg::Step> hs;
     std::vector<CUtensorMap> maps;
-    // fp16x2 GEMM phase for the pair steps when this forward's weight halves are
-    // fresh (policy_forward) and H fits 64-element K blocks
-    const bool f16 = part == 0 && ws.f16_fwd && H % 64 == 0;
     const int pairs = part == 0 ? (f16 ? sg::step_pairs<0, 1>(c) : sg::step_pairs<0>(c)) : 0;
     const bool fuse = H % 32 == 0;
-    if (f16) {  // h halves: rows of every pair step (packed offsets), h0's after them
-      const size_t rows = (size_t)h_offs[tz - 1] + h_bs[tz - 1];
-      // (sized by the workspace rows: no regrowth from one minibatch to the next)
-      const size_t need = std::max(rows + (size_t)h_bs[0], 2 * ws.rows) * H;
-      ws.h16hi.reserve(c, need);
-      ws.h16lo.reserve(c, need);
-      const size_t n0 = (size_t)h_bs[0] * H;
-      ws.hmax.reserve(c, 1);
-      ws.hsc.reserve(c, 2);
-      ws.hmax.zero(1);
-      maxabs_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 2 * c->num_sms), 256, 0, c->stream>>>(
-          (int64_t)n0, h0, ws.hmax.p);
-      after_launch(c);
-      sg::hscale_kernel<<<1, 1, 0, c->stream>>>(ws.hmax.p, ws.w16inv.p + 2, ws.hsc.p);
-      after_launch(c);
-      sg::h16_kernel<<<(unsigned)std::min<size_t>(cdiv(n0, 256), 4 * c->num_sms), 256, 0, c->stream>>>(
-          (int64_t)n0, h0, ws.hsc.p, ws.h16hi.p + rows * H, ws.h16lo.p + rows * H);
-      after_launch(c);
-    }
     const bool force_fuse = env_int("VER_REC_FUSE_ALL", 0) != 0;  // tests / sanitizer
     for (int t = ta; t < tz; ++t) {
       const int B = h_bs[t];
       const int op = t == 0 ? -1 : h_offs[t - 1];
       hs.push_back(part == 0 ? sg::make_step2(B, B, h_offs[t], op, H3, H, pairs, sg::PairTile<0>::BN, fuse,
                                               force_fuse, f16 ? 64 : tc::BK)
-                             : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms));
+                             : sg::make_step(B, B, h_offs[t], op, H3, H, c->num_sms, f16 ? 64 : tc::BK));
       if (f16) {
-        const size_t rows = (size_t)h_offs[tz - 1] + h_bs[tz - 1];
         const size_t r0 = t == 0 ? rows : (size_t)h_offs[t - 1];
         maps.push_back(tc::make_map16(ws.h16hi.p + r0 * H, B, H, H, tc::BM));
         maps.push_back(tc::make_map16(ws.h16lo.p + r0 * H, B, H, H, tc::BM));
