@@ -524,8 +524,12 @@ def run_ours(args, rank, world):
             dom = max(("rec_bwd", "rec_fwd"), key=lambda k: phase.get(k, 0.0))
             dom_ms = phase.get(dom, 0.0) / n_mb
             achieved_tf = 6.0 * H_ * H_ * rows_per_mb / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
+            tr_ = traffic_entry("rec_bwd_c3") if dom == "rec_bwd" and world >= 1 and N_ == 4096 else None
             roof = {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
-                    "frac": achieved_tf / bf16s, "traffic": None,
+                    "frac": achieved_tf / bf16s,
+                    # DRAM bytes of all backward recurrence launches of one minibatch (the
+                    # same unit as `achieved`), from the committed ncu captures
+                    "traffic": tr_.get("dram_bytes_per_launch") if tr_ else None,
                     "kernel": f"GRU recurrence {dom}: {dom_ms:.3f} ms per minibatch for {rows_per_mb:.0f} rows x 6H^2",
                     "peak_kind": f"{peaks_kind} bf16 dense sustained",
                     # the backward recurrence issues 3 tf32 MMAs per product (3xTF32) at half
