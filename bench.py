@@ -524,7 +524,7 @@ def run_ours(args, rank, world):
             dom = max(("rec_bwd", "rec_fwd"), key=lambda k: phase.get(k, 0.0))
             dom_ms = phase.get(dom, 0.0) / n_mb
             achieved_tf = 6.0 * H_ * H_ * rows_per_mb / (dom_ms / 1000.0) / 1e12 if dom_ms > 0 else 0.0
-            tr_ = traffic_entry("rec_bwd_c3") if dom == "rec_bwd" and world >= 1 and N_ == 4096 else None
+            tr_ = traffic_entry("rec_bwd_c3") if dom == "rec_bwd" else None  # (captured at C3: N_ = 4096)
             roof = {"bound": "tensor", "achieved": achieved_tf, "peak": bf16s, "unit": "TFLOP/s",
                     "frac": achieved_tf / bf16s,
                     # DRAM bytes of all backward recurrence launches of one minibatch (the
